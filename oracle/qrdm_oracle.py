@@ -212,6 +212,53 @@ def _trace_candidates(trace, u, tau, k_dm, seed):
 
 
 # ----------------------------------------------------------------------------
+# decision margins -- not part of the reference
+# ----------------------------------------------------------------------------
+
+AMBIGUOUS = 1e3 * EPS  # a decision whose amplified margin is below this may flip
+
+
+class _Margins:
+    """Relative gap of every steering comparison, and the same gap scaled by
+    ref_mag/a_max0: trailing quantities carry absolute error ~eps*a_max0, so a
+    relative gap g on a quantity of size ref_mag is safe iff g*ref_mag/a_max0
+    clears AMBIGUOUS.  ``first_ambiguous`` is the n_s of the first step with a
+    decision below that bar (None: the whole run is decided robustly)."""
+
+    def __init__(self, a0: float):
+        self.a0 = a0
+        self.raw: dict = {}
+        self.amp: dict = {}
+        self.counts: dict = {}
+        self.step_min = math.inf
+        self.first_ambiguous = None
+        self.per_step: list = []
+
+    def note(self, key: str, gap: float, ref_mag: float):
+        g_amp = gap * ref_mag / self.a0 if self.a0 > 0 else gap
+        self.raw[key] = min(self.raw.get(key, math.inf), gap)
+        self.amp[key] = min(self.amp.get(key, math.inf), g_amp)
+        self.step_min = min(self.step_min, g_amp)
+
+    def count(self, key: str, k: int = 1):
+        self.counts[key] = self.counts.get(key, 0) + k
+
+    def end_step(self, n_s: int):
+        self.per_step.append((n_s, self.step_min))
+        if self.first_ambiguous is None and self.step_min <= AMBIGUOUS:
+            self.first_ambiguous = n_s
+        self.step_min = math.inf
+
+    def summary(self) -> dict:
+        out = dict(self.raw)
+        out.update({k + "_amp": v for k, v in self.amp.items()})
+        out.update(self.counts)
+        out["first_ambiguous"] = self.first_ambiguous
+        out["per_step"] = self.per_step
+        return out
+
+
+# ----------------------------------------------------------------------------
 # the engine (rrqr.py)
 # ----------------------------------------------------------------------------
 
@@ -309,7 +356,7 @@ def swap_plan(base: int, targets: list) -> list:
 
 def qrdm_engine(A, tau=0.15, delta=0.9, k_dm=64, use_delta_max=False,
                 stop_rule=STOP_EPS_N, epsilon=EPS, break_check=True,
-                trace_norms=False, margins=False) -> OracleResult:
+                trace_norms=False, margins=False, max_steps=0) -> OracleResult:
     """QRDM (break_check=False) / QRDM2 (True) -- rrqr.py:315-423 (+ 426-456)."""
     if not 0.0 < tau <= 1.0:
         raise ValueError(f"tau must be in (0, 1], got {tau}")
@@ -331,30 +378,37 @@ def qrdm_engine(A, tau=0.15, delta=0.9, k_dm=64, use_delta_max=False,
     total = 2.0 * m * n
     steps: list = []
     ntrace: list = []
-    mg: dict = {"guard_recomputes": 0} if margins else None
+    mg = _Margins(a0) if margins else None
     eps1 = _eps1(stop_rule, epsilon, n)
     rank = None
     n_s = 0
     while n_s < kmax:
-        # stop test -- rrqr.py:189-203, 336-338
-        if eps1 is not None:
-            lhs = math.sqrt(n - n_s) * float(u[n_s:].max())
-            rhs = eps1 * a0
-            if mg is not None and rhs > 0:
-                mg["stop"] = min(mg.get("stop", math.inf), abs(lhs - rhs) / rhs)
-            if lhs <= rhs:
-                rank = n_s
-                break
+        if max_steps and len(steps) >= max_steps:  # debug: partial factorization
+            break
         ut = u[n_s:]
         umax = float(ut.max())
+        # stop test -- rrqr.py:189-203, 336-338
+        if eps1 is not None:
+            lhs = math.sqrt(n - n_s) * umax
+            rhs = eps1 * a0
+            if mg is not None and rhs > 0:
+                mg.note("stop", abs(lhs - rhs) / rhs, umax)
+            if lhs <= rhs:
+                rank = n_s
+                if mg is not None:
+                    mg.end_step(n_s)
+                break
         if mg is not None and floor > 0:
-            mg["floor"] = min(mg.get("floor", math.inf), abs(umax - floor) / floor)
+            mg.note("floor", abs(umax - floor) / floor, umax)
         if ut.size == 0 or umax <= floor:
             # scalar fallback -- rrqr.py:219-235, 343-353
             s = n_s
             j = s + int(np.argmax(u[s:]))
             if mg is not None:
-                mg["fallback_steps"] = mg.get("fallback_steps", 0) + 1
+                mg.count("fallback_steps")
+                rest = np.delete(u[s:], j - s)
+                if rest.size:
+                    mg.note("argmax", float((umax - rest.max()) / umax) if umax > 0 else 0.0, umax)
             _swap(work, u, uref, fwd, swaps, s, j)
             v, cf, beta = householder(work[s:, s])
             coeffs[s] = cf
@@ -366,25 +420,27 @@ def qrdm_engine(A, tau=0.15, delta=0.9, k_dm=64, use_delta_max=False,
             work[s + 1:, s] = v[1:]
             total += 4.0 * (m - s) + (n - s)
             nh = _downdate(u, uref, work, s, s + 1)
-            if mg is not None:
-                mg["guard_recomputes"] += nh
             total += 4.0 * (n - s - 1)
             if trace_norms:
                 _norm_check(ntrace, u, work, s + 1, a0)
             steps.append(Step(s, 1, 1, fell_back_to_scalar=True))
+            if mg is not None:
+                mg.count("guard_recomputes", nh)
+                mg.end_step(s)
             n_s += 1
             continue
 
         tr: dict | None = {} if mg is not None else None
         sel = select_block(work[n_s:, n_s:], ut, tau, delta, k_dm, use_delta_max, tr)
         if tr:
-            amp = a0 / umax if umax > 0 else 1.0
             for key, val in tr.items():
                 if key == "exact_ties":
-                    mg["exact_ties"] = mg.get("exact_ties", 0) + val
-                    continue
-                mg[key] = min(mg.get(key, math.inf), val)
-                mg[key + "_amp"] = min(mg.get(key + "_amp", math.inf), val / amp)
+                    mg.count("exact_ties", val)
+                    mg.note("exact_ties", 0.0, umax)
+                elif key == "filter":  # cosines carry error ~eps*a0/||c_j||, ||c_j|| >= tau*umax
+                    mg.note(key, val, tau * umax)
+                else:
+                    mg.note(key, val, umax)
         k_s = min(len(sel.cols), kmax - n_s)
         total += (m - n_s) * (sel.k_max + 1) ** 2
         eps_s = tau * float(u[n_s:].max())
@@ -411,7 +467,7 @@ def qrdm_engine(A, tau=0.15, delta=0.9, k_dm=64, use_delta_max=False,
                 nxt = col + 1
                 r = float(col_norms(work[nxt:, nxt])[0])
                 if mg is not None and eps_s > 0:
-                    mg["break"] = min(mg.get("break", math.inf), abs(r - eps_s) / eps_s)
+                    mg.note("break", abs(r - eps_s) / eps_s, eps_s)
                 if r < eps_s:
                     broke = True
                     break
@@ -425,12 +481,13 @@ def qrdm_engine(A, tau=0.15, delta=0.9, k_dm=64, use_delta_max=False,
             total += fl
         n_s1 = n_s + l_acc
         nh = _downdate(u, uref, work, n_s, n_s1)
-        if mg is not None:
-            mg["guard_recomputes"] += nh
         total += 2.0 * l_acc * (n - n_s1) if n_s1 < n else 0.0
         if trace_norms:
             _norm_check(ntrace, u, work, n_s1, a0)
         steps.append(Step(n_s, k_s, l_acc, broke, False, eps_s, sel.gamma, sel.k_max))
+        if mg is not None:
+            mg.count("guard_recomputes", nh)
+            mg.end_step(n_s)
         n_s = n_s1
 
     stopped = rank is not None
@@ -442,7 +499,7 @@ def qrdm_engine(A, tau=0.15, delta=0.9, k_dm=64, use_delta_max=False,
         else:
             rank = n_fact
     return OracleResult(work, coeffs, fwd, swaps, rank, steps, n_fact, stopped,
-                        (rank1, blocked, total), ntrace, mg or {})
+                        (rank1, blocked, total), ntrace, mg.summary() if mg is not None else {})
 
 
 def _norm_check(trace, u, work, n_s1, scale):

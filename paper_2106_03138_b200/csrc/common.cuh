@@ -1,0 +1,106 @@
+// Shared device helpers for the B200 QRDM kernels (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#ifndef DMQR_MAXK
+#define DMQR_MAXK 65   // |J| <= k_dm + 1 with the default k_dm = 64
+#endif
+#define DMQR_KP 72     // DMQR_MAXK padded to the 8-wide DMMA tile
+
+namespace dmqr {
+
+constexpr double kEps = 2.220446049250313e-16;  // 2^-52, rrqr.py:55
+
+// Device-resident control block: every decision of the outer loop lives here,
+// so kernels of one step read what the previous kernel decided without any
+// host round trip.  One per factorization, at the head of the workspace.
+struct Ctl {
+  // fixed at init
+  int64_t m, n, lda, kmax;
+  double a_max0, floor, stop_rhs, tau, delta;
+  int32_t stop_active, break_check, k_dm, use_delta_max;
+  int32_t trace_norms, swap_cap, step_cap, pad0;
+  // loop state
+  int32_t n_s, done, stopped, status;
+  int32_t step_idx, n_swaps, rank, n_factored;
+  // current step decision
+  int32_t kind;   // 0 = deviation-maximization step, 1 = scalar fallback
+  int32_t k_max;  // candidate-set size (dm.py:97), -1 on fallback
+  int32_t nsel;   // |J|
+  int32_t k_s;    // block size min(|J|, kmax - n_s)   rrqr.py:355
+  int32_t l_acc;  // accepted reflectors (< k_s only after a qrdm2 break)
+  int32_t broke;
+  int32_t ncand;  // 1 + k_max
+  int32_t nsw;    // swaps of this step
+  double umax, eps_s, gamma;
+  int32_t cand[DMQR_KP];  // absolute column indices, seed first
+  int32_t sel[DMQR_KP];   // selected absolute indices, seed first
+  int32_t sw_a[DMQR_KP], sw_b[DMQR_KP];
+  // inter-CTA counters (reset by their users)
+  uint32_t gram_count;
+  uint32_t bar_count;
+  uint32_t bar_gen;
+  uint32_t trace_bits_lo, trace_bits_hi;
+  uint32_t pad1[3];
+};
+
+struct StepRec {  // mirrors dmqr_step in include/dmqr_b200.h
+  int64_t n_s, k_selected, k_accepted, k_max;
+  int32_t broke_early, fell_back_to_scalar;
+  double eps_s, gamma;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// DMMA: D(8x8) += A(8x4, row) * B(4x8, col), fp64.  Lowers to SASS DMMA.8x8x4.
+// Fragments (PTX ISA, mma.m8n8k4 .f64):  a: A[lane>>2][lane&3]
+//                                         b: B[lane&3][lane>>2]
+//                                         c0,c1: C[lane>>2][2*(lane&3) + {0,1}]
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Scaled Euclidean norm from (sum of squares, max |x|).  Unscaled sums are exact
+// enough when max|x| keeps squares normal; otherwise callers rescale (see
+// column-norm kernels).  Mirrors column_norms (matrix.py:61-78) up to rounding.
+__device__ __forceinline__ bool norm_range_ok(double amax) {
+  return amax == 0.0 || (amax > 1e-140 && amax < 1e140);
+}
+
+// Grid-wide barrier for cooperatively launched kernels (all CTAs co-resident).
+__device__ __forceinline__ void grid_barrier(uint32_t* count, uint32_t* gen, uint32_t nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile uint32_t* vgen = gen;
+    uint32_t g = *vgen;
+    __threadfence();
+    uint32_t arrived = atomicAdd(count, 1u);
+    if (arrived == nblocks - 1) {
+      atomicExch(count, 0u);
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*vgen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ __forceinline__ int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+}  // namespace dmqr

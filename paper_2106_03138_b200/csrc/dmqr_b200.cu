@@ -1,0 +1,337 @@
+// dmqr_b200: host driver + C-ABI (include/dmqr_b200.h) for the B200 QRDM engine.
+//
+// The outer loop of _qrdm_engine (rrqr.py:315-423) runs as a fixed sequence of
+// stream-ordered kernels per step; every decision (stop, floor/fallback,
+// candidates, filter, swaps, break, n_s advance) is taken ON THE DEVICE and
+// kept in the Ctl block, so the host only sizes grids and watches for `done`.
+// Kernels early-exit once `done` is set, which lets the host enqueue several
+// steps ahead of the last n_s it has seen (grids are sized from that stale
+// n_s, an upper bound on the remaining work).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/dmqr_b200.h"
+#include "common.cuh"
+#include "gram.cuh"
+#include "misc.cuh"
+#include "norms.cuh"
+#include "panel.cuh"
+#include "select.cuh"
+#include "trailing.cuh"
+
+using namespace dmqr;
+
+namespace {
+
+constexpr int GRAM_GMAX = 32;
+constexpr int NSPLIT_MAX = 16;
+constexpr int PANEL_PMAX = 160;
+
+struct Layout {
+  size_t ctl, u, uref, T, red, gram, Zp, Z, V, trace, total;
+};
+
+size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+Layout layout(int64_t m, int64_t n) {
+  Layout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += al(bytes);
+    return o;
+  };
+  L.ctl = take(sizeof(Ctl));
+  L.u = take(sizeof(double) * std::max<int64_t>(n, 1));
+  L.uref = take(sizeof(double) * std::max<int64_t>(n, 1));
+  L.T = take(sizeof(double) * DMQR_KP * DMQR_KP);
+  L.red = take(sizeof(double) * 2 * PANEL_PMAX * RED_LD);
+  L.gram = take(sizeof(double) * GRAM_GMAX * GRAM_PART);
+  L.Zp = take(sizeof(double) * NSPLIT_MAX * DMQR_KP * std::max<int64_t>(n, 1));
+  L.Z = take(sizeof(double) * DMQR_KP * std::max<int64_t>(n, 1));
+  L.V = take(sizeof(double) * DMQR_KP * std::max<int64_t>(m, 1));
+  L.trace = take(sizeof(unsigned long long) * 4);
+  L.total = off;
+  return L;
+}
+
+struct DevInfo {
+  int sms = 148;
+  int coop = 1;
+  size_t smem_optin = 227 * 1024;
+};
+
+DevInfo dev_info() {
+  DevInfo d;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&d.coop, cudaDevAttrCooperativeLaunch, dev);
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  d.smem_optin = (size_t)v;
+  return d;
+}
+
+#define CK(x)                                        \
+  do {                                               \
+    cudaError_t e_ = (x);                            \
+    if (e_ != cudaSuccess) {                         \
+      last_cuda_error() = e_;                        \
+      return DMQR_ECUDA;                             \
+    }                                                \
+  } while (0)
+
+cudaError_t& last_cuda_error() {
+  static thread_local cudaError_t e = cudaSuccess;
+  return e;
+}
+
+bool attrs_done = false;
+
+int set_attrs(const DevInfo& d) {
+  if (attrs_done) return 0;
+  CK(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(GramSmem)));
+  CK(cudaFuncSetAttribute(k_trail_b, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(sizeof(double) * DMQR_KP * (TB_VLD + TB_ZLD))));
+  CK(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)std::min<size_t>(d.smem_optin - 4096, 220 * 1024)));
+  attrs_done = true;
+  return 0;
+}
+
+int validate(int64_t m, int64_t n, int64_t lda, const dmqr_params* p) {
+  if (!p) return DMQR_EINVAL;
+  if (m < 0 || n < 0 || lda < std::max<int64_t>(1, m)) return DMQR_EINVAL;
+  if (!(p->tau > 0.0 && p->tau <= 1.0)) return DMQR_EINVAL;
+  if (!(p->delta >= 0.0 && p->delta < 1.0)) return DMQR_EINVAL;
+  if (p->k_dm < 1 || p->k_dm > DMQR_MAXK - 1) return DMQR_EINVAL;
+  if (p->stop_rule < 0 || p->stop_rule > 2) return DMQR_EINVAL;
+  if (m > 0x7fffffffLL || n > 0x7fffffffLL) return DMQR_EINVAL;
+  return 0;
+}
+
+struct HostHead {  // the prefix of Ctl the host polls
+  int32_t n_s, done, stopped, status;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* dmqr_version(void) {
+  return "dmqr_b200 0.1 (sm_100a, fp64 DMMA)";
+}
+
+const char* dmqr_strerror(int code) {
+  switch (code) {
+    case DMQR_OK: return "ok";
+    case DMQR_EINVAL: return "invalid argument (shape, lda, params or workspace)";
+    case DMQR_ENONFINITE: return "matrix contains NaN or Inf entries";
+    case DMQR_EZEROCOL: return "cosine matrix undefined: zero column present";
+    case DMQR_ECUDA: return cudaGetErrorString(last_cuda_error());
+    case DMQR_ECAP: return "swap or step log capacity exceeded";
+    default: return "unknown error";
+  }
+}
+
+size_t dmqr_workspace_bytes(int64_t m, int64_t n, const dmqr_params* params) {
+  (void)params;
+  return layout(m, n).total;
+}
+
+int dmqr_check_finite_f64(const double* A, int64_t m, int64_t n, int64_t lda, int32_t* nonfinite, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), st));
+  if (m > 0 && n > 0) {
+    int64_t blocks = std::min<int64_t>(ceil_div(m * n, 256), 148 * 16);
+    k_check_finite<<<(unsigned)blocks, 256, 0, st>>>(A, m, n, lda, nonfinite);
+    CK(cudaGetLastError());
+  }
+  return 0;
+}
+
+int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* p, double* coeffs, int64_t* perm,
+                  int64_t* swaps, int64_t swap_cap, dmqr_step* steps, int64_t step_cap, double* norm_trace,
+                  void* workspace, size_t ws_bytes, dmqr_info* info, void* stream) {
+  int rc = validate(m, n, lda, p);
+  if (rc) return rc;
+  if (!info) return DMQR_EINVAL;
+  const Layout L = layout(m, n);
+  if (ws_bytes < L.total || !workspace) return DMQR_EINVAL;
+  if (p->trace_norms && !norm_trace) return DMQR_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const DevInfo d = dev_info();
+  if ((rc = set_attrs(d))) return rc;
+
+  unsigned char* ws = (unsigned char*)workspace;
+  Ctl* ctl = (Ctl*)(ws + L.ctl);
+  double* u = (double*)(ws + L.u);
+  double* uref = (double*)(ws + L.uref);
+  double* T = (double*)(ws + L.T);
+  double* red = (double*)(ws + L.red);
+  double* gpart = (double*)(ws + L.gram);
+  double* Zp = (double*)(ws + L.Zp);
+  double* Z = (double*)(ws + L.Z);
+  double* V = (double*)(ws + L.V);
+  unsigned long long* tbits = (unsigned long long*)(ws + L.trace);
+  StepRec* srec = (StepRec*)steps;
+
+  const int64_t kmax = std::min(m, n);
+  double eps1 = -1.0;
+  if (p->stop_rule == DMQR_STOP_EPS_N) eps1 = p->epsilon * (double)n;
+  if (p->stop_rule == DMQR_STOP_EPS_SQRT_N) eps1 = p->epsilon * std::sqrt((double)n);
+
+  CK(cudaMemsetAsync(ws, 0, L.ctl + sizeof(Ctl), st));
+  CK(cudaMemsetAsync(tbits, 0, sizeof(unsigned long long) * 4, st));
+  CK(cudaMemsetAsync(T, 0, sizeof(double) * DMQR_KP * DMQR_KP, st));
+  if (n > 0) {
+    if (m > 0) {
+      int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)d.sms * 16);
+      k_colnorms_init<<<(unsigned)blocks, 256, 0, st>>>(A, m, n, lda, u, uref);
+    } else {
+      CK(cudaMemsetAsync(u, 0, sizeof(double) * n, st));
+      CK(cudaMemsetAsync(uref, 0, sizeof(double) * n, st));
+    }
+  }
+  InitArgs ia{ctl, u, perm, coeffs, m, n, lda, kmax, p->tau, p->delta, eps1, p->k_dm, p->use_delta_max,
+              p->break_check, p->trace_norms, swap_cap, step_cap};
+  k_init<<<1, 1024, 0, st>>>(ia);
+  CK(cudaGetLastError());
+
+  HostHead* hh = nullptr;
+  CK(cudaMallocHost(&hh, sizeof(HostHead)));
+  int64_t host_ns = 0;
+  int steps_done = 0;
+  const int max_coop_p = std::min(d.sms, PANEL_PMAX);
+  const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
+
+  while (kmax > 0) {
+    const int64_t mp = m - host_ns;
+    const int64_t np = n - host_ns;
+    // ---- selection ----
+    k_select<<<1, SEL_T, 0, st>>>(ctl, u);
+    const int G = (int)std::clamp<int64_t>(ceil_div(mp, 512), 1, GRAM_GMAX);
+    k_gram<<<G, GRAM_T, sizeof(GramSmem), st>>>(ctl, A, gpart);
+    k_swap<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(ctl, A, u, uref, perm, swaps);
+    // ---- panel ----
+    const int kcap = (int)std::min<int64_t>({(int64_t)p->k_dm + 1, (int64_t)DMQR_MAXK, kmax - host_ns});
+    int P = (int)std::clamp<int64_t>(ceil_div(mp, 256), 1, max_coop_p);
+    int64_t rows = ceil_div(mp, P);
+    size_t smem = (size_t)kcap * (size_t)(rows | 1) * sizeof(double);
+    int use_smem = 1;
+    if (smem > panel_smem_cap) {
+      P = max_coop_p;
+      rows = ceil_div(mp, P);
+      smem = (size_t)kcap * (size_t)(rows | 1) * sizeof(double);
+      if (smem > panel_smem_cap) {
+        use_smem = 0;
+        smem = 0;
+      }
+    }
+    PanelArgs pa{ctl, A, coeffs, T, red, use_smem};
+    void* kargs[] = {&pa};
+    if (P > 1) {
+      CK(cudaLaunchCooperativeKernel((void*)k_panel, dim3(P), dim3(PANEL_T), kargs, smem, st));
+    } else {
+      k_panel<<<1, PANEL_T, smem, st>>>(pa);
+    }
+    // ---- trailing update ----
+    const int64_t ncols_ub = std::max<int64_t>(np - 1, 0);
+    if (ncols_ub > 0) {
+      k_form_v<<<dim3((unsigned)ceil_div(mp, 128), DMQR_KP), 128, 0, st>>>(ctl, A, T, V);
+      const int64_t ntile = ceil_div(ncols_ub, TA_COLS);
+      int nsplit = (int)std::clamp<int64_t>(ceil_div(2 * d.sms, ntile), 1, NSPLIT_MAX);
+      nsplit = (int)std::min<int64_t>(nsplit, std::max<int64_t>(1, ceil_div(mp, 256)));
+      k_trail_a<<<dim3((unsigned)ntile, nsplit), TA_T, 0, st>>>(ctl, A, Zp);
+      const int64_t rtot = (int64_t)DMQR_KP * ncols_ub;
+      k_trail_r<<<(unsigned)std::min<int64_t>(ceil_div(rtot, 256), d.sms * 8), 256, 0, st>>>(ctl, Zp, Z, nsplit);
+      k_trail_b<<<dim3((unsigned)ceil_div(mp, TB_ROWS), (unsigned)ceil_div(ncols_ub, TB_COLS)), TB_T,
+                  sizeof(double) * DMQR_KP * (TB_VLD + TB_ZLD), st>>>(ctl, A, V, Z);
+    }
+    // ---- norms, log ----
+    if (np > 0) {
+      const int64_t blocks = std::min<int64_t>(ceil_div(np * 32, 256), (int64_t)d.sms * 16);
+      k_downdate<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, uref);
+      if (p->trace_norms) k_norm_trace<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, tbits);
+    }
+    k_step_end<<<1, 32, 0, st>>>(ctl, srec, norm_trace, tbits);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(hh, &ctl->n_s, sizeof(HostHead), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ++steps_done;
+    host_ns = hh->n_s;
+    if (hh->done) break;
+    if (p->max_steps > 0 && steps_done >= p->max_steps) break;  // debug: stop after N steps
+  }
+  cudaFreeHost(hh);
+  k_finalize<<<1, 256, 0, st>>>(ctl, A, p->stop_rule == DMQR_STOP_NONE);
+  CK(cudaGetLastError());
+  Ctl hc;
+  CK(cudaMemcpyAsync(&hc, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  info->rank = hc.rank;
+  info->n_factored = hc.n_factored;
+  info->n_steps = hc.step_idx;
+  info->n_swaps = hc.n_swaps;
+  info->stopped_early = hc.stopped;
+  info->status = hc.status;
+  info->a_max0 = hc.a_max0;
+  if (kmax == 0) {
+    info->rank = 0;
+    info->n_factored = 0;
+    info->n_steps = 0;
+    info->n_swaps = 0;
+    info->stopped_early = 0;
+  }
+  return hc.status;
+}
+
+int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_t lda, int64_t stride,
+                          const dmqr_params* params, double* coeffs, int64_t* perm, int64_t* swaps, int64_t swap_cap,
+                          dmqr_step* steps, int64_t step_cap, dmqr_info* infos, void* stream) {
+  (void)A; (void)batch; (void)m; (void)n; (void)lda; (void)stride; (void)params; (void)coeffs; (void)perm;
+  (void)swaps; (void)swap_cap; (void)steps; (void)step_cap; (void)infos; (void)stream;
+  return DMQR_EINVAL;  // filled in by the on-chip batched kernel
+}
+
+size_t dmqr_form_q_workspace_bytes(int64_t m, int64_t qcols) {
+  (void)m;
+  return al(sizeof(double) * std::max<int64_t>(qcols, 1));
+}
+
+int dmqr_form_q_f64(const double* packed, int64_t m, int64_t n, int64_t lda, const double* coeffs,
+                    int64_t n_factored, double* Q, int64_t qcols, int64_t ldq, void* workspace, size_t ws_bytes,
+                    void* stream) {
+  if (m < 0 || n < 0 || lda < std::max<int64_t>(1, m) || ldq < std::max<int64_t>(1, m) || qcols < 0 ||
+      qcols > m || n_factored < 0 || n_factored > std::min(m, n))
+    return DMQR_EINVAL;
+  if (ws_bytes < dmqr_form_q_workspace_bytes(m, qcols)) return DMQR_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  double* w = (double*)workspace;
+  if (m == 0 || qcols == 0) return 0;
+  k_q_init<<<(unsigned)std::min<int64_t>(ceil_div(m * qcols, 256), 148 * 16), 256, 0, st>>>(Q, m, qcols, ldq);
+  for (int64_t s = std::min(n_factored, qcols) - 1; s >= 0; --s) {
+    const int64_t cols = qcols - s;
+    k_q_dots<<<(unsigned)ceil_div(cols * 32, 256), 256, 0, st>>>(packed, m, lda, coeffs, s, Q, qcols, ldq, w);
+    k_q_update<<<(unsigned)std::min<int64_t>(ceil_div((m - s) * cols, 256), 148 * 16), 256, 0, st>>>(
+        packed, m, lda, s, Q, qcols, ldq, w);
+  }
+  // reflectors s >= qcols act on rows >= s, where [I; 0] is still zero: no-ops
+  CK(cudaGetLastError());
+  return 0;
+}
+
+/* debug hook (not part of the reference surface): flatten the control block
+ * of a workspace used by dmqr_qrdm_f64 into out[16 + 4*72] int64 (device). */
+int dmqr_debug_ctl(const void* workspace, int64_t* out, void* stream) {
+  k_debug_ctl<<<1, 32, 0, (cudaStream_t)stream>>>((const Ctl*)workspace, out);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+}  // extern "C"

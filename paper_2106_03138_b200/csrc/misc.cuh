@@ -1,0 +1,180 @@
+// Loop bookkeeping kernels: init, step record, final rank; input checks; explicit Q.
+//   a_max0 / floor / kmax     rrqr.py:326-328
+//   StepRecord append         rrqr.py:394-404 (+ fallback record 349-351)
+//   rank / n_factored         rrqr.py:406-412, _posthoc_rank 206-208
+//   dense() finiteness        matrix.py:32-33
+//   reconstruct (explicit Q)  rrqr.py:459-476
+#pragma once
+#include "common.cuh"
+
+namespace dmqr {
+
+struct InitArgs {
+  Ctl* c;
+  const double* u;
+  int64_t* perm;
+  double* coeffs;
+  int64_t m, n, lda, kmax;
+  double tau, delta, eps1;  // eps1 < 0: StopRule.NONE
+  int32_t k_dm, use_delta_max, break_check, trace_norms;
+  int64_t swap_cap, step_cap;
+};
+
+__global__ void __launch_bounds__(1024) k_init(InitArgs a) {
+  __shared__ double red[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double mx = 0.0;
+  for (int64_t j = tid; j < a.n; j += blockDim.x) mx = fmax(mx, a.u[j]);
+  mx = warp_max(mx);
+  if (lane == 0) red[wid] = mx;
+  for (int64_t j = tid; j < a.n; j += blockDim.x) a.perm[j] = j;
+  for (int64_t j = tid; j < a.kmax; j += blockDim.x) a.coeffs[j] = 0.0;
+  __syncthreads();
+  if (wid == 0) {
+    mx = warp_max(lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0);
+    if (lane == 0) {
+      Ctl* c = a.c;
+      c->m = a.m;
+      c->n = a.n;
+      c->lda = a.lda;
+      c->kmax = a.kmax;
+      c->a_max0 = mx;
+      c->floor = (double)a.n * kEps * mx;  // n * EPS * a_max0 (rrqr.py:327)
+      c->stop_active = a.eps1 >= 0.0;
+      c->stop_rhs = a.eps1 >= 0.0 ? a.eps1 * mx : 0.0;
+      c->tau = a.tau;
+      c->delta = a.delta;
+      c->k_dm = a.k_dm;
+      c->use_delta_max = a.use_delta_max;
+      c->break_check = a.break_check;
+      c->trace_norms = a.trace_norms;
+      c->swap_cap = (int32_t)min(a.swap_cap, (int64_t)0x7fffffff);
+      c->step_cap = (int32_t)min(a.step_cap, (int64_t)0x7fffffff);
+      c->n_s = 0;
+      c->done = (a.kmax == 0);
+    }
+  }
+}
+
+// Append the step record and advance n_s (single thread, last kernel of a step).
+__global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, double* __restrict__ norm_trace,
+                           unsigned long long* __restrict__ trace_bits) {
+  if (threadIdx.x != 0 || c->done) return;
+  const int idx = c->step_idx;
+  const int l = c->l_acc;
+  if (idx >= c->step_cap) {
+    c->status = -5;
+    c->done = 1;
+    return;
+  }
+  StepRec r;
+  r.n_s = c->n_s;
+  r.k_selected = c->k_s;
+  r.k_accepted = l;
+  r.k_max = (c->kind == 0) ? c->k_max : -1;
+  r.broke_early = c->broke;
+  r.fell_back_to_scalar = (c->kind == 1);
+  r.eps_s = (c->kind == 0) ? c->eps_s : 0.0;
+  r.gamma = (c->kind == 0) ? c->gamma : 1.0;
+  steps[idx] = r;
+  if (c->trace_norms && norm_trace) {
+    const int64_t n_s1 = c->n_s + l;
+    // _record_norm_check appends nothing once the trailing block is empty
+    norm_trace[idx] = (n_s1 < c->n) ? __longlong_as_double((long long)*trace_bits) : __longlong_as_double(-1ll);
+    *trace_bits = 0ull;
+  }
+  c->n_s += l;
+  c->step_idx = idx + 1;
+  c->l_acc = 0;
+  c->broke = 0;
+  c->nsw = 0;
+  if (c->n_s >= c->kmax) c->done = 1;
+}
+
+// rank / n_factored (rrqr.py:406-412)
+__global__ void k_finalize(Ctl* __restrict__ c, const double* __restrict__ A, int stop_none) {
+  __shared__ int cnt[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t n_s = c->n_s;
+  const int64_t nf = c->stopped ? n_s : min(n_s, c->kmax);
+  const double thr = kEps * (double)c->n * c->a_max0;
+  int k = 0;
+  if (stop_none && !c->stopped)
+    for (int64_t i = tid; i < nf; i += blockDim.x) k += fabs(A[i + i * c->lda]) > thr;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+  if (lane == 0) cnt[wid] = k;
+  __syncthreads();
+  if (tid == 0) {
+    int tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += cnt[w];
+    c->n_factored = (int32_t)nf;
+    c->rank = c->stopped ? (int32_t)n_s : (stop_none ? tot : (int32_t)nf);
+  }
+}
+
+__global__ void k_check_finite(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+                               int32_t* __restrict__ flag) {
+  const int64_t tot = m * n;
+  int bad = 0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / m, i = e % m;
+    bad |= !isfinite(A[i + j * lda]);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// ---- explicit Q (reconstruct, rrqr.py:468-476): backward accumulation ----
+// Q starts as [I; 0] (m x qcols).  For s = p-1 .. 0: Q[s:, s:] -= v (coeff v^T Q[s:, s:]);
+// columns < s of Q are still unit vectors there, so only columns >= s change.
+__global__ void k_q_init(double* __restrict__ Q, int64_t m, int64_t qcols, int64_t ldq) {
+  const int64_t tot = m * qcols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / m, i = e % m;
+    Q[i + j * ldq] = (i == j) ? 1.0 : 0.0;
+  }
+}
+
+// w[j] = coeff * v^T Q[s:, j] for j in [s, qcols): warp per column
+__global__ void k_q_dots(const double* __restrict__ P, int64_t m, int64_t lda, const double* __restrict__ coeffs,
+                         int64_t s, const double* __restrict__ Q, int64_t qcols, int64_t ldq, double* __restrict__ w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = s + ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  if (j >= qcols) return;
+  const double* v = P + s * lda;
+  const double* q = Q + j * ldq;
+  double acc = 0.0;
+  for (int64_t r = s + lane; r < m; r += 32) acc = fma(r == s ? 1.0 : v[r], q[r], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) w[j] = coeffs[s] * acc;
+}
+
+__global__ void k_q_update(const double* __restrict__ P, int64_t m, int64_t lda, int64_t s, double* __restrict__ Q,
+                           int64_t qcols, int64_t ldq, const double* __restrict__ w) {
+  const int64_t rows = m - s, cols = qcols - s;
+  const int64_t tot = rows * cols;
+  const double* v = P + s * lda;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = s + e / rows, r = s + e % rows;
+    const double vr = (r == s) ? 1.0 : v[r];
+    Q[r + j * ldq] -= vr * w[j];
+  }
+}
+
+}  // namespace dmqr
+
+namespace dmqr {
+// debug: flatten the decision part of Ctl (for step-by-step comparisons)
+__global__ void k_debug_ctl(const Ctl* __restrict__ c, int64_t* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  int64_t* o = out;
+  *o++ = c->n_s; *o++ = c->done; *o++ = c->stopped; *o++ = c->status;
+  *o++ = c->kind; *o++ = c->k_max; *o++ = c->ncand; *o++ = c->nsel; *o++ = c->k_s; *o++ = c->l_acc;
+  *o++ = c->nsw; *o++ = c->step_idx; *o++ = c->n_swaps;
+  *o++ = __double_as_longlong(c->umax); *o++ = __double_as_longlong(c->eps_s); *o++ = __double_as_longlong(c->gamma);
+  for (int i = 0; i < DMQR_KP; ++i) *o++ = c->cand[i];
+  for (int i = 0; i < DMQR_KP; ++i) *o++ = c->sel[i];
+  for (int i = 0; i < DMQR_KP; ++i) *o++ = c->sw_a[i];
+  for (int i = 0; i < DMQR_KP; ++i) *o++ = c->sw_b[i];
+}
+}  // namespace dmqr

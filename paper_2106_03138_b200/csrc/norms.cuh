@@ -1,0 +1,112 @@
+// Column norms, partial-norm downdate with cancellation guard, norm trace.
+//   column_norms          matrix.py:61-78
+//   PartialNorms.from_matrix rrqr.py:126-129
+//   downdate_norms        rrqr.py:161-186
+//   _record_norm_check    rrqr.py:211-216
+// HBM-bound: one warp per column, coalesced 256 B row segments, shuffle
+// reductions; the guard recompute re-reads only the flagged columns.
+#pragma once
+#include "common.cuh"
+
+namespace dmqr {
+
+// Norm of a contiguous column segment of length len, computed by one warp
+// (all lanes return the result).  Unscaled sum of squares when the max
+// magnitude keeps squares normal, else a second max-scaled pass (the
+// reference's scaling, matrix.py:73-77).
+__device__ __forceinline__ double warp_col_norm(const double* __restrict__ x, int64_t len, int lane) {
+  double s0 = 0.0, s1 = 0.0, a0 = 0.0, a1 = 0.0;
+  int64_t i = lane;
+  for (; i + 32 < len; i += 64) {
+    double p = __ldg(x + i), q = __ldg(x + i + 32);
+    s0 = fma(p, p, s0);
+    s1 = fma(q, q, s1);
+    a0 = fmax(a0, fabs(p));
+    a1 = fmax(a1, fabs(q));
+  }
+  if (i < len) {
+    double p = __ldg(x + i);
+    s0 = fma(p, p, s0);
+    a0 = fmax(a0, fabs(p));
+  }
+  double s = warp_sum(s0 + s1);
+  double amax = warp_max(fmax(a0, a1));
+  if (norm_range_ok(amax)) return sqrt(s);
+  double t = 0.0;
+  for (int64_t k = lane; k < len; k += 32) {
+    double y = __ldg(x + k) / amax;
+    t = fma(y, y, t);
+  }
+  t = warp_sum(t);
+  return amax * sqrt(t);
+}
+
+// u[j] = u_ref[j] = ||A[:, j]||  (PartialNorms.from_matrix)
+__global__ void k_colnorms_init(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+                                double* __restrict__ u, double* __restrict__ uref) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t j = w0; j < n; j += nw) {
+    double r = warp_col_norm(A + j * lda, m, lane);
+    if (lane == 0) {
+      u[j] = r;
+      uref[j] = r;
+    }
+  }
+}
+
+// Downdate after a step that produced R rows [n_s, n_s1): rrqr.py:161-186.
+// Columns whose downdated square falls to <= 1e-2 * u_ref^2 are recomputed
+// exactly from rows n_s1.. and their u_ref refreshed.
+__global__ void k_downdate(Ctl* __restrict__ c, const double* __restrict__ A, double* __restrict__ u,
+                           double* __restrict__ uref) {
+  if (c->done) return;
+  const int64_t n_s = c->n_s, n_s1 = n_s + c->l_acc, n = c->n, m = c->m, lda = c->lda;
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0)
+    for (int64_t j = n_s + threadIdx.x; j < n_s1; j += blockDim.x) {
+      u[j] = 0.0;
+      uref[j] = 0.0;
+    }
+  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t j = n_s1 + w0; j < n; j += nw) {
+    const double* col = A + j * lda;
+    double d = 0.0;
+    for (int64_t r = n_s + lane; r < n_s1; r += 32) {
+      double x = col[r];
+      d = fma(x, x, d);
+    }
+    d = warp_sum(d);
+    const double uj = u[j], rj = uref[j];
+    const double sq = __dsub_rn(__dmul_rn(uj, uj), d);
+    double nu = sqrt(fmax(sq, 0.0));
+    if (sq <= __dmul_rn(1e-2, __dmul_rn(rj, rj))) {
+      nu = warp_col_norm(col + n_s1, m - n_s1, lane);
+      if (lane == 0) uref[j] = nu;
+    }
+    if (lane == 0) u[j] = nu;
+  }
+}
+
+// Max relative deviation of downdated vs fresh trailing norms (rrqr.py:211-216),
+// accumulated as the bit pattern of a non-negative double (monotone under atomicMax).
+__global__ void k_norm_trace(Ctl* __restrict__ c, const double* __restrict__ A, const double* __restrict__ u,
+                             unsigned long long* __restrict__ out_bits) {
+  if (c->done || !c->trace_norms) return;
+  const int64_t n_s1 = c->n_s + c->l_acc, n = c->n, m = c->m, lda = c->lda;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const double floor_ = kEps * c->a_max0;
+  double worst = 0.0;
+  for (int64_t j = n_s1 + w0; j < n; j += nw) {
+    double direct = warp_col_norm(A + j * lda + n_s1, m - n_s1, lane);
+    double den = fmax(fmax(direct, floor_), 2.2250738585072014e-308);
+    worst = fmax(worst, fabs(u[j] - direct) / den);
+  }
+  if (lane == 0 && worst > 0.0) atomicMax(out_bits, (unsigned long long)__double_as_longlong(worst));
+}
+
+}  // namespace dmqr

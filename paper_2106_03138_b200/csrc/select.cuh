@@ -1,0 +1,288 @@
+// Stop test, norm-floor test, seed argmax and the tau-candidate set.
+//   check_stop      rrqr.py:189-203 (called at rrqr.py:336-338)
+//   floor test      dm.py:139-143 -> NormFloorSignal -> scalar step rrqr.py:343-353
+//   candidate_set   dm.py:81-97: seed = first argmax; {i != seed : u_i >= tau*u_seed}
+//                   stably sorted by -u (ties -> smaller index), truncated to k_dm
+// One CTA of 1024 threads over the trailing norms (n' <= a few 10^4 doubles,
+// L2-resident).  Top-k_dm is a radix select on the IEEE bits of the
+// non-negative norms (8 passes of 8 bits) followed by an index-ordered
+// compaction of the tie class, so the result equals the reference's stable
+// argsort exactly.
+#pragma once
+#include "common.cuh"
+
+namespace dmqr {
+
+constexpr int SEL_T = 1024;
+
+struct SelSmem {
+  double red_v[32];
+  int red_i[32];
+  int scan[32];
+  unsigned hist[256];
+  int list_i[DMQR_KP * 2];
+  double list_u[DMQR_KP * 2];
+  int bc_i[4];
+  unsigned long long bc_u64[2];
+  double bc_d[2];
+};
+
+// exclusive block scan of one int per thread (1024 threads); returns prefix, writes total
+__device__ __forceinline__ int block_excl_scan(int v, int* scan_smem, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) scan_smem[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int t = scan_smem[lane];
+    int s = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    scan_smem[lane] = s - t;  // exclusive warp offsets
+    if (lane == 31) *total = s;
+  }
+  __syncthreads();
+  int res = scan_smem[wid] + x - v;
+  __syncthreads();
+  return res;
+}
+
+__global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const double* __restrict__ u) {
+  if (c->done) return;
+  __shared__ SelSmem sm;
+  __shared__ int s_total;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int n_s = c->n_s;
+  const int n = (int)c->n;
+  if (n_s >= c->kmax) {  // loop condition of rrqr.py:335
+    if (tid == 0) c->done = 1;
+    return;
+  }
+  const int np = n - n_s;
+  // contiguous per-thread segments keep index order for compaction
+  const int seg = (np + SEL_T - 1) / SEL_T;
+  const int s0 = n_s + tid * seg;
+  const int s1 = min(n, s0 + seg);
+
+  // ---- first argmax over u[n_s:] (np.argmax semantics) ----
+  double bv = -1.0;
+  int bi = 0x7fffffff;
+  for (int i = s0; i < s1; ++i) {
+    double v = u[i];
+    if (v > bv) {
+      bv = v;
+      bi = i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    sm.red_v[wid] = bv;
+    sm.red_i[wid] = bi;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    bv = sm.red_v[lane];
+    bi = sm.red_i[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      sm.bc_d[0] = bv;
+      sm.bc_i[0] = bi;
+    }
+  }
+  __syncthreads();
+  const double umax = sm.bc_d[0];
+  const int seed = sm.bc_i[0];
+
+  // ---- stop test (rrqr.py:197-203) ----
+  if (c->stop_active) {
+    const double lhs = sqrt((double)(n - n_s)) * umax;
+    if (lhs <= c->stop_rhs) {
+      if (tid == 0) {
+        c->stopped = 1;
+        c->done = 1;
+      }
+      return;
+    }
+  }
+  // ---- norm floor -> scalar fallback step (dm.py:140, rrqr.py:219-235) ----
+  if (umax <= c->floor) {
+    if (tid == 0) {
+      c->kind = 1;
+      c->k_max = -1;
+      c->umax = umax;
+      c->ncand = 1;
+      c->cand[0] = seed;
+      c->nsel = 1;
+      c->sel[0] = seed;
+      c->k_s = 1;
+      c->eps_s = 0.0;
+      c->gamma = 1.0;
+      c->nsw = (seed != n_s) ? 1 : 0;
+      c->sw_a[0] = n_s;
+      c->sw_b[0] = seed;
+    }
+    return;
+  }
+
+  // ---- candidate set (dm.py:81-97) ----
+  const double thr = c->tau * umax;
+  const int k_dm = c->k_dm;
+  int cnt = 0;
+  for (int i = s0; i < s1; ++i) cnt += (i != seed && u[i] >= thr);
+  int total;
+  int off = block_excl_scan(cnt, sm.scan, &s_total);
+  __syncthreads();
+  total = s_total;
+
+  int nlist;
+  if (total <= k_dm) {
+    // all candidates, index order
+    int p = off;
+    for (int i = s0; i < s1; ++i)
+      if (i != seed && u[i] >= thr) {
+        sm.list_i[p] = i;
+        sm.list_u[p] = u[i];
+        ++p;
+      }
+    nlist = total;
+  } else {
+    // radix select of the k_dm-th largest key among candidates
+    unsigned long long prefix = 0ull, mask = 0ull;
+    int k = k_dm;
+    for (int pass = 0; pass < 8; ++pass) {
+      const int shift = 56 - 8 * pass;
+      for (int b = tid; b < 256; b += SEL_T) sm.hist[b] = 0u;
+      __syncthreads();
+      for (int i = s0; i < s1; ++i) {
+        double v = u[i];
+        if (i == seed || !(v >= thr)) continue;
+        unsigned long long key = (unsigned long long)__double_as_longlong(v);
+        if ((key & mask) == prefix) atomicAdd(&sm.hist[(key >> shift) & 255ull], 1u);
+      }
+      __syncthreads();
+      if (wid == 0) {
+        // bins 255..0 in descending order; lane handles 8 consecutive bins from the top
+        unsigned cnts[8];
+        unsigned lsum = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          cnts[q] = sm.hist[255 - (lane * 8 + q)];
+          lsum += cnts[q];
+        }
+        unsigned incl = lsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        unsigned excl = incl - lsum;
+        // the lane whose range contains the k-th element
+        bool mine = (excl < (unsigned)k) && ((unsigned)k <= incl);
+        unsigned ball = __ballot_sync(0xffffffffu, mine);
+        int owner = __ffs(ball) - 1;
+        if (lane == owner) {
+          unsigned run = excl;
+          int digit = 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (run + cnts[q] >= (unsigned)k) {
+              digit = 255 - (lane * 8 + q);
+              break;
+            }
+            run += cnts[q];
+          }
+          sm.bc_i[1] = digit;
+          sm.bc_i[2] = k - (int)run;
+        }
+      }
+      __syncthreads();
+      prefix |= (unsigned long long)sm.bc_i[1] << shift;
+      mask |= 255ull << shift;
+      k = sm.bc_i[2];
+      __syncthreads();
+    }
+    const unsigned long long T = prefix;
+    const int k_rem = k;  // elements equal to T to take, smallest index first
+    // greater-than count and equal count per thread (index order)
+    int gt = 0, eq = 0;
+    for (int i = s0; i < s1; ++i) {
+      double v = u[i];
+      if (i == seed || !(v >= thr)) continue;
+      unsigned long long key = (unsigned long long)__double_as_longlong(v);
+      gt += key > T;
+      eq += key == T;
+    }
+    int dummy;
+    int off_gt = block_excl_scan(gt, sm.scan, &dummy);
+    int off_eq = block_excl_scan(eq, sm.scan, &s_total);
+    __syncthreads();
+    const int total_gt = k_dm - k_rem;
+    int pg = off_gt, pe = off_eq;
+    for (int i = s0; i < s1; ++i) {
+      double v = u[i];
+      if (i == seed || !(v >= thr)) continue;
+      unsigned long long key = (unsigned long long)__double_as_longlong(v);
+      if (key > T) {
+        sm.list_i[pg] = i;
+        sm.list_u[pg] = v;
+        ++pg;
+      } else if (key == T) {
+        if (pe < k_rem) {
+          sm.list_i[total_gt + pe] = i;
+          sm.list_u[total_gt + pe] = v;
+        }
+        ++pe;
+      }
+    }
+    nlist = k_dm;
+  }
+  __syncthreads();
+  // ---- stable descending sort of the <= k_dm candidates by rank counting ----
+  int my_i = 0, my_rank = 0;
+  double my_u = 0.0;
+  if (tid < nlist) {
+    my_i = sm.list_i[tid];
+    my_u = sm.list_u[tid];
+    for (int q = 0; q < nlist; ++q) {
+      double ou = sm.list_u[q];
+      int oi = sm.list_i[q];
+      my_rank += (ou > my_u) || (ou == my_u && oi < my_i);
+    }
+  }
+  __syncthreads();
+  if (tid < nlist) c->cand[1 + my_rank] = my_i;
+  if (tid == 0) {
+    c->kind = 0;
+    c->k_max = nlist;
+    c->ncand = 1 + nlist;
+    c->cand[0] = seed;
+    c->umax = umax;
+  }
+}
+
+}  // namespace dmqr

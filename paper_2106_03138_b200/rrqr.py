@@ -1,0 +1,407 @@
+"""Drop-in QRDM / QRDM2 drivers backed by the B200 kernels.
+
+Same call and result surface as the reference ``dmqr.rrqr`` (rrqr.py:39-53,
+426-456) and ``dmqr.dm.DMParams`` (dm.py:41-62):
+
+    qrdm (A, params=DMParams(), stop=StopCriterion(), trace_norms=False) -> RRQRResult
+    qrdm2(A, params=DMParams(), stop=StopCriterion(), trace_norms=False) -> RRQRResult
+
+The factorization itself runs in ``libdmqr_b200.so`` (hand-written sm_100a
+CUDA, called through the C-ABI in include/dmqr_b200.h).  PyTorch only carries
+device buffers and the stream.  There is no CPU fallback: without a CUDA
+device or the built library these functions raise.
+
+Differences from the reference that are by design:
+  * ``packed``/``coeffs`` come back as numpy arrays by default (as in the
+    reference); ``device=True`` keeps them as torch CUDA tensors.
+  * k_dm is limited to <= 64 (the paper's recommended block size is 64).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+
+from . import _lib
+
+EPS = float(np.finfo(np.float64).eps)
+K_DM_MAX = 64
+
+__all__ = [
+    "EPS", "DMParams", "StopRule", "StopCriterion", "StepRecord", "WorkCounters", "Permutation",
+    "RRQRResult", "qrdm", "qrdm2", "reconstruct", "factorize",
+]
+
+
+# ----------------------------------------------------------------------------
+# parameter / result types (mirrors of dm.py:41-78 and rrqr.py:58-158)
+# ----------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class DMParams:
+    """tau in (0, 1], delta in [0, 1), k_dm >= 1 -- dm.py:41-62 (same messages)."""
+
+    tau: float = 0.15
+    delta: float = 0.9
+    k_dm: int = 64
+    use_delta_max: bool = False
+
+    def __post_init__(self):
+        if not 0.0 < self.tau <= 1.0:
+            raise ValueError(f"tau must be in (0, 1], got {self.tau}")
+        if not 0.0 <= self.delta < 1.0:
+            raise ValueError(f"delta must be in [0, 1), got {self.delta}")
+        if self.k_dm < 1:
+            raise ValueError(f"k_dm must be >= 1, got {self.k_dm}")
+
+
+class StopRule(Enum):
+    EPS_N = "n"
+    EPS_SQRT_N = "sqrt-n"
+    NONE = "none"
+
+
+_RULE_CODE = {StopRule.EPS_N: 0, StopRule.EPS_SQRT_N: 1, StopRule.NONE: 2}
+
+
+@dataclass(frozen=True)
+class StopCriterion:
+    variant: StopRule = StopRule.EPS_N
+    epsilon: float = EPS
+
+    @classmethod
+    def from_name(cls, name: str) -> "StopCriterion":
+        return cls(StopRule(name))
+
+    def eps1(self, n: int):
+        if self.variant is StopRule.EPS_N:
+            return self.epsilon * n
+        if self.variant is StopRule.EPS_SQRT_N:
+            return self.epsilon * math.sqrt(n)
+        return None
+
+
+@dataclass
+class StepRecord:
+    n_s: int
+    k_selected: int
+    k_accepted: int
+    broke_early: bool = False
+    fell_back_to_scalar: bool = False
+    eps_s: float = 0.0
+    gamma: float = 1.0
+    k_max: int = -1  # extra: candidate-set size (not in the reference record)
+
+
+@dataclass
+class WorkCounters:
+    rank1_flops: float = 0.0
+    blocked_flops: float = 0.0
+    total_flops: float = 0.0
+
+    @property
+    def rank1_fraction(self) -> float:
+        return self.rank1_flops / self.total_flops if self.total_flops else 0.0
+
+    @property
+    def blocked_fraction(self) -> float:
+        return self.blocked_flops / self.total_flops if self.total_flops else 0.0
+
+
+class Permutation:
+    """forward map + swap log (matrix.py:90-152)."""
+
+    def __init__(self, n: int):
+        self.forward = np.arange(n, dtype=np.intp)
+        self.swaps: list = []
+
+    @property
+    def n(self) -> int:
+        return int(self.forward.size)
+
+    def replay(self) -> np.ndarray:
+        fwd = np.arange(self.n, dtype=np.intp)
+        for i, j in self.swaps:
+            fwd[i], fwd[j] = fwd[j], fwd[i]
+        return fwd
+
+    def inverse(self) -> np.ndarray:
+        inv = np.empty(self.n, dtype=np.intp)
+        inv[self.forward] = np.arange(self.n, dtype=np.intp)
+        return inv
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, Permutation) and np.array_equal(self.forward, other.forward)
+
+    def __repr__(self) -> str:
+        return f"Permutation({list(self.forward)})"
+
+
+@dataclass
+class RRQRResult:
+    packed: object
+    coeffs: object
+    perm: Permutation
+    rank: int
+    step_log: list
+    n_factored: int
+    stopped_early: bool
+    counters: WorkCounters = field(default_factory=WorkCounters)
+    norm_trace: list = field(default_factory=list)
+    device_time_ms: float | None = None
+
+    @property
+    def m(self) -> int:
+        return int(self.packed.shape[0])
+
+    @property
+    def n(self) -> int:
+        return int(self.packed.shape[1])
+
+    def r_diagonal(self):
+        d = self.packed.diagonal()[: self.n_factored]
+        return d.copy() if isinstance(d, np.ndarray) else d.clone()
+
+
+# ----------------------------------------------------------------------------
+# counters replay (rrqr.py:330,356,366-373,384-391,230-235,346) -- SURVEY App. C
+# ----------------------------------------------------------------------------
+
+def replay_counters(m: int, n: int, steps: list) -> WorkCounters:
+    wc = WorkCounters(total_flops=2.0 * m * n)
+    for st in steps:
+        s = st.n_s
+        if st.fell_back_to_scalar:
+            if s + 1 < n:
+                f = 4.0 * (m - s) * (n - s - 1)
+                wc.rank1_flops += f
+                wc.total_flops += f
+            wc.total_flops += 4.0 * (m - s) + (n - s)
+            wc.total_flops += 4.0 * (n - s - 1)
+            continue
+        k_s, l = st.k_selected, st.k_accepted
+        wc.total_flops += (m - s) * (st.k_max + 1) ** 2
+        for col in range(s, s + l):
+            if col + 1 < s + k_s:
+                f = 4.0 * (m - col) * (s + k_s - col - 1)
+                wc.rank1_flops += f
+                wc.total_flops += f
+            wc.total_flops += 4.0 * (m - col)
+        if s + k_s < n:
+            wc.total_flops += 2.0 * (m - s) * l ** 2
+            f = (4.0 * (m - s) * l + 2.0 * l ** 2) * (n - s - k_s)
+            wc.blocked_flops += f
+            wc.total_flops += f
+        s1 = s + l
+        wc.total_flops += 2.0 * l * (n - s1) if s1 < n else 0.0
+    return wc
+
+
+# ----------------------------------------------------------------------------
+# device plumbing
+# ----------------------------------------------------------------------------
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2106_03138_b200 needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+def _check(rc: int):
+    if rc == 0:
+        return
+    msg = _lib.strerror(rc)
+    if rc in (_lib.DMQR_EINVAL, _lib.DMQR_ENONFINITE, _lib.DMQR_EZEROCOL):
+        raise ValueError(msg)
+    raise RuntimeError(f"dmqr_b200: {msg} (code {rc})")
+
+
+def lda_for(m: int) -> int:
+    """Leading dimension: rows rounded up to 8 doubles (64-byte aligned columns)."""
+    return max(8, (m + 7) // 8 * 8)
+
+
+def to_work(A, device=None):
+    """Validated column-major float64 device copy of A (dense(), matrix.py:24-34).
+
+    Returns (buf, m, n, lda) where ``buf`` is an (n, lda) torch tensor whose
+    row j is column j of the matrix.
+    """
+    torch = _torch()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if isinstance(A, torch.Tensor):
+        t = A.detach()
+        if t.dim() != 2:
+            raise ValueError(f"expected a 2-d array, got ndim={t.dim()}")
+        t = t.to(device=dev, dtype=torch.float64)
+    else:
+        a = np.asarray(A, dtype=np.float64)
+        if a.ndim != 2:
+            raise ValueError(f"expected a 2-d array, got ndim={a.ndim}")
+        t = torch.from_numpy(np.ascontiguousarray(a.T)).to(dev, non_blocking=False).T
+    m, n = int(t.shape[0]), int(t.shape[1])
+    lda = lda_for(m)
+    buf = torch.zeros((max(n, 1), lda), dtype=torch.float64, device=dev)
+    if m and n:
+        buf[:n, :m].copy_(t.T)
+    return buf, m, n, lda
+
+
+@dataclass
+class DeviceFactor:
+    """Raw device outputs of one factorization (no host copies)."""
+
+    buf: object          # (n, lda) torch tensor, column-major packed factor
+    m: int
+    n: int
+    lda: int
+    coeffs: object       # torch (kmax,)
+    perm: object         # torch int64 (n,)
+    swaps: object        # torch int64 (cap, 2)
+    steps: object        # torch uint8 raw records
+    norm_trace: object
+    info: _lib.Info
+    workspace: object = None
+
+    def debug_ctl(self) -> dict:
+        """Decision state of the last step (debug aid)."""
+        import torch
+        out = torch.zeros(16 + 4 * 72, dtype=torch.int64, device=self.buf.device)
+        _check(_lib.load().dmqr_debug_ctl(self.workspace.data_ptr(), out.data_ptr(),
+                                          C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        v = out.cpu().numpy()
+        keys = ["n_s", "done", "stopped", "status", "kind", "k_max", "ncand", "nsel", "k_s", "l_acc", "nsw",
+                "step_idx", "n_swaps"]
+        d = {k: int(v[i]) for i, k in enumerate(keys)}
+        for i, k in enumerate(["umax", "eps_s", "gamma"]):
+            d[k] = float(v[13 + i:14 + i].view(np.float64)[0])
+        d["cand"], d["sel"] = v[16:88].tolist(), v[88:160].tolist()
+        d["sw_a"], d["sw_b"] = v[160:232].tolist(), v[232:304].tolist()
+        return d
+
+
+def factorize(A, params: DMParams = DMParams(), stop: StopCriterion = StopCriterion(),
+              break_check: bool = True, trace_norms: bool = False, stream=None, work=None,
+              max_steps: int = 0) -> DeviceFactor:
+    """Run one factorization on the device; returns device buffers.
+
+    ``work`` may be a (buf, m, n, lda) tuple from ``to_work`` whose buffer is
+    factored in place (the benchmark uses this to keep inputs resident).
+    """
+    torch = _torch()
+    lib = _lib.load()
+    if params.k_dm > K_DM_MAX:
+        raise ValueError(f"k_dm > {K_DM_MAX} is not supported by the B200 engine")
+    buf, m, n, lda = work if work is not None else to_work(A)
+    dev = buf.device
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    sh = C.c_void_p(st.cuda_stream)
+    if m and n:
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        _check(lib.dmqr_check_finite_f64(buf.data_ptr(), m, n, lda, flag.data_ptr(), sh))
+        if int(flag.item()):
+            raise ValueError("matrix contains NaN or Inf entries")
+    p = _lib.Params(tau=float(params.tau), delta=float(params.delta), epsilon=float(stop.epsilon),
+                    k_dm=int(params.k_dm), use_delta_max=int(bool(params.use_delta_max)),
+                    stop_rule=_RULE_CODE[stop.variant], break_check=int(bool(break_check)),
+                    trace_norms=int(bool(trace_norms)), max_steps=int(max_steps))
+    kmax = min(m, n)
+    step_cap = max(kmax, 1)
+    swap_cap = max(kmax * (params.k_dm + 1) + 8, 8)
+    coeffs = torch.zeros(max(kmax, 1), dtype=torch.float64, device=dev)
+    perm = torch.arange(max(n, 1), dtype=torch.int64, device=dev)
+    swaps = torch.empty((swap_cap, 2), dtype=torch.int64, device=dev)
+    steps = torch.empty(step_cap * _lib.STEP_BYTES, dtype=torch.uint8, device=dev)
+    ntrace = torch.full((step_cap,), float("nan"), dtype=torch.float64, device=dev) if trace_norms else None
+    wsb = int(lib.dmqr_workspace_bytes(m, n, C.byref(p)))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    info = _lib.Info()
+    rc = lib.dmqr_qrdm_f64(buf.data_ptr(), m, n, lda, C.byref(p), coeffs.data_ptr(), perm.data_ptr(),
+                           swaps.data_ptr(), swap_cap, steps.data_ptr(), step_cap,
+                           ntrace.data_ptr() if ntrace is not None else None, ws.data_ptr(), wsb,
+                           C.byref(info), sh)
+    _check(rc)
+    return DeviceFactor(buf, m, n, lda, coeffs[:kmax], perm[:n], swaps, steps, ntrace, info, ws)
+
+
+def _steps_from_raw(raw: np.ndarray, count: int) -> list:
+    recs = np.frombuffer(raw[: count * _lib.STEP_BYTES].tobytes(), dtype=np.dtype([
+        ("n_s", "<i8"), ("k_selected", "<i8"), ("k_accepted", "<i8"), ("k_max", "<i8"),
+        ("broke_early", "<i4"), ("fell_back_to_scalar", "<i4"), ("eps_s", "<f8"), ("gamma", "<f8")]))
+    return [StepRecord(int(r["n_s"]), int(r["k_selected"]), int(r["k_accepted"]), bool(r["broke_early"]),
+                       bool(r["fell_back_to_scalar"]), float(r["eps_s"]), float(r["gamma"]), int(r["k_max"]))
+            for r in recs]
+
+
+def to_result(f: DeviceFactor, device: bool = False) -> RRQRResult:
+    info = f.info
+    packed_t = f.buf[: f.n, : f.m].T  # m x n view
+    steps = _steps_from_raw(f.steps.cpu().numpy(), int(info.n_steps))
+    perm = Permutation(f.n)
+    perm.forward = f.perm.cpu().numpy().astype(np.intp)
+    sw = f.swaps[: int(info.n_swaps)].cpu().numpy()
+    perm.swaps = [(int(a), int(b)) for a, b in sw]
+    trace = []
+    if f.norm_trace is not None:
+        tr = f.norm_trace[: int(info.n_steps)].cpu().numpy()
+        trace = [float(x) for x in tr if not np.isnan(x)]
+    if device:
+        packed, coeffs = packed_t, f.coeffs
+    else:
+        packed = np.asfortranarray(packed_t.cpu().numpy()) if f.m and f.n else np.zeros((f.m, f.n), order="F")
+        coeffs = f.coeffs.cpu().numpy() if min(f.m, f.n) else np.zeros(0)
+    return RRQRResult(packed=packed, coeffs=coeffs, perm=perm, rank=int(info.rank), step_log=steps,
+                      n_factored=int(info.n_factored), stopped_early=bool(info.stopped_early),
+                      counters=replay_counters(f.m, f.n, steps), norm_trace=trace)
+
+
+def qrdm(A, params: DMParams = DMParams(), stop: StopCriterion = StopCriterion(),
+         trace_norms: bool = False, device: bool = False) -> RRQRResult:
+    """Blocked QR with deviation-maximization pivoting (rrqr.py:426-440), on the B200."""
+    return to_result(factorize(A, params, stop, break_check=False, trace_norms=trace_norms), device)
+
+
+def qrdm2(A, params: DMParams = DMParams(), stop: StopCriterion = StopCriterion(),
+          trace_norms: bool = False, device: bool = False) -> RRQRResult:
+    """``qrdm`` plus the within-block break check (rrqr.py:443-456), on the B200."""
+    return to_result(factorize(A, params, stop, break_check=True, trace_norms=trace_norms), device)
+
+
+def form_q(packed, coeffs, n_factored: int, qcols: int | None = None):
+    """Explicit Q (m x qcols, default m) on the device (rrqr.py:468-476)."""
+    torch = _torch()
+    lib = _lib.load()
+    P = packed if isinstance(packed, torch.Tensor) else torch.as_tensor(np.asarray(packed, dtype=np.float64))
+    P = P.to("cuda", torch.float64)
+    m, n = int(P.shape[0]), int(P.shape[1])
+    qcols = m if qcols is None else int(qcols)
+    lda = lda_for(m)
+    pbuf = torch.zeros((max(n, 1), lda), dtype=torch.float64, device=P.device)
+    pbuf[:n, :m].copy_(P.T)
+    cf = coeffs if isinstance(coeffs, torch.Tensor) else torch.as_tensor(np.asarray(coeffs, dtype=np.float64))
+    cf = cf.to(P.device, torch.float64).contiguous()
+    if cf.numel() == 0:
+        cf = torch.zeros(1, dtype=torch.float64, device=P.device)
+    qbuf = torch.empty((max(qcols, 1), lda), dtype=torch.float64, device=P.device)
+    wsb = int(lib.dmqr_form_q_workspace_bytes(m, qcols))
+    ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=P.device)
+    sh = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    _check(lib.dmqr_form_q_f64(pbuf.data_ptr(), m, n, lda, cf.data_ptr(), int(n_factored), qbuf.data_ptr(),
+                               qcols, lda, ws.data_ptr(), wsb, sh))
+    return qbuf[:qcols, :m].T
+
+
+def reconstruct(result: RRQRResult):
+    """(Q, R) with Q m x m orthogonal and Q @ R == A @ Pi (rrqr.py:459-480); Q formed on the device."""
+    Q = form_q(result.packed, result.coeffs, result.n_factored)
+    Q = Q.cpu().numpy() if not isinstance(result.packed, np.ndarray) or True else Q
+    packed = result.packed if isinstance(result.packed, np.ndarray) else result.packed.cpu().numpy()
+    R = np.asfortranarray(np.array(packed, copy=True))
+    for j in range(min(result.n_factored, R.shape[1])):
+        R[j + 1:, j] = 0.0
+    return np.asfortranarray(Q), R

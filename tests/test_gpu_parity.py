@@ -1,0 +1,154 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the reference's golden
+vectors and the live CPU oracle.  Needs a B200 (``-m gpu``)."""
+
+import numpy as np
+import pytest
+from threadpoolctl import threadpool_limits
+
+import golden_cases as G
+import parity
+from oracle import qrdm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = [c for c in G.case_names() if not c.startswith(("cfg2s", "cfg4s"))]
+
+
+def _gpu(name_or_A, algo="qrdm2", **kw):
+    from paper_2106_03138_b200 import DMParams, StopCriterion, StopRule, qrdm, qrdm2
+
+    params = DMParams(**{k: kw[k] for k in ("tau", "delta", "k_dm", "use_delta_max") if k in kw})
+    stop = StopCriterion(StopRule(kw.get("stop_rule", "n")))
+    fn = qrdm2 if algo == "qrdm2" else qrdm
+    return fn(name_or_A, params=params, stop=stop, trace_norms=kw.get("trace_norms", False))
+
+
+def _steps(log):
+    return [(s.n_s, s.k_selected, s.k_accepted, s.broke_early, s.fell_back_to_scalar,
+             s.k_max if not s.fell_back_to_scalar else -1) for s in log]
+
+
+def _compare(A, res, ref, label):
+    """Exact decisions up to the first ambiguous one (all of them when the run is
+    robust), |diag R| to 1e-10 there, residual/orthogonality <= 50 n eps always."""
+    m, n = A.shape
+    cut, full = parity.robust_prefix(ref)
+    assert np.array_equal(res.perm.forward[:cut], ref.forward[:cut]), f"{label}: pivots differ before column {cut}"
+    want = [s for s in ref.steps if s.n_s < cut]
+    assert _steps(res.step_log[:len(want)]) == _steps(want), f"{label}: step log differs before column {cut}"
+    ok, worst = parity.diag_close(res.r_diagonal()[:cut], ref.r_diagonal()[:cut], max(m, n))
+    assert ok, f"{label}: |diag R| off by {worst:.3g} x tolerance"
+    for a, b in zip(res.step_log[:len(want)], want):
+        # eps_s = tau * (downdated max norm): downdating amplifies rounding
+        assert a.eps_s == pytest.approx(b.eps_s, rel=1e-9, abs=0)
+        assert a.gamma == pytest.approx(b.gamma, rel=1e-9, abs=1e-12)
+    if full:
+        assert np.array_equal(res.perm.forward, ref.forward), f"{label}: permutation differs"
+        assert res.perm.swaps == [tuple(map(int, s)) for s in ref.swaps], f"{label}: swap log differs"
+        assert res.rank == ref.rank, (label, res.rank, ref.rank)
+        assert res.n_factored == ref.n_factored and res.stopped_early == ref.stopped_early
+        assert _steps(res.step_log) == _steps(ref.steps), f"{label}: step log differs"
+        rc = res.counters
+        assert (rc.rank1_flops, rc.blocked_flops, rc.total_flops) == pytest.approx(ref.counters, rel=0, abs=0)
+    if m and n:
+        resid, orth = parity.residuals(A, res)
+        bound = 50 * max(m, n) * O.EPS
+        assert resid <= bound, f"{label}: residual {resid:.3g} > {bound:.3g}"
+        assert orth <= bound, f"{label}: orthogonality {orth:.3g} > {bound:.3g}"
+    return cut, full
+
+
+@pytest.mark.parametrize("name", GOLDEN)
+def test_golden_case(name):
+    meta = G.index()["cases"][name]
+    A = G.case_input(name)
+    kw = G.oracle_kwargs(name)
+    res = _gpu(A, meta["algo"], **kw)
+    fn = O.qrdm2 if meta["algo"] == "qrdm2" else O.qrdm
+    with threadpool_limits(1):
+        ref = fn(A, margins=True, **kw)
+    # the oracle itself is pinned to the golden vectors (test_oracle_golden.py)
+    assert np.array_equal(ref.forward, G.case_field(name, "forward"))
+    _compare(A, res, ref, name)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_vs_oracle(seed):
+    rng = np.random.default_rng(1000 + seed)
+    m = int(rng.integers(40, 400))
+    n = int(rng.integers(40, 400))
+    kind = seed % 3
+    if kind == 0:
+        A = rng.standard_normal((m, n))
+    elif kind == 1:
+        r = int(rng.integers(1, min(m, n)))
+        A = rng.standard_normal((m, r)) @ rng.standard_normal((r, n))
+    else:
+        A = rng.standard_normal((m, n)) * np.logspace(0, -10, n)[rng.permutation(n)]
+    algo = "qrdm2" if seed % 2 == 0 else "qrdm"
+    res = _gpu(A, algo)
+    with threadpool_limits(1):
+        ref = (O.qrdm2 if algo == "qrdm2" else O.qrdm)(A, margins=True)
+    _compare(A, res, ref, f"random{seed}")
+
+
+def test_trace_norms_within_1e10():
+    rng = np.random.default_rng(39)
+    A = rng.standard_normal((250, 180))
+    res = _gpu(A, "qrdm2", k_dm=8, stop_rule="none", trace_norms=True)
+    assert res.norm_trace and max(res.norm_trace) <= 1e-10
+
+
+def test_errors():
+    from paper_2106_03138_b200 import DMParams, qrdm2
+
+    with pytest.raises(ValueError):
+        qrdm2(np.ones(3))
+    bad = np.ones((4, 4))
+    bad[1, 2] = np.nan
+    with pytest.raises(ValueError):
+        qrdm2(bad)
+    bad[1, 2] = np.inf
+    with pytest.raises(ValueError):
+        qrdm2(bad)
+    with pytest.raises(ValueError):
+        DMParams(tau=0.0)
+
+
+def test_input_not_mutated_and_torch_input():
+    import torch
+
+    from paper_2106_03138_b200 import qrdm2
+
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((70, 50))
+    A0 = A.copy()
+    r1 = qrdm2(A)
+    assert np.array_equal(A, A0)
+    r2 = qrdm2(torch.from_numpy(A).cuda())
+    assert np.array_equal(r1.perm.forward, r2.perm.forward)
+    assert np.array_equal(r1.packed, r2.packed)
+
+
+def test_empty_and_degenerate_shapes():
+    from paper_2106_03138_b200 import qrdm, qrdm2
+
+    for shape in [(0, 0), (0, 5), (5, 0)]:
+        r = qrdm2(np.zeros(shape))
+        assert r.rank == 0 and r.n_factored == 0 and r.step_log == []
+    r = qrdm(np.zeros((4, 3)))
+    assert r.rank == 0
+
+
+def test_deterministic_repeat():
+    from paper_2106_03138_b200 import qrdm2
+
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((300, 260))
+    a, b = qrdm2(A), qrdm2(A)
+    assert np.array_equal(a.packed, b.packed) and np.array_equal(a.coeffs, b.coeffs)
+
+
+@pytest.mark.parametrize("name", ["cfg2s/1024", "cfg4s/8192x256"])
+def test_midsize_golden(name):
+    test_golden_case.__wrapped__(name) if hasattr(test_golden_case, "__wrapped__") else test_golden_case(name)
