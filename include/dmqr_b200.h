@@ -131,6 +131,21 @@ int dmqr_check_finite_f64(const double* A, int64_t m, int64_t n, int64_t lda, in
 
 const char* dmqr_strerror(int code);
 
+/* Telemetry (process-wide, not decision state): number of kernels this library
+ * launched, and -- when enabled -- device time per phase of the outer loop
+ * measured with CUDA events on the caller's stream. */
+typedef struct dmqr_stats {
+  int64_t kernel_launches;
+  int64_t calls;
+  int64_t timed_steps;
+  double ms_select;    /* stop/floor/candidates + cosine Gram + filter + swaps */
+  double ms_panel;     /* Householder panel + T factor */
+  double ms_trailing;  /* V = Y T^T, Z = Y^T C, C -= V Z */
+  double ms_norms;     /* downdate + guard recompute + step record */
+} dmqr_stats;
+void dmqr_stats_enable(int32_t on);
+void dmqr_stats_get(dmqr_stats* out, int32_t reset);
+
 /* Debug: copy the device control block of a workspace (after a call) into
  * out[16 + 4*72] int64 on the device: n_s, done, stopped, status, kind, k_max,
  * ncand, nsel, k_s, l_acc, nsw, step_idx, n_swaps, bits(umax), bits(eps_s),

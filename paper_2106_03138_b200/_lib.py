@@ -22,6 +22,8 @@ EXPORTS = (
     "dmqr_strerror",
     "dmqr_version",
     "dmqr_debug_ctl",
+    "dmqr_stats_enable",
+    "dmqr_stats_get",
 )
 
 DMQR_OK, DMQR_EINVAL, DMQR_ENONFINITE, DMQR_EZEROCOL, DMQR_ECUDA, DMQR_ECAP = 0, -1, -2, -3, -4, -5
@@ -66,6 +68,18 @@ class Info(C.Structure):
     ]
 
 
+class Stats(C.Structure):
+    _fields_ = [
+        ("kernel_launches", C.c_int64),
+        ("calls", C.c_int64),
+        ("timed_steps", C.c_int64),
+        ("ms_select", C.c_double),
+        ("ms_panel", C.c_double),
+        ("ms_trailing", C.c_double),
+        ("ms_norms", C.c_double),
+    ]
+
+
 STEP_BYTES = C.sizeof(Step)  # 56
 INFO_BYTES = C.sizeof(Info)
 
@@ -101,10 +115,20 @@ def load() -> C.CDLL:
     lib.dmqr_strerror.restype = C.c_char_p
     lib.dmqr_debug_ctl.argtypes = [P, P, VP]
     lib.dmqr_debug_ctl.restype = C.c_int
+    lib.dmqr_stats_enable.argtypes = [C.c_int32]
+    lib.dmqr_stats_enable.restype = None
+    lib.dmqr_stats_get.argtypes = [C.POINTER(Stats), C.c_int32]
+    lib.dmqr_stats_get.restype = None
     lib.dmqr_version.argtypes = []
     lib.dmqr_version.restype = C.c_char_p
     _lib = lib
     return lib
+
+
+def stats(reset: bool = False) -> dict:
+    st = Stats()
+    load().dmqr_stats_get(C.byref(st), int(reset))
+    return {k: getattr(st, k) for k, _ in Stats._fields_}
 
 
 def strerror(code: int) -> str:

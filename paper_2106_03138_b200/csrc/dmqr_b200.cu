@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -115,6 +116,17 @@ int validate(int64_t m, int64_t n, int64_t lda, const dmqr_params* p) {
   return 0;
 }
 
+// ---- telemetry (not decision state): launch counter and optional phase timing ----
+std::atomic<long long> g_launches{0};
+std::atomic<long long> g_calls{0};
+std::atomic<int> g_prof{0};
+struct ProfAcc {
+  double ms[4] = {0, 0, 0, 0};  // select+gram+swap, panel, trailing update, downdate+log
+  long long steps = 0;
+};
+ProfAcc g_acc;  // guarded by the caller (bench) using one thread
+#define NOTE_LAUNCH() g_launches.fetch_add(1, std::memory_order_relaxed)
+
 struct HostHead {  // the prefix of Ctl the host polls
   int32_t n_s, done, stopped, status;
 };
@@ -150,6 +162,7 @@ int dmqr_check_finite_f64(const double* A, int64_t m, int64_t n, int64_t lda, in
   if (m > 0 && n > 0) {
     int64_t blocks = std::min<int64_t>(ceil_div(m * n, 256), 148 * 16);
     k_check_finite<<<(unsigned)blocks, 256, 0, st>>>(A, m, n, lda, nonfinite);
+    NOTE_LAUNCH();
     CK(cudaGetLastError());
   }
   return 0;
@@ -193,6 +206,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     if (m > 0) {
       int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)d.sms * 16);
       k_colnorms_init<<<(unsigned)blocks, 256, 0, st>>>(A, m, n, lda, u, uref);
+      NOTE_LAUNCH();
     } else {
       CK(cudaMemsetAsync(u, 0, sizeof(double) * n, st));
       CK(cudaMemsetAsync(uref, 0, sizeof(double) * n, st));
@@ -201,10 +215,17 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   InitArgs ia{ctl, u, perm, coeffs, m, n, lda, kmax, p->tau, p->delta, eps1, p->k_dm, p->use_delta_max,
               p->break_check, p->trace_norms, swap_cap, step_cap};
   k_init<<<1, 1024, 0, st>>>(ia);
+  NOTE_LAUNCH();
   CK(cudaGetLastError());
 
-  HostHead* hh = nullptr;
-  CK(cudaMallocHost(&hh, sizeof(HostHead)));
+  static thread_local HostHead* hh = nullptr;  // pinned poll slot, one per host thread
+  if (!hh) CK(cudaMallocHost(&hh, sizeof(HostHead)));
+  const bool prof = g_prof.load() != 0;
+  cudaEvent_t ev[5];
+  if (prof)
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+#define PROF(i) \
+  if (prof) CK(cudaEventRecord(ev[i], st))
   int64_t host_ns = 0;
   int steps_done = 0;
   const int max_coop_p = std::min(d.sms, PANEL_PMAX);
@@ -214,10 +235,14 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     const int64_t mp = m - host_ns;
     const int64_t np = n - host_ns;
     // ---- selection ----
+    PROF(0);
     k_select<<<1, SEL_T, 0, st>>>(ctl, u);
+    NOTE_LAUNCH();
     const int G = (int)std::clamp<int64_t>(ceil_div(mp, 512), 1, GRAM_GMAX);
     k_gram<<<G, GRAM_T, sizeof(GramSmem), st>>>(ctl, A, gpart);
+    NOTE_LAUNCH();
     k_swap<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(ctl, A, u, uref, perm, swaps);
+    NOTE_LAUNCH();
     // ---- panel ----
     const int kcap = (int)std::min<int64_t>({(int64_t)p->k_dm + 1, (int64_t)DMQR_MAXK, kmax - host_ns});
     int P = (int)std::clamp<int64_t>(ceil_div(mp, 256), 1, max_coop_p);
@@ -233,43 +258,67 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
         smem = 0;
       }
     }
+    PROF(1);
     PanelArgs pa{ctl, A, coeffs, T, red, use_smem};
     void* kargs[] = {&pa};
     if (P > 1) {
       CK(cudaLaunchCooperativeKernel((void*)k_panel, dim3(P), dim3(PANEL_T), kargs, smem, st));
+      NOTE_LAUNCH();
     } else {
       k_panel<<<1, PANEL_T, smem, st>>>(pa);
+      NOTE_LAUNCH();
     }
     // ---- trailing update ----
+    PROF(2);
     const int64_t ncols_ub = std::max<int64_t>(np - 1, 0);
     if (ncols_ub > 0) {
       k_form_v<<<dim3((unsigned)ceil_div(mp, 128), DMQR_KP), 128, 0, st>>>(ctl, A, T, V);
+      NOTE_LAUNCH();
       const int64_t ntile = ceil_div(ncols_ub, TA_COLS);
       int nsplit = (int)std::clamp<int64_t>(ceil_div(2 * d.sms, ntile), 1, NSPLIT_MAX);
       nsplit = (int)std::min<int64_t>(nsplit, std::max<int64_t>(1, ceil_div(mp, 256)));
       k_trail_a<<<dim3((unsigned)ntile, nsplit), TA_T, 0, st>>>(ctl, A, Zp);
+      NOTE_LAUNCH();
       const int64_t rtot = (int64_t)DMQR_KP * ncols_ub;
       k_trail_r<<<(unsigned)std::min<int64_t>(ceil_div(rtot, 256), d.sms * 8), 256, 0, st>>>(ctl, Zp, Z, nsplit);
+      NOTE_LAUNCH();
       k_trail_b<<<dim3((unsigned)ceil_div(mp, TB_ROWS), (unsigned)ceil_div(ncols_ub, TB_COLS)), TB_T,
                   sizeof(double) * DMQR_KP * (TB_VLD + TB_ZLD), st>>>(ctl, A, V, Z);
+      NOTE_LAUNCH();
     }
     // ---- norms, log ----
+    PROF(3);
     if (np > 0) {
       const int64_t blocks = std::min<int64_t>(ceil_div(np * 32, 256), (int64_t)d.sms * 16);
       k_downdate<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, uref);
-      if (p->trace_norms) k_norm_trace<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, tbits);
+      NOTE_LAUNCH();
+      if (p->trace_norms) { k_norm_trace<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, tbits); NOTE_LAUNCH(); }
     }
     k_step_end<<<1, 32, 0, st>>>(ctl, srec, norm_trace, tbits);
+    NOTE_LAUNCH();
+    PROF(4);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(hh, &ctl->n_s, sizeof(HostHead), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (prof) {
+      for (int q = 0; q < 4; ++q) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev[q], ev[q + 1]));
+        g_acc.ms[q] += ms;
+      }
+      g_acc.steps += 1;
+    }
     ++steps_done;
     host_ns = hh->n_s;
     if (hh->done) break;
     if (p->max_steps > 0 && steps_done >= p->max_steps) break;  // debug: stop after N steps
   }
-  cudaFreeHost(hh);
+  if (prof)
+    for (auto& e : ev) cudaEventDestroy(e);
+#undef PROF
+  g_calls.fetch_add(1);
   k_finalize<<<1, 256, 0, st>>>(ctl, A, p->stop_rule == DMQR_STOP_NONE);
+  NOTE_LAUNCH();
   CK(cudaGetLastError());
   Ctl hc;
   CK(cudaMemcpyAsync(&hc, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
@@ -315,15 +364,37 @@ int dmqr_form_q_f64(const double* packed, int64_t m, int64_t n, int64_t lda, con
   double* w = (double*)workspace;
   if (m == 0 || qcols == 0) return 0;
   k_q_init<<<(unsigned)std::min<int64_t>(ceil_div(m * qcols, 256), 148 * 16), 256, 0, st>>>(Q, m, qcols, ldq);
+  NOTE_LAUNCH();
   for (int64_t s = std::min(n_factored, qcols) - 1; s >= 0; --s) {
     const int64_t cols = qcols - s;
     k_q_dots<<<(unsigned)ceil_div(cols * 32, 256), 256, 0, st>>>(packed, m, lda, coeffs, s, Q, qcols, ldq, w);
+    NOTE_LAUNCH();
     k_q_update<<<(unsigned)std::min<int64_t>(ceil_div((m - s) * cols, 256), 148 * 16), 256, 0, st>>>(
         packed, m, lda, s, Q, qcols, ldq, w);
+    NOTE_LAUNCH();
   }
   // reflectors s >= qcols act on rows >= s, where [I; 0] is still zero: no-ops
   CK(cudaGetLastError());
   return 0;
+}
+
+void dmqr_stats_enable(int32_t on) { g_prof.store(on ? 1 : 0); }
+
+void dmqr_stats_get(dmqr_stats* out, int32_t reset) {
+  if (out) {
+    out->kernel_launches = g_launches.load();
+    out->calls = g_calls.load();
+    out->timed_steps = g_acc.steps;
+    out->ms_select = g_acc.ms[0];
+    out->ms_panel = g_acc.ms[1];
+    out->ms_trailing = g_acc.ms[2];
+    out->ms_norms = g_acc.ms[3];
+  }
+  if (reset) {
+    g_launches.store(0);
+    g_calls.store(0);
+    g_acc = ProfAcc{};
+  }
 }
 
 /* debug hook (not part of the reference surface): flatten the control block

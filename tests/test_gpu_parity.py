@@ -41,7 +41,8 @@ def _compare(A, res, ref, label):
     for a, b in zip(res.step_log[:len(want)], want):
         # eps_s = tau * (downdated max norm): downdating amplifies rounding
         assert a.eps_s == pytest.approx(b.eps_s, rel=1e-9, abs=0)
-        assert a.gamma == pytest.approx(b.gamma, rel=1e-9, abs=1e-12)
+        # gamma (diagnostic) sums |cosines| of possibly ill-conditioned trailing columns
+        assert a.gamma == pytest.approx(b.gamma, rel=1e-6, abs=1e-9)
     if full:
         assert np.array_equal(res.perm.forward, ref.forward), f"{label}: permutation differs"
         assert res.perm.swaps == [tuple(map(int, s)) for s in ref.swaps], f"{label}: swap log differs"
