@@ -151,6 +151,9 @@ void dmqr_stats_get(dmqr_stats* out, int32_t reset);
  * ncand, nsel, k_s, l_acc, nsw, step_idx, n_swaps, bits(umax), bits(eps_s),
  * bits(gamma), cand[72], sel[72], sw_a[72], sw_b[72]. */
 int dmqr_debug_ctl(const void* workspace, int64_t* out, void* stream);
+/* Debug: per-reflector phase clocks (clock64) of one panel CTA at step 2, recorded
+ * when dmqr_stats_enable(2) was set; out = 64 x 8 int64 on the host. */
+int dmqr_debug_panel_clocks(const void* workspace, int64_t m, int64_t n, int64_t* out);
 
 /* Build identification (compile arch, version) for logs and the loader check. */
 const char* dmqr_version(void);

@@ -37,6 +37,9 @@ struct Ctl {
   int32_t cand[DMQR_KP];  // absolute column indices, seed first
   int32_t sel[DMQR_KP];   // selected absolute indices, seed first
   int32_t sw_a[DMQR_KP], sw_b[DMQR_KP];
+  // the same transposition sequence composed into column moves: new[dst] = old[src]
+  int32_t nmv;
+  int32_t mv_dst[2 * DMQR_KP], mv_src[2 * DMQR_KP];
   // inter-CTA counters (reset by their users)
   uint32_t gram_count;
   uint32_t bar_count;
@@ -79,7 +82,24 @@ __device__ __forceinline__ bool norm_range_ok(double amax) {
   return amax == 0.0 || (amax > 1e-140 && amax < 1e140);
 }
 
-// Grid-wide barrier for cooperatively launched kernels (all CTAs co-resident).
+// Grid-wide barrier for cooperatively launched kernels (all CTAs co-resident):
+// a monotonic arrival counter (zeroed by an earlier kernel of the step) --
+// arrive with a gpu-scope release add, wait with acquire loads until the
+// counter reaches `target` = (barrier ordinal) x (grid size).  No last-arriver
+// reset, so the barrier completes one L2 round trip after the last arrival.
+__device__ __forceinline__ void grid_sync_count(uint32_t* count, uint32_t target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(count) : "memory");
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(count) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+// (legacy) generation barrier
 __device__ __forceinline__ void grid_barrier(uint32_t* count, uint32_t* gen, uint32_t nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {

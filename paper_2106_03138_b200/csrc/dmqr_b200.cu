@@ -21,6 +21,7 @@
 #include "misc.cuh"
 #include "norms.cuh"
 #include "panel.cuh"
+#include "panel_rr.cuh"
 #include "select.cuh"
 #include "trailing.cuh"
 
@@ -28,12 +29,12 @@ using namespace dmqr;
 
 namespace {
 
-constexpr int GRAM_GMAX = 32;
+constexpr int GRAM_GMAX = 148;
 constexpr int NSPLIT_MAX = 16;
 constexpr int PANEL_PMAX = 160;
 
 struct Layout {
-  size_t ctl, u, uref, T, red, gram, Zp, Z, V, trace, total;
+  size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, swp, trace, pdbg, total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -52,10 +53,12 @@ Layout layout(int64_t m, int64_t n) {
   L.T = take(sizeof(double) * DMQR_KP * DMQR_KP);
   L.red = take(sizeof(double) * 2 * PANEL_PMAX * RED_LD);
   L.gram = take(sizeof(double) * GRAM_GMAX * GRAM_PART);
+  L.gfin = take(sizeof(double) * DMQR_KP * DMQR_KP);
   L.Zp = take(sizeof(double) * NSPLIT_MAX * DMQR_KP * std::max<int64_t>(n, 1));
   L.Z = take(sizeof(double) * DMQR_KP * std::max<int64_t>(n, 1));
-  L.V = take(sizeof(double) * DMQR_KP * std::max<int64_t>(m, 1));
+  L.swp = take(sizeof(double) * 2 * DMQR_KP * std::max<int64_t>(m, 1));
   L.trace = take(sizeof(unsigned long long) * 4);
+  L.pdbg = take(sizeof(long long) * 64 * 8);
   L.total = off;
   return L;
 }
@@ -93,14 +96,34 @@ cudaError_t& last_cuda_error() {
 }
 
 bool attrs_done = false;
+bool cluster16 = false;
 
 int set_attrs(const DevInfo& d) {
   if (attrs_done) return 0;
-  CK(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(GramSmem)));
+  CK(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GRAM_SMEM));
+  CK(cudaFuncSetAttribute(k_trail_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TW_SMEM));
+  CK(cudaFuncSetAttribute(k_gram_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FinSmem)));
   CK(cudaFuncSetAttribute(k_trail_b, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(sizeof(double) * DMQR_KP * (TB_VLD + TB_ZLD))));
   CK(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)std::min<size_t>(d.smem_optin - 4096, 220 * 1024)));
+  // 16-CTA (non-portable) clusters for the register-resident panel
+  if (cudaFuncSetAttribute(k_panel_rr<ClusterRed>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+      cudaSuccess) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16);
+    cfg.blockDim = dim3(PANEL_T);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 16;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    cluster16 = cudaOccupancyMaxActiveClusters(&ncl, k_panel_rr<ClusterRed>, &cfg) == cudaSuccess && ncl >= 1;
+  }
+  cudaGetLastError();
   attrs_done = true;
   return 0;
 }
@@ -160,7 +183,7 @@ int dmqr_check_finite_f64(const double* A, int64_t m, int64_t n, int64_t lda, in
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), st));
   if (m > 0 && n > 0) {
-    int64_t blocks = std::min<int64_t>(ceil_div(m * n, 256), 148 * 16);
+    int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), 148 * 16);
     k_check_finite<<<(unsigned)blocks, 256, 0, st>>>(A, m, n, lda, nonfinite);
     NOTE_LAUNCH();
     CK(cudaGetLastError());
@@ -188,10 +211,12 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   double* T = (double*)(ws + L.T);
   double* red = (double*)(ws + L.red);
   double* gpart = (double*)(ws + L.gram);
+  double* gfin = (double*)(ws + L.gfin);
   double* Zp = (double*)(ws + L.Zp);
   double* Z = (double*)(ws + L.Z);
-  double* V = (double*)(ws + L.V);
+  double* swp = (double*)(ws + L.swp);
   unsigned long long* tbits = (unsigned long long*)(ws + L.trace);
+  long long* pdbg = (long long*)(ws + L.pdbg);
   StepRec* srec = (StepRec*)steps;
 
   const int64_t kmax = std::min(m, n);
@@ -201,11 +226,12 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
 
   CK(cudaMemsetAsync(ws, 0, L.ctl + sizeof(Ctl), st));
   CK(cudaMemsetAsync(tbits, 0, sizeof(unsigned long long) * 4, st));
+  int32_t* nonfinite = (int32_t*)(tbits + 2);
   CK(cudaMemsetAsync(T, 0, sizeof(double) * DMQR_KP * DMQR_KP, st));
   if (n > 0) {
     if (m > 0) {
       int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)d.sms * 16);
-      k_colnorms_init<<<(unsigned)blocks, 256, 0, st>>>(A, m, n, lda, u, uref);
+      k_colnorms_init<<<(unsigned)blocks, 256, 0, st>>>(A, m, n, lda, u, uref, nonfinite);
       NOTE_LAUNCH();
     } else {
       CK(cudaMemsetAsync(u, 0, sizeof(double) * n, st));
@@ -213,7 +239,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     }
   }
   InitArgs ia{ctl, u, perm, coeffs, m, n, lda, kmax, p->tau, p->delta, eps1, p->k_dm, p->use_delta_max,
-              p->break_check, p->trace_norms, swap_cap, step_cap};
+              p->break_check, p->trace_norms, swap_cap, step_cap, nonfinite};
   k_init<<<1, 1024, 0, st>>>(ia);
   NOTE_LAUNCH();
   CK(cudaGetLastError());
@@ -229,6 +255,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   int64_t host_ns = 0;
   int steps_done = 0;
   const int max_coop_p = std::min(d.sms, PANEL_PMAX);
+  const int max_cluster = cluster16 ? 16 : 8;
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
 
   while (kmax > 0) {
@@ -238,19 +265,29 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     PROF(0);
     k_select<<<1, SEL_T, 0, st>>>(ctl, u);
     NOTE_LAUNCH();
-    const int G = (int)std::clamp<int64_t>(ceil_div(mp, 512), 1, GRAM_GMAX);
-    k_gram<<<G, GRAM_T, sizeof(GramSmem), st>>>(ctl, A, gpart);
+    const int GG = (int)std::clamp<int64_t>(ceil_div(mp, 2 * GRAM_ROWS), 1, std::min(GRAM_GMAX, d.sms));
+    k_gram<<<GG, GRAM_T, GRAM_SMEM, st>>>(ctl, A, gpart);
     NOTE_LAUNCH();
-    k_swap<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(ctl, A, u, uref, perm, swaps);
+    k_gram_finish<<<45, GRAM_T, sizeof(FinSmem), st>>>(ctl, A, gpart, GG, gfin);
     NOTE_LAUNCH();
+    {
+      const dim3 gs((unsigned)ceil_div(m, 256), (unsigned)ceil_div(2 * DMQR_KP, SWAP_MG));
+      k_swap_gather<<<gs, 256, 0, st>>>(ctl, A, swp);
+      NOTE_LAUNCH();
+      k_swap_scatter<<<gs, 256, 0, st>>>(ctl, A, u, uref, perm, swaps, swp);
+      NOTE_LAUNCH();
+    }
     // ---- panel ----
     const int kcap = (int)std::min<int64_t>({(int64_t)p->k_dm + 1, (int64_t)DMQR_MAXK, kmax - host_ns});
-    int P = (int)std::clamp<int64_t>(ceil_div(mp, 256), 1, max_coop_p);
+    // row CTAs (+1 T-builder CTA when the panel spans several CTAs); the T
+    // builder (or the single CTA) also keeps T (KP x KP) in shared memory
+    const size_t tbytes = sizeof(double) * DMQR_KP * DMQR_KP;
+    int P = (int)std::clamp<int64_t>(ceil_div(mp, 256), 1, max_coop_p - 1);
     int64_t rows = ceil_div(mp, P);
-    size_t smem = (size_t)kcap * (size_t)(rows | 1) * sizeof(double);
+    size_t smem = (size_t)kcap * (size_t)(rows | 1) * sizeof(double) + (P == 1 ? tbytes : 0);
     int use_smem = 1;
     if (smem > panel_smem_cap) {
-      P = max_coop_p;
+      P = max_coop_p - 1;
       rows = ceil_div(mp, P);
       smem = (size_t)kcap * (size_t)(rows | 1) * sizeof(double);
       if (smem > panel_smem_cap) {
@@ -258,11 +295,38 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
         smem = 0;
       }
     }
+    smem = std::max(smem, tbytes);
     PROF(1);
-    PanelArgs pa{ctl, A, coeffs, T, red, use_smem};
+    // register-resident panel (<= 256 rows per CTA): one thread-block cluster
+    // (DSMEM all-reduce) when it fits in 16 CTAs, else a cooperative grid
+    const int Prr = (int)std::max<int64_t>(1, ceil_div(mp, RR_RMAX));
+    const bool rr_path = Prr <= max_coop_p - 1;
+    const bool cl_path = rr_path && Prr > 1 && Prr <= max_cluster;
+    if (rr_path) P = Prr;
+    const int G = cl_path ? P : ((P > 1) ? P + 1 : 1);
+    PanelArgs pa{ctl, A, coeffs, T, red, use_smem, P, (g_prof.load() == 2 && steps_done == 2) ? pdbg : nullptr};
     void* kargs[] = {&pa};
-    if (P > 1) {
-      CK(cudaLaunchCooperativeKernel((void*)k_panel, dim3(P), dim3(PANEL_T), kargs, smem, st));
+    if (cl_path) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(G);
+      cfg.blockDim = dim3(PANEL_T);
+      cfg.dynamicSmemBytes = 0;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = G;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CK(cudaLaunchKernelEx(&cfg, k_panel_rr<ClusterRed>, pa));
+      NOTE_LAUNCH();
+    } else if (G > 1) {
+      void* kfn = rr_path ? (void*)k_panel_rr<GridRed> : (void*)k_panel;
+      CK(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(PANEL_T), kargs, rr_path ? 0 : smem, st));
+      NOTE_LAUNCH();
+    } else if (rr_path) {
+      k_panel_rr<GridRed><<<1, PANEL_T, 0, st>>>(pa);
       NOTE_LAUNCH();
     } else {
       k_panel<<<1, PANEL_T, smem, st>>>(pa);
@@ -272,18 +336,15 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     PROF(2);
     const int64_t ncols_ub = std::max<int64_t>(np - 1, 0);
     if (ncols_ub > 0) {
-      k_form_v<<<dim3((unsigned)ceil_div(mp, 128), DMQR_KP), 128, 0, st>>>(ctl, A, T, V);
-      NOTE_LAUNCH();
       const int64_t ntile = ceil_div(ncols_ub, TA_COLS);
       int nsplit = (int)std::clamp<int64_t>(ceil_div(2 * d.sms, ntile), 1, NSPLIT_MAX);
       nsplit = (int)std::min<int64_t>(nsplit, std::max<int64_t>(1, ceil_div(mp, 256)));
       k_trail_a<<<dim3((unsigned)ntile, nsplit), TA_T, 0, st>>>(ctl, A, Zp);
       NOTE_LAUNCH();
-      const int64_t rtot = (int64_t)DMQR_KP * ncols_ub;
-      k_trail_r<<<(unsigned)std::min<int64_t>(ceil_div(rtot, 256), d.sms * 8), 256, 0, st>>>(ctl, Zp, Z, nsplit);
+      k_trail_w<<<(unsigned)ceil_div(ncols_ub, 64), 256, TW_SMEM, st>>>(ctl, Zp, T, Z, nsplit);
       NOTE_LAUNCH();
       k_trail_b<<<dim3((unsigned)ceil_div(mp, TB_ROWS), (unsigned)ceil_div(ncols_ub, TB_COLS)), TB_T,
-                  sizeof(double) * DMQR_KP * (TB_VLD + TB_ZLD), st>>>(ctl, A, V, Z);
+                  sizeof(double) * DMQR_KP * (TB_VLD + TB_ZLD), st>>>(ctl, A, Z);
       NOTE_LAUNCH();
     }
     // ---- norms, log ----
@@ -378,7 +439,7 @@ int dmqr_form_q_f64(const double* packed, int64_t m, int64_t n, int64_t lda, con
   return 0;
 }
 
-void dmqr_stats_enable(int32_t on) { g_prof.store(on ? 1 : 0); }
+void dmqr_stats_enable(int32_t on) { g_prof.store(on); }
 
 void dmqr_stats_get(dmqr_stats* out, int32_t reset) {
   if (out) {
@@ -399,6 +460,13 @@ void dmqr_stats_get(dmqr_stats* out, int32_t reset) {
 
 /* debug hook (not part of the reference surface): flatten the control block
  * of a workspace used by dmqr_qrdm_f64 into out[16 + 4*72] int64 (device). */
+/* debug: panel phase clocks of step 2 (when stats were enabled with mode 2) */
+int dmqr_debug_panel_clocks(const void* workspace, int64_t m, int64_t n, int64_t* out) {
+  const Layout L = layout(m, n);
+  CK(cudaMemcpy(out, (const unsigned char*)workspace + L.pdbg, sizeof(long long) * 64 * 8, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
 int dmqr_debug_ctl(const void* workspace, int64_t* out, void* stream) {
   k_debug_ctl<<<1, 32, 0, (cudaStream_t)stream>>>((const Ctl*)workspace, out);
   CK(cudaGetLastError());

@@ -3,214 +3,319 @@
 //   dm_select filter       dm.py:151-177 (+ delta_max guard), gamma
 //   k_s, eps_s             rrqr.py:355-357
 //   _move_selected_to_front rrqr.py:294-312: exact transposition sequence with position patching
-// The Gram reduction over m' rows is split across CTAs (fixed-order, deterministic
-// combine); each CTA stages a 32-row slab of the <= 65 gathered candidate columns
-// in shared memory and runs 8x8x4 fp64 MMAs (SASS DMMA) on the upper tiles.  The
-// last CTA to finish reduces the partials, builds Theta and runs the filter with
-// one warp (ballots over the chosen set), then writes the swap plan for k_swap.
+// k_gram: the Gram reduction over m' rows is split across up to one CTA per SM;
+// each CTA streams 64-row slabs of the <= 65 gathered candidate columns into
+// shared memory with cp.async (double-buffered) and runs 8x8x4 fp64 MMAs
+// (SASS DMMA) on the upper tiles, writing per-CTA partials.
+// k_gram_finish: one CTA per upper tile sums the partials in fixed order
+// (deterministic); the last CTA to finish builds Theta, runs the greedy filter
+// with one warp (ballots over the chosen set), and writes the swap plan.
 #pragma once
 #include "common.cuh"
 
 namespace dmqr {
 
 constexpr int GRAM_T = 256;
-constexpr int GRAM_LD = 36;   // 32 rows + 4: conflict-free fragment loads (ld = 4 mod 16)
-constexpr int GRAM_PART = DMQR_KP * DMQR_KP + DMQR_KP;
+constexpr int GRAM_ROWS = 64;  // slab height
+constexpr int GRAM_LD = 68;    // 64 rows + 4: conflict-free fragment loads (ld = 4 mod 16)
+constexpr int GRAM_PART = DMQR_KP * DMQR_KP;
+constexpr size_t GRAM_SMEM = sizeof(double) * 2 * DMQR_KP * GRAM_LD;
 
-// selection finalize (thread 0): k_s, eps_s and the swap plan.  c->sel[0..nsel)
-// must already hold the selected absolute column indices, seed first.
-__device__ __noinline__ void finalize_selection(Ctl* c, int nsel, double gamma) {
+// Selection finalize, one warp, shared-memory scratch (rrqr.py:294-312, 355-357).
+// c->sel[0..nsel) holds the selected absolute columns (seed first).  Writes
+// k_s, eps_s, gamma, the reference's exact transposition sequence
+// (tgt = n_s+i, src = position of sel[i] at time i, with the "first later
+// pos == tgt -> src" patch) and the same sequence composed into column moves
+// new[dst] = old[src] for k_swap_*.
+//
+// The patch rule means sel[i] moves only when it sits in a window slot n_s+d
+// that is filled earlier (d < i): it then jumps to src_d.  Slots strictly
+// increase along such a chain, so src_i = follow(sel[i]) over already known
+// src_d -- a short sequential loop on one lane; everything else is parallel.
+struct PlanSmem {
+  int src[DMQR_KP];    // src_i
+  int win[DMQR_KP];    // content of window slot n_s+i at time i (W_i)
+  int lastw[DMQR_KP];  // latest content written into window slot d (-1: none)
+};
+
+__device__ void plan_swaps_warp(Ctl* c, int nsel, double gamma, PlanSmem& ps) {
+  const int lane = threadIdx.x & 31;
   const int n_s = c->n_s;
   const int k_s = (int)min((int64_t)nsel, c->kmax - n_s);
-  c->nsel = nsel;
-  c->k_s = k_s;
-  c->gamma = gamma;
-  c->eps_s = c->tau * c->umax;
-  int p[DMQR_KP];
-  int where[DMQR_KP];
-#pragma unroll 1
-  for (int d = 0; d < DMQR_KP; ++d) where[d] = -1;
-#pragma unroll 1
-  for (int h = 0; h < k_s; ++h) {
-    p[h] = c->sel[h];
-    const int d = p[h] - n_s;
-    if (d >= 0 && d < DMQR_KP) where[d] = h;
-  }
-  int ns = 0;
-#pragma unroll 1
-  for (int i = 0; i < k_s; ++i) {
-    const int tgt = n_s + i, src = p[i];
-    if (src == tgt) continue;
-    c->sw_a[ns] = tgt;
-    c->sw_b[ns] = src;
-    ++ns;
-    const int h = where[i];
-    if (h > i) {  // first later position holding tgt now holds src (rrqr.py:309-312)
-      p[h] = src;
-      where[i] = -1;
-      const int d = src - n_s;
-      if (d >= 0 && d < DMQR_KP) where[d] = h;
+  for (int d = lane; d < DMQR_KP; d += 32) ps.lastw[d] = -1;
+  __syncwarp();
+  if (lane == 0) {
+    c->nsel = nsel;
+    c->k_s = k_s;
+    c->gamma = gamma;
+    c->eps_s = c->tau * c->umax;
+    for (int i = 0; i < k_s; ++i) {
+      int p = c->sel[i];
+      int d = p - n_s;
+      while (d >= 0 && d < i) {  // sel[i] sat in slot n_s+d when it was filled
+        p = ps.src[d];
+        d = p - n_s;
+      }
+      ps.src[i] = p;
+      const int wi = (ps.lastw[i] >= 0) ? ps.lastw[i] : n_s + i;
+      ps.win[i] = wi;
+      const int ds = p - n_s;
+      if (p != n_s + i && ds >= 0 && ds < DMQR_KP) ps.lastw[ds] = wi;
     }
   }
-  c->nsw = ns;
+  __syncwarp();
+  // transposition list in order (compaction by ballot)
+  int ns = 0;
+  for (int i0 = 0; i0 < k_s; i0 += 32) {
+    const int i = i0 + lane;
+    const bool sw = (i < k_s) && ps.src[i] != n_s + i;
+    const unsigned b = __ballot_sync(0xffffffffu, sw);
+    if (sw) {
+      const int at = ns + __popc(b & ((1u << lane) - 1u));
+      c->sw_a[at] = n_s + i;
+      c->sw_b[at] = ps.src[i];
+    }
+    ns += __popc(b);
+  }
+  // moves: window slots (selected block, plus later slots that received content),
+  // then out-of-window sources whose last write is swap i
+  int nm = 0;
+  for (int d0 = 0; d0 < DMQR_KP; d0 += 32) {
+    const int d = d0 + lane;
+    int src = -1;
+    if (d < k_s)
+      src = c->sel[d];
+    else if (d < DMQR_KP && ps.lastw[d] >= 0)
+      src = ps.lastw[d];
+    const bool mv = (src >= 0) && src != n_s + d;
+    const unsigned b = __ballot_sync(0xffffffffu, mv);
+    if (mv) {
+      const int at = nm + __popc(b & ((1u << lane) - 1u));
+      c->mv_dst[at] = n_s + d;
+      c->mv_src[at] = src;
+    }
+    nm += __popc(b);
+  }
+  for (int i0 = 0; i0 < k_s; i0 += 32) {
+    const int i = i0 + lane;
+    bool mv = false;
+    int p = 0;
+    if (i < k_s) {
+      p = ps.src[i];
+      const int dp = p - n_s;
+      if (p != n_s + i && !(dp >= 0 && dp < DMQR_KP)) {
+        mv = true;
+        for (int t = i + 1; t < k_s; ++t) mv &= (ps.src[t] != p);
+      }
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, mv);
+    if (mv) {
+      const int at = nm + __popc(b & ((1u << lane) - 1u));
+      c->mv_dst[at] = p;
+      c->mv_src[at] = ps.win[i];
+    }
+    nm += __popc(b);
+  }
+  if (lane == 0) {
+    c->nsw = ns;
+    c->nmv = nm;
+  }
 }
 
-struct GramSmem {
-  double cs[DMQR_KP * GRAM_LD];     // slab, column-major by candidate: cs[col*LD + row]
-  double g[DMQR_KP * DMQR_KP];      // reduced Gram / Theta (last CTA)
-  double amax[DMQR_KP];
-  double inv[DMQR_KP];
-  double rowsum[DMQR_KP];
-  int chosen[DMQR_KP];
-  int is_last;
-  int nchosen;
-};
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// upper-triangular tile t of an nt x nt tile grid -> (ti, tj)
+__device__ __forceinline__ void tile_ij(int t, int nt, int& ti, int& tj) {
+  ti = 0;
+  while (t >= nt - ti) {
+    t -= nt - ti;
+    ++ti;
+  }
+  tj = ti + t;
+}
 
 __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, const double* __restrict__ A,
                                                  double* __restrict__ part) {
   if (c->done || c->kind != 0) return;
-  extern __shared__ __align__(16) unsigned char gram_raw[];
-  GramSmem& sm = *reinterpret_cast<GramSmem*>(gram_raw);
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int ncand = c->ncand;
   if (ncand == 1) {  // no candidates: J = [seed], gamma = 1 (dm.py:145-146)
-    if (blockIdx.x == 0 && tid == 0) {
-      c->sel[0] = c->cand[0];
-      finalize_selection(c, 1, 1.0);
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+      __shared__ PlanSmem ps1;
+      if (threadIdx.x == 0) c->sel[0] = c->cand[0];
+      __syncwarp();
+      plan_swaps_warp(c, 1, 1.0, ps1);
     }
     return;
   }
+  extern __shared__ __align__(16) double gsm[];  // [2][KP][GRAM_LD]
+  __shared__ int s_cand[DMQR_KP];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t n_s = c->n_s, m = c->m, lda = c->lda;
   const int64_t mp = m - n_s;
   const int np8 = round_up(ncand, 8);
   const int nt = np8 / 8;
   const int ntiles = nt * (nt + 1) / 2;
+  for (int q = tid; q < DMQR_KP; q += GRAM_T) s_cand[q] = (q < ncand) ? c->cand[q] : 0;
 
-  // rows of this CTA
-  const int64_t rpc = ceil_div(ceil_div(mp, (int64_t)gridDim.x), 32) * 32;
+  const int64_t rpc = ceil_div(ceil_div(mp, (int64_t)gridDim.x), GRAM_ROWS) * GRAM_ROWS;
   const int64_t r_begin = (int64_t)blockIdx.x * rpc;
   const int64_t r_end = min(mp, r_begin + rpc);
 
   double acc[6][2];
-  int tile_i[6], tile_j[6];
+  int tij[6];
   int my_tiles = 0;
   for (int t = wid, q = 0; t < ntiles; t += GRAM_T / 32, ++q) {
-    // t -> (ti, tj) upper-triangular enumeration
-    int ti = 0, rem = t;
-    while (rem >= nt - ti) {
-      rem -= nt - ti;
-      ++ti;
-    }
-    tile_i[q] = ti;
-    tile_j[q] = ti + rem;
+    int ti, tj;
+    tile_ij(t, nt, ti, tj);
+    tij[q] = ti * 16 + tj;
     acc[q][0] = acc[q][1] = 0.0;
     my_tiles = q + 1;
   }
-  double lmax[DMQR_KP / 8 + 1];
-#pragma unroll
-  for (int q = 0; q < DMQR_KP / 8 + 1; ++q) lmax[q] = 0.0;
-
-  for (int64_t r0 = r_begin; r0 < r_end; r0 += 32) {
-    // stage 32 rows x np8 candidate columns (zero padded)
-#pragma unroll
-    for (int q = 0; q < DMQR_KP / 8; ++q) {
-      const int col = wid + 8 * q;
-      if (col < np8) {
-        double v = 0.0;
-        const int64_t r = r0 + lane;
-        if (col < ncand && r < r_end) v = A[(n_s + r) + (int64_t)c->cand[col] * lda];
-        sm.cs[col * GRAM_LD + lane] = v;
-        lmax[q] = fmax(lmax[q], fabs(v));
-      }
+  __syncthreads();
+  const int nslab = (r_end > r_begin) ? (int)ceil_div(r_end - r_begin, GRAM_ROWS) : 0;
+  auto issue = [&](int sl) {
+    double* buf = gsm + (sl & 1) * DMQR_KP * GRAM_LD;
+    const int64_t r0 = r_begin + (int64_t)sl * GRAM_ROWS;
+    for (int e = tid; e < np8 * GRAM_ROWS; e += GRAM_T) {
+      const int col = e / GRAM_ROWS, row = e % GRAM_ROWS;
+      const int64_t r = r0 + row;
+      double* dst = buf + col * GRAM_LD + row;
+      if (col < ncand && r < r_end)
+        cp_async8(dst, A + (n_s + r) + (int64_t)s_cand[col] * lda);
+      else
+        *dst = 0.0;
+    }
+    cp_async_commit();
+  };
+  if (nslab > 0) issue(0);
+  for (int sl = 0; sl < nslab; ++sl) {
+    if (sl + 1 < nslab) {
+      issue(sl + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
+    const double* buf = gsm + (sl & 1) * DMQR_KP * GRAM_LD;
+#pragma unroll 4
+    for (int ks = 0; ks < GRAM_ROWS / 4; ++ks) {
       const int kr = 4 * ks + (lane & 3);
       for (int q = 0; q < my_tiles; ++q) {
-        double a = sm.cs[(tile_i[q] * 8 + (lane >> 2)) * GRAM_LD + kr];
-        double b = sm.cs[(tile_j[q] * 8 + (lane >> 2)) * GRAM_LD + kr];
-        dmma884(acc[q][0], acc[q][1], a, b);
+        const double av = buf[((tij[q] >> 4) * 8 + (lane >> 2)) * GRAM_LD + kr];
+        const double bv = buf[((tij[q] & 15) * 8 + (lane >> 2)) * GRAM_LD + kr];
+        dmma884(acc[q][0], acc[q][1], av, bv);
       }
     }
     __syncthreads();
   }
-  // write partials
   double* my = part + (int64_t)blockIdx.x * GRAM_PART;
   for (int q = 0; q < my_tiles; ++q) {
-    const int row = tile_i[q] * 8 + (lane >> 2);
-    const int col = tile_j[q] * 8 + 2 * (lane & 3);
+    const int row = (tij[q] >> 4) * 8 + (lane >> 2);
+    const int col = (tij[q] & 15) * 8 + 2 * (lane & 3);
     my[row * DMQR_KP + col] = acc[q][0];
     my[row * DMQR_KP + col + 1] = acc[q][1];
   }
-#pragma unroll
-  for (int q = 0; q < DMQR_KP / 8; ++q) {
-    double v = warp_max(lmax[q]);
-    const int col = wid + 8 * q;
-    if (lane == 0 && col < np8) my[DMQR_KP * DMQR_KP + col] = v;
+}
+
+struct FinSmem {
+  double g[DMQR_KP * DMQR_KP];  // Gram, then Theta (upper)
+  double inv[DMQR_KP];
+  double rowsum[DMQR_KP];
+  double amax[DMQR_KP];
+  int chosen[DMQR_KP];
+  int is_last, bad, zero;
+  PlanSmem plan;
+};
+
+// grid: one CTA per upper 8x8 tile (45 for 65 candidates), GRAM_T threads.
+__global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, const double* __restrict__ A,
+                                                        const double* __restrict__ part, int G,
+                                                        double* __restrict__ gfin) {
+  if (c->done || c->kind != 0) return;
+  const int ncand = c->ncand;
+  if (ncand == 1) return;
+  extern __shared__ __align__(16) unsigned char fin_raw[];
+  FinSmem& sm = *reinterpret_cast<FinSmem*>(fin_raw);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int np8 = round_up(ncand, 8);
+  const int nt = np8 / 8;
+  const int ntiles = nt * (nt + 1) / 2;
+  if ((int)blockIdx.x < ntiles) {
+    int ti, tj;
+    tile_ij(blockIdx.x, nt, ti, tj);
+    // 64 entries x 4 threads, each summing a quarter of the partials; fixed combine order
+    const int e = tid >> 2, g4 = tid & 3;
+    const int i = ti * 8 + (e >> 3), j = tj * 8 + (e & 7);
+    double s = 0.0;
+    for (int b = g4; b < G; b += 4) s += __ldcg(part + (int64_t)b * GRAM_PART + i * DMQR_KP + j);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (g4 == 0) gfin[i * DMQR_KP + j] = s;
   }
   __threadfence();
   __syncthreads();
   if (tid == 0) {
-    unsigned prev = atomicAdd(&c->gram_count, 1u);
+    const unsigned prev = atomicAdd(&c->gram_count, 1u);
     sm.is_last = (prev == gridDim.x - 1);
   }
   __syncthreads();
   if (!sm.is_last) return;
   __threadfence();
-  if (tid == 0) c->gram_count = 0u;
-
-  // ---- last CTA: fixed-order reduction of the partials ----
-  const int G = gridDim.x;
-  for (int e = tid; e < np8 * np8; e += GRAM_T) {
-    const int i = e / np8, j = e % np8;
-    if (j < (i / 8) * 8) continue;  // only upper tiles were written
-    double s = 0.0;
-    for (int b = 0; b < G; ++b) s += __ldcg(part + (int64_t)b * GRAM_PART + i * DMQR_KP + j);
-    sm.g[i * DMQR_KP + j] = s;
-  }
-  for (int i = tid; i < np8; i += GRAM_T) {
-    double a = 0.0;
-    for (int b = 0; b < G; ++b) a = fmax(a, __ldcg(part + (int64_t)b * GRAM_PART + DMQR_KP * DMQR_KP + i));
-    sm.amax[i] = a;
-  }
-  __syncthreads();
-  // range check: rescale by exact powers of two if squares could over/underflow
-  __shared__ int s_bad;
   if (tid == 0) {
-    int bad = 0;
-    for (int i = 0; i < ncand; ++i) bad |= !norm_range_ok(sm.amax[i]);
-    s_bad = bad;
+    c->gram_count = 0u;
+    sm.bad = 0;
+    sm.zero = 0;
+  }
+  for (int e = tid; e < ncand * ncand; e += GRAM_T) {
+    const int i = e / ncand, j = e % ncand;
+    if (j >= i) sm.g[i * DMQR_KP + j] = __ldcg(gfin + i * DMQR_KP + j);
   }
   __syncthreads();
-  if (s_bad) {
-    // slow path (extreme magnitudes only): one CTA recomputes the Gram with
-    // per-column scales 2^-e so that max|scaled| is in [0.5, 1).
+  // over/underflow risk: the diagonal (sums of squares) bounds every entry
+  for (int i = tid; i < ncand; i += GRAM_T) {
+    const double d = sm.g[i * DMQR_KP + i];
+    if (!(d > 1e-280 && d < 1e280)) sm.bad = 1;
+  }
+  __syncthreads();
+  const int64_t n_s = c->n_s, m = c->m, lda = c->lda, mp = m - n_s;
+  if (sm.bad) {
+    // slow path (extreme magnitudes only): recompute with exact 2^-e column scales
+    for (int i = wid; i < ncand; i += GRAM_T / 32) {
+      const double* ci = A + (int64_t)c->cand[i] * lda + n_s;
+      double am = 0.0;
+      for (int64_t r = lane; r < mp; r += 32) am = fmax(am, fabs(ci[r]));
+      am = warp_max(am);
+      if (lane == 0) sm.amax[i] = am;
+    }
+    __syncthreads();
     for (int e = tid; e < ncand * ncand; e += GRAM_T) {
       const int i = e / ncand, j = e % ncand;
       if (j < i) continue;
-      int ei, ej;
-      frexp(sm.amax[i], &ei);
-      frexp(sm.amax[j], &ej);
+      int ei = 0, ej = 0;
+      if (sm.amax[i] > 0.0) frexp(sm.amax[i], &ei);
+      if (sm.amax[j] > 0.0) frexp(sm.amax[j], &ej);
       const double* ci = A + (int64_t)c->cand[i] * lda + n_s;
       const double* cj = A + (int64_t)c->cand[j] * lda + n_s;
-      double s = 0.0;
-      for (int64_t r = 0; r < mp; ++r) s = fma(ldexp(ci[r], -ei), ldexp(cj[r], -ej), s);
-      sm.g[i * DMQR_KP + j] = s;
+      double acc = 0.0;
+      for (int64_t r = 0; r < mp; ++r) acc = fma(ldexp(ci[r], -ei), ldexp(cj[r], -ej), acc);
+      sm.g[i * DMQR_KP + j] = acc;
     }
     __syncthreads();
   }
   // norms, zero-column check (dm.py:107-109)
-  __shared__ int s_zero;
-  if (tid == 0) s_zero = 0;
-  __syncthreads();
   for (int i = tid; i < ncand; i += GRAM_T) {
-    double nr = sqrt(sm.g[i * DMQR_KP + i]);
-    if (nr == 0.0) s_zero = 1;
+    const double nr = sqrt(sm.g[i * DMQR_KP + i]);
+    if (nr == 0.0) sm.zero = 1;
     sm.inv[i] = 1.0 / nr;
   }
   __syncthreads();
-  if (s_zero) {
+  if (sm.zero) {
     if (tid == 0) {
       c->status = -3;
       c->done = 1;
@@ -224,76 +329,61 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, const doub
     sm.g[i * DMQR_KP + j] = __dmul_rn(__dmul_rn(sm.g[i * DMQR_KP + j], sm.inv[i]), sm.inv[j]);
   }
   __syncthreads();
-
+  if (wid != 0) return;
   // ---- greedy filter, one warp (dm.py:151-173) ----
-  if (wid == 0) {
-    const bool dmax = c->use_delta_max != 0;
-    const double tau2 = c->tau * c->tau;
-    const double delta = dmax ? tau2 / (double)max(c->k_max - 1, 1) : c->delta;
-    const double guard = tau2;
-    int nch = 1;
-    if (lane == 0) {
-      sm.chosen[0] = 0;
-      sm.rowsum[0] = 0.0;
-    }
-    __syncwarp();
-    for (int t = 1; t < ncand; ++t) {
-      bool ok = true;
-      double gsum = 0.0;
-      for (int q = lane; q < nch; q += 32) {
-        const int j = sm.chosen[q];
-        const double th = fabs(j < t ? sm.g[j * DMQR_KP + t] : sm.g[t * DMQR_KP + j]);
-        ok &= (th < delta);
-        gsum += th;
-      }
-      bool all_ok = __all_sync(0xffffffffu, ok);
-      if (!all_ok) continue;
-      if (dmax) {
-        // total of gains in chosen order (the reference sums the gains vector)
-        double tot = 0.0;
-        if (lane == 0)
-          for (int q = 0; q < nch; ++q) {
-            const int j = sm.chosen[q];
-            tot += fabs(j < t ? sm.g[j * DMQR_KP + t] : sm.g[t * DMQR_KP + j]);
-          }
-        tot = __shfl_sync(0xffffffffu, tot, 0);
-        bool rej = tot >= guard;
-        for (int q = lane; q < nch; q += 32) {
-          const int j = sm.chosen[q];
-          const double th = fabs(j < t ? sm.g[j * DMQR_KP + t] : sm.g[t * DMQR_KP + j]);
-          rej |= (sm.rowsum[j] + th >= guard);
-        }
-        if (__any_sync(0xffffffffu, rej)) continue;
-        for (int q = lane; q < nch; q += 32) {
-          const int j = sm.chosen[q];
-          sm.rowsum[j] += fabs(j < t ? sm.g[j * DMQR_KP + t] : sm.g[t * DMQR_KP + j]);
-        }
-        __syncwarp();
-        if (lane == 0) sm.rowsum[t] = tot;
-      }
-      (void)gsum;
-      if (lane == 0) sm.chosen[nch] = t;
-      ++nch;
-      __syncwarp();
-    }
-    // gamma = min_i 1 - (sum_j |theta_ij| - 1) over the chosen submatrix (dm.py:175-176)
-    double gmin = 1e300;
-    for (int p = lane; p < nch; p += 32) {
-      const int i = sm.chosen[p];
-      double s = 0.0;
-      for (int q = 0; q < nch; ++q) {
-        const int j = sm.chosen[q];
-        s += (i == j) ? 1.0 : fabs(j < i ? sm.g[j * DMQR_KP + i] : sm.g[i * DMQR_KP + j]);
-      }
-      gmin = fmin(gmin, 1.0 - (s - 1.0));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) gmin = fmin(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
-    for (int q = lane; q < nch; q += 32) c->sel[q] = c->cand[sm.chosen[q]];
-    __syncwarp();
-    __threadfence_block();
-    if (lane == 0) finalize_selection(c, nch, gmin);
+  const bool dmax = c->use_delta_max != 0;
+  const double tau2 = c->tau * c->tau;
+  const double delta = dmax ? tau2 / (double)max(c->k_max - 1, 1) : c->delta;
+  const double guard = tau2;
+  auto th = [&](int i, int j) { return fabs(i < j ? sm.g[i * DMQR_KP + j] : sm.g[j * DMQR_KP + i]); };
+  int nch = 1;
+  if (lane == 0) {
+    sm.chosen[0] = 0;
+    sm.rowsum[0] = 0.0;
   }
+  __syncwarp();
+  for (int t = 1; t < ncand; ++t) {
+    bool ok = true;
+    for (int q = lane; q < nch; q += 32) ok &= (th(sm.chosen[q], t) < delta);
+    if (!__all_sync(0xffffffffu, ok)) continue;
+    if (dmax) {
+      double tot = 0.0;
+      if (lane == 0)
+        for (int q = 0; q < nch; ++q) tot += th(sm.chosen[q], t);
+      tot = __shfl_sync(0xffffffffu, tot, 0);
+      bool rej = tot >= guard;
+      for (int q = lane; q < nch; q += 32) {
+        const int jj = sm.chosen[q];
+        rej |= (sm.rowsum[jj] + th(jj, t) >= guard);
+      }
+      if (__any_sync(0xffffffffu, rej)) continue;
+      for (int q = lane; q < nch; q += 32) {
+        const int jj = sm.chosen[q];
+        sm.rowsum[jj] += th(jj, t);
+      }
+      __syncwarp();
+      if (lane == 0) sm.rowsum[t] = tot;
+    }
+    if (lane == 0) sm.chosen[nch] = t;
+    ++nch;
+    __syncwarp();
+  }
+  // gamma = min_i 1 - (sum_j |theta_ij| - 1) over the chosen submatrix (dm.py:175-176)
+  double gmin = 1e300;
+  for (int p = lane; p < nch; p += 32) {
+    const int i = sm.chosen[p];
+    double sacc = 0.0;
+    for (int q = 0; q < nch; ++q) {
+      const int jj = sm.chosen[q];
+      sacc += (i == jj) ? 1.0 : th(i, jj);
+    }
+    gmin = fmin(gmin, 1.0 - (sacc - 1.0));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) gmin = fmin(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
+  for (int q = lane; q < nch; q += 32) c->sel[q] = c->cand[sm.chosen[q]];
+  __syncwarp();
+  plan_swaps_warp(c, nch, gmin, sm.plan);
 }
 
 }  // namespace dmqr

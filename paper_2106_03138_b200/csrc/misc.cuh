@@ -18,6 +18,7 @@ struct InitArgs {
   double tau, delta, eps1;  // eps1 < 0: StopRule.NONE
   int32_t k_dm, use_delta_max, break_check, trace_norms;
   int64_t swap_cap, step_cap;
+  const int32_t* nonfinite;  // set by k_colnorms_init
 };
 
 __global__ void __launch_bounds__(1024) k_init(InitArgs a) {
@@ -52,6 +53,10 @@ __global__ void __launch_bounds__(1024) k_init(InitArgs a) {
       c->step_cap = (int32_t)min(a.step_cap, (int64_t)0x7fffffff);
       c->n_s = 0;
       c->done = (a.kmax == 0);
+      if (a.nonfinite && *a.nonfinite) {  // ValueError in dense() (matrix.py:32-33)
+        c->status = -2;
+        c->done = 1;
+      }
     }
   }
 }
@@ -88,6 +93,7 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
   c->l_acc = 0;
   c->broke = 0;
   c->nsw = 0;
+  c->nmv = 0;
   if (c->n_s >= c->kmax) c->done = 1;
 }
 
@@ -115,13 +121,13 @@ __global__ void k_finalize(Ctl* __restrict__ c, const double* __restrict__ A, in
 
 __global__ void k_check_finite(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
                                int32_t* __restrict__ flag) {
-  const int64_t tot = m * n;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   int bad = 0;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = e / m, i = e % m;
-    bad |= !isfinite(A[i + j * lda]);
-  }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+  for (int64_t j = w0; j < n; j += nw)
+    for (int64_t i = lane; i < m; i += 32) bad |= !isfinite(__ldg(A + i + j * lda));
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
 }
 
 // ---- explicit Q (reconstruct, rrqr.py:468-476): backward accumulation ----

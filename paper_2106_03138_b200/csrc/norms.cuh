@@ -41,14 +41,48 @@ __device__ __forceinline__ double warp_col_norm(const double* __restrict__ x, in
   return amax * sqrt(t);
 }
 
-// u[j] = u_ref[j] = ||A[:, j]||  (PartialNorms.from_matrix)
+// u[j] = u_ref[j] = ||A[:, j]||  (PartialNorms.from_matrix).  A NaN/Inf entry
+// makes the column's sum of squares NaN or its max magnitude Inf, which is
+// flagged here (dense() rejects such input, matrix.py:32-33) -- so the input
+// validation costs no extra pass over the matrix.
 __global__ void k_colnorms_init(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
-                                double* __restrict__ u, double* __restrict__ uref) {
+                                double* __restrict__ u, double* __restrict__ uref, int32_t* __restrict__ nonfinite) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t j = w0; j < n; j += nw) {
-    double r = warp_col_norm(A + j * lda, m, lane);
+    const double* x = A + j * lda;
+    double s0 = 0.0, s1 = 0.0, a0 = 0.0, a1 = 0.0;
+    int bad = 0;
+    int64_t i = lane;
+    for (; i + 32 < m; i += 64) {
+      const double p = __ldg(x + i), q = __ldg(x + i + 32);
+      s0 = fma(p, p, s0);
+      s1 = fma(q, q, s1);
+      a0 = fmax(a0, fabs(p));
+      a1 = fmax(a1, fabs(q));
+      bad |= !isfinite(p) | !isfinite(q);
+    }
+    if (i < m) {
+      const double p = __ldg(x + i);
+      s0 = fma(p, p, s0);
+      a0 = fmax(a0, fabs(p));
+      bad |= !isfinite(p);
+    }
+    const double s = warp_sum(s0 + s1);
+    const double amax = warp_max(fmax(a0, a1));
+    double r;
+    if (norm_range_ok(amax)) {
+      r = sqrt(s);
+    } else {
+      double t = 0.0;
+      for (int64_t k = lane; k < m; k += 32) {
+        const double y = __ldg(x + k) / amax;
+        t = fma(y, y, t);
+      }
+      r = amax * sqrt(warp_sum(t));
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(nonfinite, 1);
     if (lane == 0) {
       u[j] = r;
       uref[j] = r;

@@ -5,59 +5,92 @@
 //   QRDM2 break           rrqr.py:375-379 (||next column|| < eps_s stops the panel)
 //   accumulate_wy         householder.py:92-114 (T = W, upper triangular)
 //
-// The panel is factored by a cooperatively launched grid: CTA b owns a
-// contiguous slice of panel rows and keeps it resident in shared memory for
-// the whole panel.  Each reflector needs two grid-wide all-reductions (the
-// column norm; the v^T C dots + the z = Y^T v for T), done as
-// write-partials / barrier / fixed-order sum, so every CTA holds bitwise
+// The panel is factored by a cooperatively launched grid: CTAs 0..P-1 each own
+// a contiguous slice of panel rows and keep it resident in shared memory for
+// the whole panel; CTA P owns no rows and builds T (the reference's W) from
+// the reduced z vectors off the critical path.  One grid-wide all-reduction
+// per reflector carries the v^T C dots, z = Y^T v, and the three partial sums
+// that give the next column's norm by the identity
+//     ||x - v w||^2 = a - 2 w b + w^2 c ,
+// accepted only without cancellation (>= a/2; else an exact re-reduction),
+// written as partials / barrier / fixed-order sum, so every CTA holds bitwise
 // identical scalars (beta, coeff, w) without a broadcast.
 #pragma once
 #include "common.cuh"
 
 namespace dmqr {
 
-// Apply the step's transposition sequence to full-height columns (row-parallel:
-// each thread replays all swaps on its row, so the sequence order is exact),
-// and to u, u_ref, perm, plus the swap log.
-__global__ void k_swap(Ctl* __restrict__ c, double* __restrict__ A, double* __restrict__ u,
-                       double* __restrict__ uref, int64_t* __restrict__ perm, int64_t* __restrict__ swaplog) {
+// Apply the step's column moves (the composed transposition sequence) to
+// full-height columns in two fully parallel passes: gather every source
+// column into scratch, then scatter into the destinations (grid: row blocks x
+// move groups).  u, u_ref and perm get the same moves; the transposition log
+// itself is appended verbatim.
+constexpr int SWAP_MG = 8;  // moves per thread
+
+__global__ void k_swap_gather(const Ctl* __restrict__ c, const double* __restrict__ A, double* __restrict__ scratch) {
   if (c->done) return;
-  const int nsw = c->nsw;
-  if (nsw == 0) return;
+  const int nmv = c->nmv;
+  const int t0 = blockIdx.y * SWAP_MG;
+  if (t0 >= nmv) return;
   const int64_t m = c->m, lda = c->lda;
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < m) {
-    for (int s = 0; s < nsw; ++s) {
-      double* pa = A + (int64_t)c->sw_a[s] * lda + r;
-      double* pb = A + (int64_t)c->sw_b[s] * lda + r;
-      double t = *pa;
-      *pa = *pb;
-      *pb = t;
-    }
+  if (r >= m) return;
+  double v[SWAP_MG];
+#pragma unroll
+  for (int q = 0; q < SWAP_MG; ++q)
+    if (t0 + q < nmv) v[q] = A[(int64_t)c->mv_src[t0 + q] * lda + r];
+#pragma unroll
+  for (int q = 0; q < SWAP_MG; ++q)
+    if (t0 + q < nmv) scratch[(int64_t)(t0 + q) * m + r] = v[q];
+}
+
+__global__ void k_swap_scatter(Ctl* __restrict__ c, double* __restrict__ A, double* __restrict__ u,
+                               double* __restrict__ uref, int64_t* __restrict__ perm, int64_t* __restrict__ swaplog,
+                               const double* __restrict__ scratch) {
+  if (c->done) return;
+  const int nmv = c->nmv;
+  const int t0 = blockIdx.y * SWAP_MG;
+  const int64_t m = c->m, lda = c->lda;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t0 < nmv && r < m) {
+    double v[SWAP_MG];
+#pragma unroll
+    for (int q = 0; q < SWAP_MG; ++q)
+      if (t0 + q < nmv) v[q] = scratch[(int64_t)(t0 + q) * m + r];
+#pragma unroll
+    for (int q = 0; q < SWAP_MG; ++q)
+      if (t0 + q < nmv) A[(int64_t)c->mv_dst[t0 + q] * lda + r] = v[q];
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    int ns = c->n_swaps;
-    for (int s = 0; s < nsw; ++s) {
-      const int a = c->sw_a[s], b = c->sw_b[s];
-      double t = u[a];
-      u[a] = u[b];
-      u[b] = t;
-      t = uref[a];
-      uref[a] = uref[b];
-      uref[b] = t;
-      int64_t p = perm[a];
-      perm[a] = perm[b];
-      perm[b] = p;
-      if (ns < c->swap_cap) {
-        swaplog[2 * ns] = a;
-        swaplog[2 * ns + 1] = b;
-      }
-      ++ns;
+  if (blockIdx.x == 0 && blockIdx.y == 0) {
+    __shared__ double su[2 * DMQR_KP], sr[2 * DMQR_KP];
+    __shared__ int64_t sp[2 * DMQR_KP];
+    const int t = threadIdx.x;
+    if (t < nmv) {
+      const int src = c->mv_src[t];
+      su[t] = u[src];
+      sr[t] = uref[src];
+      sp[t] = perm[src];
     }
-    c->n_swaps = ns;
-    if (ns > c->swap_cap) {
-      c->status = -5;
-      c->done = 1;
+    __syncthreads();
+    if (t < nmv) {
+      const int dst = c->mv_dst[t];
+      u[dst] = su[t];
+      uref[dst] = sr[t];
+      perm[dst] = sp[t];
+    }
+    const int nsw = c->nsw, ns0 = c->n_swaps;
+    for (int s = t; s < nsw; s += blockDim.x)
+      if (ns0 + s < c->swap_cap) {
+        swaplog[2 * (ns0 + s)] = c->sw_a[s];
+        swaplog[2 * (ns0 + s) + 1] = c->sw_b[s];
+      }
+    __syncthreads();
+    if (t == 0) {
+      c->n_swaps = ns0 + nsw;
+      if (ns0 + nsw > c->swap_cap) {
+        c->status = -5;
+        c->done = 1;
+      }
     }
   }
 }
@@ -73,30 +106,32 @@ struct PanelArgs {
   double* T;     // KP x KP row-major, T[i*KP + j], upper triangular (= reference W)
   double* red;   // [2][gridDim][RED_LD] partials
   int use_smem;  // panel slice resident in shared memory
+  int prows;     // CTAs that own rows (gridDim.x - 1 when a T-builder CTA exists, else gridDim.x)
+  long long* dbg;  // optional phase clocks of CTA 1 (debug builds of the benchmark only)
 };
 
 // deterministic all-reduce of `len` doubles across the grid; in: s_part (this
 // CTA's partials, smem), out: s_tot (smem).  `it` selects the double buffer.
 __device__ __forceinline__ void grid_allreduce(const PanelArgs& a, const double* s_part, double* s_tot, int len,
                                                int it) {
-  const int P = gridDim.x;
-  if (P == 1) {
+  const int G = gridDim.x;
+  if (G == 1) {
     __syncthreads();
     for (int q = threadIdx.x; q < len; q += PANEL_T) s_tot[q] = s_part[q];
     __syncthreads();
     return;
   }
-  double* buf = a.red + (int64_t)(it & 1) * P * RED_LD;
+  double* buf = a.red + (int64_t)(it & 1) * G * RED_LD;
   __syncthreads();
   for (int q = threadIdx.x; q < len; q += PANEL_T) buf[(int64_t)blockIdx.x * RED_LD + q] = s_part[q];
-  grid_barrier(&a.c->bar_count, &a.c->bar_gen, P);
+  grid_sync_count(&a.c->bar_count, (uint32_t)(it + 1) * (uint32_t)G);
   // 8 threads per slot, fixed association order -> identical result in every CTA
   const int slot = threadIdx.x >> 3, g = threadIdx.x & 7;
   for (int q0 = 0; q0 < len; q0 += PANEL_T / 8) {
     const int q = q0 + slot;
     double s = 0.0;
     if (q < len)
-      for (int b = g; b < P; b += 8) s += __ldcg(buf + (int64_t)b * RED_LD + q);
+      for (int b = g; b < G; b += 8) s += __ldcg(buf + (int64_t)b * RED_LD + q);
     s += __shfl_xor_sync(0xffffffffu, s, 4);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     s += __shfl_xor_sync(0xffffffffu, s, 1);
@@ -105,13 +140,27 @@ __device__ __forceinline__ void grid_allreduce(const PanelArgs& a, const double*
   __syncthreads();
 }
 
+// block-level fixed-order sum of per-thread values (PANEL_T threads) into s_part[slot]
+__device__ __forceinline__ void block_sum_into(double v, double* wscr, double* dst) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) wscr[wid] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < PANEL_W; ++w) t += wscr[w];
+    *dst = t;
+  }
+}
+
 __global__ void __launch_bounds__(PANEL_T, 1) k_panel(PanelArgs a) {
   Ctl* c = a.c;
   if (c->done) return;
   extern __shared__ __align__(16) double psm[];
   __shared__ double s_part[RED_LD];
   __shared__ double s_tot[RED_LD];
-  __shared__ double s_wsum[PANEL_W][3];
+  __shared__ double s_w[PANEL_W][4];
+  __shared__ double s_scr[PANEL_W];
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t n_s = c->n_s, m = c->m, lda = c->lda;
@@ -119,95 +168,94 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel(PanelArgs a) {
   const int k = c->k_s;
   const int brk = c->break_check && c->kind == 0;
   const double eps_s = c->eps_s;
-  const int P = gridDim.x;
-  const int64_t r0 = (int64_t)blockIdx.x * mp / P;
-  const int64_t r1 = (int64_t)(blockIdx.x + 1) * mp / P;
+  const int P = a.prows;
+  const bool tcta = (int)blockIdx.x >= P;  // T builder, owns no rows
+  const bool tlocal = (gridDim.x == 1);    // single CTA: builds T itself
+  const int64_t r0 = tcta ? mp : (int64_t)blockIdx.x * mp / P;
+  const int64_t r1 = tcta ? mp : (int64_t)(blockIdx.x + 1) * mp / P;
   const int64_t R = r1 - r0;
 
   // element (t, r) of the panel, r panel-relative in [r0, r1): base[t*ld + (r - r0)]
   double* base;
   int64_t ld;
   double* gpanel = a.A + n_s * lda + n_s + r0;
-  if (a.use_smem) {
+  if (a.use_smem && !tcta) {
     ld = R | 1;  // odd stride spreads columns across banks
     base = psm;
-    for (int64_t e = tid; e < (int64_t)k * R; e += PANEL_T) {
-      const int64_t t = e / R, rr = e % R;
-      base[t * ld + rr] = gpanel[t * lda + rr];
-    }
+    for (int t = wid; t < k; t += PANEL_W)
+      for (int64_t rr = lane; rr < R; rr += 32) base[t * ld + rr] = gpanel[t * lda + rr];
     __syncthreads();
   } else {
     base = gpanel;
     ld = lda;
   }
 #define PEL(t, r) base[(int64_t)(t) * ld + ((r) - r0)]
+  // T (KP x KP) in shared memory: the T-builder's whole dynamic smem, or after
+  // the single CTA's slice (the host sizes the launch for it)
+  double* s_T = tcta ? psm : psm + (a.use_smem ? (int64_t)k * ld : 0);
 
   int l_acc = k;
   int broke = 0;
   int red_it = 0;
-  for (int j = 0; j < k; ++j) {
-    // ---- reduction 1: ||x||^2, max|x|, x0 over rows >= j of column j ----
+  double nrm = 0.0, x0 = 0.0;
+  // ---- exact norm of column j over rows >= j (+ x0) as one all-reduce ----
+  auto exact_norm = [&](int j) {
     const int64_t rs = max(r0, (int64_t)j);
-    double ss = 0.0, am = 0.0, x0 = 0.0;
+    double ss = 0.0, am = 0.0, xx = 0.0;
     for (int64_t r = rs + tid; r < r1; r += PANEL_T) {
-      double x = PEL(j, r);
+      const double x = PEL(j, r);
       ss = fma(x, x, ss);
       am = fmax(am, fabs(x));
-      if (r == j) x0 = x;
+      if (r == j) xx = x;
     }
     ss = warp_sum(ss);
     am = warp_max(am);
-    x0 = warp_sum(x0);
+    xx = warp_sum(xx);
     if (lane == 0) {
-      s_wsum[wid][0] = ss;
-      s_wsum[wid][1] = am;
-      s_wsum[wid][2] = x0;
+      s_w[wid][0] = ss;
+      s_w[wid][1] = am;
+      s_w[wid][2] = xx;
     }
     __syncthreads();
     if (tid == 0) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0;
       for (int w = 0; w < PANEL_W; ++w) {
-        a0 += s_wsum[w][0];
-        a1 = fmax(a1, s_wsum[w][1]);
-        a2 += s_wsum[w][2];
+        t0 += s_w[w][0];
+        t1 = fmax(t1, s_w[w][1]);
+        t2 += s_w[w][2];
       }
-      s_part[0] = a0;
-      s_part[1] = a1;
-      s_part[2] = a2;
+      s_part[0] = t0;
+      s_part[1] = t1;
+      s_part[2] = t2;
     }
-    __syncthreads();
     grid_allreduce(a, s_part, s_tot, 3, red_it++);
-    // s_tot[1] is the sum of per-CTA maxima: zero iff the column is zero, and an
-    // upper bound (<= P x) of max|x| used only to pick an exact 2^-e rescale.
-    const double nrm2 = s_tot[0];
-    const double xx0 = s_tot[2];
-    const double amax_bound = s_tot[1];
-    double nrm;
-    if (amax_bound == 0.0) {
+    // s_tot[1] = sum of per-CTA maxima: zero iff the column is zero; an upper
+    // bound (<= G x) of max|x| used only to pick an exact 2^-e rescale.
+    const double nrm2 = s_tot[0], abound = s_tot[1];
+    x0 = s_tot[2];
+    if (abound == 0.0) {
       nrm = 0.0;
     } else if (nrm2 > 1e-280 && nrm2 < 1e280) {
       nrm = sqrt(nrm2);
     } else {
-      // rare: recompute with exact power-of-two scaling by the max bound
       int e;
-      frexp(amax_bound, &e);
+      frexp(abound, &e);
       double sc = 0.0;
       for (int64_t r = rs + tid; r < r1; r += PANEL_T) {
-        double y = ldexp(PEL(j, r), -e);
+        const double y = ldexp(PEL(j, r), -e);
         sc = fma(y, y, sc);
       }
-      sc = warp_sum(sc);
-      if (lane == 0) s_wsum[wid][0] = sc;
-      __syncthreads();
-      if (tid == 0) {
-        double t0 = 0.0;
-        for (int w = 0; w < PANEL_W; ++w) t0 += s_wsum[w][0];
-        s_part[0] = t0;
-      }
-      __syncthreads();
+      block_sum_into(sc, s_scr, &s_part[0]);
       grid_allreduce(a, s_part, s_tot, 1, red_it++);
       nrm = ldexp(sqrt(s_tot[0]), e);
     }
+  };
+  exact_norm(0);
+  const bool rec = a.dbg && blockIdx.x == (gridDim.x > 1 ? 1 : 0) && tid == 0;
+#define STAMP(ph) \
+  if (rec && j < 64) a.dbg[j * 8 + (ph)] = clock64()
+  for (int j = 0; j < k; ++j) {
+    STAMP(0);
     // ---- QRDM2 break: residual of the next selected column (rrqr.py:375-379) ----
     if (brk && j > 0 && nrm < eps_s) {
       l_acc = j;
@@ -221,62 +269,135 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel(PanelArgs a) {
       coeff = 0.0;
       u0 = 1.0;
     } else {
-      beta = (xx0 != 0.0) ? -copysign(nrm, xx0) : -nrm;
-      u0 = xx0 - beta;
-      coeff = (beta - xx0) / beta;
+      beta = (x0 != 0.0) ? -copysign(nrm, x0) : -nrm;
+      u0 = x0 - beta;
+      coeff = (beta - x0) / beta;
     }
-    // v below the diagonal, beta on it
+    // local row range [rb, R) of this CTA for rows >= j, and [rb1, R) for rows > j
+    const int rb = (int)(max(r0, (int64_t)j) - r0);
+    const int rb1 = (int)(max(r0, (int64_t)j + 1) - r0);
+    const int Ri = (int)R;
+    const bool owner = (j >= r0 && j < r1);
+    double* vj = base + (int64_t)j * ld;  // v over local rows; v_j = 1 stored at row j during the update
     if (nrm != 0.0)
-      for (int64_t r = max(rs, (int64_t)j + 1) + tid; r < r1; r += PANEL_T) PEL(j, r) = PEL(j, r) / u0;
+      for (int r = rb1 + tid; r < Ri; r += PANEL_T) vj[r] = vj[r] / u0;
+    if (owner && tid == 0) vj[j - r0] = 1.0;
     __syncthreads();
-    // ---- reduction 2: d_t = v^T C_t (t > j) and z_i = Y[:, i]^T v (i < j) ----
+    // ---- one all-reduce: d_q = v^T C_q (q > j), z_q = Y_q^T v (q < j), and the
+    //      next column's a = ||x||^2, b = v.x, c = ||v||^2 over rows > j ----
+    const bool has_next = (j + 1 < k);
     for (int q = wid; q < k; q += PANEL_W) {
-      double s = 0.0;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
       if (q != j) {
-        for (int64_t r = rs + lane; r < r1; r += 32) {
-          const double v = (r == j) ? 1.0 : PEL(j, r);
-          s = fma(v, PEL(q, r), s);
+        const double* cq = base + (int64_t)q * ld;
+        int r = rb + lane;
+        for (; r + 96 < Ri; r += 128) {
+          s0 = fma(vj[r], cq[r], s0);
+          s1 = fma(vj[r + 32], cq[r + 32], s1);
+          s2 = fma(vj[r + 64], cq[r + 64], s2);
+          s3 = fma(vj[r + 96], cq[r + 96], s3);
+        }
+        for (; r < Ri; r += 32) s0 = fma(vj[r], cq[r], s0);
+      }
+      const double sdot = warp_sum((s0 + s1) + (s2 + s3));
+      if (lane == 0) s_part[q] = sdot;
+    }
+    if (has_next) {
+      double pa = 0.0, pb = 0.0, pc = 0.0, px = 0.0, pv = 0.0;
+      const double* cn = base + (int64_t)(j + 1) * ld;
+      for (int r = rb1 + tid; r < Ri; r += PANEL_T) {
+        const double x = cn[r], v = vj[r];
+        pa = fma(x, x, pa);
+        pb = fma(v, x, pb);
+        pc = fma(v, v, pc);
+        if (r + r0 == j + 1) {
+          px = x;
+          pv = v;
         }
       }
-      s = warp_sum(s);
-      if (lane == 0) s_part[q] = s;
-    }
-    __syncthreads();
-    grid_allreduce(a, s_part, s_tot, k, red_it++);
-    // diagonal entry (owner)
-    if (j >= r0 && j < r1 && tid == 0) PEL(j, j) = beta;
-    // ---- rank-1 update of the rest of the selected block (householder.py:88-89) ----
-    if (coeff != 0.0) {
-      const int nc = k - j - 1;
-      const int64_t nr = r1 - rs;
-      for (int64_t e = tid; e < (int64_t)nc * nr; e += PANEL_T) {
-        const int t = j + 1 + (int)(e / nr);
-        const int64_t r = rs + e % nr;
-        const double v = (r == j) ? 1.0 : PEL(j, r);
-        const double w = coeff * s_tot[t];
-        PEL(t, r) = PEL(t, r) - v * w;
+      pa = warp_sum(pa);
+      pb = warp_sum(pb);
+      pc = warp_sum(pc);
+      px = warp_sum(px);
+      pv = warp_sum(pv);
+      __shared__ double s_abc[PANEL_W][5];
+      if (lane == 0) {
+        s_abc[wid][0] = pa;
+        s_abc[wid][1] = pb;
+        s_abc[wid][2] = pc;
+        s_abc[wid][3] = px;
+        s_abc[wid][4] = pv;
+      }
+      __syncthreads();
+      if (tid < 5) {
+        double t = 0.0;
+        for (int w = 0; w < PANEL_W; ++w) t += s_abc[w][tid];
+        s_part[k + tid] = t;
       }
     }
-    // ---- T column j (householder.py:109-113): T[:j, j] = -coeff T[:j,:j] z ; T[j,j] = coeff ----
-    if (blockIdx.x == 0) {
-      for (int i = tid; i < j; i += PANEL_T) {
-        double s = 0.0;
-        for (int q = i; q < j; ++q) s += a.T[i * DMQR_KP + q] * s_tot[q];
-        a.T[i * DMQR_KP + j] = -coeff * s;
+    STAMP(1);
+    grid_allreduce(a, s_part, s_tot, k + (has_next ? 5 : 0), red_it++);
+    STAMP(2);
+    // ---- rank-1 update of the rest of the selected block (householder.py:88-89) ----
+    if (coeff != 0.0 && !tcta) {
+      for (int q = j + 1 + wid; q < k; q += PANEL_W) {
+        const double w = coeff * s_tot[q];
+        double* cq = base + (int64_t)q * ld;
+        int r = rb + lane;
+        for (; r + 96 < Ri; r += 128) {
+          cq[r] = fma(-vj[r], w, cq[r]);
+          cq[r + 32] = fma(-vj[r + 32], w, cq[r + 32]);
+          cq[r + 64] = fma(-vj[r + 64], w, cq[r + 64]);
+          cq[r + 96] = fma(-vj[r + 96], w, cq[r + 96]);
+        }
+        for (; r < Ri; r += 32) cq[r] = fma(-vj[r], w, cq[r]);
+      }
+    }
+    STAMP(3);
+    // ---- T column j (householder.py:109-113), on the T-builder CTA, in smem ----
+    if (tcta || tlocal) {
+      for (int i = wid; i < j; i += PANEL_W) {
+        double sacc = 0.0;
+        for (int q = i + lane; q < j; q += 32) sacc = fma(s_T[i * DMQR_KP + q], s_tot[q], sacc);
+        sacc = warp_sum(sacc);
+        if (lane == 0) s_T[i * DMQR_KP + j] = -coeff * sacc;
       }
       if (tid == 0) {
-        a.T[j * DMQR_KP + j] = coeff;
+        s_T[j * DMQR_KP + j] = coeff;
         a.coeffs[n_s + j] = coeff;
       }
     }
+    STAMP(4);
+    // ---- next column's norm ----
+    if (has_next) {
+      const double w = coeff * s_tot[j + 1];
+      const double pa = s_tot[k], pb = s_tot[k + 1], pc = s_tot[k + 2];
+      const double nx = fma(-s_tot[k + 4], w, s_tot[k + 3]);
+      const double nn2 = (coeff != 0.0) ? pa - 2.0 * w * pb + w * w * pc : pa;
+      __syncthreads();
+      if (nn2 >= 0.5 * pa && pa > 1e-280 && pa < 1e280) {
+        nrm = sqrt(nn2);
+        x0 = nx;
+      } else {
+        exact_norm(j + 1);  // cancellation (or range): recompute from the updated column
+      }
+    }
     __syncthreads();
+    if (owner && tid == 0) vj[j - r0] = beta;  // diagonal of R (after every reader of v_j = 1)
+    STAMP(5);
   }
 #undef PEL
-  if (a.use_smem) {
+#undef STAMP
+  if (a.use_smem && !tcta) {
     __syncthreads();
-    for (int64_t e = tid; e < (int64_t)k * R; e += PANEL_T) {
-      const int64_t t = e / R, rr = e % R;
-      gpanel[t * lda + rr] = base[t * ld + rr];
+    for (int t = wid; t < k; t += PANEL_W)
+      for (int64_t rr = lane; rr < R; rr += 32) gpanel[t * lda + rr] = base[t * ld + rr];
+  }
+  if (tcta || tlocal) {
+    __syncthreads();
+    for (int e = tid; e < l_acc * l_acc; e += PANEL_T) {
+      const int i = e / l_acc, jj = e % l_acc;
+      if (i <= jj) a.T[i * DMQR_KP + jj] = s_T[i * DMQR_KP + jj];
     }
   }
   if (blockIdx.x == 0 && tid == 0) {

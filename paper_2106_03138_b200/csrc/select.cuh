@@ -58,6 +58,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* scan_smem, int* total
 
 __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const double* __restrict__ u) {
   if (c->done) return;
+  if (threadIdx.x == 0) c->bar_count = 0u;  // the panel's grid-barrier counter restarts each step
   __shared__ SelSmem sm;
   __shared__ int s_total;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -145,6 +146,11 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const dou
       c->nsw = (seed != n_s) ? 1 : 0;
       c->sw_a[0] = n_s;
       c->sw_b[0] = seed;
+      c->nmv = (seed != n_s) ? 2 : 0;
+      c->mv_dst[0] = n_s;
+      c->mv_src[0] = seed;
+      c->mv_dst[1] = seed;
+      c->mv_src[1] = n_s;
     }
     return;
   }
@@ -178,11 +184,18 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const dou
       const int shift = 56 - 8 * pass;
       for (int b = tid; b < 256; b += SEL_T) sm.hist[b] = 0u;
       __syncthreads();
-      for (int i = s0; i < s1; ++i) {
-        double v = u[i];
-        if (i == seed || !(v >= thr)) continue;
-        unsigned long long key = (unsigned long long)__double_as_longlong(v);
-        if ((key & mask) == prefix) atomicAdd(&sm.hist[(key >> shift) & 255ull], 1u);
+      // warp-aggregated histogram: norms cluster in few bins, so plain shared
+      // atomics would serialize; one atomic per distinct digit per warp step.
+      for (int it = 0; it < seg; ++it) {
+        const int i = s0 + it;
+        unsigned dig = 0xffffffffu;
+        if (i < s1) {
+          const double v = u[i];
+          const unsigned long long key = (unsigned long long)__double_as_longlong(v);
+          if (i != seed && v >= thr && (key & mask) == prefix) dig = (unsigned)((key >> shift) & 255ull);
+        }
+        const unsigned grp = __match_any_sync(0xffffffffu, dig);
+        if (dig != 0xffffffffu && lane == __ffs(grp) - 1) atomicAdd(&sm.hist[dig], (unsigned)__popc(grp));
       }
       __syncthreads();
       if (wid == 0) {

@@ -1,10 +1,9 @@
 // Trailing block-reflector update (larfb 'L','T', forward, columnwise):
 //   apply_block_left  householder.py:117-128 + gemm matrix.py:37-58
 //   C <- (I - Y T^T Y^T) C  on work[n_s:, n_s+k_s:]  (rrqr.py:382-388)
-// evaluated as   Z = Y^T C   (trail_a, split-K over rows, fp64 DMMA)
-//                Z = sum of split partials (trail_r)
-//                V = Y T^T   (form_v, m' x l, once per step)
-//                C -= V Z    (trail_b, fp64 DMMA, C tile in registers)
+// evaluated as   Z  = Y^T C            (trail_a, split-K over rows, fp64 DMMA)
+//                Wt = T^T (sum of Z splits)   (trail_w, fp64 DMMA, l x n'')
+//                C -= Y Wt             (trail_b, fp64 DMMA, C tile in registers)
 // Y is the unit-lower-trapezoidal reflector block read straight out of the
 // packed panel (diagonal 1, zeros above).  The l accepted reflectors update
 // every column right of the selected block; after a QRDM2 break the rejected
@@ -79,35 +78,52 @@ __global__ void __launch_bounds__(TA_T) k_trail_a(const Ctl* __restrict__ c, con
   }
 }
 
-// Z[i][c] = sum_s Zp[s][i][c]  (fixed order), i < 8*ceil(l/8)
-__global__ void k_trail_r(const Ctl* __restrict__ c, const double* __restrict__ Zp, double* __restrict__ Z,
-                          int nsplit) {
+// Wt[i][c] = sum_{t<=i} T[t][i] * (sum_s Zp[s][t][c])  (split sum in fixed order)
+// grid: ceil(n''/64) CTAs of 256 threads; DMMA with M = i (72), N = c (64), K = t.
+constexpr int TW_LD = DMQR_KP;  // 72 = 8 mod 16
+constexpr size_t TW_SMEM = sizeof(double) * 2 * DMQR_KP * TW_LD;
+__global__ void __launch_bounds__(256) k_trail_w(const Ctl* __restrict__ c, const double* __restrict__ Zp,
+                                                 const double* __restrict__ T, double* __restrict__ Wt, int nsplit) {
   if (c->done) return;
   const int64_t n = c->n, ncols = n - (c->n_s + c->k_s);
-  const int l = c->l_acc, lp = (l + 7) / 8 * 8;
-  const int64_t tot = (int64_t)lp * ncols;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / ncols, cc = e % ncols;
-    double s = 0.0;
-    for (int sp = 0; sp < nsplit; ++sp) s += Zp[(int64_t)sp * DMQR_KP * n + i * n + cc];
-    Z[i * n + cc] = s;
+  const int l = c->l_acc;
+  const int64_t col0 = (int64_t)blockIdx.x * 64;
+  if (l == 0 || col0 >= ncols) return;
+  const int lp4 = (l + 3) / 4 * 4, lt = (l + 7) / 8;
+  extern __shared__ __align__(16) double twsm[];
+  double* ts = twsm;                       // ts[t][i] = T[t][i]
+  double* zs = twsm + DMQR_KP * TW_LD;     // zs[t][c]
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int e = tid; e < lp4 * DMQR_KP; e += 256) {
+    const int t = e / DMQR_KP, i = e % DMQR_KP;
+    ts[t * TW_LD + i] = (t < l && i < l && t <= i) ? T[t * DMQR_KP + i] : 0.0;
   }
-}
-
-// V = Y T^T  (m' x lp, column-major with ld m): V[r][t] = sum_{i >= t} Y[r][i] T[t][i]
-// grid (ceil(m'/128), KP): thread = row r, blockIdx.y = t; Y reads coalesced along r.
-__global__ void k_form_v(const Ctl* __restrict__ c, const double* __restrict__ A, const double* __restrict__ T,
-                         double* __restrict__ V) {
-  if (c->done) return;
-  const int64_t n_s = c->n_s, m = c->m, lda = c->lda, mp = m - n_s;
-  const int l = c->l_acc, lp = (l + 7) / 8 * 8;
-  const int t = blockIdx.y;
-  if (c->n_s + c->k_s >= c->n || l == 0 || t >= lp) return;
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= mp) return;
-  double s = 0.0;
-  for (int i = t; i < l; ++i) s = fma(y_elem(A, lda, n_s, r, i, l, mp), __ldg(T + t * DMQR_KP + i), s);
-  V[(int64_t)t * m + r] = (t < l) ? s : 0.0;
+  for (int e = tid; e < lp4 * 64; e += 256) {
+    const int t = e >> 6, cc = e & 63;
+    double sacc = 0.0;
+    if (t < l && col0 + cc < ncols)
+      for (int sp = 0; sp < nsplit; ++sp) sacc += Zp[(int64_t)sp * DMQR_KP * n + (int64_t)t * n + col0 + cc];
+    zs[t * TW_LD + cc] = sacc;
+  }
+  __syncthreads();
+  double acc[DMQR_KP / 8][2];
+#pragma unroll
+  for (int q = 0; q < DMQR_KP / 8; ++q) acc[q][0] = acc[q][1] = 0.0;
+  for (int ks = 0; ks < lp4; ks += 4) {
+    const int t = ks + (lane & 3);
+    const double b = zs[t * TW_LD + wid * 8 + (lane >> 2)];
+#pragma unroll
+    for (int q = 0; q < DMQR_KP / 8; ++q)
+      if (q < lt) dmma884(acc[q][0], acc[q][1], ts[t * TW_LD + q * 8 + (lane >> 2)], b);
+  }
+  const int64_t cc = col0 + wid * 8 + 2 * (lane & 3);
+#pragma unroll
+  for (int q = 0; q < DMQR_KP / 8; ++q) {
+    if (q >= lt) break;
+    const int i = q * 8 + (lane >> 2);
+    if (cc < ncols) Wt[(int64_t)i * n + cc] = acc[q][0];
+    if (cc + 1 < ncols) Wt[(int64_t)i * n + cc + 1] = acc[q][1];
+  }
 }
 
 constexpr int TB_T = 256;     // 8 warps: 4 (rows) x 2 (cols), each 32x32
@@ -116,9 +132,9 @@ constexpr int TB_COLS = 64;
 constexpr int TB_VLD = TB_ROWS + 8;   // 136 = 8 mod 16
 constexpr int TB_ZLD = TB_COLS + 8;   // 72  = 8 mod 16
 
-// C[r][c] -= sum_t V[r][t] Z[t][c] over the trailing block; grid (ceil(m'/128), ceil(n''/64))
+// C[r][c] -= sum_t Y[r][t] Wt[t][c] over the trailing block; grid (ceil(m'/128), ceil(n''/64))
 __global__ void __launch_bounds__(TB_T) k_trail_b(const Ctl* __restrict__ c, double* __restrict__ A,
-                                                  const double* __restrict__ V, const double* __restrict__ Z) {
+                                                  const double* __restrict__ Z) {
   if (c->done) return;
   const int64_t n_s = c->n_s, m = c->m, n = c->n, lda = c->lda;
   const int k_s = c->k_s, l = c->l_acc;
@@ -127,13 +143,13 @@ __global__ void __launch_bounds__(TB_T) k_trail_b(const Ctl* __restrict__ c, dou
   if (row0 >= mp || col0 >= ncols || l == 0) return;
   const int lp4 = (l + 3) / 4 * 4;
   extern __shared__ __align__(16) double tbs[];
-  double* vs = tbs;                       // [KP][136]: vs[t*VLD + r]
-  double* zs = tbs + DMQR_KP * TB_VLD;    // [KP][72]:  zs[t*ZLD + c] = -Z
+  double* vs = tbs;                       // [KP][136]: vs[t*VLD + r] = Y[r][t]
+  double* zs = tbs + DMQR_KP * TB_VLD;    // [KP][72]:  zs[t*ZLD + c] = -Wt[t][c]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (int e = tid; e < lp4 * TB_ROWS; e += TB_T) {
     const int t = e / TB_ROWS, rr = e % TB_ROWS;
     const int64_t r = row0 + rr;
-    vs[t * TB_VLD + rr] = (t < l && r < mp) ? V[(int64_t)t * m + r] : 0.0;
+    vs[t * TB_VLD + rr] = y_elem(A, lda, n_s, r, t, l, mp);
   }
   for (int e = tid; e < lp4 * TB_COLS; e += TB_T) {
     const int t = e / TB_COLS, cc = e % TB_COLS;

@@ -301,11 +301,6 @@ def factorize(A, params: DMParams = DMParams(), stop: StopCriterion = StopCriter
     dev = buf.device
     st = stream if stream is not None else torch.cuda.current_stream(dev)
     sh = C.c_void_p(st.cuda_stream)
-    if m and n:
-        flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        _check(lib.dmqr_check_finite_f64(buf.data_ptr(), m, n, lda, flag.data_ptr(), sh))
-        if int(flag.item()):
-            raise ValueError("matrix contains NaN or Inf entries")
     p = _lib.Params(tau=float(params.tau), delta=float(params.delta), epsilon=float(stop.epsilon),
                     k_dm=int(params.k_dm), use_delta_max=int(bool(params.use_delta_max)),
                     stop_rule=_RULE_CODE[stop.variant], break_check=int(bool(break_check)),

@@ -107,3 +107,53 @@ def test_product_path_has_no_oracle_import():
         src = p.read_text()
         assert "oracle" not in re.sub(r"#.*", "", src).replace('"""', "").split("import")[0] or True
         assert "from oracle" not in src and "import oracle" not in src, p
+
+
+def _plan_like_cuda(n_s, sel, KP=72):
+    """Python mirror of plan_swaps_warp (csrc/gram.cuh) for a CPU check."""
+    k = len(sel)
+    src, win, lastw = [0] * k, [0] * k, [-1] * KP
+    for i in range(k):
+        p = sel[i]
+        d = p - n_s
+        while 0 <= d < i:
+            p = src[d]
+            d = p - n_s
+        src[i] = p
+        wi = lastw[i] if lastw[i] >= 0 else n_s + i
+        win[i] = wi
+        ds = p - n_s
+        if p != n_s + i and 0 <= ds < KP:
+            lastw[ds] = wi
+    swaps = [(n_s + i, src[i]) for i in range(k) if src[i] != n_s + i]
+    moves = []
+    for d in range(KP):
+        s_ = sel[d] if d < k else (lastw[d] if lastw[d] >= 0 else -1)
+        if s_ >= 0 and s_ != n_s + d:
+            moves.append((n_s + d, s_))
+    for i in range(k):
+        p = src[i]
+        dp = p - n_s
+        if p != n_s + i and not (0 <= dp < KP) and all(src[t] != p for t in range(i + 1, k)):
+            moves.append((p, win[i]))
+    return swaps, moves
+
+
+def test_swap_plan_and_moves_match_sequential_swaps():
+    from oracle.qrdm_oracle import swap_plan
+
+    rng = np.random.default_rng(7)
+    for trial in range(400):
+        n = int(rng.integers(2, 300))
+        n_s = int(rng.integers(0, n - 1))
+        k = int(rng.integers(1, min(65, n - n_s) + 1))
+        sel = [int(x) for x in n_s + rng.choice(n - n_s, size=k, replace=False)]
+        swaps, moves = _plan_like_cuda(n_s, sel)
+        assert swaps == swap_plan(n_s, sel)
+        cols = list(range(n))
+        for a, b in swaps:
+            cols[a], cols[b] = cols[b], cols[a]
+        moved = list(range(n))
+        for dst, s_ in moves:
+            moved[dst] = s_
+        assert moved == cols, (n_s, sel)
