@@ -58,7 +58,7 @@ Layout layout(int64_t m, int64_t n) {
   L.Z = take(sizeof(double) * DMQR_KP * std::max<int64_t>(n, 1));
   L.swp = take(sizeof(double) * 2 * DMQR_KP * std::max<int64_t>(m, 1));
   L.trace = take(sizeof(unsigned long long) * 4);
-  L.pdbg = take(sizeof(long long) * 64 * 8);
+  L.pdbg = take(sizeof(long long) * 64 * 16);
   L.total = off;
   return L;
 }
@@ -107,12 +107,14 @@ int set_attrs(const DevInfo& d) {
                           (int)(sizeof(double) * DMQR_KP * (TB_VLD + TB_ZLD))));
   CK(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)std::min<size_t>(d.smem_optin - 4096, 220 * 1024)));
+  CK(cudaFuncSetAttribute(k_panel_rr<ClusterRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RR_CL_SMEM));
   // 16-CTA (non-portable) clusters for the register-resident panel
   if (cudaFuncSetAttribute(k_panel_rr<ClusterRed>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
       cudaSuccess) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(16);
     cfg.blockDim = dim3(PANEL_T);
+    cfg.dynamicSmemBytes = RR_CL_SMEM;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 16;
@@ -304,13 +306,13 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     const bool cl_path = rr_path && Prr > 1 && Prr <= max_cluster;
     if (rr_path) P = Prr;
     const int G = cl_path ? P : ((P > 1) ? P + 1 : 1);
-    PanelArgs pa{ctl, A, coeffs, T, red, use_smem, P, (g_prof.load() == 2 && steps_done == 2) ? pdbg : nullptr};
+    PanelArgs pa{ctl, A, coeffs, T, red, use_smem, P, (g_prof.load() >= 2 && steps_done == 2) ? pdbg : nullptr, std::max(0, g_prof.load() - 2)};
     void* kargs[] = {&pa};
     if (cl_path) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(G);
       cfg.blockDim = dim3(PANEL_T);
-      cfg.dynamicSmemBytes = 0;
+      cfg.dynamicSmemBytes = RR_CL_SMEM;
       cfg.stream = st;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
@@ -463,7 +465,7 @@ void dmqr_stats_get(dmqr_stats* out, int32_t reset) {
 /* debug: panel phase clocks of step 2 (when stats were enabled with mode 2) */
 int dmqr_debug_panel_clocks(const void* workspace, int64_t m, int64_t n, int64_t* out) {
   const Layout L = layout(m, n);
-  CK(cudaMemcpy(out, (const unsigned char*)workspace + L.pdbg, sizeof(long long) * 64 * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out, (const unsigned char*)workspace + L.pdbg, sizeof(long long) * 64 * 16, cudaMemcpyDeviceToHost));
   return 0;
 }
 

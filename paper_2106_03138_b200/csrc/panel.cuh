@@ -107,7 +107,8 @@ struct PanelArgs {
   double* red;   // [2][gridDim][RED_LD] partials
   int use_smem;  // panel slice resident in shared memory
   int prows;     // CTAs that own rows (gridDim.x - 1 when a T-builder CTA exists, else gridDim.x)
-  long long* dbg;  // optional phase clocks of CTA 1 (debug builds of the benchmark only)
+  long long* dbg;  // optional phase clocks of CTA dbg_cta (debug builds of the benchmark only)
+  int dbg_cta;
 };
 
 // deterministic all-reduce of `len` doubles across the grid; in: s_part (this
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel(PanelArgs a) {
     }
   };
   exact_norm(0);
-  const bool rec = a.dbg && blockIdx.x == (gridDim.x > 1 ? 1 : 0) && tid == 0;
+  const bool rec = a.dbg && blockIdx.x == (gridDim.x > 1 ? a.dbg_cta : 0) && tid == 0;
 #define STAMP(ph) \
   if (rec && j < 64) a.dbg[j * 8 + (ph)] = clock64()
   for (int j = 0; j < k; ++j) {
