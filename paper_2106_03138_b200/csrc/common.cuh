@@ -40,6 +40,8 @@ struct Ctl {
   // the same transposition sequence composed into column moves: new[dst] = old[src]
   int32_t nmv;
   int32_t mv_dst[2 * DMQR_KP], mv_src[2 * DMQR_KP];
+  int32_t cq_fail;  // 1: the CholeskyQR2 panel declined, the Householder panel must run
+  int32_t tc0;      // first column of the trailing update (n_s + k_s, or n_s + l after a CholQR break)
   // inter-CTA counters (reset by their users)
   uint32_t gram_count;
   uint32_t bar_count;

@@ -13,6 +13,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/dmqr_b200.h"
@@ -22,6 +23,7 @@
 #include "norms.cuh"
 #include "panel.cuh"
 #include "panel_rr.cuh"
+#include "panel_cq.cuh"
 #include "select.cuh"
 #include "trailing.cuh"
 
@@ -51,7 +53,8 @@ Layout layout(int64_t m, int64_t n) {
   L.u = take(sizeof(double) * std::max<int64_t>(n, 1));
   L.uref = take(sizeof(double) * std::max<int64_t>(n, 1));
   L.T = take(sizeof(double) * DMQR_KP * DMQR_KP);
-  L.red = take(sizeof(double) * 2 * PANEL_PMAX * RED_LD);
+  // panel all-reduce partials; the CholeskyQR2 panel also keeps R, Y1 and per-rank R = R2 R1 here
+  L.red = take(sizeof(double) * std::max<size_t>(2 * PANEL_PMAX * RED_LD, 19 * DMQR_KP * DMQR_KP));
   L.gram = take(sizeof(double) * GRAM_GMAX * GRAM_PART);
   L.gfin = take(sizeof(double) * DMQR_KP * DMQR_KP);
   L.Zp = take(sizeof(double) * NSPLIT_MAX * DMQR_KP * std::max<int64_t>(n, 1));
@@ -108,6 +111,8 @@ int set_attrs(const DevInfo& d) {
   CK(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)std::min<size_t>(d.smem_optin - 4096, 220 * 1024)));
   CK(cudaFuncSetAttribute(k_panel_rr<ClusterRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RR_CL_SMEM));
+  CK(cudaFuncSetAttribute(k_panel_cq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CQ_SMEM));
+  cudaFuncSetAttribute(k_panel_cq, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   // 16-CTA (non-portable) clusters for the register-resident panel
   if (cudaFuncSetAttribute(k_panel_rr<ClusterRed>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
       cudaSuccess) {
@@ -258,6 +263,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   int steps_done = 0;
   const int max_coop_p = std::min(d.sms, PANEL_PMAX);
   const int max_cluster = cluster16 ? 16 : 8;
+  const bool use_cq = getenv("DMQR_NO_CHOLQR") == nullptr;  // debug switch: Householder panel only
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
 
   while (kmax > 0) {
@@ -306,22 +312,34 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     const bool cl_path = rr_path && Prr > 1 && Prr <= max_cluster;
     if (rr_path) P = Prr;
     const int G = cl_path ? P : ((P > 1) ? P + 1 : 1);
-    PanelArgs pa{ctl, A, coeffs, T, red, use_smem, P, (g_prof.load() >= 2 && steps_done == 2) ? pdbg : nullptr, std::max(0, g_prof.load() - 2)};
+    PanelArgs pa{ctl, A, coeffs, T, red, use_smem, P,
+                 (g_prof.load() >= 2 && steps_done == 2) ? pdbg : nullptr, std::max(0, g_prof.load() - 2), 0};
     void* kargs[] = {&pa};
-    if (cl_path) {
+    auto launch_cluster = [&](const void* fn, int ncta, unsigned threads, size_t dsm) -> cudaError_t {
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(G);
-      cfg.blockDim = dim3(PANEL_T);
-      cfg.dynamicSmemBytes = RR_CL_SMEM;
+      cfg.gridDim = dim3(ncta);
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = dsm;
       cfg.stream = st;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = G;
+      at[0].val.clusterDim.x = ncta;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      CK(cudaLaunchKernelEx(&cfg, k_panel_rr<ClusterRed>, pa));
+      return cudaLaunchKernelExC(&cfg, fn, kargs);
+    };
+    // CholeskyQR2 panel (one cluster, <= 256 rows per CTA) first; the Householder
+    // kernels behind it run only if it declined (ill-conditioned panel)
+    const bool cq_path = use_cq && Prr <= max_cluster;
+    if (cq_path) {
+      CK(launch_cluster((const void*)k_panel_cq, Prr, PANEL_T, CQ_SMEM));
+      NOTE_LAUNCH();
+      pa.only_if_fail = 1;
+    }
+    if (cl_path) {
+      CK(launch_cluster((const void*)k_panel_rr<ClusterRed>, G, PANEL_T, RR_CL_SMEM));
       NOTE_LAUNCH();
     } else if (G > 1) {
       void* kfn = rr_path ? (void*)k_panel_rr<GridRed> : (void*)k_panel;

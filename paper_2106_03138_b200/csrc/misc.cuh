@@ -177,7 +177,7 @@ __global__ void k_debug_ctl(const Ctl* __restrict__ c, int64_t* __restrict__ out
   *o++ = c->n_s; *o++ = c->done; *o++ = c->stopped; *o++ = c->status;
   *o++ = c->kind; *o++ = c->k_max; *o++ = c->ncand; *o++ = c->nsel; *o++ = c->k_s; *o++ = c->l_acc;
   *o++ = c->nsw; *o++ = c->step_idx; *o++ = c->n_swaps;
-  *o++ = __double_as_longlong(c->umax); *o++ = __double_as_longlong(c->eps_s); *o++ = __double_as_longlong(c->gamma);
+  *o++ = __double_as_longlong(c->umax); *o++ = __double_as_longlong(c->eps_s); *o++ = c->cq_fail * 1000000LL + c->tc0;
   for (int i = 0; i < DMQR_KP; ++i) *o++ = c->cand[i];
   for (int i = 0; i < DMQR_KP; ++i) *o++ = c->sel[i];
   for (int i = 0; i < DMQR_KP; ++i) *o++ = c->sw_a[i];

@@ -109,6 +109,7 @@ struct PanelArgs {
   int prows;     // CTAs that own rows (gridDim.x - 1 when a T-builder CTA exists, else gridDim.x)
   long long* dbg;  // optional phase clocks of CTA dbg_cta (debug builds of the benchmark only)
   int dbg_cta;
+  int only_if_fail;  // Householder fallback behind the CholeskyQR2 panel: run only if it declined
 };
 
 // deterministic all-reduce of `len` doubles across the grid; in: s_part (this
@@ -404,6 +405,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel(PanelArgs a) {
   if (blockIdx.x == 0 && tid == 0) {
     c->l_acc = l_acc;
     c->broke = broke;
+    c->tc0 = (int32_t)(n_s + k);
   }
 }
 

@@ -49,7 +49,7 @@ constexpr size_t RR_CL_SMEM = sizeof(double) * 2 * RR_MAXCL * RED_LD;  // receiv
 template <class Red>
 __global__ void __launch_bounds__(PANEL_T, 1) k_panel_rr(PanelArgs a) {
   Ctl* c = a.c;
-  if (c->done) return;
+  if (c->done || (a.only_if_fail && !c->cq_fail)) return;
   __shared__ double vbuf[RR_RMAX];
   __shared__ double xs4[RR_RMAX];  // column 64 (warp 0, slot 4)
   __shared__ double s_part[RED_LD];
@@ -404,6 +404,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_rr(PanelArgs a) {
   if (blockIdx.x == 0 && tid == 0) {
     c->l_acc = l_acc;
     c->broke = broke;
+    c->tc0 = (int32_t)(n_s + k);
   }
   if constexpr (Red::cluster()) cg::this_cluster().sync();  // no rank exits while others may push
 }

@@ -58,7 +58,10 @@ __device__ __forceinline__ int block_excl_scan(int v, int* scan_smem, int* total
 
 __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const double* __restrict__ u) {
   if (c->done) return;
-  if (threadIdx.x == 0) c->bar_count = 0u;  // the panel's grid-barrier counter restarts each step
+  if (threadIdx.x == 0) {
+    c->bar_count = 0u;  // the panel's grid-barrier counter restarts each step
+    c->cq_fail = 1;     // the CholeskyQR2 panel (if launched) clears this on success
+  }
   __shared__ SelSmem sm;
   __shared__ int s_total;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(TA_T) k_trail_a(const Ctl* __restrict__ c, con
   if (c->done) return;
   const int64_t n_s = c->n_s, m = c->m, n = c->n, lda = c->lda;
   const int k_s = c->k_s, l = c->l_acc;
-  const int64_t c0 = n_s + k_s;       // first trailing column
+  const int64_t c0 = c->tc0;          // first trailing column (n_s + k_s; n_s + l after a CholQR break)
   const int64_t ncols = n - c0;
   const int64_t col0 = (int64_t)blockIdx.x * TA_COLS;
   if (col0 >= ncols || l == 0) return;
@@ -85,7 +85,7 @@ constexpr size_t TW_SMEM = sizeof(double) * 2 * DMQR_KP * TW_LD;
 __global__ void __launch_bounds__(256) k_trail_w(const Ctl* __restrict__ c, const double* __restrict__ Zp,
                                                  const double* __restrict__ T, double* __restrict__ Wt, int nsplit) {
   if (c->done) return;
-  const int64_t n = c->n, ncols = n - (c->n_s + c->k_s);
+  const int64_t n = c->n, ncols = n - c->tc0;
   const int l = c->l_acc;
   const int64_t col0 = (int64_t)blockIdx.x * 64;
   if (l == 0 || col0 >= ncols) return;
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(TB_T) k_trail_b(const Ctl* __restrict__ c, dou
   if (c->done) return;
   const int64_t n_s = c->n_s, m = c->m, n = c->n, lda = c->lda;
   const int k_s = c->k_s, l = c->l_acc;
-  const int64_t c0 = n_s + k_s, ncols = n - c0, mp = m - n_s;
+  const int64_t c0 = c->tc0, ncols = n - c0, mp = m - n_s;
   const int64_t row0 = (int64_t)blockIdx.x * TB_ROWS, col0 = (int64_t)blockIdx.y * TB_COLS;
   if (row0 >= mp || col0 >= ncols || l == 0) return;
   const int lp4 = (l + 3) / 4 * 4;
