@@ -36,7 +36,7 @@ constexpr int NSPLIT_MAX = 16;
 constexpr int PANEL_PMAX = 160;
 
 struct Layout {
-  size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, swp, trace, pdbg, total;
+  size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, swp, trace, pdbg, tcount, total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -62,6 +62,7 @@ Layout layout(int64_t m, int64_t n) {
   L.swp = take(sizeof(double) * 2 * DMQR_KP * std::max<int64_t>(m, 1));
   L.trace = take(sizeof(unsigned long long) * 4);
   L.pdbg = take(sizeof(long long) * 64 * 16);
+  L.tcount = take(sizeof(unsigned) * (ceil_div(std::max<int64_t>(n, 1), TA_COLS) + 1));
   L.total = off;
   return L;
 }
@@ -104,10 +105,9 @@ bool cluster16 = false;
 int set_attrs(const DevInfo& d) {
   if (attrs_done) return 0;
   CK(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GRAM_SMEM));
-  CK(cudaFuncSetAttribute(k_trail_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TW_SMEM));
+  CK(cudaFuncSetAttribute(k_trail_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA_SMEM));
   CK(cudaFuncSetAttribute(k_gram_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FinSmem)));
-  CK(cudaFuncSetAttribute(k_trail_b, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)(sizeof(double) * DMQR_KP * (TB_VLD + TB_ZLD))));
+  CK(cudaFuncSetAttribute(k_trail_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
   CK(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)std::min<size_t>(d.smem_optin - 4096, 220 * 1024)));
   CK(cudaFuncSetAttribute(k_panel_rr<ClusterRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RR_CL_SMEM));
@@ -224,6 +224,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   double* swp = (double*)(ws + L.swp);
   unsigned long long* tbits = (unsigned long long*)(ws + L.trace);
   long long* pdbg = (long long*)(ws + L.pdbg);
+  unsigned* tcount = (unsigned*)(ws + L.tcount);
   StepRec* srec = (StepRec*)steps;
 
   const int64_t kmax = std::min(m, n);
@@ -235,6 +236,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   CK(cudaMemsetAsync(tbits, 0, sizeof(unsigned long long) * 4, st));
   int32_t* nonfinite = (int32_t*)(tbits + 2);
   CK(cudaMemsetAsync(T, 0, sizeof(double) * DMQR_KP * DMQR_KP, st));
+  CK(cudaMemsetAsync(tcount, 0, sizeof(unsigned) * (ceil_div(std::max<int64_t>(n, 1), TA_COLS) + 1), st));
   if (n > 0) {
     if (m > 0) {
       int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)d.sms * 16);
@@ -359,12 +361,10 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
       const int64_t ntile = ceil_div(ncols_ub, TA_COLS);
       int nsplit = (int)std::clamp<int64_t>(ceil_div(2 * d.sms, ntile), 1, NSPLIT_MAX);
       nsplit = (int)std::min<int64_t>(nsplit, std::max<int64_t>(1, ceil_div(mp, 256)));
-      k_trail_a<<<dim3((unsigned)ntile, nsplit), TA_T, 0, st>>>(ctl, A, Zp);
+      k_trail_a<<<dim3((unsigned)ntile, nsplit), TA_T, TA_SMEM, st>>>(ctl, A, Zp, T, Z, tcount);
       NOTE_LAUNCH();
-      k_trail_w<<<(unsigned)ceil_div(ncols_ub, 64), 256, TW_SMEM, st>>>(ctl, Zp, T, Z, nsplit);
-      NOTE_LAUNCH();
-      k_trail_b<<<dim3((unsigned)ceil_div(mp, TB_ROWS), (unsigned)ceil_div(ncols_ub, TB_COLS)), TB_T,
-                  sizeof(double) * DMQR_KP * (TB_VLD + TB_ZLD), st>>>(ctl, A, Z);
+      k_trail_b<<<dim3((unsigned)ceil_div(mp, TB_ROWS), (unsigned)ceil_div(ncols_ub, TB_COLS)), TB_T, TB_SMEM, st>>>(
+          ctl, A, Z);
       NOTE_LAUNCH();
     }
     // ---- norms, log ----

@@ -122,14 +122,6 @@ __device__ void plan_swaps_warp(Ctl* c, int nsel, double gamma, PlanSmem& ps) {
   }
 }
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
 // upper-triangular tile t of an nt x nt tile grid -> (ti, tj)
 __device__ __forceinline__ void tile_ij(int t, int nt, int& ti, int& tj) {
   ti = 0;
