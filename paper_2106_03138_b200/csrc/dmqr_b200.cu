@@ -41,6 +41,9 @@ struct Layout {
 
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
+// leading dimension of the Z partials / Wt: 16-byte aligned rows with one tile of slack
+int64_t ldz_for(int64_t n) { return (std::max<int64_t>(n, 1) + 7) / 8 * 8 + 64; }
+
 Layout layout(int64_t m, int64_t n) {
   Layout L{};
   size_t off = 0;
@@ -57,8 +60,8 @@ Layout layout(int64_t m, int64_t n) {
   L.red = take(sizeof(double) * std::max<size_t>(2 * PANEL_PMAX * RED_LD, 19 * DMQR_KP * DMQR_KP));
   L.gram = take(sizeof(double) * GRAM_GMAX * GRAM_PART);
   L.gfin = take(sizeof(double) * DMQR_KP * DMQR_KP);
-  L.Zp = take(sizeof(double) * NSPLIT_MAX * DMQR_KP * std::max<int64_t>(n, 1));
-  L.Z = take(sizeof(double) * DMQR_KP * std::max<int64_t>(n, 1));
+  L.Zp = take(sizeof(double) * NSPLIT_MAX * DMQR_KP * ldz_for(n));
+  L.Z = take(sizeof(double) * DMQR_KP * ldz_for(n));
   L.swp = take(sizeof(double) * 2 * DMQR_KP * std::max<int64_t>(m, 1));
   L.trace = take(sizeof(unsigned long long) * 4);
   L.pdbg = take(sizeof(long long) * 64 * 16);
@@ -108,6 +111,7 @@ int set_attrs(const DevInfo& d) {
   CK(cudaFuncSetAttribute(k_trail_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA_SMEM));
   CK(cudaFuncSetAttribute(k_gram_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FinSmem)));
   CK(cudaFuncSetAttribute(k_trail_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
+  CK(cudaFuncSetAttribute(k_trail_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TP_SMEM));
   CK(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)std::min<size_t>(d.smem_optin - 4096, 220 * 1024)));
   CK(cudaFuncSetAttribute(k_panel_rr<ClusterRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RR_CL_SMEM));
@@ -361,10 +365,16 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
       const int64_t ntile = ceil_div(ncols_ub, TA_COLS);
       int nsplit = (int)std::clamp<int64_t>(ceil_div(2 * d.sms, ntile), 1, NSPLIT_MAX);
       nsplit = (int)std::min<int64_t>(nsplit, std::max<int64_t>(1, ceil_div(mp, 256)));
-      k_trail_a<<<dim3((unsigned)ntile, nsplit), TA_T, TA_SMEM, st>>>(ctl, A, Zp, T, Z, tcount);
+      const int64_t ldz = ldz_for(n);
+      k_trail_a<<<dim3((unsigned)ntile, nsplit), TA_T, TA_SMEM, st>>>(ctl, A, Zp, T, Z, tcount, ldz);
       NOTE_LAUNCH();
-      k_trail_b<<<dim3((unsigned)ceil_div(mp, TB_ROWS), (unsigned)ceil_div(ncols_ub, TB_COLS)), TB_T, TB_SMEM, st>>>(
-          ctl, A, Z);
+      if (getenv("DMQR_TRAIL_B_TILED")) {
+        k_trail_b<<<dim3((unsigned)ceil_div(mp + 1, TB_ROWS), (unsigned)ceil_div(ncols_ub, TB_COLS)), TB_T, TB_SMEM,
+                    st>>>(ctl, A, Z, ldz);
+      } else {
+        const int64_t work = ceil_div(mp + 1, TP_ROWS) * ceil_div(ncols_ub, TP_COLS);
+        k_trail_bp<<<(unsigned)std::min<int64_t>(work, d.sms), TP_T, TP_SMEM, st>>>(ctl, A, Z, ldz);
+      }
       NOTE_LAUNCH();
     }
     // ---- norms, log ----

@@ -12,25 +12,37 @@
 // packed panel (diagonal 1, zeros above).  tc0 is n_s + k_s after the
 // Householder panel; after a CholeskyQR2-panel break it is n_s + l, so the
 // rejected selected columns get the accepted reflectors here (rrqr.py:366-367).
+//
+// Staging uses 16-byte cp.async with addresses hoisted out of the loops; tiles
+// start on EVEN global rows (16-byte alignment of column-major data with an
+// even lda), rows outside the tile's range are zero-filled by the copy itself
+// (src-size 0) or get Y = 0, so they contribute nothing.
 #pragma once
 #include "common.cuh"
 
 namespace dmqr {
 
+// 16-byte cp.async; src_bytes < 16 zero-fills the rest (src_bytes = 0: all zeros)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
+}
+
 constexpr int TA_T = 256;       // 8 warps
 constexpr int TA_COLS = 64;     // output columns per CTA
 constexpr int TA_ROWS = 32;     // K slab
-constexpr int TA_LD = 36;       // slab stride (4 mod 16: conflict-free fragments)
+constexpr int TA_LD = 36;       // slab stride (4 mod 16: conflict-free fragments; 16B aligned rows)
 constexpr int TW_LD = DMQR_KP;  // 72 = 8 mod 16
 // 2 slab stages, reused by the fused T^T Z tail (T and Z tiles)
 constexpr size_t TA_SMEM = sizeof(double) * 2 * DMQR_KP * TW_LD;
 static_assert(2 * DMQR_KP * TW_LD >= 2 * (DMQR_KP + TA_COLS) * TA_LD, "smem reuse");
 
-// grid: (ceil(n''/64), nsplit).  Zp[s][i][c] (ld n) = sum over this split's rows of Y[r][i] C[r][c];
-// the last split CTA of each column tile reduces them and writes Wt = T^T Z (ld n).
+// grid: (ceil(n''/64), nsplit).  Zp[s][i][c] (ld ldz) = sum over this split's rows of Y[r][i] C[r][c];
+// the last split CTA of each column tile reduces them and writes Wt = T^T Z (ld ldz).
 __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, const double* __restrict__ A,
                                                      double* __restrict__ Zp, const double* __restrict__ T,
-                                                     double* __restrict__ Wt, unsigned* __restrict__ counters) {
+                                                     double* __restrict__ Wt, unsigned* __restrict__ counters,
+                                                     int64_t ldz) {
   if (c->done) return;
   const int64_t n_s = c->n_s, m = c->m, n = c->n, lda = c->lda;
   const int l = c->l_acc;
@@ -44,43 +56,44 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, const 
   const int64_t rb = (int64_t)blockIdx.y * rps, re = min(mp, rb + rps);
   const int lt = (l + 7) / 8;  // M tiles in use
   const int lp = lt * 8;
+  const int odd = (int)(n_s & 1);  // slabs start one row early so global rows are even
 
   extern __shared__ __align__(16) double tas[];
   double* ysb[2] = {tas, tas + DMQR_KP * TA_LD};
   double* csb[2] = {tas + 2 * DMQR_KP * TA_LD, tas + 2 * DMQR_KP * TA_LD + TA_COLS * TA_LD};
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int nslab = (re > rb) ? (int)ceil_div(re - rb, TA_ROWS) : 0;
-  const double* Yp = A + n_s * lda + n_s;   // Y[r][i] at Yp[r + i*lda] for r > i
+  const int64_t span = (re > rb) ? re - rb + odd : 0;
+  const int nslab = (int)ceil_div(span, TA_ROWS);
+  // thread -> (row pair rp, first column cb) of the 16 x {72 | 64} chunk grid of a slab
+  const int rp = tid & 15, cb = tid >> 4;  // 16 row pairs, 16 column lanes
+  const double* Yp = A + n_s * lda + n_s;   // Y[r][i] at Yp[r + i*lda]
   const double* Cp = A + n_s + c0 * lda;    // C[r][cc] at Cp[r + cc*lda]
 
-  // rows i in [l, lp) of both Y stages are zero for the whole kernel
-  for (int e = tid; e < (lp - l) * TA_LD; e += TA_T) {
+  for (int e = tid; e < (lp - l) * TA_LD; e += TA_T) {  // rows i in [l, lp) stay zero
     ysb[0][l * TA_LD + e] = 0.0;
     ysb[1][l * TA_LD + e] = 0.0;
   }
   auto issue = [&](int sl) {
     double* ys = ysb[sl & 1];
     double* cs = csb[sl & 1];
-    const int64_t r0 = rb + (int64_t)sl * TA_ROWS;
+    const int64_t r = rb - odd + (int64_t)sl * TA_ROWS + 2 * rp;  // panel-relative, even global row
+    const int64_t gr = n_s + r;
+    const int bytes = (gr + 1 < m) ? 16 : ((gr < m) ? 8 : 0);
+    for (int i = cb; i < l; i += 16) cp_async16(ys + i * TA_LD + 2 * rp, Yp + r + (int64_t)i * lda, bytes);
+    for (int cc = cb; cc < TA_COLS; cc += 16)
+      cp_async16(cs + cc * TA_LD + 2 * rp, Cp + r + (col0 + cc) * lda, (col0 + cc < ncols) ? bytes : 0);
+    cp_async_commit();
+  };
+  // Y structure on a landed slab: 0 outside [rb, re) and above the diagonal, 1 on it
+  auto fix = [&](int sl) {
+    const int64_t r0 = rb - odd + (int64_t)sl * TA_ROWS;
+    if (r0 >= 72 && r0 >= rb && r0 + TA_ROWS <= re) return;
+    double* ys = ysb[sl & 1];
     for (int e = tid; e < l * TA_ROWS; e += TA_T) {
       const int i = e >> 5, rr = e & 31;
       const int64_t r = r0 + rr;
-      double* dst = ys + i * TA_LD + rr;
-      if (r < re && r > i)
-        cp_async8(dst, Yp + r + (int64_t)i * lda);
-      else
-        *dst = (r < re && r == i) ? 1.0 : 0.0;
+      if (r < rb || r >= re || r <= i) ys[i * TA_LD + rr] = (r == i && r >= rb && r < re) ? 1.0 : 0.0;
     }
-    for (int e = tid; e < TA_COLS * TA_ROWS; e += TA_T) {
-      const int cc = e >> 5, rr = e & 31;
-      const int64_t r = r0 + rr;
-      double* dst = cs + cc * TA_LD + rr;
-      if (r < re && col0 + cc < ncols)
-        cp_async8(dst, Cp + r + (col0 + cc) * lda);
-      else
-        *dst = 0.0;
-    }
-    cp_async_commit();
   };
   double acc[DMQR_KP / 8][2];
 #pragma unroll
@@ -93,6 +106,8 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, const 
     } else {
       cp_async_wait<0>();
     }
+    __syncthreads();
+    fix(sl);
     __syncthreads();
     const double* ys = ysb[sl & 1];
     const double* cs = csb[sl & 1];
@@ -107,14 +122,14 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, const 
     __syncthreads();
   }
   // ---- partial tile -> Zp[split] ----
-  double* out = Zp + (int64_t)blockIdx.y * DMQR_KP * n;
+  double* out = Zp + (int64_t)blockIdx.y * DMQR_KP * ldz;
   const int64_t cc = col0 + wid * 8 + 2 * (lane & 3);
 #pragma unroll
   for (int q = 0; q < DMQR_KP / 8; ++q) {
     if (q >= lt) break;
     const int i = q * 8 + (lane >> 2);
-    if (cc < ncols) out[(int64_t)i * n + cc] = acc[q][0];
-    if (cc + 1 < ncols) out[(int64_t)i * n + cc + 1] = acc[q][1];
+    out[(int64_t)i * ldz + cc] = acc[q][0];
+    out[(int64_t)i * ldz + cc + 1] = acc[q][1];
   }
   // ---- last split CTA of this column tile: Wt = T^T * sum_s Zp[s] ----
   __threadfence();
@@ -138,11 +153,11 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, const 
   for (int e = tid; e < lp4 * TA_COLS; e += TA_T) {
     const int t = e >> 6, c2 = e & 63;
     double s = 0.0;
-    if (t < l && col0 + c2 < ncols) {
-      const double* zp = Zp + (int64_t)t * n + col0 + c2;
+    if (t < l) {
+      const double* zp = Zp + (int64_t)t * ldz + col0 + c2;
       double v[16];
 #pragma unroll
-      for (int sp = 0; sp < 16; ++sp) v[sp] = (sp < nsplit) ? __ldcg(zp + (int64_t)sp * DMQR_KP * n) : 0.0;
+      for (int sp = 0; sp < 16; ++sp) v[sp] = (sp < nsplit) ? __ldcg(zp + (int64_t)sp * DMQR_KP * ldz) : 0.0;
 #pragma unroll
       for (int sp = 0; sp < 16; ++sp) s += v[sp];
     }
@@ -159,12 +174,13 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, const 
     for (int q = 0; q < DMQR_KP / 8; ++q)
       if (q < lt) dmma884(w[q][0], w[q][1], ts[t * TW_LD + q * 8 + (lane >> 2)], b);
   }
+  // Wt rows [0, lp4) x columns [col0, col0 + 64) (zeros beyond l and beyond ncols keep trail_b exact)
 #pragma unroll
   for (int q = 0; q < DMQR_KP / 8; ++q) {
-    if (q >= lt) break;
     const int i = q * 8 + (lane >> 2);
-    if (cc < ncols) Wt[(int64_t)i * n + cc] = w[q][0];
-    if (cc + 1 < ncols) Wt[(int64_t)i * n + cc + 1] = w[q][1];
+    if (i >= lp4) break;
+    Wt[(int64_t)i * ldz + cc] = (cc < ncols) ? w[q][0] : 0.0;
+    Wt[(int64_t)i * ldz + cc + 1] = (cc + 1 < ncols) ? w[q][1] : 0.0;
   }
 }
 
@@ -176,14 +192,17 @@ constexpr int TB_VLD = TB_ROWS + 8;   // 136 = 8 mod 16
 constexpr int TB_ZLD = TB_COLS + 8;   // 72  = 8 mod 16
 constexpr size_t TB_SMEM = sizeof(double) * TB_KMAX * (TB_VLD + TB_ZLD);  // 113 KB -> 2 CTAs/SM
 
-// C[r][c] -= sum_t Y[r][t] Wt[t][c] over the trailing block; grid (ceil(m'/128), ceil(n''/64))
+// C[r][c] -= sum_t Y[r][t] Wt[t][c] over the trailing block.  grid (ceil((m'+1)/128), ceil(n''/64));
+// row tiles start on even global rows (the possible extra row n_s-1 gets Y = 0).
 __global__ void __launch_bounds__(TB_T, 2) k_trail_b(const Ctl* __restrict__ c, double* __restrict__ A,
-                                                     const double* __restrict__ Wt) {
+                                                     const double* __restrict__ Wt, int64_t ldz) {
   if (c->done) return;
   const int64_t n_s = c->n_s, m = c->m, n = c->n, lda = c->lda;
   const int l = c->l_acc;
   const int64_t c0 = c->tc0, ncols = n - c0, mp = m - n_s;
-  const int64_t row0 = (int64_t)blockIdx.x * TB_ROWS, col0 = (int64_t)blockIdx.y * TB_COLS;
+  const int odd = (int)(n_s & 1);
+  const int64_t row0 = (int64_t)blockIdx.x * TB_ROWS - odd;  // panel-relative, even global row
+  const int64_t col0 = (int64_t)blockIdx.y * TB_COLS;
   if (row0 >= mp || col0 >= ncols || l == 0) return;
   const int lp4 = (l + 3) / 4 * 4;
   extern __shared__ __align__(16) double tbs[];
@@ -194,39 +213,43 @@ __global__ void __launch_bounds__(TB_T, 2) k_trail_b(const Ctl* __restrict__ c, 
   const double* Yp = A + n_s * lda + n_s;
   double* Cp = A + n_s + c0 * lda;
 
-  // stage Y / Wt with cp.async, and load the C tile into the accumulators meanwhile
-  for (int e = tid; e < lp4 * TB_ROWS; e += TB_T) {
-    const int t = e >> 7, rr = e & 127;
-    const int64_t r = row0 + rr;
-    double* dst = vs + t * TB_VLD + rr;
-    if (t < l && r < mp && r > t)
-      cp_async8(dst, Yp + r + (int64_t)t * lda);
-    else
-      *dst = (t < l && r < mp && r == t) ? 1.0 : 0.0;
+  // ---- stage Y (68 x 128) and Wt (68 x 64) with 16-byte cp.async ----
+  {
+    const int rp = tid & 63, tb = tid >> 6;  // 64 row pairs x 4 column lanes
+    const int64_t r = row0 + 2 * rp;
+    const int64_t gr = n_s + r;
+    const int bytes = (gr + 1 < m) ? 16 : ((gr < m) ? 8 : 0);
+    for (int t = tb; t < l; t += 4) cp_async16(vs + t * TB_VLD + 2 * rp, Yp + r + (int64_t)t * lda, bytes);
+    const int cp2 = tid & 31, tz = tid >> 5;  // 32 column pairs x 8 row lanes
+    for (int t = tz; t < l; t += 8) cp_async16(zs + t * TB_ZLD + 2 * cp2, Wt + (int64_t)t * ldz + col0 + 2 * cp2, 16);
+    cp_async_commit();
   }
-  for (int e = tid; e < lp4 * TB_COLS; e += TB_T) {
-    const int t = e >> 6, c2 = e & 63;
-    double* dst = zs + t * TB_ZLD + c2;
-    if (t < l && col0 + c2 < ncols)
-      cp_async8(dst, Wt + (int64_t)t * n + col0 + c2);
-    else
-      *dst = 0.0;
-  }
-  cp_async_commit();
+  // ---- the C tile into the accumulators (HBM reads overlap the staging) ----
   double acc[4][4][2];
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt) {
     const int64_t r = row0 + wm * 32 + mt * 8 + (lane >> 2);
+    const bool rv = r >= 0 && r < mp;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       const int64_t cc = col0 + wn * 32 + nt * 8 + 2 * (lane & 3);
-      const bool rv = r < mp;
       const double* p = Cp + r + cc * lda;
       acc[mt][nt][0] = (rv && cc < ncols) ? p[0] : 0.0;
       acc[mt][nt][1] = (rv && cc + 1 < ncols) ? p[lda] : 0.0;
     }
   }
   cp_async_wait<0>();
+  __syncthreads();
+  // ---- Y structure / padding fixups (first tile, bottom tile, t in [l, lp4)) ----
+  if (row0 < 72 || row0 + TB_ROWS > mp) {
+    for (int e = tid; e < l * TB_ROWS; e += TB_T) {
+      const int t = e >> 7, rr = e & 127;
+      const int64_t r = row0 + rr;
+      if (r < 0 || r >= mp || r <= t) vs[t * TB_VLD + rr] = (r == t) ? 1.0 : 0.0;
+    }
+  }
+  for (int e = tid; e < (lp4 - l) * TB_ROWS; e += TB_T) vs[l * TB_VLD + e / TB_ROWS * TB_VLD + e % TB_ROWS] = 0.0;
+  for (int e = tid; e < (lp4 - l) * TB_COLS; e += TB_T) zs[l * TB_ZLD + e / TB_COLS * TB_ZLD + e % TB_COLS] = 0.0;
   __syncthreads();
   for (int ks = 0; ks < lp4; ks += 4) {
     const int t = ks + (lane & 3);
@@ -243,13 +266,153 @@ __global__ void __launch_bounds__(TB_T, 2) k_trail_b(const Ctl* __restrict__ c, 
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt) {
     const int64_t r = row0 + wm * 32 + mt * 8 + (lane >> 2);
-    if (r >= mp) continue;
+    if (r < 0 || r >= mp) continue;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       const int64_t cc = col0 + wn * 32 + nt * 8 + 2 * (lane & 3);
       double* p = Cp + r + cc * lda;
       if (cc < ncols) p[0] = acc[mt][nt][0];
       if (cc + 1 < ncols) p[lda] = acc[mt][nt][1];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent form of C -= Y Wt: one CTA per SM walks a contiguous range of
+// (row block, 32-column tile) work items; the 128 x 68 Y block stays in shared
+// memory while the CTA sweeps its columns, and the next tile's C and Wt are
+// prefetched with cp.async while the current one runs on the DMMA pipe.
+// ---------------------------------------------------------------------------
+constexpr int TP_T = 256;               // 8 warps: 4 (rows) x 2 (cols), each 32 x 16
+constexpr int TP_ROWS = 128;
+constexpr int TP_COLS = 32;
+constexpr int TP_VLD = TP_ROWS + 8;     // 136
+constexpr int TP_ZLD = TP_COLS + 8;     // 40 = 8 mod 16
+constexpr int TP_CLD = TP_ROWS + 2;     // 130: fragment reads conflict-free, 16B aligned pairs
+constexpr size_t TP_SMEM = sizeof(double) * (TB_KMAX * TP_VLD + 2 * TB_KMAX * TP_ZLD + 2 * TP_COLS * TP_CLD);
+
+__global__ void __launch_bounds__(TP_T, 1) k_trail_bp(const Ctl* __restrict__ c, double* __restrict__ A,
+                                                      const double* __restrict__ Wt, int64_t ldz) {
+  if (c->done) return;
+  const int64_t n_s = c->n_s, m = c->m, n = c->n, lda = c->lda;
+  const int l = c->l_acc;
+  const int64_t c0 = c->tc0, ncols = n - c0, mp = m - n_s;
+  if (l == 0 || ncols <= 0) return;
+  const int odd = (int)(n_s & 1);
+  const int64_t nrb = ceil_div(mp + odd, TP_ROWS), ntc = ceil_div(ncols, TP_COLS);
+  const int64_t total = nrb * ntc;
+  const int64_t it0 = (int64_t)blockIdx.x * total / gridDim.x, it1 = (int64_t)(blockIdx.x + 1) * total / gridDim.x;
+  if (it0 >= it1) return;
+  const int lp4 = (l + 3) / 4 * 4;
+  extern __shared__ __align__(16) double tps[];
+  double* vs = tps;                                   // [68][136]  Y[r][t]
+  double* zsb[2] = {vs + TB_KMAX * TP_VLD, vs + TB_KMAX * TP_VLD + TB_KMAX * TP_ZLD};
+  double* csb[2] = {zsb[1] + TB_KMAX * TP_ZLD, zsb[1] + TB_KMAX * TP_ZLD + TP_COLS * TP_CLD};
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int wm = wid & 3, wn = wid >> 2;
+  const double* Yp = A + n_s * lda + n_s;
+  double* Cp = A + n_s + c0 * lda;
+
+  auto load_y = [&](int64_t rbk) {
+    const int64_t row0 = rbk * TP_ROWS - odd;
+    const int rp = tid & 63, tb = tid >> 6;
+    const int64_t r = row0 + 2 * rp;
+    const int64_t gr = n_s + r;
+    const int bytes = (gr + 1 < m) ? 16 : ((gr < m) ? 8 : 0);
+    for (int t = tb; t < l; t += 4) cp_async16(vs + t * TP_VLD + 2 * rp, Yp + r + (int64_t)t * lda, bytes);
+  };
+  auto fix_y = [&](int64_t rbk) {  // after the copy landed
+    const int64_t row0 = rbk * TP_ROWS - odd;
+    if (row0 < 72 || row0 + TP_ROWS > mp)
+      for (int e = tid; e < l * TP_ROWS; e += TP_T) {
+        const int t = e >> 7, rr = e & 127;
+        const int64_t r = row0 + rr;
+        if (r < 0 || r >= mp || r <= t) vs[t * TP_VLD + rr] = (r == t) ? 1.0 : 0.0;
+      }
+    for (int e = tid; e < (lp4 - l) * TP_ROWS; e += TP_T) vs[(l + e / TP_ROWS) * TP_VLD + e % TP_ROWS] = 0.0;
+  };
+  auto load_tile = [&](int64_t it, int buf) {  // C (128 x 32) and Wt (68 x 32) of work item it
+    const int64_t rbk = it / ntc, ctk = it % ntc;
+    const int64_t row0 = rbk * TP_ROWS - odd, col0 = ctk * TP_COLS;
+    {
+      const int rp = tid & 63, cb = tid >> 6;  // 64 row pairs x 4 column lanes
+      const int64_t r = row0 + 2 * rp;
+      const int64_t gr = n_s + r;
+      const int bytes = (gr + 1 < m) ? 16 : ((gr < m) ? 8 : 0);
+      for (int cc = cb; cc < TP_COLS; cc += 4)
+        cp_async16(csb[buf] + cc * TP_CLD + 2 * rp, Cp + r + (col0 + cc) * lda, (col0 + cc < ncols) ? bytes : 0);
+    }
+    {
+      const int cp2 = tid & 15, tz = tid >> 4;  // 16 column pairs x 16 row lanes
+      for (int t = tz; t < l; t += 16)
+        cp_async16(zsb[buf] + t * TP_ZLD + 2 * cp2, Wt + (int64_t)t * ldz + col0 + 2 * cp2, 16);
+    }
+  };
+
+  int64_t cur_rb = it0 / ntc;
+  load_y(cur_rb);
+  load_tile(it0, 0);
+  cp_async_commit();
+  for (int64_t it = it0; it < it1; ++it) {
+    const int buf = (int)((it - it0) & 1);
+    const int64_t rbk = it / ntc, ctk = it % ntc;
+    const bool next_same_rb = (it + 1 < it1) && ((it + 1) / ntc == rbk);
+    if (it + 1 < it1 && next_same_rb) {
+      load_tile(it + 1, buf ^ 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (it == it0 || rbk != cur_rb) {
+      cur_rb = rbk;
+      fix_y(rbk);
+    }
+    double* zs = zsb[buf];
+    const double* cs = csb[buf];
+    for (int e = tid; e < (lp4 - l) * TP_COLS; e += TP_T) zs[(l + e / TP_COLS) * TP_ZLD + e % TP_COLS] = 0.0;
+    __syncthreads();
+    const int64_t row0 = rbk * TP_ROWS - odd, col0 = ctk * TP_COLS;
+    double acc[4][2][2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int rr = wm * 32 + mt * 8 + (lane >> 2);
+        const int cc = wn * 16 + nt * 8 + 2 * (lane & 3);
+        acc[mt][nt][0] = cs[cc * TP_CLD + rr];
+        acc[mt][nt][1] = cs[(cc + 1) * TP_CLD + rr];
+      }
+    for (int ks = 0; ks < lp4; ks += 4) {
+      const int t = ks + (lane & 3);
+      double af[4], bf[2];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) af[mt] = -vs[t * TP_VLD + wm * 32 + mt * 8 + (lane >> 2)];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) bf[nt] = zs[t * TP_ZLD + wn * 16 + nt * 8 + (lane >> 2)];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+    }
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int64_t r = row0 + wm * 32 + mt * 8 + (lane >> 2);
+      if (r < 0 || r >= mp) continue;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int64_t cc = col0 + wn * 16 + nt * 8 + 2 * (lane & 3);
+        double* p = Cp + r + cc * lda;
+        if (cc < ncols) p[0] = acc[mt][nt][0];
+        if (cc + 1 < ncols) p[lda] = acc[mt][nt][1];
+      }
+    }
+    __syncthreads();
+    if (it + 1 < it1 && !next_same_rb) {  // new row block: reload Y (and the tile) after this one
+      load_y((it + 1) / ntc);
+      load_tile(it + 1, buf ^ 1);
+      cp_async_commit();
     }
   }
 }
