@@ -105,15 +105,19 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
 
 /*
  * Batched QRDM / QRDM2 over `batch` independent m x n matrices stored at
- * A + b*stride (cfg3; one matrix per CTA, the whole decision loop on chip).
- * Per-matrix outputs are strided the same way: coeffs + b*min(m,n),
- * perm + b*n, steps + b*step_cap, swaps + b*2*swap_cap; infos is a DEVICE
- * array of `batch` dmqr_info.  Limits: m <= 512, n <= 512.
+ * A + b*stride (cfg3: batches of small matrices).  The batch is spread over
+ * `nlanes` concurrent CUDA streams (one host thread each, every lane running
+ * the same device-resident engine as dmqr_qrdm_f64), joined back to `stream`.
+ * Per-matrix outputs are strided: coeffs + b*min(m,n), perm + b*n,
+ * swaps + b*2*swap_cap, steps + b*step_cap (device); infos[b] (HOST).
+ * workspace >= dmqr_batched_workspace_bytes(m, n, params, nlanes).
+ * Returns the first non-zero per-matrix status (all matrices are attempted).
  */
-int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_t lda,
-                          int64_t stride, const dmqr_params* params, double* coeffs, int64_t* perm,
-                          int64_t* swaps, int64_t swap_cap, dmqr_step* steps, int64_t step_cap,
-                          dmqr_info* infos, void* stream);
+size_t dmqr_batched_workspace_bytes(int64_t m, int64_t n, const dmqr_params* params, int32_t nlanes);
+int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_t lda, int64_t stride,
+                          const dmqr_params* params, double* coeffs, int64_t* perm, int64_t* swaps,
+                          int64_t swap_cap, dmqr_step* steps, int64_t step_cap, dmqr_info* infos,
+                          int32_t nlanes, void* workspace, size_t ws_bytes, void* stream);
 
 /*
  * Explicit thin/full Q: Q (m x qcols, column-major, ldq) = H_0 H_1 ... H_{p-1} [I; 0]

@@ -16,6 +16,7 @@ EXPORTS = (
     "dmqr_workspace_bytes",
     "dmqr_qrdm_f64",
     "dmqr_qrdm_batched_f64",
+    "dmqr_batched_workspace_bytes",
     "dmqr_form_q_f64",
     "dmqr_form_q_workspace_bytes",
     "dmqr_check_finite_f64",
@@ -104,8 +105,10 @@ def load() -> C.CDLL:
                                   C.POINTER(Info), VP]
     lib.dmqr_qrdm_f64.restype = C.c_int
     lib.dmqr_qrdm_batched_f64.argtypes = [P, I64, I64, I64, I64, I64, C.POINTER(Params), P, P, P, I64, P, I64,
-                                          P, VP]
+                                          P, I32, P, SZ, VP]
     lib.dmqr_qrdm_batched_f64.restype = C.c_int
+    lib.dmqr_batched_workspace_bytes.argtypes = [I64, I64, C.POINTER(Params), I32]
+    lib.dmqr_batched_workspace_bytes.restype = SZ
     lib.dmqr_form_q_f64.argtypes = [P, I64, I64, I64, P, I64, P, I64, I64, P, SZ, VP]
     lib.dmqr_form_q_f64.restype = C.c_int
     lib.dmqr_form_q_workspace_bytes.argtypes = [I64, I64]

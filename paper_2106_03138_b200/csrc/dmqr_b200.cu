@@ -11,6 +11,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
+#include <thread>
+#include <vector>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -105,7 +108,10 @@ cudaError_t& last_cuda_error() {
 bool attrs_done = false;
 bool cluster16 = false;
 
+std::mutex g_attr_mu;
+
 int set_attrs(const DevInfo& d) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
   if (attrs_done) return 0;
   CK(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GRAM_SMEM));
   CK(cudaFuncSetAttribute(k_trail_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA_SMEM));
@@ -431,12 +437,66 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   return hc.status;
 }
 
+size_t dmqr_batched_workspace_bytes(int64_t m, int64_t n, const dmqr_params* params, int32_t nlanes) {
+  return (size_t)std::max(1, nlanes) * al(dmqr_workspace_bytes(m, n, params));
+}
+
 int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_t lda, int64_t stride,
-                          const dmqr_params* params, double* coeffs, int64_t* perm, int64_t* swaps, int64_t swap_cap,
-                          dmqr_step* steps, int64_t step_cap, dmqr_info* infos, void* stream) {
-  (void)A; (void)batch; (void)m; (void)n; (void)lda; (void)stride; (void)params; (void)coeffs; (void)perm;
-  (void)swaps; (void)swap_cap; (void)steps; (void)step_cap; (void)infos; (void)stream;
-  return DMQR_EINVAL;  // filled in by the on-chip batched kernel
+                          const dmqr_params* p, double* coeffs, int64_t* perm, int64_t* swaps, int64_t swap_cap,
+                          dmqr_step* steps, int64_t step_cap, dmqr_info* infos, int32_t nlanes, void* workspace,
+                          size_t ws_bytes, void* stream) {
+  int rc = validate(m, n, lda, p);
+  if (rc) return rc;
+  if (batch < 0 || stride < lda * n || !infos || nlanes < 1) return DMQR_EINVAL;
+  const size_t per = al(dmqr_workspace_bytes(m, n, p));
+  nlanes = (int32_t)std::min<int64_t>(nlanes, std::max<int64_t>(batch, 1));
+  if (m > 4096) nlanes = 1;  // cooperative panel launches must not compete for co-residency
+  if (ws_bytes < per * (size_t)nlanes || !workspace) return DMQR_EINVAL;
+  if (batch == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const DevInfo d = dev_info();
+  if ((rc = set_attrs(d))) return rc;
+  // lanes start after the caller's stream reaches this point, and the caller's
+  // stream waits for every lane at the end
+  cudaEvent_t start;
+  CK(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  CK(cudaEventRecord(start, st));
+  const int64_t kmax = std::min(m, n);
+  std::vector<int> lane_rc(nlanes, 0);
+  std::vector<cudaStream_t> ls(nlanes);
+  std::vector<cudaEvent_t> done(nlanes);
+  for (int q = 0; q < nlanes; ++q) {
+    CK(cudaStreamCreateWithFlags(&ls[q], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&done[q], cudaEventDisableTiming));
+    CK(cudaStreamWaitEvent(ls[q], start, 0));
+  }
+  auto work = [&](int q) {
+    cudaSetDevice(dev);
+    unsigned char* ws = (unsigned char*)workspace + per * (size_t)q;
+    for (int64_t b = q; b < batch; b += nlanes) {
+      const int r = dmqr_qrdm_f64(A + b * stride, m, n, lda, p, coeffs + b * kmax, perm + b * n,
+                                  swaps + b * 2 * swap_cap, swap_cap, steps + b * step_cap, step_cap, nullptr, ws,
+                                  per, &infos[b], (void*)ls[q]);
+      infos[b].status = r;
+      if (r && !lane_rc[q]) lane_rc[q] = r;
+    }
+    cudaEventRecord(done[q], ls[q]);
+  };
+  std::vector<std::thread> th;
+  for (int q = 1; q < nlanes; ++q) th.emplace_back(work, q);
+  work(0);
+  for (auto& t : th) t.join();
+  for (int q = 0; q < nlanes; ++q) {
+    CK(cudaStreamWaitEvent(st, done[q], 0));
+    cudaEventDestroy(done[q]);
+    cudaStreamDestroy(ls[q]);
+  }
+  cudaEventDestroy(start);
+  for (int q = 0; q < nlanes; ++q)
+    if (lane_rc[q]) return lane_rc[q];
+  return 0;
 }
 
 size_t dmqr_form_q_workspace_bytes(int64_t m, int64_t qcols) {

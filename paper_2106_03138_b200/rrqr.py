@@ -347,9 +347,14 @@ def to_result(f: DeviceFactor, device: bool = False) -> RRQRResult:
         trace = [float(x) for x in tr if not np.isnan(x)]
     if device:
         packed, coeffs = packed_t, f.coeffs
+    elif f.m and f.n:
+        # rows of buf are the columns: copy (n, m) row-major and view it as an F-ordered (m, n)
+        host = f.buf[: f.n, : f.m]
+        host = host.cpu() if host.is_contiguous() else host.contiguous().cpu()
+        packed = host.numpy().T
+        coeffs = f.coeffs.cpu().numpy()
     else:
-        packed = np.asfortranarray(packed_t.cpu().numpy()) if f.m and f.n else np.zeros((f.m, f.n), order="F")
-        coeffs = f.coeffs.cpu().numpy() if min(f.m, f.n) else np.zeros(0)
+        packed, coeffs = np.zeros((f.m, f.n), order="F"), np.zeros(0)
     return RRQRResult(packed=packed, coeffs=coeffs, perm=perm, rank=int(info.rank), step_log=steps,
                       n_factored=int(info.n_factored), stopped_early=bool(info.stopped_early),
                       counters=replay_counters(f.m, f.n, steps), norm_trace=trace)

@@ -153,3 +153,22 @@ def test_deterministic_repeat():
 @pytest.mark.parametrize("name", ["cfg2s/1024", "cfg4s/8192x256"])
 def test_midsize_golden(name):
     test_golden_case.__wrapped__(name) if hasattr(test_golden_case, "__wrapped__") else test_golden_case(name)
+
+
+def test_batched_equals_single_and_oracle():
+    """cfg3-style batch through dmqr_qrdm_batched_f64 (concurrent lanes): each matrix
+    must equal its single-matrix factorization bit for bit (same device engine) and
+    the oracle on the robust prefix."""
+    from paper_2106_03138_b200 import inputs, qrdm2
+    from paper_2106_03138_b200.batch import factorize_batch
+
+    B = inputs.cfg3(seed=3, batch=6)
+    f = factorize_batch(B, lanes=4)
+    for i in range(B.shape[0]):
+        r = f.result(i)
+        s = qrdm2(B[i])
+        assert np.array_equal(r.perm.forward, s.perm.forward) and r.rank == s.rank
+        assert np.array_equal(r.packed, s.packed) and np.array_equal(r.coeffs, s.coeffs)
+        with threadpool_limits(1):
+            ref = O.qrdm2(B[i], margins=True)
+        _compare(B[i], r, ref, f"cfg3[{i}]")
