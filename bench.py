@@ -252,12 +252,12 @@ def run_b200(args, rank, world):
     pinned = torch.from_numpy(np.ascontiguousarray(A)).pin_memory()
     e2e_ms = []
     res = None
-    for i in range(args.steps + 1):
+    for i in range(args.steps + 2):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         res = rrqr.qrdm2(pinned)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_ms = e2e_ms[1:]
+    e2e_ms = e2e_ms[2:]  # first two calls populate the device and pinned-host caches
     e2e_step = statistics.mean(e2e_ms)
     kmax = min(n, n)
     h2d = 8 * n * n
@@ -312,7 +312,7 @@ def run_b200(args, rank, world):
                 "ms_per_step": e2e_step, "path": "paper_2106_03138_b200.qrdm2(pinned host tensor) -> numpy result"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": (achieved / peak_tf) if achieved else None, "traffic": traffic,
-                     "kernel": "trailing update (k_form_v + k_trail_a + k_trail_r + k_trail_b, DMMA)",
+                     "kernel": "trailing update (k_trail_a: Wt = T^T Y^T C split-K + k_trail_b: C -= Y Wt, DMMA m8n8k4 f64)",
                      "peak_source": "cuBLAS DGEMM 8192^3 best-of-5 measured in this run (FP64 peak; "
                                     "MEASURED_PEAKS.json has bf16 only)",
                      "algorithmic_flops_per_step": ftr},

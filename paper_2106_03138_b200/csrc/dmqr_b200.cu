@@ -276,6 +276,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   const int max_coop_p = std::min(d.sms, PANEL_PMAX);
   const int max_cluster = cluster16 ? 16 : 8;
   const bool use_cq = getenv("DMQR_NO_CHOLQR") == nullptr;  // debug switch: Householder panel only
+  const bool trail_persistent = getenv("DMQR_TRAIL_PERSISTENT") != nullptr;  // A/B switch
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
 
   while (kmax > 0) {
@@ -374,7 +375,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
       const int64_t ldz = ldz_for(n);
       k_trail_a<<<dim3((unsigned)ntile, nsplit), TA_T, TA_SMEM, st>>>(ctl, A, Zp, T, Z, tcount, ldz);
       NOTE_LAUNCH();
-      if (getenv("DMQR_TRAIL_B_TILED")) {
+      if (!trail_persistent) {
         k_trail_b<<<dim3((unsigned)ceil_div(mp + 1, TB_ROWS), (unsigned)ceil_div(ncols_ub, TB_COLS)), TB_T, TB_SMEM,
                     st>>>(ctl, A, Z, ldz);
       } else {

@@ -53,25 +53,78 @@ __device__ __forceinline__ double cq_rsqrt(double d) {
 
 // upper Cholesky (A = R^T R) of the leading n x n of A (upper triangle read,
 // destroyed); R -> out (upper, zero below).  Returns the first j whose pivot
-// fails pivot > tol * orig[j] (or n); piv[j] receives the pivots.
-// One barrier per column; the trailing update is warp-per-row over the upper triangle.
+// fails pivot > tol * orig[j] (or n); piv[j] receives the pivots.  On a failure
+// at j the leading j x j of R is complete.
+// Blocked by 8 (right-looking): warp 0 factors the diagonal block in registers
+// (lane c = column c, shuffles), then a triangular solve for the block row
+// (thread per column) and a rank-8 update of the trailing upper triangle.
 __device__ int cq_chol(double* A, double* out, double* piv, const double* orig, int n, double tol) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int e = threadIdx.x; e < DMQR_KP * DMQR_KP; e += blockDim.x) out[e] = 0.0;
+  __shared__ int s_fail;
+  __shared__ double s_rs[DMQR_KP];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int e = tid; e < DMQR_KP * DMQR_KP; e += blockDim.x) out[e] = 0.0;
   __syncthreads();
-  for (int j = 0; j < n; ++j) {
-    const double d = A[j * DMQR_KP + j];
-    if (!(d > tol * orig[j] && d > 0.0)) {
-      __syncthreads();
-      return j;
+  for (int b0 = 0; b0 < n; b0 += 8) {
+    const int bw = min(8, n - b0);
+    if (tid < 32) {
+      double a[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) a[r] = (lane < bw && r <= lane) ? A[(b0 + r) * DMQR_KP + b0 + lane] : 0.0;
+      int fail = n;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j < bw && fail == n) {
+          const double d = __shfl_sync(0xffffffffu, a[j], j);
+          if (!(d > tol * orig[b0 + j] && d > 0.0)) {
+            fail = b0 + j;
+          } else {
+            const double rs = cq_rsqrt(d);
+            const double rjc = (lane == j) ? d * rs : a[j] * rs;  // R[j][lane]
+            if (lane >= j && lane < bw) out[(b0 + j) * DMQR_KP + b0 + lane] = rjc;
+            if (lane == 0) {
+              piv[b0 + j] = d;
+              s_rs[b0 + j] = rs;
+            }
+#pragma unroll
+            for (int r = j + 1; r < 8; ++r) {
+              const double rjr = __shfl_sync(0xffffffffu, rjc, r);
+              if (r <= lane) a[r] -= rjr * rjc;
+            }
+          }
+        }
+      }
+      if (lane == 0) s_fail = fail;
     }
-    const double rs = cq_rsqrt(d);
-    const double rd = rs * rs;
-    for (int cc = j + threadIdx.x; cc < n; cc += blockDim.x) out[j * DMQR_KP + cc] = (cc == j) ? d * rs : A[j * DMQR_KP + cc] * rs;
-    if (threadIdx.x == 0) piv[j] = d;
-    for (int r = j + 1 + wid; r < n; r += nw) {
-      const double f = A[j * DMQR_KP + r] * rd;
-      for (int cc = r + lane; cc < n; cc += 32) A[r * DMQR_KP + cc] -= f * A[j * DMQR_KP + cc];
+    __syncthreads();
+    if (s_fail < n) return s_fail;
+    const int c0 = b0 + bw;
+    // block row: R[b0+j][cc] = (A[b0+j][cc] - sum_{t<j} R[b0+t][b0+j] R[b0+t][cc]) / R_jj
+    for (int cc = c0 + tid; cc < n; cc += blockDim.x) {
+      double x[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        x[j] = 0.0;
+        if (j < bw) {
+          double s = A[(b0 + j) * DMQR_KP + cc];
+#pragma unroll
+          for (int t = 0; t < j; ++t) s -= out[(b0 + t) * DMQR_KP + b0 + j] * x[t];
+          x[j] = s * s_rs[b0 + j];
+          out[(b0 + j) * DMQR_KP + cc] = x[j];
+        }
+      }
+    }
+    __syncthreads();
+    // trailing upper triangle: A[i][j] -= sum_t R[b0+t][i] R[b0+t][j]
+    const int nt = n - c0;
+    for (int e = tid; e < nt * nt; e += blockDim.x) {
+      const int i = c0 + e / nt, j = c0 + e % nt;
+      if (j >= i) {
+        double s = 0.0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (t < bw) s += out[(b0 + t) * DMQR_KP + i] * out[(b0 + t) * DMQR_KP + j];
+        A[i * DMQR_KP + j] -= s;
+      }
     }
     __syncthreads();
   }
@@ -79,12 +132,13 @@ __device__ int cq_chol(double* A, double* out, double* piv, const double* orig, 
 }
 
 // X = U^-1 for upper triangular U (leading n x n of a KP row-major array);
-// X[i][j] is stored at X[i*xr + j*xc].  Blocked by 8: diagonal blocks by
-// back substitution (thread per column), then one block diagonal at a time.
+// X[i][j] is stored at X[i*xr + j*xc].  Blocked by 8: diagonal blocks by back
+// substitution (thread per column), then one block diagonal at a time, each
+// off-diagonal block X_ij = -X_ii (sum_t U_it X_tj) by one warp on DMMA.
 __device__ void cq_trinv_upper(const double* U, double* X, int n, int xr = DMQR_KP, int xc = 1) {
   const int nb = (n + 7) / 8;
   __shared__ double rdiag[DMQR_KP];
-  __shared__ double tmp[DMQR_KP * 8];
+  __shared__ double wst[PANEL_T / 32][64];
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) X[(e / n) * xr + (e % n) * xc] = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) rdiag[i] = 1.0 / U[i * DMQR_KP + i];
   __syncthreads();
@@ -94,8 +148,7 @@ __device__ void cq_trinv_upper(const double* U, double* X, int n, int xr = DMQR_
       double xv[8];
       const int i0 = b * 8, nl = cix - i0;  // local column index within the block
 #pragma unroll
-      for (int q = 0; q < 8; ++q) xv[q] = 0.0;
-      xv[nl] = rdiag[cix];
+      for (int q = 0; q < 8; ++q) xv[q] = (q == nl) ? rdiag[cix] : 0.0;
 #pragma unroll
       for (int q = 7; q >= 0; --q) {
         if (q >= nl) continue;
@@ -112,43 +165,122 @@ __device__ void cq_trinv_upper(const double* U, double* X, int n, int xr = DMQR_
     }
   }
   __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lr = lane >> 2, lk = lane & 3;
+  double* w = wst[wid];
   for (int d = 1; d < nb; ++d) {
-    const int nblk = nb - d;
-    for (int e = threadIdx.x; e < nblk * 64; e += blockDim.x) {
-      const int bi = e >> 6, r = (e >> 3) & 7, cc = e & 7;
-      const int i = bi * 8 + r, jj = (bi + d) * 8 + cc;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      if (i < n && jj < n) {
-        int t = (bi + 1) * 8;
-        for (; t + 3 <= jj; t += 4) {
-          s0 += U[i * DMQR_KP + t] * X[t * xr + jj * xc];
-          s1 += U[i * DMQR_KP + t + 1] * X[(t + 1) * xr + jj * xc];
-          s2 += U[i * DMQR_KP + t + 2] * X[(t + 2) * xr + jj * xc];
-          s3 += U[i * DMQR_KP + t + 3] * X[(t + 3) * xr + jj * xc];
-        }
-        for (; t <= jj; ++t) s0 += U[i * DMQR_KP + t] * X[t * xr + jj * xc];
+    for (int bi = wid; bi < nb - d; bi += nw) {
+      const int bj = bi + d;
+      const int ar = bi * 8 + lr, bc = bj * 8 + lr;
+      double c0 = 0.0, c1 = 0.0;
+      for (int t0 = (bi + 1) * 8; t0 < (bj + 1) * 8; t0 += 4) {
+        const int t = t0 + lk;
+        const double av = (ar < n && t < n) ? U[ar * DMQR_KP + t] : 0.0;
+        const double bv = (t < n && bc < n) ? X[t * xr + bc * xc] : 0.0;
+        dmma884(c0, c1, av, bv);
       }
-      tmp[bi * 64 + r * 8 + cc] = (s0 + s1) + (s2 + s3);
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < nblk * 64; e += blockDim.x) {
-      const int bi = e >> 6, r = (e >> 3) & 7, cc = e & 7;
-      const int i = bi * 8 + r, jj = (bi + d) * 8 + cc;
-      if (i < n && jj < n) {
-        double s = 0.0;
+      w[lr * 8 + 2 * lk] = c0;
+      w[lr * 8 + 2 * lk + 1] = c1;
+      __syncwarp();
+      double e0 = 0.0, e1 = 0.0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int t = bi * 8 + q;
-          if (t >= i && t < n) s += X[i * xr + t * xc] * tmp[bi * 64 + q * 8 + cc];
-        }
-        X[i * xr + jj * xc] = -s;
+      for (int k0 = 0; k0 < 8; k0 += 4) {
+        const int kc = bi * 8 + k0 + lk;
+        const double av = (ar < n && kc < n) ? X[ar * xr + kc * xc] : 0.0;
+        dmma884(e0, e1, av, w[(k0 + lk) * 8 + lr]);
       }
+      const int oc = bj * 8 + 2 * lk;
+      if (ar < n && oc < n) X[ar * xr + oc * xc] = -e0;
+      if (ar < n && oc + 1 < n) X[ar * xr + (oc + 1) * xc] = -e1;
+      __syncwarp();
     }
     __syncthreads();
   }
 }
 
-// slice[:, 0:ncol] <- slice[:, 0:kin] * M (M: kin x ncol, KP row-major) in place,
+// Modified LU (Ballard et al.) of the leading l x l of A (KP row-major), in
+// place: strict lower <- multipliers L_ij = -S_j q'_ij / (1 + |q'_jj|), upper
+// <- the eliminated q' (unsigned); S_j = -sign(q'_jj) -> vS, pivots -> vpiv.
+// Blocked by 8: warp 0 eliminates the 8-column panel over all rows (lane =
+// row, shuffles), then the block rows' columns to the right (thread per
+// column) and a rank-8 update of the trailing block.
+__device__ void cq_mlu(double* A, double* vS, double* vpiv, int l) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int b0 = 0; b0 < l; b0 += 8) {
+    const int bw = min(8, l - b0);
+    if (tid < 32) {
+      double v[3][8];
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int i = b0 + lane + 32 * s;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[s][c] = (i < l && c < bw) ? A[i * DMQR_KP + b0 + c] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j < bw) {
+          double qj[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) qj[c] = __shfl_sync(0xffffffffu, v[0][c], j);
+          const double qjj = qj[j];
+          const double sg = (qjj >= 0.0) ? -1.0 : 1.0;  // S_j = -sign(q'_jj), sign(+0) = +
+          const double pv = 1.0 - sg * qjj;             // pivot = 1 + |q'_jj|
+          const double f0 = -sg / pv;
+#pragma unroll
+          for (int s = 0; s < 3; ++s) {
+            const int i = b0 + lane + 32 * s;
+            if (i > b0 + j && i < l) {
+              const double L = f0 * v[s][j];
+#pragma unroll
+              for (int c = j + 1; c < 8; ++c) v[s][c] -= L * qj[c];
+              v[s][j] = L;
+            }
+          }
+          if (lane == 0) {
+            vS[b0 + j] = sg;
+            vpiv[b0 + j] = pv;
+          }
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int i = b0 + lane + 32 * s;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (i < l && c < bw) A[i * DMQR_KP + b0 + c] = v[s][c];
+      }
+    }
+    __syncthreads();
+    const int c0 = b0 + bw;
+    // block rows, columns >= c0: forward elimination with the block's multipliers
+    for (int cc = c0 + tid; cc < l; cc += blockDim.x) {
+      double x[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = (j < bw) ? A[(b0 + j) * DMQR_KP + cc] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int i = j + 1; i < 8; ++i)
+          if (i < bw) x[i] -= A[(b0 + i) * DMQR_KP + b0 + j] * x[j];
+#pragma unroll
+      for (int j = 1; j < 8; ++j)
+        if (j < bw) A[(b0 + j) * DMQR_KP + cc] = x[j];
+    }
+    __syncthreads();
+    const int nt = l - c0;
+    for (int e = tid; e < nt * nt; e += blockDim.x) {
+      const int i = c0 + e / nt, cc = c0 + e % nt;
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < bw) s += A[i * DMQR_KP + b0 + j] * A[(b0 + j) * DMQR_KP + cc];
+      A[i * DMQR_KP + cc] -= s;
+    }
+    __syncthreads();
+  }
+}
+
+// slice[:, 0:ncol] <- slice[:, 0:kin] * M (M: kin x ncol upper triangular, KP row-major) in place,
 // rows [0, R); each warp owns 8-row tiles (DMMA 8x8x4, accumulators in registers).
 __device__ void cq_slice_gemm(double* sl, int R, int kin, int ncol, const double* M) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -163,7 +295,7 @@ __device__ void cq_slice_gemm(double* sl, int R, int kin, int ncol, const double
       const double av = (kc < kin) ? sl[kc * CQ_LDS + r] : 0.0;
 #pragma unroll
       for (int q = 0; q < DMQR_KP / 8; ++q)
-        if (q < nt_n) {
+        if (q < nt_n && 4 * ks < 8 * (q + 1)) {  // M upper triangular: rows > 8q+7 are zero
           const int cc = q * 8 + (lane >> 2);
           const double bv = (kc < kin) ? M[kc * DMQR_KP + cc] : 0.0;
           dmma884(acc[q][0], acc[q][1], av, bv);
@@ -182,17 +314,18 @@ __device__ void cq_slice_gemm(double* sl, int R, int kin, int ncol, const double
   }
 }
 
-// C = A B for n x n upper-triangular A, B given as element loaders (KP padded),
-// result -> C (KP row-major, zero below); DMMA over 8x8 tiles, warp per tile.
-template <class LA, class LB>
+// C = A B for n x n upper-triangular B and upper-triangular (or, AFULL, full) A
+// given as element loaders (KP padded), result -> C (KP row-major; zero below
+// unless AFULL); DMMA over 8x8 tiles, warp per tile.
+template <bool AFULL = false, class LA, class LB>
 __device__ void cq_small_gemm(LA la, LB lb, double* C, int n) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int nt = (n + 7) / 8;
   for (int t = wid; t < nt * nt; t += nw) {
     const int ti = t / nt, tj = t % nt;
     double c0 = 0.0, c1 = 0.0;
-    if (tj >= ti)
-      for (int ks = ti * 2; ks <= tj * 2 + 1; ++ks) {  // k range of the triangular product
+    if (AFULL || tj >= ti)
+      for (int ks = AFULL ? 0 : ti * 2; ks <= tj * 2 + 1; ++ks) {  // k range of the triangular product
         const int kc = 4 * ks + (lane & 3);
         const int ar = ti * 8 + (lane >> 2), bc = tj * 8 + (lane >> 2);
         const double av = (ar < n && kc < n) ? la(ar, kc) : 0.0;
@@ -200,8 +333,8 @@ __device__ void cq_small_gemm(LA la, LB lb, double* C, int n) {
         dmma884(c0, c1, av, bv);
       }
     const int row = ti * 8 + (lane >> 2), col = tj * 8 + 2 * (lane & 3);
-    C[row * DMQR_KP + col] = (col >= row) ? c0 : 0.0;
-    C[row * DMQR_KP + col + 1] = (col + 1 >= row) ? c1 : 0.0;
+    C[row * DMQR_KP + col] = (AFULL || col >= row) ? c0 : 0.0;
+    C[row * DMQR_KP + col + 1] = (AFULL || col + 1 >= row) ? c1 : 0.0;
   }
 }
 
@@ -411,43 +544,22 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       const int i = e / l, j = e % l;
       a.red[i * DMQR_KP + j] = (j >= i) ? A2[i * DMQR_KP + j] : 0.0;
     }
-  // ---- P11/P12: Q = Q1 R2^-1 (first l columns; R2 upper in A1) ----
+  // ---- P11: R2^-1 -> A2 (rank 0; R2 upper in A1) ----
   __syncthreads();
   CQT();
-  cq_trinv_upper(A1, A2, l);
-  CQT();
-  cq_slice_gemm(sl, R4, l, l, A2);
-  CQT();
-  __syncthreads();
-  // ---- P13/P14 (rank 0): modified LU of the top l x l block of Q ----
+  double* gR2i = a.red + DMQR_KP * DMQR_KP;  // rank 0's copy of R2^-1 (global scratch)
   if (me == 0) {
-    // A1 <- top block; eliminate in place: strict lower = L (multipliers), upper = q' (unsigned)
-    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
-      const int i = e / DMQR_KP, j = e % DMQR_KP;
-      A1[e] = (i < l && j < l) ? sl[j * CQ_LDS + i] : 0.0;
-    }
+    cq_trinv_upper(A1, A2, l);
+    CQT();
+    for (int e = tid; e < l * l; e += PANEL_T) gR2i[(e / l) * DMQR_KP + e % l] = A2[(e / l) * DMQR_KP + e % l];
+    // ---- P12: top l x l block of Q = Q1 R2^-1 -> A1 ----
+    cq_small_gemm<true>([&](int i, int t) { return sl[t * CQ_LDS + i]; },
+                        [&](int t, int j) { return A2[t * DMQR_KP + j]; }, A1, l);
     __syncthreads();
-    {
-      const int lane = tid & 31, wid = tid >> 5;
-      for (int j = 0; j < l; ++j) {
-        const double qjj = A1[j * DMQR_KP + j];
-        const double sg = (qjj >= 0.0) ? -1.0 : 1.0;  // S_j = -sign(q'_jj), sign(+0) = +
-        const double pv = 1.0 - sg * qjj;             // pivot = 1 + |q'_jj|
-        const double f0 = -sg / pv;
-        // rows i > j: multiplier L_ij = -S_j q'_ij / pivot, then q'_ic -= L_ij q'_jc (c > j)
-        for (int i = j + 1 + wid; i < l; i += PANEL_T / 32) {
-          const double Lij = f0 * A1[i * DMQR_KP + j];
-          for (int cc = j + 1 + lane; cc < l; cc += 32) A1[i * DMQR_KP + cc] -= Lij * A1[j * DMQR_KP + cc];
-          __syncwarp();
-          if (lane == 0) A1[i * DMQR_KP + j] = Lij;
-        }
-        if (tid == 0) {
-          vS[j] = sg;
-          vpiv[j] = pv;
-        }
-        __syncthreads();
-      }
-    }
+    CQT();
+    // ---- P13: modified LU of the top block: strict lower = L (Y1), upper = q' ----
+    cq_mlu(A1, vS, vpiv, l);
+    CQT();
     // U (upper) -> A2: U_jj = pivot, U_jc = -S_c q'_jc
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
       const int i = e / DMQR_KP, j = e % DMQR_KP;
@@ -468,35 +580,36 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       if (j == i) A1[i * DMQR_KP + i] = 1.0;
     }
     __syncthreads();
-    // Z = (Y1^T)^-1 into the (now unused) top l x l block of the slice, Z[i][j] at sl[j*LDS + i]
+    // Z = (Y1^T)^-1 into the top l x l block of the slice (rows < l of Y come
+    // from Y1 at write-back), Z[i][j] at sl[j*LDS + i]
     cq_trinv_upper(A1, sl, l, 1, CQ_LDS);
     // T = U Z (householder.py accumulate_wy's W), tau_j = U_jj
     cq_small_gemm([&](int i, int t) { return A2[i * DMQR_KP + t]; },
                   [&](int t, int j) { return sl[j * CQ_LDS + t]; }, a.T, l);
     for (int j = tid; j < l; j += PANEL_T) a.coeffs[n_s + j] = vpiv[j];
     __syncthreads();
-    // U^-1 -> A1 (upper), broadcast below
+    // U^-1 -> A1 (upper)
     cq_trinv_upper(A2, A1, l);
+    __syncthreads();
+    // M = -R2^-1 S U^-1 -> A2 (upper): Y_below = -(Q1 R2^-1 S) U^-1 = Q1 M
+    cq_small_gemm([&](int i, int t) { return -vS[t] * gR2i[i * DMQR_KP + t]; },
+                  [&](int t, int j) { return A1[t * DMQR_KP + j]; }, A2, l);
+    CQT();
   }
   cl.sync();
-  if (me != 0) {  // pull U^-1 (upper of rank 0's A1) and S from rank 0
-    const double* A1r = cl.map_shared_rank(A1, 0);
+  if (me != 0) {  // pull M (upper of rank 0's A2) and S from rank 0
+    const double* A2r = cl.map_shared_rank(A2, 0);
     const double* vSr = cl.map_shared_rank(vS, 0);
     for (int e = tid; e < l * l; e += PANEL_T) {
       const int i = e / l, j = e % l;
-      A1[i * DMQR_KP + j] = (j >= i) ? A1r[i * DMQR_KP + j] : 0.0;
+      A2[i * DMQR_KP + j] = (j >= i) ? A2r[i * DMQR_KP + j] : 0.0;
     }
     for (int j = tid; j < l; j += PANEL_T) vS[j] = vSr[j];
   }
   cl.sync();
-  // ---- P16: Y = -(Q S) U^-1 on this rank's rows (rank 0's rows < l are fixed below) ----
-  for (int e = tid; e < l * R4; e += PANEL_T) {
-    const int cc = e / R4, rr = e % R4;
-    sl[cc * CQ_LDS + rr] *= -vS[cc];
-  }
-  __syncthreads();
+  // ---- P16: Y = Q1 M on this rank's rows (rank 0's rows < l are fixed below) ----
   CQT();
-  cq_slice_gemm(sl, R4, l, l, A1);
+  cq_slice_gemm(sl, R4, l, l, A2);
   CQT();
   __syncthreads();
   // ---- write back: Y below the diagonal, R_H = S R on and above it (rows < l live on rank 0) ----
