@@ -42,6 +42,7 @@ struct Ctl {
   int32_t mv_dst[2 * DMQR_KP], mv_src[2 * DMQR_KP];
   int32_t cq_fail;  // 1: the CholeskyQR2 panel declined, the Householder panel must run
   int32_t tc0;      // first column of the trailing update (n_s + k_s, or n_s + l after a CholQR break)
+  double cq_diag[4];  // debug: CholQR2 health of the last panel (min pivot ratio 1, |G2 - I|, min pivot ratio 2, jstar)
   // inter-CTA counters (reset by their users)
   uint32_t gram_count;
   uint32_t bar_count;

@@ -263,15 +263,26 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   NOTE_LAUNCH();
   CK(cudaGetLastError());
 
-  static thread_local HostHead* hh = nullptr;  // pinned poll slot, one per host thread
-  if (!hh) CK(cudaMallocHost(&hh, sizeof(HostHead)));
+  // Host loop, pipelined: the host never waits for the step it just enqueued.
+  // It keeps two steps in flight and sizes each launch from a lower bound on
+  // n_s (the last step whose head it has read, plus one column for every step
+  // still in flight -- every step accepts at least one).  Grids are therefore
+  // upper bounds; kernels read the true extents from Ctl and exit surplus
+  // CTAs, and steps enqueued after `done` exit at once.
+  static thread_local HostHead* hh = nullptr;  // pinned poll slots, one pair per host thread
+  static thread_local cudaEvent_t hev[2] = {nullptr, nullptr};
+  if (!hh) {
+    CK(cudaMallocHost(&hh, 2 * sizeof(HostHead)));
+    for (auto& e : hev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   const bool prof = g_prof.load() != 0;
-  cudaEvent_t ev[5];
+  cudaEvent_t ev[2][5];
   if (prof)
-    for (auto& e : ev) CK(cudaEventCreate(&e));
+    for (auto& r : ev)
+      for (auto& e : r) CK(cudaEventCreate(&e));
+  int slot = 0;
 #define PROF(i) \
-  if (prof) CK(cudaEventRecord(ev[i], st))
-  int64_t host_ns = 0;
+  if (prof) CK(cudaEventRecord(ev[slot][i], st))
   int steps_done = 0;
   const int max_coop_p = std::min(d.sms, PANEL_PMAX);
   const int max_cluster = cluster16 ? 16 : 8;
@@ -279,7 +290,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   const bool trail_persistent = getenv("DMQR_TRAIL_PERSISTENT") != nullptr;  // A/B switch
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
 
-  while (kmax > 0) {
+  auto enqueue_step = [&](int64_t host_ns) -> int {
     const int64_t mp = m - host_ns;
     const int64_t np = n - host_ns;
     // ---- selection ----
@@ -396,23 +407,58 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     NOTE_LAUNCH();
     PROF(4);
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(hh, &ctl->n_s, sizeof(HostHead), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpyAsync(&hh[slot], &ctl->n_s, sizeof(HostHead), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(hev[slot], st));
+    return 0;
+  };
+
+  int64_t known_ns = 0;  // n_s after the last step whose head was read
+  int known = 0, enq = 0;
+  bool finished = (kmax == 0);
+  auto consume = [&]() -> int {
+    const int sl = known & 1;
+    CK(cudaEventSynchronize(hev[sl]));
     if (prof) {
       for (int q = 0; q < 4; ++q) {
         float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, ev[q], ev[q + 1]));
+        CK(cudaEventElapsedTime(&ms, ev[sl][q], ev[sl][q + 1]));
         g_acc.ms[q] += ms;
       }
       g_acc.steps += 1;
     }
+    known_ns = hh[sl].n_s;
+    ++known;
+    if (hh[sl].done) finished = true;
+    return 0;
+  };
+  while (!finished) {
+    if (enq - known >= 2) {
+      int rc = consume();
+      if (rc) return rc;
+      if (finished) break;
+    }
+    const int64_t ns_lo = known_ns + (enq - known);
+    if (ns_lo >= kmax) {  // every column is accounted for by the steps in flight
+      while (known < enq && !finished) {
+        int rc = consume();
+        if (rc) return rc;
+      }
+      break;
+    }
+    slot = enq & 1;
+    int rc = enqueue_step(ns_lo);
+    if (rc) return rc;
+    ++enq;
     ++steps_done;
-    host_ns = hh->n_s;
-    if (hh->done) break;
     if (p->max_steps > 0 && steps_done >= p->max_steps) break;  // debug: stop after N steps
   }
+  while (known < enq) {  // drain (profiling reads; the steps themselves are ordered on st)
+    int rc = consume();
+    if (rc) return rc;
+  }
   if (prof)
-    for (auto& e : ev) cudaEventDestroy(e);
+    for (auto& r : ev)
+      for (auto& e : r) cudaEventDestroy(e);
 #undef PROF
   g_calls.fetch_add(1);
   k_finalize<<<1, 256, 0, st>>>(ctl, A, p->stop_rule == DMQR_STOP_NONE);

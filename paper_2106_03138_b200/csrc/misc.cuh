@@ -182,5 +182,6 @@ __global__ void k_debug_ctl(const Ctl* __restrict__ c, int64_t* __restrict__ out
   for (int i = 0; i < DMQR_KP; ++i) *o++ = c->sel[i];
   for (int i = 0; i < DMQR_KP; ++i) *o++ = c->sw_a[i];
   for (int i = 0; i < DMQR_KP; ++i) *o++ = c->sw_b[i];
+  for (int i = 0; i < 4; ++i) *o++ = __double_as_longlong(c->cq_diag[i]);
 }
 }  // namespace dmqr

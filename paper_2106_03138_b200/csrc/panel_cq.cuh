@@ -20,7 +20,7 @@
 //
 // Safety: CholeskyQR2 is accurate only while pass 1 is well conditioned, so the
 // kernel checks every Cholesky pivot (relative to the column's squared norm)
-// and the orthogonality of Q1 (|G2 - I|).  An unhealthy pivot is accepted only
+// and the orthogonality of Q1 (|G2 - I|), see CQ_PIVOT_TOL / CQ_ORTH_TOL.  An unhealthy pivot is accepted only
 // when it proves a QRDM2 break at that column; anything else sets
 // Ctl::cq_fail and exits without writing, and the register-resident
 // Householder panel (panel_rr.cuh) launched right behind it does the panel.
@@ -36,6 +36,13 @@ namespace dmqr {
 constexpr int CQ_KC = DMQR_MAXK;  // stored slice columns (65)
 constexpr int CQ_LDS = 260;       // slice column stride (rows <= 256; 4 mod 16)
 constexpr int CQ_RMAX = 256;
+// Health limits.  Q1 = P R1^-1 goes through an explicit triangular inverse, so
+// its residual |P - Q1 R1| grows like cond(R1) eps: a panel whose pass-1
+// pivots fall below CQ_PIVOT_TOL of the column's squared norm, or whose pass-1
+// Q1 is off orthogonal by CQ_ORTH_TOL (~cond^2 eps, i.e. cond > ~7e3), goes to
+// the Householder panel instead.
+constexpr double CQ_PIVOT_TOL = 1e-7;
+constexpr double CQ_ORTH_TOL = 1e-8;
 constexpr size_t CQ_SMEM =
     sizeof(double) * ((size_t)CQ_KC * CQ_LDS + 2 * DMQR_KP * DMQR_KP + 4 * DMQR_KP);  // ~220 KB
 
@@ -43,52 +50,97 @@ constexpr size_t CQ_SMEM =
 // CTA-wide small dense helpers (all 512 threads call them), row-major KP x KP
 // ---------------------------------------------------------------------------
 
-// rsqrt(d) to full double precision (MUFU estimate + two Newton steps) -- one
-// long-latency op per sequential step instead of sqrt + two divisions
+// rsqrt(d) to full double precision: MUFU estimate (rsqrt.approx.f64, ~23
+// bits) + two Newton steps -- the Cholesky pivot chain's one long-latency op
 __device__ __forceinline__ double cq_rsqrt(double d) {
-  double y = rsqrt(d);
-  y = y * fma(-0.5 * d * y, y, 1.5);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  const double hd = 0.5 * d;
+  y = y * fma(-hd * y, y, 1.5);
+  y = y * fma(-hd * y, y, 1.5);
   return y;
 }
+
+// phase ticks of the small helpers (tools/micro/cq_small.cu defines them)
+#ifndef CQ_TICK
+#define CQ_TICK(i)
+#endif
 
 // upper Cholesky (A = R^T R) of the leading n x n of A (upper triangle read,
 // destroyed); R -> out (upper, zero below).  Returns the first j whose pivot
 // fails pivot > tol * orig[j] (or n); piv[j] receives the pivots.  On a failure
 // at j the leading j x j of R is complete.
-// Blocked by 8 (right-looking): warp 0 factors the diagonal block in registers
-// (lane c = column c, shuffles), then a triangular solve for the block row
-// (thread per column) and a rank-8 update of the trailing upper triangle.
+// Blocked by 8 (right-looking): warp 0 factors the 8-row block row (lane =
+// column, 3 columns per lane, shuffles for the block's pivot row), then all
+// warps apply the rank-8 update to the trailing upper triangle on DMMA.
 __device__ int cq_chol(double* A, double* out, double* piv, const double* orig, int n, double tol) {
   __shared__ int s_fail;
-  __shared__ double s_rs[DMQR_KP];
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
   for (int e = tid; e < DMQR_KP * DMQR_KP; e += blockDim.x) out[e] = 0.0;
   __syncthreads();
   for (int b0 = 0; b0 < n; b0 += 8) {
     const int bw = min(8, n - b0);
     if (tid < 32) {
-      double a[8];
+      // every lane: the 8 x 8 diagonal block (upper); lane: 2 columns right of it
+      double D[8][8], a[2][8];
+      // (unconditional loads from clamped in-bounds addresses, then select:
+      // predicated shared loads cost an address rebuild each)
+      const double* Ab = A + b0 * DMQR_KP + b0;
 #pragma unroll
-      for (int r = 0; r < 8; ++r) a[r] = (lane < bw && r <= lane) ? A[(b0 + r) * DMQR_KP + b0 + lane] : 0.0;
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = r; c < 8; ++c) {
+          const double v = Ab[r * DMQR_KP + c];
+          D[r][c] = (c < bw) ? v : 0.0;
+        }
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int c = b0 + 8 + lane + 32 * s;
+        const double* Ac = A + b0 * DMQR_KP + min(c, DMQR_KP - 1);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const double v = Ac[r * DMQR_KP];
+          a[s][r] = (c < n && r < bw) ? v : 0.0;
+        }
+      }
+      double thr[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) thr[j] = tol * orig[min(b0 + j, DMQR_KP - 1)];
+      // branch-free: after the first failing pivot the block is garbage but
+      // only the leading fail x fail of R is used
       int fail = n;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (j < bw && fail == n) {
-          const double d = __shfl_sync(0xffffffffu, a[j], j);
-          if (!(d > tol * orig[b0 + j] && d > 0.0)) {
-            fail = b0 + j;
-          } else {
+        if (j < bw) {
+          const double d = D[j][j];
+          if (fail == n && !(d > thr[j] && d > 0.0)) fail = b0 + j;
+          {
             const double rs = cq_rsqrt(d);
-            const double rjc = (lane == j) ? d * rs : a[j] * rs;  // R[j][lane]
-            if (lane >= j && lane < bw) out[(b0 + j) * DMQR_KP + b0 + lane] = rjc;
+            double rd[8];
+#pragma unroll
+            for (int c = j + 1; c < 8; ++c) rd[c] = D[j][c] * rs;  // R[b0+j][b0+c]
+#pragma unroll
+            for (int r = j + 1; r < 8; ++r)
+#pragma unroll
+              for (int c = r; c < 8; ++c) D[r][c] -= rd[r] * rd[c];
+            double x[2];
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              x[s] = a[s][j] * rs;
+#pragma unroll
+              for (int r = j + 1; r < 8; ++r) a[s][r] -= rd[r] * x[s];
+            }
             if (lane == 0) {
               piv[b0 + j] = d;
-              s_rs[b0 + j] = rs;
+              out[(b0 + j) * DMQR_KP + b0 + j] = d * rs;
+#pragma unroll
+              for (int c = j + 1; c < 8; ++c)
+                if (c < bw) out[(b0 + j) * DMQR_KP + b0 + c] = rd[c];
             }
 #pragma unroll
-            for (int r = j + 1; r < 8; ++r) {
-              const double rjr = __shfl_sync(0xffffffffu, rjc, r);
-              if (r <= lane) a[r] -= rjr * rjc;
+            for (int s = 0; s < 2; ++s) {
+              const int c = b0 + 8 + lane + 32 * s;
+              if (c < n) out[(b0 + j) * DMQR_KP + c] = x[s];
             }
           }
         }
@@ -96,37 +148,46 @@ __device__ int cq_chol(double* A, double* out, double* piv, const double* orig, 
       if (lane == 0) s_fail = fail;
     }
     __syncthreads();
+    CQ_TICK(0);
     if (s_fail < n) return s_fail;
-    const int c0 = b0 + bw;
-    // block row: R[b0+j][cc] = (A[b0+j][cc] - sum_{t<j} R[b0+t][b0+j] R[b0+t][cc]) / R_jj
-    for (int cc = c0 + tid; cc < n; cc += blockDim.x) {
-      double x[8];
+    // trailing upper triangle on DMMA: A[i][j] -= sum_t R[b0+t][i] R[b0+t][j]
+    // (upper 8 x 8 tiles, up to 3 per warp interleaved)
+    const int c0 = b0 + 8, nt = (n - c0 + 7) / 8;
+    const int ntiles = nt * (nt + 1) / 2;
+    if (wid < ntiles) {
+      const int lr = lane >> 2, lk = lane & 3;
+      int ri[3], cj[3];
+      double x[3][2];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        x[j] = 0.0;
-        if (j < bw) {
-          double s = A[(b0 + j) * DMQR_KP + cc];
-#pragma unroll
-          for (int t = 0; t < j; ++t) s -= out[(b0 + t) * DMQR_KP + b0 + j] * x[t];
-          x[j] = s * s_rs[b0 + j];
-          out[(b0 + j) * DMQR_KP + cc] = x[j];
+      for (int q = 0; q < 3; ++q) {
+        int t = wid + q * nw, ti = 0;
+        if (t >= ntiles) t = -1;
+        int rem = t < 0 ? 0 : t;
+        while (rem >= nt - ti) {
+          rem -= nt - ti;
+          ++ti;
         }
+        ri[q] = t < 0 ? -1 : c0 + ti * 8;
+        cj[q] = c0 + (ti + rem) * 8;
+        x[q][0] = x[q][1] = 0.0;
       }
-    }
-    __syncthreads();
-    // trailing upper triangle: A[i][j] -= sum_t R[b0+t][i] R[b0+t][j]
-    const int nt = n - c0;
-    for (int e = tid; e < nt * nt; e += blockDim.x) {
-      const int i = c0 + e / nt, j = c0 + e % nt;
-      if (j >= i) {
-        double s = 0.0;
 #pragma unroll
-        for (int t = 0; t < 8; ++t)
-          if (t < bw) s += out[(b0 + t) * DMQR_KP + i] * out[(b0 + t) * DMQR_KP + j];
-        A[i * DMQR_KP + j] -= s;
+      for (int k0 = 0; k0 < 8; k0 += 4) {
+        const int kr = (b0 + k0 + lk) * DMQR_KP;
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          if (ri[q] >= 0) dmma884(x[q][0], x[q][1], out[kr + ri[q] + lr], out[kr + cj[q] + lr]);
       }
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (ri[q] >= 0) {
+          const int r = ri[q] + lr, oc = cj[q] + 2 * lk;
+          if (r < n && oc < n) A[r * DMQR_KP + oc] -= x[q][0];
+          if (r < n && oc + 1 < n) A[r * DMQR_KP + oc + 1] -= x[q][1];
+        }
     }
     __syncthreads();
+    CQ_TICK(1);
   }
   return n;
 }
@@ -165,6 +226,7 @@ __device__ void cq_trinv_upper(const double* U, double* X, int n, int xr = DMQR_
     }
   }
   __syncthreads();
+  CQ_TICK(2);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int lr = lane >> 2, lk = lane & 3;
   double* w = wst[wid];
@@ -196,45 +258,79 @@ __device__ void cq_trinv_upper(const double* U, double* X, int n, int xr = DMQR_
     }
     __syncthreads();
   }
+  CQ_TICK(3);
+}
+
+// 1/x for x in [1, 2] (modified-LU pivots): MUFU estimate + two Newton steps
+__device__ __forceinline__ double cq_rcp12(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-x, y, 2.0);
+  y = y * fma(-x, y, 2.0);
+  return y;
 }
 
 // Modified LU (Ballard et al.) of the leading l x l of A (KP row-major), in
 // place: strict lower <- multipliers L_ij = -S_j q'_ij / (1 + |q'_jj|), upper
 // <- the eliminated q' (unsigned); S_j = -sign(q'_jj) -> vS, pivots -> vpiv.
-// Blocked by 8: warp 0 eliminates the 8-column panel over all rows (lane =
-// row, shuffles), then the block rows' columns to the right (thread per
-// column) and a rank-8 update of the trailing block.
+// Blocked by 8: warp 0 eliminates the 8-column block over all rows below
+// (lane = row, 3 rows per lane) and, in the same pass, the block's 8 rows over
+// the columns to its right (lane = column, 2 per lane); then all warps apply
+// the rank-8 update to the trailing block on DMMA.
 __device__ void cq_mlu(double* A, double* vS, double* vpiv, int l) {
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
   for (int b0 = 0; b0 < l; b0 += 8) {
     const int bw = min(8, l - b0);
+    const int c0 = b0 + 8;
     if (tid < 32) {
-      double v[3][8];
+      double v[3][8];  // rows b0 + lane + 32 s, block columns
+      double w[2][8];  // block rows, columns c0 + lane + 32 s
 #pragma unroll
       for (int s = 0; s < 3; ++s) {
         const int i = b0 + lane + 32 * s;
+        const double* Ai = A + min(i, DMQR_KP - 1) * DMQR_KP + b0;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) v[s][c] = (i < l && c < bw) ? A[i * DMQR_KP + b0 + c] : 0.0;
+        for (int c = 0; c < 8; ++c) {
+          const double x = Ai[c];
+          v[s][c] = (i < l && c < bw) ? x : 0.0;
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int c = c0 + lane + 32 * s;
+        const double* Ac = A + b0 * DMQR_KP + min(c, DMQR_KP - 1);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const double x = Ac[r * DMQR_KP];
+          w[s][r] = (c < l && r < bw) ? x : 0.0;
+        }
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         if (j < bw) {
           double qj[8];
 #pragma unroll
-          for (int c = 0; c < 8; ++c) qj[c] = __shfl_sync(0xffffffffu, v[0][c], j);
+          for (int c = j; c < 8; ++c) qj[c] = __shfl_sync(0xffffffffu, v[0][c], j);  // row b0+j
           const double qjj = qj[j];
           const double sg = (qjj >= 0.0) ? -1.0 : 1.0;  // S_j = -sign(q'_jj), sign(+0) = +
           const double pv = 1.0 - sg * qjj;             // pivot = 1 + |q'_jj|
-          const double f0 = -sg / pv;
+          const double f0 = -sg * cq_rcp12(pv);
 #pragma unroll
           for (int s = 0; s < 3; ++s) {
             const int i = b0 + lane + 32 * s;
-            if (i > b0 + j && i < l) {
+            if (i > b0 + j) {  // rows past l hold zeros and are never stored
               const double L = f0 * v[s][j];
 #pragma unroll
               for (int c = j + 1; c < 8; ++c) v[s][c] -= L * qj[c];
               v[s][j] = L;
             }
+          }
+          // block rows i > j, columns right of the block: q'_ic -= L_ij q'_jc
+#pragma unroll
+          for (int i = j + 1; i < 8; ++i) {
+            const double Lij = __shfl_sync(0xffffffffu, v[0][j], i);  // row b0+i lives on lane i
+#pragma unroll
+            for (int s = 0; s < 2; ++s) w[s][i] -= Lij * w[s][j];
           }
           if (lane == 0) {
             vS[b0 + j] = sg;
@@ -245,38 +341,59 @@ __device__ void cq_mlu(double* A, double* vS, double* vpiv, int l) {
 #pragma unroll
       for (int s = 0; s < 3; ++s) {
         const int i = b0 + lane + 32 * s;
+        if (i < l) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          if (i < l && c < bw) A[i * DMQR_KP + b0 + c] = v[s][c];
+          for (int c = 0; c < 8; ++c)
+            if (c < bw) A[i * DMQR_KP + b0 + c] = v[s][c];
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int c = c0 + lane + 32 * s;
+        if (c < l) {
+#pragma unroll
+          for (int r = 1; r < 8; ++r)
+            if (r < bw) A[(b0 + r) * DMQR_KP + c] = w[s][r];
+        }
       }
     }
     __syncthreads();
-    const int c0 = b0 + bw;
-    // block rows, columns >= c0: forward elimination with the block's multipliers
-    for (int cc = c0 + tid; cc < l; cc += blockDim.x) {
-      double x[8];
+    CQ_TICK(4);
+    // trailing block on DMMA: A[i][c] -= sum_j L[i][b0+j] q'[b0+j][c]
+    const int nt = (l - c0 + 7) / 8;
+    if (nt > 0) {
+      const int lr = lane >> 2, lk = lane & 3;
+      for (int t0 = wid; t0 < nt * nt; t0 += 4 * nw) {
+        int ti[4], tj[4];
+        double x[4][2];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] = (j < bw) ? A[(b0 + j) * DMQR_KP + cc] : 0.0;
+        for (int q = 0; q < 4; ++q) {
+          const int t = t0 + q * nw;
+          ti[q] = (t < nt * nt) ? t / nt : -1;
+          tj[q] = (t < nt * nt) ? t % nt : 0;
+          x[q][0] = x[q][1] = 0.0;
+        }
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
+        for (int k0 = 0; k0 < 8; k0 += 4) {
 #pragma unroll
-        for (int i = j + 1; i < 8; ++i)
-          if (i < bw) x[i] -= A[(b0 + i) * DMQR_KP + b0 + j] * x[j];
+          for (int q = 0; q < 4; ++q)
+            if (ti[q] >= 0) {
+              const int r = min(c0 + ti[q] * 8 + lr, DMQR_KP - 1), cc = min(c0 + tj[q] * 8 + lr, DMQR_KP - 1);
+              dmma884(x[q][0], x[q][1], A[r * DMQR_KP + b0 + k0 + lk], A[(b0 + k0 + lk) * DMQR_KP + cc]);
+            }
+        }
+        __syncwarp();
 #pragma unroll
-      for (int j = 1; j < 8; ++j)
-        if (j < bw) A[(b0 + j) * DMQR_KP + cc] = x[j];
+        for (int q = 0; q < 4; ++q)
+          if (ti[q] >= 0) {
+            const int r = c0 + ti[q] * 8 + lr, oc = c0 + tj[q] * 8 + 2 * lk;
+            if (r < l && oc < l) A[r * DMQR_KP + oc] -= x[q][0];
+            if (r < l && oc + 1 < l) A[r * DMQR_KP + oc + 1] -= x[q][1];
+          }
+      }
     }
     __syncthreads();
-    const int nt = l - c0;
-    for (int e = tid; e < nt * nt; e += blockDim.x) {
-      const int i = c0 + e / nt, cc = c0 + e % nt;
-      double s = 0.0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < bw) s += A[i * DMQR_KP + b0 + j] * A[(b0 + j) * DMQR_KP + cc];
-      A[i * DMQR_KP + cc] -= s;
-    }
-    __syncthreads();
+    CQ_TICK(5);
   }
 }
 
@@ -449,14 +566,15 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   for (int j = tid; j < k; j += PANEL_T) vpiv[DMQR_KP + j] = A1[j * DMQR_KP + j];
   __syncthreads();
   // ---- P3: R1 = chol(G) -> A2 ----
-  const int jstar = cq_chol(A1, A2, vpiv, vpiv + DMQR_KP, k, 1e-10);
+  const int jstar = cq_chol(A1, A2, vpiv, vpiv + DMQR_KP, k, CQ_PIVOT_TOL);
   CQT();
   // accepted pass-1 prefix kk = jstar; decide early whether an unhealthy pivot proves a break
   int kk = jstar;
   bool fail = false;
   if (jstar < k) {
-    // pivot d ~ R_jj^2 with absolute error ~eps*G_jj: R_jj <= 1e-5 ||a_j|| + noise
-    const double bound = 1e-4 * sqrt(vpiv[DMQR_KP + jstar]);
+    // pivot d ~ R_jj^2 <= CQ_PIVOT_TOL G_jj (+ rounding ~n eps max_j G_jj):
+    // R_jj <= 3.2e-4 ||a_j|| + noise; break iff R_jj < eps_s
+    const double bound = 1e-3 * sqrt(vpiv[DMQR_KP + jstar]);
     if (!brk || jstar == 0 || !(bound < eps_s)) fail = true;
   }
   if (!fail && kk > 0) {
@@ -490,13 +608,14 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       const int i = e / kk, j = e % kk;
       if (j >= i) {
         const double g = A2[i * DMQR_KP + j] - (i == j ? 1.0 : 0.0);
-        if (!(fabs(g) < 1e-2)) s_flag[0] = 1;
+        if (!(fabs(g) < CQ_ORTH_TOL)) s_flag[0] = 1;
       }
     }
     for (int j = tid; j < kk; j += PANEL_T) vpiv[DMQR_KP + j] = A2[j * DMQR_KP + j];
     __syncthreads();
     if (s_flag[0]) fail = true;
   }
+  if (me == 0 && tid == 0) c->cq_diag[3] = jstar;
   int l = kk;
   if (!fail && kk > 0) {
     // ---- P8: R2 = chol(G2) -> A1 (reads/destroys the upper of A2) ----

@@ -40,6 +40,8 @@ def main():
     h = rows[hdr]
     ia, isamp = h.index("Address"), h.index("Warp Stall Sampling (All Samples)")
     agg = defaultdict(int)
+    reasons = defaultdict(lambda: defaultdict(int))
+    rcols = [(i, k[6:]) for i, k in enumerate(h) if k.startswith("stall_") and "Not Issued" not in k]
     tot = 0
     base = None
     for r in rows[hdr + 1:]:
@@ -55,9 +57,15 @@ def main():
         key = amap.get(addr - base, ("?", 0))
         agg[key] += s
         tot += s
+        for i, k in rcols:
+            try:
+                reasons[key][k] += int(r[i] or 0)
+            except ValueError:
+                pass
     print("total samples", tot, "mapped lines", len(agg))
     for k, v in sorted(agg.items(), key=lambda kv: -kv[1])[:top]:
-        print(f"{v:7d} {100 * v / max(tot, 1):5.1f}%  {k[0]}:{k[1]}")
+        top3 = sorted(reasons[k].items(), key=lambda kv: -kv[1])[:3]
+        print(f"{v:7d} {100 * v / max(tot, 1):5.1f}%  {k[0]}:{k[1]}  " + " ".join(f"{a}={b}" for a, b in top3 if b))
 
 
 if __name__ == "__main__":
