@@ -297,7 +297,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     PROF(0);
     k_select<<<1, SEL_T, 0, st>>>(ctl, u);
     NOTE_LAUNCH();
-    const int GG = (int)std::clamp<int64_t>(ceil_div(mp, 2 * GRAM_ROWS), 1, std::min(GRAM_GMAX, d.sms));
+    const int GG = (int)std::clamp<int64_t>(ceil_div(mp, GRAM_ROWS), 1, std::min(GRAM_GMAX, d.sms));
     k_gram<<<GG, GRAM_T, GRAM_SMEM, st>>>(ctl, A, gpart);
     NOTE_LAUNCH();
     k_gram_finish<<<45, GRAM_T, sizeof(FinSmem), st>>>(ctl, A, gpart, GG, gfin);

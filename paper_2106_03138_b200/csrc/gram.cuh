@@ -159,15 +159,21 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, const doub
   const int64_t r_begin = (int64_t)blockIdx.x * rpc;
   const int64_t r_end = min(mp, r_begin + rpc);
 
+  // tiles wid, wid + 8, ... (<= 6 per warp); static indexing keeps the
+  // accumulators in registers
   double acc[6][2];
   int tij[6];
   int my_tiles = 0;
-  for (int t = wid, q = 0; t < ntiles; t += GRAM_T / 32, ++q) {
-    int ti, tj;
-    tile_ij(t, nt, ti, tj);
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const int t = wid + q * (GRAM_T / 32);
+    int ti = 0, tj = 0;
+    if (t < ntiles) {
+      tile_ij(t, nt, ti, tj);
+      my_tiles = q + 1;
+    }
     tij[q] = ti * 16 + tj;
     acc[q][0] = acc[q][1] = 0.0;
-    my_tiles = q + 1;
   }
   __syncthreads();
   const int nslab = (r_end > r_begin) ? (int)ceil_div(r_end - r_begin, GRAM_ROWS) : 0;
@@ -198,21 +204,25 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, const doub
 #pragma unroll 4
     for (int ks = 0; ks < GRAM_ROWS / 4; ++ks) {
       const int kr = 4 * ks + (lane & 3);
-      for (int q = 0; q < my_tiles; ++q) {
-        const double av = buf[((tij[q] >> 4) * 8 + (lane >> 2)) * GRAM_LD + kr];
-        const double bv = buf[((tij[q] & 15) * 8 + (lane >> 2)) * GRAM_LD + kr];
-        dmma884(acc[q][0], acc[q][1], av, bv);
-      }
+#pragma unroll
+      for (int q = 0; q < 6; ++q)
+        if (q < my_tiles) {
+          const double av = buf[((tij[q] >> 4) * 8 + (lane >> 2)) * GRAM_LD + kr];
+          const double bv = buf[((tij[q] & 15) * 8 + (lane >> 2)) * GRAM_LD + kr];
+          dmma884(acc[q][0], acc[q][1], av, bv);
+        }
     }
     __syncthreads();
   }
   double* my = part + (int64_t)blockIdx.x * GRAM_PART;
-  for (int q = 0; q < my_tiles; ++q) {
-    const int row = (tij[q] >> 4) * 8 + (lane >> 2);
-    const int col = (tij[q] & 15) * 8 + 2 * (lane & 3);
-    my[row * DMQR_KP + col] = acc[q][0];
-    my[row * DMQR_KP + col + 1] = acc[q][1];
-  }
+#pragma unroll
+  for (int q = 0; q < 6; ++q)
+    if (q < my_tiles) {
+      const int row = (tij[q] >> 4) * 8 + (lane >> 2);
+      const int col = (tij[q] & 15) * 8 + 2 * (lane & 3);
+      my[row * DMQR_KP + col] = acc[q][0];
+      my[row * DMQR_KP + col + 1] = acc[q][1];
+    }
 }
 
 struct FinSmem {
@@ -221,7 +231,8 @@ struct FinSmem {
   double rowsum[DMQR_KP];
   double amax[DMQR_KP];
   int chosen[DMQR_KP];
-  int is_last, bad, zero;
+  unsigned long long conf[DMQR_KP];
+  int is_last, bad, zero, nch;
   PlanSmem plan;
 };
 
@@ -244,8 +255,17 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
     // 64 entries x 4 threads, each summing a quarter of the partials; fixed combine order
     const int e = tid >> 2, g4 = tid & 3;
     const int i = ti * 8 + (e >> 3), j = tj * 8 + (e & 7);
-    double s = 0.0;
-    for (int b = g4; b < G; b += 4) s += __ldcg(part + (int64_t)b * GRAM_PART + i * DMQR_KP + j);
+    // 8 independent loads in flight per thread; the combine order is fixed by G
+    const double* pp = part + i * DMQR_KP + j;
+    double sv[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int b0 = g4; b0 < G; b0 += 32) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int b = b0 + 4 * q;
+        if (b < G) sv[q] += __ldcg(pp + (int64_t)b * GRAM_PART);
+      }
+    }
+    double s = ((sv[0] + sv[1]) + (sv[2] + sv[3])) + ((sv[4] + sv[5]) + (sv[6] + sv[7]));
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     if (g4 == 0) gfin[i * DMQR_KP + j] = s;
@@ -264,6 +284,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
     sm.bad = 0;
     sm.zero = 0;
   }
+#pragma unroll 4
   for (int e = tid; e < ncand * ncand; e += GRAM_T) {
     const int i = e / ncand, j = e % ncand;
     if (j >= i) sm.g[i * DMQR_KP + j] = __ldcg(gfin + i * DMQR_KP + j);
@@ -321,9 +342,57 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
     sm.g[i * DMQR_KP + j] = __dmul_rn(__dmul_rn(sm.g[i * DMQR_KP + j], sm.inv[i]), sm.inv[j]);
   }
   __syncthreads();
-  if (wid != 0) return;
-  // ---- greedy filter, one warp (dm.py:151-173) ----
   const bool dmax = c->use_delta_max != 0;
+  if (!dmax) {
+    // ---- greedy filter (dm.py:151-173) via conflict masks: bit q of conf[t] is
+    // set when candidate q < t fails |theta_qt| < delta; then t is accepted iff
+    // no accepted q conflicts -- one 64-step bit loop on one thread ----
+    const double delta = c->delta;
+    for (int t = wid + 1; t < ncand; t += GRAM_T / 32) {
+      const double a0 = (lane < t) ? fabs(sm.g[lane * DMQR_KP + t]) : 0.0;
+      const double a1 = (lane + 32 < t) ? fabs(sm.g[(lane + 32) * DMQR_KP + t]) : 0.0;
+      const unsigned lo = __ballot_sync(0xffffffffu, lane < t && !(a0 < delta));
+      const unsigned hi = __ballot_sync(0xffffffffu, lane + 32 < t && !(a1 < delta));
+      if (lane == 0) sm.conf[t] = ((unsigned long long)hi << 32) | lo;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long acc = 1ull;
+      int nch = 1;
+      sm.chosen[0] = 0;
+      for (int t = 1; t < ncand; ++t)
+        if (!(sm.conf[t] & acc)) {
+          acc |= 1ull << t;
+          sm.chosen[nch++] = t;
+        }
+      sm.nch = nch;
+    }
+    __syncthreads();
+    const int nch = sm.nch;
+    // gamma = min_i 1 - (sum_j |theta_ij| - 1) over the chosen submatrix (dm.py:175-176)
+    for (int p = wid; p < nch; p += GRAM_T / 32) {
+      const int i = sm.chosen[p];
+      double sacc = 0.0;
+      for (int q = lane; q < nch; q += 32) {
+        const int jj = sm.chosen[q];
+        sacc += (i == jj) ? 1.0 : fabs(i < jj ? sm.g[i * DMQR_KP + jj] : sm.g[jj * DMQR_KP + i]);
+      }
+      sacc = warp_sum(sacc);
+      if (lane == 0) sm.rowsum[p] = 1.0 - (sacc - 1.0);
+    }
+    __syncthreads();
+    if (wid != 0) return;
+    double gmin = 1e300;
+    for (int p = lane; p < nch; p += 32) gmin = fmin(gmin, sm.rowsum[p]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gmin = fmin(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
+    for (int q = lane; q < nch; q += 32) c->sel[q] = c->cand[sm.chosen[q]];
+    __syncwarp();
+    plan_swaps_warp(c, nch, gmin, sm.plan);
+    return;
+  }
+  if (wid != 0) return;
+  // ---- greedy filter with the delta_max guard, one warp (dm.py:151-173) ----
   const double tau2 = c->tau * c->tau;
   const double delta = dmax ? tau2 / (double)max(c->k_max - 1, 1) : c->delta;
   const double guard = tau2;

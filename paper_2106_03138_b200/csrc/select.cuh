@@ -180,15 +180,28 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const dou
       }
     nlist = total;
   } else {
-    // radix select of the k_dm-th largest key among candidates
+    // radix select of the k_dm-th largest key among candidates.  Every
+    // candidate key lies in [key(thr), key(umax)], so the digits above their
+    // highest differing bit are common and need no histogram; and once the
+    // bucket holding the k-th key is taken whole the select is done (the keys
+    // matching the prefix under `mask` are then all selected).
+    const unsigned long long khi = (unsigned long long)__double_as_longlong(umax);
+    const unsigned long long klo = (unsigned long long)__double_as_longlong(thr);
+    const int hb = (khi == klo) ? 0 : 63 - __clzll(khi ^ klo);
     unsigned long long prefix = 0ull, mask = 0ull;
     int k = k_dm;
     for (int pass = 0; pass < 8; ++pass) {
       const int shift = 56 - 8 * pass;
+      if (shift > hb) {  // common digit
+        prefix |= khi & (255ull << shift);
+        mask |= 255ull << shift;
+        continue;
+      }
       for (int b = tid; b < 256; b += SEL_T) sm.hist[b] = 0u;
       __syncthreads();
       // warp-aggregated histogram: norms cluster in few bins, so plain shared
       // atomics would serialize; one atomic per distinct digit per warp step.
+#pragma unroll 4
       for (int it = 0; it < seg; ++it) {
         const int i = s0 + it;
         unsigned dig = 0xffffffffu;
@@ -234,22 +247,25 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const dou
           }
           sm.bc_i[1] = digit;
           sm.bc_i[2] = k - (int)run;
+          sm.bc_i[3] = (k - (int)run == (int)sm.hist[digit]);  // bucket taken whole
         }
       }
       __syncthreads();
       prefix |= (unsigned long long)sm.bc_i[1] << shift;
       mask |= 255ull << shift;
       k = sm.bc_i[2];
+      const bool whole = sm.bc_i[3] != 0;
       __syncthreads();
+      if (whole) break;
     }
     const unsigned long long T = prefix;
-    const int k_rem = k;  // elements equal to T to take, smallest index first
+    const int k_rem = k;  // keys matching T under mask to take, smallest index first
     // greater-than count and equal count per thread (index order)
     int gt = 0, eq = 0;
     for (int i = s0; i < s1; ++i) {
       double v = u[i];
       if (i == seed || !(v >= thr)) continue;
-      unsigned long long key = (unsigned long long)__double_as_longlong(v);
+      unsigned long long key = (unsigned long long)__double_as_longlong(v) & mask;
       gt += key > T;
       eq += key == T;
     }
@@ -262,7 +278,7 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const dou
     for (int i = s0; i < s1; ++i) {
       double v = u[i];
       if (i == seed || !(v >= thr)) continue;
-      unsigned long long key = (unsigned long long)__double_as_longlong(v);
+      unsigned long long key = (unsigned long long)__double_as_longlong(v) & mask;
       if (key > T) {
         sm.list_i[pg] = i;
         sm.list_u[pg] = v;
