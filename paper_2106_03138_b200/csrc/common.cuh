@@ -43,6 +43,12 @@ struct Ctl {
   int32_t cq_fail;  // 1: the CholeskyQR2 panel declined, the Householder panel must run
   int32_t tc0;      // first column of the trailing update (n_s + k_s, or n_s + l after a CholQR break)
   double cq_diag[4];  // debug: CholQR2 health of the last panel (min pivot ratio 1, |G2 - I|, min pivot ratio 2, jstar)
+  // look-ahead (la): step k's C -= Y Wt on the rows below its R is still
+  // pending (pend) for every trailing column not flagged in the per-column
+  // `upd` bytes; snapshot of that step (its n_s and accepted reflectors)
+  int32_t la, pend, pend_ns, pend_l;
+  int32_t gcount;   // guard columns of the current step (norm recompute list)
+  int32_t pad2;
   // inter-CTA counters (reset by their users)
   uint32_t gram_count;
   uint32_t bar_count;

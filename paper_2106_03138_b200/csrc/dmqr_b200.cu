@@ -39,7 +39,7 @@ constexpr int NSPLIT_MAX = 16;
 constexpr int PANEL_PMAX = 160;
 
 struct Layout {
-  size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, swp, trace, pdbg, tcount, total;
+  size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, swp, trace, pdbg, tcount, upd, lacount, total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -65,10 +65,12 @@ Layout layout(int64_t m, int64_t n) {
   L.gfin = take(sizeof(double) * DMQR_KP * DMQR_KP);
   L.Zp = take(sizeof(double) * NSPLIT_MAX * DMQR_KP * ldz_for(n));
   L.Z = take(sizeof(double) * DMQR_KP * ldz_for(n));
-  L.swp = take(sizeof(double) * 2 * DMQR_KP * std::max<int64_t>(m, 1));
+  L.swp = take(sizeof(double) * 2 * DMQR_KP * (std::max<int64_t>(m, 1) + DMQR_KP));
   L.trace = take(sizeof(unsigned long long) * 4);
   L.pdbg = take(sizeof(long long) * 64 * 16);
   L.tcount = take(sizeof(unsigned) * (ceil_div(std::max<int64_t>(n, 1), TA_COLS) + 1));
+  L.upd = take(std::max<int64_t>(n, 1));                      // look-ahead column flags
+  L.lacount = take(sizeof(unsigned) * 4);                     // look-ahead last-CTA counters
   L.total = off;
   return L;
 }
@@ -116,7 +118,8 @@ int set_attrs(const DevInfo& d) {
   CK(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GRAM_SMEM));
   CK(cudaFuncSetAttribute(k_trail_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA_SMEM));
   CK(cudaFuncSetAttribute(k_gram_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FinSmem)));
-  CK(cudaFuncSetAttribute(k_trail_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
+  CK(cudaFuncSetAttribute(k_trail_b<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
+  CK(cudaFuncSetAttribute(k_trail_b<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
   CK(cudaFuncSetAttribute(k_trail_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TP_SMEM));
   CK(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)std::min<size_t>(d.smem_optin - 4096, 220 * 1024)));
@@ -235,7 +238,15 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   unsigned long long* tbits = (unsigned long long*)(ws + L.trace);
   long long* pdbg = (long long*)(ws + L.pdbg);
   unsigned* tcount = (unsigned*)(ws + L.tcount);
+  uint8_t* upd = (uint8_t*)(ws + L.upd);
+  unsigned* lacount = (unsigned*)(ws + L.lacount);
   StepRec* srec = (StepRec*)steps;
+  // Look-ahead (default; not with the per-step norm trace, which needs fully
+  // updated columns at every step end): step k's C -= Y Wt below its R rows
+  // runs beside step k+1's panel (programmatic dependent launch); step k+1's
+  // candidates get it first (in k_gram).
+  const bool la = !p->trace_norms && getenv("DMQR_NO_LOOKAHEAD") == nullptr && m > 0 && n > 0;
+
 
   const int64_t kmax = std::min(m, n);
   double eps1 = -1.0;
@@ -247,6 +258,8 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   int32_t* nonfinite = (int32_t*)(tbits + 2);
   CK(cudaMemsetAsync(T, 0, sizeof(double) * DMQR_KP * DMQR_KP, st));
   CK(cudaMemsetAsync(tcount, 0, sizeof(unsigned) * (ceil_div(std::max<int64_t>(n, 1), TA_COLS) + 1), st));
+  CK(cudaMemsetAsync(upd, 0, (size_t)std::max<int64_t>(n, 1), st));
+  CK(cudaMemsetAsync(lacount, 0, sizeof(unsigned) * 4, st));
   if (n > 0) {
     if (m > 0) {
       int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)d.sms * 16);
@@ -258,7 +271,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     }
   }
   InitArgs ia{ctl, u, perm, coeffs, m, n, lda, kmax, p->tau, p->delta, eps1, p->k_dm, p->use_delta_max,
-              p->break_check, p->trace_norms, swap_cap, step_cap, nonfinite};
+              p->break_check, p->trace_norms, swap_cap, step_cap, nonfinite, la ? 1 : 0};
   k_init<<<1, 1024, 0, st>>>(ia);
   NOTE_LAUNCH();
   CK(cudaGetLastError());
@@ -290,6 +303,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   const bool trail_persistent = getenv("DMQR_TRAIL_PERSISTENT") != nullptr;  // A/B switch
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
 
+  int64_t prev_ns_lo = 0;  // the lower bound the previous step was sized with
   auto enqueue_step = [&](int64_t host_ns) -> int {
     const int64_t mp = m - host_ns;
     const int64_t np = n - host_ns;
@@ -297,18 +311,38 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     PROF(0);
     k_select<<<1, SEL_T, 0, st>>>(ctl, u);
     NOTE_LAUNCH();
+    const int64_t ldz = ldz_for(n);
     const int GG = (int)std::clamp<int64_t>(ceil_div(mp, GRAM_ROWS), 1, std::min(GRAM_GMAX, d.sms));
-    k_gram<<<GG, GRAM_T, GRAM_SMEM, st>>>(ctl, A, gpart);
+    k_gram<<<GG, GRAM_T, GRAM_SMEM, st>>>(ctl, A, gpart, Z, ldz, upd);
     NOTE_LAUNCH();
-    k_gram_finish<<<45, GRAM_T, sizeof(FinSmem), st>>>(ctl, A, gpart, GG, gfin);
+    k_gram_finish<<<45, GRAM_T, sizeof(FinSmem), st>>>(ctl, A, gpart, GG, gfin, upd);
     NOTE_LAUNCH();
     {
-      const dim3 gs((unsigned)ceil_div(m, 256), (unsigned)ceil_div(2 * DMQR_KP, SWAP_MG));
-      k_swap_gather<<<gs, 256, 0, st>>>(ctl, A, swp);
+      const dim3 gs((unsigned)ceil_div(m + (la ? DMQR_KP : 0), 256), (unsigned)ceil_div(2 * DMQR_KP, SWAP_MG));
+      k_swap_gather<<<gs, 256, 0, st>>>(ctl, A, swp, Z, ldz);
       NOTE_LAUNCH();
-      k_swap_scatter<<<gs, 256, 0, st>>>(ctl, A, u, uref, perm, swaps, swp);
+      k_swap_scatter<<<gs, 256, 0, st>>>(ctl, A, u, uref, perm, swaps, swp, Z, ldz, upd);
       NOTE_LAUNCH();
     }
+    // the rest of the previous step's update: beside the CholeskyQR2 panel as
+    // its programmatic dependent, else (other panel kernels) before the panel
+    const dim3 lag((unsigned)ceil_div(m - prev_ns_lo + 1, TB_ROWS),
+                   (unsigned)std::max<int64_t>(1, ceil_div(n - host_ns, TB_COLS)));
+    auto launch_la_rest = [&](bool pdl) -> cudaError_t {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = lag;
+      cfg.blockDim = dim3(TB_T);
+      cfg.dynamicSmemBytes = TB_SMEM;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = pdl ? 1 : 0;
+      NOTE_LAUNCH();
+      return cudaLaunchKernelEx(&cfg, k_trail_b<true>, ctl, A, (const double*)Z, ldz, upd, lacount + 1);
+    };
+    const bool la_rest = la && host_ns > 0;
     // ---- panel ----
     const int kcap = (int)std::min<int64_t>({(int64_t)p->k_dm + 1, (int64_t)DMQR_MAXK, kmax - host_ns});
     // row CTAs (+1 T-builder CTA when the panel spans several CTAs); the T
@@ -357,10 +391,12 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     // CholeskyQR2 panel (one cluster, <= 256 rows per CTA) first; the Householder
     // kernels behind it run only if it declined (ill-conditioned panel)
     const bool cq_path = use_cq && Prr <= max_cluster;
+    if (la_rest && !cq_path) CK(launch_la_rest(false));
     if (cq_path) {
       CK(launch_cluster((const void*)k_panel_cq, Prr, PANEL_T, CQ_SMEM));
       NOTE_LAUNCH();
       pa.only_if_fail = 1;
+      if (la_rest) CK(launch_la_rest(true));
     }
     if (cl_path) {
       CK(launch_cluster((const void*)k_panel_rr<ClusterRed>, G, PANEL_T, RR_CL_SMEM));
@@ -383,27 +419,32 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
       const int64_t ntile = ceil_div(ncols_ub, TA_COLS);
       int nsplit = (int)std::clamp<int64_t>(ceil_div(2 * d.sms, ntile), 1, NSPLIT_MAX);
       nsplit = (int)std::min<int64_t>(nsplit, std::max<int64_t>(1, ceil_div(mp, 256)));
-      const int64_t ldz = ldz_for(n);
-      k_trail_a<<<dim3((unsigned)ntile, nsplit), TA_T, TA_SMEM, st>>>(ctl, A, Zp, T, Z, tcount, ldz);
+      k_trail_a<<<dim3((unsigned)ntile, nsplit), TA_T, TA_SMEM, st>>>(ctl, A, Zp, T, Z, tcount, ldz, u, uref,
+                                                                          upd);
       NOTE_LAUNCH();
-      if (!trail_persistent) {
-        k_trail_b<<<dim3((unsigned)ceil_div(mp + 1, TB_ROWS), (unsigned)ceil_div(ncols_ub, TB_COLS)), TB_T, TB_SMEM,
-                    st>>>(ctl, A, Z, ldz);
+      if (la) {
+        // the rest of C -= Y Wt runs beside the next step's panel
+      } else if (!trail_persistent) {
+        k_trail_b<false><<<dim3((unsigned)ceil_div(mp + 1, TB_ROWS), (unsigned)ceil_div(ncols_ub, TB_COLS)), TB_T,
+                           TB_SMEM, st>>>(ctl, A, Z, ldz, upd, lacount + 1);
+        NOTE_LAUNCH();
       } else {
         const int64_t work = ceil_div(mp + 1, TP_ROWS) * ceil_div(ncols_ub, TP_COLS);
         k_trail_bp<<<(unsigned)std::min<int64_t>(work, d.sms), TP_T, TP_SMEM, st>>>(ctl, A, Z, ldz);
+        NOTE_LAUNCH();
       }
-      NOTE_LAUNCH();
     }
     // ---- norms, log ----
     PROF(3);
-    if (np > 0) {
+    if (la) {
+      // norms: downdated in k_trail_a's epilogue (guard columns recomputed there)
+    } else if (np > 0) {
       const int64_t blocks = std::min<int64_t>(ceil_div(np * 32, 256), (int64_t)d.sms * 16);
       k_downdate<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, uref);
       NOTE_LAUNCH();
       if (p->trace_norms) { k_norm_trace<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, tbits); NOTE_LAUNCH(); }
     }
-    k_step_end<<<1, 32, 0, st>>>(ctl, srec, norm_trace, tbits);
+    k_step_end<<<1, 32, 0, st>>>(ctl, srec, norm_trace, tbits, A, Z, ldz, u, uref, upd);
     NOTE_LAUNCH();
     PROF(4);
     CK(cudaGetLastError());
@@ -448,9 +489,17 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     slot = enq & 1;
     int rc = enqueue_step(ns_lo);
     if (rc) return rc;
+    prev_ns_lo = ns_lo;
     ++enq;
     ++steps_done;
     if (p->max_steps > 0 && steps_done >= p->max_steps) break;  // debug: stop after N steps
+  }
+  if (la && enq > 0) {  // the last step's pending update
+    const int64_t ldz = ldz_for(n);
+    k_trail_b<true><<<dim3((unsigned)ceil_div(m - prev_ns_lo + 1, TB_ROWS),
+                           (unsigned)std::max<int64_t>(1, ceil_div(n - prev_ns_lo, TB_COLS))),
+                      TB_T, TB_SMEM, st>>>(ctl, A, Z, ldz, upd, lacount + 1);
+    NOTE_LAUNCH();
   }
   while (known < enq) {  // drain (profiling reads; the steps themselves are ordered on st)
     int rc = consume();

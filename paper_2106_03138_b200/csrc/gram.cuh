@@ -19,7 +19,8 @@ constexpr int GRAM_T = 256;
 constexpr int GRAM_ROWS = 64;  // slab height
 constexpr int GRAM_LD = 68;    // 64 rows + 4: conflict-free fragment loads (ld = 4 mod 16)
 constexpr int GRAM_PART = DMQR_KP * DMQR_KP;
-constexpr size_t GRAM_SMEM = sizeof(double) * 2 * DMQR_KP * GRAM_LD;
+// [2][KP][LD] candidate slabs, [2][KP][LD] pending-panel Y slabs, [KP][KP] Wt of the candidates
+constexpr size_t GRAM_SMEM = sizeof(double) * (4 * DMQR_KP * GRAM_LD + DMQR_KP * DMQR_KP);
 
 // Selection finalize, one warp, shared-memory scratch (rrqr.py:294-312, 355-357).
 // c->sel[0..nsel) holds the selected absolute columns (seed first).  Writes
@@ -132,28 +133,52 @@ __device__ __forceinline__ void tile_ij(int t, int nt, int& ti, int& tj) {
   tj = ti + t;
 }
 
-__global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, const double* __restrict__ A,
-                                                 double* __restrict__ part) {
-  if (c->done || c->kind != 0) return;
-  const int ncand = c->ncand;
-  if (ncand == 1) {  // no candidates: J = [seed], gamma = 1 (dm.py:145-146)
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
-      __shared__ PlanSmem ps1;
-      if (threadIdx.x == 0) c->sel[0] = c->cand[0];
-      __syncwarp();
-      plan_swaps_warp(c, 1, 1.0, ps1);
-    }
-    return;
+// Look-ahead (Ctl::pend): the candidate columns still lack the previous
+// step's C -= Y Wt below its R rows.  Each slab is brought up to date in
+// shared memory (the same DMMA sequence per element as k_trail_b, so the
+// values are bitwise the serial update's), written back, and only then enters
+// the Gram; k_gram_finish flags the candidates (upd) once every CTA is done.
+// A scalar-fallback step (kind 1) runs the same update on its single column.
+__global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __restrict__ A,
+                                                 double* __restrict__ part, const double* __restrict__ Wt,
+                                                 int64_t ldz, const uint8_t* __restrict__ upd) {
+  if (c->done) return;
+  const bool pendu = c->la && c->pend;
+  if (c->kind != 0 && !pendu) return;
+  const int ncand = (c->kind == 0) ? c->ncand : 1;
+  if (ncand == 1 && c->kind == 0 && blockIdx.x == 0 && threadIdx.x < 32) {
+    // no candidates: J = [seed], gamma = 1 (dm.py:145-146)
+    __shared__ PlanSmem ps1;
+    if (threadIdx.x == 0) c->sel[0] = c->cand[0];
+    __syncwarp();
+    plan_swaps_warp(c, 1, 1.0, ps1);
   }
-  extern __shared__ __align__(16) double gsm[];  // [2][KP][GRAM_LD]
+  if (ncand == 1 && !pendu) return;
+  const bool gram = c->kind == 0 && ncand > 1;
+  extern __shared__ __align__(16) double gsm[];  // [2][KP][GRAM_LD] slabs, [2][KP][GRAM_LD] Y, [KP][KP] Wt
   __shared__ int s_cand[DMQR_KP];
+  __shared__ int s_live[DMQR_KP];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t n_s = c->n_s, m = c->m, lda = c->lda;
   const int64_t mp = m - n_s;
   const int np8 = round_up(ncand, 8);
   const int nt = np8 / 8;
-  const int ntiles = nt * (nt + 1) / 2;
-  for (int q = tid; q < DMQR_KP; q += GRAM_T) s_cand[q] = (q < ncand) ? c->cand[q] : 0;
+  const int ntiles = gram ? nt * (nt + 1) / 2 : 0;
+  const int pl = pendu ? c->pend_l : 0;
+  const int64_t pns = pendu ? c->pend_ns : 0;
+  const int plp4 = (pl + 3) / 4 * 4;
+  double* ysl = gsm + 2 * DMQR_KP * GRAM_LD;
+  double* wsm = gsm + 4 * DMQR_KP * GRAM_LD;
+  for (int q = tid; q < DMQR_KP; q += GRAM_T) {
+    s_cand[q] = (q < ncand) ? c->cand[q] : 0;
+    s_live[q] = (q < ncand) && pendu && !upd[c->cand[q]];
+  }
+  __syncthreads();
+  if (pendu)  // Wt columns of the candidates (indexed from n_s = pending n_s + l)
+    for (int e = tid; e < plp4 * DMQR_KP; e += GRAM_T) {
+      const int t = e / DMQR_KP, q = e % DMQR_KP;
+      wsm[t * DMQR_KP + q] = (t < pl && s_live[q]) ? Wt[t * ldz + (s_cand[q] - n_s)] : 0.0;
+    }
 
   const int64_t rpc = ceil_div(ceil_div(mp, (int64_t)gridDim.x), GRAM_ROWS) * GRAM_ROWS;
   const int64_t r_begin = (int64_t)blockIdx.x * rpc;
@@ -179,6 +204,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, const doub
   const int nslab = (r_end > r_begin) ? (int)ceil_div(r_end - r_begin, GRAM_ROWS) : 0;
   auto issue = [&](int sl) {
     double* buf = gsm + (sl & 1) * DMQR_KP * GRAM_LD;
+    double* ys = ysl + (sl & 1) * DMQR_KP * GRAM_LD;
     const int64_t r0 = r_begin + (int64_t)sl * GRAM_ROWS;
     for (int e = tid; e < np8 * GRAM_ROWS; e += GRAM_T) {
       const int col = e / GRAM_ROWS, row = e % GRAM_ROWS;
@@ -186,6 +212,16 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, const doub
       double* dst = buf + col * GRAM_LD + row;
       if (col < ncand && r < r_end)
         cp_async8(dst, A + (n_s + r) + (int64_t)s_cand[col] * lda);
+      else
+        *dst = 0.0;
+    }
+    // Y of the pending panel on these rows (all strictly below its diagonal)
+    for (int e = tid; e < plp4 * GRAM_ROWS; e += GRAM_T) {
+      const int t = e / GRAM_ROWS, row = e % GRAM_ROWS;
+      const int64_t r = r0 + row;
+      double* dst = ys + t * GRAM_LD + row;
+      if (t < pl && r < r_end)
+        cp_async8(dst, A + (n_s + r) + (pns + t) * lda);
       else
         *dst = 0.0;
     }
@@ -200,7 +236,39 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, const doub
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double* buf = gsm + (sl & 1) * DMQR_KP * GRAM_LD;
+    double* buf = gsm + (sl & 1) * DMQR_KP * GRAM_LD;
+    if (pendu) {
+      // buf[col][row] += (-Y) Wt for live candidates: warp w owns rows 8w..8w+7
+      const double* ys = ysl + (sl & 1) * DMQR_KP * GRAM_LD;
+      const int rr = wid * 8 + (lane >> 2);
+      const int64_t r0 = r_begin + (int64_t)sl * GRAM_ROWS;
+      for (int q0 = 0; q0 < nt; q0 += 3) {
+        double u3[3][2];
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) u3[q][h] = (q0 + q < nt) ? buf[((q0 + q) * 8 + 2 * (lane & 3) + h) * GRAM_LD + rr] : 0.0;
+        for (int ks = 0; ks < plp4; ks += 4) {
+          const int t = ks + (lane & 3);
+          const double a = -ys[t * GRAM_LD + rr];
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            if (q0 + q < nt) dmma884(u3[q][0], u3[q][1], a, wsm[t * DMQR_KP + (q0 + q) * 8 + (lane >> 2)]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = (q0 + q) * 8 + 2 * (lane & 3) + h;
+            if (q0 + q < nt && col < ncand && s_live[col]) {
+              buf[col * GRAM_LD + rr] = u3[q][h];
+              if (r0 + rr < r_end) A[(n_s + r0 + rr) + (int64_t)s_cand[col] * lda] = u3[q][h];
+            }
+          }
+      }
+      __syncthreads();
+    }
 #pragma unroll 4
     for (int ks = 0; ks < GRAM_ROWS / 4; ++ks) {
       const int kr = 4 * ks + (lane & 3);
@@ -239,8 +307,13 @@ struct FinSmem {
 // grid: one CTA per upper 8x8 tile (45 for 65 candidates), GRAM_T threads.
 __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, const double* __restrict__ A,
                                                         const double* __restrict__ part, int G,
-                                                        double* __restrict__ gfin) {
-  if (c->done || c->kind != 0) return;
+                                                        double* __restrict__ gfin, uint8_t* __restrict__ upd) {
+  if (c->done) return;
+  if (c->la && c->pend && blockIdx.x == 0) {  // k_gram brought the candidates up to date
+    const int nc = (c->kind == 0) ? c->ncand : 1;
+    for (int q = threadIdx.x; q < nc; q += blockDim.x) upd[c->cand[q]] = 1;
+  }
+  if (c->kind != 0) return;
   const int ncand = c->ncand;
   if (ncand == 1) return;
   extern __shared__ __align__(16) unsigned char fin_raw[];

@@ -6,6 +6,7 @@
 //   reconstruct (explicit Q)  rrqr.py:459-476
 #pragma once
 #include "common.cuh"
+#include "trailing.cuh"
 
 namespace dmqr {
 
@@ -19,6 +20,7 @@ struct InitArgs {
   int32_t k_dm, use_delta_max, break_check, trace_norms;
   int64_t swap_cap, step_cap;
   const int32_t* nonfinite;  // set by k_colnorms_init
+  int32_t lookahead;
 };
 
 __global__ void __launch_bounds__(1024) k_init(InitArgs a) {
@@ -49,6 +51,9 @@ __global__ void __launch_bounds__(1024) k_init(InitArgs a) {
       c->use_delta_max = a.use_delta_max;
       c->break_check = a.break_check;
       c->trace_norms = a.trace_norms;
+      c->la = a.lookahead;
+      c->pend = 0;
+      c->gcount = 0;
       c->swap_cap = (int32_t)min(a.swap_cap, (int64_t)0x7fffffff);
       c->step_cap = (int32_t)min(a.step_cap, (int64_t)0x7fffffff);
       c->n_s = 0;
@@ -63,8 +68,15 @@ __global__ void __launch_bounds__(1024) k_init(InitArgs a) {
 
 // Append the step record and advance n_s (single thread, last kernel of a step).
 __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, double* __restrict__ norm_trace,
-                           unsigned long long* __restrict__ trace_bits) {
-  if (threadIdx.x != 0 || c->done) return;
+                           unsigned long long* __restrict__ trace_bits, const double* __restrict__ A,
+                           double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
+                           double* __restrict__ uref, uint8_t* __restrict__ upd) {
+  if (c->done) return;
+  // look-ahead with no trailing columns past tc0: k_trail_a had no tile to do
+  // the panel-column bookkeeping (one warp does it here)
+  if (c->la && c->tc0 >= c->n) la_panel_columns(c, A, Wt, ldz, u, uref, upd, c->n_s, c->l_acc, c->tc0);
+  __syncwarp();
+  if (threadIdx.x != 0) return;
   const int idx = c->step_idx;
   const int l = c->l_acc;
   if (idx >= c->step_cap) {
@@ -87,6 +99,12 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
     // _record_norm_check appends nothing once the trailing block is empty
     norm_trace[idx] = (n_s1 < c->n) ? __longlong_as_double((long long)*trace_bits) : __longlong_as_double(-1ll);
     *trace_bits = 0ull;
+  }
+  if (c->la) {  // this step's update is now pending below its R rows (look-ahead)
+    c->pend = (l > 0 && c->n_s + l < c->m && c->tc0 < c->n) ? 1 : 0;
+    c->pend_ns = (int32_t)c->n_s;
+    c->pend_l = l;
+    c->gcount = 0;
   }
   c->n_s += l;
   c->step_idx = idx + 1;

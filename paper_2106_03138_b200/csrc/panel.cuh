@@ -27,49 +27,72 @@ namespace dmqr {
 // itself is appended verbatim.
 constexpr int SWAP_MG = 8;  // moves per thread
 
-__global__ void k_swap_gather(const Ctl* __restrict__ c, const double* __restrict__ A, double* __restrict__ scratch) {
+// Look-ahead: while the previous step's update is pending, a column's Wt
+// column (l rows, indexed from n_s) and its `upd` flag travel with it; they
+// ride as extra rows m .. m + l of the scratch.
+__device__ __forceinline__ bool swap_wt(const Ctl* c) { return c->la && c->pend; }
+
+__global__ void k_swap_gather(const Ctl* __restrict__ c, const double* __restrict__ A, double* __restrict__ scratch,
+                              const double* __restrict__ Wt, int64_t ldz) {
   if (c->done) return;
   const int nmv = c->nmv;
   const int t0 = blockIdx.y * SWAP_MG;
   if (t0 >= nmv) return;
-  const int64_t m = c->m, lda = c->lda;
+  const int64_t m = c->m, lda = c->lda, sld = m + DMQR_KP;
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= m) return;
+  const int64_t nrow = m + (swap_wt(c) ? c->pend_l : 0);
+  if (r >= nrow) return;
+  const int64_t n_s = c->n_s;
   double v[SWAP_MG];
 #pragma unroll
   for (int q = 0; q < SWAP_MG; ++q)
-    if (t0 + q < nmv) v[q] = A[(int64_t)c->mv_src[t0 + q] * lda + r];
+    if (t0 + q < nmv) {
+      const int64_t src = c->mv_src[t0 + q];
+      v[q] = (r < m) ? A[src * lda + r] : Wt[(r - m) * ldz + (src - n_s)];
+    }
 #pragma unroll
   for (int q = 0; q < SWAP_MG; ++q)
-    if (t0 + q < nmv) scratch[(int64_t)(t0 + q) * m + r] = v[q];
+    if (t0 + q < nmv) scratch[(int64_t)(t0 + q) * sld + r] = v[q];
 }
 
 __global__ void k_swap_scatter(Ctl* __restrict__ c, double* __restrict__ A, double* __restrict__ u,
                                double* __restrict__ uref, int64_t* __restrict__ perm, int64_t* __restrict__ swaplog,
-                               const double* __restrict__ scratch) {
+                               const double* __restrict__ scratch, double* __restrict__ Wt, int64_t ldz,
+                               uint8_t* __restrict__ upd) {
   if (c->done) return;
   const int nmv = c->nmv;
   const int t0 = blockIdx.y * SWAP_MG;
-  const int64_t m = c->m, lda = c->lda;
+  const int64_t m = c->m, lda = c->lda, sld = m + DMQR_KP;
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t0 < nmv && r < m) {
+  const bool wt = swap_wt(c);
+  const int64_t nrow = m + (wt ? c->pend_l : 0);
+  const int64_t n_s = c->n_s;
+  if (t0 < nmv && r < nrow) {
     double v[SWAP_MG];
 #pragma unroll
     for (int q = 0; q < SWAP_MG; ++q)
-      if (t0 + q < nmv) v[q] = scratch[(int64_t)(t0 + q) * m + r];
+      if (t0 + q < nmv) v[q] = scratch[(int64_t)(t0 + q) * sld + r];
 #pragma unroll
     for (int q = 0; q < SWAP_MG; ++q)
-      if (t0 + q < nmv) A[(int64_t)c->mv_dst[t0 + q] * lda + r] = v[q];
+      if (t0 + q < nmv) {
+        const int64_t dst = c->mv_dst[t0 + q];
+        if (r < m)
+          A[dst * lda + r] = v[q];
+        else
+          Wt[(r - m) * ldz + (dst - n_s)] = v[q];
+      }
   }
   if (blockIdx.x == 0 && blockIdx.y == 0) {
     __shared__ double su[2 * DMQR_KP], sr[2 * DMQR_KP];
     __shared__ int64_t sp[2 * DMQR_KP];
+    __shared__ uint8_t sf[2 * DMQR_KP];
     const int t = threadIdx.x;
     if (t < nmv) {
       const int src = c->mv_src[t];
       su[t] = u[src];
       sr[t] = uref[src];
       sp[t] = perm[src];
+      if (wt) sf[t] = upd[src];
     }
     __syncthreads();
     if (t < nmv) {
@@ -77,6 +100,7 @@ __global__ void k_swap_scatter(Ctl* __restrict__ c, double* __restrict__ A, doub
       u[dst] = su[t];
       uref[dst] = sr[t];
       perm[dst] = sp[t];
+      if (wt) upd[dst] = sf[t];
     }
     const int nsw = c->nsw, ns0 = c->n_swaps;
     for (int s = t; s < nsw; s += blockDim.x)

@@ -523,6 +523,8 @@ __device__ void cq_cluster_reduce(double* part, double* tot, int k) {
 }
 
 __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
+  // the look-ahead trailing grid behind this one may start now (trailing.cuh)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   Ctl* c = a.c;
   if (c->done) return;
   cg::cluster_group cl = cg::this_cluster();

@@ -19,6 +19,7 @@
 // (src-size 0) or get Y = 0, so they contribute nothing.
 #pragma once
 #include "common.cuh"
+#include "norms.cuh"
 
 namespace dmqr {
 
@@ -37,12 +38,53 @@ constexpr int TW_LD = DMQR_KP;  // 72 = 8 mod 16
 constexpr size_t TA_SMEM = sizeof(double) * 2 * DMQR_KP * TW_LD;
 static_assert(2 * DMQR_KP * TW_LD >= 2 * (DMQR_KP + TA_COLS) * TA_LD, "smem reuse");
 
+// Look-ahead bookkeeping of a step's own panel columns, by one CTA: u of the
+// accepted columns is cleared; the columns [n_s + l, tc0) that the Householder
+// panel already updated in full (after a QRDM2 break) are downdated with
+// k_downdate's arithmetic and, while an update is pending, flagged; their Wt
+// slots (Wt is indexed from n_s + l) are zeroed for the next step's moves.
+__device__ void la_panel_columns(Ctl* __restrict__ c, const double* __restrict__ A, double* __restrict__ Wt,
+                                 int64_t ldz, double* __restrict__ u, double* __restrict__ uref,
+                                 uint8_t* __restrict__ upd, int64_t n_s, int l, int64_t tc0) {
+  const int64_t m = c->m, n = c->n, lda = c->lda, base = n_s + l;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  tc0 = min(tc0, n);
+  const bool will_pend = base < m && tc0 < n;
+  for (int64_t j = n_s + threadIdx.x; j < base; j += blockDim.x) {
+    u[j] = 0.0;
+    uref[j] = 0.0;
+  }
+  for (int64_t j = base + wid; j < tc0; j += nw) {
+    const double* col = A + j * lda;
+    double d = 0.0;
+    for (int64_t r = n_s + lane; r < base; r += 32) {
+      const double x = col[r];
+      d = fma(x, x, d);
+    }
+    d = warp_sum(d);
+    const double uj = u[j], rj = uref[j];
+    const double sq = __dsub_rn(__dmul_rn(uj, uj), d);
+    double nu = sqrt(fmax(sq, 0.0));
+    if (sq <= __dmul_rn(1e-2, __dmul_rn(rj, rj))) {
+      nu = warp_col_norm(col + base, m - base, lane);
+      if (lane == 0) uref[j] = nu;
+    }
+    if (lane == 0) {
+      u[j] = nu;
+      if (will_pend) upd[j] = 1;
+    }
+  }
+  for (int64_t e = threadIdx.x; e < (int64_t)l * (tc0 - base); e += blockDim.x)
+    Wt[(e / (tc0 - base)) * ldz + e % (tc0 - base)] = 0.0;
+}
+
 // grid: (ceil(n''/64), nsplit).  Zp[s][i][c] (ld ldz) = sum over this split's rows of Y[r][i] C[r][c];
 // the last split CTA of each column tile reduces them and writes Wt = T^T Z (ld ldz).
-__global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, const double* __restrict__ A,
+__global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double* __restrict__ A,
                                                      double* __restrict__ Zp, const double* __restrict__ T,
                                                      double* __restrict__ Wt, unsigned* __restrict__ counters,
-                                                     int64_t ldz) {
+                                                     int64_t ldz, double* __restrict__ u,
+                                                     double* __restrict__ uref, uint8_t* __restrict__ upd) {
   if (c->done) return;
   const int64_t n_s = c->n_s, m = c->m, n = c->n, lda = c->lda;
   const int l = c->l_acc;
@@ -174,14 +216,138 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, const 
     for (int q = 0; q < DMQR_KP / 8; ++q)
       if (q < lt) dmma884(w[q][0], w[q][1], ts[t * TW_LD + q * 8 + (lane >> 2)], b);
   }
-  // Wt rows [0, lp4) x columns [col0, col0 + 64) (zeros beyond l and beyond ncols keep trail_b exact)
+  // Wt rows [0, lp4) x columns [col0, col0 + 64) (zeros beyond l and beyond ncols keep trail_b exact).
+  // Look-ahead indexes Wt from n_s + l (not tc0) so column moves of the next
+  // step always find a slot.
+  const int64_t n_s1 = n_s + l;
+  const int64_t wofs = c->la ? c0 - n_s1 : 0;
 #pragma unroll
   for (int q = 0; q < DMQR_KP / 8; ++q) {
     const int i = q * 8 + (lane >> 2);
     if (i >= lp4) break;
-    Wt[(int64_t)i * ldz + cc] = (cc < ncols) ? w[q][0] : 0.0;
-    Wt[(int64_t)i * ldz + cc + 1] = (cc + 1 < ncols) ? w[q][1] : 0.0;
+    Wt[(int64_t)i * ldz + wofs + cc] = (cc < ncols) ? w[q][0] : 0.0;
+    Wt[(int64_t)i * ldz + wofs + cc + 1] = (cc + 1 < ncols) ? w[q][1] : 0.0;
   }
+  if (!c->la) return;
+  // ---- look-ahead: R12 = C_top - Y1 Wt on this tile, then the norm downdate
+  // (k_downdate's arithmetic); guard columns go to glist for an exact norm ----
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < DMQR_KP / 8; ++q) {
+    const int i = q * 8 + (lane >> 2);
+    if (i >= lp4) break;
+    zs[i * TW_LD + wid * 8 + 2 * (lane & 3)] = (cc < ncols) ? w[q][0] : 0.0;
+    zs[i * TW_LD + wid * 8 + 2 * (lane & 3) + 1] = (cc + 1 < ncols) ? w[q][1] : 0.0;
+  }
+  for (int e = tid; e < lp4 * lp4; e += TA_T) {  // Y1 (unit lower) -> ts[i][t], column-major reads
+    const int t = e / lp4, i = e % lp4;
+    double y = 0.0;
+    if (i < l && t < l) y = (t < i) ? A[(n_s + t) * lda + n_s + i] : ((t == i) ? 1.0 : 0.0);
+    ts[i * TW_LD + t] = y;
+  }
+  __syncthreads();
+  // same DMMA sequence per element as k_trail_b (acc = C, += (-Y) Wt in
+  // ascending k groups), so the result is bitwise the serial update's
+  double pv[DMQR_KP / 8][2];
+#pragma unroll
+  for (int q = 0; q < DMQR_KP / 8; ++q) {
+    const int i = q * 8 + (lane >> 2);
+    const double* p = A + (n_s + i) + (c0 + cc) * lda;
+    pv[q][0] = (q < lt && i < l && cc < ncols) ? p[0] : 0.0;
+    pv[q][1] = (q < lt && i < l && cc + 1 < ncols) ? p[lda] : 0.0;
+  }
+  for (int ks = 0; ks < lp4; ks += 4) {
+    const int t = ks + (lane & 3);
+    const double b = zs[t * TW_LD + wid * 8 + (lane >> 2)];
+#pragma unroll
+    for (int q = 0; q < DMQR_KP / 8; ++q)
+      if (q < lt) dmma884(pv[q][0], pv[q][1], -ts[(q * 8 + (lane >> 2)) * TW_LD + t], b);
+  }
+#pragma unroll
+  for (int q = 0; q < DMQR_KP / 8; ++q) {
+    const int i = q * 8 + (lane >> 2);
+    if (q >= lt) break;
+    if (i < l) {
+      double* p = A + (n_s + i) + (c0 + cc) * lda;
+      if (cc < ncols) p[0] = pv[q][0];
+      if (cc + 1 < ncols) p[lda] = pv[q][1];
+    }
+  }
+  __syncthreads();
+  // the warp's 8 columns at once (k_downdate's per-column arithmetic and order)
+  double d[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int64_t j = min(c0 + col0 + wid * 8 + q, n - 1);
+    const double* col = A + j * lda;
+    d[q] = 0.0;
+    for (int64_t r = n_s + lane; r < n_s1; r += 32) {
+      const double x = col[r];
+      d[q] = fma(x, x, d[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) d[q] = warp_sum(d[q]);
+  __shared__ int s_ng;
+  __shared__ int s_g[TA_COLS];
+  if (tid == 0) s_ng = 0;
+  __syncthreads();
+  if (lane < 8) {
+    double dq = d[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q)
+      if (lane == q) dq = d[q];
+    const int64_t j = c0 + col0 + wid * 8 + lane;
+    if (j < n) {
+      const double uj = u[j], rj = uref[j];
+      const double sq = __dsub_rn(__dmul_rn(uj, uj), dq);
+      if (sq <= __dmul_rn(1e-2, __dmul_rn(rj, rj)) && n_s1 < m)
+        s_g[atomicAdd(&s_ng, 1)] = wid * 8 + lane;  // guard: exact norm of the updated column
+      else
+        u[j] = sqrt(fmax(sq, 0.0));
+    }
+  }
+  __syncthreads();
+  const int ng = s_ng;
+  if (ng > 0) {
+    // full update of the guard columns on rows [n_s1, m) (k_trail_b's DMMA
+    // sequence per element), then their norms exactly as k_downdate does
+    const int ngt = (ng + 7) / 8;
+    for (int64_t r8 = n_s1 + 8 * wid; r8 < m; r8 += 8 * (TA_T / 32)) {
+      const int64_t r = r8 + (lane >> 2);
+      for (int gt = 0; gt < ngt; ++gt) {
+        double x[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gq = gt * 8 + 2 * (lane & 3) + h;
+          x[h] = (gq < ng && r < m) ? A[(c0 + col0 + s_g[gq]) * lda + r] : 0.0;
+        }
+        for (int ks = 0; ks < lp4; ks += 4) {
+          const int t = ks + (lane & 3);
+          const double a = (t < l && r < m) ? -A[(n_s + t) * lda + r] : 0.0;
+          const int gb = gt * 8 + (lane >> 2);
+          const double b = (gb < ng) ? zs[t * TW_LD + s_g[gb]] : 0.0;
+          dmma884(x[0], x[1], a, b);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gq = gt * 8 + 2 * (lane & 3) + h;
+          if (gq < ng && r < m) A[(c0 + col0 + s_g[gq]) * lda + r] = x[h];
+        }
+      }
+    }
+    __syncthreads();
+    for (int gq = wid; gq < ng; gq += TA_T / 32) {
+      const int64_t j = c0 + col0 + s_g[gq];
+      const double nu = warp_col_norm(A + j * lda + n_s1, m - n_s1, lane);
+      if (lane == 0) {
+        u[j] = nu;
+        uref[j] = nu;
+        upd[j] = 1;  // (n_s1 < m and tc0 < n here: an update is pending)
+      }
+    }
+  }
+  if (blockIdx.x == 0) la_panel_columns(c, A, Wt, ldz, u, uref, upd, n_s, l, c0);
 }
 
 constexpr int TB_T = 256;     // 8 warps: 4 (rows) x 2 (cols), each 32x32
@@ -194,16 +360,11 @@ constexpr size_t TB_SMEM = sizeof(double) * TB_KMAX * (TB_VLD + TB_ZLD);  // 113
 
 // C[r][c] -= sum_t Y[r][t] Wt[t][c] over the trailing block.  grid (ceil((m'+1)/128), ceil(n''/64));
 // row tiles start on even global rows (the possible extra row n_s-1 gets Y = 0).
-__global__ void __launch_bounds__(TB_T, 2) k_trail_b(const Ctl* __restrict__ c, double* __restrict__ A,
-                                                     const double* __restrict__ Wt, int64_t ldz) {
-  if (c->done) return;
-  const int64_t n_s = c->n_s, m = c->m, n = c->n, lda = c->lda;
-  const int l = c->l_acc;
-  const int64_t c0 = c->tc0, ncols = n - c0, mp = m - n_s;
-  const int odd = (int)(n_s & 1);
-  const int64_t row0 = (int64_t)blockIdx.x * TB_ROWS - odd;  // panel-relative, even global row
-  const int64_t col0 = (int64_t)blockIdx.y * TB_COLS;
-  if (row0 >= mp || col0 >= ncols || l == 0) return;
+template <bool LA>
+__device__ __forceinline__ void trail_b_tile(double* __restrict__ A, const double* __restrict__ Wt, int64_t ldz,
+                                             const uint8_t* __restrict__ upd, int64_t n_s, int64_t m, int64_t lda,
+                                             int l, int64_t c0, int64_t ncols, int64_t mp, int64_t row0,
+                                             int64_t col0) {
   const int lp4 = (l + 3) / 4 * 4;
   extern __shared__ __align__(16) double tbs[];
   double* vs = tbs;                      // [68][136]: vs[t*VLD + r] = Y[r][t]
@@ -266,16 +427,62 @@ __global__ void __launch_bounds__(TB_T, 2) k_trail_b(const Ctl* __restrict__ c, 
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt) {
     const int64_t r = row0 + wm * 32 + mt * 8 + (lane >> 2);
-    if (r < 0 || r >= mp) continue;
+    if (r < (LA ? (int64_t)l : 0) || r >= mp) continue;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       const int64_t cc = col0 + wn * 32 + nt * 8 + 2 * (lane & 3);
       double* p = Cp + r + cc * lda;
-      if (cc < ncols) p[0] = acc[mt][nt][0];
-      if (cc + 1 < ncols) p[lda] = acc[mt][nt][1];
+      if (cc < ncols && !(LA && upd[c0 + cc])) p[0] = acc[mt][nt][0];
+      if (cc + 1 < ncols && !(LA && upd[c0 + cc + 1])) p[lda] = acc[mt][nt][1];
     }
   }
 }
+
+// Look-ahead form (LA): the pending update of the previous step (Ctl::pend_*),
+// launched right behind the next panel as its programmatic dependent (the
+// panel triggers at entry, so this grid fills the SMs the panel left free and
+// runs beside it): the top l rows already hold R12 (k_trail_a) and flagged
+// columns (upd) are done -- or are the panel's -- so neither is stored; Wt is
+// indexed from n_s + l.  The last CTA clears the flags and the pending bit;
+// every CTA ends in griddepcontrol.wait, so this grid completes only after
+// the panel (stream order for the kernels behind it).
+template <bool LA>
+__global__ void __launch_bounds__(TB_T, 2) k_trail_b(Ctl* __restrict__ c, double* __restrict__ A,
+                                                     const double* __restrict__ Wt, int64_t ldz,
+                                                     uint8_t* __restrict__ upd, unsigned* __restrict__ counter) {
+  if (LA ? !c->pend : c->done) return;  // (uniform: a dependent-free grid completes with the panel's stream order)
+  const int64_t m = c->m, n = c->n, lda = c->lda;
+  const int64_t n_s = LA ? c->pend_ns : c->n_s;
+  const int l = LA ? c->pend_l : c->l_acc;
+  const int64_t c0 = LA ? n_s + l : c->tc0, ncols = n - c0, mp = m - n_s;
+  const int odd = (int)(n_s & 1);
+  const int64_t row0 = (int64_t)blockIdx.x * TB_ROWS - odd;  // panel-relative, even global row
+  const int64_t col0 = (int64_t)blockIdx.y * TB_COLS;
+  if (!(row0 >= mp || col0 >= ncols || l == 0 || (LA && row0 + TB_ROWS <= l)))
+    trail_b_tile<LA>(A, Wt, ldz, upd, n_s, m, lda, l, c0, ncols, mp, row0, col0);
+  if (LA) {
+    __syncthreads();
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned prev = atomicAdd(counter, 1u);
+      s_last = (prev == gridDim.x * gridDim.y - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      for (int64_t j = threadIdx.x; j < n; j += blockDim.x) upd[j] = 0;
+      if (threadIdx.x == 0) {
+        *counter = 0u;
+        c->pend = 0;
+      }
+      // only the last CTA holds its SM until the panel completes: the grid's
+      // completion then implies the panel's for the kernels behind it
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
+  }
+}
+
 
 // ---------------------------------------------------------------------------
 // Persistent form of C -= Y Wt: one CTA per SM walks a contiguous range of
