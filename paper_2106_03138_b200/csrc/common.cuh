@@ -47,8 +47,11 @@ struct Ctl {
   // pending (pend) for every trailing column not flagged in the per-column
   // `upd` bytes; snapshot of that step (its n_s and accepted reflectors)
   int32_t la, pend, pend_ns, pend_l;
-  int32_t gcount;   // guard columns of the current step (norm recompute list)
-  int32_t pad2;
+  int32_t gcount;   // (unused)
+  // the CholeskyQR2 panel publishes Q1 = P R1^-1 for the spare-SM G = Q1^T C:
+  // q1_count CTAs have written their rows (q1_fail: no usable Q1 this step)
+  uint32_t q1_count;
+  int32_t q1_fail, q1_kk;
   // inter-CTA counters (reset by their users)
   uint32_t gram_count;
   uint32_t bar_count;
@@ -56,6 +59,9 @@ struct Ctl {
   uint32_t trace_bits_lo, trace_bits_hi;
   uint32_t pad1[3];
 };
+
+// leading dimension of the published Q1 buffer (host: lda_of), multiple of 8
+__host__ __device__ __forceinline__ int64_t q1_ld(int64_t m) { return (m > 0 ? (m + 7) / 8 * 8 : 8) + 8; }
 
 struct StepRec {  // mirrors dmqr_step in include/dmqr_b200.h
   int64_t n_s, k_selected, k_accepted, k_max;

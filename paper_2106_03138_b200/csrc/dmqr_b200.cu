@@ -39,13 +39,14 @@ constexpr int NSPLIT_MAX = 16;
 constexpr int PANEL_PMAX = 160;
 
 struct Layout {
-  size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, swp, trace, pdbg, tcount, upd, lacount, total;
+  size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, swp, trace, pdbg, tcount, upd, lacount, q1g, total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 // leading dimension of the Z partials / Wt: 16-byte aligned rows with one tile of slack
 int64_t ldz_for(int64_t n) { return (std::max<int64_t>(n, 1) + 7) / 8 * 8 + 64; }
+
 
 Layout layout(int64_t m, int64_t n) {
   Layout L{};
@@ -60,7 +61,7 @@ Layout layout(int64_t m, int64_t n) {
   L.uref = take(sizeof(double) * std::max<int64_t>(n, 1));
   L.T = take(sizeof(double) * DMQR_KP * DMQR_KP);
   // panel all-reduce partials; the CholeskyQR2 panel also keeps R, Y1 and per-rank R = R2 R1 here
-  L.red = take(sizeof(double) * std::max<size_t>(2 * PANEL_PMAX * RED_LD, 19 * DMQR_KP * DMQR_KP));
+  L.red = take(sizeof(double) * std::max<size_t>(2 * PANEL_PMAX * RED_LD, 21 * DMQR_KP * DMQR_KP));
   L.gram = take(sizeof(double) * GRAM_GMAX * GRAM_PART);
   L.gfin = take(sizeof(double) * DMQR_KP * DMQR_KP);
   L.Zp = take(sizeof(double) * NSPLIT_MAX * DMQR_KP * ldz_for(n));
@@ -70,7 +71,8 @@ Layout layout(int64_t m, int64_t n) {
   L.pdbg = take(sizeof(long long) * 64 * 16);
   L.tcount = take(sizeof(unsigned) * (ceil_div(std::max<int64_t>(n, 1), TA_COLS) + 1));
   L.upd = take(std::max<int64_t>(n, 1));                      // look-ahead column flags
-  L.lacount = take(sizeof(unsigned) * 4);                     // look-ahead last-CTA counters
+  L.lacount = take(sizeof(unsigned) * 8);                     // look-ahead work / last-CTA counters
+  L.q1g = take(sizeof(double) * DMQR_KP * q1_ld(m));  // published Q1 (k_spare)
   L.total = off;
   return L;
 }
@@ -120,6 +122,8 @@ int set_attrs(const DevInfo& d) {
   CK(cudaFuncSetAttribute(k_gram_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FinSmem)));
   CK(cudaFuncSetAttribute(k_trail_b<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
   CK(cudaFuncSetAttribute(k_trail_b<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
+  CK(cudaFuncSetAttribute(k_spare, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SP_SMEM));
+  CK(cudaFuncSetAttribute(k_trail_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TW_SMEM));
   CK(cudaFuncSetAttribute(k_trail_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TP_SMEM));
   CK(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)std::min<size_t>(d.smem_optin - 4096, 220 * 1024)));
@@ -239,6 +243,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   long long* pdbg = (long long*)(ws + L.pdbg);
   unsigned* tcount = (unsigned*)(ws + L.tcount);
   uint8_t* upd = (uint8_t*)(ws + L.upd);
+  double* q1g = (double*)(ws + L.q1g);
   unsigned* lacount = (unsigned*)(ws + L.lacount);
   StepRec* srec = (StepRec*)steps;
   // Look-ahead (default; not with the per-step norm trace, which needs fully
@@ -259,7 +264,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   CK(cudaMemsetAsync(T, 0, sizeof(double) * DMQR_KP * DMQR_KP, st));
   CK(cudaMemsetAsync(tcount, 0, sizeof(unsigned) * (ceil_div(std::max<int64_t>(n, 1), TA_COLS) + 1), st));
   CK(cudaMemsetAsync(upd, 0, (size_t)std::max<int64_t>(n, 1), st));
-  CK(cudaMemsetAsync(lacount, 0, sizeof(unsigned) * 4, st));
+  CK(cudaMemsetAsync(lacount, 0, sizeof(unsigned) * 8, st));
   if (n > 0) {
     if (m > 0) {
       int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)d.sms * 16);
@@ -371,7 +376,8 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     if (rr_path) P = Prr;
     const int G = cl_path ? P : ((P > 1) ? P + 1 : 1);
     PanelArgs pa{ctl, A, coeffs, T, red, use_smem, P,
-                 (g_prof.load() >= 2 && steps_done == 2) ? pdbg : nullptr, std::max(0, g_prof.load() - 2), 0};
+                 (g_prof.load() >= 2 && steps_done == 2) ? pdbg : nullptr, std::max(0, g_prof.load() - 2), 0,
+                 nullptr};
     void* kargs[] = {&pa};
     auto launch_cluster = [&](const void* fn, int ncta, unsigned threads, size_t dsm) -> cudaError_t {
       cudaLaunchConfig_t cfg = {};
@@ -391,12 +397,32 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     // CholeskyQR2 panel (one cluster, <= 256 rows per CTA) first; the Householder
     // kernels behind it run only if it declined (ill-conditioned panel)
     const bool cq_path = use_cq && Prr <= max_cluster;
+    const bool spare = la && cq_path;  // k_spare beside the panel, then k_trail_w
+    const int64_t ntile_g = std::max<int64_t>(1, ceil_div(np, TA_COLS));
+    const int nsplit_g = (int)std::min<int64_t>(
+        std::clamp<int64_t>(ceil_div(2 * (d.sms - Prr), ntile_g), 1, NSPLIT_MAX), std::max<int64_t>(1, ceil_div(mp, 256)));
     if (la_rest && !cq_path) CK(launch_la_rest(false));
     if (cq_path) {
+      pa.q1g = spare ? q1g : nullptr;
       CK(launch_cluster((const void*)k_panel_cq, Prr, PANEL_T, CQ_SMEM));
       NOTE_LAUNCH();
       pa.only_if_fail = 1;
-      if (la_rest) CK(launch_la_rest(true));
+      pa.q1g = nullptr;
+      if (spare) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(2 * std::max(1, d.sms - Prr)));
+        cfg.blockDim = dim3(TB_T);
+        cfg.dynamicSmemBytes = SP_SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        NOTE_LAUNCH();
+        CK(cudaLaunchKernelEx(&cfg, k_spare, ctl, A, (const double*)Z, ldz, upd, (const double*)q1g, Zp,
+                              lacount + 4, Prr, nsplit_g));
+      }
     }
     if (cl_path) {
       CK(launch_cluster((const void*)k_panel_rr<ClusterRed>, G, PANEL_T, RR_CL_SMEM));
@@ -419,8 +445,13 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
       const int64_t ntile = ceil_div(ncols_ub, TA_COLS);
       int nsplit = (int)std::clamp<int64_t>(ceil_div(2 * d.sms, ntile), 1, NSPLIT_MAX);
       nsplit = (int)std::min<int64_t>(nsplit, std::max<int64_t>(1, ceil_div(mp, 256)));
+      if (spare) {
+        k_trail_w<<<(unsigned)ntile, TA_T, TW_SMEM, st>>>(ctl, A, Zp, nsplit_g, T, red + 19 * DMQR_KP * DMQR_KP, Z,
+                                                          ldz, u, uref, upd);
+        NOTE_LAUNCH();
+      }
       k_trail_a<<<dim3((unsigned)ntile, nsplit), TA_T, TA_SMEM, st>>>(ctl, A, Zp, T, Z, tcount, ldz, u, uref,
-                                                                          upd);
+                                                                          upd, spare ? 1 : 0);
       NOTE_LAUNCH();
       if (la) {
         // the rest of C -= Y Wt runs beside the next step's panel

@@ -134,6 +134,7 @@ struct PanelArgs {
   long long* dbg;  // optional phase clocks of CTA dbg_cta (debug builds of the benchmark only)
   int dbg_cta;
   int only_if_fail;  // Householder fallback behind the CholeskyQR2 panel: run only if it declined
+  double* q1g;       // CholeskyQR2 panel: publish Q1 here for k_spare (look-ahead), or null
 };
 
 // deterministic all-reduce of `len` doubles across the grid; in: s_part (this

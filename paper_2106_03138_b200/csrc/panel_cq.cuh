@@ -579,12 +579,27 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     const double bound = 1e-3 * sqrt(vpiv[DMQR_KP + jstar]);
     if (!brk || jstar == 0 || !(bound < eps_s)) fail = true;
   }
+  const int qodd = (int)(n_s & 1);
+  const bool q1_pub = a.q1g != nullptr && !fail && kk > 0;
   if (!fail && kk > 0) {
     // ---- P4/P5: Q1 = P R1^-1 (in place) ----
     cq_trinv_upper(A2, A1, kk);
     CQT();
     cq_slice_gemm(sl, R4, kk, kk, A1);
     CQT();
+    if (q1_pub) {  // publish this rank's Q1 rows for the spare-SM G = Q1^T C (k_spare)
+      __syncthreads();
+      for (int e = tid; e < kk * R; e += PANEL_T) {
+        const int cc = e / R, rr = e % R;
+        a.q1g[(int64_t)cc * q1_ld(m) + qodd + r0 + rr] = sl[cc * CQ_LDS + rr];
+      }
+      __syncthreads();
+      if (tid == 0) {
+        c->q1_kk = kk;
+        __threadfence();
+        atomicAdd(&c->q1_count, 1u);
+      }
+    }
     // keep R1: transpose into the lower triangle of A2, diagonal in vD
     __syncthreads();
     for (int e = tid; e < kk * kk; e += PANEL_T) {
@@ -618,6 +633,11 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     if (s_flag[0]) fail = true;
   }
   if (me == 0 && tid == 0) c->cq_diag[3] = jstar;
+  if (a.q1g != nullptr && !q1_pub && tid == 0) {  // nothing to publish: release k_spare
+    c->q1_fail = 1;
+    __threadfence();
+    atomicAdd(&c->q1_count, 1u);
+  }
   int l = kk;
   if (!fail && kk > 0) {
     // ---- P8: R2 = chol(G2) -> A1 (reads/destroys the upper of A2) ----
@@ -751,6 +771,22 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   }
   CQT();
 #undef CQT
+  if (me == 0 && a.q1g != nullptr) {
+    // k_trail_w forms Wt = T^T (E C_top + M^T G) from G = Q1^T C: publish
+    // F = Y1 - Q1_top M (E = F^T) and M (both l x l, row-major)
+    __syncthreads();
+    cq_small_gemm<true>([&](int i, int t) { return a.q1g[(int64_t)t * q1_ld(m) + qodd + i]; },
+                        [&](int t, int j) { return A2[t * DMQR_KP + j]; }, A1, l);
+    __syncthreads();
+    double* gF = a.red + 19 * DMQR_KP * DMQR_KP;
+    double* gM = gF + DMQR_KP * DMQR_KP;
+    for (int e = tid; e < l * l; e += PANEL_T) {
+      const int i = e / l, j = e % l;
+      const double y1 = (i > j) ? a.red[2 * DMQR_KP * DMQR_KP + i * DMQR_KP + j] : ((i == j) ? 1.0 : 0.0);
+      gF[i * DMQR_KP + j] = y1 - A1[i * DMQR_KP + j];
+      gM[i * DMQR_KP + j] = (j >= i) ? A2[i * DMQR_KP + j] : 0.0;
+    }
+  }
   if (me == 0 && tid == 0) {
     c->l_acc = l;
     c->broke = (l < k);

@@ -78,14 +78,139 @@ __device__ void la_panel_columns(Ctl* __restrict__ c, const double* __restrict__
     Wt[(e / (tc0 - base)) * ldz + e % (tc0 - base)] = 0.0;
 }
 
+// Look-ahead tail of a Wt column tile (k_trail_a, k_trail_w): zs holds the
+// tile's Wt (rows < lp4, 64 columns, zeros past the last column); ts is
+// scratch.  R12 = C_top - Y1 Wt is written with k_trail_b's DMMA sequence per
+// element (so it is bitwise the serial update's), the norms are downdated with
+// k_downdate's arithmetic, guard columns get their full update and an exact
+// norm, and tile 0 does the panel-column bookkeeping.
+__device__ void la_tile_epilogue(Ctl* __restrict__ c, double* __restrict__ A, double* __restrict__ Wt, int64_t ldz,
+                                 double* __restrict__ u, double* __restrict__ uref, uint8_t* __restrict__ upd,
+                                 const double* zs, double* ts, int64_t n_s, int l, int64_t c0, int64_t col0) {
+  const int64_t m = c->m, n = c->n, lda = c->lda, ncols = n - c0, n_s1 = n_s + l;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int lt = (l + 7) / 8, lp4 = (l + 3) / 4 * 4;
+  const int64_t cc = col0 + wid * 8 + 2 * (lane & 3);
+  for (int e = tid; e < lp4 * lp4; e += TA_T) {  // Y1 (unit lower) -> ts[i][t], column-major reads
+    const int t = e / lp4, i = e % lp4;
+    double y = 0.0;
+    if (i < l && t < l) y = (t < i) ? A[(n_s + t) * lda + n_s + i] : ((t == i) ? 1.0 : 0.0);
+    ts[i * TW_LD + t] = y;
+  }
+  __syncthreads();
+  // same DMMA sequence per element as k_trail_b (acc = C, += (-Y) Wt in
+  // ascending k groups), so the result is bitwise the serial update's
+  double pv[DMQR_KP / 8][2];
+#pragma unroll
+  for (int q = 0; q < DMQR_KP / 8; ++q) {
+    const int i = q * 8 + (lane >> 2);
+    const double* p = A + (n_s + i) + (c0 + cc) * lda;
+    pv[q][0] = (q < lt && i < l && cc < ncols) ? p[0] : 0.0;
+    pv[q][1] = (q < lt && i < l && cc + 1 < ncols) ? p[lda] : 0.0;
+  }
+  for (int ks = 0; ks < lp4; ks += 4) {
+    const int t = ks + (lane & 3);
+    const double b = zs[t * TW_LD + wid * 8 + (lane >> 2)];
+#pragma unroll
+    for (int q = 0; q < DMQR_KP / 8; ++q)
+      if (q < lt) dmma884(pv[q][0], pv[q][1], -ts[(q * 8 + (lane >> 2)) * TW_LD + t], b);
+  }
+#pragma unroll
+  for (int q = 0; q < DMQR_KP / 8; ++q) {
+    const int i = q * 8 + (lane >> 2);
+    if (q >= lt) break;
+    if (i < l) {
+      double* p = A + (n_s + i) + (c0 + cc) * lda;
+      if (cc < ncols) p[0] = pv[q][0];
+      if (cc + 1 < ncols) p[lda] = pv[q][1];
+    }
+  }
+  __syncthreads();
+  // the warp's 8 columns at once (k_downdate's per-column arithmetic and order)
+  double d[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int64_t j = min(c0 + col0 + wid * 8 + q, n - 1);
+    const double* col = A + j * lda;
+    d[q] = 0.0;
+    for (int64_t r = n_s + lane; r < n_s1; r += 32) {
+      const double x = col[r];
+      d[q] = fma(x, x, d[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) d[q] = warp_sum(d[q]);
+  __shared__ int s_ng;
+  __shared__ int s_g[TA_COLS];
+  if (tid == 0) s_ng = 0;
+  __syncthreads();
+  if (lane < 8) {
+    double dq = d[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q)
+      if (lane == q) dq = d[q];
+    const int64_t j = c0 + col0 + wid * 8 + lane;
+    if (j < n) {
+      const double uj = u[j], rj = uref[j];
+      const double sq = __dsub_rn(__dmul_rn(uj, uj), dq);
+      if (sq <= __dmul_rn(1e-2, __dmul_rn(rj, rj)) && n_s1 < m)
+        s_g[atomicAdd(&s_ng, 1)] = wid * 8 + lane;  // guard: exact norm of the updated column
+      else
+        u[j] = sqrt(fmax(sq, 0.0));
+    }
+  }
+  __syncthreads();
+  const int ng = s_ng;
+  if (ng > 0) {
+    // full update of the guard columns on rows [n_s1, m) (k_trail_b's DMMA
+    // sequence per element), then their norms exactly as k_downdate does
+    const int ngt = (ng + 7) / 8;
+    for (int64_t r8 = n_s1 + 8 * wid; r8 < m; r8 += 8 * (TA_T / 32)) {
+      const int64_t r = r8 + (lane >> 2);
+      for (int gt = 0; gt < ngt; ++gt) {
+        double x[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gq = gt * 8 + 2 * (lane & 3) + h;
+          x[h] = (gq < ng && r < m) ? A[(c0 + col0 + s_g[gq]) * lda + r] : 0.0;
+        }
+        for (int ks = 0; ks < lp4; ks += 4) {
+          const int t = ks + (lane & 3);
+          const double a = (t < l && r < m) ? -A[(n_s + t) * lda + r] : 0.0;
+          const int gb = gt * 8 + (lane >> 2);
+          const double b = (gb < ng) ? zs[t * TW_LD + s_g[gb]] : 0.0;
+          dmma884(x[0], x[1], a, b);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gq = gt * 8 + 2 * (lane & 3) + h;
+          if (gq < ng && r < m) A[(c0 + col0 + s_g[gq]) * lda + r] = x[h];
+        }
+      }
+    }
+    __syncthreads();
+    for (int gq = wid; gq < ng; gq += TA_T / 32) {
+      const int64_t j = c0 + col0 + s_g[gq];
+      const double nu = warp_col_norm(A + j * lda + n_s1, m - n_s1, lane);
+      if (lane == 0) {
+        u[j] = nu;
+        uref[j] = nu;
+        upd[j] = 1;  // (n_s1 < m and tc0 < n here: an update is pending)
+      }
+    }
+  }
+  if (blockIdx.x == 0) la_panel_columns(c, A, Wt, ldz, u, uref, upd, n_s, l, c0);
+}
+
 // grid: (ceil(n''/64), nsplit).  Zp[s][i][c] (ld ldz) = sum over this split's rows of Y[r][i] C[r][c];
 // the last split CTA of each column tile reduces them and writes Wt = T^T Z (ld ldz).
 __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double* __restrict__ A,
                                                      double* __restrict__ Zp, const double* __restrict__ T,
                                                      double* __restrict__ Wt, unsigned* __restrict__ counters,
                                                      int64_t ldz, double* __restrict__ u,
-                                                     double* __restrict__ uref, uint8_t* __restrict__ upd) {
-  if (c->done) return;
+                                                     double* __restrict__ uref, uint8_t* __restrict__ upd,
+                                                     int only_if_cq_fail) {
+  if (c->done || (only_if_cq_fail && !c->cq_fail)) return;  // (k_trail_w did it)
   const int64_t n_s = c->n_s, m = c->m, n = c->n, lda = c->lda;
   const int l = c->l_acc;
   const int64_t c0 = c->tc0;
@@ -229,8 +354,7 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
     Wt[(int64_t)i * ldz + wofs + cc + 1] = (cc + 1 < ncols) ? w[q][1] : 0.0;
   }
   if (!c->la) return;
-  // ---- look-ahead: R12 = C_top - Y1 Wt on this tile, then the norm downdate
-  // (k_downdate's arithmetic); guard columns go to glist for an exact norm ----
+  // ---- look-ahead: R12, norm downdate, guard columns (la_tile_epilogue) ----
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < DMQR_KP / 8; ++q) {
@@ -239,115 +363,7 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
     zs[i * TW_LD + wid * 8 + 2 * (lane & 3)] = (cc < ncols) ? w[q][0] : 0.0;
     zs[i * TW_LD + wid * 8 + 2 * (lane & 3) + 1] = (cc + 1 < ncols) ? w[q][1] : 0.0;
   }
-  for (int e = tid; e < lp4 * lp4; e += TA_T) {  // Y1 (unit lower) -> ts[i][t], column-major reads
-    const int t = e / lp4, i = e % lp4;
-    double y = 0.0;
-    if (i < l && t < l) y = (t < i) ? A[(n_s + t) * lda + n_s + i] : ((t == i) ? 1.0 : 0.0);
-    ts[i * TW_LD + t] = y;
-  }
-  __syncthreads();
-  // same DMMA sequence per element as k_trail_b (acc = C, += (-Y) Wt in
-  // ascending k groups), so the result is bitwise the serial update's
-  double pv[DMQR_KP / 8][2];
-#pragma unroll
-  for (int q = 0; q < DMQR_KP / 8; ++q) {
-    const int i = q * 8 + (lane >> 2);
-    const double* p = A + (n_s + i) + (c0 + cc) * lda;
-    pv[q][0] = (q < lt && i < l && cc < ncols) ? p[0] : 0.0;
-    pv[q][1] = (q < lt && i < l && cc + 1 < ncols) ? p[lda] : 0.0;
-  }
-  for (int ks = 0; ks < lp4; ks += 4) {
-    const int t = ks + (lane & 3);
-    const double b = zs[t * TW_LD + wid * 8 + (lane >> 2)];
-#pragma unroll
-    for (int q = 0; q < DMQR_KP / 8; ++q)
-      if (q < lt) dmma884(pv[q][0], pv[q][1], -ts[(q * 8 + (lane >> 2)) * TW_LD + t], b);
-  }
-#pragma unroll
-  for (int q = 0; q < DMQR_KP / 8; ++q) {
-    const int i = q * 8 + (lane >> 2);
-    if (q >= lt) break;
-    if (i < l) {
-      double* p = A + (n_s + i) + (c0 + cc) * lda;
-      if (cc < ncols) p[0] = pv[q][0];
-      if (cc + 1 < ncols) p[lda] = pv[q][1];
-    }
-  }
-  __syncthreads();
-  // the warp's 8 columns at once (k_downdate's per-column arithmetic and order)
-  double d[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int64_t j = min(c0 + col0 + wid * 8 + q, n - 1);
-    const double* col = A + j * lda;
-    d[q] = 0.0;
-    for (int64_t r = n_s + lane; r < n_s1; r += 32) {
-      const double x = col[r];
-      d[q] = fma(x, x, d[q]);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 8; ++q) d[q] = warp_sum(d[q]);
-  __shared__ int s_ng;
-  __shared__ int s_g[TA_COLS];
-  if (tid == 0) s_ng = 0;
-  __syncthreads();
-  if (lane < 8) {
-    double dq = d[0];
-#pragma unroll
-    for (int q = 1; q < 8; ++q)
-      if (lane == q) dq = d[q];
-    const int64_t j = c0 + col0 + wid * 8 + lane;
-    if (j < n) {
-      const double uj = u[j], rj = uref[j];
-      const double sq = __dsub_rn(__dmul_rn(uj, uj), dq);
-      if (sq <= __dmul_rn(1e-2, __dmul_rn(rj, rj)) && n_s1 < m)
-        s_g[atomicAdd(&s_ng, 1)] = wid * 8 + lane;  // guard: exact norm of the updated column
-      else
-        u[j] = sqrt(fmax(sq, 0.0));
-    }
-  }
-  __syncthreads();
-  const int ng = s_ng;
-  if (ng > 0) {
-    // full update of the guard columns on rows [n_s1, m) (k_trail_b's DMMA
-    // sequence per element), then their norms exactly as k_downdate does
-    const int ngt = (ng + 7) / 8;
-    for (int64_t r8 = n_s1 + 8 * wid; r8 < m; r8 += 8 * (TA_T / 32)) {
-      const int64_t r = r8 + (lane >> 2);
-      for (int gt = 0; gt < ngt; ++gt) {
-        double x[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int gq = gt * 8 + 2 * (lane & 3) + h;
-          x[h] = (gq < ng && r < m) ? A[(c0 + col0 + s_g[gq]) * lda + r] : 0.0;
-        }
-        for (int ks = 0; ks < lp4; ks += 4) {
-          const int t = ks + (lane & 3);
-          const double a = (t < l && r < m) ? -A[(n_s + t) * lda + r] : 0.0;
-          const int gb = gt * 8 + (lane >> 2);
-          const double b = (gb < ng) ? zs[t * TW_LD + s_g[gb]] : 0.0;
-          dmma884(x[0], x[1], a, b);
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int gq = gt * 8 + 2 * (lane & 3) + h;
-          if (gq < ng && r < m) A[(c0 + col0 + s_g[gq]) * lda + r] = x[h];
-        }
-      }
-    }
-    __syncthreads();
-    for (int gq = wid; gq < ng; gq += TA_T / 32) {
-      const int64_t j = c0 + col0 + s_g[gq];
-      const double nu = warp_col_norm(A + j * lda + n_s1, m - n_s1, lane);
-      if (lane == 0) {
-        u[j] = nu;
-        uref[j] = nu;
-        upd[j] = 1;  // (n_s1 < m and tc0 < n here: an update is pending)
-      }
-    }
-  }
-  if (blockIdx.x == 0) la_panel_columns(c, A, Wt, ldz, u, uref, upd, n_s, l, c0);
+  la_tile_epilogue(c, A, Wt, ldz, u, uref, upd, zs, ts, n_s, l, c0, col0);
 }
 
 constexpr int TB_T = 256;     // 8 warps: 4 (rows) x 2 (cols), each 32x32
@@ -483,6 +499,289 @@ __global__ void __launch_bounds__(TB_T, 2) k_trail_b(Ctl* __restrict__ c, double
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Spare-SM worker (look-ahead, CholeskyQR2 panel path): the programmatic
+// dependent of k_panel_cq, so it runs on the SMs the panel's cluster leaves
+// free while the panel factors.  Persistent CTAs pull work items:
+//   phase 1  the previous step's pending C -= Y Wt (k_trail_b tiles); the CTA
+//            finishing the last tile clears the flags and the pending bit;
+//   phase 2  once phase 1 is done and the panel has published Q1 = P R1^-1
+//            (its first CholeskyQR pass): split-K partials of G = Q1^T C over
+//            all panel rows and the columns from n_s.  With Y2 = Q1_bot M
+//            (rows past the top l) the update's Y^T C = E C_top + M^T G, so
+//            k_trail_w needs only small l x l products after the panel.
+// The last CTA to leave waits for the panel (griddepcontrol.wait), so this
+// grid's completion implies the panel's for the kernels behind it.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// split-K partial of Q1^T C for one 64-column tile and one row split (the
+// k_trail_a main loop with a dense Y = Q1, stored with the row parity of A)
+__device__ void g_partial(const double* __restrict__ A, const double* __restrict__ Q1g, double* __restrict__ Gp,
+                          int64_t ldz, int64_t n_s, int64_t m, int64_t lda, int l, int64_t ncols, int64_t col0,
+                          int split, int nsplit) {
+  const int64_t mp = m - n_s;
+  const int64_t rps = ceil_div(ceil_div(mp, nsplit), TA_ROWS) * TA_ROWS;
+  const int64_t rb = (int64_t)split * rps, re = min(mp, rb + rps);
+  const int lt = (l + 7) / 8, lp = lt * 8;
+  const int odd = (int)(n_s & 1);
+  extern __shared__ __align__(16) double gps[];
+  double* ysb[2] = {gps, gps + DMQR_KP * TA_LD};
+  double* csb[2] = {gps + 2 * DMQR_KP * TA_LD, gps + 2 * DMQR_KP * TA_LD + TA_COLS * TA_LD};
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t span = (re > rb) ? re - rb + odd : 0;
+  const int nslab = (int)ceil_div(span, TA_ROWS);
+  const int rp = tid & 15, cb = tid >> 4;
+  const int64_t ldq = q1_ld(m);
+  const double* Yp = Q1g + odd;            // Q1[r][i] at Yp[r + i*ldq]
+  const double* Cp = A + n_s + n_s * lda;  // C[r][cc] at Cp[r + cc*lda], columns from n_s
+  for (int e = tid; e < (lp - l) * TA_LD; e += TA_T) {
+    ysb[0][l * TA_LD + e] = 0.0;
+    ysb[1][l * TA_LD + e] = 0.0;
+  }
+  auto issue = [&](int sl) {
+    double* ys = ysb[sl & 1];
+    double* cs = csb[sl & 1];
+    const int64_t r = rb - odd + (int64_t)sl * TA_ROWS + 2 * rp;
+    const int64_t gr = n_s + r;
+    const int bytes = (gr + 1 < m) ? 16 : ((gr < m) ? 8 : 0);
+    for (int i = cb; i < l; i += 16) cp_async16(ys + i * TA_LD + 2 * rp, Yp + r + (int64_t)i * ldq, bytes);
+    for (int cc = cb; cc < TA_COLS; cc += 16)
+      cp_async16(cs + cc * TA_LD + 2 * rp, Cp + r + (col0 + cc) * lda, (col0 + cc < ncols) ? bytes : 0);
+    cp_async_commit();
+  };
+  auto fix = [&](int sl) {  // rows outside [rb, re) contribute nothing
+    const int64_t r0 = rb - odd + (int64_t)sl * TA_ROWS;
+    if (r0 >= rb && r0 + TA_ROWS <= re) return;
+    double* ys = ysb[sl & 1];
+    for (int e = tid; e < l * TA_ROWS; e += TA_T) {
+      const int i = e >> 5, rr = e & 31;
+      const int64_t r = r0 + rr;
+      if (r < rb || r >= re) ys[i * TA_LD + rr] = 0.0;
+    }
+  };
+  double acc[DMQR_KP / 8][2];
+#pragma unroll
+  for (int q = 0; q < DMQR_KP / 8; ++q) acc[q][0] = acc[q][1] = 0.0;
+  if (nslab > 0) issue(0);
+  for (int sl = 0; sl < nslab; ++sl) {
+    if (sl + 1 < nslab) {
+      issue(sl + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    fix(sl);
+    __syncthreads();
+    const double* ys = ysb[sl & 1];
+    const double* cs = csb[sl & 1];
+#pragma unroll
+    for (int ks = 0; ks < TA_ROWS / 4; ++ks) {
+      const int kr = 4 * ks + (lane & 3);
+      const double b = cs[(wid * 8 + (lane >> 2)) * TA_LD + kr];
+#pragma unroll
+      for (int q = 0; q < DMQR_KP / 8; ++q)
+        if (q < lt) dmma884(acc[q][0], acc[q][1], ys[(q * 8 + (lane >> 2)) * TA_LD + kr], b);
+    }
+    __syncthreads();
+  }
+  double* out = Gp + (int64_t)split * DMQR_KP * ldz;
+  const int64_t cc = col0 + wid * 8 + 2 * (lane & 3);
+#pragma unroll
+  for (int q = 0; q < DMQR_KP / 8; ++q) {
+    if (q >= lt) break;
+    const int i = q * 8 + (lane >> 2);
+    out[(int64_t)i * ldz + cc] = acc[q][0];
+    out[(int64_t)i * ldz + cc + 1] = acc[q][1];
+  }
+}
+
+constexpr size_t SP_SMEM = TB_SMEM > TA_SMEM ? TB_SMEM : TA_SMEM;
+
+__global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* __restrict__ A,
+                                                   const double* __restrict__ Wt, int64_t ldz,
+                                                   uint8_t* __restrict__ upd, const double* __restrict__ Q1g,
+                                                   double* __restrict__ Gp, unsigned* __restrict__ ctr, int P,
+                                                   int nsplit_g) {
+  __shared__ int s_item, s_flag;
+  const int tid = threadIdx.x;
+  const int64_t m = c->m, n = c->n, lda = c->lda;
+  // ---- phase 1: the pending update of the previous step ----
+  const bool pend = c->la && c->pend;
+  const int64_t pns = c->pend_ns;
+  const int pl = c->pend_l;
+  const int64_t pc0 = pns + pl, pmp = m - pns, pncols = n - pc0;
+  const int podd = (int)(pns & 1);
+  const int ntx = (int)ceil_div(pmp + 1, TB_ROWS);
+  const int ntb = (pend && pncols > 0 && pl > 0) ? ntx * (int)ceil_div(pncols, TB_COLS) : 0;
+  for (;;) {
+    if (tid == 0) s_item = (int)atomicAdd(&ctr[0], 1u);
+    __syncthreads();
+    const int it = s_item;
+    __syncthreads();
+    if (it >= ntb) break;
+    const int64_t row0 = (int64_t)(it % ntx) * TB_ROWS - podd, col0 = (int64_t)(it / ntx) * TB_COLS;
+    if (!(row0 >= pmp || col0 >= pncols || row0 + TB_ROWS <= pl))
+      trail_b_tile<true>(A, Wt, ldz, upd, pns, m, lda, pl, pc0, pncols, pmp, row0, col0);
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      s_flag = (atomicAdd(&ctr[1], 1u) == (unsigned)ntb - 1);
+    }
+    __syncthreads();
+    if (s_flag) {  // every tile has read the flags
+      for (int64_t j = tid; j < n; j += blockDim.x) upd[j] = 0;
+      if (tid == 0) c->pend = 0;
+    }
+  }
+  // ---- phase 2: G = Q1^T C once phase 1 is done and Q1 is published ----
+  if (!c->done) {
+    if (tid == 0) {
+      while (ld_acquire(&ctr[1]) < (unsigned)ntb) __nanosleep(200);
+      while (ld_acquire(&c->q1_count) < (unsigned)P) __nanosleep(200);
+      s_flag = !c->q1_fail;
+    }
+    __syncthreads();
+    if (s_flag) {
+      const int64_t n_s = c->n_s;
+      const int kk = c->q1_kk;
+      const int64_t ncols = n - n_s;
+      const int ntile = (int)ceil_div(ncols, TA_COLS);
+      const int ng = ntile * nsplit_g;
+      for (;;) {
+        if (tid == 0) s_item = (int)atomicAdd(&ctr[2], 1u);
+        __syncthreads();
+        const int it = s_item;
+        __syncthreads();
+        if (it >= ng) break;
+        g_partial(A, Q1g, Gp, ldz, n_s, m, lda, kk, ncols, (int64_t)(it % ntile) * TA_COLS, it / ntile, nsplit_g);
+        __syncthreads();
+      }
+    }
+  }
+  // ---- the last CTA: reset the counters, then hold until the panel completes ----
+  if (tid == 0) {
+    __threadfence();
+    s_flag = (atomicAdd(&ctr[3], 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_flag) {
+    if (tid == 0) ctr[0] = ctr[1] = ctr[2] = ctr[3] = 0u;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
+}
+
+// Wt for the CholeskyQR2 panel path (look-ahead): per 64-column tile from
+// n_s + l, V = E C_top + M^T G (G summed over k_spare's split-K partials,
+// E = F^T and M published by k_panel_cq), Wt = T^T V, then la_tile_epilogue.
+// Exits when the panel declined (cq_fail): k_trail_a then runs as usual.
+constexpr size_t TW_SMEM = sizeof(double) * 5 * DMQR_KP * TW_LD;
+
+__global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* __restrict__ c, double* __restrict__ A,
+                                                  const double* __restrict__ Gp, int nsplit_g,
+                                                  const double* __restrict__ T, const double* __restrict__ FM,
+                                                  double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
+                                                  double* __restrict__ uref, uint8_t* __restrict__ upd) {
+  if (c->done || c->cq_fail) return;
+  const int64_t n_s = c->n_s, m = c->m, n = c->n, lda = c->lda;
+  const int l = c->l_acc;
+  const int64_t c0 = n_s + l, ncols = n - c0;
+  const int64_t col0 = (int64_t)blockIdx.x * TA_COLS;
+  if (col0 >= ncols || l == 0) return;
+  extern __shared__ __align__(16) double tws[];
+  double* gs = tws;                      // G[t][c]     (sum of partials)
+  double* cts = tws + DMQR_KP * TW_LD;   // C_top[t][c]
+  double* fs = cts + DMQR_KP * TW_LD;    // F[t][i]  (E = F^T)
+  double* ms = fs + DMQR_KP * TW_LD;     // M[t][i]
+  double* ts = ms + DMQR_KP * TW_LD;     // T[t][i], then V / scratch
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int lt = (l + 7) / 8, lp4 = (l + 3) / 4 * 4;
+  const double* gF = FM;
+  const double* gM = FM + DMQR_KP * DMQR_KP;
+  for (int e = tid; e < lp4 * TA_COLS; e += TA_T) {
+    const int t = e / TA_COLS, c2 = e % TA_COLS;
+    const int64_t col = col0 + c2;
+    double gsum = 0.0, ct = 0.0;
+    if (t < l && col < ncols) {
+      const double* gp = Gp + (int64_t)t * ldz + l + col;  // G columns are indexed from n_s
+      double v[16];
+#pragma unroll
+      for (int sp = 0; sp < 16; ++sp) v[sp] = (sp < nsplit_g) ? __ldcg(gp + (int64_t)sp * DMQR_KP * ldz) : 0.0;
+#pragma unroll
+      for (int sp = 0; sp < 16; ++sp) gsum += v[sp];
+      ct = A[(n_s + t) + (c0 + col) * lda];
+    }
+    gs[t * TW_LD + c2] = gsum;
+    cts[t * TW_LD + c2] = ct;
+  }
+  for (int e = tid; e < lp4 * lp4; e += TA_T) {
+    const int t = e / lp4, i = e % lp4;
+    const bool in = t < l && i < l;
+    fs[t * TW_LD + i] = in ? gF[t * DMQR_KP + i] : 0.0;
+    ms[t * TW_LD + i] = in ? gM[t * DMQR_KP + i] : 0.0;
+    ts[t * TW_LD + i] = in ? T[t * DMQR_KP + i] : 0.0;
+  }
+  __syncthreads();
+  // V[i][c] = sum_t F[t][i] C_top[t][c] + M[t][i] G[t][c]
+  double v[DMQR_KP / 8][2];
+#pragma unroll
+  for (int q = 0; q < DMQR_KP / 8; ++q) v[q][0] = v[q][1] = 0.0;
+  for (int ks = 0; ks < lp4; ks += 4) {
+    const int t = ks + (lane & 3);
+    const double b1 = cts[t * TW_LD + wid * 8 + (lane >> 2)];
+    const double b2 = gs[t * TW_LD + wid * 8 + (lane >> 2)];
+#pragma unroll
+    for (int q = 0; q < DMQR_KP / 8; ++q)
+      if (q < lt) {
+        dmma884(v[q][0], v[q][1], fs[t * TW_LD + q * 8 + (lane >> 2)], b1);
+        dmma884(v[q][0], v[q][1], ms[t * TW_LD + q * 8 + (lane >> 2)], b2);
+      }
+  }
+  __syncthreads();
+  // V -> gs (reuse); Wt = T^T V
+#pragma unroll
+  for (int q = 0; q < DMQR_KP / 8; ++q) {
+    const int i = q * 8 + (lane >> 2);
+    if (i >= lp4) break;
+    gs[i * TW_LD + wid * 8 + 2 * (lane & 3)] = v[q][0];
+    gs[i * TW_LD + wid * 8 + 2 * (lane & 3) + 1] = v[q][1];
+  }
+  __syncthreads();
+  double w[DMQR_KP / 8][2];
+#pragma unroll
+  for (int q = 0; q < DMQR_KP / 8; ++q) w[q][0] = w[q][1] = 0.0;
+  for (int ks = 0; ks < lp4; ks += 4) {
+    const int t = ks + (lane & 3);
+    const double b = gs[t * TW_LD + wid * 8 + (lane >> 2)];
+#pragma unroll
+    for (int q = 0; q < DMQR_KP / 8; ++q)
+      if (q < lt) dmma884(w[q][0], w[q][1], ts[t * TW_LD + q * 8 + (lane >> 2)], b);
+  }
+  const int64_t cc = col0 + wid * 8 + 2 * (lane & 3);
+#pragma unroll
+  for (int q = 0; q < DMQR_KP / 8; ++q) {
+    const int i = q * 8 + (lane >> 2);
+    if (i >= lp4) break;
+    Wt[(int64_t)i * ldz + cc] = (cc < ncols) ? w[q][0] : 0.0;
+    Wt[(int64_t)i * ldz + cc + 1] = (cc + 1 < ncols) ? w[q][1] : 0.0;
+  }
+  __syncthreads();
+  double* zs = cts;  // Wt tile for the epilogue (C_top no longer needed: reloaded there)
+#pragma unroll
+  for (int q = 0; q < DMQR_KP / 8; ++q) {
+    const int i = q * 8 + (lane >> 2);
+    if (i >= lp4) break;
+    zs[i * TW_LD + wid * 8 + 2 * (lane & 3)] = (cc < ncols) ? w[q][0] : 0.0;
+    zs[i * TW_LD + wid * 8 + 2 * (lane & 3) + 1] = (cc + 1 < ncols) ? w[q][1] : 0.0;
+  }
+  la_tile_epilogue(c, A, Wt, ldz, u, uref, upd, zs, fs, n_s, l, c0, col0);
+}
 
 // ---------------------------------------------------------------------------
 // Persistent form of C -= Y Wt: one CTA per SM walks a contiguous range of
