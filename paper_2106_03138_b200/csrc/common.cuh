@@ -60,6 +60,31 @@ struct Ctl {
   uint32_t pad1[3];
 };
 
+// Entry snapshot of the scalar decision state.  Every field is loaded
+// unconditionally and independently at kernel entry, so the loads overlap in
+// one L2 round trip instead of trickling through early-exit branches (unused
+// fields are dead code).  Only for values a kernel does not change itself.
+struct CtlSnap {
+  int64_t m, n, lda, kmax;
+  double floor, stop_rhs, tau, delta, umax;
+  int32_t stop_active, break_check, k_dm, use_delta_max, trace_norms, swap_cap, step_cap;
+  int32_t n_s, done, step_idx, n_swaps, kind, k_max, nsel, k_s, l_acc, ncand, nsw, nmv;
+  int32_t cq_fail, tc0, la, pend, pend_ns, pend_l, q1_fail, q1_kk;
+};
+__device__ __forceinline__ CtlSnap snap(const Ctl* __restrict__ c) {
+  CtlSnap s;
+  s.m = c->m; s.n = c->n; s.lda = c->lda; s.kmax = c->kmax;
+  s.floor = c->floor; s.stop_rhs = c->stop_rhs; s.tau = c->tau; s.delta = c->delta; s.umax = c->umax;
+  s.stop_active = c->stop_active; s.break_check = c->break_check; s.k_dm = c->k_dm;
+  s.use_delta_max = c->use_delta_max; s.trace_norms = c->trace_norms; s.swap_cap = c->swap_cap;
+  s.step_cap = c->step_cap; s.n_s = c->n_s; s.done = c->done; s.step_idx = c->step_idx; s.n_swaps = c->n_swaps;
+  s.kind = c->kind; s.k_max = c->k_max; s.nsel = c->nsel; s.k_s = c->k_s; s.l_acc = c->l_acc;
+  s.ncand = c->ncand; s.nsw = c->nsw; s.nmv = c->nmv; s.cq_fail = c->cq_fail; s.tc0 = c->tc0;
+  s.la = c->la; s.pend = c->pend; s.pend_ns = c->pend_ns; s.pend_l = c->pend_l;
+  s.q1_fail = c->q1_fail; s.q1_kk = c->q1_kk;
+  return s;
+}
+
 // leading dimension of the published Q1 buffer (host: lda_of), multiple of 8
 __host__ __device__ __forceinline__ int64_t q1_ld(int64_t m) { return (m > 0 ? (m + 7) / 8 * 8 : 8) + 8; }
 

@@ -421,7 +421,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
         cfg.numAttrs = 1;
         NOTE_LAUNCH();
         CK(cudaLaunchKernelEx(&cfg, k_spare, ctl, A, (const double*)Z, ldz, upd, (const double*)q1g, Zp,
-                              lacount + 4, Prr, nsplit_g));
+                              lacount + 4, Prr, nsplit_g, tcount));
       }
     }
     if (cl_path) {

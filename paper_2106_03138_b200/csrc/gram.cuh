@@ -39,17 +39,17 @@ struct PlanSmem {
   int lastw[DMQR_KP];  // latest content written into window slot d (-1: none)
 };
 
-__device__ void plan_swaps_warp(Ctl* c, int nsel, double gamma, PlanSmem& ps) {
+__device__ void plan_swaps_warp(Ctl* c, const CtlSnap& S, int nsel, double gamma, PlanSmem& ps) {
   const int lane = threadIdx.x & 31;
-  const int n_s = c->n_s;
-  const int k_s = (int)min((int64_t)nsel, c->kmax - n_s);
+  const int n_s = S.n_s;
+  const int k_s = (int)min((int64_t)nsel, S.kmax - n_s);
   for (int d = lane; d < DMQR_KP; d += 32) ps.lastw[d] = -1;
   __syncwarp();
   if (lane == 0) {
     c->nsel = nsel;
     c->k_s = k_s;
     c->gamma = gamma;
-    c->eps_s = c->tau * c->umax;
+    c->eps_s = S.tau * S.umax;
     for (int i = 0; i < k_s; ++i) {
       int p = c->sel[i];
       int d = p - n_s;
@@ -142,30 +142,31 @@ __device__ __forceinline__ void tile_ij(int t, int nt, int& ti, int& tj) {
 __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __restrict__ A,
                                                  double* __restrict__ part, const double* __restrict__ Wt,
                                                  int64_t ldz, const uint8_t* __restrict__ upd) {
-  if (c->done) return;
-  const bool pendu = c->la && c->pend;
-  if (c->kind != 0 && !pendu) return;
-  const int ncand = (c->kind == 0) ? c->ncand : 1;
-  if (ncand == 1 && c->kind == 0 && blockIdx.x == 0 && threadIdx.x < 32) {
+  const CtlSnap S = snap(c);
+  if (S.done) return;
+  const bool pendu = S.la && S.pend;
+  if (S.kind != 0 && !pendu) return;
+  const int ncand = (S.kind == 0) ? S.ncand : 1;
+  if (ncand == 1 && S.kind == 0 && blockIdx.x == 0 && threadIdx.x < 32) {
     // no candidates: J = [seed], gamma = 1 (dm.py:145-146)
     __shared__ PlanSmem ps1;
     if (threadIdx.x == 0) c->sel[0] = c->cand[0];
     __syncwarp();
-    plan_swaps_warp(c, 1, 1.0, ps1);
+    plan_swaps_warp(c, S, 1, 1.0, ps1);
   }
   if (ncand == 1 && !pendu) return;
-  const bool gram = c->kind == 0 && ncand > 1;
+  const bool gram = S.kind == 0 && ncand > 1;
   extern __shared__ __align__(16) double gsm[];  // [2][KP][GRAM_LD] slabs, [2][KP][GRAM_LD] Y, [KP][KP] Wt
   __shared__ int s_cand[DMQR_KP];
   __shared__ int s_live[DMQR_KP];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t n_s = c->n_s, m = c->m, lda = c->lda;
+  const int64_t n_s = S.n_s, m = S.m, lda = S.lda;
   const int64_t mp = m - n_s;
   const int np8 = round_up(ncand, 8);
   const int nt = np8 / 8;
   const int ntiles = gram ? nt * (nt + 1) / 2 : 0;
-  const int pl = pendu ? c->pend_l : 0;
-  const int64_t pns = pendu ? c->pend_ns : 0;
+  const int pl = pendu ? S.pend_l : 0;
+  const int64_t pns = pendu ? S.pend_ns : 0;
   const int plp4 = (pl + 3) / 4 * 4;
   double* ysl = gsm + 2 * DMQR_KP * GRAM_LD;
   double* wsm = gsm + 4 * DMQR_KP * GRAM_LD;
@@ -308,13 +309,14 @@ struct FinSmem {
 __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, const double* __restrict__ A,
                                                         const double* __restrict__ part, int G,
                                                         double* __restrict__ gfin, uint8_t* __restrict__ upd) {
-  if (c->done) return;
-  if (c->la && c->pend && blockIdx.x == 0) {  // k_gram brought the candidates up to date
-    const int nc = (c->kind == 0) ? c->ncand : 1;
+  const CtlSnap S = snap(c);
+  if (S.done) return;
+  if (S.la && S.pend && blockIdx.x == 0) {  // k_gram brought the candidates up to date
+    const int nc = (S.kind == 0) ? S.ncand : 1;
     for (int q = threadIdx.x; q < nc; q += blockDim.x) upd[c->cand[q]] = 1;
   }
-  if (c->kind != 0) return;
-  const int ncand = c->ncand;
+  if (S.kind != 0) return;
+  const int ncand = S.ncand;
   if (ncand == 1) return;
   extern __shared__ __align__(16) unsigned char fin_raw[];
   FinSmem& sm = *reinterpret_cast<FinSmem*>(fin_raw);
@@ -369,7 +371,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
     if (!(d > 1e-280 && d < 1e280)) sm.bad = 1;
   }
   __syncthreads();
-  const int64_t n_s = c->n_s, m = c->m, lda = c->lda, mp = m - n_s;
+  const int64_t n_s = S.n_s, m = S.m, lda = S.lda, mp = m - n_s;
   if (sm.bad) {
     // slow path (extreme magnitudes only): recompute with exact 2^-e column scales
     for (int i = wid; i < ncand; i += GRAM_T / 32) {
@@ -415,12 +417,12 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
     sm.g[i * DMQR_KP + j] = __dmul_rn(__dmul_rn(sm.g[i * DMQR_KP + j], sm.inv[i]), sm.inv[j]);
   }
   __syncthreads();
-  const bool dmax = c->use_delta_max != 0;
+  const bool dmax = S.use_delta_max != 0;
   if (!dmax) {
     // ---- greedy filter (dm.py:151-173) via conflict masks: bit q of conf[t] is
     // set when candidate q < t fails |theta_qt| < delta; then t is accepted iff
     // no accepted q conflicts -- one 64-step bit loop on one thread ----
-    const double delta = c->delta;
+    const double delta = S.delta;
     for (int t = wid + 1; t < ncand; t += GRAM_T / 32) {
       const double a0 = (lane < t) ? fabs(sm.g[lane * DMQR_KP + t]) : 0.0;
       const double a1 = (lane + 32 < t) ? fabs(sm.g[(lane + 32) * DMQR_KP + t]) : 0.0;
@@ -461,12 +463,12 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
     for (int o = 16; o > 0; o >>= 1) gmin = fmin(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
     for (int q = lane; q < nch; q += 32) c->sel[q] = c->cand[sm.chosen[q]];
     __syncwarp();
-    plan_swaps_warp(c, nch, gmin, sm.plan);
+    plan_swaps_warp(c, S, nch, gmin, sm.plan);
     return;
   }
   if (wid != 0) return;
   // ---- greedy filter with the delta_max guard, one warp (dm.py:151-173) ----
-  const double tau2 = c->tau * c->tau;
+  const double tau2 = S.tau * S.tau;
   const double delta = dmax ? tau2 / (double)max(c->k_max - 1, 1) : c->delta;
   const double guard = tau2;
   auto th = [&](int i, int j) { return fabs(i < j ? sm.g[i * DMQR_KP + j] : sm.g[j * DMQR_KP + i]); };
@@ -517,7 +519,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
   for (int o = 16; o > 0; o >>= 1) gmin = fmin(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
   for (int q = lane; q < nch; q += 32) c->sel[q] = c->cand[sm.chosen[q]];
   __syncwarp();
-  plan_swaps_warp(c, nch, gmin, sm.plan);
+  plan_swaps_warp(c, S, nch, gmin, sm.plan);
 }
 
 }  // namespace dmqr

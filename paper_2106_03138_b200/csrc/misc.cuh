@@ -71,48 +71,50 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
                            unsigned long long* __restrict__ trace_bits, const double* __restrict__ A,
                            double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
                            double* __restrict__ uref, uint8_t* __restrict__ upd) {
-  if (c->done) return;
+  const CtlSnap S = snap(c);
+  if (S.done) return;
   // look-ahead with no trailing columns past tc0: k_trail_a had no tile to do
   // the panel-column bookkeeping (one warp does it here)
-  if (c->la && c->tc0 >= c->n) la_panel_columns(c, A, Wt, ldz, u, uref, upd, c->n_s, c->l_acc, c->tc0);
+  if (S.la && S.tc0 >= S.n) la_panel_columns(c, A, Wt, ldz, u, uref, upd, S.n_s, S.l_acc, S.tc0);
   __syncwarp();
   if (threadIdx.x != 0) return;
-  const int idx = c->step_idx;
-  const int l = c->l_acc;
-  if (idx >= c->step_cap) {
+  const int idx = S.step_idx;
+  const int l = S.l_acc;
+  if (idx >= S.step_cap) {
     c->status = -5;
     c->done = 1;
     return;
   }
+  const int broke = c->broke;
+  const double eps_s = c->eps_s, gamma = c->gamma;
   StepRec r;
-  r.n_s = c->n_s;
-  r.k_selected = c->k_s;
+  r.n_s = S.n_s;
+  r.k_selected = S.k_s;
   r.k_accepted = l;
-  r.k_max = (c->kind == 0) ? c->k_max : -1;
-  r.broke_early = c->broke;
-  r.fell_back_to_scalar = (c->kind == 1);
-  r.eps_s = (c->kind == 0) ? c->eps_s : 0.0;
-  r.gamma = (c->kind == 0) ? c->gamma : 1.0;
+  r.k_max = (S.kind == 0) ? S.k_max : -1;
+  r.broke_early = broke;
+  r.fell_back_to_scalar = (S.kind == 1);
+  r.eps_s = (S.kind == 0) ? eps_s : 0.0;
+  r.gamma = (S.kind == 0) ? gamma : 1.0;
   steps[idx] = r;
-  if (c->trace_norms && norm_trace) {
-    const int64_t n_s1 = c->n_s + l;
+  if (S.trace_norms && norm_trace) {
+    const int64_t n_s1 = S.n_s + l;
     // _record_norm_check appends nothing once the trailing block is empty
-    norm_trace[idx] = (n_s1 < c->n) ? __longlong_as_double((long long)*trace_bits) : __longlong_as_double(-1ll);
+    norm_trace[idx] = (n_s1 < S.n) ? __longlong_as_double((long long)*trace_bits) : __longlong_as_double(-1ll);
     *trace_bits = 0ull;
   }
-  if (c->la) {  // this step's update is now pending below its R rows (look-ahead)
-    c->pend = (l > 0 && c->n_s + l < c->m && c->tc0 < c->n) ? 1 : 0;
-    c->pend_ns = (int32_t)c->n_s;
+  if (S.la) {  // this step's update is now pending below its R rows (look-ahead)
+    c->pend = (l > 0 && S.n_s + l < S.m && S.tc0 < S.n) ? 1 : 0;
+    c->pend_ns = S.n_s;
     c->pend_l = l;
-    c->gcount = 0;
   }
-  c->n_s += l;
+  c->n_s = S.n_s + l;
   c->step_idx = idx + 1;
   c->l_acc = 0;
   c->broke = 0;
   c->nsw = 0;
   c->nmv = 0;
-  if (c->n_s >= c->kmax) c->done = 1;
+  if (S.n_s + l >= S.kmax) c->done = 1;
 }
 
 // rank / n_factored (rrqr.py:406-412)

@@ -34,15 +34,16 @@ __device__ __forceinline__ bool swap_wt(const Ctl* c) { return c->la && c->pend;
 
 __global__ void k_swap_gather(const Ctl* __restrict__ c, const double* __restrict__ A, double* __restrict__ scratch,
                               const double* __restrict__ Wt, int64_t ldz) {
-  if (c->done) return;
-  const int nmv = c->nmv;
+  const CtlSnap S = snap(c);
+  if (S.done) return;
+  const int nmv = S.nmv;
   const int t0 = blockIdx.y * SWAP_MG;
   if (t0 >= nmv) return;
-  const int64_t m = c->m, lda = c->lda, sld = m + DMQR_KP;
+  const int64_t m = S.m, lda = S.lda, sld = m + DMQR_KP;
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nrow = m + (swap_wt(c) ? c->pend_l : 0);
+  const int64_t nrow = m + ((S.la && S.pend) ? S.pend_l : 0);
   if (r >= nrow) return;
-  const int64_t n_s = c->n_s;
+  const int64_t n_s = S.n_s;
   double v[SWAP_MG];
 #pragma unroll
   for (int q = 0; q < SWAP_MG; ++q)
@@ -59,14 +60,15 @@ __global__ void k_swap_scatter(Ctl* __restrict__ c, double* __restrict__ A, doub
                                double* __restrict__ uref, int64_t* __restrict__ perm, int64_t* __restrict__ swaplog,
                                const double* __restrict__ scratch, double* __restrict__ Wt, int64_t ldz,
                                uint8_t* __restrict__ upd) {
-  if (c->done) return;
-  const int nmv = c->nmv;
+  const CtlSnap S = snap(c);
+  if (S.done) return;
+  const int nmv = S.nmv;
   const int t0 = blockIdx.y * SWAP_MG;
-  const int64_t m = c->m, lda = c->lda, sld = m + DMQR_KP;
+  const int64_t m = S.m, lda = S.lda, sld = m + DMQR_KP;
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool wt = swap_wt(c);
-  const int64_t nrow = m + (wt ? c->pend_l : 0);
-  const int64_t n_s = c->n_s;
+  const bool wt = S.la && S.pend;
+  const int64_t nrow = m + (wt ? S.pend_l : 0);
+  const int64_t n_s = S.n_s;
   if (t0 < nmv && r < nrow) {
     double v[SWAP_MG];
 #pragma unroll
@@ -102,16 +104,16 @@ __global__ void k_swap_scatter(Ctl* __restrict__ c, double* __restrict__ A, doub
       perm[dst] = sp[t];
       if (wt) upd[dst] = sf[t];
     }
-    const int nsw = c->nsw, ns0 = c->n_swaps;
+    const int nsw = S.nsw, ns0 = S.n_swaps;
     for (int s = t; s < nsw; s += blockDim.x)
-      if (ns0 + s < c->swap_cap) {
+      if (ns0 + s < S.swap_cap) {
         swaplog[2 * (ns0 + s)] = c->sw_a[s];
         swaplog[2 * (ns0 + s) + 1] = c->sw_b[s];
       }
     __syncthreads();
     if (t == 0) {
       c->n_swaps = ns0 + nsw;
-      if (ns0 + nsw > c->swap_cap) {
+      if (ns0 + nsw > S.swap_cap) {
         c->status = -5;
         c->done = 1;
       }

@@ -526,7 +526,8 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   // the look-ahead trailing grid behind this one may start now (trailing.cuh)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   Ctl* c = a.c;
-  if (c->done) return;
+  const CtlSnap S = snap(c);
+  if (S.done) return;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double cqs[];
   double* sl = cqs;                              // [CQ_KC][CQ_LDS]
@@ -539,10 +540,10 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
 
   const int tid = threadIdx.x;
   const int me = (int)cl.block_rank(), nr = (int)cl.num_blocks();
-  const int64_t n_s = c->n_s, m = c->m, lda = c->lda;
+  const int64_t n_s = S.n_s, m = S.m, lda = S.lda;
   const int64_t mp = m - n_s;
-  const int k = c->k_s;
-  const bool brk = c->break_check && c->kind == 0;
+  const int k = S.k_s;
+  const bool brk = S.break_check && S.kind == 0;
   const double eps_s = c->eps_s;
   const int r0 = (int)((int64_t)me * mp / nr), r1 = (int)((int64_t)(me + 1) * mp / nr);
   const int R = r1 - r0, R4 = (R + 3) & ~3;

@@ -49,7 +49,10 @@ constexpr size_t RR_CL_SMEM = sizeof(double) * 2 * RR_MAXCL * RED_LD;  // receiv
 template <class Red>
 __global__ void __launch_bounds__(PANEL_T, 1) k_panel_rr(PanelArgs a) {
   Ctl* c = a.c;
-  if (c->done || (a.only_if_fail && !c->cq_fail)) return;
+  {
+    const int done = c->done, cqf = c->cq_fail;  // (both loads in flight together)
+    if (done || (a.only_if_fail && !cqf)) return;
+  }
   __shared__ double vbuf[RR_RMAX];
   __shared__ double xs4[RR_RMAX];  // column 64 (warp 0, slot 4)
   __shared__ double s_part[RED_LD];

@@ -57,7 +57,8 @@ __device__ __forceinline__ int block_excl_scan(int v, int* scan_smem, int* total
 }
 
 __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const double* __restrict__ u) {
-  if (c->done) return;
+  const CtlSnap S = snap(c);
+  if (S.done) return;
   if (threadIdx.x == 0) {
     c->bar_count = 0u;  // the panel's grid-barrier counter restarts each step
     c->cq_fail = 1;     // the CholeskyQR2 panel (if launched) clears this on success
@@ -67,9 +68,9 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const dou
   __shared__ SelSmem sm;
   __shared__ int s_total;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int n_s = c->n_s;
-  const int n = (int)c->n;
-  if (n_s >= c->kmax) {  // loop condition of rrqr.py:335
+  const int n_s = S.n_s;
+  const int n = (int)S.n;
+  if (n_s >= S.kmax) {  // loop condition of rrqr.py:335
     if (tid == 0) c->done = 1;
     return;
   }
@@ -125,9 +126,9 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const dou
   const int seed = sm.bc_i[0];
 
   // ---- stop test (rrqr.py:197-203) ----
-  if (c->stop_active) {
+  if (S.stop_active) {
     const double lhs = sqrt((double)(n - n_s)) * umax;
-    if (lhs <= c->stop_rhs) {
+    if (lhs <= S.stop_rhs) {
       if (tid == 0) {
         c->stopped = 1;
         c->done = 1;
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const dou
     }
   }
   // ---- norm floor -> scalar fallback step (dm.py:140, rrqr.py:219-235) ----
-  if (umax <= c->floor) {
+  if (umax <= S.floor) {
     if (tid == 0) {
       c->kind = 1;
       c->k_max = -1;
@@ -161,8 +162,8 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const dou
   }
 
   // ---- candidate set (dm.py:81-97) ----
-  const double thr = c->tau * umax;
-  const int k_dm = c->k_dm;
+  const double thr = S.tau * umax;
+  const int k_dm = S.k_dm;
   int cnt = 0;
   for (int i = s0; i < s1; ++i) cnt += (i != seed && u[i] >= thr);
   int total;

@@ -210,10 +210,11 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
                                                      int64_t ldz, double* __restrict__ u,
                                                      double* __restrict__ uref, uint8_t* __restrict__ upd,
                                                      int only_if_cq_fail) {
-  if (c->done || (only_if_cq_fail && !c->cq_fail)) return;  // (k_trail_w did it)
-  const int64_t n_s = c->n_s, m = c->m, n = c->n, lda = c->lda;
-  const int l = c->l_acc;
-  const int64_t c0 = c->tc0;
+  const CtlSnap S = snap(c);
+  if (S.done || (only_if_cq_fail && !S.cq_fail)) return;  // (k_trail_w did it)
+  const int64_t n_s = S.n_s, m = S.m, n = S.n, lda = S.lda;
+  const int l = S.l_acc;
+  const int64_t c0 = S.tc0;
   const int64_t ncols = n - c0;
   const int64_t col0 = (int64_t)blockIdx.x * TA_COLS;
   if (col0 >= ncols || l == 0) return;
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
   // Look-ahead indexes Wt from n_s + l (not tc0) so column moves of the next
   // step always find a slot.
   const int64_t n_s1 = n_s + l;
-  const int64_t wofs = c->la ? c0 - n_s1 : 0;
+  const int64_t wofs = S.la ? c0 - n_s1 : 0;
 #pragma unroll
   for (int q = 0; q < DMQR_KP / 8; ++q) {
     const int i = q * 8 + (lane >> 2);
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
     Wt[(int64_t)i * ldz + wofs + cc] = (cc < ncols) ? w[q][0] : 0.0;
     Wt[(int64_t)i * ldz + wofs + cc + 1] = (cc + 1 < ncols) ? w[q][1] : 0.0;
   }
-  if (!c->la) return;
+  if (!S.la) return;
   // ---- look-ahead: R12, norm downdate, guard columns (la_tile_epilogue) ----
   __syncthreads();
 #pragma unroll
@@ -466,11 +467,12 @@ template <bool LA>
 __global__ void __launch_bounds__(TB_T, 2) k_trail_b(Ctl* __restrict__ c, double* __restrict__ A,
                                                      const double* __restrict__ Wt, int64_t ldz,
                                                      uint8_t* __restrict__ upd, unsigned* __restrict__ counter) {
-  if (LA ? !c->pend : c->done) return;  // (uniform: a dependent-free grid completes with the panel's stream order)
-  const int64_t m = c->m, n = c->n, lda = c->lda;
-  const int64_t n_s = LA ? c->pend_ns : c->n_s;
-  const int l = LA ? c->pend_l : c->l_acc;
-  const int64_t c0 = LA ? n_s + l : c->tc0, ncols = n - c0, mp = m - n_s;
+  const CtlSnap S = snap(c);
+  if (LA ? !S.pend : S.done) return;
+  const int64_t m = S.m, n = S.n, lda = S.lda;
+  const int64_t n_s = LA ? S.pend_ns : S.n_s;
+  const int l = LA ? S.pend_l : S.l_acc;
+  const int64_t c0 = LA ? n_s + l : S.tc0, ncols = n - c0, mp = m - n_s;
   const int odd = (int)(n_s & 1);
   const int64_t row0 = (int64_t)blockIdx.x * TB_ROWS - odd;  // panel-relative, even global row
   const int64_t col0 = (int64_t)blockIdx.y * TB_COLS;
@@ -603,19 +605,21 @@ __device__ void g_partial(const double* __restrict__ A, const double* __restrict
 }
 
 constexpr size_t SP_SMEM = TB_SMEM > TA_SMEM ? TB_SMEM : TA_SMEM;
+constexpr int NSPLIT_MAXG = 16;
 
 __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* __restrict__ A,
                                                    const double* __restrict__ Wt, int64_t ldz,
                                                    uint8_t* __restrict__ upd, const double* __restrict__ Q1g,
                                                    double* __restrict__ Gp, unsigned* __restrict__ ctr, int P,
-                                                   int nsplit_g) {
+                                                   int nsplit_g, unsigned* __restrict__ tcnt) {
   __shared__ int s_item, s_flag;
   const int tid = threadIdx.x;
-  const int64_t m = c->m, n = c->n, lda = c->lda;
+  const CtlSnap S = snap(c);
+  const int64_t m = S.m, n = S.n, lda = S.lda;
   // ---- phase 1: the pending update of the previous step ----
-  const bool pend = c->la && c->pend;
-  const int64_t pns = c->pend_ns;
-  const int pl = c->pend_l;
+  const bool pend = S.la && S.pend;
+  const int64_t pns = S.pend_ns;
+  const int pl = S.pend_l;
   const int64_t pc0 = pns + pl, pmp = m - pns, pncols = n - pc0;
   const int podd = (int)(pns & 1);
   const int ntx = (int)ceil_div(pmp + 1, TB_ROWS);
@@ -641,7 +645,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
     }
   }
   // ---- phase 2: G = Q1^T C once phase 1 is done and Q1 is published ----
-  if (!c->done) {
+  if (!S.done) {
     if (tid == 0) {
       while (ld_acquire(&ctr[1]) < (unsigned)ntb) __nanosleep(200);
       while (ld_acquire(&c->q1_count) < (unsigned)P) __nanosleep(200);
@@ -649,7 +653,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
     }
     __syncthreads();
     if (s_flag) {
-      const int64_t n_s = c->n_s;
+      const int64_t n_s = S.n_s;
       const int kk = c->q1_kk;
       const int64_t ncols = n - n_s;
       const int ntile = (int)ceil_div(ncols, TA_COLS);
@@ -660,7 +664,32 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
         const int it = s_item;
         __syncthreads();
         if (it >= ng) break;
-        g_partial(A, Q1g, Gp, ldz, n_s, m, lda, kk, ncols, (int64_t)(it % ntile) * TA_COLS, it / ntile, nsplit_g);
+        const int tile = it % ntile;
+        g_partial(A, Q1g, Gp, ldz, n_s, m, lda, kk, ncols, (int64_t)tile * TA_COLS, it / ntile, nsplit_g);
+        __syncthreads();
+        // the CTA finishing a tile's last split sums its partials into split 0
+        // (fixed order) for k_trail_w
+        if (tid == 0) {
+          __threadfence();
+          s_flag = (atomicAdd(&tcnt[tile], 1u) == (unsigned)nsplit_g - 1);
+        }
+        __syncthreads();
+        if (s_flag) {
+          __threadfence();
+          const int64_t col0 = (int64_t)tile * TA_COLS;
+          for (int e = tid; e < kk * TA_COLS; e += blockDim.x) {
+            const int i = e / TA_COLS, c2 = e % TA_COLS;
+            const double* gp = Gp + (int64_t)i * ldz + col0 + c2;
+            double v[NSPLIT_MAXG];
+#pragma unroll
+            for (int sp = 0; sp < NSPLIT_MAXG; ++sp) v[sp] = (sp < nsplit_g) ? __ldcg(gp + (int64_t)sp * DMQR_KP * ldz) : 0.0;
+            double g = 0.0;
+#pragma unroll
+            for (int sp = 0; sp < NSPLIT_MAXG; ++sp) g += v[sp];
+            Gp[(int64_t)i * ldz + col0 + c2] = g;
+          }
+          if (tid == 0) tcnt[tile] = 0u;
+        }
         __syncthreads();
       }
     }
@@ -688,9 +717,10 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* __restrict__ c, double* _
                                                   const double* __restrict__ T, const double* __restrict__ FM,
                                                   double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
                                                   double* __restrict__ uref, uint8_t* __restrict__ upd) {
-  if (c->done || c->cq_fail) return;
-  const int64_t n_s = c->n_s, m = c->m, n = c->n, lda = c->lda;
-  const int l = c->l_acc;
+  const CtlSnap S = snap(c);
+  if (S.done || S.cq_fail) return;
+  const int64_t n_s = S.n_s, m = S.m, n = S.n, lda = S.lda;
+  const int l = S.l_acc;
   const int64_t c0 = n_s + l, ncols = n - c0;
   const int64_t col0 = (int64_t)blockIdx.x * TA_COLS;
   if (col0 >= ncols || l == 0) return;
@@ -709,12 +739,7 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* __restrict__ c, double* _
     const int64_t col = col0 + c2;
     double gsum = 0.0, ct = 0.0;
     if (t < l && col < ncols) {
-      const double* gp = Gp + (int64_t)t * ldz + l + col;  // G columns are indexed from n_s
-      double v[16];
-#pragma unroll
-      for (int sp = 0; sp < 16; ++sp) v[sp] = (sp < nsplit_g) ? __ldcg(gp + (int64_t)sp * DMQR_KP * ldz) : 0.0;
-#pragma unroll
-      for (int sp = 0; sp < 16; ++sp) gsum += v[sp];
+      gsum = __ldcg(Gp + (int64_t)t * ldz + l + col);  // summed by k_spare; columns indexed from n_s
       ct = A[(n_s + t) + (c0 + col) * lda];
     }
     gs[t * TW_LD + c2] = gsum;
