@@ -446,8 +446,8 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
       int nsplit = (int)std::clamp<int64_t>(ceil_div(2 * d.sms, ntile), 1, NSPLIT_MAX);
       nsplit = (int)std::min<int64_t>(nsplit, std::max<int64_t>(1, ceil_div(mp, 256)));
       if (spare) {
-        k_trail_w<<<(unsigned)ntile, TA_T, TW_SMEM, st>>>(ctl, A, Zp, nsplit_g, T, red + 19 * DMQR_KP * DMQR_KP, Z,
-                                                          ldz, u, uref, upd);
+        k_trail_w<<<(unsigned)ceil_div(ncols_ub, TW_COLS), TA_T, TW_SMEM, st>>>(
+            ctl, A, Zp, red + 19 * DMQR_KP * DMQR_KP, Z, ldz, u, uref, upd);
         NOTE_LAUNCH();
       }
       k_trail_a<<<dim3((unsigned)ntile, nsplit), TA_T, TA_SMEM, st>>>(ctl, A, Zp, T, Z, tcount, ldz, u, uref,

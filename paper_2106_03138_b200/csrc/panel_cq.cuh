@@ -773,20 +773,26 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   CQT();
 #undef CQT
   if (me == 0 && a.q1g != nullptr) {
-    // k_trail_w forms Wt = T^T (E C_top + M^T G) from G = Q1^T C: publish
-    // F = Y1 - Q1_top M (E = F^T) and M (both l x l, row-major)
+    // k_trail_w forms Wt = T^T (E C_top + M^T G) from G = Q1^T C, with
+    // E = F^T, F = Y1 - Q1_top M (both l x l)
     __syncthreads();
     cq_small_gemm<true>([&](int i, int t) { return a.q1g[(int64_t)t * q1_ld(m) + qodd + i]; },
                         [&](int t, int j) { return A2[t * DMQR_KP + j]; }, A1, l);
     __syncthreads();
-    double* gF = a.red + 19 * DMQR_KP * DMQR_KP;
-    double* gM = gF + DMQR_KP * DMQR_KP;
+    // F = Y1 - Q1_top M -> A1 (in place), then FT = F T, MT = M T (the
+    // products k_trail_w applies, transposed) -> global
     for (int e = tid; e < l * l; e += PANEL_T) {
       const int i = e / l, j = e % l;
       const double y1 = (i > j) ? a.red[2 * DMQR_KP * DMQR_KP + i * DMQR_KP + j] : ((i == j) ? 1.0 : 0.0);
-      gF[i * DMQR_KP + j] = y1 - A1[i * DMQR_KP + j];
-      gM[i * DMQR_KP + j] = (j >= i) ? A2[i * DMQR_KP + j] : 0.0;
+      A1[i * DMQR_KP + j] = y1 - A1[i * DMQR_KP + j];
     }
+    __syncthreads();
+    double* gFT = a.red + 19 * DMQR_KP * DMQR_KP;
+    double* gMT = gFT + DMQR_KP * DMQR_KP;
+    cq_small_gemm<true>([&](int i, int t) { return A1[i * DMQR_KP + t]; },
+                        [&](int t, int j) { return a.T[t * DMQR_KP + j]; }, gFT, l);
+    cq_small_gemm([&](int i, int t) { return A2[i * DMQR_KP + t]; },
+                  [&](int t, int j) { return a.T[t * DMQR_KP + j]; }, gMT, l);
   }
   if (me == 0 && tid == 0) {
     c->l_acc = l;

@@ -78,7 +78,53 @@ __device__ void la_panel_columns(Ctl* __restrict__ c, const double* __restrict__
     Wt[(e / (tc0 - base)) * ldz + e % (tc0 - base)] = 0.0;
 }
 
-// Look-ahead tail of a Wt column tile (k_trail_a, k_trail_w): zs holds the
+// Guard columns of a look-ahead tile (downdated square <= 1e-2 u_ref^2): their
+// full update on rows [n_s + l, m) with k_trail_b's DMMA sequence per element
+// (Wt of the tile in zs, ld zld; columns cbase + s_g[q]), then their exact norms.
+__device__ void la_guard_columns(Ctl* __restrict__ c, double* __restrict__ A, double* __restrict__ u,
+                                 double* __restrict__ uref, uint8_t* __restrict__ upd, const double* zs, int zld,
+                                 const int* s_g, int ng, int64_t n_s, int l, int64_t cbase) {
+  if (ng <= 0) return;
+  const int64_t m = c->m, lda = c->lda, n_s1 = n_s + l;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lp4 = (l + 3) / 4 * 4;
+  const int ngt = (ng + 7) / 8;
+  for (int64_t r8 = n_s1 + 8 * wid; r8 < m; r8 += 8 * nw) {
+    const int64_t r = r8 + (lane >> 2);
+    for (int gt = 0; gt < ngt; ++gt) {
+      double x[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gq = gt * 8 + 2 * (lane & 3) + h;
+        x[h] = (gq < ng && r < m) ? A[(cbase + s_g[gq]) * lda + r] : 0.0;
+      }
+      for (int ks = 0; ks < lp4; ks += 4) {
+        const int t = ks + (lane & 3);
+        const double a = (t < l && r < m) ? -A[(n_s + t) * lda + r] : 0.0;
+        const int gb = gt * 8 + (lane >> 2);
+        const double b = (gb < ng) ? zs[t * zld + s_g[gb]] : 0.0;
+        dmma884(x[0], x[1], a, b);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gq = gt * 8 + 2 * (lane & 3) + h;
+        if (gq < ng && r < m) A[(cbase + s_g[gq]) * lda + r] = x[h];
+      }
+    }
+  }
+  __syncthreads();
+  for (int gq = wid; gq < ng; gq += nw) {
+    const int64_t j = cbase + s_g[gq];
+    const double nu = warp_col_norm(A + j * lda + n_s1, m - n_s1, lane);
+    if (lane == 0) {
+      u[j] = nu;
+      uref[j] = nu;
+      upd[j] = 1;  // (n_s1 < m and tc0 < n here: an update is pending)
+    }
+  }
+}
+
+// Look-ahead tail of a Wt column tile (k_trail_a): zs holds the
 // tile's Wt (rows < lp4, 64 columns, zeros past the last column); ts is
 // scratch.  R12 = C_top - Y1 Wt is written with k_trail_b's DMMA sequence per
 // element (so it is bitwise the serial update's), the norms are downdated with
@@ -160,45 +206,7 @@ __device__ void la_tile_epilogue(Ctl* __restrict__ c, double* __restrict__ A, do
     }
   }
   __syncthreads();
-  const int ng = s_ng;
-  if (ng > 0) {
-    // full update of the guard columns on rows [n_s1, m) (k_trail_b's DMMA
-    // sequence per element), then their norms exactly as k_downdate does
-    const int ngt = (ng + 7) / 8;
-    for (int64_t r8 = n_s1 + 8 * wid; r8 < m; r8 += 8 * (TA_T / 32)) {
-      const int64_t r = r8 + (lane >> 2);
-      for (int gt = 0; gt < ngt; ++gt) {
-        double x[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int gq = gt * 8 + 2 * (lane & 3) + h;
-          x[h] = (gq < ng && r < m) ? A[(c0 + col0 + s_g[gq]) * lda + r] : 0.0;
-        }
-        for (int ks = 0; ks < lp4; ks += 4) {
-          const int t = ks + (lane & 3);
-          const double a = (t < l && r < m) ? -A[(n_s + t) * lda + r] : 0.0;
-          const int gb = gt * 8 + (lane >> 2);
-          const double b = (gb < ng) ? zs[t * TW_LD + s_g[gb]] : 0.0;
-          dmma884(x[0], x[1], a, b);
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int gq = gt * 8 + 2 * (lane & 3) + h;
-          if (gq < ng && r < m) A[(c0 + col0 + s_g[gq]) * lda + r] = x[h];
-        }
-      }
-    }
-    __syncthreads();
-    for (int gq = wid; gq < ng; gq += TA_T / 32) {
-      const int64_t j = c0 + col0 + s_g[gq];
-      const double nu = warp_col_norm(A + j * lda + n_s1, m - n_s1, lane);
-      if (lane == 0) {
-        u[j] = nu;
-        uref[j] = nu;
-        upd[j] = 1;  // (n_s1 < m and tc0 < n here: an update is pending)
-      }
-    }
-  }
+  la_guard_columns(c, A, u, uref, upd, zs, TW_LD, s_g, s_ng, n_s, l, c0 + col0);
   if (blockIdx.x == 0) la_panel_columns(c, A, Wt, ldz, u, uref, upd, n_s, l, c0);
 }
 
@@ -706,106 +714,147 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
   }
 }
 
-// Wt for the CholeskyQR2 panel path (look-ahead): per 64-column tile from
-// n_s + l, V = E C_top + M^T G (G summed over k_spare's split-K partials,
-// E = F^T and M published by k_panel_cq), Wt = T^T V, then la_tile_epilogue.
-// Exits when the panel declined (cq_fail): k_trail_a then runs as usual.
-constexpr size_t TW_SMEM = sizeof(double) * 5 * DMQR_KP * TW_LD;
+// Wt for the CholeskyQR2 panel path (look-ahead), after the panel: per
+// 32-column tile from n_s + l,  Wt = A1 C_top + A2 G  (G = Q1^T C summed by
+// k_spare; A1 = T^T E and A2 = T^T M^T published by k_panel_cq as (F T) and
+// (M T)), then R12 = C_top - Y1 Wt, the norm downdate (k_downdate's order),
+// guard columns and the panel-column bookkeeping.  Warp w: columns
+// 8 (w & 3) .. +8, row tiles [5 (w >> 2), +5).  Exits when the panel declined
+// (cq_fail): k_trail_a then runs as usual.
+constexpr int TW_COLS = 32;
+constexpr int TW_CLD = TW_COLS + 8;  // 40 = 8 mod 16
+constexpr size_t TW_SMEM = sizeof(double) * (3 * DMQR_KP * DMQR_KP + 3 * DMQR_KP * TW_CLD);
 
 __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* __restrict__ c, double* __restrict__ A,
-                                                  const double* __restrict__ Gp, int nsplit_g,
-                                                  const double* __restrict__ T, const double* __restrict__ FM,
+                                                  const double* __restrict__ Gp, const double* __restrict__ FM,
                                                   double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
                                                   double* __restrict__ uref, uint8_t* __restrict__ upd) {
   const CtlSnap S = snap(c);
   if (S.done || S.cq_fail) return;
   const int64_t n_s = S.n_s, m = S.m, n = S.n, lda = S.lda;
   const int l = S.l_acc;
-  const int64_t c0 = n_s + l, ncols = n - c0;
-  const int64_t col0 = (int64_t)blockIdx.x * TA_COLS;
-  if (col0 >= ncols || l == 0) return;
+  const int64_t c0 = n_s + l, ncols = n - c0, n_s1 = c0;
+  const int64_t col0 = (int64_t)blockIdx.x * TW_COLS;
+  if (col0 >= ncols || l == 0) return;  // (no trailing columns: k_step_end does the bookkeeping)
   extern __shared__ __align__(16) double tws[];
-  double* gs = tws;                      // G[t][c]     (sum of partials)
-  double* cts = tws + DMQR_KP * TW_LD;   // C_top[t][c]
-  double* fs = cts + DMQR_KP * TW_LD;    // F[t][i]  (E = F^T)
-  double* ms = fs + DMQR_KP * TW_LD;     // M[t][i]
-  double* ts = ms + DMQR_KP * TW_LD;     // T[t][i], then V / scratch
+  double* a1 = tws;                          // FT[t][i]  (A1 = FT^T)
+  double* a2 = a1 + DMQR_KP * DMQR_KP;       // MT[t][i]  (A2 = MT^T)
+  double* y1 = a2 + DMQR_KP * DMQR_KP;       // Y1[i][t] (unit lower)
+  double* gs = y1 + DMQR_KP * DMQR_KP;       // G[t][c], then R12[i][c]
+  double* cts = gs + DMQR_KP * TW_CLD;       // C_top[t][c]
+  double* ws = cts + DMQR_KP * TW_CLD;       // Wt[t][c]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int lt = (l + 7) / 8, lp4 = (l + 3) / 4 * 4;
-  const double* gF = FM;
-  const double* gM = FM + DMQR_KP * DMQR_KP;
-  for (int e = tid; e < lp4 * TA_COLS; e += TA_T) {
-    const int t = e / TA_COLS, c2 = e % TA_COLS;
+  const int lp4 = (l + 3) / 4 * 4, lt = (l + 7) / 8;
+  const int cb = wid & 3, q0 = (wid >> 2) * 5, q1 = min(q0 + 5, lt);
+  const double* gFT = FM;
+  const double* gMT = FM + DMQR_KP * DMQR_KP;
+  for (int e = tid; e < lp4 * TW_COLS; e += TA_T) {
+    const int t = e / TW_COLS, c2 = e % TW_COLS;
     const int64_t col = col0 + c2;
-    double gsum = 0.0, ct = 0.0;
-    if (t < l && col < ncols) {
-      gsum = __ldcg(Gp + (int64_t)t * ldz + l + col);  // summed by k_spare; columns indexed from n_s
-      ct = A[(n_s + t) + (c0 + col) * lda];
-    }
-    gs[t * TW_LD + c2] = gsum;
-    cts[t * TW_LD + c2] = ct;
+    const bool in = t < l && col < ncols;
+    gs[t * TW_CLD + c2] = in ? __ldcg(Gp + (int64_t)t * ldz + l + col) : 0.0;  // G columns from n_s
+    cts[t * TW_CLD + c2] = in ? A[(n_s + t) + (c0 + col) * lda] : 0.0;
   }
   for (int e = tid; e < lp4 * lp4; e += TA_T) {
     const int t = e / lp4, i = e % lp4;
     const bool in = t < l && i < l;
-    fs[t * TW_LD + i] = in ? gF[t * DMQR_KP + i] : 0.0;
-    ms[t * TW_LD + i] = in ? gM[t * DMQR_KP + i] : 0.0;
-    ts[t * TW_LD + i] = in ? T[t * DMQR_KP + i] : 0.0;
+    a1[t * DMQR_KP + i] = in ? gFT[t * DMQR_KP + i] : 0.0;
+    a2[t * DMQR_KP + i] = in ? gMT[t * DMQR_KP + i] : 0.0;
+    // Y1[i][t] from the packed panel (column n_s + t, row n_s + i): coalesced over i
+    y1[i * DMQR_KP + t] = in ? ((t < i) ? A[(n_s + t) * lda + n_s + i] : ((t == i) ? 1.0 : 0.0)) : 0.0;
   }
   __syncthreads();
-  // V[i][c] = sum_t F[t][i] C_top[t][c] + M[t][i] G[t][c]
-  double v[DMQR_KP / 8][2];
+  const int lr = lane >> 2, lk = lane & 3;
+  const int64_t cc = col0 + cb * 8 + 2 * lk;
+  // ---- Wt = A1 C_top + A2 G ----
+  double w[5][2];
 #pragma unroll
-  for (int q = 0; q < DMQR_KP / 8; ++q) v[q][0] = v[q][1] = 0.0;
+  for (int q = 0; q < 5; ++q) w[q][0] = w[q][1] = 0.0;
   for (int ks = 0; ks < lp4; ks += 4) {
-    const int t = ks + (lane & 3);
-    const double b1 = cts[t * TW_LD + wid * 8 + (lane >> 2)];
-    const double b2 = gs[t * TW_LD + wid * 8 + (lane >> 2)];
+    const int t = ks + lk;
+    const double b1 = cts[t * TW_CLD + cb * 8 + lr];
+    const double b2 = gs[t * TW_CLD + cb * 8 + lr];
 #pragma unroll
-    for (int q = 0; q < DMQR_KP / 8; ++q)
-      if (q < lt) {
-        dmma884(v[q][0], v[q][1], fs[t * TW_LD + q * 8 + (lane >> 2)], b1);
-        dmma884(v[q][0], v[q][1], ms[t * TW_LD + q * 8 + (lane >> 2)], b2);
+    for (int q = 0; q < 5; ++q)
+      if (q0 + q < q1) {
+        const int i = (q0 + q) * 8 + lr;
+        dmma884(w[q][0], w[q][1], a1[t * DMQR_KP + i], b1);
+        dmma884(w[q][0], w[q][1], a2[t * DMQR_KP + i], b2);
       }
   }
-  __syncthreads();
-  // V -> gs (reuse); Wt = T^T V
 #pragma unroll
-  for (int q = 0; q < DMQR_KP / 8; ++q) {
-    const int i = q * 8 + (lane >> 2);
-    if (i >= lp4) break;
-    gs[i * TW_LD + wid * 8 + 2 * (lane & 3)] = v[q][0];
-    gs[i * TW_LD + wid * 8 + 2 * (lane & 3) + 1] = v[q][1];
-  }
+  for (int q = 0; q < 5; ++q)
+    if (q0 + q < q1) {
+      const int i = (q0 + q) * 8 + lr;
+      if (i < lp4) {
+        const double w0 = (cc < ncols) ? w[q][0] : 0.0, w1 = (cc + 1 < ncols) ? w[q][1] : 0.0;
+        Wt[(int64_t)i * ldz + cc] = w0;
+        Wt[(int64_t)i * ldz + cc + 1] = w1;
+        ws[i * TW_CLD + cb * 8 + 2 * lk] = w0;
+        ws[i * TW_CLD + cb * 8 + 2 * lk + 1] = w1;
+      }
+    }
   __syncthreads();
-  double w[DMQR_KP / 8][2];
+  // ---- R12 = C_top - Y1 Wt -> A and gs ----
+  double r[5][2];
 #pragma unroll
-  for (int q = 0; q < DMQR_KP / 8; ++q) w[q][0] = w[q][1] = 0.0;
+  for (int q = 0; q < 5; ++q)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) r[q][h] = (q0 + q < q1) ? cts[((q0 + q) * 8 + lr) * TW_CLD + cb * 8 + 2 * lk + h] : 0.0;
   for (int ks = 0; ks < lp4; ks += 4) {
-    const int t = ks + (lane & 3);
-    const double b = gs[t * TW_LD + wid * 8 + (lane >> 2)];
+    const int t = ks + lk;
+    const double b = ws[t * TW_CLD + cb * 8 + lr];
 #pragma unroll
-    for (int q = 0; q < DMQR_KP / 8; ++q)
-      if (q < lt) dmma884(w[q][0], w[q][1], ts[t * TW_LD + q * 8 + (lane >> 2)], b);
+    for (int q = 0; q < 5; ++q)
+      if (q0 + q < q1) dmma884(r[q][0], r[q][1], -y1[((q0 + q) * 8 + lr) * DMQR_KP + t], b);
   }
-  const int64_t cc = col0 + wid * 8 + 2 * (lane & 3);
+  __syncthreads();  // all reads of gs (G) are done
 #pragma unroll
-  for (int q = 0; q < DMQR_KP / 8; ++q) {
-    const int i = q * 8 + (lane >> 2);
-    if (i >= lp4) break;
-    Wt[(int64_t)i * ldz + cc] = (cc < ncols) ? w[q][0] : 0.0;
-    Wt[(int64_t)i * ldz + cc + 1] = (cc + 1 < ncols) ? w[q][1] : 0.0;
+  for (int q = 0; q < 5; ++q)
+    if (q0 + q < q1) {
+      const int i = (q0 + q) * 8 + lr;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const bool in = i < l && cc + h < ncols;
+        gs[i * TW_CLD + cb * 8 + 2 * lk + h] = in ? r[q][h] : 0.0;
+        if (in) A[(n_s + i) + (c0 + cc + h) * lda] = r[q][h];
+      }
+    }
+  __syncthreads();
+  // ---- downdate: warp w, columns 4w .. 4w+3 (k_downdate's per-column order) ----
+  __shared__ int s_ng;
+  __shared__ int s_g[TW_COLS];
+  if (tid == 0) s_ng = 0;
+  double d[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    d[q] = 0.0;
+    for (int rr = lane; rr < l; rr += 32) {
+      const double x = gs[rr * TW_CLD + wid * 4 + q];
+      d[q] = fma(x, x, d[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) d[q] = warp_sum(d[q]);
+  __syncthreads();
+  if (lane < 4) {
+    double dq = d[0];
+#pragma unroll
+    for (int q = 1; q < 4; ++q)
+      if (lane == q) dq = d[q];
+    const int64_t j = c0 + col0 + wid * 4 + lane;
+    if (j < n) {
+      const double uj = u[j], rj = uref[j];
+      const double sq = __dsub_rn(__dmul_rn(uj, uj), dq);
+      if (sq <= __dmul_rn(1e-2, __dmul_rn(rj, rj)) && n_s1 < m)
+        s_g[atomicAdd(&s_ng, 1)] = wid * 4 + lane;
+      else
+        u[j] = sqrt(fmax(sq, 0.0));
+    }
   }
   __syncthreads();
-  double* zs = cts;  // Wt tile for the epilogue (C_top no longer needed: reloaded there)
-#pragma unroll
-  for (int q = 0; q < DMQR_KP / 8; ++q) {
-    const int i = q * 8 + (lane >> 2);
-    if (i >= lp4) break;
-    zs[i * TW_LD + wid * 8 + 2 * (lane & 3)] = (cc < ncols) ? w[q][0] : 0.0;
-    zs[i * TW_LD + wid * 8 + 2 * (lane & 3) + 1] = (cc + 1 < ncols) ? w[q][1] : 0.0;
-  }
-  la_tile_epilogue(c, A, Wt, ldz, u, uref, upd, zs, fs, n_s, l, c0, col0);
+  la_guard_columns(c, A, u, uref, upd, ws, TW_CLD, s_g, s_ng, n_s, l, c0 + col0);
+  if (blockIdx.x == 0) la_panel_columns(c, A, Wt, ldz, u, uref, upd, n_s, l, c0);
 }
 
 // ---------------------------------------------------------------------------
