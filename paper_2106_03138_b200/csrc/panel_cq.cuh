@@ -43,6 +43,8 @@ constexpr int CQ_RMAX = 256;
 // the Householder panel instead.
 constexpr double CQ_PIVOT_TOL = 1e-7;
 constexpr double CQ_ORTH_TOL = 1e-8;
+// |G2 - I| at or below this: pass-2 factors by a two-term expansion (see P8')
+constexpr double CQ_NEAR_ID = 1e-10;
 constexpr size_t CQ_SMEM =
     sizeof(double) * ((size_t)CQ_KC * CQ_LDS + 2 * DMQR_KP * DMQR_KP + 4 * DMQR_KP);  // ~220 KB
 
@@ -619,14 +621,18 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     CQT();
     cq_cluster_reduce(A1, A2, kk);
     CQT();
-    // orthogonality of Q1: |G2 - I|_max
-    if (tid == 0) s_flag[0] = 0;
+    // orthogonality of Q1: |G2 - I|_max (s_flag[2]: beyond the near-identity regime)
+    if (tid == 0) {
+      s_flag[0] = 0;
+      s_flag[2] = 0;
+    }
     __syncthreads();
     for (int e = tid; e < kk * kk; e += PANEL_T) {
       const int i = e / kk, j = e % kk;
       if (j >= i) {
         const double g = A2[i * DMQR_KP + j] - (i == j ? 1.0 : 0.0);
         if (!(fabs(g) < CQ_ORTH_TOL)) s_flag[0] = 1;
+        if (!(fabs(g) <= CQ_NEAR_ID)) s_flag[2] = 1;
       }
     }
     for (int j = tid; j < kk; j += PANEL_T) vpiv[DMQR_KP + j] = A2[j * DMQR_KP + j];
@@ -640,9 +646,41 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     atomicAdd(&c->q1_count, 1u);
   }
   int l = kk;
+  // G2 = I + E with |E| <= CQ_NEAR_ID (the usual case): R2 = I + X from the
+  // fixed point X = Phi(E - X^T X) (Phi: strict upper + half diagonal), two
+  // terms, error O(|E|^3) -- instead of a 65-pivot Cholesky chain
+  const bool near_id = !s_flag[2];
   if (!fail && kk > 0) {
-    // ---- P8: R2 = chol(G2) -> A1 (reads/destroys the upper of A2) ----
-    if (cq_chol(A2, A1, vpiv, vpiv + DMQR_KP, kk, 1e-6) < kk) fail = true;
+    if (near_id) {
+      // ---- P8': X0 = Phi(E) -> A1; P = X0^T X0 -> scratch; R2 = I + Phi(E - P) -> A1 ----
+      for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+        const int i = e / DMQR_KP, j = e % DMQR_KP;
+        double x = 0.0;
+        if (i < kk && j < kk && j >= i) {
+          const double ev = A2[e] - (i == j ? 1.0 : 0.0);
+          x = (i == j) ? 0.5 * ev : ev;
+        }
+        A1[e] = x;
+      }
+      __syncthreads();
+      double* Pg = a.red + 3 * DMQR_KP * DMQR_KP + (size_t)blockIdx.x * DMQR_KP * DMQR_KP;
+      cq_small_gemm<true>([&](int i, int t) { return A1[t * DMQR_KP + i]; },
+                          [&](int t, int j) { return A1[t * DMQR_KP + j]; }, Pg, kk);
+      __syncthreads();
+      for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+        const int i = e / DMQR_KP, j = e % DMQR_KP;
+        double r = 0.0;
+        if (i < kk && j < kk && j >= i) {
+          const double ev = A2[e] - (i == j ? 1.0 : 0.0) - Pg[e];
+          r = (i == j) ? 1.0 + 0.5 * ev : ev;
+        }
+        A1[e] = r;
+      }
+      __syncthreads();
+    } else {
+      // ---- P8: R2 = chol(G2) -> A1 (reads/destroys the upper of A2) ----
+      if (cq_chol(A2, A1, vpiv, vpiv + DMQR_KP, kk, 1e-6) < kk) fail = true;
+    }
     CQT();
   }
   if (!fail && kk > 0) {
@@ -691,7 +729,21 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   CQT();
   double* gR2i = a.red + DMQR_KP * DMQR_KP;  // rank 0's copy of R2^-1 (global scratch)
   if (me == 0) {
-    cq_trinv_upper(A1, A2, l);
+    if (near_id) {  // R2^-1 = I - X + X^2 (error O(|X|^3)), X = R2 - I
+      cq_small_gemm([&](int i, int t) { return A1[i * DMQR_KP + t] - (i == t ? 1.0 : 0.0); },
+                    [&](int t, int j) { return A1[t * DMQR_KP + j] - (t == j ? 1.0 : 0.0); }, A2, l);
+      __syncthreads();
+      for (int e = tid; e < l * l; e += PANEL_T) {
+        const int i = e / l, j = e % l;
+        if (j >= i) {
+          const double x = A1[i * DMQR_KP + j] - (i == j ? 1.0 : 0.0);
+          A2[i * DMQR_KP + j] = (i == j ? 1.0 : 0.0) - x + A2[i * DMQR_KP + j];
+        }
+      }
+      __syncthreads();
+    } else {
+      cq_trinv_upper(A1, A2, l);
+    }
     CQT();
     for (int e = tid; e < l * l; e += PANEL_T) gR2i[(e / l) * DMQR_KP + e % l] = A2[(e / l) * DMQR_KP + e % l];
     // ---- P12: top l x l block of Q = Q1 R2^-1 -> A1 ----
