@@ -250,7 +250,8 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   // updated columns at every step end): step k's C -= Y Wt below its R rows
   // runs beside step k+1's panel (programmatic dependent launch); step k+1's
   // candidates get it first (in k_gram).
-  const bool la = !p->trace_norms && getenv("DMQR_NO_LOOKAHEAD") == nullptr && m > 0 && n > 0;
+  // (small problems -- e.g. the 256^2 batch of cfg3 -- are launch-bound: serial form)
+  const bool la = !p->trace_norms && getenv("DMQR_NO_LOOKAHEAD") == nullptr && m * n >= (int64_t)1 << 20;
 
 
   const int64_t kmax = std::min(m, n);
@@ -410,7 +411,9 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
       pa.q1g = nullptr;
       if (spare) {
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)(2 * std::max(1, d.sms - Prr)));
+        // persistent CTAs: two per SM the panel leaves free, but no more than work items
+        const int64_t items = (int64_t)lag.x * lag.y * (la_rest ? 1 : 0) + ntile_g * nsplit_g;
+        cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(2 * std::max(1, d.sms - Prr), items)));
         cfg.blockDim = dim3(TB_T);
         cfg.dynamicSmemBytes = SP_SMEM;
         cfg.stream = st;

@@ -317,15 +317,16 @@ __device__ void cq_mlu(double* A, double* vS, double* vpiv, int l) {
           const double sg = (qjj >= 0.0) ? -1.0 : 1.0;  // S_j = -sign(q'_jj), sign(+0) = +
           const double pv = 1.0 - sg * qjj;             // pivot = 1 + |q'_jj|
           const double f0 = -sg * cq_rcp12(pv);
+          // rows i > b0 + j: multiplier and elimination; rows at or above
+          // the pivot (slot 0 only) get L = 0, which leaves them unchanged
+          // (branch-free; rows past l hold zeros and are never stored)
 #pragma unroll
           for (int s = 0; s < 3; ++s) {
-            const int i = b0 + lane + 32 * s;
-            if (i > b0 + j) {  // rows past l hold zeros and are never stored
-              const double L = f0 * v[s][j];
+            const bool below = (s > 0) || (lane > j);
+            const double L = below ? f0 * v[s][j] : 0.0;
 #pragma unroll
-              for (int c = j + 1; c < 8; ++c) v[s][c] -= L * qj[c];
-              v[s][j] = L;
-            }
+            for (int c = j + 1; c < 8; ++c) v[s][c] = fma(-L, qj[c], v[s][c]);
+            v[s][j] = below ? L : v[s][j];
           }
           // block rows i > j, columns right of the block: q'_ic -= L_ij q'_jc
 #pragma unroll
