@@ -725,11 +725,12 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       const int i = e / l, j = e % l;
       a.red[i * DMQR_KP + j] = (j >= i) ? A2[i * DMQR_KP + j] : 0.0;
     }
-  // ---- P11: R2^-1 -> A2 (rank 0; R2 upper in A1) ----
+  // ---- P11: R2^-1 -> A2 (R2 upper in A1): rank 0 for Q_top; rank 1 too,
+  // beside rank 0's LU, for M (with two or more ranks rank 1 forms M) ----
   __syncthreads();
   CQT();
-  double* gR2i = a.red + DMQR_KP * DMQR_KP;  // rank 0's copy of R2^-1 (global scratch)
-  if (me == 0) {
+  const bool m_on_1 = nr > 1;  // M = -R2^-1 S U^-1 on rank 1, in parallel with rank 0's T
+  auto r2_inverse = [&]() {
     if (near_id) {  // R2^-1 = I - X + X^2 (error O(|X|^3)), X = R2 - I
       cq_small_gemm([&](int i, int t) { return A1[i * DMQR_KP + t] - (i == t ? 1.0 : 0.0); },
                     [&](int t, int j) { return A1[t * DMQR_KP + j] - (t == j ? 1.0 : 0.0); }, A2, l);
@@ -744,9 +745,15 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       __syncthreads();
     } else {
       cq_trinv_upper(A1, A2, l);
+      __syncthreads();
     }
+  };
+  double* gR2i = a.red + DMQR_KP * DMQR_KP;  // rank 0's copy of R2^-1 (global scratch)
+  if (me == 0) {
+    r2_inverse();
     CQT();
-    for (int e = tid; e < l * l; e += PANEL_T) gR2i[(e / l) * DMQR_KP + e % l] = A2[(e / l) * DMQR_KP + e % l];
+    if (!m_on_1)
+      for (int e = tid; e < l * l; e += PANEL_T) gR2i[(e / l) * DMQR_KP + e % l] = A2[(e / l) * DMQR_KP + e % l];
     // ---- P12: top l x l block of Q = Q1 R2^-1 -> A1 ----
     cq_small_gemm<true>([&](int i, int t) { return sl[t * CQ_LDS + i]; },
                         [&](int t, int j) { return A2[t * DMQR_KP + j]; }, A1, l);
@@ -775,6 +782,11 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       if (j == i) A1[i * DMQR_KP + i] = 1.0;
     }
     __syncthreads();
+  } else if (me == 1) {
+    r2_inverse();  // (overlaps rank 0's Q_top and LU)
+  }
+  cl.sync();  // U and S ready on rank 0
+  if (me == 0) {
     // Z = (Y1^T)^-1 into the top l x l block of the slice (rows < l of Y come
     // from Y1 at write-back), Z[i][j] at sl[j*LDS + i]
     cq_trinv_upper(A1, sl, l, 1, CQ_LDS);
@@ -783,23 +795,48 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
                   [&](int t, int j) { return sl[j * CQ_LDS + t]; }, a.T, l);
     for (int j = tid; j < l; j += PANEL_T) a.coeffs[n_s + j] = vpiv[j];
     __syncthreads();
-    // U^-1 -> A1 (upper)
-    cq_trinv_upper(A2, A1, l);
-    __syncthreads();
-    // M = -R2^-1 S U^-1 -> A2 (upper): Y_below = -(Q1 R2^-1 S) U^-1 = Q1 M
-    cq_small_gemm([&](int i, int t) { return -vS[t] * gR2i[i * DMQR_KP + t]; },
-                  [&](int t, int j) { return A1[t * DMQR_KP + j]; }, A2, l);
+    if (!m_on_1) {
+      // U^-1 -> A1 (upper)
+      cq_trinv_upper(A2, A1, l);
+      __syncthreads();
+      // M = -R2^-1 S U^-1 -> A2 (upper): Y_below = -(Q1 R2^-1 S) U^-1 = Q1 M
+      cq_small_gemm([&](int i, int t) { return -vS[t] * gR2i[i * DMQR_KP + t]; },
+                    [&](int t, int j) { return A1[t * DMQR_KP + j]; }, A2, l);
+    }
     CQT();
-  }
-  cl.sync();
-  if (me != 0) {  // pull M (upper of rank 0's A2) and S from rank 0
+  } else if (me == 1) {
+    // pull U (upper of rank 0's A2) and S, then U^-1 -> global scratch, M -> A1
     const double* A2r = cl.map_shared_rank(A2, 0);
     const double* vSr = cl.map_shared_rank(vS, 0);
     for (int e = tid; e < l * l; e += PANEL_T) {
       const int i = e / l, j = e % l;
-      A2[i * DMQR_KP + j] = (j >= i) ? A2r[i * DMQR_KP + j] : 0.0;
+      A1[i * DMQR_KP + j] = (j >= i) ? A2r[i * DMQR_KP + j] : 0.0;
     }
     for (int j = tid; j < l; j += PANEL_T) vS[j] = vSr[j];
+    __syncthreads();
+    double* Ug = a.red + 3 * DMQR_KP * DMQR_KP + (size_t)blockIdx.x * DMQR_KP * DMQR_KP;
+    cq_trinv_upper(A1, Ug, l);
+    __syncthreads();
+    // M = -R2^-1 S U^-1 (R2^-1 in A2 from above)
+    cq_small_gemm([&](int i, int t) { return -vS[t] * A2[i * DMQR_KP + t]; },
+                  [&](int t, int j) { return Ug[t * DMQR_KP + j]; }, A1, l);
+  }
+  cl.sync();  // M ready (rank 1's A1, or rank 0's A2)
+  if (m_on_1 ? (me != 1) : (me != 0)) {  // pull M and S
+    const double* Mr = m_on_1 ? cl.map_shared_rank(A1, 1) : cl.map_shared_rank(A2, 0);
+    const double* vSr = cl.map_shared_rank(vS, 0);
+    for (int e = tid; e < l * l; e += PANEL_T) {
+      const int i = e / l, j = e % l;
+      A2[i * DMQR_KP + j] = (j >= i) ? Mr[i * DMQR_KP + j] : 0.0;
+    }
+    if (me != 0)
+      for (int j = tid; j < l; j += PANEL_T) vS[j] = vSr[j];
+  } else if (m_on_1) {  // rank 1: its M into A2 for the Y product
+    __syncthreads();
+    for (int e = tid; e < l * l; e += PANEL_T) {
+      const int i = e / l, j = e % l;
+      A2[i * DMQR_KP + j] = (j >= i) ? A1[i * DMQR_KP + j] : 0.0;
+    }
   }
   cl.sync();
   // ---- P16: Y = Q1 M on this rank's rows (rank 0's rows < l are fixed below) ----
