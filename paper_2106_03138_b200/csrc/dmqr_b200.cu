@@ -39,7 +39,7 @@ constexpr int NSPLIT_MAX = 16;
 constexpr int PANEL_PMAX = 160;
 
 struct Layout {
-  size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, swp, trace, pdbg, tcount, upd, lacount, q1g, total;
+  size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, trace, pdbg, tcount, upd, lacount, q1g, total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -66,7 +66,6 @@ Layout layout(int64_t m, int64_t n) {
   L.gfin = take(sizeof(double) * DMQR_KP * DMQR_KP);
   L.Zp = take(sizeof(double) * NSPLIT_MAX * DMQR_KP * ldz_for(n));
   L.Z = take(sizeof(double) * DMQR_KP * ldz_for(n));
-  L.swp = take(sizeof(double) * 2 * DMQR_KP * (std::max<int64_t>(m, 1) + DMQR_KP));
   L.trace = take(sizeof(unsigned long long) * 4);
   L.pdbg = take(sizeof(long long) * 64 * 16);
   L.tcount = take(sizeof(unsigned) * (ceil_div(std::max<int64_t>(n, 1), TA_COLS) + 1));
@@ -238,7 +237,6 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   double* gfin = (double*)(ws + L.gfin);
   double* Zp = (double*)(ws + L.Zp);
   double* Z = (double*)(ws + L.Z);
-  double* swp = (double*)(ws + L.swp);
   unsigned long long* tbits = (unsigned long long*)(ws + L.trace);
   long long* pdbg = (long long*)(ws + L.pdbg);
   unsigned* tcount = (unsigned*)(ws + L.tcount);
@@ -324,10 +322,8 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     k_gram_finish<<<45, GRAM_T, sizeof(FinSmem), st>>>(ctl, A, gpart, GG, gfin, upd);
     NOTE_LAUNCH();
     {
-      const dim3 gs((unsigned)ceil_div(m + (la ? DMQR_KP : 0), 256), (unsigned)ceil_div(2 * DMQR_KP, SWAP_MG));
-      k_swap_gather<<<gs, 256, 0, st>>>(ctl, A, swp, Z, ldz);
-      NOTE_LAUNCH();
-      k_swap_scatter<<<gs, 256, 0, st>>>(ctl, A, u, uref, perm, swaps, swp, Z, ldz, upd);
+      k_swap<<<(unsigned)ceil_div(m + (la ? DMQR_KP : 0), SWAP_ROWS), SWAP_T, SWAP_SMEM, st>>>(
+          ctl, A, u, uref, perm, swaps, Z, ldz, upd);
       NOTE_LAUNCH();
     }
     // the rest of the previous step's update: beside the CholeskyQR2 panel as

@@ -21,97 +21,89 @@
 namespace dmqr {
 
 // Apply the step's column moves (the composed transposition sequence) to
-// full-height columns in two fully parallel passes: gather every source
-// column into scratch, then scatter into the destinations (grid: row blocks x
-// move groups).  u, u_ref and perm get the same moves; the transposition log
-// itself is appended verbatim.
-constexpr int SWAP_MG = 8;  // moves per thread
-
+// full-height columns in one pass: every CTA owns a range of rows, reads the
+// sources of all moves on those rows into shared memory, then writes the
+// destinations -- moves only exchange columns, so each row range is closed
+// under them and needs no global scratch.  u, u_ref, perm (and the look-ahead
+// flags) get the same moves in block 0; the transposition log itself is
+// appended verbatim.
 // Look-ahead: while the previous step's update is pending, a column's Wt
-// column (l rows, indexed from n_s) and its `upd` flag travel with it; they
-// ride as extra rows m .. m + l of the scratch.
-__device__ __forceinline__ bool swap_wt(const Ctl* c) { return c->la && c->pend; }
+// column (l rows, indexed from n_s) rides along as extra rows m .. m + l.
+constexpr int SWAP_ROWS = 16;                  // rows per CTA
+constexpr int SWAP_T = 256;
+constexpr int SWAP_MAXMV = 2 * DMQR_KP;        // 144
+constexpr size_t SWAP_SMEM = sizeof(double) * SWAP_MAXMV * SWAP_ROWS;  // 36 KB
 
-__global__ void k_swap_gather(const Ctl* __restrict__ c, const double* __restrict__ A, double* __restrict__ scratch,
-                              const double* __restrict__ Wt, int64_t ldz) {
+__global__ void __launch_bounds__(SWAP_T) k_swap(Ctl* __restrict__ c, double* __restrict__ A, double* __restrict__ u,
+                                                 double* __restrict__ uref, int64_t* __restrict__ perm,
+                                                 int64_t* __restrict__ swaplog, double* __restrict__ Wt, int64_t ldz,
+                                                 uint8_t* __restrict__ upd) {
   const CtlSnap S = snap(c);
   if (S.done) return;
   const int nmv = S.nmv;
-  const int t0 = blockIdx.y * SWAP_MG;
-  if (t0 >= nmv) return;
-  const int64_t m = S.m, lda = S.lda, sld = m + DMQR_KP;
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nrow = m + ((S.la && S.pend) ? S.pend_l : 0);
-  if (r >= nrow) return;
-  const int64_t n_s = S.n_s;
-  double v[SWAP_MG];
-#pragma unroll
-  for (int q = 0; q < SWAP_MG; ++q)
-    if (t0 + q < nmv) {
-      const int64_t src = c->mv_src[t0 + q];
-      v[q] = (r < m) ? A[src * lda + r] : Wt[(r - m) * ldz + (src - n_s)];
-    }
-#pragma unroll
-  for (int q = 0; q < SWAP_MG; ++q)
-    if (t0 + q < nmv) scratch[(int64_t)(t0 + q) * sld + r] = v[q];
-}
-
-__global__ void k_swap_scatter(Ctl* __restrict__ c, double* __restrict__ A, double* __restrict__ u,
-                               double* __restrict__ uref, int64_t* __restrict__ perm, int64_t* __restrict__ swaplog,
-                               const double* __restrict__ scratch, double* __restrict__ Wt, int64_t ldz,
-                               uint8_t* __restrict__ upd) {
-  const CtlSnap S = snap(c);
-  if (S.done) return;
-  const int nmv = S.nmv;
-  const int t0 = blockIdx.y * SWAP_MG;
-  const int64_t m = S.m, lda = S.lda, sld = m + DMQR_KP;
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t m = S.m, lda = S.lda;
   const bool wt = S.la && S.pend;
   const int64_t nrow = m + (wt ? S.pend_l : 0);
   const int64_t n_s = S.n_s;
-  if (t0 < nmv && r < nrow) {
-    double v[SWAP_MG];
-#pragma unroll
-    for (int q = 0; q < SWAP_MG; ++q)
-      if (t0 + q < nmv) v[q] = scratch[(int64_t)(t0 + q) * sld + r];
-#pragma unroll
-    for (int q = 0; q < SWAP_MG; ++q)
-      if (t0 + q < nmv) {
-        const int64_t dst = c->mv_dst[t0 + q];
-        if (r < m)
-          A[dst * lda + r] = v[q];
-        else
-          Wt[(r - m) * ldz + (dst - n_s)] = v[q];
-      }
+  const int tid = threadIdx.x;
+  __shared__ int s_src[SWAP_MAXMV], s_dst[SWAP_MAXMV];
+  extern __shared__ __align__(16) double sws[];  // [move][row]
+  for (int q = tid; q < nmv; q += SWAP_T) {
+    s_src[q] = c->mv_src[q];
+    s_dst[q] = c->mv_dst[q];
   }
-  if (blockIdx.x == 0 && blockIdx.y == 0) {
-    __shared__ double su[2 * DMQR_KP], sr[2 * DMQR_KP];
-    __shared__ int64_t sp[2 * DMQR_KP];
-    __shared__ uint8_t sf[2 * DMQR_KP];
-    const int t = threadIdx.x;
-    if (t < nmv) {
-      const int src = c->mv_src[t];
+  __syncthreads();
+  const int64_t r0 = (int64_t)blockIdx.x * SWAP_ROWS;
+  if (nmv > 0 && r0 < nrow) {
+#pragma unroll 9
+    for (int e = tid; e < nmv * SWAP_ROWS; e += SWAP_T) {
+      const int q = e / SWAP_ROWS, rr = e % SWAP_ROWS;
+      const int64_t r = r0 + rr;
+      if (r < nrow) {
+        const int64_t src = s_src[q];
+        sws[e] = (r < m) ? A[src * lda + r] : Wt[(r - m) * ldz + (src - n_s)];
+      }
+    }
+    __syncthreads();
+#pragma unroll 9
+    for (int e = tid; e < nmv * SWAP_ROWS; e += SWAP_T) {
+      const int q = e / SWAP_ROWS, rr = e % SWAP_ROWS;
+      const int64_t r = r0 + rr;
+      if (r < nrow) {
+        const int64_t dst = s_dst[q];
+        if (r < m)
+          A[dst * lda + r] = sws[e];
+        else
+          Wt[(r - m) * ldz + (dst - n_s)] = sws[e];
+      }
+    }
+  }
+  if (blockIdx.x == 0) {
+    __shared__ double su[SWAP_MAXMV], sr[SWAP_MAXMV];
+    __shared__ int64_t sp[SWAP_MAXMV];
+    __shared__ uint8_t sf[SWAP_MAXMV];
+    for (int t = tid; t < nmv; t += SWAP_T) {
+      const int src = s_src[t];
       su[t] = u[src];
       sr[t] = uref[src];
       sp[t] = perm[src];
       if (wt) sf[t] = upd[src];
     }
     __syncthreads();
-    if (t < nmv) {
-      const int dst = c->mv_dst[t];
+    for (int t = tid; t < nmv; t += SWAP_T) {
+      const int dst = s_dst[t];
       u[dst] = su[t];
       uref[dst] = sr[t];
       perm[dst] = sp[t];
       if (wt) upd[dst] = sf[t];
     }
     const int nsw = S.nsw, ns0 = S.n_swaps;
-    for (int s = t; s < nsw; s += blockDim.x)
+    for (int s = tid; s < nsw; s += SWAP_T)
       if (ns0 + s < S.swap_cap) {
         swaplog[2 * (ns0 + s)] = c->sw_a[s];
         swaplog[2 * (ns0 + s) + 1] = c->sw_b[s];
       }
-    __syncthreads();
-    if (t == 0) {
+    if (tid == 0) {
       c->n_swaps = ns0 + nsw;
       if (ns0 + nsw > S.swap_cap) {
         c->status = -5;
