@@ -379,8 +379,8 @@ constexpr int TB_T = 256;     // 8 warps: 4 (rows) x 2 (cols), each 32x32
 constexpr int TB_ROWS = 128;
 constexpr int TB_COLS = 64;
 constexpr int TB_KMAX = 68;           // l <= 65 rounded up to 4
-constexpr int TB_VLD = TB_ROWS + 8;   // 136 = 8 mod 16
-constexpr int TB_ZLD = TB_COLS + 8;   // 72  = 8 mod 16
+constexpr int TB_VLD = TB_ROWS + 4;   // 132 = 4 mod 16: the 4 (k) x 4 (row) half-warp fragment reads hit 16 distinct bank pairs
+constexpr int TB_ZLD = TB_COLS + 4;   // 68  = 4 mod 16 (same)
 constexpr size_t TB_SMEM = sizeof(double) * TB_KMAX * (TB_VLD + TB_ZLD);  // 113 KB -> 2 CTAs/SM
 
 // C[r][c] -= sum_t Y[r][t] Wt[t][c] over the trailing block.  grid (ceil((m'+1)/128), ceil(n''/64));
@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
 // 8 (w & 3) .. +8, row tiles [5 (w >> 2), +5).  Exits when the panel declined
 // (cq_fail): k_trail_a then runs as usual.
 constexpr int TW_COLS = 32;
-constexpr int TW_CLD = TW_COLS + 8;  // 40 = 8 mod 16
+constexpr int TW_CLD = TW_COLS + 4;  // 36 = 4 mod 16 (conflict-free 4 x 4 half-warp fragments)
 constexpr size_t TW_SMEM = sizeof(double) * (3 * DMQR_KP * DMQR_KP + 3 * DMQR_KP * TW_CLD);
 
 __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* __restrict__ c, double* __restrict__ A,
