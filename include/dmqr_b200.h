@@ -104,6 +104,20 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
                   size_t ws_bytes, dmqr_info* info, void* stream);
 
 /*
+ * dmqr_qrdm_f64 that also streams the packed factor to the host while it runs:
+ * columns [0, n_s) are final after every outer step, so they are copied to
+ * host_packed (HOST, pinned for overlap; column-major, ld host_ld >= m) on a
+ * side stream as the host learns n_s; the rest follows the last step.  The
+ * reference's caller gets its numpy `packed` (rrqr.py:415-423) without a
+ * trailing device-to-host copy.  host_packed = NULL: same as dmqr_qrdm_f64.
+ */
+int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* params,
+                         double* coeffs, int64_t* perm, int64_t* swaps, int64_t swap_cap,
+                         dmqr_step* steps, int64_t step_cap, double* norm_trace, void* workspace,
+                         size_t ws_bytes, dmqr_info* info, double* host_packed, int64_t host_ld,
+                         void* stream);
+
+/*
  * Batched QRDM / QRDM2 over `batch` independent m x n matrices stored at
  * A + b*stride (cfg3: batches of small matrices).  The batch is spread over
  * `nlanes` concurrent CUDA streams (one host thread each, every lane running

@@ -15,6 +15,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libdmqr_b200.so"
 EXPORTS = (
     "dmqr_workspace_bytes",
     "dmqr_qrdm_f64",
+    "dmqr_qrdm_stream_f64",
     "dmqr_qrdm_batched_f64",
     "dmqr_batched_workspace_bytes",
     "dmqr_form_q_f64",
@@ -104,6 +105,9 @@ def load() -> C.CDLL:
     lib.dmqr_qrdm_f64.argtypes = [P, I64, I64, I64, C.POINTER(Params), P, P, P, I64, P, I64, P, P, SZ,
                                   C.POINTER(Info), VP]
     lib.dmqr_qrdm_f64.restype = C.c_int
+    lib.dmqr_qrdm_stream_f64.argtypes = [P, I64, I64, I64, C.POINTER(Params), P, P, P, I64, P, I64, P, P, SZ,
+                                         C.POINTER(Info), P, I64, VP]
+    lib.dmqr_qrdm_stream_f64.restype = C.c_int
     lib.dmqr_qrdm_batched_f64.argtypes = [P, I64, I64, I64, I64, I64, C.POINTER(Params), P, P, P, I64, P, I64,
                                           P, I32, P, SZ, VP]
     lib.dmqr_qrdm_batched_f64.restype = C.c_int

@@ -217,6 +217,15 @@ int dmqr_check_finite_f64(const double* A, int64_t m, int64_t n, int64_t lda, in
 int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* p, double* coeffs, int64_t* perm,
                   int64_t* swaps, int64_t swap_cap, dmqr_step* steps, int64_t step_cap, double* norm_trace,
                   void* workspace, size_t ws_bytes, dmqr_info* info, void* stream) {
+  return dmqr_qrdm_stream_f64(A, m, n, lda, p, coeffs, perm, swaps, swap_cap, steps, step_cap, norm_trace,
+                              workspace, ws_bytes, info, nullptr, 0, stream);
+}
+
+int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* p, double* coeffs,
+                         int64_t* perm, int64_t* swaps, int64_t swap_cap, dmqr_step* steps, int64_t step_cap,
+                         double* norm_trace, void* workspace, size_t ws_bytes, dmqr_info* info,
+                         double* host_packed, int64_t host_ld, void* stream) {
+  if (host_packed && host_ld < m) return DMQR_EINVAL;
   int rc = validate(m, n, lda, p);
   if (rc) return rc;
   if (!info) return DMQR_EINVAL;
@@ -483,6 +492,20 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     return 0;
   };
 
+  // streamed packed factor: final columns go to the host on a side stream
+  static thread_local cudaStream_t sCopy = nullptr;
+  if (host_packed && !sCopy) CK(cudaStreamCreateWithFlags(&sCopy, cudaStreamNonBlocking));
+  int64_t copied = 0;
+  auto stream_cols = [&](int64_t upto, cudaEvent_t after) -> int {
+    upto = std::min(upto, n);
+    if (!host_packed || upto <= copied || m == 0) return 0;
+    CK(cudaStreamWaitEvent(sCopy, after, 0));
+    CK(cudaMemcpy2DAsync(host_packed + copied * host_ld, sizeof(double) * host_ld, A + copied * lda,
+                         sizeof(double) * lda, sizeof(double) * m, (size_t)(upto - copied), cudaMemcpyDeviceToHost,
+                         sCopy));
+    copied = upto;
+    return 0;
+  };
   int64_t known_ns = 0;  // n_s after the last step whose head was read
   int known = 0, enq = 0;
   bool finished = (kmax == 0);
@@ -500,7 +523,7 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
     known_ns = hh[sl].n_s;
     ++known;
     if (hh[sl].done) finished = true;
-    return 0;
+    return stream_cols(known_ns, hev[sl]);  // columns left of n_s are final
   };
   while (!finished) {
     if (enq - known >= 2) {
@@ -543,6 +566,12 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
   k_finalize<<<1, 256, 0, st>>>(ctl, A, p->stop_rule == DMQR_STOP_NONE);
   NOTE_LAUNCH();
   CK(cudaGetLastError());
+  if (host_packed && m > 0 && n > 0) {  // the rest of the packed factor
+    CK(cudaEventRecord(hev[0], st));
+    copied = std::min(copied, n);
+    if (stream_cols(n, hev[0])) return DMQR_ECUDA;
+    CK(cudaStreamSynchronize(sCopy));
+  }
   Ctl hc;
   CK(cudaMemcpyAsync(&hc, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));

@@ -171,6 +171,31 @@ class RRQRResult:
 # counters replay (rrqr.py:330,356,366-373,384-391,230-235,346) -- SURVEY App. C
 # ----------------------------------------------------------------------------
 
+class LazyCounters:
+    """WorkCounters replayed from the step log on first access (the replay is a
+    Python loop over every accepted column; most callers never read it)."""
+
+    def __init__(self, m: int, n: int, steps: list):
+        self._args = (m, n, steps)
+        self._wc = None
+
+    def _get(self) -> WorkCounters:
+        if self._wc is None:
+            self._wc = replay_counters(*self._args)
+        return self._wc
+
+    def __getattr__(self, name):
+        if name.startswith("_"):
+            raise AttributeError(name)
+        return getattr(self._get(), name)
+
+    def __eq__(self, other):
+        return self._get() == (other._get() if isinstance(other, LazyCounters) else other)
+
+    def __repr__(self):
+        return repr(self._get())
+
+
 def replay_counters(m: int, n: int, steps: list) -> WorkCounters:
     wc = WorkCounters(total_flops=2.0 * m * n)
     for st in steps:
@@ -267,6 +292,7 @@ class DeviceFactor:
     norm_trace: object
     info: _lib.Info
     workspace: object = None
+    host_packed: object = None  # pinned (n, m) host copy streamed by the engine, if requested
 
     def debug_ctl(self) -> dict:
         """Decision state of the last step (debug aid)."""
@@ -288,7 +314,7 @@ class DeviceFactor:
 
 def factorize(A, params: DMParams = DMParams(), stop: StopCriterion = StopCriterion(),
               break_check: bool = True, trace_norms: bool = False, stream=None, work=None,
-              max_steps: int = 0) -> DeviceFactor:
+              max_steps: int = 0, host_packed=None) -> DeviceFactor:
     """Run one factorization on the device; returns device buffers.
 
     ``work`` may be a (buf, m, n, lda) tuple from ``to_work`` whose buffer is
@@ -317,12 +343,15 @@ def factorize(A, params: DMParams = DMParams(), stop: StopCriterion = StopCriter
     wsb = int(lib.dmqr_workspace_bytes(m, n, C.byref(p)))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     info = _lib.Info()
-    rc = lib.dmqr_qrdm_f64(buf.data_ptr(), m, n, lda, C.byref(p), coeffs.data_ptr(), perm.data_ptr(),
-                           swaps.data_ptr(), swap_cap, steps.data_ptr(), step_cap,
-                           ntrace.data_ptr() if ntrace is not None else None, ws.data_ptr(), wsb,
-                           C.byref(info), sh)
+    # host_packed: pinned (n, m) host tensor; the engine streams the finished
+    # columns of the packed factor into it while it runs
+    hp = host_packed.data_ptr() if host_packed is not None else None
+    rc = lib.dmqr_qrdm_stream_f64(buf.data_ptr(), m, n, lda, C.byref(p), coeffs.data_ptr(), perm.data_ptr(),
+                                  swaps.data_ptr(), swap_cap, steps.data_ptr(), step_cap,
+                                  ntrace.data_ptr() if ntrace is not None else None, ws.data_ptr(), wsb,
+                                  C.byref(info), hp, m, sh)
     _check(rc)
-    return DeviceFactor(buf, m, n, lda, coeffs[:kmax], perm[:n], swaps, steps, ntrace, info, ws)
+    return DeviceFactor(buf, m, n, lda, coeffs[:kmax], perm[:n], swaps, steps, ntrace, info, ws, host_packed)
 
 
 def _steps_from_raw(raw: np.ndarray, count: int) -> list:
@@ -358,28 +387,40 @@ def to_result(f: DeviceFactor, device: bool = False) -> RRQRResult:
     if device:
         packed, coeffs = packed_t, f.coeffs
     elif f.m and f.n:
-        # rows of buf are the columns: copy (n, m) row-major and view it as an F-ordered (m, n)
-        # (into page-locked memory from torch's caching host allocator: a pageable
-        # copy of a 4096^2 factor runs at ~2 GB/s, a pinned one at ~55 GB/s)
-        packed = _pinned_copy(f.buf[: f.n, : f.m]).numpy().T
+        # rows of buf are the columns: an (n, m) row-major host copy viewed as an
+        # F-ordered (m, n) -- streamed by the engine during the factorization when
+        # a pinned buffer was passed, else copied now into page-locked memory
+        # (a pageable copy of a 4096^2 factor runs at ~2 GB/s, a pinned one at ~55)
+        hp = f.host_packed
+        packed = (hp if hp is not None else _pinned_copy(f.buf[: f.n, : f.m])).numpy().T
         coeffs = f.coeffs.cpu().numpy()
     else:
         packed, coeffs = np.zeros((f.m, f.n), order="F"), np.zeros(0)
     return RRQRResult(packed=packed, coeffs=coeffs, perm=perm, rank=int(info.rank), step_log=steps,
                       n_factored=int(info.n_factored), stopped_early=bool(info.stopped_early),
-                      counters=replay_counters(f.m, f.n, steps), norm_trace=trace)
+                      counters=LazyCounters(f.m, f.n, steps), norm_trace=trace)
+
+
+def _run(A, params, stop, break_check, trace_norms, device) -> RRQRResult:
+    torch = _torch()
+    work = to_work(A)
+    hp = None
+    if not device and work[1] and work[2]:
+        hp = torch.empty((work[2], work[1]), dtype=torch.float64, pin_memory=True)
+    return to_result(factorize(None, params, stop, break_check=break_check, trace_norms=trace_norms, work=work,
+                               host_packed=hp), device)
 
 
 def qrdm(A, params: DMParams = DMParams(), stop: StopCriterion = StopCriterion(),
          trace_norms: bool = False, device: bool = False) -> RRQRResult:
     """Blocked QR with deviation-maximization pivoting (rrqr.py:426-440), on the B200."""
-    return to_result(factorize(A, params, stop, break_check=False, trace_norms=trace_norms), device)
+    return _run(A, params, stop, False, trace_norms, device)
 
 
 def qrdm2(A, params: DMParams = DMParams(), stop: StopCriterion = StopCriterion(),
           trace_norms: bool = False, device: bool = False) -> RRQRResult:
     """``qrdm`` plus the within-block break check (rrqr.py:443-456), on the B200."""
-    return to_result(factorize(A, params, stop, break_check=True, trace_norms=trace_norms), device)
+    return _run(A, params, stop, True, trace_norms, device)
 
 
 def form_q(packed, coeffs, n_factored: int, qcols: int | None = None):
