@@ -39,7 +39,7 @@ constexpr int NSPLIT_MAX = 16;
 constexpr int PANEL_PMAX = 160;
 
 struct Layout {
-  size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, trace, pdbg, tcount, upd, lacount, q1g, total;
+  size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, trace, pdbg, tcount, upd, lacount, q1g, glist, total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -72,6 +72,7 @@ Layout layout(int64_t m, int64_t n) {
   L.upd = take(std::max<int64_t>(n, 1));                      // look-ahead column flags
   L.lacount = take(sizeof(unsigned) * 8);                     // look-ahead work / last-CTA counters
   L.q1g = take(sizeof(double) * DMQR_KP * q1_ld(m));  // published Q1 (k_spare)
+  L.glist = take(sizeof(int32_t) * std::max<int64_t>(n, 1));  // look-ahead guard columns
   L.total = off;
   return L;
 }
@@ -123,6 +124,7 @@ int set_attrs(const DevInfo& d) {
   CK(cudaFuncSetAttribute(k_trail_b<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
   CK(cudaFuncSetAttribute(k_spare, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SP_SMEM));
   CK(cudaFuncSetAttribute(k_trail_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TW_SMEM));
+  CK(cudaFuncSetAttribute(k_guard, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GU_SMEM));
   CK(cudaFuncSetAttribute(k_trail_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TP_SMEM));
   CK(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)std::min<size_t>(d.smem_optin - 4096, 220 * 1024)));
@@ -251,6 +253,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
   unsigned* tcount = (unsigned*)(ws + L.tcount);
   uint8_t* upd = (uint8_t*)(ws + L.upd);
   double* q1g = (double*)(ws + L.q1g);
+  int32_t* glist = (int32_t*)(ws + L.glist);
   unsigned* lacount = (unsigned*)(ws + L.lacount);
   StepRec* srec = (StepRec*)steps;
   // Look-ahead (default; not with the per-step norm trace, which needs fully
@@ -258,7 +261,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
   // runs beside step k+1's panel (programmatic dependent launch); step k+1's
   // candidates get it first (in k_gram).
   // (small problems -- e.g. the 256^2 batch of cfg3 -- are launch-bound: serial form)
-  const bool la = !p->trace_norms && getenv("DMQR_NO_LOOKAHEAD") == nullptr && m * n >= (int64_t)1 << 20;
+  const bool la_all = !p->trace_norms && getenv("DMQR_NO_LOOKAHEAD") == nullptr && m * n >= (int64_t)1 << 20;
 
 
   const int64_t kmax = std::min(m, n);
@@ -284,7 +287,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
     }
   }
   InitArgs ia{ctl, u, perm, coeffs, m, n, lda, kmax, p->tau, p->delta, eps1, p->k_dm, p->use_delta_max,
-              p->break_check, p->trace_norms, swap_cap, step_cap, nonfinite, la ? 1 : 0};
+              p->break_check, p->trace_norms, swap_cap, step_cap, nonfinite, 0};
   k_init<<<1, 1024, 0, st>>>(ia);
   NOTE_LAUNCH();
   CK(cudaGetLastError());
@@ -317,9 +320,20 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
 
   int64_t prev_ns_lo = 0;  // the lower bound the previous step was sized with
+  // Look-ahead runs on the CholeskyQR2-panel steps only (m' <= 16 x 256 rows):
+  // the other panels have no spare SMs to hide the rest of the update behind,
+  // and their norm guards are cheaper on updated columns.  m' only shrinks, so
+  // the schedule switches once, serial -> look-ahead (k_set_la).
+  bool la_on = false;
   auto enqueue_step = [&](int64_t host_ns) -> int {
     const int64_t mp = m - host_ns;
     const int64_t np = n - host_ns;
+    const bool la = la_on || (la_all && use_cq && ceil_div(mp, RR_RMAX) <= max_cluster);
+    if (la && !la_on) {
+      k_set_la<<<1, 32, 0, st>>>(ctl);
+      NOTE_LAUNCH();
+      la_on = true;
+    }
     // ---- selection ----
     PROF(0);
     k_select<<<1, SEL_T, 0, st>>>(ctl, u);
@@ -455,11 +469,11 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
       nsplit = (int)std::min<int64_t>(nsplit, std::max<int64_t>(1, ceil_div(mp, 256)));
       if (spare) {
         k_trail_w<<<(unsigned)ceil_div(ncols_ub, TW_COLS), TA_T, TW_SMEM, st>>>(
-            ctl, A, Zp, red + 19 * DMQR_KP * DMQR_KP, Z, ldz, u, uref, upd);
+            ctl, A, Zp, red + 19 * DMQR_KP * DMQR_KP, Z, ldz, u, uref, upd, glist);
         NOTE_LAUNCH();
       }
       k_trail_a<<<dim3((unsigned)ntile, nsplit), TA_T, TA_SMEM, st>>>(ctl, A, Zp, T, Z, tcount, ldz, u, uref,
-                                                                          upd, spare ? 1 : 0);
+                                                                          upd, spare ? 1 : 0, glist);
       NOTE_LAUNCH();
       if (la) {
         // the rest of C -= Y Wt runs beside the next step's panel
@@ -476,7 +490,10 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
     // ---- norms, log ----
     PROF(3);
     if (la) {
-      // norms: downdated in k_trail_a's epilogue (guard columns recomputed there)
+      // norms: downdated in the Wt epilogues; guard columns recomputed here
+      k_guard<<<(unsigned)std::max<int64_t>(1, ceil_div(mp, GU_ROWS)), GU_T, GU_SMEM, st>>>(
+          ctl, A, Z, ldz, upd, u, uref, glist, lacount + 2);
+      NOTE_LAUNCH();
     } else if (np > 0) {
       const int64_t blocks = std::min<int64_t>(ceil_div(np * 32, 256), (int64_t)d.sms * 16);
       k_downdate<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, uref);
@@ -547,7 +564,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
     ++steps_done;
     if (p->max_steps > 0 && steps_done >= p->max_steps) break;  // debug: stop after N steps
   }
-  if (la && enq > 0) {  // the last step's pending update
+  if (la_on && enq > 0) {  // the last step's pending update
     const int64_t ldz = ldz_for(n);
     k_trail_b<true><<<dim3((unsigned)ceil_div(m - prev_ns_lo + 1, TB_ROWS),
                            (unsigned)std::max<int64_t>(1, ceil_div(n - prev_ns_lo, TB_COLS))),

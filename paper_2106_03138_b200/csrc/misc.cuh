@@ -107,6 +107,7 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
     c->pend = (l > 0 && S.n_s + l < S.m && S.tc0 < S.n) ? 1 : 0;
     c->pend_ns = S.n_s;
     c->pend_l = l;
+    c->gcount = 0;
   }
   c->n_s = S.n_s + l;
   c->step_idx = idx + 1;
@@ -115,6 +116,11 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
   c->nsw = 0;
   c->nmv = 0;
   if (S.n_s + l >= S.kmax) c->done = 1;
+}
+
+// switch the control block to the look-ahead schedule (from the next kernel on)
+__global__ void k_set_la(Ctl* __restrict__ c) {
+  if (threadIdx.x == 0) c->la = 1;
 }
 
 // rank / n_factored (rrqr.py:406-412)

@@ -78,52 +78,6 @@ __device__ void la_panel_columns(Ctl* __restrict__ c, const double* __restrict__
     Wt[(e / (tc0 - base)) * ldz + e % (tc0 - base)] = 0.0;
 }
 
-// Guard columns of a look-ahead tile (downdated square <= 1e-2 u_ref^2): their
-// full update on rows [n_s + l, m) with k_trail_b's DMMA sequence per element
-// (Wt of the tile in zs, ld zld; columns cbase + s_g[q]), then their exact norms.
-__device__ void la_guard_columns(Ctl* __restrict__ c, double* __restrict__ A, double* __restrict__ u,
-                                 double* __restrict__ uref, uint8_t* __restrict__ upd, const double* zs, int zld,
-                                 const int* s_g, int ng, int64_t n_s, int l, int64_t cbase) {
-  if (ng <= 0) return;
-  const int64_t m = c->m, lda = c->lda, n_s1 = n_s + l;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int lp4 = (l + 3) / 4 * 4;
-  const int ngt = (ng + 7) / 8;
-  for (int64_t r8 = n_s1 + 8 * wid; r8 < m; r8 += 8 * nw) {
-    const int64_t r = r8 + (lane >> 2);
-    for (int gt = 0; gt < ngt; ++gt) {
-      double x[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int gq = gt * 8 + 2 * (lane & 3) + h;
-        x[h] = (gq < ng && r < m) ? A[(cbase + s_g[gq]) * lda + r] : 0.0;
-      }
-      for (int ks = 0; ks < lp4; ks += 4) {
-        const int t = ks + (lane & 3);
-        const double a = (t < l && r < m) ? -A[(n_s + t) * lda + r] : 0.0;
-        const int gb = gt * 8 + (lane >> 2);
-        const double b = (gb < ng) ? zs[t * zld + s_g[gb]] : 0.0;
-        dmma884(x[0], x[1], a, b);
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int gq = gt * 8 + 2 * (lane & 3) + h;
-        if (gq < ng && r < m) A[(cbase + s_g[gq]) * lda + r] = x[h];
-      }
-    }
-  }
-  __syncthreads();
-  for (int gq = wid; gq < ng; gq += nw) {
-    const int64_t j = cbase + s_g[gq];
-    const double nu = warp_col_norm(A + j * lda + n_s1, m - n_s1, lane);
-    if (lane == 0) {
-      u[j] = nu;
-      uref[j] = nu;
-      upd[j] = 1;  // (n_s1 < m and tc0 < n here: an update is pending)
-    }
-  }
-}
-
 // Look-ahead tail of a Wt column tile (k_trail_a): zs holds the
 // tile's Wt (rows < lp4, 64 columns, zeros past the last column); ts is
 // scratch.  R12 = C_top - Y1 Wt is written with k_trail_b's DMMA sequence per
@@ -132,7 +86,8 @@ __device__ void la_guard_columns(Ctl* __restrict__ c, double* __restrict__ A, do
 // norm, and tile 0 does the panel-column bookkeeping.
 __device__ void la_tile_epilogue(Ctl* __restrict__ c, double* __restrict__ A, double* __restrict__ Wt, int64_t ldz,
                                  double* __restrict__ u, double* __restrict__ uref, uint8_t* __restrict__ upd,
-                                 const double* zs, double* ts, int64_t n_s, int l, int64_t c0, int64_t col0) {
+                                 const double* zs, double* ts, int64_t n_s, int l, int64_t c0, int64_t col0,
+                                 int32_t* __restrict__ glist) {
   const int64_t m = c->m, n = c->n, lda = c->lda, ncols = n - c0, n_s1 = n_s + l;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int lt = (l + 7) / 8, lp4 = (l + 3) / 4 * 4;
@@ -186,10 +141,6 @@ __device__ void la_tile_epilogue(Ctl* __restrict__ c, double* __restrict__ A, do
   }
 #pragma unroll
   for (int q = 0; q < 8; ++q) d[q] = warp_sum(d[q]);
-  __shared__ int s_ng;
-  __shared__ int s_g[TA_COLS];
-  if (tid == 0) s_ng = 0;
-  __syncthreads();
   if (lane < 8) {
     double dq = d[0];
 #pragma unroll
@@ -200,13 +151,11 @@ __device__ void la_tile_epilogue(Ctl* __restrict__ c, double* __restrict__ A, do
       const double uj = u[j], rj = uref[j];
       const double sq = __dsub_rn(__dmul_rn(uj, uj), dq);
       if (sq <= __dmul_rn(1e-2, __dmul_rn(rj, rj)) && n_s1 < m)
-        s_g[atomicAdd(&s_ng, 1)] = wid * 8 + lane;  // guard: exact norm of the updated column
+        glist[atomicAdd(&c->gcount, 1)] = (int32_t)j;  // guard: k_guard recomputes it
       else
         u[j] = sqrt(fmax(sq, 0.0));
     }
   }
-  __syncthreads();
-  la_guard_columns(c, A, u, uref, upd, zs, TW_LD, s_g, s_ng, n_s, l, c0 + col0);
   if (blockIdx.x == 0) la_panel_columns(c, A, Wt, ldz, u, uref, upd, n_s, l, c0);
 }
 
@@ -217,7 +166,7 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
                                                      double* __restrict__ Wt, unsigned* __restrict__ counters,
                                                      int64_t ldz, double* __restrict__ u,
                                                      double* __restrict__ uref, uint8_t* __restrict__ upd,
-                                                     int only_if_cq_fail) {
+                                                     int only_if_cq_fail, int32_t* __restrict__ glist) {
   const CtlSnap S = snap(c);
   if (S.done || (only_if_cq_fail && !S.cq_fail)) return;  // (k_trail_w did it)
   const int64_t n_s = S.n_s, m = S.m, n = S.n, lda = S.lda;
@@ -372,7 +321,7 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
     zs[i * TW_LD + wid * 8 + 2 * (lane & 3)] = (cc < ncols) ? w[q][0] : 0.0;
     zs[i * TW_LD + wid * 8 + 2 * (lane & 3) + 1] = (cc + 1 < ncols) ? w[q][1] : 0.0;
   }
-  la_tile_epilogue(c, A, Wt, ldz, u, uref, upd, zs, ts, n_s, l, c0, col0);
+  la_tile_epilogue(c, A, Wt, ldz, u, uref, upd, zs, ts, n_s, l, c0, col0, glist);
 }
 
 constexpr int TB_T = 256;     // 8 warps: 4 (rows) x 2 (cols), each 32x32
@@ -728,7 +677,8 @@ constexpr size_t TW_SMEM = sizeof(double) * (3 * DMQR_KP * DMQR_KP + 3 * DMQR_KP
 __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* __restrict__ c, double* __restrict__ A,
                                                   const double* __restrict__ Gp, const double* __restrict__ FM,
                                                   double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
-                                                  double* __restrict__ uref, uint8_t* __restrict__ upd) {
+                                                  double* __restrict__ uref, uint8_t* __restrict__ upd,
+                                                  int32_t* __restrict__ glist) {
   const CtlSnap S = snap(c);
   if (S.done || S.cq_fail) return;
   const int64_t n_s = S.n_s, m = S.m, n = S.n, lda = S.lda;
@@ -822,9 +772,6 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* __restrict__ c, double* _
     }
   __syncthreads();
   // ---- downdate: warp w, columns 4w .. 4w+3 (k_downdate's per-column order) ----
-  __shared__ int s_ng;
-  __shared__ int s_g[TW_COLS];
-  if (tid == 0) s_ng = 0;
   double d[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -847,14 +794,110 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* __restrict__ c, double* _
       const double uj = u[j], rj = uref[j];
       const double sq = __dsub_rn(__dmul_rn(uj, uj), dq);
       if (sq <= __dmul_rn(1e-2, __dmul_rn(rj, rj)) && n_s1 < m)
-        s_g[atomicAdd(&s_ng, 1)] = wid * 4 + lane;
+        glist[atomicAdd(&c->gcount, 1)] = (int32_t)j;  // guard: k_guard recomputes it
       else
         u[j] = sqrt(fmax(sq, 0.0));
     }
   }
-  __syncthreads();
-  la_guard_columns(c, A, u, uref, upd, ws, TW_CLD, s_g, s_ng, n_s, l, c0 + col0);
   if (blockIdx.x == 0) la_panel_columns(c, A, Wt, ldz, u, uref, upd, n_s, l, c0);
+}
+
+// ---------------------------------------------------------------------------
+// Look-ahead guard columns (downdated square <= 1e-2 u_ref^2, listed by the
+// Wt epilogues): their update C -= Y Wt on rows [n_s + l, m) with
+// k_trail_b's DMMA sequence per element, then (last CTA) their exact norms as
+// k_downdate computes them, and the flag that they are done.  One CTA per 64
+// rows, DMMA on 64 x 72 column groups; exits at once when the list is empty.
+// ---------------------------------------------------------------------------
+constexpr int GU_T = 256;
+constexpr int GU_ROWS = 64;
+constexpr int GU_LD = GU_ROWS + 4;  // 4 mod 16
+constexpr size_t GU_SMEM = sizeof(double) * (2 * DMQR_KP * GU_LD + DMQR_KP * DMQR_KP);
+
+__global__ void __launch_bounds__(GU_T) k_guard(Ctl* __restrict__ c, double* __restrict__ A,
+                                                const double* __restrict__ Wt, int64_t ldz,
+                                                uint8_t* __restrict__ upd, double* __restrict__ u,
+                                                double* __restrict__ uref, const int32_t* __restrict__ glist,
+                                                unsigned* __restrict__ counter) {
+  const CtlSnap S = snap(c);
+  const int cnt = c->gcount;
+  if (S.done || cnt == 0) return;
+  const int64_t m = S.m, lda = S.lda, n_s = S.n_s;
+  const int l = S.l_acc;
+  const int64_t base = n_s + l;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  extern __shared__ __align__(16) double gus[];
+  double* ys = gus;                        // ys[t][rr] = Y[r0 + rr][t]
+  double* cs = gus + DMQR_KP * GU_LD;      // cs[q][rr] = C[r0 + rr][col_q]
+  double* ws = gus + 2 * DMQR_KP * GU_LD;  // ws[t][q]  = Wt[t][col_q]
+  __shared__ int s_col[DMQR_KP];
+  const int64_t r0 = base + (int64_t)blockIdx.x * GU_ROWS;
+  const int lp4 = (l + 3) / 4 * 4;
+  if (r0 < m) {
+    const int nr = (int)min((int64_t)GU_ROWS, m - r0);
+    for (int e = tid; e < lp4 * GU_ROWS; e += GU_T) {
+      const int t = e / GU_ROWS, rr = e % GU_ROWS;
+      ys[t * GU_LD + rr] = (t < l && rr < nr) ? A[(n_s + t) * lda + r0 + rr] : 0.0;
+    }
+    for (int g0 = 0; g0 < cnt; g0 += DMQR_KP) {
+      const int ng = min(DMQR_KP, cnt - g0);
+      if (tid < DMQR_KP) s_col[tid] = (tid < ng) ? glist[g0 + tid] : -1;
+      __syncthreads();
+      for (int e = tid; e < lp4 * DMQR_KP; e += GU_T) {
+        const int t = e / DMQR_KP, q = e % DMQR_KP;
+        const int j = s_col[q];
+        ws[t * DMQR_KP + q] = (t < l && j >= 0) ? Wt[t * ldz + (j - base)] : 0.0;
+      }
+      for (int e = tid; e < DMQR_KP * GU_ROWS; e += GU_T) {
+        const int q = e / GU_ROWS, rr = e % GU_ROWS;
+        const int j = s_col[q];
+        cs[q * GU_LD + rr] = (j >= 0 && rr < nr) ? A[(int64_t)j * lda + r0 + rr] : 0.0;
+      }
+      __syncthreads();
+      const int rr = wid * 8 + (lane >> 2);
+      double acc[DMQR_KP / 8][2];
+#pragma unroll
+      for (int q = 0; q < DMQR_KP / 8; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) acc[q][h] = cs[(q * 8 + 2 * (lane & 3) + h) * GU_LD + rr];
+      for (int ks = 0; ks < lp4; ks += 4) {
+        const int t = ks + (lane & 3);
+        const double a = -ys[t * GU_LD + rr];
+#pragma unroll
+        for (int q = 0; q < DMQR_KP / 8; ++q) dmma884(acc[q][0], acc[q][1], a, ws[t * DMQR_KP + q * 8 + (lane >> 2)]);
+      }
+      if (rr < nr) {
+#pragma unroll
+        for (int q = 0; q < DMQR_KP / 8; ++q)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int qq = q * 8 + 2 * (lane & 3) + h;
+            const int j = s_col[qq];
+            if (j >= 0) A[(int64_t)j * lda + r0 + rr] = acc[q][h];
+          }
+      }
+      __syncthreads();
+    }
+  }
+  __shared__ int s_last;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (tid == 0) *counter = 0u;
+  for (int q = wid; q < cnt; q += GU_T / 32) {
+    const int64_t j = glist[q];
+    const double nu = warp_col_norm(A + j * lda + base, m - base, lane);
+    if (lane == 0) {
+      u[j] = nu;
+      uref[j] = nu;
+      upd[j] = 1;  // (an update is pending: guards exist only with rows below and tiles past tc0)
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
