@@ -172,3 +172,39 @@ def test_batched_equals_single_and_oracle():
         with threadpool_limits(1):
             ref = O.qrdm2(B[i], margins=True)
         _compare(B[i], r, ref, f"cfg3[{i}]")
+
+
+def test_streamed_packed_equals_device_copy():
+    """dmqr_qrdm_stream_f64 (the qrdm2 default) hands back the same packed factor
+    as a device-side result copied afterwards."""
+    from paper_2106_03138_b200 import qrdm2
+
+    rng = np.random.default_rng(21)
+    A = rng.standard_normal((1200, 1000))
+    a = qrdm2(A)
+    b = qrdm2(A, device=True)
+    assert np.array_equal(a.packed, b.packed.cpu().numpy())
+    assert np.array_equal(a.perm.forward, b.perm.forward)
+
+
+@pytest.mark.parametrize("shape", [(1100, 1000), (6000, 700)])
+def test_lookahead_matches_serial_schedule(shape, monkeypatch):
+    """The look-ahead schedule (panel || rest of the previous update, Wt from
+    G = Q1^T C) against the serial one on the same input: identical decisions,
+    factors equal to rounding.  (6000 rows starts on the Householder panel and
+    switches schedule once m' <= 4096.)"""
+    from paper_2106_03138_b200 import qrdm2
+
+    rng = np.random.default_rng(22)
+    m, n = shape
+    A = rng.standard_normal((m, n)) * np.logspace(0, -3, n)[rng.permutation(n)]
+    la = qrdm2(A)
+    monkeypatch.setenv("DMQR_NO_LOOKAHEAD", "1")
+    se = qrdm2(A)
+    assert np.array_equal(la.perm.forward, se.perm.forward) and la.rank == se.rank
+    assert [(s.n_s, s.k_selected, s.k_accepted) for s in la.step_log] == \
+        [(s.n_s, s.k_selected, s.k_accepted) for s in se.step_log]
+    scale = np.abs(se.packed).max()
+    assert np.abs(la.packed - se.packed).max() <= 1e-10 * scale
+    resid, orth = parity.residuals(A, la)
+    assert resid <= 50 * max(m, n) * O.EPS and orth <= 50 * max(m, n) * O.EPS
