@@ -24,6 +24,8 @@ struct Ctl {
   // loop state
   int32_t n_s, done, stopped, status;
   int32_t step_idx, n_swaps, rank, n_factored;
+  int32_t la_bad;  // look-ahead meets many norm guards here (graded / tall input): host goes serial
+  int32_t pad4;
   // current step decision
   int32_t kind;   // 0 = deviation-maximization step, 1 = scalar fallback
   int32_t k_max;  // candidate-set size (dm.py:97), -1 on fallback
@@ -47,11 +49,13 @@ struct Ctl {
   // pending (pend) for every trailing column not flagged in the per-column
   // `upd` bytes; snapshot of that step (its n_s and accepted reflectors)
   int32_t la, pend, pend_ns, pend_l;
-  int32_t gcount;   // (unused)
+  int32_t gcount;   // look-ahead guard columns of the current step (k_guard's list)
   // the CholeskyQR2 panel publishes Q1 = P R1^-1 for the spare-SM G = Q1^T C:
   // q1_count CTAs have written their rows (q1_fail: no usable Q1 this step)
   uint32_t q1_count;
   int32_t q1_fail, q1_kk;
+  int32_t pend_done;  // k_guard finished the whole update of this step (nothing pending)
+  int32_t pad3;
   // inter-CTA counters (reset by their users)
   uint32_t gram_count;
   uint32_t bar_count;

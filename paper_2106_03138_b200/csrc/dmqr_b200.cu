@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstddef>
 #include <cstring>
 
 #include "../../include/dmqr_b200.h"
@@ -61,7 +62,7 @@ Layout layout(int64_t m, int64_t n) {
   L.uref = take(sizeof(double) * std::max<int64_t>(n, 1));
   L.T = take(sizeof(double) * DMQR_KP * DMQR_KP);
   // panel all-reduce partials; the CholeskyQR2 panel also keeps R, Y1 and per-rank R = R2 R1 here
-  L.red = take(sizeof(double) * std::max<size_t>(2 * PANEL_PMAX * RED_LD, 21 * DMQR_KP * DMQR_KP));
+  L.red = take(sizeof(double) * std::max<size_t>(2 * PANEL_PMAX * RED_LD, 37 * DMQR_KP * DMQR_KP));
   L.gram = take(sizeof(double) * GRAM_GMAX * GRAM_PART);
   L.gfin = take(sizeof(double) * DMQR_KP * DMQR_KP);
   L.Zp = take(sizeof(double) * NSPLIT_MAX * DMQR_KP * ldz_for(n));
@@ -177,7 +178,10 @@ ProfAcc g_acc;  // guarded by the caller (bench) using one thread
 
 struct HostHead {  // the prefix of Ctl the host polls
   int32_t n_s, done, stopped, status;
+  int32_t step_idx, n_swaps, rank, n_factored;
+  int32_t la_bad, pad4;
 };
+static_assert(offsetof(Ctl, la_bad) - offsetof(Ctl, n_s) == offsetof(HostHead, la_bad), "HostHead mirrors Ctl");
 
 }  // namespace
 
@@ -261,7 +265,9 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
   // runs beside step k+1's panel (programmatic dependent launch); step k+1's
   // candidates get it first (in k_gram).
   // (small problems -- e.g. the 256^2 batch of cfg3 -- are launch-bound: serial form)
-  const bool la_all = !p->trace_norms && getenv("DMQR_NO_LOOKAHEAD") == nullptr && m * n >= (int64_t)1 << 20;
+  // (tall inputs -- m > 4n, like cfg4 -- hit norm guards too often: serial)
+  const bool la_all = !p->trace_norms && getenv("DMQR_NO_LOOKAHEAD") == nullptr && m * n >= (int64_t)1 << 20 &&
+                      m <= 4 * n;
 
 
   const int64_t kmax = std::min(m, n);
@@ -320,17 +326,30 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
 
   int64_t prev_ns_lo = 0;  // the lower bound the previous step was sized with
-  // Look-ahead runs on the CholeskyQR2-panel steps only (m' <= 16 x 256 rows):
-  // the other panels have no spare SMs to hide the rest of the update behind,
-  // and their norm guards are cheaper on updated columns.  m' only shrinks, so
-  // the schedule switches once, serial -> look-ahead (k_set_la).
-  bool la_on = false;
+  // Look-ahead runs on the CholeskyQR2-panel steps (all of them unless the
+  // Householder panel is forced): the other panels have no spare SMs to hide
+  // the rest of the update behind.  Once on, it stays on
+  // (k_set_la switches the control block).
+  // The look-ahead pays off when norm guards are rare; k_guard flags a step
+  // that needed one for most trailing columns (la_bad, with nothing left
+  // pending), and the host then stays serial: flush + k_set_la(0).
+  bool la_on = false, la_off = false, want_serial = false;
   auto enqueue_step = [&](int64_t host_ns) -> int {
     const int64_t mp = m - host_ns;
     const int64_t np = n - host_ns;
-    const bool la = la_on || (la_all && use_cq && ceil_div(mp, RR_RMAX) <= max_cluster);
+    if (la_on && want_serial && !la_off) {
+      const int64_t ldz0 = ldz_for(n);
+      k_trail_b<true><<<dim3((unsigned)ceil_div(m - prev_ns_lo + 1, TB_ROWS),
+                             (unsigned)std::max<int64_t>(1, ceil_div(n - prev_ns_lo, TB_COLS))),
+                        TB_T, TB_SMEM, st>>>(ctl, A, Z, ldz0, upd, lacount + 1);
+      NOTE_LAUNCH();
+      k_set_la<<<1, 32, 0, st>>>(ctl, 0);
+      NOTE_LAUNCH();
+      la_off = true;
+    }
+    const bool la = !la_off && (la_on || (la_all && use_cq));
     if (la && !la_on) {
-      k_set_la<<<1, 32, 0, st>>>(ctl);
+      k_set_la<<<1, 32, 0, st>>>(ctl, 1);
       NOTE_LAUNCH();
       la_on = true;
     }
@@ -397,7 +416,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
     const int G = cl_path ? P : ((P > 1) ? P + 1 : 1);
     PanelArgs pa{ctl, A, coeffs, T, red, use_smem, P,
                  (g_prof.load() >= 2 && steps_done == 2) ? pdbg : nullptr, std::max(0, g_prof.load() - 2), 0,
-                 nullptr};
+                 q1g, 0};
     void* kargs[] = {&pa};
     auto launch_cluster = [&](const void* fn, int ncta, unsigned threads, size_t dsm) -> cudaError_t {
       cudaLaunchConfig_t cfg = {};
@@ -416,23 +435,25 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
     };
     // CholeskyQR2 panel (one cluster, <= 256 rows per CTA) first; the Householder
     // kernels behind it run only if it declined (ill-conditioned panel)
-    const bool cq_path = use_cq && Prr <= max_cluster;
+    // (more than max_cluster x 256 rows: the cluster streams its rows in chunks)
+    const bool cq_path = use_cq;
+    const int Pcq = (int)std::min<int64_t>(Prr, max_cluster);
     const bool spare = la && cq_path;  // k_spare beside the panel, then k_trail_w
     const int64_t ntile_g = std::max<int64_t>(1, ceil_div(np, TA_COLS));
     const int nsplit_g = (int)std::min<int64_t>(
-        std::clamp<int64_t>(ceil_div(2 * (d.sms - Prr), ntile_g), 1, NSPLIT_MAX), std::max<int64_t>(1, ceil_div(mp, 256)));
+        std::clamp<int64_t>(ceil_div(2 * (d.sms - Pcq), ntile_g), 1, NSPLIT_MAX), std::max<int64_t>(1, ceil_div(mp, 256)));
     if (la_rest && !cq_path) CK(launch_la_rest(false));
     if (cq_path) {
-      pa.q1g = spare ? q1g : nullptr;
-      CK(launch_cluster((const void*)k_panel_cq, Prr, PANEL_T, CQ_SMEM));
+      pa.spare = spare ? 1 : 0;
+      CK(launch_cluster((const void*)k_panel_cq, Pcq, PANEL_T, CQ_SMEM));
       NOTE_LAUNCH();
       pa.only_if_fail = 1;
-      pa.q1g = nullptr;
+      pa.spare = 0;
       if (spare) {
         cudaLaunchConfig_t cfg = {};
         // persistent CTAs: two per SM the panel leaves free, but no more than work items
         const int64_t items = (int64_t)lag.x * lag.y * (la_rest ? 1 : 0) + ntile_g * nsplit_g;
-        cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(2 * std::max(1, d.sms - Prr), items)));
+        cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(2 * std::max(1, d.sms - Pcq), items)));
         cfg.blockDim = dim3(TB_T);
         cfg.dynamicSmemBytes = SP_SMEM;
         cfg.stream = st;
@@ -443,7 +464,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
         cfg.numAttrs = 1;
         NOTE_LAUNCH();
         CK(cudaLaunchKernelEx(&cfg, k_spare, ctl, A, (const double*)Z, ldz, upd, (const double*)q1g, Zp,
-                              lacount + 4, Prr, nsplit_g, tcount));
+                              lacount + 4, Pcq, nsplit_g, tcount));
       }
     }
     if (cl_path) {
@@ -491,8 +512,9 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
     PROF(3);
     if (la) {
       // norms: downdated in the Wt epilogues; guard columns recomputed here
-      k_guard<<<(unsigned)std::max<int64_t>(1, ceil_div(mp, GU_ROWS)), GU_T, GU_SMEM, st>>>(
-          ctl, A, Z, ldz, upd, u, uref, glist, lacount + 2);
+      k_guard<<<dim3((unsigned)std::max<int64_t>(1, ceil_div(mp, GU_ROWS)),
+                     (unsigned)std::max<int64_t>(1, ceil_div(np, GU_GROUPS * DMQR_KP))),
+                GU_T, GU_SMEM, st>>>(ctl, A, Z, ldz, upd, u, uref, glist, lacount + 2);
       NOTE_LAUNCH();
     } else if (np > 0) {
       const int64_t blocks = std::min<int64_t>(ceil_div(np * 32, 256), (int64_t)d.sms * 16);
@@ -540,6 +562,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
     known_ns = hh[sl].n_s;
     ++known;
     if (hh[sl].done) finished = true;
+    if (hh[sl].la_bad) want_serial = true;
     return stream_cols(known_ns, hev[sl]);  // columns left of n_s are final
   };
   while (!finished) {

@@ -104,7 +104,8 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
     *trace_bits = 0ull;
   }
   if (S.la) {  // this step's update is now pending below its R rows (look-ahead)
-    c->pend = (l > 0 && S.n_s + l < S.m && S.tc0 < S.n) ? 1 : 0;
+    c->pend = (l > 0 && S.n_s + l < S.m && S.tc0 < S.n && !c->pend_done) ? 1 : 0;
+    c->pend_done = 0;
     c->pend_ns = S.n_s;
     c->pend_l = l;
     c->gcount = 0;
@@ -119,8 +120,8 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
 }
 
 // switch the control block to the look-ahead schedule (from the next kernel on)
-__global__ void k_set_la(Ctl* __restrict__ c) {
-  if (threadIdx.x == 0) c->la = 1;
+__global__ void k_set_la(Ctl* __restrict__ c, int on) {
+  if (threadIdx.x == 0) c->la = on;
 }
 
 // rank / n_factored (rrqr.py:406-412)

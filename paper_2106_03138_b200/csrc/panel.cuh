@@ -128,7 +128,8 @@ struct PanelArgs {
   long long* dbg;  // optional phase clocks of CTA dbg_cta (debug builds of the benchmark only)
   int dbg_cta;
   int only_if_fail;  // Householder fallback behind the CholeskyQR2 panel: run only if it declined
-  double* q1g;       // CholeskyQR2 panel: publish Q1 here for k_spare (look-ahead), or null
+  double* q1g;       // CholeskyQR2 panel: Q1 buffer (chunked panels; read by k_spare under look-ahead)
+  int spare;         // look-ahead: release k_spare, publish the Wt factors for k_trail_w
 };
 
 // deterministic all-reduce of `len` doubles across the grid; in: s_part (this
@@ -176,7 +177,10 @@ __device__ __forceinline__ void block_sum_into(double v, double* wscr, double* d
 
 __global__ void __launch_bounds__(PANEL_T, 1) k_panel(PanelArgs a) {
   Ctl* c = a.c;
-  if (c->done) return;
+  {
+    const int done = c->done, cqf = c->cq_fail;  // (the CholeskyQR2 panel may have done the step)
+    if (done || (a.only_if_fail && !cqf)) return;
+  }
   extern __shared__ __align__(16) double psm[];
   __shared__ double s_part[RED_LD];
   __shared__ double s_tot[RED_LD];

@@ -557,15 +557,41 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
 #define CQT() \
   if (rec) a.dbg[ts++] = clock64()
   CQT();
-  // ---- P0: slice <- P (rows zero-padded to a multiple of 4) ----
-  for (int e = tid; e < k * R4; e += PANEL_T) {
-    const int cc = e / R4, rr = e % R4;
-    sl[cc * CQ_LDS + rr] = (rr < R) ? gA[(int64_t)cc * lda + rr] : 0.0;
+  // Rows per CTA beyond CQ_RMAX (m' > 16 x 256): the slice streams through
+  // shared memory in chunks of CQ_RMAX rows; Q1 then lives in the published
+  // buffer (q1g) and each pass over the rows reloads its chunks.
+  const int nch = (R + CQ_RMAX - 1) / CQ_RMAX;
+  const bool chunked = nch > 1;
+  const int64_t ldq = q1_ld(m);
+  const int qodd = (int)(n_s & 1);
+  auto load_chunk = [&](const double* src, int64_t ld, int ch, int ncol) {  // rows of chunk ch -> sl
+    const int c0r = ch * CQ_RMAX, cR = min(CQ_RMAX, R - c0r), cR4 = (cR + 3) & ~3;
+    for (int e = tid; e < ncol * cR4; e += PANEL_T) {
+      const int cc = e / cR4, rr = e % cR4;
+      sl[cc * CQ_LDS + rr] = (rr < cR) ? src[(int64_t)cc * ld + c0r + rr] : 0.0;
+    }
+    __syncthreads();
+    return cR4;
+  };
+  double* gacc = a.red + 3 * DMQR_KP * DMQR_KP + (size_t)blockIdx.x * DMQR_KP * DMQR_KP;  // per-CTA scratch
+  double* vQ = a.red + 21 * DMQR_KP * DMQR_KP + (size_t)blockIdx.x * DMQR_KP * DMQR_KP;    // per-CTA scratch
+  // ---- P0/P1: slice <- P (rows zero-padded to a multiple of 4), G = P^T P ----
+  if (!chunked) {
+    load_chunk(gA, lda, 0, k);
+    CQT();
+    cq_gram(sl, R4, k, A2);
+  } else {
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) A2[e] = 0.0;
+    CQT();
+    for (int ch = 0; ch < nch; ++ch) {
+      const int cR4 = load_chunk(gA, lda, ch, k);
+      cq_gram(sl, cR4, k, A1);
+      __syncthreads();
+      for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T)  // upper tiles written by cq_gram
+        if ((e % DMQR_KP) / 8 >= (e / DMQR_KP) / 8) A2[e] += A1[e];
+      __syncthreads();
+    }
   }
-  __syncthreads();
-  // ---- P1/P2: G = P^T P ----
-  CQT();
-  cq_gram(sl, R4, k, A2);
   CQT();
   cq_cluster_reduce(A2, A1, k);
   CQT();
@@ -583,27 +609,18 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     const double bound = 1e-3 * sqrt(vpiv[DMQR_KP + jstar]);
     if (!brk || jstar == 0 || !(bound < eps_s)) fail = true;
   }
-  const int qodd = (int)(n_s & 1);
-  const bool q1_pub = a.q1g != nullptr && !fail && kk > 0;
+  const bool q1_pub = a.spare && !fail && kk > 0;
+  auto store_q1 = [&](int ch) {  // sl rows of chunk ch -> q1g (the row parity of A)
+    const int c0r = ch * CQ_RMAX, cR = min(CQ_RMAX, R - c0r);
+    for (int e = tid; e < kk * cR; e += PANEL_T) {
+      const int cc = e / cR, rr = e % cR;
+      a.q1g[(int64_t)cc * ldq + qodd + r0 + c0r + rr] = sl[cc * CQ_LDS + rr];
+    }
+  };
   if (!fail && kk > 0) {
     // ---- P4/P5: Q1 = P R1^-1 (in place) ----
     cq_trinv_upper(A2, A1, kk);
     CQT();
-    cq_slice_gemm(sl, R4, kk, kk, A1);
-    CQT();
-    if (q1_pub) {  // publish this rank's Q1 rows for the spare-SM G = Q1^T C (k_spare)
-      __syncthreads();
-      for (int e = tid; e < kk * R; e += PANEL_T) {
-        const int cc = e / R, rr = e % R;
-        a.q1g[(int64_t)cc * q1_ld(m) + qodd + r0 + rr] = sl[cc * CQ_LDS + rr];
-      }
-      __syncthreads();
-      if (tid == 0) {
-        c->q1_kk = kk;
-        __threadfence();
-        atomicAdd(&c->q1_count, 1u);
-      }
-    }
     // keep R1: transpose into the lower triangle of A2, diagonal in vD
     __syncthreads();
     for (int e = tid; e < kk * kk; e += PANEL_T) {
@@ -612,8 +629,39 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       if (i == j) vD[i] = A2[i * DMQR_KP + i];
     }
     __syncthreads();
-    // ---- P6/P7: G2 = Q1^T Q1 (partial -> A1, total -> upper A2) ----
-    cq_gram(sl, R4, kk, A1);
+    if (!chunked) {
+      cq_slice_gemm(sl, R4, kk, kk, A1);
+      CQT();
+      if (q1_pub) {  // publish this rank's Q1 rows for the spare-SM G = Q1^T C (k_spare)
+        __syncthreads();
+        store_q1(0);
+      }
+      __syncthreads();
+      // ---- P6/P7: G2 = Q1^T Q1 (partial -> A1, total -> upper A2) ----
+      cq_gram(sl, R4, kk, A1);
+    } else {
+      // per chunk: Q1 = P R1^-1 -> q1g; the Q1 Gram accumulates in global scratch
+      for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) gacc[e] = 0.0;
+      for (int ch = 0; ch < nch; ++ch) {
+        const int cR4 = load_chunk(gA, lda, ch, kk);
+        cq_slice_gemm(sl, cR4, kk, kk, A1);
+        __syncthreads();
+        store_q1(ch);
+        cq_gram(sl, cR4, kk, vQ);
+        __syncthreads();
+        for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T)
+          if ((e % DMQR_KP) / 8 >= (e / DMQR_KP) / 8) gacc[e] += vQ[e];
+        __syncthreads();
+      }
+      CQT();
+      for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) A1[e] = gacc[e];
+      __syncthreads();
+    }
+    if (q1_pub && tid == 0) {
+      c->q1_kk = kk;
+      __threadfence();
+      atomicAdd(&c->q1_count, 1u);
+    }
     // zero the upper of A2 (incl. diag) on this rank first: reduce writes it
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
       const int i = e / DMQR_KP, j = e % DMQR_KP;
@@ -641,7 +689,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     if (s_flag[0]) fail = true;
   }
   if (me == 0 && tid == 0) c->cq_diag[3] = jstar;
-  if (a.q1g != nullptr && !q1_pub && tid == 0) {  // nothing to publish: release k_spare
+  if (a.spare && !q1_pub && tid == 0) {  // nothing to publish: release k_spare
     c->q1_fail = 1;
     __threadfence();
     atomicAdd(&c->q1_count, 1u);
@@ -755,8 +803,12 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     if (!m_on_1)
       for (int e = tid; e < l * l; e += PANEL_T) gR2i[(e / l) * DMQR_KP + e % l] = A2[(e / l) * DMQR_KP + e % l];
     // ---- P12: top l x l block of Q = Q1 R2^-1 -> A1 ----
-    cq_small_gemm<true>([&](int i, int t) { return sl[t * CQ_LDS + i]; },
-                        [&](int t, int j) { return A2[t * DMQR_KP + j]; }, A1, l);
+    if (!chunked)
+      cq_small_gemm<true>([&](int i, int t) { return sl[t * CQ_LDS + i]; },
+                          [&](int t, int j) { return A2[t * DMQR_KP + j]; }, A1, l);
+    else  // (rank 0's first rows, published)
+      cq_small_gemm<true>([&](int i, int t) { return a.q1g[(int64_t)t * ldq + qodd + i]; },
+                          [&](int t, int j) { return A2[t * DMQR_KP + j]; }, A1, l);
     __syncthreads();
     CQT();
     // ---- P13: modified LU of the top block: strict lower = L (Y1), upper = q' ----
@@ -841,28 +893,42 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   cl.sync();
   // ---- P16: Y = Q1 M on this rank's rows (rank 0's rows < l are fixed below) ----
   CQT();
-  cq_slice_gemm(sl, R4, l, l, A2);
-  CQT();
-  __syncthreads();
-  // ---- write back: Y below the diagonal, R_H = S R on and above it (rows < l live on rank 0) ----
-  for (int e = tid; e < l * R; e += PANEL_T) {
-    const int cc = e / R, rr = e % R;
-    const int p = r0 + rr;  // panel row
-    double v;
-    if (p > cc) {
-      if (p < l) {  // Y1 (unit lower) multipliers saved by rank 0
-        v = a.red[2 * DMQR_KP * DMQR_KP + p * DMQR_KP + cc];
+  auto write_back = [&](int c0r, int cR) {
+    // Y below the diagonal, R_H = S R on and above it (rows < l live on rank 0)
+    for (int e = tid; e < l * cR; e += PANEL_T) {
+      const int cc = e / cR, rr = e % cR;
+      const int p = r0 + c0r + rr;  // panel row
+      double v;
+      if (p > cc) {
+        if (p < l) {  // Y1 (unit lower) multipliers saved by rank 0
+          v = a.red[2 * DMQR_KP * DMQR_KP + p * DMQR_KP + cc];
+        } else {
+          v = sl[cc * CQ_LDS + rr];
+        }
       } else {
-        v = sl[cc * CQ_LDS + rr];
+        v = vS[p] * a.red[p * DMQR_KP + cc];  // R_H = S R
       }
-    } else {
-      v = vS[p] * a.red[p * DMQR_KP + cc];  // R_H = S R
+      gA[(int64_t)cc * lda + c0r + rr] = v;
     }
-    gA[(int64_t)cc * lda + rr] = v;
+  };
+  if (chunked) {
+    for (int ch = 0; ch < nch; ++ch) {
+      const int cR4 = load_chunk(a.q1g + qodd + r0, ldq, ch, l);
+      cq_slice_gemm(sl, cR4, l, l, A2);
+      __syncthreads();
+      write_back(ch * CQ_RMAX, min(CQ_RMAX, R - ch * CQ_RMAX));
+      __syncthreads();
+    }
+  } else {
+    cq_slice_gemm(sl, R4, l, l, A2);
   }
   CQT();
+  __syncthreads();
+  // ---- write back ----
+  if (!chunked) write_back(0, R);
+  CQT();
 #undef CQT
-  if (me == 0 && a.q1g != nullptr) {
+  if (me == 0 && a.spare) {
     // k_trail_w forms Wt = T^T (E C_top + M^T G) from G = Q1^T C, with
     // E = F^T, F = Y1 - Q1_top M (both l x l)
     __syncthreads();

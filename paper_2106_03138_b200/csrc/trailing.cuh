@@ -813,6 +813,7 @@ constexpr int GU_T = 256;
 constexpr int GU_ROWS = 64;
 constexpr int GU_LD = GU_ROWS + 4;  // 4 mod 16
 constexpr size_t GU_SMEM = sizeof(double) * (2 * DMQR_KP * GU_LD + DMQR_KP * DMQR_KP);
+constexpr int GU_GROUPS = 4;  // column groups of 72 per CTA (grid.y spreads the rest)
 
 __global__ void __launch_bounds__(GU_T) k_guard(Ctl* __restrict__ c, double* __restrict__ A,
                                                 const double* __restrict__ Wt, int64_t ldz,
@@ -825,6 +826,11 @@ __global__ void __launch_bounds__(GU_T) k_guard(Ctl* __restrict__ c, double* __r
   const int64_t m = S.m, lda = S.lda, n_s = S.n_s;
   const int l = S.l_acc;
   const int64_t base = n_s + l;
+  // many guard columns (graded / tall matrices): finish this step's whole
+  // update now -- every column not yet updated -- and leave nothing pending
+  const int64_t ntr = S.n - base;
+  const bool full = (int64_t)cnt * 8 > ntr;
+  const int nlist = full ? (int)ntr : cnt;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   extern __shared__ __align__(16) double gus[];
   double* ys = gus;                        // ys[t][rr] = Y[r0 + rr][t]
@@ -839,9 +845,18 @@ __global__ void __launch_bounds__(GU_T) k_guard(Ctl* __restrict__ c, double* __r
       const int t = e / GU_ROWS, rr = e % GU_ROWS;
       ys[t * GU_LD + rr] = (t < l && rr < nr) ? A[(n_s + t) * lda + r0 + rr] : 0.0;
     }
-    for (int g0 = 0; g0 < cnt; g0 += DMQR_KP) {
-      const int ng = min(DMQR_KP, cnt - g0);
-      if (tid < DMQR_KP) s_col[tid] = (tid < ng) ? glist[g0 + tid] : -1;
+    // blockIdx.y: a range of GU_GROUPS column groups of the list
+    const int gbeg = blockIdx.y * GU_GROUPS * DMQR_KP, gend = min(nlist, gbeg + GU_GROUPS * DMQR_KP);
+    for (int g0 = gbeg; g0 < gend; g0 += DMQR_KP) {
+      const int ng = min(DMQR_KP, gend - g0);
+      if (tid < DMQR_KP) {
+        int j = -1;
+        if (tid < ng) {
+          j = full ? (int)(base + g0 + tid) : glist[g0 + tid];
+          if (full && upd[j]) j = -1;  // (the panel's own columns: already final)
+        }
+        s_col[tid] = j;
+      }
       __syncthreads();
       for (int e = tid; e < lp4 * DMQR_KP; e += GU_T) {
         const int t = e / DMQR_KP, q = e % DMQR_KP;
@@ -883,20 +898,28 @@ __global__ void __launch_bounds__(GU_T) k_guard(Ctl* __restrict__ c, double* __r
   __syncthreads();
   if (tid == 0) {
     __threadfence();
-    s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    s_last = (atomicAdd(counter, 1u) == gridDim.x * gridDim.y - 1);
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (tid == 0) *counter = 0u;
+  if (tid == 0) {
+    *counter = 0u;
+    if (full) c->pend_done = 1;      // k_step_end: nothing is pending after this step
+    if (full || cnt > 32) c->la_bad = 1;  // guards are not rare here: the host goes serial
+  }
   for (int q = wid; q < cnt; q += GU_T / 32) {
     const int64_t j = glist[q];
     const double nu = warp_col_norm(A + j * lda + base, m - base, lane);
     if (lane == 0) {
       u[j] = nu;
       uref[j] = nu;
-      upd[j] = 1;  // (an update is pending: guards exist only with rows below and tiles past tc0)
+      if (!full) upd[j] = 1;  // (an update is pending: guards exist only with rows below and tiles past tc0)
     }
+  }
+  if (full) {
+    __syncthreads();
+    for (int64_t j = tid; j < S.n; j += GU_T) upd[j] = 0;
   }
 }
 
