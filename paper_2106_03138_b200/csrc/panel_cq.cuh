@@ -263,6 +263,57 @@ __device__ void cq_trinv_upper(const double* U, double* X, int n, int xr = DMQR_
   CQ_TICK(3);
 }
 
+// In place X <- X U^-1 for upper triangular U (leading n x n of a KP
+// row-major array; UNIT: unit diagonal, not read): solves X U = B for X.
+// X[i][j] at X[i*xr + j*xc].  Blocked by 8 columns: the block column takes the
+// update from the columns left of it on DMMA (warp per 8-row tile), then each
+// row solves its 8 x 8 triangle (thread per row) -- no inverse, no scratch.
+template <bool UNIT>
+__device__ void cq_trsm_right_upper(double* X, const double* U, int n, int xr, int xc) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const int nb = (n + 7) / 8, lr = lane >> 2, lk = lane & 3;
+  __shared__ double s_rd[DMQR_KP];
+  if (!UNIT)
+    for (int i = tid; i < n; i += blockDim.x) s_rd[i] = 1.0 / U[i * DMQR_KP + i];
+  __syncthreads();
+  for (int J = 0; J < nb; ++J) {
+    const int c0 = J * 8;
+    if (J > 0)
+      for (int rt = wid; rt < nb; rt += nw) {  // X[:, J] -= X[:, <J] U[<J, J]
+        const int r = rt * 8 + lr;
+        double a0 = 0.0, a1 = 0.0;
+        for (int k0 = 0; k0 < c0; k0 += 4) {
+          const int k = k0 + lk;
+          const double av = (r < n) ? X[r * xr + k * xc] : 0.0;
+          const int cc = c0 + lr;
+          const double bv = (cc < n) ? U[k * DMQR_KP + cc] : 0.0;
+          dmma884(a0, a1, av, bv);
+        }
+        const int oc = c0 + 2 * lk;
+        if (r < n && oc < n) X[r * xr + oc * xc] -= a0;
+        if (r < n && oc + 1 < n) X[r * xr + (oc + 1) * xc] -= a1;
+      }
+    __syncthreads();
+    for (int r = tid; r < n; r += blockDim.x) {  // the 8 x 8 triangle, row r
+      double x[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int cj = c0 + j;
+        if (cj < n) {
+          double b = X[r * xr + cj * xc];
+#pragma unroll
+          for (int t = 0; t < j; ++t) b -= x[t] * U[(c0 + t) * DMQR_KP + cj];
+          x[j] = UNIT ? b : b * s_rd[cj];
+          X[r * xr + cj * xc] = x[j];
+        } else {
+          x[j] = 0.0;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // 1/x for x in [1, 2] (modified-LU pivots): MUFU estimate + two Newton steps
 __device__ __forceinline__ double cq_rcp12(double x) {
   double y;
@@ -839,12 +890,19 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   }
   cl.sync();  // U and S ready on rank 0
   if (me == 0) {
-    // Z = (Y1^T)^-1 into the top l x l block of the slice (rows < l of Y come
-    // from Y1 at write-back), Z[i][j] at sl[j*LDS + i]
-    cq_trinv_upper(A1, sl, l, 1, CQ_LDS);
-    // T = U Z (householder.py accumulate_wy's W), tau_j = U_jj
-    cq_small_gemm([&](int i, int t) { return A2[i * DMQR_KP + t]; },
-                  [&](int t, int j) { return sl[j * CQ_LDS + t]; }, a.T, l);
+    // T = U (Y1^T)^-1 (householder.py accumulate_wy's W), tau_j = U_jj: U copied
+    // into the top l x l block of the slice (rows < l of Y come from Y1 at
+    // write-back), then T Y1^T = U solved in place
+    for (int e = tid; e < l * l; e += PANEL_T) {
+      const int i = e / l, j = e % l;
+      sl[j * CQ_LDS + i] = A2[i * DMQR_KP + j];
+    }
+    __syncthreads();
+    cq_trsm_right_upper<true>(sl, A1, l, 1, CQ_LDS);
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int i = e / DMQR_KP, j = e % DMQR_KP;
+      a.T[e] = (i < l && j < l && j >= i) ? sl[j * CQ_LDS + i] : 0.0;
+    }
     for (int j = tid; j < l; j += PANEL_T) a.coeffs[n_s + j] = vpiv[j];
     __syncthreads();
     if (!m_on_1) {
@@ -857,7 +915,8 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     }
     CQT();
   } else if (me == 1) {
-    // pull U (upper of rank 0's A2) and S, then U^-1 -> global scratch, M -> A1
+    // pull U (upper of rank 0's A2) and S; M = -R2^-1 S U^-1 by solving
+    // M U = -R2^-1 S in place (R2^-1 in A2 from above)
     const double* A2r = cl.map_shared_rank(A2, 0);
     const double* vSr = cl.map_shared_rank(vS, 0);
     for (int e = tid; e < l * l; e += PANEL_T) {
@@ -866,16 +925,16 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     }
     for (int j = tid; j < l; j += PANEL_T) vS[j] = vSr[j];
     __syncthreads();
-    double* Ug = a.red + 3 * DMQR_KP * DMQR_KP + (size_t)blockIdx.x * DMQR_KP * DMQR_KP;
-    cq_trinv_upper(A1, Ug, l);
+    for (int e = tid; e < l * l; e += PANEL_T) {
+      const int i = e / l, j = e % l;
+      A2[i * DMQR_KP + j] = (j >= i) ? -vS[j] * A2[i * DMQR_KP + j] : 0.0;
+    }
     __syncthreads();
-    // M = -R2^-1 S U^-1 (R2^-1 in A2 from above)
-    cq_small_gemm([&](int i, int t) { return -vS[t] * A2[i * DMQR_KP + t]; },
-                  [&](int t, int j) { return Ug[t * DMQR_KP + j]; }, A1, l);
+    cq_trsm_right_upper<false>(A2, A1, l, DMQR_KP, 1);
   }
-  cl.sync();  // M ready (rank 1's A1, or rank 0's A2)
+  cl.sync();  // M ready (rank 1's A2, or rank 0's A2)
   if (m_on_1 ? (me != 1) : (me != 0)) {  // pull M and S
-    const double* Mr = m_on_1 ? cl.map_shared_rank(A1, 1) : cl.map_shared_rank(A2, 0);
+    const double* Mr = m_on_1 ? cl.map_shared_rank(A2, 1) : cl.map_shared_rank(A2, 0);
     const double* vSr = cl.map_shared_rank(vS, 0);
     for (int e = tid; e < l * l; e += PANEL_T) {
       const int i = e / l, j = e % l;
@@ -883,12 +942,6 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     }
     if (me != 0)
       for (int j = tid; j < l; j += PANEL_T) vS[j] = vSr[j];
-  } else if (m_on_1) {  // rank 1: its M into A2 for the Y product
-    __syncthreads();
-    for (int e = tid; e < l * l; e += PANEL_T) {
-      const int i = e / l, j = e % l;
-      A2[i * DMQR_KP + j] = (j >= i) ? A1[i * DMQR_KP + j] : 0.0;
-    }
   }
   cl.sync();
   // ---- P16: Y = Q1 M on this rank's rows (rank 0's rows < l are fixed below) ----
