@@ -16,8 +16,8 @@
 namespace dmqr {
 
 constexpr int GRAM_T = 256;
-constexpr int GRAM_ROWS = 64;  // slab height
-constexpr int GRAM_LD = 68;    // 64 rows + 4: conflict-free fragment loads (ld = 4 mod 16)
+constexpr int GRAM_ROWS = 32;  // slab height (one slab per CTA up to 148 x 32 rows)
+constexpr int GRAM_LD = 36;    // 32 rows + 4: conflict-free fragment loads (ld = 4 mod 16)
 constexpr int GRAM_PART = DMQR_KP * DMQR_KP;
 // [2][KP][LD] candidate slabs, [2][KP][LD] pending-panel Y slabs, [KP][KP] Wt of the candidates
 constexpr size_t GRAM_SMEM = sizeof(double) * (4 * DMQR_KP * GRAM_LD + DMQR_KP * DMQR_KP);
@@ -239,22 +239,24 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __
     __syncthreads();
     double* buf = gsm + (sl & 1) * DMQR_KP * GRAM_LD;
     if (pendu) {
-      // buf[col][row] += (-Y) Wt for live candidates: warp w owns rows 8w..8w+7
+      // buf[col][row] += (-Y) Wt for live candidates: warp w owns rows
+      // 8 (w & 3) .. +8 and column tiles [5 (w >> 2), +5)
       const double* ys = ysl + (sl & 1) * DMQR_KP * GRAM_LD;
-      const int rr = wid * 8 + (lane >> 2);
+      const int rr = (wid & 3) * 8 + (lane >> 2);
       const int64_t r0 = r_begin + (int64_t)sl * GRAM_ROWS;
-      for (int q0 = 0; q0 < nt; q0 += 3) {
+      const int qh1 = min(nt, (wid >> 2) * 5 + 5);
+      for (int q0 = (wid >> 2) * 5; q0 < qh1; q0 += 3) {
         double u3[3][2];
 #pragma unroll
         for (int q = 0; q < 3; ++q)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) u3[q][h] = (q0 + q < nt) ? buf[((q0 + q) * 8 + 2 * (lane & 3) + h) * GRAM_LD + rr] : 0.0;
+          for (int h = 0; h < 2; ++h) u3[q][h] = (q0 + q < qh1) ? buf[((q0 + q) * 8 + 2 * (lane & 3) + h) * GRAM_LD + rr] : 0.0;
         for (int ks = 0; ks < plp4; ks += 4) {
           const int t = ks + (lane & 3);
           const double a = -ys[t * GRAM_LD + rr];
 #pragma unroll
           for (int q = 0; q < 3; ++q)
-            if (q0 + q < nt) dmma884(u3[q][0], u3[q][1], a, wsm[t * DMQR_KP + (q0 + q) * 8 + (lane >> 2)]);
+            if (q0 + q < qh1) dmma884(u3[q][0], u3[q][1], a, wsm[t * DMQR_KP + (q0 + q) * 8 + (lane >> 2)]);
         }
         __syncwarp();
 #pragma unroll
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int col = (q0 + q) * 8 + 2 * (lane & 3) + h;
-            if (q0 + q < nt && col < ncand && s_live[col]) {
+            if (q0 + q < qh1 && col < ncand && s_live[col]) {
               buf[col * GRAM_LD + rr] = u3[q][h];
               if (r0 + rr < r_end) A[(n_s + r0 + rr) + (int64_t)s_cand[col] * lda] = u3[q][h];
             }
