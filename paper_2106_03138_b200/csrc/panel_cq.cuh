@@ -332,10 +332,11 @@ __device__ __forceinline__ double cq_rcp12(double x) {
 // the rank-8 update to the trailing block on DMMA.
 __device__ void cq_mlu(double* A, double* vS, double* vpiv, int l) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  for (int b0 = 0; b0 < l; b0 += 8) {
+  const int nbk = (l + 7) / 8;
+  auto warp_panel = [&](int b0) {
     const int bw = min(8, l - b0);
     const int c0 = b0 + 8;
-    if (tid < 32) {
+    {
       double v[3][8];  // rows b0 + lane + 32 s, block columns
       double w[2][8];  // block rows, columns c0 + lane + 32 s
 #pragma unroll
@@ -411,40 +412,62 @@ __device__ void cq_mlu(double* A, double* vS, double* vpiv, int l) {
         }
       }
     }
-    __syncthreads();
-    CQ_TICK(4);
-    // trailing block on DMMA: A[i][c] -= sum_j L[i][b0+j] q'[b0+j][c]
-    const int nt = (l - c0 + 7) / 8;
-    if (nt > 0) {
-      const int lr = lane >> 2, lk = lane & 3;
-      for (int t0 = wid; t0 < nt * nt; t0 += 4 * nw) {
-        int ti[4], tj[4];
-        double x[4][2];
+  };
+  // A[tile rt][tile ct] -= L[rows][pb0 .. pb0+8) q'[pb0 .. pb0+8)[cols] for the
+  // tiles tile_of(t), t < ntl, spread over warps w0, w0 + ws, ...
+  auto upd_tiles = [&](int pb0, auto tile_of, int ntl, int w0, int ws) {
+    const int lr = lane >> 2, lk = lane & 3;
+    for (int t0 = wid - w0; t0 < ntl; t0 += 4 * ws) {
+      if (t0 < 0) break;
+      int ti[4], tj[4];
+      double x[4][2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int t = t0 + q * nw;
-          ti[q] = (t < nt * nt) ? t / nt : -1;
-          tj[q] = (t < nt * nt) ? t % nt : 0;
-          x[q][0] = x[q][1] = 0.0;
-        }
+      for (int q = 0; q < 4; ++q) {
+        const int t = t0 + q * ws;
+        ti[q] = -1;
+        tj[q] = 0;
+        if (t < ntl) tile_of(t, ti[q], tj[q]);
+        x[q][0] = x[q][1] = 0.0;
+      }
 #pragma unroll
-        for (int k0 = 0; k0 < 8; k0 += 4) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (ti[q] >= 0) {
-              const int r = min(c0 + ti[q] * 8 + lr, DMQR_KP - 1), cc = min(c0 + tj[q] * 8 + lr, DMQR_KP - 1);
-              dmma884(x[q][0], x[q][1], A[r * DMQR_KP + b0 + k0 + lk], A[(b0 + k0 + lk) * DMQR_KP + cc]);
-            }
-        }
-        __syncwarp();
+      for (int k0 = 0; k0 < 8; k0 += 4) {
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           if (ti[q] >= 0) {
-            const int r = c0 + ti[q] * 8 + lr, oc = c0 + tj[q] * 8 + 2 * lk;
-            if (r < l && oc < l) A[r * DMQR_KP + oc] -= x[q][0];
-            if (r < l && oc + 1 < l) A[r * DMQR_KP + oc + 1] -= x[q][1];
+            const int r = min(ti[q] * 8 + lr, DMQR_KP - 1), cc = min(tj[q] * 8 + lr, DMQR_KP - 1);
+            dmma884(x[q][0], x[q][1], A[r * DMQR_KP + pb0 + k0 + lk], A[(pb0 + k0 + lk) * DMQR_KP + cc]);
           }
       }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (ti[q] >= 0) {
+          const int r = ti[q] * 8 + lr, oc = tj[q] * 8 + 2 * lk;
+          if (r < l && oc < l) A[r * DMQR_KP + oc] -= x[q][0];
+          if (r < l && oc + 1 < l) A[r * DMQR_KP + oc + 1] -= x[q][1];
+        }
+    }
+  };
+  // Look-ahead over the 8-column blocks: warp 0 eliminates block b while the
+  // other warps finish block b-1's trailing update (rows and columns past
+  // block b -- disjoint from block b's column and row); then all warps bring
+  // block b+1's column and row up to date with block b.
+  for (int b = 0; b < nbk; ++b) {
+    const int b0 = b * 8;
+    if (wid == 0) {
+      warp_panel(b0);
+    } else if (b > 0) {
+      const int pb0 = b0 - 8, tb = b + 1, nr = nbk - tb;  // rest of block b-1: tiles >= (b+1, b+1)
+      if (nr > 0)
+        upd_tiles(pb0, [&](int t, int& ri, int& ci) { ri = tb + t / nr; ci = tb + t % nr; }, nr * nr, 1, nw - 1);
+    }
+    __syncthreads();
+    CQ_TICK(4);
+    if (b + 1 < nbk) {  // block b+1's column (rows >= b0+8) and row (columns >= b0+16) with block b
+      const int tb = b + 1, nr = nbk - tb;
+      upd_tiles(b0, [&](int t, int& ri, int& ci) {
+        if (t < nr) { ri = tb + t; ci = tb; } else { ri = tb; ci = tb + 1 + (t - nr); }
+      }, nr + (nr - 1), 0, nw);
     }
     __syncthreads();
     CQ_TICK(5);
