@@ -78,11 +78,13 @@ __device__ __forceinline__ double cq_rsqrt(double d) {
 __device__ int cq_chol(double* A, double* out, double* piv, const double* orig, int n, double tol) {
   __shared__ int s_fail;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const int nbk = (n + 7) / 8;
   for (int e = tid; e < DMQR_KP * DMQR_KP; e += blockDim.x) out[e] = 0.0;
+  if (tid == 0) s_fail = n;
   __syncthreads();
-  for (int b0 = 0; b0 < n; b0 += 8) {
+  auto warp_rowblock = [&](int b0) {
     const int bw = min(8, n - b0);
-    if (tid < 32) {
+    {
       // every lane: the 8 x 8 diagonal block (upper); lane: 2 columns right of it
       double D[8][8], a[2][8];
       // (unconditional loads from clamped in-bounds addresses, then select:
@@ -149,33 +151,27 @@ __device__ int cq_chol(double* A, double* out, double* piv, const double* orig, 
       }
       if (lane == 0) s_fail = fail;
     }
-    __syncthreads();
-    CQ_TICK(0);
-    if (s_fail < n) return s_fail;
-    // trailing upper triangle on DMMA: A[i][j] -= sum_t R[b0+t][i] R[b0+t][j]
-    // (upper 8 x 8 tiles, up to 3 per warp interleaved)
-    const int c0 = b0 + 8, nt = (n - c0 + 7) / 8;
-    const int ntiles = nt * (nt + 1) / 2;
-    if (wid < ntiles) {
-      const int lr = lane >> 2, lk = lane & 3;
+  };
+  // A[tile ri][tile cj] -= R[pb0 .. pb0+8)[rows]^T R[pb0 .. pb0+8)[cols] for the
+  // tiles tile_of(t), t < ntl, on warps w0, w0 + ws, ... (3 interleaved per warp)
+  auto syrk_tiles = [&](int pb0, auto tile_of, int ntl, int w0, int ws) {
+    const int lr = lane >> 2, lk = lane & 3;
+    for (int t0 = wid - w0; t0 < ntl; t0 += 3 * ws) {
+      if (t0 < 0) break;
       int ri[3], cj[3];
       double x[3][2];
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        int t = wid + q * nw, ti = 0;
-        if (t >= ntiles) t = -1;
-        int rem = t < 0 ? 0 : t;
-        while (rem >= nt - ti) {
-          rem -= nt - ti;
-          ++ti;
-        }
-        ri[q] = t < 0 ? -1 : c0 + ti * 8;
-        cj[q] = c0 + (ti + rem) * 8;
+        const int t = t0 + q * ws;
+        int ti = -1, tj = 0;
+        if (t < ntl) tile_of(t, ti, tj);
+        ri[q] = ti < 0 ? -1 : ti * 8;
+        cj[q] = tj * 8;
         x[q][0] = x[q][1] = 0.0;
       }
 #pragma unroll
       for (int k0 = 0; k0 < 8; k0 += 4) {
-        const int kr = (b0 + k0 + lk) * DMQR_KP;
+        const int kr = (pb0 + k0 + lk) * DMQR_KP;
 #pragma unroll
         for (int q = 0; q < 3; ++q)
           if (ri[q] >= 0) dmma884(x[q][0], x[q][1], out[kr + ri[q] + lr], out[kr + cj[q] + lr]);
@@ -187,6 +183,30 @@ __device__ int cq_chol(double* A, double* out, double* piv, const double* orig, 
           if (r < n && oc < n) A[r * DMQR_KP + oc] -= x[q][0];
           if (r < n && oc + 1 < n) A[r * DMQR_KP + oc + 1] -= x[q][1];
         }
+    }
+  };
+  // Look-ahead: warp 0 factors block row b while the other warps finish block
+  // b-1's trailing update past block row b+1; then all warps bring block row
+  // b+1 up to date with block b.
+  for (int b = 0; b < nbk; ++b) {
+    const int b0 = b * 8;
+    if (wid == 0) {
+      warp_rowblock(b0);
+    } else if (b > 0) {
+      const int tb = b + 1, nr = nbk - tb;  // upper tiles (ri, cj), tb <= ri <= cj
+      if (nr > 0)
+        syrk_tiles(b0 - 8, [&](int t, int& ti, int& tj) {
+          int r = 0;
+          while (t >= nr - r) { t -= nr - r; ++r; }
+          ti = tb + r; tj = tb + r + t;
+        }, nr * (nr + 1) / 2, 1, nw - 1);
+    }
+    __syncthreads();
+    CQ_TICK(0);
+    if (s_fail < n) return s_fail;
+    if (b + 1 < nbk) {  // block row b+1 with block b
+      const int tb = b + 1, nr = nbk - tb;
+      syrk_tiles(b0, [&](int t, int& ti, int& tj) { ti = tb; tj = tb + t; }, nr, 0, nw);
     }
     __syncthreads();
     CQ_TICK(1);
