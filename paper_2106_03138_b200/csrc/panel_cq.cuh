@@ -658,11 +658,15 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   const bool chunked = nch > 1;
   const int64_t ldq = q1_ld(m);
   const int qodd = (int)(n_s & 1);
+  // row-parallel copies: thread t owns row (t & 255) and every other column
+  // from (t >> 8) -- coalesced, and no index division in the loops
+  const int trow = tid & (CQ_RMAX - 1), tcol0 = tid / CQ_RMAX, tcstep = PANEL_T / CQ_RMAX;
   auto load_chunk = [&](const double* src, int64_t ld, int ch, int ncol) {  // rows of chunk ch -> sl
     const int c0r = ch * CQ_RMAX, cR = min(CQ_RMAX, R - c0r), cR4 = (cR + 3) & ~3;
-    for (int e = tid; e < ncol * cR4; e += PANEL_T) {
-      const int cc = e / cR4, rr = e % cR4;
-      sl[cc * CQ_LDS + rr] = (rr < cR) ? src[(int64_t)cc * ld + c0r + rr] : 0.0;
+    if (trow < cR4) {
+      const double* sp = src + c0r + trow;
+#pragma unroll 4
+      for (int cc = tcol0; cc < ncol; cc += tcstep) sl[cc * CQ_LDS + trow] = (trow < cR) ? sp[(int64_t)cc * ld] : 0.0;
     }
     __syncthreads();
     return cR4;
@@ -706,9 +710,10 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   const bool q1_pub = a.spare && !fail && kk > 0;
   auto store_q1 = [&](int ch) {  // sl rows of chunk ch -> q1g (the row parity of A)
     const int c0r = ch * CQ_RMAX, cR = min(CQ_RMAX, R - c0r);
-    for (int e = tid; e < kk * cR; e += PANEL_T) {
-      const int cc = e / cR, rr = e % cR;
-      a.q1g[(int64_t)cc * ldq + qodd + r0 + c0r + rr] = sl[cc * CQ_LDS + rr];
+    if (trow < cR) {
+      double* dp = a.q1g + qodd + r0 + c0r + trow;
+#pragma unroll 4
+      for (int cc = tcol0; cc < kk; cc += tcstep) dp[(int64_t)cc * ldq] = sl[cc * CQ_LDS + trow];
     }
   };
   if (!fail && kk > 0) {
@@ -991,20 +996,18 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   CQT();
   auto write_back = [&](int c0r, int cR) {
     // Y below the diagonal, R_H = S R on and above it (rows < l live on rank 0)
-    for (int e = tid; e < l * cR; e += PANEL_T) {
-      const int cc = e / cR, rr = e % cR;
-      const int p = r0 + c0r + rr;  // panel row
-      double v;
-      if (p > cc) {
-        if (p < l) {  // Y1 (unit lower) multipliers saved by rank 0
-          v = a.red[2 * DMQR_KP * DMQR_KP + p * DMQR_KP + cc];
-        } else {
-          v = sl[cc * CQ_LDS + rr];
-        }
-      } else {
-        v = vS[p] * a.red[p * DMQR_KP + cc];  // R_H = S R
+    if (trow < cR && r0 + c0r + trow >= l) {  // rows of Y from the slice
+      double* dp = gA + c0r + trow;
+#pragma unroll 4
+      for (int cc = tcol0; cc < l; cc += tcstep) dp[(int64_t)cc * lda] = sl[cc * CQ_LDS + trow];
+    }
+    if (r0 + c0r < l) {  // the top l x l block (rank 0's first chunk), spread over all threads
+#pragma unroll 4
+      for (int e = tid; e < l * l; e += PANEL_T) {
+        const int p = e / l, cc = e % l;
+        gA[(int64_t)cc * lda + p] = (p > cc) ? a.red[2 * DMQR_KP * DMQR_KP + p * DMQR_KP + cc]  // Y1 multipliers
+                                             : vS[p] * a.red[p * DMQR_KP + cc];              // R_H = S R
       }
-      gA[(int64_t)cc * lda + c0r + rr] = v;
     }
   };
   if (chunked) {
