@@ -722,8 +722,9 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     CQT();
     // keep R1: transpose into the lower triangle of A2, diagonal in vD
     __syncthreads();
-    for (int e = tid; e < kk * kk; e += PANEL_T) {
-      const int i = e / kk, j = e % kk;
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int i = e / DMQR_KP, j = e % DMQR_KP;
+      if (i >= kk || j >= kk) continue;
       if (i < j) A2[j * DMQR_KP + i] = A2[i * DMQR_KP + j];
       if (i == j) vD[i] = A2[i * DMQR_KP + i];
     }
@@ -775,8 +776,9 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       s_flag[2] = 0;
     }
     __syncthreads();
-    for (int e = tid; e < kk * kk; e += PANEL_T) {
-      const int i = e / kk, j = e % kk;
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int i = e / DMQR_KP, j = e % DMQR_KP;
+      if (i >= kk || j >= kk) continue;
       if (j >= i) {
         const double g = A2[i * DMQR_KP + j] - (i == j ? 1.0 : 0.0);
         if (!(fabs(g) < CQ_ORTH_TOL)) s_flag[0] = 1;
@@ -839,8 +841,9 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     cq_small_gemm([&](int i, int t) { return A1[i * DMQR_KP + t]; },
                   [&](int t, int j) { return (t < j) ? A2[j * DMQR_KP + t] : ((t == j) ? vD[j] : 0.0); }, Rg, kk);
     __syncthreads();
-    for (int e = tid; e < kk * kk; e += PANEL_T) {
-      const int i = e / kk, j = e % kk;
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int i = e / DMQR_KP, j = e % DMQR_KP;
+      if (i >= kk || j >= kk) continue;
       if (j >= i) A2[i * DMQR_KP + j] = Rg[i * DMQR_KP + j];
     }
     __syncthreads();
@@ -868,8 +871,9 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   }
   // rank 0 keeps R (rows < l) in global scratch for the final write-back
   if (me == 0)
-    for (int e = tid; e < l * l; e += PANEL_T) {
-      const int i = e / l, j = e % l;
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int i = e / DMQR_KP, j = e % DMQR_KP;
+      if (i >= l || j >= l) continue;
       a.red[i * DMQR_KP + j] = (j >= i) ? A2[i * DMQR_KP + j] : 0.0;
     }
   // ---- P11: R2^-1 -> A2 (R2 upper in A1): rank 0 for Q_top; rank 1 too,
@@ -882,8 +886,9 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       cq_small_gemm([&](int i, int t) { return A1[i * DMQR_KP + t] - (i == t ? 1.0 : 0.0); },
                     [&](int t, int j) { return A1[t * DMQR_KP + j] - (t == j ? 1.0 : 0.0); }, A2, l);
       __syncthreads();
-      for (int e = tid; e < l * l; e += PANEL_T) {
-        const int i = e / l, j = e % l;
+      for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+        const int i = e / DMQR_KP, j = e % DMQR_KP;
+        if (i >= l || j >= l) continue;
         if (j >= i) {
           const double x = A1[i * DMQR_KP + j] - (i == j ? 1.0 : 0.0);
           A2[i * DMQR_KP + j] = (i == j ? 1.0 : 0.0) - x + A2[i * DMQR_KP + j];
@@ -921,14 +926,16 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       A2[e] = u;
     }
     // keep Y1 (strict lower of A1 = multipliers) for the write-back of rows < l
-    for (int e = tid; e < l * l; e += PANEL_T) {
-      const int i = e / l, j = e % l;
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int i = e / DMQR_KP, j = e % DMQR_KP;
+      if (i >= l || j >= l) continue;
       if (i > j) a.red[2 * DMQR_KP * DMQR_KP + i * DMQR_KP + j] = A1[i * DMQR_KP + j];
     }
     __syncthreads();
     // Y1^T (unit upper) into the upper of A1
-    for (int e = tid; e < l * l; e += PANEL_T) {
-      const int i = e / l, j = e % l;
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int i = e / DMQR_KP, j = e % DMQR_KP;
+      if (i >= l || j >= l) continue;
       if (j > i) A1[i * DMQR_KP + j] = A1[j * DMQR_KP + i];
       if (j == i) A1[i * DMQR_KP + i] = 1.0;
     }
@@ -941,8 +948,9 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     // T = U (Y1^T)^-1 (householder.py accumulate_wy's W), tau_j = U_jj: U copied
     // into the top l x l block of the slice (rows < l of Y come from Y1 at
     // write-back), then T Y1^T = U solved in place
-    for (int e = tid; e < l * l; e += PANEL_T) {
-      const int i = e / l, j = e % l;
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int i = e / DMQR_KP, j = e % DMQR_KP;
+      if (i >= l || j >= l) continue;
       sl[j * CQ_LDS + i] = A2[i * DMQR_KP + j];
     }
     __syncthreads();
@@ -967,14 +975,16 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     // M U = -R2^-1 S in place (R2^-1 in A2 from above)
     const double* A2r = cl.map_shared_rank(A2, 0);
     const double* vSr = cl.map_shared_rank(vS, 0);
-    for (int e = tid; e < l * l; e += PANEL_T) {
-      const int i = e / l, j = e % l;
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int i = e / DMQR_KP, j = e % DMQR_KP;
+      if (i >= l || j >= l) continue;
       A1[i * DMQR_KP + j] = (j >= i) ? A2r[i * DMQR_KP + j] : 0.0;
     }
     for (int j = tid; j < l; j += PANEL_T) vS[j] = vSr[j];
     __syncthreads();
-    for (int e = tid; e < l * l; e += PANEL_T) {
-      const int i = e / l, j = e % l;
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int i = e / DMQR_KP, j = e % DMQR_KP;
+      if (i >= l || j >= l) continue;
       A2[i * DMQR_KP + j] = (j >= i) ? -vS[j] * A2[i * DMQR_KP + j] : 0.0;
     }
     __syncthreads();
@@ -984,8 +994,9 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   if (m_on_1 ? (me != 1) : (me != 0)) {  // pull M and S
     const double* Mr = m_on_1 ? cl.map_shared_rank(A2, 1) : cl.map_shared_rank(A2, 0);
     const double* vSr = cl.map_shared_rank(vS, 0);
-    for (int e = tid; e < l * l; e += PANEL_T) {
-      const int i = e / l, j = e % l;
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int i = e / DMQR_KP, j = e % DMQR_KP;
+      if (i >= l || j >= l) continue;
       A2[i * DMQR_KP + j] = (j >= i) ? Mr[i * DMQR_KP + j] : 0.0;
     }
     if (me != 0)
@@ -1003,8 +1014,9 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     }
     if (r0 + c0r < l) {  // the top l x l block (rank 0's first chunk), spread over all threads
 #pragma unroll 4
-      for (int e = tid; e < l * l; e += PANEL_T) {
-        const int p = e / l, cc = e % l;
+      for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+        const int p = e / DMQR_KP, cc = e % DMQR_KP;
+        if (p >= l || cc >= l) continue;
         gA[(int64_t)cc * lda + p] = (p > cc) ? a.red[2 * DMQR_KP * DMQR_KP + p * DMQR_KP + cc]  // Y1 multipliers
                                              : vS[p] * a.red[p * DMQR_KP + cc];              // R_H = S R
       }
@@ -1036,8 +1048,9 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     __syncthreads();
     // F = Y1 - Q1_top M -> A1 (in place), then FT = F T, MT = M T (the
     // products k_trail_w applies, transposed) -> global
-    for (int e = tid; e < l * l; e += PANEL_T) {
-      const int i = e / l, j = e % l;
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int i = e / DMQR_KP, j = e % DMQR_KP;
+      if (i >= l || j >= l) continue;
       const double y1 = (i > j) ? a.red[2 * DMQR_KP * DMQR_KP + i * DMQR_KP + j] : ((i == j) ? 1.0 : 0.0);
       A1[i * DMQR_KP + j] = y1 - A1[i * DMQR_KP + j];
     }
