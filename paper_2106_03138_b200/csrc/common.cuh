@@ -89,6 +89,15 @@ __device__ __forceinline__ CtlSnap snap(const Ctl* __restrict__ c) {
   return s;
 }
 
+// Programmatic dependent launch: the per-step kernels are launched so the
+// next one may be scheduled while this one runs; each lets its dependents go
+// at entry and waits for its predecessor (completion + memory) before
+// touching anything.  No-ops for a normal launch.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // leading dimension of the published Q1 buffer (host: lda_of), multiple of 8
 __host__ __device__ __forceinline__ int64_t q1_ld(int64_t m) { return (m > 0 ? (m + 7) / 8 * 8 : 8) + 8; }
 

@@ -176,6 +176,23 @@ struct ProfAcc {
 ProfAcc g_acc;  // guarded by the caller (bench) using one thread
 #define NOTE_LAUNCH() g_launches.fetch_add(1, std::memory_order_relaxed)
 
+// Launch with programmatic stream serialization: the kernel may be scheduled
+// while its predecessor runs (it waits in pdl_enter before touching memory).
+template <typename... KArgs, typename... Args>
+cudaError_t pdl_launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 struct HostHead {  // the prefix of Ctl the host polls
   int32_t n_s, done, stopped, status;
   int32_t step_idx, n_swaps, rank, n_factored;
@@ -355,17 +372,19 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
     }
     // ---- selection ----
     PROF(0);
-    k_select<<<1, SEL_T, 0, st>>>(ctl, u);
+    CK(pdl_launch(k_select, dim3(1), dim3(SEL_T), 0, st, ctl, (const double*)u));
     NOTE_LAUNCH();
     const int64_t ldz = ldz_for(n);
     const int GG = (int)std::clamp<int64_t>(ceil_div(mp, GRAM_ROWS), 1, std::min(GRAM_GMAX, d.sms));
-    k_gram<<<GG, GRAM_T, GRAM_SMEM, st>>>(ctl, A, gpart, Z, ldz, upd);
+    CK(pdl_launch(k_gram, dim3(GG), dim3(GRAM_T), GRAM_SMEM, st, ctl, A, gpart, (const double*)Z, ldz,
+                  (const uint8_t*)upd));
     NOTE_LAUNCH();
-    k_gram_finish<<<45, GRAM_T, sizeof(FinSmem), st>>>(ctl, A, gpart, GG, gfin, upd);
+    CK(pdl_launch(k_gram_finish, dim3(45), dim3(GRAM_T), sizeof(FinSmem), st, ctl, (const double*)A,
+                  (const double*)gpart, GG, gfin, upd));
     NOTE_LAUNCH();
     {
-      k_swap<<<(unsigned)ceil_div(m + (la ? DMQR_KP : 0), SWAP_ROWS), SWAP_T, SWAP_SMEM, st>>>(
-          ctl, A, u, uref, perm, swaps, Z, ldz, upd);
+      CK(pdl_launch(k_swap, dim3((unsigned)ceil_div(m + (la ? DMQR_KP : 0), SWAP_ROWS)), dim3(SWAP_T), SWAP_SMEM,
+                    st, ctl, A, u, uref, perm, swaps, Z, ldz, upd));
       NOTE_LAUNCH();
     }
     // the rest of the previous step's update: beside the CholeskyQR2 panel as
@@ -424,13 +443,15 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
       cfg.blockDim = dim3(threads);
       cfg.dynamicSmemBytes = dsm;
       cfg.stream = st;
-      cudaLaunchAttribute at[1];
+      cudaLaunchAttribute at[2];
       at[0].id = cudaLaunchAttributeClusterDimension;
       at[0].val.clusterDim.x = ncta;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // (pdl_enter in the panels)
+      at[1].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = at;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = 2;
       return cudaLaunchKernelExC(&cfg, fn, kargs);
     };
     // CholeskyQR2 panel (one cluster, <= 256 rows per CTA) first; the Householder
@@ -489,12 +510,13 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
       int nsplit = (int)std::clamp<int64_t>(ceil_div(2 * d.sms, ntile), 1, NSPLIT_MAX);
       nsplit = (int)std::min<int64_t>(nsplit, std::max<int64_t>(1, ceil_div(mp, 256)));
       if (spare) {
-        k_trail_w<<<(unsigned)ceil_div(ncols_ub, TW_COLS), TA_T, TW_SMEM, st>>>(
-            ctl, A, Zp, red + 19 * DMQR_KP * DMQR_KP, Z, ldz, u, uref, upd, glist);
+        CK(pdl_launch(k_trail_w, dim3((unsigned)ceil_div(ncols_ub, TW_COLS)), dim3(TA_T), TW_SMEM, st, ctl, A,
+                      (const double*)Zp, (const double*)(red + 19 * DMQR_KP * DMQR_KP), Z, ldz, u, uref, upd,
+                      glist));
         NOTE_LAUNCH();
       }
-      k_trail_a<<<dim3((unsigned)ntile, nsplit), TA_T, TA_SMEM, st>>>(ctl, A, Zp, T, Z, tcount, ldz, u, uref,
-                                                                          upd, spare ? 1 : 0, glist);
+      CK(pdl_launch(k_trail_a, dim3((unsigned)ntile, nsplit), dim3(TA_T), TA_SMEM, st, ctl, A, Zp,
+                    (const double*)T, Z, tcount, ldz, u, uref, upd, spare ? 1 : 0, glist));
       NOTE_LAUNCH();
       if (la) {
         // the rest of C -= Y Wt runs beside the next step's panel
@@ -512,9 +534,11 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
     PROF(3);
     if (la) {
       // norms: downdated in the Wt epilogues; guard columns recomputed here
-      k_guard<<<dim3((unsigned)std::max<int64_t>(1, ceil_div(mp, GU_ROWS)),
-                     (unsigned)std::max<int64_t>(1, ceil_div(np, GU_GROUPS * DMQR_KP))),
-                GU_T, GU_SMEM, st>>>(ctl, A, Z, ldz, upd, u, uref, glist, lacount + 2);
+      CK(pdl_launch(k_guard,
+                    dim3((unsigned)std::max<int64_t>(1, ceil_div(mp, GU_ROWS)),
+                         (unsigned)std::max<int64_t>(1, ceil_div(np, GU_GROUPS * DMQR_KP))),
+                    dim3(GU_T), GU_SMEM, st, ctl, A, (const double*)Z, ldz, upd, u, uref, (const int32_t*)glist,
+                    lacount + 2));
       NOTE_LAUNCH();
     } else if (np > 0) {
       const int64_t blocks = std::min<int64_t>(ceil_div(np * 32, 256), (int64_t)d.sms * 16);
@@ -522,7 +546,8 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
       NOTE_LAUNCH();
       if (p->trace_norms) { k_norm_trace<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, tbits); NOTE_LAUNCH(); }
     }
-    k_step_end<<<1, 32, 0, st>>>(ctl, srec, norm_trace, tbits, A, Z, ldz, u, uref, upd);
+    CK(pdl_launch(k_step_end, dim3(1), dim3(32), 0, st, ctl, srec, norm_trace, tbits, (const double*)A, Z, ldz, u,
+                  uref, upd));
     NOTE_LAUNCH();
     PROF(4);
     CK(cudaGetLastError());

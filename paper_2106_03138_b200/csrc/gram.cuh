@@ -142,6 +142,7 @@ __device__ __forceinline__ void tile_ij(int t, int nt, int& ti, int& tj) {
 __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __restrict__ A,
                                                  double* __restrict__ part, const double* __restrict__ Wt,
                                                  int64_t ldz, const uint8_t* __restrict__ upd) {
+  pdl_enter();
   const CtlSnap S = snap(c);
   if (S.done) return;
   const bool pendu = S.la && S.pend;
@@ -311,6 +312,7 @@ struct FinSmem {
 __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, const double* __restrict__ A,
                                                         const double* __restrict__ part, int G,
                                                         double* __restrict__ gfin, uint8_t* __restrict__ upd) {
+  pdl_enter();
   const CtlSnap S = snap(c);
   if (S.done) return;
   if (S.la && S.pend && blockIdx.x == 0) {  // k_gram brought the candidates up to date

@@ -71,6 +71,7 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
                            unsigned long long* __restrict__ trace_bits, const double* __restrict__ A,
                            double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
                            double* __restrict__ uref, uint8_t* __restrict__ upd) {
+  pdl_enter();
   const CtlSnap S = snap(c);
   if (S.done) return;
   // look-ahead with no trailing columns past tc0: k_trail_a had no tile to do
@@ -121,6 +122,7 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
 
 // switch the control block to the look-ahead schedule (from the next kernel on)
 __global__ void k_set_la(Ctl* __restrict__ c, int on) {
+  pdl_enter();
   if (threadIdx.x == 0) c->la = on;
 }
 

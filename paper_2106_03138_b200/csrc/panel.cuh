@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(SWAP_T) k_swap(Ctl* __restrict__ c, double* __
                                                  double* __restrict__ uref, int64_t* __restrict__ perm,
                                                  int64_t* __restrict__ swaplog, double* __restrict__ Wt, int64_t ldz,
                                                  uint8_t* __restrict__ upd) {
+  pdl_enter();
   const CtlSnap S = snap(c);
   if (S.done) return;
   const int nmv = S.nmv;
@@ -176,6 +177,7 @@ __device__ __forceinline__ void block_sum_into(double v, double* wscr, double* d
 }
 
 __global__ void __launch_bounds__(PANEL_T, 1) k_panel(PanelArgs a) {
+  pdl_enter();
   Ctl* c = a.c;
   {
     const int done = c->done, cqf = c->cq_fail;  // (the CholeskyQR2 panel may have done the step)

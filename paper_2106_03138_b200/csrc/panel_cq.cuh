@@ -620,7 +620,9 @@ __device__ void cq_cluster_reduce(double* part, double* tot, int k) {
 }
 
 __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
-  // the look-ahead trailing grid behind this one may start now (trailing.cuh)
+  // wait for the step's column swaps, then let the look-ahead grid behind this
+  // one start (trailing.cuh: it runs beside the panel and must see the swaps)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   Ctl* c = a.c;
   const CtlSnap S = snap(c);

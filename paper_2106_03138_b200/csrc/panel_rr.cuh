@@ -48,6 +48,7 @@ constexpr size_t RR_CL_SMEM = sizeof(double) * 2 * RR_MAXCL * RED_LD;  // receiv
 
 template <class Red>
 __global__ void __launch_bounds__(PANEL_T, 1) k_panel_rr(PanelArgs a) {
+  pdl_enter();
   Ctl* c = a.c;
   {
     const int done = c->done, cqf = c->cq_fail;  // (both loads in flight together)

@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
                                                      int64_t ldz, double* __restrict__ u,
                                                      double* __restrict__ uref, uint8_t* __restrict__ upd,
                                                      int only_if_cq_fail, int32_t* __restrict__ glist) {
+  pdl_enter();
   const CtlSnap S = snap(c);
   if (S.done || (only_if_cq_fail && !S.cq_fail)) return;  // (k_trail_w did it)
   const int64_t n_s = S.n_s, m = S.m, n = S.n, lda = S.lda;
@@ -424,6 +425,7 @@ template <bool LA>
 __global__ void __launch_bounds__(TB_T, 2) k_trail_b(Ctl* __restrict__ c, double* __restrict__ A,
                                                      const double* __restrict__ Wt, int64_t ldz,
                                                      uint8_t* __restrict__ upd, unsigned* __restrict__ counter) {
+  pdl_enter();
   const CtlSnap S = snap(c);
   if (LA ? !S.pend : S.done) return;
   const int64_t m = S.m, n = S.n, lda = S.lda;
@@ -679,6 +681,7 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* __restrict__ c, double* _
                                                   double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
                                                   double* __restrict__ uref, uint8_t* __restrict__ upd,
                                                   int32_t* __restrict__ glist) {
+  pdl_enter();
   const CtlSnap S = snap(c);
   if (S.done || S.cq_fail) return;
   const int64_t n_s = S.n_s, m = S.m, n = S.n, lda = S.lda;
@@ -820,6 +823,7 @@ __global__ void __launch_bounds__(GU_T) k_guard(Ctl* __restrict__ c, double* __r
                                                 uint8_t* __restrict__ upd, double* __restrict__ u,
                                                 double* __restrict__ uref, const int32_t* __restrict__ glist,
                                                 unsigned* __restrict__ counter) {
+  pdl_enter();
   const CtlSnap S = snap(c);
   const int cnt = c->gcount;
   if (S.done || cnt == 0) return;
