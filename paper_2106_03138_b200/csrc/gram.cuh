@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __
   }
   __syncthreads();
   if (pendu)  // Wt columns of the candidates (indexed from n_s = pending n_s + l)
+#pragma unroll 6
     for (int e = tid; e < plp4 * DMQR_KP; e += GRAM_T) {
       const int t = e / DMQR_KP, q = e % DMQR_KP;
       wsm[t * DMQR_KP + q] = (t < pl && s_live[q]) ? Wt[t * ldz + (s_cand[q] - n_s)] : 0.0;
@@ -337,6 +338,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
     // 8 independent loads in flight per thread; the combine order is fixed by G
     const double* pp = part + i * DMQR_KP + j;
     double sv[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 5
     for (int b0 = g4; b0 < G; b0 += 32) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {

@@ -701,15 +701,18 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* __restrict__ c, double* _
   const int cb = wid & 3, q0 = (wid >> 2) * 5, q1 = min(q0 + 5, lt);
   const double* gFT = FM;
   const double* gMT = FM + DMQR_KP * DMQR_KP;
-  for (int e = tid; e < lp4 * TW_COLS; e += TA_T) {
+  // (unrolled so the L2 loads of several iterations are in flight together)
+#pragma unroll 9
+  for (int e = tid; e < DMQR_KP * TW_COLS; e += TA_T) {
     const int t = e / TW_COLS, c2 = e % TW_COLS;
     const int64_t col = col0 + c2;
     const bool in = t < l && col < ncols;
     gs[t * TW_CLD + c2] = in ? __ldcg(Gp + (int64_t)t * ldz + l + col) : 0.0;  // G columns from n_s
     cts[t * TW_CLD + c2] = in ? A[(n_s + t) + (c0 + col) * lda] : 0.0;
   }
-  for (int e = tid; e < lp4 * lp4; e += TA_T) {
-    const int t = e / lp4, i = e % lp4;
+#pragma unroll 6
+  for (int e = tid; e < DMQR_KP * DMQR_KP; e += TA_T) {
+    const int t = e / DMQR_KP, i = e % DMQR_KP;
     const bool in = t < l && i < l;
     a1[t * DMQR_KP + i] = in ? gFT[t * DMQR_KP + i] : 0.0;
     a2[t * DMQR_KP + i] = in ? gMT[t * DMQR_KP + i] : 0.0;
