@@ -62,7 +62,7 @@ Layout layout(int64_t m, int64_t n) {
   L.uref = take(sizeof(double) * std::max<int64_t>(n, 1));
   L.T = take(sizeof(double) * DMQR_KP * DMQR_KP);
   // panel all-reduce partials; the CholeskyQR2 panel also keeps R, Y1 and per-rank R = R2 R1 here
-  L.red = take(sizeof(double) * std::max<size_t>(2 * PANEL_PMAX * RED_LD, 37 * DMQR_KP * DMQR_KP));
+  L.red = take(sizeof(double) * std::max<size_t>(2 * PANEL_PMAX * RED_LD, 38 * DMQR_KP * DMQR_KP));
   L.gram = take(sizeof(double) * GRAM_GMAX * GRAM_PART);
   L.gfin = take(sizeof(double) * DMQR_KP * DMQR_KP);
   L.Zp = take(sizeof(double) * NSPLIT_MAX * DMQR_KP * ldz_for(n));
@@ -126,6 +126,7 @@ int set_attrs(const DevInfo& d) {
   CK(cudaFuncSetAttribute(k_spare, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SP_SMEM));
   CK(cudaFuncSetAttribute(k_trail_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TW_SMEM));
   CK(cudaFuncSetAttribute(k_guard, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GU_SMEM));
+  CK(cudaFuncSetAttribute(k_ygemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YG_SMEM));
   CK(cudaFuncSetAttribute(k_trail_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TP_SMEM));
   CK(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)std::min<size_t>(d.smem_optin - 4096, 220 * 1024)));
@@ -500,6 +501,11 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
       NOTE_LAUNCH();
     } else {
       k_panel<<<1, PANEL_T, smem, st>>>(pa);
+      NOTE_LAUNCH();
+    }
+    if (cq_path && mp > 1) {  // Y below the top block of a CholeskyQR2 panel, on every SM
+      CK(pdl_launch(k_ygemm, dim3((unsigned)ceil_div(mp - 1, YG_ROWS)), dim3(256), YG_SMEM, st, ctl, A,
+                    (const double*)q1g, (const double*)(red + 37 * DMQR_KP * DMQR_KP)));
       NOTE_LAUNCH();
     }
     // ---- trailing update ----

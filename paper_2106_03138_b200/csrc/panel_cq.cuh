@@ -734,10 +734,10 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     if (!chunked) {
       cq_slice_gemm(sl, R4, kk, kk, A1);
       CQT();
-      if (q1_pub) {  // publish this rank's Q1 rows for the spare-SM G = Q1^T C (k_spare)
-        __syncthreads();
-        store_q1(0);
-      }
+      // publish this rank's Q1 rows: k_ygemm forms Y = Q1 M from them, and
+      // (look-ahead) k_spare's G = Q1^T C
+      __syncthreads();
+      store_q1(0);
       __syncthreads();
       // ---- P6/P7: G2 = Q1^T Q1 (partial -> A1, total -> upper A2) ----
       cq_gram(sl, R4, kk, A1);
@@ -1005,40 +1005,26 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       for (int j = tid; j < l; j += PANEL_T) vS[j] = vSr[j];
   }
   cl.sync();
-  // ---- P16: Y = Q1 M on this rank's rows (rank 0's rows < l are fixed below) ----
+  // ---- P16: M (and the top l x l block) out; Y = Q1 M below the top block is
+  // formed by k_ygemm on every SM from the published Q1 ----
   CQT();
-  auto write_back = [&](int c0r, int cR) {
-    // Y below the diagonal, R_H = S R on and above it (rows < l live on rank 0)
-    if (trow < cR && r0 + c0r + trow >= l) {  // rows of Y from the slice
-      double* dp = gA + c0r + trow;
+  if (me == 0) {
+    double* gM = a.red + 37 * DMQR_KP * DMQR_KP;
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int i = e / DMQR_KP, j = e % DMQR_KP;
+      gM[e] = (i < l && j < l && j >= i) ? A2[e] : 0.0;
+    }
+    // R_H = S R on and above the diagonal, Y1 below it
 #pragma unroll 4
-      for (int cc = tcol0; cc < l; cc += tcstep) dp[(int64_t)cc * lda] = sl[cc * CQ_LDS + trow];
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int p = e / DMQR_KP, cc = e % DMQR_KP;
+      if (p >= l || cc >= l) continue;
+      gA[(int64_t)cc * lda + p] = (p > cc) ? a.red[2 * DMQR_KP * DMQR_KP + p * DMQR_KP + cc]  // Y1 multipliers
+                                           : vS[p] * a.red[p * DMQR_KP + cc];              // R_H = S R
     }
-    if (r0 + c0r < l) {  // the top l x l block (rank 0's first chunk), spread over all threads
-#pragma unroll 4
-      for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
-        const int p = e / DMQR_KP, cc = e % DMQR_KP;
-        if (p >= l || cc >= l) continue;
-        gA[(int64_t)cc * lda + p] = (p > cc) ? a.red[2 * DMQR_KP * DMQR_KP + p * DMQR_KP + cc]  // Y1 multipliers
-                                             : vS[p] * a.red[p * DMQR_KP + cc];              // R_H = S R
-      }
-    }
-  };
-  if (chunked) {
-    for (int ch = 0; ch < nch; ++ch) {
-      const int cR4 = load_chunk(a.q1g + qodd + r0, ldq, ch, l);
-      cq_slice_gemm(sl, cR4, l, l, A2);
-      __syncthreads();
-      write_back(ch * CQ_RMAX, min(CQ_RMAX, R - ch * CQ_RMAX));
-      __syncthreads();
-    }
-  } else {
-    cq_slice_gemm(sl, R4, l, l, A2);
   }
-  CQT();
   __syncthreads();
-  // ---- write back ----
-  if (!chunked) write_back(0, R);
+  CQT();
   CQT();
 #undef CQT
   if (me == 0 && a.spare) {
@@ -1071,6 +1057,63 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     c->tc0 = (int32_t)(n_s + l);
   }
   cl.sync();
+}
+
+
+// Y = Q1 M below the panel's top l rows (rows l .. m' of the accepted
+// columns), after a successful CholeskyQR2 panel: one CTA per 64 rows, all
+// SMs, instead of the panel's 16.  Q1 comes from the published buffer, M from
+// the panel (gM); the DMMA sequence is the panel's slice product (triangular M).
+constexpr int YG_ROWS = 64;
+constexpr int YG_LD = YG_ROWS + 4;
+constexpr size_t YG_SMEM = sizeof(double) * (DMQR_KP * DMQR_KP + DMQR_KP * YG_LD);
+
+__global__ void __launch_bounds__(256) k_ygemm(Ctl* __restrict__ c, double* __restrict__ A,
+                                               const double* __restrict__ q1g, const double* __restrict__ gM) {
+  pdl_enter();
+  const CtlSnap S = snap(c);
+  if (S.done || S.cq_fail) return;
+  const int l = S.l_acc;
+  const int64_t n_s = S.n_s, m = S.m, lda = S.lda, mp = m - n_s;
+  const int64_t r0 = l + (int64_t)blockIdx.x * YG_ROWS;  // panel-relative
+  if (l == 0 || r0 >= mp) return;
+  const int64_t ldq = q1_ld(m);
+  const int qodd = (int)(n_s & 1);
+  extern __shared__ __align__(16) double ygs[];
+  double* ms = ygs;                        // M[k][c], KP row-major
+  double* qs = ygs + DMQR_KP * DMQR_KP;    // Q1[r][k] at qs[k * YG_LD + r]
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nr = (int)min((int64_t)YG_ROWS, mp - r0);
+  const int lp4 = (l + 3) / 4 * 4;
+#pragma unroll 6
+  for (int e = tid; e < DMQR_KP * DMQR_KP; e += blockDim.x) ms[e] = __ldcg(gM + e);
+#pragma unroll 6
+  for (int e = tid; e < lp4 * YG_ROWS; e += blockDim.x) {
+    const int k = e / YG_ROWS, rr = e % YG_ROWS;
+    qs[k * YG_LD + rr] = (k < l && rr < nr) ? __ldcg(q1g + (int64_t)k * ldq + qodd + r0 + rr) : 0.0;
+  }
+  __syncthreads();
+  const int nt_n = (l + 7) / 8;
+  const int r = wid * 8 + (lane >> 2);
+  double acc[DMQR_KP / 8][2];
+#pragma unroll
+  for (int q = 0; q < DMQR_KP / 8; ++q) acc[q][0] = acc[q][1] = 0.0;
+  for (int ks = 0; ks < lp4 / 4; ++ks) {
+    const int kc = 4 * ks + (lane & 3);
+    const double av = qs[kc * YG_LD + r];
+#pragma unroll
+    for (int q = 0; q < DMQR_KP / 8; ++q)
+      if (q < nt_n && 4 * ks < 8 * (q + 1)) dmma884(acc[q][0], acc[q][1], av, ms[kc * DMQR_KP + q * 8 + (lane >> 2)]);
+  }
+  if (r < nr) {
+    double* dp = A + (n_s + r0 + r) + n_s * lda;
+#pragma unroll
+    for (int q = 0; q < DMQR_KP / 8; ++q) {
+      const int c0 = q * 8 + 2 * (lane & 3);
+      if (c0 < l) dp[(int64_t)c0 * lda] = acc[q][0];
+      if (c0 + 1 < l) dp[(int64_t)(c0 + 1) * lda] = acc[q][1];
+    }
+  }
 }
 
 }  // namespace dmqr
