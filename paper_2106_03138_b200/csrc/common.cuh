@@ -98,6 +98,12 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // leading dimension of the published Q1 buffer (host: lda_of), multiple of 8
 __host__ __device__ __forceinline__ int64_t q1_ld(int64_t m) { return (m > 0 ? (m + 7) / 8 * 8 : 8) + 8; }
 

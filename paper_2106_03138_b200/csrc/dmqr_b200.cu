@@ -340,6 +340,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
   const int max_coop_p = std::min(d.sms, PANEL_PMAX);
   const int max_cluster = cluster16 ? 16 : 8;
   const bool use_cq = getenv("DMQR_NO_CHOLQR") == nullptr;  // debug switch: Householder panel only
+  long long* tline = getenv("DMQR_TIMELINE") ? pdbg : nullptr;  // debug: panel / k_spare timestamps
   const bool trail_persistent = getenv("DMQR_TRAIL_PERSISTENT") != nullptr;  // A/B switch
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
 
@@ -381,7 +382,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
                   (const uint8_t*)upd));
     NOTE_LAUNCH();
     CK(pdl_launch(k_gram_finish, dim3(45), dim3(GRAM_T), sizeof(FinSmem), st, ctl, (const double*)A,
-                  (const double*)gpart, GG, gfin, upd));
+                  (const double*)gpart, GG, gfin, upd, tline));
     NOTE_LAUNCH();
     {
       CK(pdl_launch(k_swap, dim3((unsigned)ceil_div(m + (la ? DMQR_KP : 0), SWAP_ROWS)), dim3(SWAP_T), SWAP_SMEM,
@@ -436,7 +437,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
     const int G = cl_path ? P : ((P > 1) ? P + 1 : 1);
     PanelArgs pa{ctl, A, coeffs, T, red, use_smem, P,
                  (g_prof.load() >= 2 && steps_done == 2) ? pdbg : nullptr, std::max(0, g_prof.load() - 2), 0,
-                 q1g, 0};
+                 q1g, 0, tline};
     void* kargs[] = {&pa};
     auto launch_cluster = [&](const void* fn, int ncta, unsigned threads, size_t dsm) -> cudaError_t {
       cudaLaunchConfig_t cfg = {};
@@ -486,7 +487,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
         cfg.numAttrs = 1;
         NOTE_LAUNCH();
         CK(cudaLaunchKernelEx(&cfg, k_spare, ctl, A, (const double*)Z, ldz, upd, (const double*)q1g, Zp,
-                              lacount + 4, Pcq, nsplit_g, tcount));
+                              lacount + 4, Pcq, nsplit_g, tcount, tline));
       }
     }
     if (cl_path) {

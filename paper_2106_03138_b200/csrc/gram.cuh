@@ -34,6 +34,7 @@ constexpr size_t GRAM_SMEM = sizeof(double) * (4 * DMQR_KP * GRAM_LD + DMQR_KP *
 // increase along such a chain, so src_i = follow(sel[i]) over already known
 // src_d -- a short sequential loop on one lane; everything else is parallel.
 struct PlanSmem {
+  int sel[DMQR_KP];    // c->sel staged in shared memory (the serial loop's reads)
   int src[DMQR_KP];    // src_i
   int win[DMQR_KP];    // content of window slot n_s+i at time i (W_i)
   int lastw[DMQR_KP];  // latest content written into window slot d (-1: none)
@@ -43,7 +44,10 @@ __device__ void plan_swaps_warp(Ctl* c, const CtlSnap& S, int nsel, double gamma
   const int lane = threadIdx.x & 31;
   const int n_s = S.n_s;
   const int k_s = (int)min((int64_t)nsel, S.kmax - n_s);
-  for (int d = lane; d < DMQR_KP; d += 32) ps.lastw[d] = -1;
+  for (int d = lane; d < DMQR_KP; d += 32) {
+    ps.lastw[d] = -1;
+    ps.sel[d] = (d < nsel) ? c->sel[d] : 0;
+  }
   __syncwarp();
   if (lane == 0) {
     c->nsel = nsel;
@@ -51,7 +55,7 @@ __device__ void plan_swaps_warp(Ctl* c, const CtlSnap& S, int nsel, double gamma
     c->gamma = gamma;
     c->eps_s = S.tau * S.umax;
     for (int i = 0; i < k_s; ++i) {
-      int p = c->sel[i];
+      int p = ps.sel[i];
       int d = p - n_s;
       while (d >= 0 && d < i) {  // sel[i] sat in slot n_s+d when it was filled
         p = ps.src[d];
@@ -85,7 +89,7 @@ __device__ void plan_swaps_warp(Ctl* c, const CtlSnap& S, int nsel, double gamma
     const int d = d0 + lane;
     int src = -1;
     if (d < k_s)
-      src = c->sel[d];
+      src = ps.sel[d];
     else if (d < DMQR_KP && ps.lastw[d] >= 0)
       src = ps.lastw[d];
     const bool mv = (src >= 0) && src != n_s + d;
@@ -312,10 +316,14 @@ struct FinSmem {
 // grid: one CTA per upper 8x8 tile (45 for 65 candidates), GRAM_T threads.
 __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, const double* __restrict__ A,
                                                         const double* __restrict__ part, int G,
-                                                        double* __restrict__ gfin, uint8_t* __restrict__ upd) {
+                                                        double* __restrict__ gfin, uint8_t* __restrict__ upd,
+                                                        long long* __restrict__ tline) {
+  const long long t_in = gtimer();
   pdl_enter();
   const CtlSnap S = snap(c);
   if (S.done) return;
+#define GFT(k) \
+  if (tline && threadIdx.x == 0) tline[512 + 8 * (S.step_idx & 63) + (k)] = gtimer()
   if (S.la && S.pend && blockIdx.x == 0) {  // k_gram brought the candidates up to date
     const int nc = (S.kind == 0) ? S.ncand : 1;
     for (int q = threadIdx.x; q < nc; q += blockDim.x) upd[c->cand[q]] = 1;
@@ -360,15 +368,17 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
   __syncthreads();
   if (!sm.is_last) return;
   __threadfence();
+  if (tline && tid == 0) tline[512 + 8 * (S.step_idx & 63) + 0] = t_in;
+  GFT(1);
   if (tid == 0) {
     c->gram_count = 0u;
     sm.bad = 0;
     sm.zero = 0;
   }
 #pragma unroll 4
-  for (int e = tid; e < ncand * ncand; e += GRAM_T) {
-    const int i = e / ncand, j = e % ncand;
-    if (j >= i) sm.g[i * DMQR_KP + j] = __ldcg(gfin + i * DMQR_KP + j);
+  for (int e = tid; e < DMQR_KP * DMQR_KP; e += GRAM_T) {
+    const int i = e / DMQR_KP, j = e % DMQR_KP;
+    if (j >= i && j < ncand) sm.g[e] = __ldcg(gfin + e);
   }
   __syncthreads();
   // over/underflow risk: the diagonal (sums of squares) bounds every entry
@@ -416,39 +426,54 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
     }
     return;
   }
+  GFT(2);
   // Theta upper triangle: (G_ij * inv_i) * inv_j, i < j (dm.py:112)
-  for (int e = tid; e < ncand * ncand; e += GRAM_T) {
-    const int i = e / ncand, j = e % ncand;
-    if (j <= i) continue;
-    sm.g[i * DMQR_KP + j] = __dmul_rn(__dmul_rn(sm.g[i * DMQR_KP + j], sm.inv[i]), sm.inv[j]);
+  // (mirrored into the lower triangle: the filter and gamma read rows only,
+  // which is bank-conflict free)
+  for (int e = tid; e < DMQR_KP * DMQR_KP; e += GRAM_T) {
+    const int i = e / DMQR_KP, j = e % DMQR_KP;
+    if (j <= i || j >= ncand) continue;
+    const double th = __dmul_rn(__dmul_rn(sm.g[e], sm.inv[i]), sm.inv[j]);
+    sm.g[e] = th;
+    sm.g[j * DMQR_KP + i] = th;
   }
   __syncthreads();
   const bool dmax = S.use_delta_max != 0;
+  GFT(3);
   if (!dmax) {
     // ---- greedy filter (dm.py:151-173) via conflict masks: bit q of conf[t] is
     // set when candidate q < t fails |theta_qt| < delta; then t is accepted iff
     // no accepted q conflicts -- one 64-step bit loop on one thread ----
     const double delta = S.delta;
     for (int t = wid + 1; t < ncand; t += GRAM_T / 32) {
-      const double a0 = (lane < t) ? fabs(sm.g[lane * DMQR_KP + t]) : 0.0;
-      const double a1 = (lane + 32 < t) ? fabs(sm.g[(lane + 32) * DMQR_KP + t]) : 0.0;
+      const double a0 = (lane < t) ? fabs(sm.g[t * DMQR_KP + lane]) : 0.0;
+      const double a1 = (lane + 32 < t) ? fabs(sm.g[t * DMQR_KP + lane + 32]) : 0.0;
       const unsigned lo = __ballot_sync(0xffffffffu, lane < t && !(a0 < delta));
       const unsigned hi = __ballot_sync(0xffffffffu, lane + 32 < t && !(a1 < delta));
       if (lane == 0) sm.conf[t] = ((unsigned long long)hi << 32) | lo;
     }
     __syncthreads();
-    if (tid == 0) {
-      unsigned long long acc = 1ull;
+    GFT(6);
+    if (tid == 0) {  // (masks loaded 8 at a time: only the AND chain is serial)
+      unsigned long long acc = 1ull;  // accepted q < 64 (t = 64 is the last candidate)
       int nch = 1;
       sm.chosen[0] = 0;
-      for (int t = 1; t < ncand; ++t)
-        if (!(sm.conf[t] & acc)) {
-          acc |= 1ull << t;
-          sm.chosen[nch++] = t;
-        }
+      for (int t0 = 1; t0 < ncand; t0 += 8) {
+        unsigned long long cf[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) cf[q] = (t0 + q < ncand) ? sm.conf[t0 + q] : ~0ull;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (!(cf[q] & acc)) {
+            const int t = t0 + q;
+            if (t < 64) acc |= 1ull << t;
+            sm.chosen[nch++] = t;
+          }
+      }
       sm.nch = nch;
     }
     __syncthreads();
+    GFT(7);
     const int nch = sm.nch;
     // gamma = min_i 1 - (sum_j |theta_ij| - 1) over the chosen submatrix (dm.py:175-176)
     for (int p = wid; p < nch; p += GRAM_T / 32) {
@@ -456,7 +481,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
       double sacc = 0.0;
       for (int q = lane; q < nch; q += 32) {
         const int jj = sm.chosen[q];
-        sacc += (i == jj) ? 1.0 : fabs(i < jj ? sm.g[i * DMQR_KP + jj] : sm.g[jj * DMQR_KP + i]);
+        sacc += (i == jj) ? 1.0 : fabs(sm.g[i * DMQR_KP + jj]);
       }
       sacc = warp_sum(sacc);
       if (lane == 0) sm.rowsum[p] = 1.0 - (sacc - 1.0);
@@ -469,7 +494,9 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
     for (int o = 16; o > 0; o >>= 1) gmin = fmin(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
     for (int q = lane; q < nch; q += 32) c->sel[q] = c->cand[sm.chosen[q]];
     __syncwarp();
+    GFT(4);
     plan_swaps_warp(c, S, nch, gmin, sm.plan);
+    GFT(5);
     return;
   }
   if (wid != 0) return;

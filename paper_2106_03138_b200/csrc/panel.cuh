@@ -131,6 +131,7 @@ struct PanelArgs {
   int only_if_fail;  // Householder fallback behind the CholeskyQR2 panel: run only if it declined
   double* q1g;       // CholeskyQR2 panel: Q1 buffer (chunked panels; read by k_spare under look-ahead)
   int spare;         // look-ahead: release k_spare, publish the Wt factors for k_trail_w
+  long long* tline;  // debug timeline (globaltimer at panel end, per step), or null
 };
 
 // deterministic all-reduce of `len` doubles across the grid; in: s_part (this

@@ -625,6 +625,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   Ctl* c = a.c;
+  const long long t_start = gtimer();
   const CtlSnap S = snap(c);
   if (S.done) return;
   cg::cluster_group cl = cg::this_cluster();
@@ -1051,6 +1052,10 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
                   [&](int t, int j) { return a.T[t * DMQR_KP + j]; }, gMT, l);
   }
   if (me == 0 && tid == 0) {
+    if (a.tline) {
+      a.tline[4 * (c->step_idx & 255) + 0] = t_start;
+      a.tline[4 * (c->step_idx & 255) + 1] = gtimer();
+    }
     c->l_acc = l;
     c->broke = (l < k);
     c->cq_fail = 0;

@@ -570,7 +570,9 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
                                                    const double* __restrict__ Wt, int64_t ldz,
                                                    uint8_t* __restrict__ upd, const double* __restrict__ Q1g,
                                                    double* __restrict__ Gp, unsigned* __restrict__ ctr, int P,
-                                                   int nsplit_g, unsigned* __restrict__ tcnt) {
+                                                   int nsplit_g, unsigned* __restrict__ tcnt,
+                                                   long long* __restrict__ tline) {
+  const long long t_first = gtimer();
   __shared__ int s_item, s_flag;
   const int tid = threadIdx.x;
   const CtlSnap S = snap(c);
@@ -660,7 +662,13 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
   }
   __syncthreads();
   if (s_flag) {
-    if (tid == 0) ctr[0] = ctr[1] = ctr[2] = ctr[3] = 0u;
+    if (tid == 0) {
+      ctr[0] = ctr[1] = ctr[2] = ctr[3] = 0u;
+      if (tline) {
+        tline[4 * (c->step_idx & 255) + 2] = t_first;
+        tline[4 * (c->step_idx & 255) + 3] = gtimer();
+      }
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");
   }
 }
