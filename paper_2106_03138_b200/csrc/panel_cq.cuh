@@ -836,32 +836,23 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     }
     CQT();
   }
+  // ---- break: first j >= 1 with |R_jj| < eps_s; an unhealthy pivot at jstar
+  // is a break.  R = R2 R1 is triangular, so R_jj = R2_jj R1_jj exactly as the
+  // product's single nonzero term (R itself is formed off rank 0's chain) ----
   if (!fail && kk > 0) {
-    // ---- P9: R = R2 R1 -> slice-free scratch (a.red), then upper A2 ----
-    // R1[t][j] lives transposed in the strict lower of A2 (diag in vD); R2 upper in A1
-    __syncthreads();
-    double* Rg = a.red + 3 * DMQR_KP * DMQR_KP + (size_t)blockIdx.x * DMQR_KP * DMQR_KP;
-    cq_small_gemm([&](int i, int t) { return A1[i * DMQR_KP + t]; },
-                  [&](int t, int j) { return (t < j) ? A2[j * DMQR_KP + t] : ((t == j) ? vD[j] : 0.0); }, Rg, kk);
-    __syncthreads();
-    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
-      const int i = e / DMQR_KP, j = e % DMQR_KP;
-      if (i >= kk || j >= kk) continue;
-      if (j >= i) A2[i * DMQR_KP + j] = Rg[i * DMQR_KP + j];
-    }
-    __syncthreads();
-  }
-  if (!fail) {
-    // ---- break: first j >= 1 with |R_jj| < eps_s; an unhealthy pivot at jstar is a break ----
-    if (tid == 0) {
+    if (tid < 32) {
       int lb = kk;
       if (brk)
-        for (int j = 1; j < kk; ++j)
-          if (fabs(A2[j * DMQR_KP + j]) < eps_s) {
-            lb = j;
+        for (int b0 = 0; b0 < kk; b0 += 32) {
+          const int j = b0 + tid;
+          const bool hit = j >= 1 && j < kk && fabs(__dmul_rn(A1[j * DMQR_KP + j], vD[j])) < eps_s;
+          const unsigned bal = __ballot_sync(0xffffffffu, hit);
+          if (bal) {
+            lb = b0 + __ffs(bal) - 1;
             break;
           }
-      s_flag[1] = lb;
+        }
+      if (tid == 0) s_flag[1] = lb;
     }
     __syncthreads();
     l = s_flag[1];
@@ -872,19 +863,29 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     cl.sync();
     return;
   }
-  // rank 0 keeps R (rows < l) in global scratch for the final write-back
-  if (me == 0)
-    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
-      const int i = e / DMQR_KP, j = e % DMQR_KP;
-      if (i >= l || j >= l) continue;
-      a.red[i * DMQR_KP + j] = (j >= i) ? A2[i * DMQR_KP + j] : 0.0;
-    }
-  // ---- P11: R2^-1 -> A2 (R2 upper in A1): rank 0 for Q_top; rank 1 too,
-  // beside rank 0's LU, for M (with two or more ranks rank 1 forms M) ----
+  // Work after the break, by rank:
+  //   rank 0:        R2^-1, Q_top, modified LU, then T = U Y1^-T (and FT = Y1^-T)
+  //   rank_R:        R = R2 R1 -> global; after the LU, R_H = S R into the packed top block
+  //   rank_M:        M = -R2^-1 S U^-1 -> gM (k_ygemm: Y below the top block = Q1 M)
+  //   rank_MT:       MT = M T = -R2^-1 S Y1^-T -> gMT (look-ahead only)
+  // (F = Y1 - Q1_top M = U^-1 since Y1 U = I - Q_top S, so FT = F T = Y1^-T.)
+  // With fewer ranks the tasks fold onto the highest rank available.
+  const int rk_M = min(1, nr - 1), rk_MT = min(2, nr - 1), rk_R = min(3, nr - 1);
+  const bool do_mt = a.spare != 0;
+  double* gR = a.red;                                   // R (l x l upper), global
+  double* gM = a.red + 37 * DMQR_KP * DMQR_KP;          // M for k_ygemm
+  double* gFT = a.red + 19 * DMQR_KP * DMQR_KP;         // k_trail_w's factors
+  double* gMT = gFT + DMQR_KP * DMQR_KP;
+  double* gTop = a.A + n_s * lda + n_s;                 // the panel's top l x l block
   __syncthreads();
   CQT();
-  const bool m_on_1 = nr > 1;  // M = -R2^-1 S U^-1 on rank 1, in parallel with rank 0's T
-  auto r2_inverse = [&]() {
+  if (me == rk_R) {
+    // R1[t][j] lives transposed in the strict lower of A2 (diag in vD); R2 upper in A1
+    cq_small_gemm([&](int i, int t) { return A1[i * DMQR_KP + t]; },
+                  [&](int t, int j) { return (t < j) ? A2[j * DMQR_KP + t] : ((t == j) ? vD[j] : 0.0); }, gR, l);
+    __syncthreads();
+  }
+  auto r2_inverse = [&]() {  // R2^-1 -> A2 (R2 upper in A1)
     if (near_id) {  // R2^-1 = I - X + X^2 (error O(|X|^3)), X = R2 - I
       cq_small_gemm([&](int i, int t) { return A1[i * DMQR_KP + t] - (i == t ? 1.0 : 0.0); },
                     [&](int t, int j) { return A1[t * DMQR_KP + j] - (t == j ? 1.0 : 0.0); }, A2, l);
@@ -903,12 +904,35 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       __syncthreads();
     }
   };
-  double* gR2i = a.red + DMQR_KP * DMQR_KP;  // rank 0's copy of R2^-1 (global scratch)
+  // aux task: out = (-R2^-1 S) src^-1 for an upper triangular src (l x l, KP
+  // row-major, possibly in rank 0's shared memory); r2i: R2^-1 (upper), sg: S;
+  // scr: two KP x KP scratch blocks
+  auto aux = [&](const double* src, const double* r2i, const double* sg, double* scr, double* out) {
+    double* P = scr;
+    double* X = scr + DMQR_KP * DMQR_KP;
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int i = e / DMQR_KP, j = e % DMQR_KP;
+      P[e] = (i < l && j < l && j >= i) ? src[e] : 0.0;
+    }
+    __syncthreads();
+    cq_trinv_upper(P, X, l);
+    __syncthreads();
+    cq_small_gemm([&](int i, int t) { return -sg[t] * r2i[i * DMQR_KP + t]; },
+                  [&](int t, int j) { return X[t * DMQR_KP + j]; }, P, l);
+    __syncthreads();
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int i = e / DMQR_KP, j = e % DMQR_KP;
+      out[e] = (i < l && j < l && j >= i) ? P[e] : 0.0;
+    }
+    __syncthreads();
+  };
+  // rank 0's shared scratch after Q_top (the slice is no longer read):
+  // sl[0 .. KP^2): R2^-1 copy (tasks folded onto rank 0), then two blocks
+  double* r2c = sl;
+  double* scr0 = sl + DMQR_KP * DMQR_KP;
   if (me == 0) {
     r2_inverse();
     CQT();
-    if (!m_on_1)
-      for (int e = tid; e < l * l; e += PANEL_T) gR2i[(e / l) * DMQR_KP + e % l] = A2[(e / l) * DMQR_KP + e % l];
     // ---- P12: top l x l block of Q = Q1 R2^-1 -> A1 ----
     if (!chunked)
       cq_small_gemm<true>([&](int i, int t) { return sl[t * CQ_LDS + i]; },
@@ -917,25 +941,21 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       cq_small_gemm<true>([&](int i, int t) { return a.q1g[(int64_t)t * ldq + qodd + i]; },
                           [&](int t, int j) { return A2[t * DMQR_KP + j]; }, A1, l);
     __syncthreads();
+    if (nr <= 2)
+      for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) r2c[e] = A2[e];
     CQT();
     // ---- P13: modified LU of the top block: strict lower = L (Y1), upper = q' ----
     cq_mlu(A1, vS, vpiv, l);
     CQT();
-    // U (upper) -> A2: U_jj = pivot, U_jc = -S_c q'_jc
+    // U (upper) -> A2: U_jj = pivot, U_jc = -S_c q'_jc; Y1^T (unit upper) into
+    // the upper of A1 (the strict lower keeps Y1)
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
       const int i = e / DMQR_KP, j = e % DMQR_KP;
       double u = 0.0;
       if (i < l && j < l && j >= i) u = (i == j) ? vpiv[i] : -vS[j] * A1[i * DMQR_KP + j];
       A2[e] = u;
     }
-    // keep Y1 (strict lower of A1 = multipliers) for the write-back of rows < l
-    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
-      const int i = e / DMQR_KP, j = e % DMQR_KP;
-      if (i >= l || j >= l) continue;
-      if (i > j) a.red[2 * DMQR_KP * DMQR_KP + i * DMQR_KP + j] = A1[i * DMQR_KP + j];
-    }
     __syncthreads();
-    // Y1^T (unit upper) into the upper of A1
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
       const int i = e / DMQR_KP, j = e % DMQR_KP;
       if (i >= l || j >= l) continue;
@@ -943,114 +963,59 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       if (j == i) A1[i * DMQR_KP + i] = 1.0;
     }
     __syncthreads();
-  } else if (me == 1) {
+  } else if (me == rk_M || (do_mt && me == rk_MT)) {
     r2_inverse();  // (overlaps rank 0's Q_top and LU)
   }
-  cl.sync();  // U and S ready on rank 0
+  cl.sync();  // U, Y1^T, S ready on rank 0
+  CQT();
+  const double* A1r = cl.map_shared_rank(A1, 0);
+  const double* A2r = cl.map_shared_rank(A2, 0);
+  const double* vSr = cl.map_shared_rank(vS, 0);
   if (me == 0) {
-    // T = U (Y1^T)^-1 (householder.py accumulate_wy's W), tau_j = U_jj: U copied
-    // into the top l x l block of the slice (rows < l of Y come from Y1 at
-    // write-back), then T Y1^T = U solved in place
+    // packed top block, strict lower: the Y1 multipliers (R_H above it: rank_R)
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
-      const int i = e / DMQR_KP, j = e % DMQR_KP;
-      if (i >= l || j >= l) continue;
-      sl[j * CQ_LDS + i] = A2[i * DMQR_KP + j];
+      const int p = e / DMQR_KP, cc = e % DMQR_KP;
+      if (p < l && cc < p) gA[(int64_t)cc * lda + p] = A1[p * DMQR_KP + cc];
     }
+    // X = (Y1^T)^-1 = FT; T = U X (householder.py accumulate_wy's W; tau_j = U_jj)
+    double* X = scr0;
+    double* Tt = scr0 + DMQR_KP * DMQR_KP;
+    cq_trinv_upper(A1, X, l);
     __syncthreads();
-    cq_trsm_right_upper<true>(sl, A1, l, 1, CQ_LDS);
+    cq_small_gemm([&](int i, int t) { return A2[i * DMQR_KP + t]; },
+                  [&](int t, int j) { return X[t * DMQR_KP + j]; }, Tt, l);
+    __syncthreads();
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
       const int i = e / DMQR_KP, j = e % DMQR_KP;
-      a.T[e] = (i < l && j < l && j >= i) ? sl[j * CQ_LDS + i] : 0.0;
+      const bool in = i < l && j < l && j >= i;
+      a.T[e] = in ? Tt[e] : 0.0;
+      if (do_mt) gFT[e] = in ? X[e] : 0.0;
     }
     for (int j = tid; j < l; j += PANEL_T) a.coeffs[n_s + j] = vpiv[j];
     __syncthreads();
-    if (!m_on_1) {
-      // U^-1 -> A1 (upper)
-      cq_trinv_upper(A2, A1, l);
-      __syncthreads();
-      // M = -R2^-1 S U^-1 -> A2 (upper): Y_below = -(Q1 R2^-1 S) U^-1 = Q1 M
-      cq_small_gemm([&](int i, int t) { return -vS[t] * gR2i[i * DMQR_KP + t]; },
-                    [&](int t, int j) { return A1[t * DMQR_KP + j]; }, A2, l);
-    }
     CQT();
-  } else if (me == 1) {
-    // pull U (upper of rank 0's A2) and S; M = -R2^-1 S U^-1 by solving
-    // M U = -R2^-1 S in place (R2^-1 in A2 from above)
-    const double* A2r = cl.map_shared_rank(A2, 0);
-    const double* vSr = cl.map_shared_rank(vS, 0);
-    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
-      const int i = e / DMQR_KP, j = e % DMQR_KP;
-      if (i >= l || j >= l) continue;
-      A1[i * DMQR_KP + j] = (j >= i) ? A2r[i * DMQR_KP + j] : 0.0;
-    }
-    for (int j = tid; j < l; j += PANEL_T) vS[j] = vSr[j];
-    __syncthreads();
-    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
-      const int i = e / DMQR_KP, j = e % DMQR_KP;
-      if (i >= l || j >= l) continue;
-      A2[i * DMQR_KP + j] = (j >= i) ? -vS[j] * A2[i * DMQR_KP + j] : 0.0;
-    }
-    __syncthreads();
-    cq_trsm_right_upper<false>(A2, A1, l, DMQR_KP, 1);
   }
-  cl.sync();  // M ready (rank 1's A2, or rank 0's A2)
-  if (m_on_1 ? (me != 1) : (me != 0)) {  // pull M and S
-    const double* Mr = m_on_1 ? cl.map_shared_rank(A2, 1) : cl.map_shared_rank(A2, 0);
-    const double* vSr = cl.map_shared_rank(vS, 0);
-    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
-      const int i = e / DMQR_KP, j = e % DMQR_KP;
-      if (i >= l || j >= l) continue;
-      A2[i * DMQR_KP + j] = (j >= i) ? Mr[i * DMQR_KP + j] : 0.0;
-    }
-    if (me != 0)
-      for (int j = tid; j < l; j += PANEL_T) vS[j] = vSr[j];
-  }
-  cl.sync();
-  // ---- P16: M (and the top l x l block) out; Y = Q1 M below the top block is
-  // formed by k_ygemm on every SM from the published Q1 ----
-  CQT();
-  if (me == 0) {
-    double* gM = a.red + 37 * DMQR_KP * DMQR_KP;
-    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
-      const int i = e / DMQR_KP, j = e % DMQR_KP;
-      gM[e] = (i < l && j < l && j >= i) ? A2[e] : 0.0;
-    }
-    // R_H = S R on and above the diagonal, Y1 below it
-#pragma unroll 4
+  if (me == rk_R && me != 0) {
+    // packed top block, diagonal and above: R_H = S R (R from this rank, global)
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
       const int p = e / DMQR_KP, cc = e % DMQR_KP;
-      if (p >= l || cc >= l) continue;
-      gA[(int64_t)cc * lda + p] = (p > cc) ? a.red[2 * DMQR_KP * DMQR_KP + p * DMQR_KP + cc]  // Y1 multipliers
-                                           : vS[p] * a.red[p * DMQR_KP + cc];              // R_H = S R
+      if (p < l && cc < l && cc >= p) gTop[(int64_t)cc * lda + p] = vSr[p] * __ldcg(gR + p * DMQR_KP + cc);
     }
   }
-  __syncthreads();
+  // rank_M / rank_MT: the inverses of rank 0's U and Y1^T, times -R2^-1 S
+  const bool on0 = (me == 0);
+  if (me == rk_M) aux(A2r, on0 ? r2c : A2, vSr, on0 ? scr0 : sl, gM);
+  if (do_mt && me == rk_MT) aux(A1r, on0 ? r2c : A2, vSr, on0 ? scr0 : sl, gMT);
+  if (me == 0 && rk_R == 0) {
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      const int p = e / DMQR_KP, cc = e % DMQR_KP;
+      if (p < l && cc < l && cc >= p) gTop[(int64_t)cc * lda + p] = vS[p] * __ldcg(gR + p * DMQR_KP + cc);
+    }
+  }
+  CQT();
   CQT();
   CQT();
 #undef CQT
-  if (me == 0 && a.spare) {
-    // k_trail_w forms Wt = T^T (E C_top + M^T G) from G = Q1^T C, with
-    // E = F^T, F = Y1 - Q1_top M (both l x l)
-    __syncthreads();
-    cq_small_gemm<true>([&](int i, int t) { return a.q1g[(int64_t)t * q1_ld(m) + qodd + i]; },
-                        [&](int t, int j) { return A2[t * DMQR_KP + j]; }, A1, l);
-    __syncthreads();
-    // F = Y1 - Q1_top M -> A1 (in place), then FT = F T, MT = M T (the
-    // products k_trail_w applies, transposed) -> global
-    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
-      const int i = e / DMQR_KP, j = e % DMQR_KP;
-      if (i >= l || j >= l) continue;
-      const double y1 = (i > j) ? a.red[2 * DMQR_KP * DMQR_KP + i * DMQR_KP + j] : ((i == j) ? 1.0 : 0.0);
-      A1[i * DMQR_KP + j] = y1 - A1[i * DMQR_KP + j];
-    }
-    __syncthreads();
-    double* gFT = a.red + 19 * DMQR_KP * DMQR_KP;
-    double* gMT = gFT + DMQR_KP * DMQR_KP;
-    cq_small_gemm<true>([&](int i, int t) { return A1[i * DMQR_KP + t]; },
-                        [&](int t, int j) { return a.T[t * DMQR_KP + j]; }, gFT, l);
-    cq_small_gemm([&](int i, int t) { return A2[i * DMQR_KP + t]; },
-                  [&](int t, int j) { return a.T[t * DMQR_KP + j]; }, gMT, l);
-  }
   if (me == 0 && tid == 0) {
     if (a.tline) {
       a.tline[4 * (c->step_idx & 255) + 0] = t_start;

@@ -15,7 +15,7 @@ lib.dmqr_stats_enable(0)
 out = np.zeros(64 * 16, dtype=np.int64)
 lib.dmqr_debug_panel_clocks(f.workspace.data_ptr(), n, n, out.ctypes.data_as(C.c_void_p))
 t = out[:24].astype(np.float64)
-names = ["load", "gram1", "reduce1", "chol1", "trinv1", "Q1gemm", "gram2", "reduce2", "chol2", "R+break",
-         "trinvR2", "Qtop", "mLU", "Z+T+Uinv+M", "bcast", "Ygemm", "writeback"]
+names = ["load", "gram1", "reduce1", "chol1", "trinv1", "Q1gemm", "gram2", "reduce2", "R2", "break", "trinvR2",
+         "Qtop", "mLU", "UY+sync", "T", "aux", "end"]
 d = np.diff(t)
 print("cta", cta, {names[i] if i < len(names) else i: int(v) for i, v in enumerate(d[:17])}, "total", int(t[17] - t[0]) if t[17] else None)
