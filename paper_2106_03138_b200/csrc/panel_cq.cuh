@@ -494,6 +494,116 @@ __device__ void cq_mlu(double* A, double* vS, double* vpiv, int l) {
   }
 }
 
+// shared-memory flag with acquire/release ordering (CTA scope)
+__device__ __forceinline__ int lds_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
+// (shared-memory accesses of one warp are performed in order, so after the
+// __syncwarp that precedes it a plain volatile store publishes the warp's
+// earlier shared stores; MEMBAR.CTA of st.release costs ~1000 cycles here)
+__device__ __forceinline__ void sts_release(int* p, int v) {
+  asm volatile("st.volatile.shared::cta.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+
+// Modified LU as above (same in/out contract), as a dataflow over the 16
+// warps: column c lives in registers of warp c % 16 (lane = row, 3 rows per
+// lane).  Pivot j's owner publishes its multipliers (column-major, in Lc) and
+// bumps a counter; every warp applies pivot j to its own columns as soon as it
+// is out -- so the chain is one pivot after another with no block barriers,
+// and the next pivot's column is always up to date when its pivot arrives.
+__device__ void cq_mlu_df(double* A, double* vS, double* vpiv, int l, double* Lc) {
+  static_assert(PANEL_T == 512, "16 warps own the columns");
+  constexpr int NW = 16, NC = (DMQR_MAXK + NW - 1) / NW;
+  __shared__ int s_npub;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double q[NC][3];
+#pragma unroll
+  for (int k = 0; k < NC; ++k)
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int c = wid + NW * k, i = lane + 32 * s;
+      q[k][s] = (c < l && i < l) ? A[i * DMQR_KP + c] : 0.0;
+    }
+  const int cmax = (wid < l) ? wid + NW * ((l - 1 - wid) / NW) : -1;  // my last column
+  if (tid == 0) s_npub = 0;
+  __syncthreads();
+  for (int j = 0; j < l; ++j) {
+    const int lj = j & 31, sj = j >> 5, oj = j % NW, kj = j / NW;
+    if (wid != oj && cmax <= j) break;  // no columns right of j left
+#ifdef CQ_DF_TRACE
+    if (lane == 0 && wid == oj) CQ_DF_TRACE[100 + 4 * j] = clock64();
+#endif
+    // row j of my columns (final: pivots < j are applied)
+    double u[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const double v = (sj == 0) ? q[k][0] : ((sj == 1) ? q[k][1] : q[k][2]);
+      u[k] = __shfl_sync(0xffffffffu, v, lj);
+    }
+    double Lv[3];
+#ifdef CQ_DF_TRACE
+    if (lane == 0 && wid == oj) CQ_DF_TRACE[100 + 4 * j + 1] = clock64() + (long long)(u[0] * 0.0);
+#endif
+    if (wid == oj) {
+      double qjj = 0.0;
+#pragma unroll
+      for (int k = 0; k < NC; ++k)
+        if (k == kj) qjj = u[k];
+      const double sg = (qjj >= 0.0) ? -1.0 : 1.0;  // S_j = -sign(q'_jj), sign(+0) = +
+      const double pv = 1.0 - sg * qjj;             // pivot = 1 + |q'_jj|
+      const double f0 = -sg * cq_rcp12(pv);
+#pragma unroll
+      for (int k = 0; k < NC; ++k)
+        if (k == kj)
+#pragma unroll
+          for (int s = 0; s < 3; ++s) {
+            const int i = lane + 32 * s;
+            Lv[s] = (i > j) ? f0 * q[k][s] : 0.0;
+            q[k][s] = (i > j) ? Lv[s] : q[k][s];
+          }
+#pragma unroll
+      for (int s = 0; s < 3; ++s)
+        if (lane + 32 * s < DMQR_KP) Lc[j * DMQR_KP + lane + 32 * s] = Lv[s];
+      if (lane == 0) {
+        vS[j] = sg;
+        vpiv[j] = pv;
+      }
+      __syncwarp();
+      if (lane == 0) sts_release(&s_npub, j + 1);
+#ifdef CQ_DF_TRACE
+      if (lane == 0) CQ_DF_TRACE[j] = clock64();
+#endif
+    } else {
+      const bool next = (wid == (j + 1) % NW);  // owner of the next pivot: poll hard
+      while (lds_acquire(&s_npub) <= j) {
+        if (!next) __nanosleep(100);
+      }
+#ifdef CQ_DF_TRACE
+      if (lane == 0 && wid == (j + 1) % NW) CQ_DF_TRACE[100 + 4 * (j + 1) + 3] = clock64();
+#endif
+#pragma unroll
+      for (int s = 0; s < 3; ++s) Lv[s] = (lane + 32 * s < DMQR_KP) ? Lc[j * DMQR_KP + lane + 32 * s] : 0.0;
+    }
+    // q'_ic -= L_ij q'_jc for my columns c > j (rows <= j have L = 0)
+#pragma unroll
+    for (int k = 0; k < NC; ++k)
+      if (wid + NW * k > j)
+#pragma unroll
+        for (int s = 0; s < 3; ++s) q[k][s] = fma(-Lv[s], u[k], q[k][s]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NC; ++k)
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int c = wid + NW * k, i = lane + 32 * s;
+      if (c < l && i < l) A[i * DMQR_KP + c] = q[k][s];
+    }
+  __syncthreads();
+}
+
 // slice[:, 0:ncol] <- slice[:, 0:kin] * M (M: kin x ncol upper triangular, KP row-major) in place,
 // rows [0, R); each warp owns 8-row tiles (DMMA 8x8x4, accumulators in registers).
 __device__ void cq_slice_gemm(double* sl, int R, int kin, int ncol, const double* M) {
@@ -590,31 +700,65 @@ __device__ void cq_gram(const double* sl, int R4, int k, double* G) {
     }
 }
 
+// 32-bit shared::cluster address of p in rank `rank`'s shared memory
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ double2 ld_dsmem2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_dsmem(uint32_t a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_dsmem2(uint32_t a, double2 v) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+
 // cluster all-reduce of the upper triangle of a KP x KP matrix: partial in
-// `part` (every rank), total -> `tot` on every rank.  Element e of the upper
-// triangle is summed (fixed rank order) by rank e % nranks and pushed to all.
+// `part` (every rank), total -> `tot` on every rank (entries j >= i only; the
+// strict lower of `tot` is left alone).  The upper 8x8 tiles are cut into
+// element pairs, split evenly over the ranks; each pair is summed in fixed
+// rank order by its rank (16-byte DSMEM loads) and pushed to every rank.
 __device__ void cq_cluster_reduce(double* part, double* tot, int k) {
   cg::cluster_group cl = cg::this_cluster();
   const int nr = (int)cl.num_blocks(), me = (int)cl.block_rank();
+  const int nt = (k + 7) / 8, npair = nt * (nt + 1) / 2 * 32;
+  const int p0 = me * npair / nr, p1 = (me + 1) * npair / nr;
   cl.sync();
-  const int nup = k * (k + 1) / 2;
-  for (int e = me + nr * (int)threadIdx.x; e < nup; e += nr * (int)blockDim.x) {
-    // e -> (row, col) in the upper triangle, row-major
-    int row = 0, rem = e;
-    while (rem >= k - row) {
-      rem -= k - row;
-      ++row;
+  for (int p = p0 + (int)threadIdx.x; p < p1; p += blockDim.x) {
+    int t = p >> 5, ti = 0;
+    while (t >= nt - ti) {  // upper tiles, row-major
+      t -= nt - ti;
+      ++ti;
     }
-    const int col = row + rem, off = row * DMQR_KP + col;
-    double v[RR_MAXCL];
+    const int tj = ti + t, w = p & 31;
+    const int r = ti * 8 + (w >> 2), c = tj * 8 + 2 * (w & 3);
+    const int off = r * DMQR_KP + c;
+    double2 v[RR_MAXCL];
 #pragma unroll
-    for (int r = 0; r < RR_MAXCL; ++r) v[r] = (r < nr) ? *cl.map_shared_rank(part + off, r) : 0.0;
-    double s = 0.0;
+    for (int q = 0; q < RR_MAXCL; ++q) v[q] = (q < nr) ? ld_dsmem2(dsmem_addr(part + off, q)) : make_double2(0.0, 0.0);
+    double2 sum = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int r = 0; r < RR_MAXCL; ++r) s += v[r];
+    for (int q = 0; q < RR_MAXCL; ++q) {
+      sum.x += v[q].x;
+      sum.y += v[q].y;
+    }
+    const bool full = ti != tj || c >= r;  // both entries on or above the diagonal
+    const bool hi = c + 1 == r;            // only the second one (the diagonal)
 #pragma unroll
-    for (int r = 0; r < RR_MAXCL; ++r)
-      if (r < nr) *cl.map_shared_rank(tot + off, r) = s;
+    for (int q = 0; q < RR_MAXCL; ++q)
+      if (q < nr) {
+        const uint32_t a = dsmem_addr(tot + off, q);
+        if (full) {
+          st_dsmem2(a, sum);
+        } else if (hi) {
+          st_dsmem(a + 8, sum.y);
+        }
+      }
   }
   cl.sync();
 }
@@ -653,6 +797,8 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   int ts = 0;
 #define CQT() \
   if (rec) a.dbg[ts++] = clock64()
+#define FCQT(i) \
+  if (rec) a.dbg[32 + (i)] = clock64()
   CQT();
   // Rows per CTA beyond CQ_RMAX (m' > 16 x 256): the slice streams through
   // shared memory in chunks of CQ_RMAX rows; Q1 then lives in the published
@@ -740,8 +886,10 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       __syncthreads();
       store_q1(0);
       __syncthreads();
+      FCQT(0);
       // ---- P6/P7: G2 = Q1^T Q1 (partial -> A1, total -> upper A2) ----
       cq_gram(sl, R4, kk, A1);
+      FCQT(1);
     } else {
       // per chunk: Q1 = P R1^-1 -> q1g; the Q1 Gram accumulates in global scratch
       for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) gacc[e] = 0.0;
@@ -765,6 +913,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       __threadfence();
       atomicAdd(&c->q1_count, 1u);
     }
+    FCQT(2);
     // zero the upper of A2 (incl. diag) on this rank first: reduce writes it
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
       const int i = e / DMQR_KP, j = e % DMQR_KP;
@@ -791,6 +940,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     for (int j = tid; j < kk; j += PANEL_T) vpiv[DMQR_KP + j] = A2[j * DMQR_KP + j];
     __syncthreads();
     if (s_flag[0]) fail = true;
+    FCQT(3);
   }
   if (me == 0 && tid == 0) c->cq_diag[3] = jstar;
   if (a.spare && !q1_pub && tid == 0) {  // nothing to publish: release k_spare
@@ -816,10 +966,12 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
         A1[e] = x;
       }
       __syncthreads();
+      FCQT(4);
       double* Pg = a.red + 3 * DMQR_KP * DMQR_KP + (size_t)blockIdx.x * DMQR_KP * DMQR_KP;
       cq_small_gemm<true>([&](int i, int t) { return A1[t * DMQR_KP + i]; },
                           [&](int t, int j) { return A1[t * DMQR_KP + j]; }, Pg, kk);
       __syncthreads();
+      FCQT(5);
       for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
         const int i = e / DMQR_KP, j = e % DMQR_KP;
         double r = 0.0;
@@ -982,9 +1134,11 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     double* Tt = scr0 + DMQR_KP * DMQR_KP;
     cq_trinv_upper(A1, X, l);
     __syncthreads();
+    FCQT(7);
     cq_small_gemm([&](int i, int t) { return A2[i * DMQR_KP + t]; },
                   [&](int t, int j) { return X[t * DMQR_KP + j]; }, Tt, l);
     __syncthreads();
+    FCQT(8);
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
       const int i = e / DMQR_KP, j = e % DMQR_KP;
       const bool in = i < l && j < l && j >= i;
@@ -1016,6 +1170,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   CQT();
   CQT();
 #undef CQT
+#undef FCQT
   if (me == 0 && tid == 0) {
     if (a.tline) {
       a.tline[4 * (c->step_idx & 255) + 0] = t_start;

@@ -19,3 +19,5 @@ names = ["load", "gram1", "reduce1", "chol1", "trinv1", "Q1gemm", "gram2", "redu
          "Qtop", "mLU", "UY+sync", "T", "aux", "end"]
 d = np.diff(t)
 print("cta", cta, {names[i] if i < len(names) else i: int(v) for i, v in enumerate(d[:17])}, "total", int(t[17] - t[0]) if t[17] else None)
+f = out[32:48]
+print("fine (cycles from Q1gemm end):", [int(x - t[6]) if x else None for x in f])

@@ -23,6 +23,8 @@ __device__ __forceinline__ long long* tick_buf() {
   do {                                               \
     if (threadIdx.x == 0) tick_buf()[17] = clock64(); \
   } while (0)
+__device__ long long g_pub[400];
+#define CQ_DF_TRACE g_pub
 #include "panel_cq.cuh"
 
 using namespace dmqr;
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_bench(const double* G, const dou
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += blockDim.x) A1[e] = Qt[e];
     __syncthreads();
     t0 = clock64();
-    cq_mlu_ed(A1, vS + DMQR_KP, vpiv + DMQR_KP, k);
+    cq_mlu_df(A1, vS + DMQR_KP, vpiv + DMQR_KP, k, sl);
     __syncthreads();
     t1 = clock64();
     acc[7] += t1 - t0;
@@ -294,7 +296,20 @@ int main() {
   printf("latency: dfma %lld shfl %lld rsqrt %lld div %lld cq_rsqrt %lld lds-chain %lld dmul %lld dmma %lld\n", l[0], l[1], l[2], l[3], l[4], l[5], l[6], l[7]);
   unsigned long long nbad;
   cudaMemcpy(&nbad, dout + 2, 8, cudaMemcpyDeviceToHost);
-  printf("mlu_ed %lld cycles, mismatches vs cq_mlu %llu\n", c[7], nbad);
+  {
+    long long hp[96];
+    cudaMemcpyFromSymbol(hp, g_pub, sizeof(hp));
+    printf("df pivot deltas:");
+    for (int j = 1; j < k; ++j) printf(" %lld", hp[j] - hp[j - 1]);
+    printf("\n");
+    long long ht[400];
+    cudaMemcpyFromSymbol(ht, g_pub, sizeof(ht));
+    for (int j = 8; j < 14; ++j) {
+      long long* t = ht + 100 + 4 * j;
+      printf("j=%d: seen(prev) %lld top %lld shfl %lld pub %lld\n", j, t[3] - ht[j - 1], t[0] - ht[j - 1], t[1] - ht[j - 1], ht[j] - ht[j - 1]);
+    }
+  }
+  printf("mlu_df %lld cycles, mismatches vs cq_mlu %llu\n", c[7], nbad);
   printf("chol %lld trinv %lld mlu %lld small_gemm %lld gram(256) %lld slice_gemm(256) %lld sync x100 %lld  (chol ret %g)\n",
          c[0], c[1], c[2], c[3], c[4], c[5], c[6], o);
   // CPU Cholesky of G, compare with the device R
