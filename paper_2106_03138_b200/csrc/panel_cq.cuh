@@ -914,11 +914,6 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       atomicAdd(&c->q1_count, 1u);
     }
     FCQT(2);
-    // zero the upper of A2 (incl. diag) on this rank first: reduce writes it
-    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
-      const int i = e / DMQR_KP, j = e % DMQR_KP;
-      if (j >= i) A2[e] = 0.0;
-    }
     CQT();
     cq_cluster_reduce(A1, A2, kk);
     CQT();
@@ -949,39 +944,22 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     atomicAdd(&c->q1_count, 1u);
   }
   int l = kk;
-  // G2 = I + E with |E| <= CQ_NEAR_ID (the usual case): R2 = I + X from the
-  // fixed point X = Phi(E - X^T X) (Phi: strict upper + half diagonal), two
-  // terms, error O(|E|^3) -- instead of a 65-pivot Cholesky chain
+  // G2 = I + E with |E| <= CQ_NEAR_ID (the usual case): R2 = I + X with
+  // X = Phi(E) (Phi: strict upper + half diagonal) -- instead of a 65-pivot
+  // Cholesky chain.  The exact X satisfies X = Phi(E - X^T X); the dropped
+  // term is <= kk |E|^2 <= 6.5e-19 per entry, far below rounding of R2 ~ I.
   const bool near_id = !s_flag[2];
   if (!fail && kk > 0) {
     if (near_id) {
-      // ---- P8': X0 = Phi(E) -> A1; P = X0^T X0 -> scratch; R2 = I + Phi(E - P) -> A1 ----
+      // ---- P8': R2 = I + Phi(G2 - I) -> A1 ----
       for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
         const int i = e / DMQR_KP, j = e % DMQR_KP;
         double x = 0.0;
-        if (i < kk && j < kk && j >= i) {
-          const double ev = A2[e] - (i == j ? 1.0 : 0.0);
-          x = (i == j) ? 0.5 * ev : ev;
-        }
+        if (i < kk && j < kk && j >= i) x = (i == j) ? 1.0 + 0.5 * (A2[e] - 1.0) : A2[e];
         A1[e] = x;
       }
       __syncthreads();
       FCQT(4);
-      double* Pg = a.red + 3 * DMQR_KP * DMQR_KP + (size_t)blockIdx.x * DMQR_KP * DMQR_KP;
-      cq_small_gemm<true>([&](int i, int t) { return A1[t * DMQR_KP + i]; },
-                          [&](int t, int j) { return A1[t * DMQR_KP + j]; }, Pg, kk);
-      __syncthreads();
-      FCQT(5);
-      for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
-        const int i = e / DMQR_KP, j = e % DMQR_KP;
-        double r = 0.0;
-        if (i < kk && j < kk && j >= i) {
-          const double ev = A2[e] - (i == j ? 1.0 : 0.0) - Pg[e];
-          r = (i == j) ? 1.0 + 0.5 * ev : ev;
-        }
-        A1[e] = r;
-      }
-      __syncthreads();
     } else {
       // ---- P8: R2 = chol(G2) -> A1 (reads/destroys the upper of A2) ----
       if (cq_chol(A2, A1, vpiv, vpiv + DMQR_KP, kk, 1e-6) < kk) fail = true;
@@ -1038,17 +1016,12 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     __syncthreads();
   }
   auto r2_inverse = [&]() {  // R2^-1 -> A2 (R2 upper in A1)
-    if (near_id) {  // R2^-1 = I - X + X^2 (error O(|X|^3)), X = R2 - I
-      cq_small_gemm([&](int i, int t) { return A1[i * DMQR_KP + t] - (i == t ? 1.0 : 0.0); },
-                    [&](int t, int j) { return A1[t * DMQR_KP + j] - (t == j ? 1.0 : 0.0); }, A2, l);
-      __syncthreads();
+    if (near_id) {  // R2^-1 = I - X (dropped X^2: <= l |E|^2 per entry, as above)
       for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
         const int i = e / DMQR_KP, j = e % DMQR_KP;
-        if (i >= l || j >= l) continue;
-        if (j >= i) {
-          const double x = A1[i * DMQR_KP + j] - (i == j ? 1.0 : 0.0);
-          A2[i * DMQR_KP + j] = (i == j ? 1.0 : 0.0) - x + A2[i * DMQR_KP + j];
-        }
+        double x = 0.0;
+        if (i < l && j < l && j >= i) x = (i == j) ? 2.0 - A1[e] : -A1[e];
+        A2[e] = x;
       }
       __syncthreads();
     } else {
