@@ -27,6 +27,7 @@ EXPORTS = (
     "dmqr_stats_enable",
     "dmqr_stats_get",
     "dmqr_debug_panel_clocks",
+    "dmqr_debug_timeline",
 )
 
 DMQR_OK, DMQR_EINVAL, DMQR_ENONFINITE, DMQR_EZEROCOL, DMQR_ECUDA, DMQR_ECAP = 0, -1, -2, -3, -4, -5
@@ -129,6 +130,8 @@ def load() -> C.CDLL:
     lib.dmqr_stats_get.restype = None
     lib.dmqr_debug_panel_clocks.argtypes = [P, I64, I64, P]
     lib.dmqr_debug_panel_clocks.restype = C.c_int
+    lib.dmqr_debug_timeline.argtypes = [P]
+    lib.dmqr_debug_timeline.restype = C.c_int
     lib.dmqr_version.argtypes = []
     lib.dmqr_version.restype = C.c_char_p
     _lib = lib

@@ -104,6 +104,29 @@ __device__ __forceinline__ long long gtimer() {
   return t;
 }
 
+// per-step record the host polls (pinned, mapped host memory): written by
+// k_step_end with a release of seq = host enqueue index + 1
+struct __align__(16) HostRec {
+  int32_t n_s, done, la_bad, seq;
+};
+
+// debug timeline (DMQR_TIMELINE): per step and kernel, the first CTA's start
+// (after its dependency wait) and the last CTA's exit, globaltimer ns
+__device__ unsigned long long g_tl[64 * 32];
+__constant__ int g_tl_on;
+struct TLSpan {
+  int slot;
+  __device__ __forceinline__ TLSpan(int step, int k) : slot(-1) {
+    if (threadIdx.x == 0 && g_tl_on) {
+      slot = (step & 63) * 32 + 2 * k;
+      atomicMin(&g_tl[slot], (unsigned long long)gtimer());
+    }
+  }
+  __device__ __forceinline__ ~TLSpan() {
+    if (slot >= 0) atomicMax(&g_tl[slot + 1], (unsigned long long)gtimer());
+  }
+};
+
 // leading dimension of the published Q1 buffer (host: lda_of), multiple of 8
 __host__ __device__ __forceinline__ int64_t q1_ld(int64_t m) { return (m > 0 ? (m + 7) / 8 * 8 : 8) + 8; }
 

@@ -194,12 +194,6 @@ cudaError_t pdl_launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
-struct HostHead {  // the prefix of Ctl the host polls
-  int32_t n_s, done, stopped, status;
-  int32_t step_idx, n_swaps, rank, n_factored;
-  int32_t la_bad, pad4;
-};
-static_assert(offsetof(Ctl, la_bad) - offsetof(Ctl, n_s) == offsetof(HostHead, la_bad), "HostHead mirrors Ctl");
 
 }  // namespace
 
@@ -322,12 +316,13 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
   // still in flight -- every step accepts at least one).  Grids are therefore
   // upper bounds; kernels read the true extents from Ctl and exit surplus
   // CTAs, and steps enqueued after `done` exit at once.
-  static thread_local HostHead* hh = nullptr;  // pinned poll slots, one pair per host thread
+  static thread_local HostRec* hrec = nullptr;  // pinned poll slots, one pair per host thread
   static thread_local cudaEvent_t hev[2] = {nullptr, nullptr};
-  if (!hh) {
-    CK(cudaMallocHost(&hh, 2 * sizeof(HostHead)));
+  if (!hrec) {
+    CK(cudaMallocHost(&hrec, 2 * sizeof(HostRec)));
     for (auto& e : hev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
+  for (int q = 0; q < 2; ++q) ((volatile HostRec*)hrec)[q].seq = -1;
   const bool prof = g_prof.load() != 0;
   cudaEvent_t ev[2][5];
   if (prof)
@@ -341,6 +336,15 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
   const int max_cluster = cluster16 ? 16 : 8;
   const bool use_cq = getenv("DMQR_NO_CHOLQR") == nullptr;  // debug switch: Householder panel only
   long long* tline = getenv("DMQR_TIMELINE") ? pdbg : nullptr;  // debug: panel / k_spare timestamps
+  {
+    const int on = tline ? 1 : 0;
+    if (tline) {
+      static unsigned long long init[64 * 32];
+      for (int q = 0; q < 64 * 32; ++q) init[q] = (q & 1) ? 0ull : ~0ull;
+      CK(cudaMemcpyToSymbolAsync(g_tl, init, sizeof(init), 0, cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaMemcpyToSymbolAsync(g_tl_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+  }
   const bool trail_persistent = getenv("DMQR_TRAIL_PERSISTENT") != nullptr;  // A/B switch
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
 
@@ -353,7 +357,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
   // that needed one for most trailing columns (la_bad, with nothing left
   // pending), and the host then stays serial: flush + k_set_la(0).
   bool la_on = false, la_off = false, want_serial = false;
-  auto enqueue_step = [&](int64_t host_ns) -> int {
+  auto enqueue_step = [&](int64_t host_ns, int eidx) -> int {
     const int64_t mp = m - host_ns;
     const int64_t np = n - host_ns;
     if (la_on && want_serial && !la_off) {
@@ -554,12 +558,10 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
       if (p->trace_norms) { k_norm_trace<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, tbits); NOTE_LAUNCH(); }
     }
     CK(pdl_launch(k_step_end, dim3(1), dim3(32), 0, st, ctl, srec, norm_trace, tbits, (const double*)A, Z, ldz, u,
-                  uref, upd));
+                  uref, upd, hrec, eidx));
     NOTE_LAUNCH();
     PROF(4);
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(&hh[slot], &ctl->n_s, sizeof(HostHead), cudaMemcpyDeviceToHost, st));
-    CK(cudaEventRecord(hev[slot], st));
     return 0;
   };
 
@@ -570,7 +572,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
   auto stream_cols = [&](int64_t upto, cudaEvent_t after) -> int {
     upto = std::min(upto, n);
     if (!host_packed || upto <= copied || m == 0) return 0;
-    CK(cudaStreamWaitEvent(sCopy, after, 0));
+    if (after) CK(cudaStreamWaitEvent(sCopy, after, 0));
     CK(cudaMemcpy2DAsync(host_packed + copied * host_ld, sizeof(double) * host_ld, A + copied * lda,
                          sizeof(double) * lda, sizeof(double) * m, (size_t)(upto - copied), cudaMemcpyDeviceToHost,
                          sCopy));
@@ -582,8 +584,22 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
   bool finished = (kmax == 0);
   auto consume = [&]() -> int {
     const int sl = known & 1;
-    CK(cudaEventSynchronize(hev[sl]));
+    // poll the step's record (k_step_end posts it); check the stream now and
+    // then so that a failed launch cannot hang the loop
+    volatile HostRec* r = hrec + sl;
+    for (long spins = 1; r->seq != known + 1; ++spins) {
+      if ((spins & 1023) == 0) {
+        const cudaError_t e = cudaStreamQuery(st);
+        if (e != cudaSuccess && e != cudaErrorNotReady) return DMQR_ECUDA;
+        if (e == cudaSuccess && r->seq != known + 1) {
+          std::atomic_thread_fence(std::memory_order_seq_cst);
+          if (r->seq != known + 1) return DMQR_ECUDA;  // stream drained, no record
+        }
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
     if (prof) {
+      CK(cudaEventSynchronize(ev[sl][4]));
       for (int q = 0; q < 4; ++q) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev[sl][q], ev[sl][q + 1]));
@@ -591,11 +607,11 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
       }
       g_acc.steps += 1;
     }
-    known_ns = hh[sl].n_s;
+    known_ns = r->n_s;
     ++known;
-    if (hh[sl].done) finished = true;
-    if (hh[sl].la_bad) want_serial = true;
-    return stream_cols(known_ns, hev[sl]);  // columns left of n_s are final
+    if (r->done) finished = true;
+    if (r->la_bad) want_serial = true;
+    return stream_cols(known_ns, nullptr);  // columns left of n_s are final (and written)
   };
   while (!finished) {
     if (enq - known >= 2) {
@@ -612,7 +628,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
       break;
     }
     slot = enq & 1;
-    int rc = enqueue_step(ns_lo);
+    int rc = enqueue_step(ns_lo, enq);
     if (rc) return rc;
     prev_ns_lo = ns_lo;
     ++enq;
@@ -781,6 +797,14 @@ void dmqr_stats_get(dmqr_stats* out, int32_t reset) {
 int dmqr_debug_panel_clocks(const void* workspace, int64_t m, int64_t n, int64_t* out) {
   const Layout L = layout(m, n);
   CK(cudaMemcpy(out, (const unsigned char*)workspace + L.pdbg, sizeof(long long) * 64 * 16, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+/* debug: per-step kernel spans of the last factorization run with
+ * DMQR_TIMELINE set: out[64 * 32], step s, kernel k -> [32 s + 2 k] first
+ * start, [32 s + 2 k + 1] last exit (globaltimer ns) */
+int dmqr_debug_timeline(int64_t* out) {
+  CK(cudaMemcpyFromSymbol(out, g_tl, sizeof(unsigned long long) * 64 * 32));
   return 0;
 }
 

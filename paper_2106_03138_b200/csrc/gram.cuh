@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __
                                                  int64_t ldz, const uint8_t* __restrict__ upd) {
   pdl_enter();
   const CtlSnap S = snap(c);
+  TLSpan tl_span(S.step_idx, 1);
   if (S.done) return;
   const bool pendu = S.la && S.pend;
   if (S.kind != 0 && !pendu) return;
@@ -321,6 +322,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
   const long long t_in = gtimer();
   pdl_enter();
   const CtlSnap S = snap(c);
+  TLSpan tl_span(S.step_idx, 2);
   if (S.done) return;
 #define GFT(k) \
   if (tline && threadIdx.x == 0) tline[512 + 8 * (S.step_idx & 63) + (k)] = gtimer()

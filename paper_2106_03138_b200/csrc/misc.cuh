@@ -67,13 +67,11 @@ __global__ void __launch_bounds__(1024) k_init(InitArgs a) {
 }
 
 // Append the step record and advance n_s (single thread, last kernel of a step).
-__global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, double* __restrict__ norm_trace,
-                           unsigned long long* __restrict__ trace_bits, const double* __restrict__ A,
-                           double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
-                           double* __restrict__ uref, uint8_t* __restrict__ upd) {
-  pdl_enter();
-  const CtlSnap S = snap(c);
-  if (S.done) return;
+__device__ __forceinline__ void step_end_body(const CtlSnap& S, Ctl* __restrict__ c, StepRec* __restrict__ steps,
+                                              double* __restrict__ norm_trace,
+                                              unsigned long long* __restrict__ trace_bits, const double* __restrict__ A,
+                                              double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
+                                              double* __restrict__ uref, uint8_t* __restrict__ upd) {
   // look-ahead with no trailing columns past tc0: k_trail_a had no tile to do
   // the panel-column bookkeeping (one warp does it here)
   if (S.la && S.tc0 >= S.n) la_panel_columns(c, A, Wt, ldz, u, uref, upd, S.n_s, S.l_acc, S.tc0);
@@ -118,6 +116,29 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
   c->nsw = 0;
   c->nmv = 0;
   if (S.n_s + l >= S.kmax) c->done = 1;
+}
+
+__global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, double* __restrict__ norm_trace,
+                           unsigned long long* __restrict__ trace_bits, const double* __restrict__ A,
+                           double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
+                           double* __restrict__ uref, uint8_t* __restrict__ upd, HostRec* __restrict__ hrec,
+                           int enq) {
+  pdl_enter();
+  const CtlSnap S = snap(c);
+  TLSpan tl_span(S.step_idx, 10);
+  if (!S.done) step_end_body(S, c, steps, norm_trace, trace_bits, A, Wt, ldz, u, uref, upd);
+  // the host's poll record of this step (no stream operation between the
+  // steps, so the programmatic launches chain across step boundaries)
+  // (columns left of n_s are final once the record is seen: this warp's own
+  // writes to them are fenced first; the record itself is one 16-byte store)
+  __threadfence();
+  __syncwarp();
+  if (threadIdx.x == 0 && hrec) {
+    const int4 rec = make_int4(c->n_s, c->done, c->la_bad, enq + 1);
+    asm volatile("st.volatile.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(hrec + (enq & 1)), "r"(rec.x), "r"(rec.y),
+                 "r"(rec.z), "r"(rec.w)
+                 : "memory");
+  }
 }
 
 // switch the control block to the look-ahead schedule (from the next kernel on)

@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(SWAP_T) k_swap(Ctl* __restrict__ c, double* __
                                                  uint8_t* __restrict__ upd) {
   pdl_enter();
   const CtlSnap S = snap(c);
+  TLSpan tl_span(S.step_idx, 3);
   if (S.done) return;
   const int nmv = S.nmv;
   const int64_t m = S.m, lda = S.lda;

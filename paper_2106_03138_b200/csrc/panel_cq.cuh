@@ -494,116 +494,6 @@ __device__ void cq_mlu(double* A, double* vS, double* vpiv, int l) {
   }
 }
 
-// shared-memory flag with acquire/release ordering (CTA scope)
-__device__ __forceinline__ int lds_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
-  return v;
-}
-// (shared-memory accesses of one warp are performed in order, so after the
-// __syncwarp that precedes it a plain volatile store publishes the warp's
-// earlier shared stores; MEMBAR.CTA of st.release costs ~1000 cycles here)
-__device__ __forceinline__ void sts_release(int* p, int v) {
-  asm volatile("st.volatile.shared::cta.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
-}
-
-// Modified LU as above (same in/out contract), as a dataflow over the 16
-// warps: column c lives in registers of warp c % 16 (lane = row, 3 rows per
-// lane).  Pivot j's owner publishes its multipliers (column-major, in Lc) and
-// bumps a counter; every warp applies pivot j to its own columns as soon as it
-// is out -- so the chain is one pivot after another with no block barriers,
-// and the next pivot's column is always up to date when its pivot arrives.
-__device__ void cq_mlu_df(double* A, double* vS, double* vpiv, int l, double* Lc) {
-  static_assert(PANEL_T == 512, "16 warps own the columns");
-  constexpr int NW = 16, NC = (DMQR_MAXK + NW - 1) / NW;
-  __shared__ int s_npub;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  double q[NC][3];
-#pragma unroll
-  for (int k = 0; k < NC; ++k)
-#pragma unroll
-    for (int s = 0; s < 3; ++s) {
-      const int c = wid + NW * k, i = lane + 32 * s;
-      q[k][s] = (c < l && i < l) ? A[i * DMQR_KP + c] : 0.0;
-    }
-  const int cmax = (wid < l) ? wid + NW * ((l - 1 - wid) / NW) : -1;  // my last column
-  if (tid == 0) s_npub = 0;
-  __syncthreads();
-  for (int j = 0; j < l; ++j) {
-    const int lj = j & 31, sj = j >> 5, oj = j % NW, kj = j / NW;
-    if (wid != oj && cmax <= j) break;  // no columns right of j left
-#ifdef CQ_DF_TRACE
-    if (lane == 0 && wid == oj) CQ_DF_TRACE[100 + 4 * j] = clock64();
-#endif
-    // row j of my columns (final: pivots < j are applied)
-    double u[NC];
-#pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      const double v = (sj == 0) ? q[k][0] : ((sj == 1) ? q[k][1] : q[k][2]);
-      u[k] = __shfl_sync(0xffffffffu, v, lj);
-    }
-    double Lv[3];
-#ifdef CQ_DF_TRACE
-    if (lane == 0 && wid == oj) CQ_DF_TRACE[100 + 4 * j + 1] = clock64() + (long long)(u[0] * 0.0);
-#endif
-    if (wid == oj) {
-      double qjj = 0.0;
-#pragma unroll
-      for (int k = 0; k < NC; ++k)
-        if (k == kj) qjj = u[k];
-      const double sg = (qjj >= 0.0) ? -1.0 : 1.0;  // S_j = -sign(q'_jj), sign(+0) = +
-      const double pv = 1.0 - sg * qjj;             // pivot = 1 + |q'_jj|
-      const double f0 = -sg * cq_rcp12(pv);
-#pragma unroll
-      for (int k = 0; k < NC; ++k)
-        if (k == kj)
-#pragma unroll
-          for (int s = 0; s < 3; ++s) {
-            const int i = lane + 32 * s;
-            Lv[s] = (i > j) ? f0 * q[k][s] : 0.0;
-            q[k][s] = (i > j) ? Lv[s] : q[k][s];
-          }
-#pragma unroll
-      for (int s = 0; s < 3; ++s)
-        if (lane + 32 * s < DMQR_KP) Lc[j * DMQR_KP + lane + 32 * s] = Lv[s];
-      if (lane == 0) {
-        vS[j] = sg;
-        vpiv[j] = pv;
-      }
-      __syncwarp();
-      if (lane == 0) sts_release(&s_npub, j + 1);
-#ifdef CQ_DF_TRACE
-      if (lane == 0) CQ_DF_TRACE[j] = clock64();
-#endif
-    } else {
-      const bool next = (wid == (j + 1) % NW);  // owner of the next pivot: poll hard
-      while (lds_acquire(&s_npub) <= j) {
-        if (!next) __nanosleep(100);
-      }
-#ifdef CQ_DF_TRACE
-      if (lane == 0 && wid == (j + 1) % NW) CQ_DF_TRACE[100 + 4 * (j + 1) + 3] = clock64();
-#endif
-#pragma unroll
-      for (int s = 0; s < 3; ++s) Lv[s] = (lane + 32 * s < DMQR_KP) ? Lc[j * DMQR_KP + lane + 32 * s] : 0.0;
-    }
-    // q'_ic -= L_ij q'_jc for my columns c > j (rows <= j have L = 0)
-#pragma unroll
-    for (int k = 0; k < NC; ++k)
-      if (wid + NW * k > j)
-#pragma unroll
-        for (int s = 0; s < 3; ++s) q[k][s] = fma(-Lv[s], u[k], q[k][s]);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < NC; ++k)
-#pragma unroll
-    for (int s = 0; s < 3; ++s) {
-      const int c = wid + NW * k, i = lane + 32 * s;
-      if (c < l && i < l) A[i * DMQR_KP + c] = q[k][s];
-    }
-  __syncthreads();
-}
-
 // slice[:, 0:ncol] <- slice[:, 0:kin] * M (M: kin x ncol upper triangular, KP row-major) in place,
 // rows [0, R); each warp owns 8-row tiles (DMMA 8x8x4, accumulators in registers).
 __device__ void cq_slice_gemm(double* sl, int R, int kin, int ncol, const double* M) {
@@ -771,6 +661,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   Ctl* c = a.c;
   const long long t_start = gtimer();
   const CtlSnap S = snap(c);
+  TLSpan tl_span(S.step_idx, 4);
   if (S.done) return;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double cqs[];
@@ -1170,6 +1061,7 @@ __global__ void __launch_bounds__(256) k_ygemm(Ctl* __restrict__ c, double* __re
                                                const double* __restrict__ q1g, const double* __restrict__ gM) {
   pdl_enter();
   const CtlSnap S = snap(c);
+  TLSpan tl_span(S.step_idx, 6);
   if (S.done || S.cq_fail) return;
   const int l = S.l_acc;
   const int64_t n_s = S.n_s, m = S.m, lda = S.lda, mp = m - n_s;

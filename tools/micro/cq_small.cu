@@ -23,83 +23,10 @@ __device__ __forceinline__ long long* tick_buf() {
   do {                                               \
     if (threadIdx.x == 0) tick_buf()[17] = clock64(); \
   } while (0)
-__device__ long long g_pub[400];
-#define CQ_DF_TRACE g_pub
 #include "panel_cq.cuh"
 
 using namespace dmqr;
 
-
-// ---- experiment: element-distributed modified LU, one barrier per step ----
-__device__ void cq_mlu_ed(double* A, double* vS, double* vpiv, int l) {
-  __shared__ double colj[2][DMQR_KP], rowj[2][DMQR_KP];
-  const int tid = threadIdx.x;
-  const int nt4 = (l + 3) / 4;               // 4x4 tiles per dimension
-  const bool own = tid < nt4 * nt4;
-  const int ti = own ? tid / nt4 : 0, tj = own ? tid % nt4 : 0;
-  const int i0 = ti * 4, c0 = tj * 4;
-  double v[4][4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) v[r][cc] = (own && i0 + r < l && c0 + cc < l) ? A[(i0 + r) * DMQR_KP + c0 + cc] : 0.0;
-  // publish column 0 and row 0
-  if (own && tj == 0)
-#pragma unroll
-    for (int r = 0; r < 4; ++r) colj[0][i0 + r] = v[r][0];
-  if (own && ti == 0)
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) rowj[0][c0 + cc] = v[0][cc];
-  __syncthreads();
-  for (int j = 0; j < l; ++j) {
-    const int b = j & 1, nb = b ^ 1;
-    const double qjj = rowj[b][j];
-    const double sg = (qjj >= 0.0) ? -1.0 : 1.0;
-    const double pv = 1.0 - sg * qjj;
-    const double f0 = -sg * cq_rcp12(pv);
-    if (own) {
-      double Li[4], Rc[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) Li[r] = (i0 + r > j) ? f0 * colj[b][i0 + r] : 0.0;
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) Rc[cc] = (c0 + cc > j) ? rowj[b][c0 + cc] : 0.0;
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) v[r][cc] -= Li[r] * Rc[cc];
-      // multipliers into column j
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc)
-        if (c0 + cc == j)
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-            if (i0 + r > j) v[r][cc] = Li[r];
-      // publish column j+1 (rows > j+1) and row j+1 (cols >= j+1)
-      const int j1 = j + 1;
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc)
-        if (c0 + cc == j1)
-#pragma unroll
-          for (int r = 0; r < 4; ++r) colj[nb][i0 + r] = v[r][cc];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (i0 + r == j1)
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc) rowj[nb][c0 + cc] = v[r][cc];
-    }
-    if (tid == 0) {
-      vS[j] = sg;
-      vpiv[j] = pv;
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc)
-      if (own && i0 + r < l && c0 + cc < l) A[(i0 + r) * DMQR_KP + c0 + cc] = v[r][cc];
-  __syncthreads();
-}
 
 __global__ void __launch_bounds__(PANEL_T, 1) k_bench(const double* G, const double* Qt, const double* P, int k, int R,
                                                       long long* cyc, double* out) {
@@ -142,23 +69,26 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_bench(const double* G, const dou
     __syncthreads();
     CQ_TICK0();
     t0 = clock64();
-    cq_mlu(A1, vS, vpiv, k);
+    cq_mlu<DMQR_KP>(A1, vS, vpiv, k);
     __syncthreads();
     t1 = clock64();
     acc[2] += t1 - t0;
-    // element-distributed LU on the same input; compare with cq_mlu's result
+    // the same LU with an odd row stride (73) on a copy; compare
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += blockDim.x) A2[e] = A1[e];  // cq_mlu result
-    for (int e = tid; e < DMQR_KP * DMQR_KP; e += blockDim.x) A1[e] = Qt[e];
+    for (int e = tid; e < DMQR_KP * (DMQR_KP + 1); e += blockDim.x) {
+      const int i = e / (DMQR_KP + 1), j = e % (DMQR_KP + 1);
+      sl[e] = (j < DMQR_KP) ? Qt[i * DMQR_KP + j] : 0.0;
+    }
     __syncthreads();
     t0 = clock64();
-    cq_mlu_df(A1, vS + DMQR_KP, vpiv + DMQR_KP, k, sl);
+    cq_mlu<DMQR_KP + 1>(sl, vS + DMQR_KP, vpiv + DMQR_KP, k);
     __syncthreads();
     t1 = clock64();
     acc[7] += t1 - t0;
     if (rep == 0) {
-      for (int e = tid; e < DMQR_KP * DMQR_KP; e += blockDim.x) {
-        const double d = fabs(A1[e] - A2[e]);
-        if (d > 1e-13) atomicAdd((unsigned long long*)&out[2], 1ull);
+      for (int e = tid; e < k * DMQR_KP; e += blockDim.x) {
+        const int i = e / DMQR_KP, j = e % DMQR_KP;
+        if (j < k && sl[i * (DMQR_KP + 1) + j] != A2[e]) atomicAdd((unsigned long long*)&out[2], 1ull);
       }
     }
     // small gemm upper x upper
@@ -296,20 +226,7 @@ int main() {
   printf("latency: dfma %lld shfl %lld rsqrt %lld div %lld cq_rsqrt %lld lds-chain %lld dmul %lld dmma %lld\n", l[0], l[1], l[2], l[3], l[4], l[5], l[6], l[7]);
   unsigned long long nbad;
   cudaMemcpy(&nbad, dout + 2, 8, cudaMemcpyDeviceToHost);
-  {
-    long long hp[96];
-    cudaMemcpyFromSymbol(hp, g_pub, sizeof(hp));
-    printf("df pivot deltas:");
-    for (int j = 1; j < k; ++j) printf(" %lld", hp[j] - hp[j - 1]);
-    printf("\n");
-    long long ht[400];
-    cudaMemcpyFromSymbol(ht, g_pub, sizeof(ht));
-    for (int j = 8; j < 14; ++j) {
-      long long* t = ht + 100 + 4 * j;
-      printf("j=%d: seen(prev) %lld top %lld shfl %lld pub %lld\n", j, t[3] - ht[j - 1], t[0] - ht[j - 1], t[1] - ht[j - 1], ht[j] - ht[j - 1]);
-    }
-  }
-  printf("mlu_df %lld cycles, mismatches vs cq_mlu %llu\n", c[7], nbad);
+  printf("mlu(ld 73) %lld cycles, mismatches vs cq_mlu %llu\n", c[7], nbad);
   printf("chol %lld trinv %lld mlu %lld small_gemm %lld gram(256) %lld slice_gemm(256) %lld sync x100 %lld  (chol ret %g)\n",
          c[0], c[1], c[2], c[3], c[4], c[5], c[6], o);
   // CPU Cholesky of G, compare with the device R

@@ -31,3 +31,37 @@ for i, r in enumerate(g[:12]):
     if r[0] == 0:
         continue
     print(i, [round(float(x - r[0]) / 1e3, 1) if x else None for x in r[1:8]])
+
+# ---- kernel spans (dmqr_debug_timeline): start after the dependency wait, end at the last CTA exit
+names = ["select", "gram", "gfinish", "swap", "panel", "spare", "ygemm", "trail_w", "trail_a", "guard", "step_end"]
+tl = np.zeros(64 * 32, dtype=np.int64)
+_lib.load().dmqr_debug_timeline(tl.ctypes.data_as(C.c_void_p))
+tl = tl.reshape(64, 32)
+ns = int(f.info.n_steps)
+U64MAX = np.int64(-1)
+rows = []
+for s in range(min(ns, 64)):
+    r = tl[s]
+    t0 = r[0]
+    if t0 in (0, U64MAX):
+        continue
+    spans = {}
+    for k, nm in enumerate(names):
+        a, b = r[2 * k], r[2 * k + 1]
+        if a == U64MAX or b == 0:
+            continue
+        spans[nm] = ((a - t0) / 1e3, (b - t0) / 1e3)
+    nxt = tl[s + 1][0] if s + 1 < 64 and tl[s + 1][0] not in (0, U64MAX) else None
+    rows.append((s, spans, (nxt - t0) / 1e3 if nxt is not None else None))
+print("\nstep: kernel [start, end] us from the step's k_select start; 'next' = next step's k_select start")
+for s, spans, nxt in rows[:4] + rows[len(rows) // 2: len(rows) // 2 + 2]:
+    print(s, " ".join(f"{k}[{a:.1f},{b:.1f}]" for k, (a, b) in spans.items()), f"next {nxt}")
+mid = [r for r in rows if 4 <= r[0] < len(rows) - 8]
+if mid:
+    print("\nmean over steps 4..%d (us): start / end / dur" % (len(rows) - 9))
+    for nm in names:
+        v = [r[1][nm] for r in mid if nm in r[1]]
+        if v:
+            a = np.mean([x[0] for x in v]); b = np.mean([x[1] for x in v])
+            print(f"  {nm:9s} {a:7.1f} {b:7.1f} {b - a:7.1f}  (n={len(v)})")
+    print("  step      ", np.mean([r[2] for r in mid if r[2]]))
