@@ -521,6 +521,74 @@ def qrdm2(A, **kw) -> OracleResult:
     return qrdm_engine(A, break_check=True, **kw)
 
 
+def qrp(A, stop_rule=STOP_EPS_N, epsilon=EPS, trace_norms=False, margins=False, max_steps=0) -> OracleResult:
+    """QR with greedy column pivoting -- rrqr.py:238-291 (one _scalar_step,
+    rrqr.py:219-235, then downdate_norms(s, s+1) per column)."""
+    work = as_work(A)
+    m, n = work.shape
+    fwd = np.arange(n, dtype=np.intp)
+    swaps: list = []
+    u = col_norms(work)
+    uref = u.copy()
+    a0 = float(u.max(initial=0.0))
+    kmax = min(m, n)
+    coeffs = np.zeros(kmax)
+    rank1 = 0.0
+    total = 2.0 * m * n
+    steps: list = []
+    ntrace: list = []
+    mg = _Margins(a0) if margins else None
+    eps1 = _eps1(stop_rule, epsilon, n)
+    rank = None
+    done = 0
+    for s in range(kmax):
+        if max_steps and s >= max_steps:
+            break
+        umax = float(u[s:].max())
+        if eps1 is not None:  # check_stop, rrqr.py:189-203
+            lhs = math.sqrt(n - s) * umax
+            rhs = eps1 * a0
+            if mg is not None and rhs > 0:
+                mg.note("stop", abs(lhs - rhs) / rhs, umax)
+            if lhs <= rhs:
+                rank = s
+                if mg is not None:
+                    mg.end_step(s)
+                break
+        j = s + int(np.argmax(u[s:]))
+        if mg is not None:
+            rest = np.delete(u[s:], j - s)
+            if rest.size:
+                mg.note("argmax", float((umax - rest.max()) / umax) if umax > 0 else 0.0, umax)
+        _swap(work, u, uref, fwd, swaps, s, j)
+        v, cf, beta = householder(work[s:, s])
+        coeffs[s] = cf
+        if s + 1 < n:
+            reflect_left(v, cf, work[s:, s + 1:])
+            rank1 += 4.0 * (m - s) * (n - s - 1)
+            total += 4.0 * (m - s) * (n - s - 1)
+        work[s, s] = beta
+        work[s + 1:, s] = v[1:]
+        total += 4.0 * (m - s) + (n - s)
+        nh = _downdate(u, uref, work, s, s + 1)
+        total += 4.0 * (n - s - 1)
+        if trace_norms:
+            _norm_check(ntrace, u, work, s + 1, a0)
+        steps.append(Step(s, 1, 1))
+        if mg is not None:
+            mg.count("guard_recomputes", nh)
+            mg.end_step(s)
+        done = s + 1
+    stopped = rank is not None
+    if rank is None:
+        if stop_rule == STOP_NONE:
+            rank = int(np.count_nonzero(np.abs(work.diagonal()[:done]) > EPS * n * a0))  # rrqr.py:206-208
+        else:
+            rank = done
+    return OracleResult(work, coeffs, fwd, swaps, rank, steps, done, stopped, (rank1, 0.0, total), ntrace,
+                        mg.summary() if mg is not None else {})
+
+
 def explicit_q(packed: np.ndarray, coeffs: np.ndarray, n_factored: int, ncols=None):
     """Q (m x ncols, default m) by backward reflector accumulation -- rrqr.py:459-480."""
     m = packed.shape[0]

@@ -59,12 +59,15 @@ def sha(a: np.ndarray) -> str:
 
 def run_ref(A, algo, params, stop):
     _KMAX.clear()
-    fn = R.qrdm2 if algo == "qrdm2" else R.qrdm
-    res = fn(A, params=params, stop=stop)
+    if algo == "qrp":  # rrqr.py:238-291 (no DM selection, no params)
+        res = R.qrp(A, stop=stop)
+    else:
+        fn = R.qrdm2 if algo == "qrdm2" else R.qrdm
+        res = fn(A, params=params, stop=stop)
     kmax_iter = iter(list(_KMAX))
     steps = []
     for rec in res.step_log:
-        km = -1 if rec.fell_back_to_scalar else next(kmax_iter)
+        km = -1 if (rec.fell_back_to_scalar or algo == "qrp") else next(kmax_iter)
         steps.append([rec.n_s, rec.k_selected, rec.k_accepted, int(rec.broke_early),
                       int(rec.fell_back_to_scalar), km])
     steps = np.array(steps, dtype=np.int64).reshape(-1, 6)
@@ -181,6 +184,30 @@ def main():
     r36 = np.random.default_rng(36)
     A = r36.standard_normal((12, 4)) @ r36.standard_normal((4, 10))
     add("kat/fallback", A, "qrdm", D, NONE, "test_rrqr.py:118-123", keep_packed=True, keep_input=True)
+
+    # 6. qrp (greedy column pivoting, rrqr.py:238-291): the blocked scalar-pivot
+    #    engine's pins (it also runs QRDM's scalar-fallback runs)
+    for i, (name, A) in enumerate(dmqr.fixture_suite()):
+        add(f"qrp/fix/{name}", A, "qrp", D, EPSN if i % 2 == 0 else NONE, "fixture",
+            keep_packed=A.shape[0] * A.shape[1] <= 96 * 96 and i % 3 == 0)
+    add("qrp/cfg1", A1, "qrp", D, EPSN, "inputs.cfg1(seed=0)")
+    add("qrp/cfg1_none", A1, "qrp", D, NONE, "inputs.cfg1(seed=0)")
+    add("qrp/cfg5s/1024", inputs.cfg5(seed=4, n=1024), "qrp", D, EPSN, "inputs.cfg5(seed=4,n=1024)")
+    rq = np.random.default_rng(238)
+    for t in range(12):
+        m = int(rq.integers(1, 100))
+        n = int(rq.integers(1, 100))
+        if t % 3 == 0:
+            A = rq.standard_normal((m, n))
+        elif t % 3 == 1:
+            r = int(rq.integers(1, min(m, n) + 1))
+            A = rq.standard_normal((m, r)) @ rq.standard_normal((r, n))
+        else:
+            A = rq.standard_normal((m, n)) * np.logspace(0, -14, n)
+        st = (EPSN, SQRT, NONE)[t % 3]
+        add(f"qrp/knob/{t}", A, "qrp", D, st, "make_golden rng(238)", keep_packed=True, keep_input=True)
+    add("qrp/kat/zeros", np.zeros((5, 4)), "qrp", D, EPSN, "zeros", keep_packed=True, keep_input=True)
+    add("qrp/kat/identity6", np.eye(6), "qrp", D, NONE, "eye(6)", keep_packed=True, keep_input=True)
 
     np.savez_compressed(HERE / "golden.npz", **store)
     (HERE / "golden_index.json").write_text(json.dumps(index, indent=1, sort_keys=True))

@@ -46,7 +46,8 @@ def case_input(name: str) -> np.ndarray:
     from paper_2106_03138_b200 import inputs
     src = meta["source"]
     if src == "fixture":
-        return _fixtures()[name.split("/")[1]]
+        parts = name.split("/")
+        return _fixtures()[parts[2] if parts[0] == "qrp" else parts[1]]
     if src.startswith("inputs.cfg1"):
         return inputs.cfg1(seed=0)
     if src.startswith("inputs.cfg2"):

@@ -20,9 +20,12 @@ def _check(name):
     meta = G.index()["cases"][name]
     A = G.case_input(name)
     assert G.sha(A) == meta["input_sha256"], "input generator does not reproduce the reference input"
-    fn = O.qrdm2 if meta["algo"] == "qrdm2" else O.qrdm
     with threadpool_limits(1):
-        res = fn(A, **G.oracle_kwargs(name))
+        if meta["algo"] == "qrp":
+            res = O.qrp(A, stop_rule=meta["stop"])
+        else:
+            fn = O.qrdm2 if meta["algo"] == "qrdm2" else O.qrdm
+            res = fn(A, **G.oracle_kwargs(name))
     f = lambda k: G.case_field(name, k)  # noqa: E731
     assert np.array_equal(res.forward, f("forward"))
     assert np.array_equal(np.array(res.swaps, dtype=np.int64).reshape(-1, 2), f("swaps"))
@@ -32,7 +35,8 @@ def _check(name):
     assert np.array_equal(res.r_diagonal(), f("diag"))
     assert np.array_equal(res.coeffs, f("coeffs"))
     steps = np.array([[s.n_s, s.k_selected, s.k_accepted, int(s.broke_early),
-                       int(s.fell_back_to_scalar), -1 if s.fell_back_to_scalar else s.k_max]
+                       int(s.fell_back_to_scalar),
+                       -1 if (s.fell_back_to_scalar or meta["algo"] == "qrp") else s.k_max]
                       for s in res.steps], dtype=np.int64).reshape(-1, 6)
     assert np.array_equal(steps, f("steps"))
     eg = np.array([[s.eps_s, s.gamma] for s in res.steps]).reshape(-1, 2)
@@ -56,6 +60,12 @@ def test_oracle_bit_exact_vs_reference_midsize(name):
 def test_fixture_count_is_40():
     import fixture_suite
     assert len(fixture_suite.suite()) == 40
+
+
+def test_qrp_cases_present():
+    names = G.case_names("qrp/")
+    assert len(names) >= 50
+    assert any(G.index()["cases"][c]["stop"] == "none" for c in names)
 
 
 def test_cfg1_rank_384():
