@@ -118,6 +118,27 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
                          void* stream);
 
 /*
+ * QR with greedy column pivoting (replaces qrp, rrqr.py:238-291): the pivot is
+ * the trailing column of largest partial norm (first index on ties), one
+ * Householder reflector per column, norms downdated with the reference's
+ * guard (rrqr.py:161-186) and the same stop rules.  It runs on the blocked
+ * scalar-pivot engine (delayed C -= Y F^T updates, LAPACK laqps form) that
+ * also executes QRDM's scalar-fallback runs (rrqr.py:343-353).  Same buffers
+ * as dmqr_qrdm_stream_f64; of `params` only stop_rule, epsilon, trace_norms
+ * and max_steps are used (tau / delta / k_dm must still be valid).  Step
+ * records are StepRecord(n_s=s, k_selected=1, k_accepted=1) with k_max = 0.
+ */
+int dmqr_qrp_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* params,
+                 double* coeffs, int64_t* perm, int64_t* swaps, int64_t swap_cap,
+                 dmqr_step* steps, int64_t step_cap, double* norm_trace, void* workspace,
+                 size_t ws_bytes, dmqr_info* info, void* stream);
+int dmqr_qrp_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* params,
+                        double* coeffs, int64_t* perm, int64_t* swaps, int64_t swap_cap,
+                        dmqr_step* steps, int64_t step_cap, double* norm_trace, void* workspace,
+                        size_t ws_bytes, dmqr_info* info, double* host_packed, int64_t host_ld,
+                        void* stream);
+
+/*
  * Batched QRDM / QRDM2 over `batch` independent m x n matrices stored at
  * A + b*stride (cfg3: batches of small matrices).  The batch is spread over
  * `nlanes` concurrent CUDA streams (one host thread each, every lane running
@@ -160,6 +181,7 @@ typedef struct dmqr_stats {
   double ms_panel;     /* Householder panel + T factor */
   double ms_trailing;  /* V = Y T^T, Z = Y^T C, C -= V Z */
   double ms_norms;     /* downdate + guard recompute + step record */
+  double ms_pivot;     /* blocked scalar pivoting: qrp, and QRDM's scalar-fallback runs */
 } dmqr_stats;
 void dmqr_stats_enable(int32_t on);
 void dmqr_stats_get(dmqr_stats* out, int32_t reset);

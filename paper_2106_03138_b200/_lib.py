@@ -16,6 +16,8 @@ EXPORTS = (
     "dmqr_workspace_bytes",
     "dmqr_qrdm_f64",
     "dmqr_qrdm_stream_f64",
+    "dmqr_qrp_f64",
+    "dmqr_qrp_stream_f64",
     "dmqr_qrdm_batched_f64",
     "dmqr_batched_workspace_bytes",
     "dmqr_form_q_f64",
@@ -81,6 +83,7 @@ class Stats(C.Structure):
         ("ms_panel", C.c_double),
         ("ms_trailing", C.c_double),
         ("ms_norms", C.c_double),
+        ("ms_pivot", C.c_double),
     ]
 
 
@@ -109,6 +112,10 @@ def load() -> C.CDLL:
     lib.dmqr_qrdm_stream_f64.argtypes = [P, I64, I64, I64, C.POINTER(Params), P, P, P, I64, P, I64, P, P, SZ,
                                          C.POINTER(Info), P, I64, VP]
     lib.dmqr_qrdm_stream_f64.restype = C.c_int
+    lib.dmqr_qrp_f64.argtypes = lib.dmqr_qrdm_f64.argtypes
+    lib.dmqr_qrp_f64.restype = C.c_int
+    lib.dmqr_qrp_stream_f64.argtypes = lib.dmqr_qrdm_stream_f64.argtypes
+    lib.dmqr_qrp_stream_f64.restype = C.c_int
     lib.dmqr_qrdm_batched_f64.argtypes = [P, I64, I64, I64, I64, I64, C.POINTER(Params), P, P, P, I64, P, I64,
                                           P, I32, P, SZ, VP]
     lib.dmqr_qrdm_batched_f64.restype = C.c_int

@@ -56,6 +56,8 @@ struct Ctl {
   int32_t q1_fail, q1_kk;
   int32_t pend_done;  // k_guard finished the whole update of this step (nothing pending)
   int32_t pad3;
+  // blocked scalar pivoting (k_qp3): columns factored by the last launch and why it ended
+  int32_t qp_cols, qp_exit;
   // inter-CTA counters (reset by their users)
   uint32_t gram_count;
   uint32_t bar_count;
@@ -106,8 +108,10 @@ __device__ __forceinline__ long long gtimer() {
 
 // per-step record the host polls (pinned, mapped host memory): written by
 // k_step_end with a release of seq = host enqueue index + 1
+// flags: 1 done, 2 la_bad (look-ahead meets many guards: go serial), 4 the
+// step was a scalar-fallback step / the blocked scalar-pivot engine continues
 struct __align__(16) HostRec {
-  int32_t n_s, done, la_bad, seq;
+  int32_t n_s, flags, step_idx, seq;
 };
 
 // debug timeline (DMQR_TIMELINE): per step and kernel, the first CTA's start

@@ -30,6 +30,7 @@
 #include "panel_cq.cuh"
 #include "select.cuh"
 #include "trailing.cuh"
+#include "qp3.cuh"
 
 using namespace dmqr;
 
@@ -40,7 +41,8 @@ constexpr int NSPLIT_MAX = 16;
 constexpr int PANEL_PMAX = 160;
 
 struct Layout {
-  size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, trace, pdbg, tcount, upd, lacount, q1g, glist, total;
+  size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, trace, pdbg, tcount, upd, lacount, q1g, glist;
+  size_t qvb, qwb, qpart, qgpart, qcnt, total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -73,7 +75,13 @@ Layout layout(int64_t m, int64_t n) {
   L.upd = take(std::max<int64_t>(n, 1));                      // look-ahead column flags
   L.lacount = take(sizeof(unsigned) * 8);                     // look-ahead work / last-CTA counters
   L.q1g = take(sizeof(double) * DMQR_KP * q1_ld(m));  // published Q1 (k_spare)
-  L.glist = take(sizeof(int32_t) * std::max<int64_t>(n, 1));  // look-ahead guard columns
+  L.glist = take(sizeof(int32_t) * std::max<int64_t>(n, 1));  // look-ahead / k_qp3 guard columns
+  // blocked scalar pivoting (k_qp3; its F = Zp, its Wt = Z: both are free between steps)
+  L.qvb = take(sizeof(double) * std::max<int64_t>(m, 1));
+  L.qwb = take(sizeof(double) * std::max<int64_t>(n, 1));
+  L.qpart = take(sizeof(double) * QP_GMAXCTA * QP_PLD);
+  L.qgpart = take(sizeof(double) * QP_GMAXCTA * QP_GMAX * 2);
+  L.qcnt = take(sizeof(unsigned) * 4);
   L.total = off;
   return L;
 }
@@ -112,6 +120,7 @@ cudaError_t& last_cuda_error() {
 
 bool attrs_done = false;
 bool cluster16 = false;
+int qp_grid = 1;  // k_qp3 cooperative grid (all CTAs co-resident)
 
 std::mutex g_attr_mu;
 
@@ -128,6 +137,12 @@ int set_attrs(const DevInfo& d) {
   CK(cudaFuncSetAttribute(k_guard, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GU_SMEM));
   CK(cudaFuncSetAttribute(k_ygemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YG_SMEM));
   CK(cudaFuncSetAttribute(k_trail_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TP_SMEM));
+  CK(cudaFuncSetAttribute(k_qp3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QP_SMEM));
+  {
+    int nb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_qp3, QP_T, QP_SMEM));
+    qp_grid = std::max(1, std::min(nb * d.sms, QP_GMAXCTA));
+  }
   CK(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)std::min<size_t>(d.smem_optin - 4096, 220 * 1024)));
   CK(cudaFuncSetAttribute(k_panel_rr<ClusterRed>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RR_CL_SMEM));
@@ -171,7 +186,7 @@ std::atomic<long long> g_launches{0};
 std::atomic<long long> g_calls{0};
 std::atomic<int> g_prof{0};
 struct ProfAcc {
-  double ms[4] = {0, 0, 0, 0};  // select+gram+swap, panel, trailing update, downdate+log
+  double ms[5] = {0, 0, 0, 0, 0};  // select+gram+swap, panel, trailing update, downdate+log, scalar pivoting
   long long steps = 0;
 };
 ProfAcc g_acc;  // guarded by the caller (bench) using one thread
@@ -239,10 +254,14 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
                               workspace, ws_bytes, info, nullptr, 0, stream);
 }
 
-int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* p, double* coeffs,
-                         int64_t* perm, int64_t* swaps, int64_t swap_cap, dmqr_step* steps, int64_t step_cap,
-                         double* norm_trace, void* workspace, size_t ws_bytes, dmqr_info* info,
-                         double* host_packed, int64_t host_ld, void* stream) {
+}  // extern "C"
+
+namespace {
+// The engine behind dmqr_qrdm*_f64 (qrp = 0) and dmqr_qrp*_f64 (qrp = 1).
+int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* p, double* coeffs, int64_t* perm,
+               int64_t* swaps, int64_t swap_cap, dmqr_step* steps, int64_t step_cap, double* norm_trace,
+               void* workspace, size_t ws_bytes, dmqr_info* info, double* host_packed, int64_t host_ld, void* stream,
+               int qrp) {
   if (host_packed && host_ld < m) return DMQR_EINVAL;
   int rc = validate(m, n, lda, p);
   if (rc) return rc;
@@ -269,6 +288,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
   unsigned* tcount = (unsigned*)(ws + L.tcount);
   uint8_t* upd = (uint8_t*)(ws + L.upd);
   double* q1g = (double*)(ws + L.q1g);
+  unsigned* qcnt = (unsigned*)(ws + L.qcnt);
   int32_t* glist = (int32_t*)(ws + L.glist);
   unsigned* lacount = (unsigned*)(ws + L.lacount);
   StepRec* srec = (StepRec*)steps;
@@ -278,8 +298,8 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
   // candidates get it first (in k_gram).
   // (small problems -- e.g. the 256^2 batch of cfg3 -- are launch-bound: serial form)
   // (tall inputs -- m > 4n, like cfg4 -- hit norm guards too often: serial)
-  const bool la_all = !p->trace_norms && getenv("DMQR_NO_LOOKAHEAD") == nullptr && m * n >= (int64_t)1 << 20 &&
-                      m <= 4 * n;
+  const bool la_all = !qrp && !p->trace_norms && getenv("DMQR_NO_LOOKAHEAD") == nullptr &&
+                      m * n >= (int64_t)1 << 20 && m <= 4 * n;
 
 
   const int64_t kmax = std::min(m, n);
@@ -329,6 +349,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
     for (auto& r : ev)
       for (auto& e : r) CK(cudaEventCreate(&e));
   int slot = 0;
+  bool qp_slot[2] = {false, false};  // the in-flight record of this slot came from a k_qp3 block
 #define PROF(i) \
   if (prof) CK(cudaEventRecord(ev[slot][i], st))
   int steps_done = 0;
@@ -580,7 +601,8 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
     return 0;
   };
   int64_t known_ns = 0;  // n_s after the last step whose head was read
-  int known = 0, enq = 0;
+  int known = 0, enq = 0, known_steps = 0;
+  bool qp_mode = qrp != 0;
   bool finished = (kmax == 0);
   auto consume = [&]() -> int {
     const int sl = known & 1;
@@ -600,20 +622,79 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
     std::atomic_thread_fence(std::memory_order_acquire);
     if (prof) {
       CK(cudaEventSynchronize(ev[sl][4]));
-      for (int q = 0; q < 4; ++q) {
+      if (qp_slot[sl]) {
         float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, ev[sl][q], ev[sl][q + 1]));
-        g_acc.ms[q] += ms;
+        CK(cudaEventElapsedTime(&ms, ev[sl][0], ev[sl][4]));
+        g_acc.ms[4] += ms;
+      } else {
+        for (int q = 0; q < 4; ++q) {
+          float ms = 0.f;
+          CK(cudaEventElapsedTime(&ms, ev[sl][q], ev[sl][q + 1]));
+          g_acc.ms[q] += ms;
+        }
       }
       g_acc.steps += 1;
     }
     known_ns = r->n_s;
+    known_steps = r->step_idx;
     ++known;
-    if (r->done) finished = true;
-    if (r->la_bad) want_serial = true;
+    if (r->flags & 1) finished = true;
+    if (r->flags & 2) want_serial = true;
+    // a scalar-fallback step hands the run to the blocked scalar-pivot engine;
+    // its blocks keep it until a fallback run ends on the floor test
+    qp_mode = qrp || (r->flags & 4) != 0;
     return stream_cols(known_ns, nullptr);  // columns left of n_s are final (and written)
   };
+  // one block of the blocked scalar-pivot engine (no step in flight)
+  auto run_qp_block = [&]() -> int {
+    if (la_on && !la_off) {  // flush the look-ahead's pending update; serial from here on
+      const int64_t ldz0 = ldz_for(n);
+      k_trail_b<true><<<dim3((unsigned)ceil_div(m - prev_ns_lo + 1, TB_ROWS),
+                             (unsigned)std::max<int64_t>(1, ceil_div(n - prev_ns_lo, TB_COLS))),
+                        TB_T, TB_SMEM, st>>>(ctl, A, Z, ldz_for(n), upd, lacount + 1);
+      (void)ldz0;
+      NOTE_LAUNCH();
+      k_set_la<<<1, 32, 0, st>>>(ctl, 0);
+      NOTE_LAUNCH();
+      la_off = true;
+    }
+    slot = enq & 1;
+    qp_slot[slot] = true;
+    PROF(0);
+    int lim = p->trace_norms ? 1 : QP_NB;
+    if (p->max_steps > 0) lim = std::min<int>(lim, std::max(0, p->max_steps - known_steps));
+    CK(cudaMemsetAsync(qcnt, 0, sizeof(unsigned) * 4, st));
+    Qp3Args qa{ctl, A, u, uref, perm, swaps, coeffs, srec, Zp, Z, ldz_for(n), (double*)(ws + L.qvb),
+               (double*)(ws + L.qwb), (double*)(ws + L.qpart), (double*)(ws + L.qgpart), glist, qcnt, qrp, lim};
+    void* qargs[] = {&qa};
+    CK(cudaLaunchCooperativeKernel((const void*)k_qp3, dim3(qp_grid), dim3(QP_T), qargs, QP_SMEM, st));
+    NOTE_LAUNCH();
+    if (p->trace_norms) {
+      const int64_t blocks = std::min<int64_t>(ceil_div(std::max<int64_t>(n, 1) * 32, 256), (int64_t)d.sms * 16);
+      k_qp3_trace<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, tbits);
+      NOTE_LAUNCH();
+    }
+    k_qp3_post<<<1, 32, 0, st>>>(ctl, p->trace_norms ? norm_trace : nullptr, tbits, hrec, enq);
+    NOTE_LAUNCH();
+    PROF(4);
+    CK(cudaGetLastError());
+    ++enq;
+    ++steps_done;
+    return consume();
+  };
   while (!finished) {
+    if (qp_mode) {
+      while (known < enq && !finished) {  // drain the steps in flight
+        int rc = consume();
+        if (rc) return rc;
+      }
+      if (finished) break;
+      if (!qp_mode) continue;
+      if (p->max_steps > 0 && known_steps >= p->max_steps) break;
+      int rc = run_qp_block();
+      if (rc) return rc;
+      continue;
+    }
     if (enq - known >= 2) {
       int rc = consume();
       if (rc) return rc;
@@ -628,6 +709,7 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
       break;
     }
     slot = enq & 1;
+    qp_slot[slot] = false;
     int rc = enqueue_step(ns_lo, enq);
     if (rc) return rc;
     prev_ns_lo = ns_lo;
@@ -678,6 +760,32 @@ int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmq
     info->stopped_early = 0;
   }
   return hc.status;
+}
+}  // namespace
+
+extern "C" {
+
+int dmqr_qrdm_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* p, double* coeffs,
+                         int64_t* perm, int64_t* swaps, int64_t swap_cap, dmqr_step* steps, int64_t step_cap,
+                         double* norm_trace, void* workspace, size_t ws_bytes, dmqr_info* info,
+                         double* host_packed, int64_t host_ld, void* stream) {
+  return run_engine(A, m, n, lda, p, coeffs, perm, swaps, swap_cap, steps, step_cap, norm_trace, workspace, ws_bytes,
+                    info, host_packed, host_ld, stream, 0);
+}
+
+int dmqr_qrp_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* p, double* coeffs,
+                        int64_t* perm, int64_t* swaps, int64_t swap_cap, dmqr_step* steps, int64_t step_cap,
+                        double* norm_trace, void* workspace, size_t ws_bytes, dmqr_info* info, double* host_packed,
+                        int64_t host_ld, void* stream) {
+  return run_engine(A, m, n, lda, p, coeffs, perm, swaps, swap_cap, steps, step_cap, norm_trace, workspace, ws_bytes,
+                    info, host_packed, host_ld, stream, 1);
+}
+
+int dmqr_qrp_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* p, double* coeffs, int64_t* perm,
+                 int64_t* swaps, int64_t swap_cap, dmqr_step* steps, int64_t step_cap, double* norm_trace,
+                 void* workspace, size_t ws_bytes, dmqr_info* info, void* stream) {
+  return dmqr_qrp_stream_f64(A, m, n, lda, p, coeffs, perm, swaps, swap_cap, steps, step_cap, norm_trace, workspace,
+                             ws_bytes, info, nullptr, 0, stream);
 }
 
 size_t dmqr_batched_workspace_bytes(int64_t m, int64_t n, const dmqr_params* params, int32_t nlanes) {
@@ -783,6 +891,7 @@ void dmqr_stats_get(dmqr_stats* out, int32_t reset) {
     out->ms_panel = g_acc.ms[1];
     out->ms_trailing = g_acc.ms[2];
     out->ms_norms = g_acc.ms[3];
+    out->ms_pivot = g_acc.ms[4];
   }
   if (reset) {
     g_launches.store(0);

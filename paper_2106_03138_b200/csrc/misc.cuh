@@ -134,7 +134,10 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
   __threadfence();
   __syncwarp();
   if (threadIdx.x == 0 && hrec) {
-    const int4 rec = make_int4(c->n_s, c->done, c->la_bad, enq + 1);
+    // (a fallback step hands the run to the blocked scalar-pivot engine, k_qp3;
+    // not with the per-step norm trace)
+    const int fb = (!S.done && S.kind == 1 && !S.trace_norms) ? 4 : 0;
+    const int4 rec = make_int4(c->n_s, (c->done ? 1 : 0) | (c->la_bad ? 2 : 0) | fb, c->step_idx, enq + 1);
     asm volatile("st.volatile.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(hrec + (enq & 1)), "r"(rec.x), "r"(rec.y),
                  "r"(rec.z), "r"(rec.w)
                  : "memory");

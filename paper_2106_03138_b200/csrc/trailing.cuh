@@ -408,8 +408,8 @@ __device__ __forceinline__ void trail_b_tile(double* __restrict__ A, const doubl
     for (int nt = 0; nt < 4; ++nt) {
       const int64_t cc = col0 + wn * 32 + nt * 8 + 2 * (lane & 3);
       double* p = Cp + r + cc * lda;
-      if (cc < ncols && !(LA && upd[c0 + cc])) p[0] = acc[mt][nt][0];
-      if (cc + 1 < ncols && !(LA && upd[c0 + cc + 1])) p[lda] = acc[mt][nt][1];
+      if (cc < ncols && !(LA && upd && upd[c0 + cc])) p[0] = acc[mt][nt][0];
+      if (cc + 1 < ncols && !(LA && upd && upd[c0 + cc + 1])) p[lda] = acc[mt][nt][1];
     }
   }
 }

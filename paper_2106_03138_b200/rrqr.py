@@ -5,6 +5,7 @@ Same call and result surface as the reference ``dmqr.rrqr`` (rrqr.py:39-53,
 
     qrdm (A, params=DMParams(), stop=StopCriterion(), trace_norms=False) -> RRQRResult
     qrdm2(A, params=DMParams(), stop=StopCriterion(), trace_norms=False) -> RRQRResult
+    qrp  (A, stop=StopCriterion(), trace_norms=False) -> RRQRResult   (rrqr.py:238-291)
 
 The factorization itself runs in ``libdmqr_b200.so`` (hand-written sm_100a
 CUDA, called through the C-ABI in include/dmqr_b200.h).  PyTorch only carries
@@ -33,7 +34,7 @@ K_DM_MAX = 64
 
 __all__ = [
     "EPS", "DMParams", "StopRule", "StopCriterion", "StepRecord", "WorkCounters", "Permutation",
-    "RRQRResult", "qrdm", "qrdm2", "reconstruct", "factorize",
+    "RRQRResult", "qrdm", "qrdm2", "qrp", "reconstruct", "factorize",
 ]
 
 
@@ -175,8 +176,8 @@ class LazyCounters:
     """WorkCounters replayed from the step log on first access (the replay is a
     Python loop over every accepted column; most callers never read it)."""
 
-    def __init__(self, m: int, n: int, steps: list):
-        self._args = (m, n, steps)
+    def __init__(self, m: int, n: int, steps: list, qrp: bool = False):
+        self._args = (m, n, steps, qrp)
         self._wc = None
 
     def _get(self) -> WorkCounters:
@@ -196,11 +197,12 @@ class LazyCounters:
         return repr(self._get())
 
 
-def replay_counters(m: int, n: int, steps: list) -> WorkCounters:
+def replay_counters(m: int, n: int, steps: list, qrp: bool = False) -> WorkCounters:
+    """qrp: every step is one _scalar_step + downdate (rrqr.py:230-235, 275)."""
     wc = WorkCounters(total_flops=2.0 * m * n)
     for st in steps:
         s = st.n_s
-        if st.fell_back_to_scalar:
+        if st.fell_back_to_scalar or qrp:
             if s + 1 < n:
                 f = 4.0 * (m - s) * (n - s - 1)
                 wc.rank1_flops += f
@@ -293,6 +295,7 @@ class DeviceFactor:
     info: _lib.Info
     workspace: object = None
     host_packed: object = None  # pinned (n, m) host copy streamed by the engine, if requested
+    algo: str = "qrdm"          # "qrp": greedy column pivoting (counters replay differs)
 
     def debug_ctl(self) -> dict:
         """Decision state of the last step (debug aid)."""
@@ -314,7 +317,7 @@ class DeviceFactor:
 
 def factorize(A, params: DMParams = DMParams(), stop: StopCriterion = StopCriterion(),
               break_check: bool = True, trace_norms: bool = False, stream=None, work=None,
-              max_steps: int = 0, host_packed=None) -> DeviceFactor:
+              max_steps: int = 0, host_packed=None, algo: str = "qrdm") -> DeviceFactor:
     """Run one factorization on the device; returns device buffers.
 
     ``work`` may be a (buf, m, n, lda) tuple from ``to_work`` whose buffer is
@@ -346,12 +349,13 @@ def factorize(A, params: DMParams = DMParams(), stop: StopCriterion = StopCriter
     # host_packed: pinned (n, m) host tensor; the engine streams the finished
     # columns of the packed factor into it while it runs
     hp = host_packed.data_ptr() if host_packed is not None else None
-    rc = lib.dmqr_qrdm_stream_f64(buf.data_ptr(), m, n, lda, C.byref(p), coeffs.data_ptr(), perm.data_ptr(),
+    entry = lib.dmqr_qrp_stream_f64 if algo == "qrp" else lib.dmqr_qrdm_stream_f64
+    rc = entry(buf.data_ptr(), m, n, lda, C.byref(p), coeffs.data_ptr(), perm.data_ptr(),
                                   swaps.data_ptr(), swap_cap, steps.data_ptr(), step_cap,
                                   ntrace.data_ptr() if ntrace is not None else None, ws.data_ptr(), wsb,
                                   C.byref(info), hp, m, sh)
     _check(rc)
-    return DeviceFactor(buf, m, n, lda, coeffs[:kmax], perm[:n], swaps, steps, ntrace, info, ws, host_packed)
+    return DeviceFactor(buf, m, n, lda, coeffs[:kmax], perm[:n], swaps, steps, ntrace, info, ws, host_packed, algo)
 
 
 def _steps_from_raw(raw: np.ndarray, count: int) -> list:
@@ -398,17 +402,18 @@ def to_result(f: DeviceFactor, device: bool = False) -> RRQRResult:
         packed, coeffs = np.zeros((f.m, f.n), order="F"), np.zeros(0)
     return RRQRResult(packed=packed, coeffs=coeffs, perm=perm, rank=int(info.rank), step_log=steps,
                       n_factored=int(info.n_factored), stopped_early=bool(info.stopped_early),
-                      counters=LazyCounters(f.m, f.n, steps), norm_trace=trace)
+                      counters=LazyCounters(f.m, f.n, steps, f.algo == "qrp"),
+                      norm_trace=trace)
 
 
-def _run(A, params, stop, break_check, trace_norms, device) -> RRQRResult:
+def _run(A, params, stop, break_check, trace_norms, device, algo="qrdm") -> RRQRResult:
     torch = _torch()
     work = to_work(A)
     hp = None
     if not device and work[1] and work[2]:
         hp = torch.empty((work[2], work[1]), dtype=torch.float64, pin_memory=True)
     return to_result(factorize(None, params, stop, break_check=break_check, trace_norms=trace_norms, work=work,
-                               host_packed=hp), device)
+                               host_packed=hp, algo=algo), device)
 
 
 def qrdm(A, params: DMParams = DMParams(), stop: StopCriterion = StopCriterion(),
@@ -421,6 +426,18 @@ def qrdm2(A, params: DMParams = DMParams(), stop: StopCriterion = StopCriterion(
           trace_norms: bool = False, device: bool = False) -> RRQRResult:
     """``qrdm`` plus the within-block break check (rrqr.py:443-456), on the B200."""
     return _run(A, params, stop, True, trace_norms, device)
+
+
+def qrp(A, stop: StopCriterion = StopCriterion(), trace_norms: bool = False,
+        device: bool = False) -> RRQRResult:
+    """QR with greedy column pivoting (rrqr.py:238-291), on the B200.
+
+    The pivot at step s is the trailing column of maximum partial norm (ties
+    to the smallest index); with an active stop rule the factorization halts
+    once the trailing block is negligible and rank = steps done, with
+    StopRule.NONE it runs to completion and counts |r_ii| > eps n max|a_j|.
+    Runs on the blocked scalar-pivot engine (delayed block updates)."""
+    return _run(A, DMParams(), stop, False, trace_norms, device, algo="qrp")
 
 
 def form_q(packed, coeffs, n_factored: int, qcols: int | None = None):

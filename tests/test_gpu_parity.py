@@ -15,10 +15,12 @@ GOLDEN = [c for c in G.case_names() if not c.startswith(("cfg2s", "cfg4s"))]
 
 
 def _gpu(name_or_A, algo="qrdm2", **kw):
-    from paper_2106_03138_b200 import DMParams, StopCriterion, StopRule, qrdm, qrdm2
+    from paper_2106_03138_b200 import DMParams, StopCriterion, StopRule, qrdm, qrdm2, qrp
 
-    params = DMParams(**{k: kw[k] for k in ("tau", "delta", "k_dm", "use_delta_max") if k in kw})
     stop = StopCriterion(StopRule(kw.get("stop_rule", "n")))
+    if algo == "qrp":
+        return qrp(name_or_A, stop=stop, trace_norms=kw.get("trace_norms", False))
+    params = DMParams(**{k: kw[k] for k in ("tau", "delta", "k_dm", "use_delta_max") if k in kw})
     fn = qrdm2 if algo == "qrdm2" else qrdm
     return fn(name_or_A, params=params, stop=stop, trace_norms=kw.get("trace_norms", False))
 
@@ -65,9 +67,11 @@ def test_golden_case(name):
     A = G.case_input(name)
     kw = G.oracle_kwargs(name)
     res = _gpu(A, meta["algo"], **kw)
-    fn = O.qrdm2 if meta["algo"] == "qrdm2" else O.qrdm
     with threadpool_limits(1):
-        ref = fn(A, margins=True, **kw)
+        if meta["algo"] == "qrp":
+            ref = O.qrp(A, margins=True, stop_rule=kw["stop_rule"])
+        else:
+            ref = (O.qrdm2 if meta["algo"] == "qrdm2" else O.qrdm)(A, margins=True, **kw)
     # the oracle itself is pinned to the golden vectors (test_oracle_golden.py)
     assert np.array_equal(ref.forward, G.case_field(name, "forward"))
     _compare(A, res, ref, name)
@@ -91,6 +95,65 @@ def test_random_vs_oracle(seed):
     with threadpool_limits(1):
         ref = (O.qrdm2 if algo == "qrdm2" else O.qrdm)(A, margins=True)
     _compare(A, res, ref, f"random{seed}")
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_qrp_random_vs_oracle(seed):
+    """qrp on the blocked scalar-pivot engine: shapes across block boundaries
+    (64 columns per block), tall / wide / rank-deficient / graded inputs."""
+    rng = np.random.default_rng(2380 + seed)
+    m = int(rng.integers(30, 700))
+    n = int(rng.integers(30, 700))
+    kind = seed % 4
+    if kind == 0:
+        A = rng.standard_normal((m, n))
+    elif kind == 1:
+        r = int(rng.integers(1, min(m, n)))
+        A = rng.standard_normal((m, r)) @ rng.standard_normal((r, n))
+    elif kind == 2:
+        A = rng.standard_normal((m, n)) * np.logspace(0, -12, n)[rng.permutation(n)]
+    else:
+        A = rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-6, 0, n)
+    stop_rule = ("n", "none", "sqrt-n", "n")[seed % 4]
+    res = _gpu(A, "qrp", stop_rule=stop_rule)
+    with threadpool_limits(1):
+        ref = O.qrp(A, margins=True, stop_rule=stop_rule)
+    _compare(A, res, ref, f"qrp-random{seed}")
+
+
+def test_qrp_guard_overflow_block_end():
+    """Many near-parallel columns: the first reflector sends most norms under the
+    guard at once (> 64 guards), so the block ends and they are recomputed from
+    the updated matrix (rrqr.py:178-184 semantics)."""
+    rng = np.random.default_rng(77)
+    x = rng.standard_normal(300)
+    A = np.outer(x, 1.0 + 0.1 * rng.standard_normal(200)) + 1e-7 * rng.standard_normal((300, 200))
+    for algo in ("qrp", "qrdm2"):
+        res = _gpu(A, algo, stop_rule="none")
+        with threadpool_limits(1):
+            ref = (O.qrp(A, margins=True, stop_rule="none") if algo == "qrp"
+                   else O.qrdm2(A, margins=True, stop_rule="none"))
+        _compare(A, res, ref, f"guard-overflow-{algo}")
+
+
+def test_qrp_midsize_blocks():
+    """1200 x 900: 15 blocks of the delayed-update engine against the oracle."""
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((1200, 900)) * np.logspace(0, -9, 900)
+    res = _gpu(A, "qrp")
+    with threadpool_limits(1):
+        ref = O.qrp(A, margins=True)
+    _compare(A, res, ref, "qrp-midsize")
+
+
+def test_qrp_trace_norms():
+    rng = np.random.default_rng(40)
+    A = rng.standard_normal((120, 90))
+    res = _gpu(A, "qrp", stop_rule="none", trace_norms=True)
+    with threadpool_limits(1):
+        ref = O.qrp(A, stop_rule="none", trace_norms=True)
+    assert len(res.norm_trace) == len(ref.norm_trace)
+    assert max(res.norm_trace) <= 1e-10
 
 
 def test_trace_norms_within_1e10():
