@@ -80,7 +80,7 @@ Layout layout(int64_t m, int64_t n) {
   L.qvb = take(sizeof(double) * std::max<int64_t>(m, 1));
   L.qwb = take(sizeof(double) * std::max<int64_t>(n, 1));
   L.qpart = take(sizeof(double) * QP_GMAXCTA * QP_PLD);
-  L.qgpart = take(sizeof(double) * QP_GMAXCTA * QP_GMAX * 2);
+  L.qgpart = take(sizeof(double) * (QP_GMAXCTA * QP_GMAX * 2 + QP_GMAX));  // + the fresh guard norms
   L.qcnt = take(sizeof(unsigned) * 4);
   L.total = off;
   return L;
@@ -646,6 +646,8 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     return stream_cols(known_ns, nullptr);  // columns left of n_s are final (and written)
   };
   // one block of the blocked scalar-pivot engine (no step in flight)
+  const int qp_clk = getenv("DMQR_QP_CLOCKS") ? atoi(getenv("DMQR_QP_CLOCKS")) : -1;
+  int qp_blocks = 0;
   auto run_qp_block = [&]() -> int {
     if (la_on && !la_off) {  // flush the look-ahead's pending update; serial from here on
       const int64_t ldz0 = ldz_for(n);
@@ -664,8 +666,13 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     int lim = p->trace_norms ? 1 : QP_NB;
     if (p->max_steps > 0) lim = std::min<int>(lim, std::max(0, p->max_steps - known_steps));
     CK(cudaMemsetAsync(qcnt, 0, sizeof(unsigned) * 4, st));
+    double* qg = (double*)(ws + L.qgpart);
+    // debug: phase clocks of CTA 0 for the k-th block (DMQR_QP_CLOCKS=k; tools/qp_clocks.py)
+    long long* qdbg = (qp_clk >= 0 && qp_blocks == qp_clk) ? pdbg : nullptr;
+    ++qp_blocks;
     Qp3Args qa{ctl, A, u, uref, perm, swaps, coeffs, srec, Zp, Z, ldz_for(n), (double*)(ws + L.qvb),
-               (double*)(ws + L.qwb), (double*)(ws + L.qpart), (double*)(ws + L.qgpart), glist, qcnt, qrp, lim};
+               (double*)(ws + L.qwb), (double*)(ws + L.qpart), qg, glist, qg + QP_GMAXCTA * QP_GMAX * 2, qcnt,
+               qdbg, qrp, lim};
     void* qargs[] = {&qa};
     CK(cudaLaunchCooperativeKernel((const void*)k_qp3, dim3(qp_grid), dim3(QP_T), qargs, QP_SMEM, st));
     NOTE_LAUNCH();

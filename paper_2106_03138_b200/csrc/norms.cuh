@@ -15,27 +15,50 @@ namespace dmqr {
 // magnitude keeps squares normal, else a second max-scaled pass (the
 // reference's scaling, matrix.py:73-77).
 __device__ __forceinline__ double warp_col_norm(const double* __restrict__ x, int64_t len, int lane) {
-  double s0 = 0.0, s1 = 0.0, a0 = 0.0, a1 = 0.0;
-  int64_t i = lane;
-  for (; i + 32 < len; i += 64) {
-    double p = __ldg(x + i), q = __ldg(x + i + 32);
-    s0 = fma(p, p, s0);
-    s1 = fma(q, q, s1);
-    a0 = fmax(a0, fabs(p));
-    a1 = fmax(a1, fabs(q));
+  // 16-byte loads from the first 16-byte aligned element, 8 pairs per lane in
+  // flight (a 16384-row column is 16 round trips, not 256)
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, a0 = 0.0, a1 = 0.0;
+  const int64_t h = (len > 0 && (reinterpret_cast<uintptr_t>(x) & 15)) ? 1 : 0;
+  if (h && lane == 0) {
+    const double p = __ldg(x);
+    s0 = p * p;
+    a0 = fabs(p);
   }
-  if (i < len) {
-    double p = __ldg(x + i);
-    s0 = fma(p, p, s0);
-    a0 = fmax(a0, fabs(p));
+  const double* y = x + h;
+  const int64_t len2 = len - h;
+  int64_t i = 2 * lane;
+  for (; i + 7 * 64 + 1 < len2; i += 8 * 64) {
+    double2 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const double2*>(y + i + 64 * k));
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+      s0 = fma(v[k].x, v[k].x, s0);
+      s1 = fma(v[k].y, v[k].y, s1);
+      s2 = fma(v[k + 1].x, v[k + 1].x, s2);
+      s3 = fma(v[k + 1].y, v[k + 1].y, s3);
+      a0 = fmax(a0, fmax(fabs(v[k].x), fabs(v[k].y)));
+      a1 = fmax(a1, fmax(fabs(v[k + 1].x), fabs(v[k + 1].y)));
+    }
   }
-  double s = warp_sum(s0 + s1);
+  for (; i + 1 < len2; i += 64) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(y + i));
+    s0 = fma(v.x, v.x, s0);
+    s1 = fma(v.y, v.y, s1);
+    a0 = fmax(a0, fmax(fabs(v.x), fabs(v.y)));
+  }
+  if (i < len2) {
+    const double p = __ldg(y + i);
+    s2 = fma(p, p, s2);
+    a1 = fmax(a1, fabs(p));
+  }
+  double s = warp_sum((s0 + s1) + (s2 + s3));
   double amax = warp_max(fmax(a0, a1));
   if (norm_range_ok(amax)) return sqrt(s);
   double t = 0.0;
   for (int64_t k = lane; k < len; k += 32) {
-    double y = __ldg(x + k) / amax;
-    t = fma(y, y, t);
+    double z = __ldg(x + k) / amax;
+    t = fma(z, z, t);
   }
   t = warp_sum(t);
   return amax * sqrt(t);

@@ -50,6 +50,8 @@ constexpr int QP_PLD = 8;     // per-CTA partial record (doubles)
 constexpr int QP_GMAXCTA = 320;  // grid cap (2 CTAs x 148 SMs fits)
 constexpr int QP_SUB = 64;       // guard phase: rows per staged sub-chunk
 constexpr size_t QP_SMEM = TB_SMEM;  // the block update's tile staging is the largest user
+constexpr int QP_XCH = 13312;        // rows of x staged per chunk in alpha (104 KB)
+static_assert(sizeof(double) * QP_XCH <= QP_SMEM, "x staging");
 static_assert(sizeof(double) * (QP_SUB * (QP_NB + 1) + QP_GMAX * (QP_NB + 1)) <= QP_SMEM, "guard staging");
 
 struct Qp3Args {
@@ -69,7 +71,9 @@ struct Qp3Args {
   double* part;     // [G][QP_PLD]
   double* gpart;    // [G][QP_GMAX][2]
   int32_t* glist;   // guard columns of the current column step (capacity n)
-  unsigned* cnt;    // [0] barrier, [1] guard count, [2] guard-phase arrivals; zeroed before launch
+  double* gfresh;   // [QP_GMAX] fresh norms of the in-place guard columns
+  unsigned* cnt;    // [0] barrier, [1] guard count, [2] guard-phase arrivals, [3] guard-done column; zeroed before launch
+  long long* dbg;   // optional phase clocks of CTA 0 (globaltimer ns): [t * 8 + phase], block end at [512..]
   int qrp;          // 1: greedy pivoting (qrp): no floor test; 0: QRDM scalar-fallback run
   int col_limit;    // columns this launch may factor (<= QP_NB)
 };
@@ -101,6 +105,8 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
   __shared__ int s_redi[QP_W];
   __shared__ double s_b[4];
   __shared__ int s_bi[2];
+#define QCLK(k) \
+  if (a.dbg && b == 0 && tid == 0 && t < 64) a.dbg[t * 8 + (k)] = gtimer()
   uint32_t bar_k = 0;
   auto gsync = [&]() {
     ++bar_k;
@@ -140,18 +146,33 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
   for (;;) {
     const int64_t s = s0 + t;
     // ================= gamma =================
-    if (wid == 0) {
+    QCLK(0);
+    if (g_prev > 0 && g_prev <= QP_GMAX) {  // the guard phase's last CTA has published the fresh norms
+      if (tid == 0) {
+        unsigned v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(a.cnt + 3) : "memory");
+        } while (v < (unsigned)t);
+      }
+      __syncthreads();
+    }
+    QCLK(1);
+    {  // argmax of the partials and the guard columns: every thread loads <= 2 partials (one L2 round trip)
       double bv = -1.0;
       int bi = 0x7fffffff;
-      for (int q = lane; q < G; q += 32) am_merge(bv, bi, __ldcg(a.part + q * QP_PLD), (int)__ldcg(a.part + q * QP_PLD + 1));
-      if (g_prev <= QP_GMAX)
-        for (int q = lane; q < g_prev; q += 32) {
-          const int col = __ldcg(a.glist + q);
-          am_merge(bv, bi, __ldcg(a.u + col), col);
-        }
+      if (tid < G) am_merge(bv, bi, __ldcg(a.part + tid * QP_PLD), (int)__ldcg(a.part + tid * QP_PLD + 1));
+      if (tid + QP_T < G)
+        am_merge(bv, bi, __ldcg(a.part + (tid + QP_T) * QP_PLD), (int)__ldcg(a.part + (tid + QP_T) * QP_PLD + 1));
+      if (tid < g_prev && g_prev <= QP_GMAX) am_merge(bv, bi, __ldcg(a.gfresh + tid), __ldcg(a.glist + tid));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) am_merge(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
       if (lane == 0) {
+        s_red[wid][0] = bv;
+        s_redi[wid] = bi;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < QP_W; ++w) am_merge(bv, bi, s_red[w][0], s_redi[w]);
         s_b[0] = bv;
         s_bi[0] = bi;
       }
@@ -184,9 +205,16 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
       }
       if (r >= s) {
         const double* yr = A + r + s0 * lda;
-        double acc = 0.0;
-        for (int q = 0; q < t; ++q) acc = fma(yr[q * lda], s_fp[q], acc);
-        x -= acc;
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+        int q = 0;
+        for (; q + 4 <= t; q += 4) {
+          c0 = fma(yr[q * lda], s_fp[q], c0);
+          c1 = fma(yr[(q + 1) * lda], s_fp[q + 1], c1);
+          c2 = fma(yr[(q + 2) * lda], s_fp[q + 2], c2);
+          c3 = fma(yr[(q + 3) * lda], s_fp[q + 3], c3);
+        }
+        for (; q < t; ++q) c0 = fma(yr[q * lda], s_fp[q], c0);
+        x -= (c0 + c1) + (c2 + c3);
         ss = fma(x, x, ss);
         am = fmax(am, fabs(x));
         if (r == s) x0 = x;
@@ -216,17 +244,34 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
     gsync();
 
     // ================= alpha =================
-    if (wid == 0) {
+    QCLK(2);
+    {
       double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-      for (int q = lane; q < G; q += 32) {
-        t0 += __ldcg(a.part + q * QP_PLD + 2);
-        t1 = fmax(t1, __ldcg(a.part + q * QP_PLD + 3));
-        t2 += __ldcg(a.part + q * QP_PLD + 4);
+      if (tid < G) {
+        t0 = __ldcg(a.part + tid * QP_PLD + 2);
+        t1 = __ldcg(a.part + tid * QP_PLD + 3);
+        t2 = __ldcg(a.part + tid * QP_PLD + 4);
+      }
+      if (tid + QP_T < G) {
+        t0 += __ldcg(a.part + (tid + QP_T) * QP_PLD + 2);
+        t1 = fmax(t1, __ldcg(a.part + (tid + QP_T) * QP_PLD + 3));
+        t2 += __ldcg(a.part + (tid + QP_T) * QP_PLD + 4);
       }
       t0 = warp_sum(t0);
       t1 = warp_max(t1);
       t2 = warp_sum(t2);
       if (lane == 0) {
+        s_red[wid][0] = t0;
+        s_red[wid][1] = t1;
+        s_red[wid][2] = t2;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < QP_W; ++w) {
+          t0 += s_red[w][0];
+          t1 = fmax(t1, s_red[w][1]);
+          t2 += s_red[w][2];
+        }
         s_b[0] = t0;
         s_b[1] = t1;
         s_b[2] = t2;
@@ -306,46 +351,68 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
     for (int64_t r = max(r_lo, s + 1) + tid; r < r_hi; r += QP_T) a.vb[r] = A[r + s * lda] / u0;
     // w_c = v^T A[s:, c] = A[s, c] + (x[s+1:] . A[s+1:, c]) / u0 for the trailing
     // columns and the block's own reflector columns (z)
+    // x is staged in shared memory by row chunks (every warp of the CTA streams
+    // its columns against it; L1 is mostly carved out for the tile staging)
     {
       const double* xcol = A + s * lda;
       const int64_t r1 = s + 1;
       const int64_t ra = (r1 + 1) & ~(int64_t)1;  // first even row >= s+1 (16-byte aligned pairs)
-      for (int64_t col = s0 + gw; col < n; col += NW) {
-        if (col == s) continue;
-        const double* ac = A + col * lda;
-        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-        if (lane == 0 && ra > r1 && r1 < m) d0 = xcol[r1] * ac[r1];
-        int64_t r = ra + 2 * lane;
-        for (; r + 3 * 64 + 1 < m; r += 4 * 64) {
-          const double2 a0 = ldcs2(ac + r), a1 = ldcs2(ac + r + 64), a2 = ldcs2(ac + r + 128),
-                        a3 = ldcs2(ac + r + 192);
-          const double2 x0v = *reinterpret_cast<const double2*>(xcol + r);
-          const double2 x1v = *reinterpret_cast<const double2*>(xcol + r + 64);
-          const double2 x2v = *reinterpret_cast<const double2*>(xcol + r + 128);
-          const double2 x3v = *reinterpret_cast<const double2*>(xcol + r + 192);
-          d0 = fma(x0v.x, a0.x, d0);
-          d1 = fma(x0v.y, a0.y, d1);
-          d2 = fma(x1v.x, a1.x, d2);
-          d3 = fma(x1v.y, a1.y, d3);
-          d0 = fma(x2v.x, a2.x, d0);
-          d1 = fma(x2v.y, a2.y, d1);
-          d2 = fma(x3v.x, a3.x, d2);
-          d3 = fma(x3v.y, a3.y, d3);
+      double* xs = qsm;
+      for (int64_t rb = ra;; rb += QP_XCH) {
+        const int64_t re = min(m, rb + QP_XCH);
+        const int nr = (int)max((int64_t)0, re - rb);
+        const bool first = (rb == ra), last = (re >= m);
+        __syncthreads();
+        for (int e = 2 * tid; e < nr; e += 2 * QP_T) {
+          if (e + 1 < nr)
+            *reinterpret_cast<double2*>(xs + e) = __ldcg(reinterpret_cast<const double2*>(xcol + rb + e));
+          else
+            xs[e] = __ldcg(xcol + rb + e);
         }
-        for (; r + 1 < m; r += 64) {
-          const double2 a0 = ldcs2(ac + r);
-          const double2 x0v = *reinterpret_cast<const double2*>(xcol + r);
-          d0 = fma(x0v.x, a0.x, d0);
-          d1 = fma(x0v.y, a0.y, d1);
+        __syncthreads();
+        for (int64_t col = s0 + gw; col < n; col += NW) {
+          if (col == s) continue;
+          const double* ac = A + col * lda;
+          double as = 0.0, prev = 0.0;
+          if (lane == 0) {
+            if (last) as = ac[s];
+            if (!first) prev = a.wb[col];
+          }
+          double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+          if (first && lane == 0 && ra > r1 && r1 < m) d0 = xcol[r1] * ac[r1];
+          const double* ap = ac + rb;
+          int r = 2 * lane;
+          for (; r + 7 * 64 + 1 < nr; r += 8 * 64) {
+            double2 av[8], xv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) av[k] = ldcs2(ap + r + 64 * k);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) xv[k] = *reinterpret_cast<const double2*>(xs + r + 64 * k);
+#pragma unroll
+            for (int k = 0; k < 8; k += 2) {
+              d0 = fma(xv[k].x, av[k].x, d0);
+              d1 = fma(xv[k].y, av[k].y, d1);
+              d2 = fma(xv[k + 1].x, av[k + 1].x, d2);
+              d3 = fma(xv[k + 1].y, av[k + 1].y, d3);
+            }
+          }
+          for (; r + 1 < nr; r += 64) {
+            const double2 a0 = ldcs2(ap + r);
+            const double2 x0v = *reinterpret_cast<const double2*>(xs + r);
+            d0 = fma(x0v.x, a0.x, d0);
+            d1 = fma(x0v.y, a0.y, d1);
+          }
+          if (r < nr) d2 = fma(xs[r], ap[r], d2);
+          const double d = warp_sum((d0 + d1) + (d2 + d3)) + prev;
+          if (lane == 0) a.wb[col] = last ? as + d / u0 : d;  // (as: the stored row s)
         }
-        if (r < m) d2 = fma(xcol[r], ac[r], d2);
-        const double d = warp_sum((d0 + d1) + (d2 + d3));
-        if (lane == 0) a.wb[col] = ac[s] + d / u0;  // (ac[s]: the stored row s)
+        if (last) break;
       }
     }
     gsync();
 
     // ================= beta =================
+    QCLK(3);
     for (int q = tid; q < t; q += QP_T) {
       s_z[q] = __ldcg(a.wb + s0 + q);
       s_y[q] = A[s + (s0 + q) * lda];
@@ -367,10 +434,15 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
           pr = a.uref[mine];
         }
         const int cnt = (int)min((int64_t)32, (n - cb + NW - 1) / NW);
+        double f0n = (lane < t) ? F[cb * QP_NB + lane] : 0.0, f1n = (lane + 32 < t) ? F[cb * QP_NB + lane + 32] : 0.0;
         for (int k = 0; k < cnt; ++k) {
           const int64_t col = cb + (int64_t)k * NW;
-          const double* fr = F + col * QP_NB;
-          const double f0 = (lane < t) ? fr[lane] : 0.0, f1 = (lane + 32 < t) ? fr[lane + 32] : 0.0;
+          const double f0 = f0n, f1 = f1n;
+          if (k + 1 < cnt) {  // next column's F row in flight while this one reduces
+            const double* fr = F + (col + NW) * QP_NB;
+            f0n = (lane < t) ? fr[lane] : 0.0;
+            f1n = (lane + 32 < t) ? fr[lane + 32] : 0.0;
+          }
           const double fz = warp_sum(fma(f0, z0, f1 * z1));
           const double fy = warp_sum(fma(f0, y0, f1 * y1));
           if (lane == k) {
@@ -421,6 +493,7 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
     gsync();
 
     // ================= guard =================
+    QCLK(4);
     const int g = (int)__ldcg(a.cnt + 1);
     g_prev = g;
     ++t;
@@ -506,12 +579,18 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
           if (lane == 0) {
             a.u[col] = fresh;
             a.uref[col] = fresh;
+            a.gfresh[gi] = fresh;
           }
         }
-        if (tid == 0) a.cnt[2] = 0u;
+        __syncthreads();
+        if (tid == 0) {
+          a.cnt[2] = 0u;
+          a.cnt[1] = 0u;  // every CTA read g before it arrived here
+          __threadfence();
+          asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(a.cnt + 3), "r"((unsigned)t) : "memory");
+        }
       }
-      gsync();
-      if (b == 0 && tid == 0) a.cnt[1] = 0u;  // every CTA has read g (before the barrier)
+      // (no barrier: the next gamma waits for cnt[3] == t)
     } else if (g > QP_GMAX) {
       // too many guards for the in-place recompute: end the block here; they are
       // recomputed from the updated matrix below
@@ -520,6 +599,7 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
 
   // ================= block end: C -= Y F^T below the block's R rows =================
   const int64_t c0 = s0 + t;
+  if (a.dbg && b == 0 && tid == 0) a.dbg[512] = gtimer();
   if (t > 0 && c0 < n && c0 < m) {
     const int64_t ncols = n - c0;
     for (int64_t e = (int64_t)b * QP_T + tid; e < (int64_t)t * ncols; e += (int64_t)G * QP_T) {
@@ -527,6 +607,7 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
       a.Wt[q * a.ldz + col] = F[(c0 + col) * QP_NB + q];
     }
     gsync();
+    if (a.dbg && b == 0 && tid == 0) a.dbg[513] = gtimer();
     const int64_t mp = m - s0;
     const int odd = (int)(s0 & 1);
     const int64_t ntr = ceil_div(mp + odd, TB_ROWS), ntc = ceil_div(ncols, TB_COLS);
@@ -536,6 +617,7 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
       __syncthreads();
       trail_b_tile<true>(A, a.Wt, a.ldz, nullptr, s0, m, lda, t, c0, ncols, mp, row0, col0);
     }
+    if (a.dbg && b == 0 && tid == 0) a.dbg[514] = gtimer();
     if (exit_reason == 5) {
       gsync();
       // exact norms of the guard columns from the updated rows [c0, m)
@@ -578,6 +660,7 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
         a.uref[__ldcg(a.glist + gi)] = 0.0;
       }
   }
+#undef QCLK
   if (b == 0 && tid == 0) {
     c->n_s = (int32_t)c0;
     c->step_idx = step_idx;
