@@ -572,6 +572,10 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
                     dim3(GU_T), GU_SMEM, st, ctl, A, (const double*)Z, ldz, upd, u, uref, (const int32_t*)glist,
                     lacount + 2));
       NOTE_LAUNCH();
+      CK(pdl_launch(k_guard_norms, dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(np * 32, 256),
+                                                                                      (int64_t)d.sms * 8))),
+                    dim3(256), 0, st, ctl, (const double*)A, upd, u, uref, (const int32_t*)glist));
+      NOTE_LAUNCH();
     } else if (np > 0) {
       const int64_t blocks = std::min<int64_t>(ceil_div(np * 32, 256), (int64_t)d.sms * 16);
       k_downdate<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, uref);

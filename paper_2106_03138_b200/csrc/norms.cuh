@@ -119,6 +119,7 @@ __global__ void k_colnorms_init(const double* __restrict__ A, int64_t m, int64_t
 __global__ void k_downdate(Ctl* __restrict__ c, const double* __restrict__ A, double* __restrict__ u,
                            double* __restrict__ uref) {
   if (c->done) return;
+  TLSpan tl_span(c->step_idx, 12);
   const int64_t n_s = c->n_s, n_s1 = n_s + c->l_acc, n = c->n, m = c->m, lda = c->lda;
   const int lane = threadIdx.x & 31;
   if (blockIdx.x == 0)

@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_trail_b(Ctl* __restrict__ c, double
                                                      uint8_t* __restrict__ upd, unsigned* __restrict__ counter) {
   pdl_enter();
   const CtlSnap S = snap(c);
+  TLSpan tl_span(S.step_idx, 11);
   if (LA ? !S.pend : S.done) return;
   const int64_t m = S.m, n = S.n, lda = S.lda;
   const int64_t n_s = LA ? S.pend_ns : S.n_s;
@@ -927,7 +928,25 @@ __global__ void __launch_bounds__(GU_T) k_guard(Ctl* __restrict__ c, double* __r
     if (full) c->pend_done = 1;      // k_step_end: nothing is pending after this step
     if (full || cnt > 32) c->la_bad = 1;  // guards are not rare here: the host goes serial
   }
-  for (int q = wid; q < cnt; q += GU_T / 32) {
+  // (the guard columns' exact norms: k_guard_norms, grid-wide, right behind)
+}
+
+// Exact norms of k_guard's columns (k_downdate's arithmetic), a warp per
+// column over the whole grid; then the columns' look-ahead flags (set while an
+// update is still pending; all cleared when k_guard finished the whole update).
+__global__ void __launch_bounds__(256) k_guard_norms(Ctl* __restrict__ c, const double* __restrict__ A,
+                                                      uint8_t* __restrict__ upd, double* __restrict__ u,
+                                                      double* __restrict__ uref, const int32_t* __restrict__ glist) {
+  pdl_enter();
+  const CtlSnap S = snap(c);
+  const int cnt = c->gcount;
+  if (S.done || cnt == 0) return;
+  const int64_t m = S.m, lda = S.lda, base = S.n_s + S.l_acc;
+  const bool full = (int64_t)cnt * 8 > S.n - base;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t q = w0; q < cnt; q += nw) {
     const int64_t j = glist[q];
     const double nu = warp_col_norm(A + j * lda + base, m - base, lane);
     if (lane == 0) {
@@ -936,10 +955,9 @@ __global__ void __launch_bounds__(GU_T) k_guard(Ctl* __restrict__ c, double* __r
       if (!full) upd[j] = 1;  // (an update is pending: guards exist only with rows below and tiles past tc0)
     }
   }
-  if (full) {
-    __syncthreads();
-    for (int64_t j = tid; j < S.n; j += GU_T) upd[j] = 0;
-  }
+  if (full)
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.n; j += (int64_t)gridDim.x * blockDim.x)
+      upd[j] = 0;
 }
 
 // ---------------------------------------------------------------------------
