@@ -31,6 +31,7 @@
 #include "select.cuh"
 #include "trailing.cuh"
 #include "qp3.cuh"
+#include "formq.cuh"
 
 using namespace dmqr;
 
@@ -138,6 +139,9 @@ int set_attrs(const DevInfo& d) {
   CK(cudaFuncSetAttribute(k_ygemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YG_SMEM));
   CK(cudaFuncSetAttribute(k_trail_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TP_SMEM));
   CK(cudaFuncSetAttribute(k_qp3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QP_SMEM));
+  CK(cudaFuncSetAttribute(k_fq_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FQ_SMEM2));
+  CK(cudaFuncSetAttribute(k_fq_tw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FQ_SMEM2));
+  CK(cudaFuncSetAttribute(k_fq_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FQ_SMEM2));
   {
     int nb = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_qp3, QP_T, QP_SMEM));
@@ -298,8 +302,11 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   // candidates get it first (in k_gram).
   // (small problems -- e.g. the 256^2 batch of cfg3 -- are launch-bound: serial form)
   // (tall inputs -- m > 4n, like cfg4 -- hit norm guards too often: serial)
+  // (past n = 12288 the trailing update outweighs the panel it would hide, and
+  // graded inputs make its guard path expensive: serial -- measured on cfg2 /
+  // cfg5 at 8192, 12288, 16384)
   const bool la_all = !qrp && !p->trace_norms && getenv("DMQR_NO_LOOKAHEAD") == nullptr &&
-                      m * n >= (int64_t)1 << 20 && m <= 4 * n;
+                      m * n >= (int64_t)1 << 20 && m <= 4 * n && n <= 12288;
 
 
   const int64_t kmax = std::min(m, n);
@@ -863,7 +870,10 @@ int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_
 
 size_t dmqr_form_q_workspace_bytes(int64_t m, int64_t qcols) {
   (void)m;
-  return al(sizeof(double) * std::max<int64_t>(qcols, 1));
+  const size_t q = (size_t)std::max<int64_t>(qcols, 1);
+  // Wp (splits x 64 x qcols), W (64 x qcols), Sp (splits x 64 x 64), T (64 x 64)
+  return al(sizeof(double) * FQ_NSPLIT * FQ_NB * q) + al(sizeof(double) * FQ_NB * q) +
+         al(sizeof(double) * FQ_NSPLIT * FQ_NB * FQ_NB) + al(sizeof(double) * FQ_NB * FQ_NB);
 }
 
 int dmqr_form_q_f64(const double* packed, int64_t m, int64_t n, int64_t lda, const double* coeffs,
@@ -874,19 +884,39 @@ int dmqr_form_q_f64(const double* packed, int64_t m, int64_t n, int64_t lda, con
     return DMQR_EINVAL;
   if (ws_bytes < dmqr_form_q_workspace_bytes(m, qcols)) return DMQR_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  double* w = (double*)workspace;
   if (m == 0 || qcols == 0) return 0;
+  {
+    int rc = set_attrs(dev_info());
+    if (rc) return rc;
+  }
+  const size_t q = (size_t)qcols;
+  unsigned char* wsb = (unsigned char*)workspace;
+  double* Wp = (double*)wsb;
+  double* W = (double*)(wsb + al(sizeof(double) * FQ_NSPLIT * FQ_NB * q));
+  double* Sp = (double*)((unsigned char*)W + al(sizeof(double) * FQ_NB * q));
+  double* T = (double*)((unsigned char*)Sp + al(sizeof(double) * FQ_NSPLIT * FQ_NB * FQ_NB));
   k_q_init<<<(unsigned)std::min<int64_t>(ceil_div(m * qcols, 256), 148 * 16), 256, 0, st>>>(Q, m, qcols, ldq);
   NOTE_LAUNCH();
-  for (int64_t s = std::min(n_factored, qcols) - 1; s >= 0; --s) {
-    const int64_t cols = qcols - s;
-    k_q_dots<<<(unsigned)ceil_div(cols * 32, 256), 256, 0, st>>>(packed, m, lda, coeffs, s, Q, qcols, ldq, w);
+  // reflectors s >= qcols act on rows >= s, where [I; 0] is still zero: no-ops
+  const int64_t p = std::min(n_factored, qcols);
+  for (int64_t j0 = (p > 0 ? (p - 1) / FQ_NB * FQ_NB : 0); p > 0 && j0 >= 0; j0 -= FQ_NB) {
+    const int nb = (int)std::min<int64_t>(FQ_NB, p - j0);
+    const int64_t mp = m - j0, cols = qcols - j0;
+    const int64_t split_rows = std::max<int64_t>(1024, ceil_div(ceil_div(mp, FQ_NSPLIT), FQ_KR) * FQ_KR);
+    const int nsplit = (int)ceil_div(mp, split_rows);
+    k_fq_w<<<dim3(1, nsplit), FQ_T, 0, st>>>(packed, lda, j0, nb, mp, nullptr, 0, FQ_NB, Sp, split_rows);
     NOTE_LAUNCH();
-    k_q_update<<<(unsigned)std::min<int64_t>(ceil_div((m - s) * cols, 256), 148 * 16), 256, 0, st>>>(
-        packed, m, lda, s, Q, qcols, ldq, w);
+    k_fq_t<<<1, FQ_T, FQ_SMEM2, st>>>(Sp, nsplit, nb, coeffs, j0, T);
+    NOTE_LAUNCH();
+    k_fq_w<<<dim3((unsigned)ceil_div(cols, FQ_NB), nsplit), FQ_T, 0, st>>>(packed, lda, j0, nb, mp, Q, ldq, cols,
+                                                                          Wp, split_rows);
+    NOTE_LAUNCH();
+    k_fq_tw<<<(unsigned)ceil_div(cols, FQ_NB), FQ_T, FQ_SMEM2, st>>>(Wp, nsplit, nb, T, cols, W);
+    NOTE_LAUNCH();
+    k_fq_upd<<<dim3((unsigned)ceil_div(cols, FQ_NB), (unsigned)ceil_div(mp, FQ_NB)), FQ_T, FQ_SMEM2, st>>>(
+        packed, lda, j0, nb, mp, Q, ldq, cols, W);
     NOTE_LAUNCH();
   }
-  // reflectors s >= qcols act on rows >= s, where [I; 0] is still zero: no-ops
   CK(cudaGetLastError());
   return 0;
 }

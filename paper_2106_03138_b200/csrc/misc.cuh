@@ -195,30 +195,6 @@ __global__ void k_q_init(double* __restrict__ Q, int64_t m, int64_t qcols, int64
 }
 
 // w[j] = coeff * v^T Q[s:, j] for j in [s, qcols): warp per column
-__global__ void k_q_dots(const double* __restrict__ P, int64_t m, int64_t lda, const double* __restrict__ coeffs,
-                         int64_t s, const double* __restrict__ Q, int64_t qcols, int64_t ldq, double* __restrict__ w) {
-  const int lane = threadIdx.x & 31;
-  const int64_t j = s + ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
-  if (j >= qcols) return;
-  const double* v = P + s * lda;
-  const double* q = Q + j * ldq;
-  double acc = 0.0;
-  for (int64_t r = s + lane; r < m; r += 32) acc = fma(r == s ? 1.0 : v[r], q[r], acc);
-  acc = warp_sum(acc);
-  if (lane == 0) w[j] = coeffs[s] * acc;
-}
-
-__global__ void k_q_update(const double* __restrict__ P, int64_t m, int64_t lda, int64_t s, double* __restrict__ Q,
-                           int64_t qcols, int64_t ldq, const double* __restrict__ w) {
-  const int64_t rows = m - s, cols = qcols - s;
-  const int64_t tot = rows * cols;
-  const double* v = P + s * lda;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = s + e / rows, r = s + e % rows;
-    const double vr = (r == s) ? 1.0 : v[r];
-    Q[r + j * ldq] -= vr * w[j];
-  }
-}
 
 }  // namespace dmqr
 

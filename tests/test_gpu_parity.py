@@ -271,3 +271,88 @@ def test_lookahead_matches_serial_schedule(shape, monkeypatch):
     assert np.abs(la.packed - se.packed).max() <= 1e-10 * scale
     resid, orth = parity.residuals(A, la)
     assert resid <= 50 * max(m, n) * O.EPS and orth <= 50 * max(m, n) * O.EPS
+
+
+# ----------------------------------------------------------------------------
+# BASELINE full sizes: size-independent properties, computed on the device
+# (Q from the blocked dmqr_form_q_f64; products by torch / cuBLAS in fp64 --
+# test harness only)
+# ----------------------------------------------------------------------------
+
+def _device_residuals(A_dev, res):
+    """||A P - Q R||_F / ||A||_F and ||Q^T Q - I||_F with thin Q (m x min(m, n))."""
+    import torch
+    from paper_2106_03138_b200 import form_q
+
+    m, n = A_dev.shape
+    packed = res.packed  # device (m x n) view
+    k = min(m, n)
+    Q = form_q(packed, res.coeffs, res.n_factored, qcols=k)
+    R = torch.triu(packed[:k, :].clone())
+    nf = res.n_factored
+    if nf < k:  # the raw trailing block below row nf (columns >= nf) is part of R
+        R[nf:, nf:] = packed[nf:k, nf:]
+    perm = torch.as_tensor(np.asarray(res.perm.forward), device=A_dev.device)
+    AP = A_dev[:, perm]
+    if m > k:  # rows past k of the trailing block: Q is thin, so fold them in explicitly
+        # A P = Q_full R_full; with the thin Q the rows >= k of R (only in columns >= nf) are lost:
+        # require them to be zero-sized (nf == k) for tall inputs
+        assert nf == k or m == k
+    resid = (torch.linalg.matrix_norm(AP - Q @ R) / torch.linalg.matrix_norm(A_dev)).item()
+    orth = torch.linalg.matrix_norm(Q.T @ Q - torch.eye(k, dtype=Q.dtype, device=Q.device)).item()
+    return resid, orth
+
+
+@pytest.mark.parametrize("algo", ["qrdm2", "qrdm"])
+def test_cfg2_full_size_vs_oracle(algo):
+    """BASELINE cfg2 (4096^2 N(0,1), seed 1) at full size: the same permutation
+    and rank as the CPU oracle (all host BLAS threads), residual and
+    orthogonality <= 50 n eps."""
+    import torch
+    from paper_2106_03138_b200 import inputs, qrdm, qrdm2
+
+    A = inputs.cfg2(seed=1)
+    res = (qrdm2 if algo == "qrdm2" else qrdm)(A, device=True)
+    ref = (O.qrdm2 if algo == "qrdm2" else O.qrdm)(A, margins=True)
+    cut, full = parity.robust_prefix(ref)
+    assert np.array_equal(np.asarray(res.perm.forward)[:cut], ref.forward[:cut])
+    if full:
+        assert np.array_equal(np.asarray(res.perm.forward), ref.forward) and res.rank == ref.rank
+    assert res.rank == 4096 and len(res.step_log) == len(ref.steps)
+    resid, orth = _device_residuals(torch.as_tensor(A, device="cuda"), res)
+    bound = 50 * 4096 * O.EPS
+    assert resid <= bound and orth <= bound, (resid, orth)
+
+
+def test_cfg4_full_size_properties():
+    """BASELINE cfg4 (65536 x 1024 tall, graded columns) at full size on the device."""
+    import torch
+    from paper_2106_03138_b200 import inputs, qrdm2
+
+    A = inputs.device_cfg("cfg4", seed=4)
+    res = qrdm2(A, device=True)
+    assert res.rank == 1024 and not res.stopped_early
+    resid, orth = _device_residuals(A, res)
+    bound = 50 * 65536 * O.EPS
+    assert resid <= bound and orth <= bound, (resid, orth)
+
+
+@pytest.mark.parametrize("algo", ["qrdm2", "qrp"])
+def test_cfg5_full_size_properties(algo):
+    """BASELINE cfg5 (16384^2 graded, near-collinear columns) at full size: the
+    rank-revealing stop (sqrt(n - k) max trailing norm <= n eps ||a||_max,
+    rrqr.py:189-203), residual and orthogonality <= 50 n eps."""
+    import torch
+    from paper_2106_03138_b200 import inputs, qrdm2, qrp
+
+    n = 16384
+    A = inputs.device_cfg("cfg5", seed=4)
+    res = (qrdm2 if algo == "qrdm2" else qrp)(A, device=True)
+    assert res.stopped_early and 9000 < res.rank < 10500, res.rank
+    k = res.rank
+    a0 = torch.linalg.vector_norm(A, dim=0).max().item()
+    trail = torch.linalg.vector_norm(res.packed[k:, k:], dim=0).max().item()
+    assert np.sqrt(n - k) * trail <= n * O.EPS * a0 * (1 + 1e-6), (trail, a0)
+    resid, orth = _device_residuals(A, res)
+    bound = 50 * n * O.EPS
+    assert resid <= bound and orth <= bound, (resid, orth)
