@@ -156,6 +156,20 @@ def test_qrp_trace_norms():
     assert max(res.norm_trace) <= 1e-10
 
 
+def test_registry_run_algorithm_on_device():
+    """registry.run_algorithm (harness.py:188-198 surface) dispatches to the device engine."""
+    from paper_2106_03138_b200 import DMParams, StopCriterion, qrp, registry
+
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((90, 70))
+    a = registry.run_algorithm("qrp", A, DMParams(), StopCriterion())
+    b = qrp(A)
+    assert np.array_equal(a.packed, b.packed) and np.array_equal(a.perm.forward, b.perm.forward)
+    ref_style = registry.register({})
+    c = ref_style["qrdm2_b200"](A, params=DMParams(), stop=StopCriterion())
+    assert c.rank == registry.run_algorithm("qrdm2", A, DMParams(), StopCriterion()).rank
+
+
 def test_trace_norms_within_1e10():
     rng = np.random.default_rng(39)
     A = rng.standard_normal((250, 180))
