@@ -58,6 +58,7 @@ struct Ctl {
   int32_t pad3;
   // blocked scalar pivoting (k_qp3): columns factored by the last launch and why it ended
   int32_t qp_cols, qp_exit;
+  uint32_t m_pub;  // k_panel_cq: step_idx + 1 once M (Y = Q1 M) and l are final
   // inter-CTA counters (reset by their users)
   uint32_t gram_count;
   uint32_t bar_count;

@@ -74,12 +74,12 @@ Layout layout(int64_t m, int64_t n) {
   L.pdbg = take(sizeof(long long) * 64 * 16);
   L.tcount = take(sizeof(unsigned) * (ceil_div(std::max<int64_t>(n, 1), TA_COLS) + 1));
   L.upd = take(std::max<int64_t>(n, 1));                      // look-ahead column flags
-  L.lacount = take(sizeof(unsigned) * 8);                     // look-ahead work / last-CTA counters
+  L.lacount = take(sizeof(unsigned) * 16);                    // look-ahead work / last-CTA counters
   L.q1g = take(sizeof(double) * DMQR_KP * q1_ld(m));  // published Q1 (k_spare)
   L.glist = take(sizeof(int32_t) * std::max<int64_t>(n, 1));  // look-ahead / k_qp3 guard columns
   // blocked scalar pivoting (k_qp3; its F = Zp, its Wt = Z: both are free between steps)
   L.qvb = take(sizeof(double) * std::max<int64_t>(m, 1));
-  L.qwb = take(sizeof(double) * std::max<int64_t>(n, 1));
+  L.qwb = take(sizeof(double) * std::max<int64_t>(n, 1) * QP_RMAX);
   L.qpart = take(sizeof(double) * QP_GMAXCTA * QP_PLD);
   L.qgpart = take(sizeof(double) * (QP_GMAXCTA * QP_GMAX * 2 + QP_GMAX));  // + the fresh guard norms
   L.qcnt = take(sizeof(unsigned) * 4);
@@ -320,7 +320,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   CK(cudaMemsetAsync(T, 0, sizeof(double) * DMQR_KP * DMQR_KP, st));
   CK(cudaMemsetAsync(tcount, 0, sizeof(unsigned) * (ceil_div(std::max<int64_t>(n, 1), TA_COLS) + 1), st));
   CK(cudaMemsetAsync(upd, 0, (size_t)std::max<int64_t>(n, 1), st));
-  CK(cudaMemsetAsync(lacount, 0, sizeof(unsigned) * 8, st));
+  CK(cudaMemsetAsync(lacount, 0, sizeof(unsigned) * 16, st));
   if (n > 0) {
     if (m > 0) {
       int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)d.sms * 16);
@@ -519,7 +519,8 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
         cfg.numAttrs = 1;
         NOTE_LAUNCH();
         CK(cudaLaunchKernelEx(&cfg, k_spare, ctl, A, (const double*)Z, ldz, upd, (const double*)q1g, Zp,
-                              lacount + 4, Pcq, nsplit_g, tcount, tline));
+                              lacount + 4, Pcq, nsplit_g, tcount, tline,
+                              (const double*)(red + 37 * DMQR_KP * DMQR_KP)));
       }
     }
     if (cl_path) {
@@ -536,7 +537,8 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
       k_panel<<<1, PANEL_T, smem, st>>>(pa);
       NOTE_LAUNCH();
     }
-    if (cq_path && mp > 1) {  // Y below the top block of a CholeskyQR2 panel, on every SM
+    if (cq_path && mp > 1 && !spare) {  // Y below the top block of a CholeskyQR2 panel, on every SM
+      // (with the look-ahead, k_spare does this as its third phase)
       CK(pdl_launch(k_ygemm, dim3((unsigned)ceil_div(mp - 1, YG_ROWS)), dim3(256), YG_SMEM, st, ctl, A,
                     (const double*)q1g, (const double*)(red + 37 * DMQR_KP * DMQR_KP)));
       NOTE_LAUNCH();
@@ -614,6 +616,9 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   int64_t known_ns = 0;  // n_s after the last step whose head was read
   int known = 0, enq = 0, known_steps = 0;
   bool qp_mode = qrp != 0;
+  // k_qp3 splits each column into at most QP_RMAX staged row segments
+  const bool qp_ok = m <= (int64_t)QP_RMAX * QP_XCH;
+  if (qrp && !qp_ok) return DMQR_EINVAL;
   bool finished = (kmax == 0);
   auto consume = [&]() -> int {
     const int sl = known & 1;
@@ -653,12 +658,13 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     if (r->flags & 2) want_serial = true;
     // a scalar-fallback step hands the run to the blocked scalar-pivot engine;
     // its blocks keep it until a fallback run ends on the floor test
-    qp_mode = qrp || (r->flags & 4) != 0;
+    qp_mode = qrp || ((r->flags & 4) != 0 && qp_ok);
     return stream_cols(known_ns, nullptr);  // columns left of n_s are final (and written)
   };
   // one block of the blocked scalar-pivot engine (no step in flight)
   const int qp_clk = getenv("DMQR_QP_CLOCKS") ? atoi(getenv("DMQR_QP_CLOCKS")) : -1;
   int qp_blocks = 0;
+  const bool qp_verbose = getenv("DMQR_QP_VERBOSE") != nullptr;  // debug: columns per block
   auto run_qp_block = [&]() -> int {
     if (la_on && !la_off) {  // flush the look-ahead's pending update; serial from here on
       const int64_t ldz0 = ldz_for(n);
@@ -698,7 +704,11 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     CK(cudaGetLastError());
     ++enq;
     ++steps_done;
-    return consume();
+    const int before = known_steps;
+    const int rc = consume();
+    if (qp_verbose) fprintf(stderr, "[dmqr] qp block %d: %d columns, n_s %lld\n", qp_blocks - 1,
+                            known_steps - before, (long long)known_ns);
+    return rc;
   };
   while (!finished) {
     if (qp_mode) {

@@ -50,7 +50,9 @@ constexpr int QP_PLD = 8;     // per-CTA partial record (doubles)
 constexpr int QP_GMAXCTA = 320;  // grid cap (2 CTAs x 148 SMs fits)
 constexpr int QP_SUB = 64;       // guard phase: rows per staged sub-chunk
 constexpr size_t QP_SMEM = TB_SMEM;  // the block update's tile staging is the largest user
-constexpr int QP_XCH = 13312;        // rows of x staged per chunk in alpha (104 KB)
+constexpr int QP_XCH = 12288;        // rows of x staged per chunk in alpha (96 KB)
+constexpr int QP_SEG = 2048;         // rows per alpha work item (at least)
+constexpr int QP_RMAX = 32;          // segment slots per column in wb
 static_assert(sizeof(double) * QP_XCH <= QP_SMEM, "x staging");
 static_assert(sizeof(double) * (QP_SUB * (QP_NB + 1) + QP_GMAX * (QP_NB + 1)) <= QP_SMEM, "guard staging");
 
@@ -67,7 +69,7 @@ struct Qp3Args {
   double* Wt;       // block update: Wt[t * ldz + (col - c0)]
   int64_t ldz;
   double* vb;       // [m] v of the current reflector
-  double* wb;       // [n] w_c (and z for the block's own columns)
+  double* wb;       // [n][QP_RMAX] per-segment partial dots of w_c (and z for the block's own columns)
   double* part;     // [G][QP_PLD]
   double* gpart;    // [G][QP_GMAX][2]
   int32_t* glist;   // guard columns of the current column step (capacity n)
@@ -84,6 +86,17 @@ __device__ __forceinline__ void am_merge(double& bv, int& bi, double ov, int oi)
     bv = ov;
     bi = oi;
   }
+}
+
+// alpha's row split of the column step at s: segment length and count (rows
+// from the first even row past s; >= 1 segment so the head row is counted)
+__device__ __forceinline__ int qp_seg_len(int64_t m, int64_t s) {
+  const int64_t nrt = max((int64_t)0, m - (((s + 1) + 1) & ~(int64_t)1));
+  return (int)max((int64_t)QP_SEG, ceil_div(ceil_div(nrt, QP_RMAX), 64) * 64);
+}
+__device__ __forceinline__ int qp_nseg(int64_t m, int64_t s) {
+  const int64_t nrt = max((int64_t)0, m - (((s + 1) + 1) & ~(int64_t)1));
+  return (int)max((int64_t)1, ceil_div(nrt, qp_seg_len(m, s)));
 }
 
 __device__ __forceinline__ double2 ldcs2(const double* p) { return __ldcs(reinterpret_cast<const double2*>(p)); }
@@ -352,16 +365,24 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
     // w_c = v^T A[s:, c] = A[s, c] + (x[s+1:] . A[s+1:, c]) / u0 for the trailing
     // columns and the block's own reflector columns (z)
     // x is staged in shared memory by row chunks (every warp of the CTA streams
-    // its columns against it; L1 is mostly carved out for the tile staging)
+    // its columns against it; L1 is mostly carved out for the tile staging).
+    // Work items are (column, 2048-row segment) pairs dealt round-robin to the
+    // warps, two at a time per warp (two independent 16-byte load streams);
+    // each item's dot goes to its own slot wb[col][seg], summed in fixed
+    // order in beta (w_c = A[s, c] + sum / u0).
     {
       const double* xcol = A + s * lda;
       const int64_t r1 = s + 1;
       const int64_t ra = (r1 + 1) & ~(int64_t)1;  // first even row >= s+1 (16-byte aligned pairs)
+      const int seg = qp_seg_len(m, s);
+      const int nseg = qp_nseg(m, s);
+      const int spc = max(1, QP_XCH / seg);        // segments per staged x chunk
+      const int64_t ncol_a = n - s0 - 1;           // columns [s0, n) except s
       double* xs = qsm;
-      for (int64_t rb = ra;; rb += QP_XCH) {
-        const int64_t re = min(m, rb + QP_XCH);
-        const int nr = (int)max((int64_t)0, re - rb);
-        const bool first = (rb == ra), last = (re >= m);
+      for (int sg0 = 0; sg0 < nseg; sg0 += spc) {
+        const int nsc = min(spc, nseg - sg0);
+        const int64_t rb = ra + (int64_t)sg0 * seg;
+        const int nr = (int)max((int64_t)0, min(m, rb + (int64_t)nsc * seg) - rb);
         __syncthreads();
         for (int e = 2 * tid; e < nr; e += 2 * QP_T) {
           if (e + 1 < nr)
@@ -370,52 +391,66 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
             xs[e] = __ldcg(xcol + rb + e);
         }
         __syncthreads();
-        for (int64_t col = s0 + gw; col < n; col += NW) {
-          if (col == s) continue;
-          const double* ac = A + col * lda;
-          double as = 0.0, prev = 0.0;
-          if (lane == 0) {
-            if (last) as = ac[s];
-            if (!first) prev = a.wb[col];
-          }
-          double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-          if (first && lane == 0 && ra > r1 && r1 < m) d0 = xcol[r1] * ac[r1];
-          const double* ap = ac + rb;
-          int r = 2 * lane;
-          for (; r + 7 * 64 + 1 < nr; r += 8 * 64) {
-            double2 av[8], xv[8];
+        const int64_t nitems = ncol_a * nsc;
+        for (int64_t i0 = gw; i0 < nitems; i0 += 2 * (int64_t)NW) {
+          const int64_t i1 = i0 + NW;
+          const bool has1 = i1 < nitems;
+          const int64_t ci0 = i0 / nsc, ci1 = has1 ? i1 / nsc : ci0;
+          const int sq0 = (int)(i0 % nsc), sq1 = has1 ? (int)(i1 % nsc) : 0;
+          const int64_t col0 = s0 + ci0 + (s0 + ci0 >= s ? 1 : 0);
+          const int64_t col1 = s0 + ci1 + (s0 + ci1 >= s ? 1 : 0);
+          const int xo0 = sq0 * seg, xo1 = sq1 * seg;
+          const int len0 = max(0, min(seg, nr - xo0)), len1 = has1 ? max(0, min(seg, nr - xo1)) : 0;
+          const double* ap0 = A + col0 * lda + rb + xo0;
+          const double* ap1 = A + col1 * lda + rb + xo1;
+          const double* xp0 = xs + xo0;
+          const double* xp1 = xs + xo1;
+          double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+          if (lane == 0 && sg0 + sq0 == 0 && ra > r1 && r1 < m) d0 = xcol[r1] * A[r1 + col0 * lda];
+          if (has1 && lane == 0 && sg0 + sq1 == 0 && ra > r1 && r1 < m) e0 = xcol[r1] * A[r1 + col1 * lda];
+          const int lmax = max(len0, len1);
+          for (int r = 2 * lane; r < lmax; r += 4 * 64) {
+            double2 av[4], bv[4];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) av[k] = ldcs2(ap + r + 64 * k);
+            for (int k = 0; k < 4; ++k) {
+              const int rr = r + 64 * k;
+              av[k] = (rr + 1 < len0) ? ldcs2(ap0 + rr) : make_double2(rr < len0 ? ap0[rr] : 0.0, 0.0);
+              bv[k] = (rr + 1 < len1) ? ldcs2(ap1 + rr) : make_double2(rr < len1 ? ap1[rr] : 0.0, 0.0);
+            }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) xv[k] = *reinterpret_cast<const double2*>(xs + r + 64 * k);
-#pragma unroll
-            for (int k = 0; k < 8; k += 2) {
-              d0 = fma(xv[k].x, av[k].x, d0);
-              d1 = fma(xv[k].y, av[k].y, d1);
-              d2 = fma(xv[k + 1].x, av[k + 1].x, d2);
-              d3 = fma(xv[k + 1].y, av[k + 1].y, d3);
+            for (int k = 0; k < 4; ++k) {
+              const int rr = r + 64 * k;
+              const double2 xa = (rr + 1 < len0) ? *reinterpret_cast<const double2*>(xp0 + rr)
+                                                 : make_double2(rr < len0 ? xp0[rr] : 0.0, 0.0);
+              const double2 xb = (rr + 1 < len1) ? *reinterpret_cast<const double2*>(xp1 + rr)
+                                                 : make_double2(rr < len1 ? xp1[rr] : 0.0, 0.0);
+              d0 = fma(xa.x, av[k].x, d0);
+              d1 = fma(xa.y, av[k].y, d1);
+              e0 = fma(xb.x, bv[k].x, e0);
+              e1 = fma(xb.y, bv[k].y, e1);
             }
           }
-          for (; r + 1 < nr; r += 64) {
-            const double2 a0 = ldcs2(ap + r);
-            const double2 x0v = *reinterpret_cast<const double2*>(xs + r);
-            d0 = fma(x0v.x, a0.x, d0);
-            d1 = fma(x0v.y, a0.y, d1);
+          const double dsum = warp_sum(d0 + d1);
+          const double esum = warp_sum(e0 + e1);
+          if (lane == 0) {
+            a.wb[col0 * QP_RMAX + sg0 + sq0] = dsum;
+            if (has1) a.wb[col1 * QP_RMAX + sg0 + sq1] = esum;
           }
-          if (r < nr) d2 = fma(xs[r], ap[r], d2);
-          const double d = warp_sum((d0 + d1) + (d2 + d3)) + prev;
-          if (lane == 0) a.wb[col] = last ? as + d / u0 : d;  // (as: the stored row s)
         }
-        if (last) break;
       }
     }
     gsync();
 
     // ================= beta =================
     QCLK(3);
+    // number of segment slots of this column step (alpha's split)
+    const int nseg_b = qp_nseg(m, s);
     for (int q = tid; q < t; q += QP_T) {
-      s_z[q] = __ldcg(a.wb + s0 + q);
-      s_y[q] = A[s + (s0 + q) * lda];
+      const double ys_ = A[s + (s0 + q) * lda];
+      double sum = 0.0;
+      for (int g = 0; g < nseg_b; ++g) sum += __ldcg(a.wb + (s0 + q) * QP_RMAX + g);
+      s_z[q] = ys_ + sum / u0;
+      s_y[q] = ys_;
     }
     __syncthreads();
     {
@@ -428,8 +463,10 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
         const int64_t mine = cb + (int64_t)lane * NW;
         double pw = 0.0, pa = 0.0, pu = 0.0, pr = 0.0;
         if (mine < n) {
-          pw = __ldcg(a.wb + mine);
           pa = A[s + mine * lda];
+          double sum = 0.0;
+          for (int g = 0; g < nseg_b; ++g) sum += __ldcg(a.wb + mine * QP_RMAX + g);
+          pw = pa + sum / u0;
           pu = a.u[mine];
           pr = a.uref[mine];
         }

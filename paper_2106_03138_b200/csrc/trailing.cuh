@@ -20,6 +20,7 @@
 #pragma once
 #include "common.cuh"
 #include "norms.cuh"
+#include "ygemm.cuh"
 
 namespace dmqr {
 
@@ -566,6 +567,7 @@ __device__ void g_partial(const double* __restrict__ A, const double* __restrict
 }
 
 constexpr size_t SP_SMEM = TB_SMEM > TA_SMEM ? TB_SMEM : TA_SMEM;
+static_assert(YG_SMEM <= SP_SMEM, "k_spare runs the Y = Q1 M tiles in its dynamic shared memory");
 constexpr int NSPLIT_MAXG = 16;
 
 __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* __restrict__ A,
@@ -573,7 +575,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
                                                    uint8_t* __restrict__ upd, const double* __restrict__ Q1g,
                                                    double* __restrict__ Gp, unsigned* __restrict__ ctr, int P,
                                                    int nsplit_g, unsigned* __restrict__ tcnt,
-                                                   long long* __restrict__ tline) {
+                                                   long long* __restrict__ tline, const double* __restrict__ gM) {
   const long long t_first = gtimer();
   __shared__ int s_item, s_flag;
   const int tid = threadIdx.x;
@@ -622,11 +624,27 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
       const int64_t ncols = n - n_s;
       const int ntile = (int)ceil_div(ncols, TA_COLS);
       const int ng = ntile * nsplit_g;
+      const int64_t nyg = ceil_div(m - n_s - 1, YG_ROWS);
       for (;;) {
-        if (tid == 0) s_item = (int)atomicAdd(&ctr[2], 1u);
+        // once the panel has published M, the Y = Q1 M tiles go first (they are
+        // latency-bound and would otherwise trail the G tiles)
+        if (tid == 0) {
+          int it = -1;
+          if (ld_acquire(&c->m_pub) == (unsigned)S.step_idx + 1u && ld_acquire(&ctr[4]) < (unsigned)nyg) {
+            const int y = (int)atomicAdd(&ctr[4], 1u);
+            if (y < nyg) it = -2 - y;
+          }
+          if (it == -1) it = (int)atomicAdd(&ctr[2], 1u);
+          s_item = it;
+        }
         __syncthreads();
         const int it = s_item;
         __syncthreads();
+        if (it <= -2) {
+          ygemm_tile(A, Q1g, gM, n_s, m, lda, c->l_acc, -2 - it);
+          __syncthreads();
+          continue;
+        }
         if (it >= ng) break;
         const int tile = it % ntile;
         g_partial(A, Q1g, Gp, ldz, n_s, m, lda, kk, ncols, (int64_t)tile * TA_COLS, it / ntile, nsplit_g);
@@ -658,7 +676,27 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
       }
     }
   }
-  // ---- the last CTA: reset the counters, then hold until the panel completes ----
+  // ---- phase 3: Y = Q1 M below the top block once the panel has completed
+  // (griddepcontrol.wait: the panel grid finished and its writes are visible),
+  // here on the spare SMs instead of a kernel behind this one ----
+  if (!S.done) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    __syncthreads();
+    if (!c->cq_fail) {
+      const int l = c->l_acc;
+      const int64_t nyg = ceil_div(m - S.n_s - 1, YG_ROWS);
+      for (;;) {
+        if (tid == 0) s_item = (int)atomicAdd(&ctr[4], 1u);
+        __syncthreads();
+        const int it = s_item;
+        __syncthreads();
+        if (it >= nyg) break;
+        ygemm_tile(A, Q1g, gM, S.n_s, m, lda, l, it);
+        __syncthreads();
+      }
+    }
+  }
+  // ---- the last CTA: reset the counters (every CTA has waited for the panel) ----
   if (tid == 0) {
     __threadfence();
     s_flag = (atomicAdd(&ctr[3], 1u) == gridDim.x - 1);
@@ -666,7 +704,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
   __syncthreads();
   if (s_flag) {
     if (tid == 0) {
-      ctr[0] = ctr[1] = ctr[2] = ctr[3] = 0u;
+      ctr[0] = ctr[1] = ctr[2] = ctr[3] = ctr[4] = 0u;
       if (tline) {
         tline[4 * (c->step_idx & 255) + 2] = t_first;
         tline[4 * (c->step_idx & 255) + 3] = gtimer();
