@@ -20,7 +20,8 @@ def main():
     work = rrqr.to_work(A)
     buf0 = work[0].clone()
     lib = _lib.load()
-    for rep in range(2):
+    best = 1e30
+    for rep in range(3):
         work[0].copy_(buf0)
         torch.cuda.synchronize()
         lib.dmqr_stats_enable(1)
@@ -29,12 +30,16 @@ def main():
         f = rrqr.factorize(None, work=work)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        st = _lib.stats(reset=True)
+        if dt < best:
+            best, st = dt, _lib.stats(reset=True)
+        else:
+            _lib.stats(reset=True)
         lib.dmqr_stats_enable(0)
     flops = 2.0 * m * nn * nn - 2.0 * nn ** 3 / 3.0 if m >= nn else 2.0 * nn * m * m - 2.0 * m ** 3 / 3.0
-    print(f"{name} {m}x{nn}: {dt * 1e3:.1f} ms, {flops / dt / 1e9:.0f} GFLOP/s, rank {int(f.info.rank)}, "
+    dt = best
+    print(f"{name} {m}x{nn}: {dt * 1e3:.1f} ms (best of 3), {flops / dt / 1e9:.0f} GFLOP/s, rank {int(f.info.rank)}, "
           f"steps {int(f.info.n_steps)}, phases " + ", ".join(f"{k} {st[k]:.1f}" for k in
-                                                              ("ms_select", "ms_panel", "ms_trailing", "ms_norms")))
+                                                              ("ms_select", "ms_panel", "ms_trailing", "ms_norms", "ms_pivot")))
 
 
 if __name__ == "__main__":
