@@ -195,7 +195,7 @@ int dmqr_debug_ctl(const void* workspace, int64_t* out, void* stream);
  * when dmqr_stats_enable(2) was set; out = 64 x 8 int64 on the host. */
 int dmqr_debug_panel_clocks(const void* workspace, int64_t m, int64_t n, int64_t* out);
 /* debug: kernel spans per step of the last factorization run with
- * DMQR_TIMELINE set (out[64 * 32] int64, globaltimer ns; see the source) */
+ * DMQR_TIMELINE set (out[64 * 32 + 1024] int64, globaltimer ns; see the source) */
 int dmqr_debug_timeline(int64_t* out);
 
 /* Build identification (compile arch, version) for logs and the loader check. */

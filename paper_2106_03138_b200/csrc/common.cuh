@@ -117,7 +117,7 @@ struct __align__(16) HostRec {
 
 // debug timeline (DMQR_TIMELINE): per step and kernel, the first CTA's start
 // (after its dependency wait) and the last CTA's exit, globaltimer ns
-__device__ unsigned long long g_tl[64 * 32];
+__device__ unsigned long long g_tl[64 * 32 + 1024];  // + k_spare per-CTA debug of step 20
 __constant__ int g_tl_on;
 struct TLSpan {
   int slot;

@@ -196,6 +196,24 @@ struct ProfAcc {
 ProfAcc g_acc;  // guarded by the caller (bench) using one thread
 #define NOTE_LAUNCH() g_launches.fetch_add(1, std::memory_order_relaxed)
 
+// Split-K count for `ntile` column tiles on `slots` concurrent CTAs: the
+// number of splits (1..maxsplit) whose item count fills its waves best
+// (items / (waves x slots)); ties go to fewer splits (less partial traffic).
+int choose_nsplit(int64_t ntile, int slots, int maxsplit) {
+  int best = 1;
+  double best_eff = -1.0;
+  for (int sp = 1; sp <= std::max(1, maxsplit); ++sp) {
+    const int64_t items = ntile * sp;
+    const int64_t waves = (items + slots - 1) / slots;
+    const double eff = (double)items / (double)(waves * slots);
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = sp;
+    }
+  }
+  return best;
+}
+
 // Launch with programmatic stream serialization: the kernel may be scheduled
 // while its predecessor runs (it waits in pdl_enter before touching memory).
 template <typename... KArgs, typename... Args>
@@ -367,8 +385,8 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   {
     const int on = tline ? 1 : 0;
     if (tline) {
-      static unsigned long long init[64 * 32];
-      for (int q = 0; q < 64 * 32; ++q) init[q] = (q & 1) ? 0ull : ~0ull;
+      static unsigned long long init[64 * 32 + 1024];
+      for (int q = 0; q < 64 * 32 + 1024; ++q) init[q] = (q >= 64 * 32 || (q & 1)) ? 0ull : ~0ull;
       CK(cudaMemcpyToSymbolAsync(g_tl, init, sizeof(init), 0, cudaMemcpyHostToDevice, st));
     }
     CK(cudaMemcpyToSymbolAsync(g_tl_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
@@ -495,8 +513,11 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     const int Pcq = (int)std::min<int64_t>(Prr, max_cluster);
     const bool spare = la && cq_path;  // k_spare beside the panel, then k_trail_w
     const int64_t ntile_g = std::max<int64_t>(1, ceil_div(np, TA_COLS));
-    const int nsplit_g = (int)std::min<int64_t>(
-        std::clamp<int64_t>(ceil_div(2 * (d.sms - Pcq), ntile_g), 1, NSPLIT_MAX), std::max<int64_t>(1, ceil_div(mp, 256)));
+    // G = Q1^T C split-K items over the spare CTAs: as many splits as keep the
+    // items within whole waves of the CTAs (a CTA with one item more than the
+    // rest sets the phase's length)
+    const int nsplit_g = choose_nsplit(ntile_g, 2 * std::max(1, d.sms - Pcq),
+                                       (int)std::min<int64_t>(NSPLIT_MAX, std::max<int64_t>(1, ceil_div(mp, 256))));
     if (la_rest && !cq_path) CK(launch_la_rest(false));
     if (cq_path) {
       pa.spare = spare ? 1 : 0;
@@ -548,8 +569,8 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     const int64_t ncols_ub = std::max<int64_t>(np - 1, 0);
     if (ncols_ub > 0) {
       const int64_t ntile = ceil_div(ncols_ub, TA_COLS);
-      int nsplit = (int)std::clamp<int64_t>(ceil_div(2 * d.sms, ntile), 1, NSPLIT_MAX);
-      nsplit = (int)std::min<int64_t>(nsplit, std::max<int64_t>(1, ceil_div(mp, 256)));
+      const int nsplit = choose_nsplit(ntile, 2 * d.sms,
+                                       (int)std::min<int64_t>(NSPLIT_MAX, std::max<int64_t>(1, ceil_div(mp, 256))));
       if (spare) {
         CK(pdl_launch(k_trail_w, dim3((unsigned)ceil_div(ncols_ub, TW_COLS)), dim3(TA_T), TW_SMEM, st, ctl, A,
                       (const double*)Zp, (const double*)(red + 19 * DMQR_KP * DMQR_KP), Z, ldz, u, uref, upd,
@@ -964,7 +985,7 @@ int dmqr_debug_panel_clocks(const void* workspace, int64_t m, int64_t n, int64_t
  * DMQR_TIMELINE set: out[64 * 32], step s, kernel k -> [32 s + 2 k] first
  * start, [32 s + 2 k + 1] last exit (globaltimer ns) */
 int dmqr_debug_timeline(int64_t* out) {
-  CK(cudaMemcpyFromSymbol(out, g_tl, sizeof(unsigned long long) * 64 * 32));
+  CK(cudaMemcpyFromSymbol(out, g_tl, sizeof(unsigned long long) * (64 * 32 + 1024)));
   return 0;
 }
 

@@ -603,6 +603,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
     if (tid == 0) {
       __threadfence();
       s_flag = (atomicAdd(&ctr[1], 1u) == (unsigned)ntb - 1);
+      if (g_tl_on) atomicMax(&g_tl[(S.step_idx & 63) * 32 + 29], (unsigned long long)gtimer());  // phase 1 end
     }
     __syncthreads();
     if (s_flag) {  // every tile has read the flags
@@ -616,6 +617,8 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
       while (ld_acquire(&ctr[1]) < (unsigned)ntb) __nanosleep(200);
       while (ld_acquire(&c->q1_count) < (unsigned)P) __nanosleep(200);
       s_flag = !c->q1_fail;
+      if (g_tl_on) atomicMin(&g_tl[(S.step_idx & 63) * 32 + 28], (unsigned long long)gtimer());  // Q1 seen
+      if (g_tl_on && S.step_idx == 20 && blockIdx.x < 256) g_tl[2048 + blockIdx.x * 4 + 0] = gtimer();
     }
     __syncthreads();
     if (s_flag) {
@@ -645,7 +648,15 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
           __syncthreads();
           continue;
         }
-        if (it >= ng) break;
+        if (it >= ng) {
+          if (tid == 0 && g_tl_on) atomicMax(&g_tl[(S.step_idx & 63) * 32 + 31], (unsigned long long)gtimer());
+          if (tid == 0 && g_tl_on && S.step_idx == 20 && blockIdx.x < 256) g_tl[2048 + blockIdx.x * 4 + 2] = gtimer();
+          break;
+        }
+        if (tid == 0 && g_tl_on && S.step_idx == 20 && blockIdx.x < 256) {
+          if (g_tl[2048 + blockIdx.x * 4 + 1] == 0) g_tl[2048 + blockIdx.x * 4 + 1] = gtimer();
+          g_tl[2048 + blockIdx.x * 4 + 3] += 1;
+        }
         const int tile = it % ntile;
         g_partial(A, Q1g, Gp, ldz, n_s, m, lda, kk, ncols, (int64_t)tile * TA_COLS, it / ntile, nsplit_g);
         __syncthreads();

@@ -34,9 +34,9 @@ for i, r in enumerate(g[:12]):
 
 # ---- kernel spans (dmqr_debug_timeline): start after the dependency wait, end at the last CTA exit
 names = ["select", "gram", "gfinish", "swap", "panel", "spare", "ygemm", "trail_w", "trail_a", "guard", "step_end"]
-tl = np.zeros(64 * 32, dtype=np.int64)
+tl = np.zeros(64 * 32 + 1024, dtype=np.int64)  # (the last 1024: k_spare per-CTA debug)
 _lib.load().dmqr_debug_timeline(tl.ctypes.data_as(C.c_void_p))
-tl = tl.reshape(64, 32)
+tl = tl[:2048].reshape(64, 32)
 ns = int(f.info.n_steps)
 U64MAX = np.int64(-1)
 rows = []
