@@ -235,8 +235,13 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
       cp_async_wait<0>();
     }
     __syncthreads();
-    fix(sl);
-    __syncthreads();
+    {  // Y structure / rows outside [rb, re): only the first and boundary slabs (uniform branch)
+      const int64_t r0 = rb - odd + (int64_t)sl * TA_ROWS;
+      if (!(r0 >= 72 && r0 >= rb && r0 + TA_ROWS <= re)) {
+        fix(sl);
+        __syncthreads();
+      }
+    }
     const double* ys = ysb[sl & 1];
     const double* cs = csb[sl & 1];
 #pragma unroll
@@ -541,8 +546,13 @@ __device__ void g_partial(const double* __restrict__ A, const double* __restrict
       cp_async_wait<0>();
     }
     __syncthreads();
-    fix(sl);
-    __syncthreads();
+    {  // rows outside [rb, re): only the boundary slabs (uniform branch, no extra barrier otherwise)
+      const int64_t r0 = rb - odd + (int64_t)sl * TA_ROWS;
+      if (!(r0 >= rb && r0 + TA_ROWS <= re)) {
+        fix(sl);
+        __syncthreads();
+      }
+    }
     const double* ys = ysb[sl & 1];
     const double* cs = csb[sl & 1];
 #pragma unroll

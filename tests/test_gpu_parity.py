@@ -370,3 +370,58 @@ def test_cfg5_full_size_properties(algo):
     resid, orth = _device_residuals(A, res)
     bound = 50 * n * O.EPS
     assert resid <= bound and orth <= bound, (resid, orth)
+
+
+# ----------------------------------------------------------------------------
+# rank-revealing quality (acceptance criterion 2, test_acceptance.py:108-132):
+# |d_i| / sigma_i within [1e-1, 1e1] over the numerical rank -- on the fixture
+# suite (sigma by LAPACK) and, beyond the reference's 512-column SVD cap, on
+# device-built matrices of known spectrum
+# ----------------------------------------------------------------------------
+
+def test_criterion2_factor10_ratios_fixture_suite():
+    import fixture_suite
+    from paper_2106_03138_b200 import DMParams, StopCriterion, StopRule, qrdm2
+    from paper_2106_03138_b200.diagnostics import ratio_fields
+
+    bad = []
+    for name, A in fixture_suite.suite():
+        s = np.linalg.svd(A, compute_uv=False)
+        nr = int(np.count_nonzero(s > max(A.shape) * O.EPS * (s[0] if s.size else 0.0)))
+        if nr == 0:
+            continue
+        res = qrdm2(A, params=DMParams(), stop=StopCriterion(StopRule.NONE))
+        d_lo, d_hi, s_lo, s_hi, flags = ratio_fields(res, s, nr)
+        if d_lo < 1e-1 or d_hi > 1e1:
+            bad.append((name, d_lo, d_hi))
+        assert s_hi <= 1.0 + 1e-8  # interlacing: sigma_i(R11) <= sigma_i(A)
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("n", [2048, 4096])
+def test_factor10_ratios_known_spectrum_beyond_cpu_cap(n):
+    """cfg1's recipe scaled up on the device: A = U diag(sigma) V^T, Haar U, V,
+    sigma_i = 10^(-4 (i-1)/(r-1)) for i <= r = 3n/4, 1e-18 after: qrdm2 must
+    reveal rank r (up to round-off-level columns) with |d_i| / sigma_i within
+    [1e-1, 1e1] over the first r."""
+    import torch
+    from paper_2106_03138_b200 import qrdm2
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n)
+
+    def haar(k):
+        q, r = torch.linalg.qr(torch.randn(k, k, generator=g, dtype=torch.float64, device="cuda"))
+        return q * torch.sign(torch.diagonal(r))
+
+    r = 3 * n // 4
+    sig = torch.full((n,), 1e-18, dtype=torch.float64, device="cuda")
+    sig[:r] = 10.0 ** (-4.0 * torch.arange(r, dtype=torch.float64, device="cuda") / (r - 1))
+    A = (haar(n) * sig) @ haar(n).T
+    res = qrdm2(A, device=True)
+    # the 1e-18 tail sits below the product's own round-off (~eps ||A||), so the
+    # stop rule may keep a few noise-level columns past r
+    assert r <= res.rank <= r + n // 256, (res.rank, r)
+    d = torch.sort(torch.abs(torch.diagonal(res.packed)[:r]), descending=True).values
+    ratios = (d / sig[:r]).cpu().numpy()
+    assert ratios.min() >= 1e-1 and ratios.max() <= 1e1, (ratios.min(), ratios.max())

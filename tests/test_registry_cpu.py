@@ -29,3 +29,17 @@ def test_register_into_reference_style_registry():
     # qrp_b200 accepts (and ignores) the params= keyword the reference passes to non-"qrp" names
     import inspect
     assert "params" in inspect.signature(ref["qrp_b200"]).parameters
+
+
+def test_ratio_fields_identity_like_reference():
+    """harness.py TestCompareRun.test_identity_all_algorithms: all ratios 1 on eye(8)."""
+    import numpy as np
+    from types import SimpleNamespace
+
+    from paper_2106_03138_b200.diagnostics import ratio_fields
+
+    res = SimpleNamespace(packed=np.eye(8), n_factored=8)
+    out = ratio_fields(res, np.ones(8), 8)
+    assert all(abs(v - 1.0) <= 1e-12 for v in out[:4]) and out[4] == ""
+    short = ratio_fields(SimpleNamespace(packed=np.eye(8), n_factored=5), np.ones(8), 8)
+    assert short[4] == "short_factorization"
