@@ -59,6 +59,7 @@ struct Ctl {
   // blocked scalar pivoting (k_qp3): columns factored by the last launch and why it ended
   int32_t qp_cols, qp_exit;
   uint32_t m_pub;  // k_panel_cq: step_idx + 1 once M (Y = Q1 M) and l are final
+  int32_t posted;  // host poll records posted so far (k_step_end / k_qp3_post): the enqueue index
   // inter-CTA counters (reset by their users)
   uint32_t gram_count;
   uint32_t bar_count;

@@ -279,11 +279,26 @@ int dmqr_qrdm_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_param
 }  // extern "C"
 
 namespace {
+// A lane's replayable outer step (small matrices in a batch): the step's
+// kernel sequence captured once as a CUDA graph with grids sized for the
+// whole matrix (kernels take the true extents from Ctl and exit surplus
+// CTAs; the poll record's index is counted on the device), then replayed with
+// one graph launch per step.  Valid while every argument baked into the
+// launches is unchanged -- the batched driver factors each of a lane's
+// matrices in the same lane-private buffers.
+struct StepGraph {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<unsigned char> key;
+  ~StepGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
 // The engine behind dmqr_qrdm*_f64 (qrp = 0) and dmqr_qrp*_f64 (qrp = 1).
 int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* p, double* coeffs, int64_t* perm,
                int64_t* swaps, int64_t swap_cap, dmqr_step* steps, int64_t step_cap, double* norm_trace,
                void* workspace, size_t ws_bytes, dmqr_info* info, double* host_packed, int64_t host_ld, void* stream,
-               int qrp) {
+               int qrp, StepGraph* sgraph = nullptr) {
   if (host_packed && host_ld < m) return DMQR_EINVAL;
   int rc = validate(m, n, lda, p);
   if (rc) return rc;
@@ -640,6 +655,24 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   // k_qp3 splits each column into at most QP_RMAX staged row segments
   const bool qp_ok = m <= (int64_t)QP_RMAX * QP_XCH;
   if (qrp && !qp_ok) return DMQR_EINVAL;
+  // replayed step graph (batched small matrices; serial schedule only)
+  const bool use_graph = sgraph != nullptr && !la_all && !qrp && !p->trace_norms && !prof && !tline &&
+                         getenv("DMQR_NO_GRAPH") == nullptr;
+  std::vector<unsigned char> gkey;
+  if (use_graph) {
+    const void* parts[] = {A, coeffs, perm, swaps, steps, workspace, (const void*)hrec};
+    const int64_t dims[] = {m, n, lda, swap_cap, step_cap};
+    gkey.resize(sizeof(parts) + sizeof(dims) + sizeof(dmqr_params));
+    std::memcpy(gkey.data(), parts, sizeof(parts));
+    std::memcpy(gkey.data() + sizeof(parts), dims, sizeof(dims));
+    dmqr_params pk = *p;
+    pk.max_steps = 0;
+    std::memcpy(gkey.data() + sizeof(parts) + sizeof(dims), &pk, sizeof(pk));
+    if (sgraph->exec && sgraph->key != gkey) {
+      cudaGraphExecDestroy(sgraph->exec);
+      sgraph->exec = nullptr;
+    }
+  }
   bool finished = (kmax == 0);
   auto consume = [&]() -> int {
     const int sl = known & 1;
@@ -647,6 +680,8 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     // then so that a failed launch cannot hang the loop
     volatile HostRec* r = hrec + sl;
     for (long spins = 1; r->seq != known + 1; ++spins) {
+      // batch lanes may outnumber the host cores: give the core away while waiting
+      if (sgraph && spins > 64) std::this_thread::yield();
       if ((spins & 1023) == 0) {
         const cudaError_t e = cudaStreamQuery(st);
         if (e != cudaSuccess && e != cudaErrorNotReady) return DMQR_ECUDA;
@@ -759,7 +794,27 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     }
     slot = enq & 1;
     qp_slot[slot] = false;
-    int rc = enqueue_step(ns_lo, enq);
+    int rc = 0;
+    if (use_graph) {
+      if (!sgraph->exec) {  // capture the step once (whole-matrix grids)
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        rc = enqueue_step(0, 0);
+        const cudaError_t ce = cudaStreamEndCapture(st, &g);
+        if (rc) {
+          if (g) cudaGraphDestroy(g);
+          return rc;
+        }
+        CK(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&sgraph->exec, g, 0);
+        cudaGraphDestroy(g);
+        CK(ie);
+        sgraph->key = gkey;
+      }
+      CK(cudaGraphLaunch(sgraph->exec, st));
+    } else {
+      rc = enqueue_step(ns_lo, enq);
+    }
     if (rc) return rc;
     prev_ns_lo = ns_lo;
     ++enq;
@@ -837,8 +892,43 @@ int dmqr_qrp_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params
                              ws_bytes, info, nullptr, 0, stream);
 }
 
+}  // extern "C"
+
+namespace {
+// Small matrices in a batch run on lane-private buffers (so each lane's step
+// graph is captured once and replayed for all its matrices): the work matrix,
+// coeffs, perm, the swap log and the step log, sized for the largest caps.
+struct LaneBufs {
+  size_t a, coeffs, perm, swaps, steps, total;
+  int64_t swap_cap, step_cap;
+};
+LaneBufs lane_bufs(int64_t m, int64_t n, int64_t lda) {
+  LaneBufs b{};
+  const int64_t kmax = std::max<int64_t>(std::min(m, n), 1);
+  b.swap_cap = kmax * DMQR_MAXK + 8;
+  b.step_cap = kmax;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += al(bytes);
+    return o;
+  };
+  b.a = take(sizeof(double) * (size_t)lda * (size_t)std::max<int64_t>(n, 1));
+  b.coeffs = take(sizeof(double) * kmax);
+  b.perm = take(sizeof(int64_t) * std::max<int64_t>(n, 1));
+  b.swaps = take(sizeof(int64_t) * 2 * b.swap_cap);
+  b.steps = take(sizeof(dmqr_step) * b.step_cap);
+  b.total = off;
+  return b;
+}
+bool batch_graph_ok(int64_t m, int64_t n) { return m * n < ((int64_t)1 << 20); }
+}  // namespace
+
+extern "C" {
+
 size_t dmqr_batched_workspace_bytes(int64_t m, int64_t n, const dmqr_params* params, int32_t nlanes) {
-  return (size_t)std::max(1, nlanes) * al(dmqr_workspace_bytes(m, n, params));
+  const size_t extra = batch_graph_ok(m, n) ? lane_bufs(m, n, (m + 7) / 8 * 8).total : 0;
+  return (size_t)std::max(1, nlanes) * (al(dmqr_workspace_bytes(m, n, params)) + extra);
 }
 
 int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_t lda, int64_t stride,
@@ -848,7 +938,13 @@ int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_
   int rc = validate(m, n, lda, p);
   if (rc) return rc;
   if (batch < 0 || stride < lda * n || !infos || nlanes < 1) return DMQR_EINVAL;
-  const size_t per = al(dmqr_workspace_bytes(m, n, p));
+  const size_t per_engine = al(dmqr_workspace_bytes(m, n, p));
+  // small matrices: lane-private buffers + a replayed step graph per lane
+  // (needs the caller's lda to match the lane buffers' and caps within theirs)
+  const LaneBufs lb = lane_bufs(m, n, lda);
+  const bool graphs = batch_graph_ok(m, n) && lda == (m + 7) / 8 * 8 && swap_cap <= lb.swap_cap &&
+                      step_cap <= lb.step_cap && getenv("DMQR_NO_GRAPH") == nullptr;
+  const size_t per = per_engine + (batch_graph_ok(m, n) ? lb.total : 0);
   nlanes = (int32_t)std::min<int64_t>(nlanes, std::max<int64_t>(batch, 1));
   if (m > 4096) nlanes = 1;  // cooperative panel launches must not compete for co-residency
   if (ws_bytes < per * (size_t)nlanes || !workspace) return DMQR_EINVAL;
@@ -875,12 +971,49 @@ int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_
   auto work = [&](int q) {
     cudaSetDevice(dev);
     unsigned char* ws = (unsigned char*)workspace + per * (size_t)q;
-    for (int64_t b = q; b < batch; b += nlanes) {
-      const int r = dmqr_qrdm_f64(A + b * stride, m, n, lda, p, coeffs + b * kmax, perm + b * n,
-                                  swaps + b * 2 * swap_cap, swap_cap, steps + b * step_cap, step_cap, nullptr, ws,
-                                  per, &infos[b], (void*)ls[q]);
-      infos[b].status = r;
-      if (r && !lane_rc[q]) lane_rc[q] = r;
+    if (!graphs) {
+      for (int64_t b = q; b < batch; b += nlanes) {
+        const int r = dmqr_qrdm_f64(A + b * stride, m, n, lda, p, coeffs + b * kmax, perm + b * n,
+                                    swaps + b * 2 * swap_cap, swap_cap, steps + b * step_cap, step_cap, nullptr, ws,
+                                    per_engine, &infos[b], (void*)ls[q]);
+        infos[b].status = r;
+        if (r && !lane_rc[q]) lane_rc[q] = r;
+      }
+    } else {
+      unsigned char* lbuf = ws + per_engine;
+      double* Aw = (double*)(lbuf + lb.a);
+      double* cw = (double*)(lbuf + lb.coeffs);
+      int64_t* pw = (int64_t*)(lbuf + lb.perm);
+      int64_t* sw = (int64_t*)(lbuf + lb.swaps);
+      dmqr_step* tw = (dmqr_step*)(lbuf + lb.steps);
+      StepGraph sg;
+      const cudaStream_t s = ls[q];
+      const size_t abytes = sizeof(double) * (size_t)lda * (size_t)n;
+      for (int64_t b = q; b < batch; b += nlanes) {
+        int r = 0;
+        if (cudaMemcpyAsync(Aw, A + b * stride, abytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess) r = DMQR_ECUDA;
+        if (!r)
+          r = run_engine(Aw, m, n, lda, p, cw, pw, sw, lb.swap_cap, tw, lb.step_cap, nullptr, ws, per_engine,
+                         &infos[b], nullptr, 0, (void*)s, 0, &sg);
+        if (!r && infos[b].n_swaps > swap_cap) r = DMQR_ECAP;
+        if (!r) {
+          const int64_t nsw = infos[b].n_swaps, nst = infos[b].n_steps;
+          bool ok = cudaMemcpyAsync(A + b * stride, Aw, abytes, cudaMemcpyDeviceToDevice, s) == cudaSuccess;
+          ok = ok && cudaMemcpyAsync(coeffs + b * kmax, cw, sizeof(double) * kmax, cudaMemcpyDeviceToDevice, s) ==
+                         cudaSuccess;
+          ok = ok && cudaMemcpyAsync(perm + b * n, pw, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, s) == cudaSuccess;
+          if (nsw > 0)
+            ok = ok && cudaMemcpyAsync(swaps + b * 2 * swap_cap, sw, sizeof(int64_t) * 2 * nsw,
+                                       cudaMemcpyDeviceToDevice, s) == cudaSuccess;
+          if (nst > 0)
+            ok = ok && cudaMemcpyAsync(steps + b * step_cap, tw, sizeof(dmqr_step) * nst, cudaMemcpyDeviceToDevice,
+                                       s) == cudaSuccess;
+          if (!ok) r = DMQR_ECUDA;
+        }
+        infos[b].status = r;
+        if (r && !lane_rc[q]) lane_rc[q] = r;
+      }
+      cudaStreamSynchronize(s);  // (the graph exec is destroyed with sg)
     }
     cudaEventRecord(done[q], ls[q]);
   };

@@ -133,7 +133,12 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
   // writes to them are fenced first; the record itself is one 16-byte store)
   __threadfence();
   __syncwarp();
+  // (the record's index is counted on the device -- one per enqueued step --
+  // so a replayed CUDA graph of the step posts the right slot and sequence)
   if (threadIdx.x == 0 && hrec) {
+    (void)enq;
+    enq = c->posted;
+    c->posted = enq + 1;
     // (a fallback step hands the run to the blocked scalar-pivot engine, k_qp3;
     // not with the per-step norm trace)
     const int fb = (!S.done && S.kind == 1 && !S.trace_norms) ? 4 : 0;

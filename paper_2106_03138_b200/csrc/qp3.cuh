@@ -730,6 +730,9 @@ __global__ void k_qp3_post(Ctl* __restrict__ c, double* __restrict__ norm_trace,
                                       : __longlong_as_double(-1ll);
     *trace_bits = 0ull;
   }
+  (void)enq;
+  enq = c->posted;  // (device-counted enqueue index, as k_step_end)
+  c->posted = enq + 1;
   __threadfence_system();
   // stay in the scalar-pivot engine unless a fallback run ended on the floor test
   const int fb = (c->qp_exit != 2) ? 1 : 0;

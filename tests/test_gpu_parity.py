@@ -233,9 +233,9 @@ def test_midsize_golden(name):
 
 
 def test_batched_equals_single_and_oracle():
-    """cfg3-style batch through dmqr_qrdm_batched_f64 (concurrent lanes): each matrix
-    must equal its single-matrix factorization bit for bit (same device engine) and
-    the oracle on the robust prefix."""
+    """cfg3-style batch through dmqr_qrdm_batched_f64 (concurrent lanes, replayed
+    step graphs): each matrix takes the single-matrix factorization's decisions,
+    equal factors to rounding, and matches the oracle on the robust prefix."""
     from paper_2106_03138_b200 import inputs, qrdm2
     from paper_2106_03138_b200.batch import factorize_batch
 
@@ -245,7 +245,13 @@ def test_batched_equals_single_and_oracle():
         r = f.result(i)
         s = qrdm2(B[i])
         assert np.array_equal(r.perm.forward, s.perm.forward) and r.rank == s.rank
-        assert np.array_equal(r.packed, s.packed) and np.array_equal(r.coeffs, s.coeffs)
+        assert [(a.n_s, a.k_selected, a.k_accepted) for a in r.step_log] == \
+            [(a.n_s, a.k_selected, a.k_accepted) for a in s.step_log]
+        # the batch replays a whole-matrix step graph per lane (split-K counts
+        # sized for the full matrix), so sums may associate differently
+        scale = np.abs(s.packed).max()
+        assert np.abs(r.packed - s.packed).max() <= 1e-12 * scale
+        assert np.allclose(r.coeffs, s.coeffs, rtol=1e-12, atol=1e-14)
         with threadpool_limits(1):
             ref = O.qrdm2(B[i], margins=True)
         _compare(B[i], r, ref, f"cfg3[{i}]")
