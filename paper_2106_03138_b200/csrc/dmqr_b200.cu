@@ -407,6 +407,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     CK(cudaMemcpyToSymbolAsync(g_tl_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
   }
   const bool trail_persistent = getenv("DMQR_TRAIL_PERSISTENT") != nullptr;  // A/B switch
+  const bool spare_all = getenv("DMQR_SPARE_FREE_ONLY") == nullptr;          // A/B switch
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
 
   int64_t prev_ns_lo = 0;  // the lower bound the previous step was sized with
@@ -542,9 +543,12 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
       pa.spare = 0;
       if (spare) {
         cudaLaunchConfig_t cfg = {};
-        // persistent CTAs: two per SM the panel leaves free, but no more than work items
+        // persistent CTAs: two per SM the panel leaves free, plus two per panel SM
+        // that start once the panel is done (they pull what is left); no more than
+        // work items
         const int64_t items = (int64_t)lag.x * lag.y * (la_rest ? 1 : 0) + ntile_g * nsplit_g;
-        cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(2 * std::max(1, d.sms - Pcq), items)));
+        const int sp_sms = spare_all ? d.sms : std::max(1, d.sms - Pcq);
+        cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(2 * sp_sms, items)));
         cfg.blockDim = dim3(TB_T);
         cfg.dynamicSmemBytes = SP_SMEM;
         cfg.stream = st;
