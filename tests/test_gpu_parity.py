@@ -431,3 +431,28 @@ def test_factor10_ratios_known_spectrum_beyond_cpu_cap(n):
     d = torch.sort(torch.abs(torch.diagonal(res.packed)[:r]), descending=True).values
     ratios = (d / sig[:r]).cpu().numpy()
     assert ratios.min() >= 1e-1 and ratios.max() <= 1e1, (ratios.min(), ratios.max())
+
+
+def test_batched_graph_lanes_with_fallback_runs():
+    """Batched lanes (replayed step graphs) on inputs whose factorization falls
+    back to scalar pivoting (the blocked scalar-pivot engine runs between graph
+    replays): same decisions as the single-matrix calls, oracle on the robust prefix."""
+    from paper_2106_03138_b200 import DMParams, StopCriterion, StopRule, qrdm2
+    from paper_2106_03138_b200.batch import factorize_batch
+
+    rng = np.random.default_rng(36)
+    B = np.stack([rng.standard_normal((48, 5)) @ rng.standard_normal((5, 40)) * (1 + i) for i in range(8)])
+    none = StopCriterion(StopRule.NONE)  # past the rank the norms sit under the floor: scalar-pivot runs
+    f = factorize_batch(B, DMParams(), none, True, lanes=3)
+    saw_fallback = False
+    for i in range(B.shape[0]):
+        r = f.result(i)
+        s = qrdm2(B[i], stop=none)
+        saw_fallback |= any(st.fell_back_to_scalar for st in s.step_log)
+        assert np.array_equal(r.perm.forward, s.perm.forward) and r.rank == s.rank
+        assert [(a.n_s, a.k_selected, a.k_accepted, a.fell_back_to_scalar) for a in r.step_log] == \
+            [(a.n_s, a.k_selected, a.k_accepted, a.fell_back_to_scalar) for a in s.step_log]
+        with threadpool_limits(1):
+            ref = O.qrdm2(B[i], margins=True, stop_rule="none")
+        _compare(B[i], r, ref, f"batch-fallback[{i}]")
+    assert saw_fallback
