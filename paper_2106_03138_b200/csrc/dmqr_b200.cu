@@ -43,7 +43,7 @@ constexpr int PANEL_PMAX = 160;
 
 struct Layout {
   size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, trace, pdbg, tcount, upd, lacount, q1g, glist;
-  size_t qvb, qwb, qpart, qgpart, qcnt, total;
+  size_t qvb, qwb, qpart, qgpart, qcnt, hpart, hR, hctr, total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -83,6 +83,10 @@ Layout layout(int64_t m, int64_t n) {
   L.qpart = take(sizeof(double) * QP_GMAXCTA * QP_PLD);
   L.qgpart = take(sizeof(double) * (QP_GMAXCTA * QP_GMAX * 2 + QP_GMAX));  // + the fresh guard norms
   L.qcnt = take(sizeof(unsigned) * 4);
+  // tall-panel helpers (k_panel_helper): per-256-row-chunk Gram partials, R1^-1, counters
+  L.hpart = take(sizeof(double) * DMQR_KP * DMQR_KP * (size_t)std::max<int64_t>(1, (m + 255) / 256));
+  L.hR = take(sizeof(double) * (DMQR_KP * DMQR_KP + 2));
+  L.hctr = take(sizeof(unsigned) * 8);
   L.total = off;
   return L;
 }
@@ -139,6 +143,7 @@ int set_attrs(const DevInfo& d) {
   CK(cudaFuncSetAttribute(k_ygemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YG_SMEM));
   CK(cudaFuncSetAttribute(k_trail_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TP_SMEM));
   CK(cudaFuncSetAttribute(k_qp3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QP_SMEM));
+  CK(cudaFuncSetAttribute(k_panel_helper, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CQH_SMEM));
   CK(cudaFuncSetAttribute(k_fq_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FQ_SMEM2));
   CK(cudaFuncSetAttribute(k_fq_tw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FQ_SMEM2));
   CK(cudaFuncSetAttribute(k_fq_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FQ_SMEM2));
@@ -408,6 +413,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   }
   const bool trail_persistent = getenv("DMQR_TRAIL_PERSISTENT") != nullptr;  // A/B switch
   const bool spare_all = getenv("DMQR_SPARE_FREE_ONLY") == nullptr;          // A/B switch
+  const bool no_helpers = getenv("DMQR_NO_HELPERS") != nullptr;               // A/B switch
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
 
   int64_t prev_ns_lo = 0;  // the lower bound the previous step was sized with
@@ -503,7 +509,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     const int G = cl_path ? P : ((P > 1) ? P + 1 : 1);
     PanelArgs pa{ctl, A, coeffs, T, red, use_smem, P,
                  (g_prof.load() >= 2 && steps_done == 2) ? pdbg : nullptr, std::max(0, g_prof.load() - 2), 0,
-                 q1g, 0, tline};
+                 q1g, 0, tline, 0, (double*)(ws + L.hpart), (double*)(ws + L.hR), (unsigned*)(ws + L.hctr)};
     void* kargs[] = {&pa};
     auto launch_cluster = [&](const void* fn, int ncta, unsigned threads, size_t dsm) -> cudaError_t {
       cudaLaunchConfig_t cfg = {};
@@ -535,12 +541,34 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     const int nsplit_g = choose_nsplit(ntile_g, 2 * std::max(1, d.sms - Pcq),
                                        (int)std::min<int64_t>(NSPLIT_MAX, std::max<int64_t>(1, ceil_div(mp, 256))));
     if (la_rest && !cq_path) CK(launch_la_rest(false));
+    // tall CholeskyQR2 panel, serial schedule: its row passes go to the free SMs
+    const bool helpers = cq_path && !spare && mp > (int64_t)Pcq * CQ_RMAX && d.sms - Pcq >= 16 && !no_helpers;
     if (cq_path) {
       pa.spare = spare ? 1 : 0;
+      pa.helpers = helpers ? 1 : 0;
+      if (helpers) {
+        CK(pdl_launch(k_hzero, dim3(1), dim3(32), 0, st, (unsigned*)(ws + L.hctr)));
+        NOTE_LAUNCH();
+      }
       CK(launch_cluster((const void*)k_panel_cq, Pcq, PANEL_T, CQ_SMEM));
       NOTE_LAUNCH();
+      if (helpers) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)std::min<int64_t>(d.sms - Pcq, ceil_div(mp, CQ_RMAX)));
+        cfg.blockDim = dim3(PANEL_T);
+        cfg.dynamicSmemBytes = CQH_SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, k_panel_helper, pa));
+        NOTE_LAUNCH();
+      }
       pa.only_if_fail = 1;
       pa.spare = 0;
+      pa.helpers = 0;
       if (spare) {
         cudaLaunchConfig_t cfg = {};
         // persistent CTAs: two per SM the panel leaves free, plus two per panel SM

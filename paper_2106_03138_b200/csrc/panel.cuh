@@ -133,6 +133,13 @@ struct PanelArgs {
   double* q1g;       // CholeskyQR2 panel: Q1 buffer (chunked panels; read by k_spare under look-ahead)
   int spare;         // look-ahead: release k_spare, publish the Wt factors for k_trail_w
   long long* tline;  // debug timeline (globaltimer at panel end, per step), or null
+  // tall CholeskyQR2 panels (m' > cluster x 256 rows, serial schedule): the
+  // row passes (G1 = P^T P; Q1 = P R1^-1 and G2 = Q1^T Q1) run on the other SMs
+  // in k_panel_helper; the cluster sums their per-chunk partials
+  int helpers;
+  double* hpart;     // [chunks][KP x KP] per-chunk Gram partials (upper tiles)
+  double* hR;        // R1^-1 (KP x KP) + [kk, fail] published by rank 0
+  unsigned* hctr;    // [0] G1 items, [1] G1 done, [2] Q1 items, [3] Q1 done, [4] R1^-1 published (step + 1)
 };
 
 // deterministic all-reduce of `len` doubles across the grid; in: s_part (this

@@ -713,8 +713,46 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   };
   double* gacc = a.red + 3 * DMQR_KP * DMQR_KP + (size_t)blockIdx.x * DMQR_KP * DMQR_KP;  // per-CTA scratch
   double* vQ = a.red + 21 * DMQR_KP * DMQR_KP + (size_t)blockIdx.x * DMQR_KP * DMQR_KP;    // per-CTA scratch
+  // helper mode: uniform over the ranks (every rank's slice exceeds 256 rows)
+  const bool hmode = a.helpers && mp > (int64_t)nr * CQ_RMAX;
+  const int64_t hnch = ceil_div(mp, CQ_RMAX);  // helper chunks (256 panel rows each)
+  // publish R1^-1 (or a 'no pass 2' flag) for the helpers; rank 0, all threads
+  auto h_publish = [&](bool hfail, int hkk) {
+    if (me != 0) return;
+    if (!hfail)
+      for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) a.hR[e] = A1[e];
+    __syncthreads();
+    if (tid == 0) {
+      a.hR[DMQR_KP * DMQR_KP] = (double)hkk;
+      a.hR[DMQR_KP * DMQR_KP + 1] = hfail ? 1.0 : 0.0;
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.hctr + 4), "r"((unsigned)S.step_idx + 1u) : "memory");
+    }
+  };
+  // sum the helper partials of chunks me, me + nr, ... (upper tiles, fixed order) into G
+  auto h_gather = [&](unsigned want_idx, double* G) {
+    if (tid == 0) {
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.hctr + want_idx) : "memory");
+        if (v < (unsigned)hnch) __nanosleep(100);
+      } while (v < (unsigned)hnch);
+    }
+    __syncthreads();
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+      double g = 0.0;
+      if ((e % DMQR_KP) / 8 >= (e / DMQR_KP) / 8)
+        for (int64_t ch = me; ch < hnch; ch += nr) g += __ldcg(a.hpart + ch * DMQR_KP * DMQR_KP + e);
+      G[e] = g;
+    }
+    __syncthreads();
+  };
+  if (a.helpers && !hmode) h_publish(true, 0);  // (nothing for the helpers' second pass)
   // ---- P0/P1: slice <- P (rows zero-padded to a multiple of 4), G = P^T P ----
-  if (!chunked) {
+  if (hmode) {
+    CQT();
+    h_gather(1, A2);
+  } else if (!chunked) {
     load_chunk(gA, lda, 0, k);
     CQT();
     cq_gram(sl, R4, k, A2);
@@ -748,6 +786,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     if (!brk || jstar == 0 || !(bound < eps_s)) fail = true;
   }
   const bool q1_pub = a.spare && !fail && kk > 0;
+  if (hmode && (fail || kk == 0)) h_publish(true, 0);
   auto store_q1 = [&](int ch) {  // sl rows of chunk ch -> q1g (the row parity of A)
     const int c0r = ch * CQ_RMAX, cR = min(CQ_RMAX, R - c0r);
     if (trow < cR) {
@@ -769,7 +808,12 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       if (i == j) vD[i] = A2[i * DMQR_KP + i];
     }
     __syncthreads();
-    if (!chunked) {
+    if (hmode) {
+      // the helpers form Q1 = P R1^-1 into q1g and the per-chunk Q1 Grams
+      h_publish(false, kk);
+      h_gather(3, A1);
+      CQT();
+    } else if (!chunked) {
       cq_slice_gemm(sl, R4, kk, kk, A1);
       CQT();
       // publish this rank's Q1 rows: k_ygemm forms Y = Q1 M from them, and
@@ -950,7 +994,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     r2_inverse();
     CQT();
     // ---- P12: top l x l block of Q = Q1 R2^-1 -> A1 ----
-    if (!chunked)
+    if (!chunked && !hmode)
       cq_small_gemm<true>([&](int i, int t) { return sl[t * CQ_LDS + i]; },
                           [&](int t, int j) { return A2[t * DMQR_KP + j]; }, A1, l);
     else  // (rank 0's first rows, published)
@@ -1054,5 +1098,121 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   }
 }
 
+
+
+// The tall panel's row passes on the SMs the cluster leaves free (launched as
+// the panel's programmatic dependent, serial schedule only): per 256-row chunk
+// of P, pass 1 writes the Gram partial P_c^T P_c; once rank 0 publishes R1^-1,
+// pass 2 writes Q1_c = P_c R1^-1 into q1g and its Gram partial.  Chunks are
+// pulled from counters; the cluster sums the partials in fixed order.
+constexpr size_t CQH_SMEM = sizeof(double) * ((size_t)CQ_KC * CQ_LDS + 2 * DMQR_KP * DMQR_KP);
+
+__global__ void __launch_bounds__(PANEL_T, 1) k_panel_helper(PanelArgs a) {
+  Ctl* c = a.c;
+  const CtlSnap S = snap(c);
+  // (every exit waits for the panel grid: the kernels behind this one -- the
+  // Householder fallback panel, k_ygemm -- must see the panel's results)
+  if (S.done) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
+  extern __shared__ __align__(16) double hsm[];
+  double* sl = hsm;
+  double* G = sl + CQ_KC * CQ_LDS;
+  double* Rs = G + DMQR_KP * DMQR_KP;
+  __shared__ int s_item;
+  __shared__ double s_hdr[2];
+  const int tid = threadIdx.x;
+  const int64_t n_s = S.n_s, m = S.m, lda = S.lda, mp = m - n_s;
+  const int k = S.k_s;
+  const int64_t nch = ceil_div(mp, CQ_RMAX);
+  const double* gA = a.A + n_s * lda + n_s;
+  const int64_t ldq = q1_ld(m);
+  const int qodd = (int)(n_s & 1);
+  const int trow = tid & (CQ_RMAX - 1), tcol0 = tid / CQ_RMAX, tcstep = PANEL_T / CQ_RMAX;
+  auto load = [&](int64_t ch, int ncol) {
+    const int64_t c0r = ch * CQ_RMAX;
+    const int cR = (int)min((int64_t)CQ_RMAX, mp - c0r), cR4 = (cR + 3) & ~3;
+    if (trow < cR4) {
+      const double* sp = gA + c0r + trow;
+#pragma unroll 4
+      for (int cc = tcol0; cc < ncol; cc += tcstep) sl[cc * CQ_LDS + trow] = (trow < cR) ? sp[(int64_t)cc * lda] : 0.0;
+    }
+    __syncthreads();
+    return cR4;
+  };
+  auto put = [&](int64_t ch) {
+    for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) a.hpart[ch * DMQR_KP * DMQR_KP + e] = G[e];
+    __syncthreads();
+  };
+  auto next = [&](int idx) {
+    if (tid == 0) s_item = (int)atomicAdd(a.hctr + idx, 1u);
+    __syncthreads();
+    const int it = s_item;
+    __syncthreads();
+    return it;
+  };
+  auto done = [&](int idx) {
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(a.hctr + idx, 1u);
+    }
+  };
+  // ---- pass 1: G1 partials ----
+  for (;;) {
+    const int ch = next(0);
+    if (ch >= nch) break;
+    const int cR4 = load(ch, k);
+    cq_gram(sl, cR4, k, G);
+    __syncthreads();
+    put(ch);
+    done(1);
+  }
+  // ---- pass 2 once R1^-1 is published (or nothing to do) ----
+  if (tid == 0) {
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.hctr + 4) : "memory");
+      if (v != (unsigned)S.step_idx + 1u) __nanosleep(200);
+    } while (v != (unsigned)S.step_idx + 1u);
+    s_hdr[0] = __ldcg(a.hR + DMQR_KP * DMQR_KP);
+    s_hdr[1] = __ldcg(a.hR + DMQR_KP * DMQR_KP + 1);
+  }
+  __syncthreads();
+  if (s_hdr[1] != 0.0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
+  const int kk = (int)s_hdr[0];
+  for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) Rs[e] = __ldcg(a.hR + e);
+  __syncthreads();
+  for (;;) {
+    const int ch = next(2);
+    if (ch >= nch) break;
+    const int cR4 = load(ch, kk);
+    cq_slice_gemm(sl, cR4, kk, kk, Rs);
+    __syncthreads();
+    {  // Q1 rows of the chunk -> q1g (the row parity of A)
+      const int64_t c0r = (int64_t)ch * CQ_RMAX;
+      const int cR = (int)min((int64_t)CQ_RMAX, mp - c0r);
+      if (trow < cR) {
+        double* dp = a.q1g + qodd + c0r + trow;
+#pragma unroll 4
+        for (int cc = tcol0; cc < kk; cc += tcstep) dp[(int64_t)cc * ldq] = sl[cc * CQ_LDS + trow];
+      }
+    }
+    cq_gram(sl, cR4, kk, G);
+    __syncthreads();
+    put(ch);
+    done(3);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// zero the helper counters (PDL chain: behind the swap, before the panel)
+__global__ void k_hzero(unsigned* __restrict__ h) {
+  pdl_enter();
+  if (threadIdx.x < 8) h[threadIdx.x] = 0u;
+}
 
 }  // namespace dmqr
