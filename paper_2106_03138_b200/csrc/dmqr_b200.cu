@@ -43,7 +43,7 @@ constexpr int PANEL_PMAX = 160;
 
 struct Layout {
   size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, trace, pdbg, tcount, upd, lacount, q1g, glist;
-  size_t qvb, qwb, qpart, qgpart, qcnt, hpart, hR, hctr, total;
+  size_t qvb, qwb, qpart, qgpart, qcnt, hpart, hR, hctr, gnp, total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -87,6 +87,8 @@ Layout layout(int64_t m, int64_t n) {
   L.hpart = take(sizeof(double) * DMQR_KP * DMQR_KP * (size_t)std::max<int64_t>(1, (m + 255) / 256));
   L.hR = take(sizeof(double) * (DMQR_KP * DMQR_KP + 2));
   L.hctr = take(sizeof(unsigned) * 8);
+  // serial guard norms: (column, 4096-row chunk) partials
+  L.gnp = take(sizeof(double) * 2 * (size_t)std::max<int64_t>(n, 1) * (size_t)std::max<int64_t>(1, (m + GN_ROWS - 1) / GN_ROWS));
   L.total = off;
   return L;
 }
@@ -331,6 +333,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   uint8_t* upd = (uint8_t*)(ws + L.upd);
   double* q1g = (double*)(ws + L.q1g);
   unsigned* qcnt = (unsigned*)(ws + L.qcnt);
+  double* gnp = (double*)(ws + L.gnp);
   int32_t* glist = (int32_t*)(ws + L.glist);
   unsigned* lacount = (unsigned*)(ws + L.lacount);
   StepRec* srec = (StepRec*)steps;
@@ -655,8 +658,17 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
       NOTE_LAUNCH();
     } else if (np > 0) {
       const int64_t blocks = std::min<int64_t>(ceil_div(np * 32, 256), (int64_t)d.sms * 16);
-      k_downdate<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, uref);
+      // tall columns: the guard columns' exact norms row-split over the grid
+      const bool gsplit = mp > 4 * GN_ROWS && !p->trace_norms;
+      k_downdate<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, uref, gsplit ? glist : nullptr);
       NOTE_LAUNCH();
+      if (gsplit) {
+        k_gnorm_part<<<(unsigned)(2 * d.sms), 256, 0, st>>>(ctl, (const double*)A, (const int32_t*)glist, gnp);
+        NOTE_LAUNCH();
+        k_gnorm_fin<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(np * 32, 256), (int64_t)d.sms * 4)),
+                      256, 0, st>>>(ctl, (const double*)A, (const int32_t*)glist, (const double*)gnp, u, uref);
+        NOTE_LAUNCH();
+      }
       if (p->trace_norms) { k_norm_trace<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, tbits); NOTE_LAUNCH(); }
     }
     CK(pdl_launch(k_step_end, dim3(1), dim3(32), 0, st, ctl, srec, norm_trace, tbits, (const double*)A, Z, ldz, u,

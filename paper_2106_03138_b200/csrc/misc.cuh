@@ -107,8 +107,8 @@ __device__ __forceinline__ void step_end_body(const CtlSnap& S, Ctl* __restrict_
     c->pend_done = 0;
     c->pend_ns = S.n_s;
     c->pend_l = l;
-    c->gcount = 0;
   }
+  c->gcount = 0;  // (look-ahead and serial guard lists)
   c->n_s = S.n_s + l;
   c->step_idx = idx + 1;
   c->l_acc = 0;

@@ -14,9 +14,11 @@ namespace dmqr {
 // (all lanes return the result).  Unscaled sum of squares when the max
 // magnitude keeps squares normal, else a second max-scaled pass (the
 // reference's scaling, matrix.py:73-77).
-__device__ __forceinline__ double warp_col_norm(const double* __restrict__ x, int64_t len, int lane) {
-  // 16-byte loads from the first 16-byte aligned element, 8 pairs per lane in
-  // flight (a 16384-row column is 16 round trips, not 256)
+// (sum of squares, max |x|) of a contiguous segment, warp-wide (all lanes
+// return both): 16-byte loads from the first 16-byte aligned element, 8 pairs
+// per lane in flight (a 16384-row column is 16 round trips, not 256)
+__device__ __forceinline__ void warp_col_sums(const double* __restrict__ x, int64_t len, int lane, double& sum,
+                                              double& amax) {
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, a0 = 0.0, a1 = 0.0;
   const int64_t h = (len > 0 && (reinterpret_cast<uintptr_t>(x) & 15)) ? 1 : 0;
   if (h && lane == 0) {
@@ -52,8 +54,13 @@ __device__ __forceinline__ double warp_col_norm(const double* __restrict__ x, in
     s2 = fma(p, p, s2);
     a1 = fmax(a1, fabs(p));
   }
-  double s = warp_sum((s0 + s1) + (s2 + s3));
-  double amax = warp_max(fmax(a0, a1));
+  sum = warp_sum((s0 + s1) + (s2 + s3));
+  amax = warp_max(fmax(a0, a1));
+}
+
+__device__ __forceinline__ double warp_col_norm(const double* __restrict__ x, int64_t len, int lane) {
+  double s, amax;
+  warp_col_sums(x, len, lane, s, amax);
   if (norm_range_ok(amax)) return sqrt(s);
   double t = 0.0;
   for (int64_t k = lane; k < len; k += 32) {
@@ -117,7 +124,7 @@ __global__ void k_colnorms_init(const double* __restrict__ A, int64_t m, int64_t
 // Columns whose downdated square falls to <= 1e-2 * u_ref^2 are recomputed
 // exactly from rows n_s1.. and their u_ref refreshed.
 __global__ void k_downdate(Ctl* __restrict__ c, const double* __restrict__ A, double* __restrict__ u,
-                           double* __restrict__ uref) {
+                           double* __restrict__ uref, int32_t* __restrict__ glist = nullptr) {
   if (c->done) return;
   TLSpan tl_span(c->step_idx, 12);
   const int64_t n_s = c->n_s, n_s1 = n_s + c->l_acc, n = c->n, m = c->m, lda = c->lda;
@@ -141,10 +148,72 @@ __global__ void k_downdate(Ctl* __restrict__ c, const double* __restrict__ A, do
     const double sq = __dsub_rn(__dmul_rn(uj, uj), d);
     double nu = sqrt(fmax(sq, 0.0));
     if (sq <= __dmul_rn(1e-2, __dmul_rn(rj, rj))) {
+      if (glist) {  // exact norm later, by k_gnorm_part / k_gnorm_fin (row-split over the grid)
+        if (lane == 0) glist[atomicAdd(&c->gcount, 1)] = (int32_t)j;
+        continue;
+      }
       nu = warp_col_norm(col + n_s1, m - n_s1, lane);
       if (lane == 0) uref[j] = nu;
     }
     if (lane == 0) u[j] = nu;
+  }
+}
+
+// Exact norms of the guard columns listed by k_downdate (rows n_s1 .. m of the
+// updated matrix): (column, GN_ROWS-row chunk) items over a persistent grid,
+// partial sum of squares and max |x| per item; k_gnorm_fin sums the chunks of
+// a column in fixed order.  A long column is read by many warps at once instead
+// of one (a 65536-row column was 128 dependent round trips for a single warp).
+constexpr int GN_ROWS = 4096;
+__global__ void __launch_bounds__(256) k_gnorm_part(const Ctl* __restrict__ c, const double* __restrict__ A,
+                                                    const int32_t* __restrict__ glist, double* __restrict__ gp) {
+  if (c->done) return;
+  const int g = c->gcount;
+  if (g == 0) return;
+  const int64_t n_s1 = c->n_s + c->l_acc, m = c->m, lda = c->lda;
+  const int64_t len = m - n_s1;
+  const int nch = (int)max((int64_t)1, ceil_div(len, GN_ROWS));
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t it = w0; it < (int64_t)g * nch; it += nw) {
+    const int gi = (int)(it / nch), ch = (int)(it % nch);
+    const int64_t j = glist[gi];
+    const int64_t r0 = n_s1 + (int64_t)ch * GN_ROWS, r1 = min(m, r0 + GN_ROWS);
+    double sv, av;
+    warp_col_sums(A + j * lda + r0, r1 - r0, lane, sv, av);
+    if (lane == 0) {
+      gp[2 * it] = sv;
+      gp[2 * it + 1] = av;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_gnorm_fin(Ctl* __restrict__ c, const double* __restrict__ A,
+                                                   const int32_t* __restrict__ glist, const double* __restrict__ gp,
+                                                   double* __restrict__ u, double* __restrict__ uref) {
+  if (c->done) return;
+  const int g = c->gcount;
+  const int64_t n_s1 = c->n_s + c->l_acc, m = c->m, lda = c->lda;
+  const int64_t len = m - n_s1;
+  const int nch = (int)max((int64_t)1, ceil_div(len, GN_ROWS));
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t gi = w0; gi < g; gi += nw) {
+    double sv = 0.0, av = 0.0;
+    for (int ch = lane; ch < nch; ch += 32) {
+      sv += gp[2 * (gi * nch + ch)];
+      av = fmax(av, gp[2 * (gi * nch + ch) + 1]);
+    }
+    sv = warp_sum(sv);
+    av = warp_max(av);
+    const int64_t j = glist[gi];
+    const double nu = norm_range_ok(av) ? sqrt(sv) : warp_col_norm(A + j * lda + n_s1, len, lane);
+    if (lane == 0) {
+      u[j] = nu;
+      uref[j] = nu;
+    }
   }
 }
 
