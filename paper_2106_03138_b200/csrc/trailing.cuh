@@ -32,12 +32,16 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src
 
 constexpr int TA_T = 256;       // 8 warps
 constexpr int TA_COLS = 64;     // output columns per CTA
-constexpr int TA_ROWS = 32;     // K slab
-constexpr int TA_LD = 36;       // slab stride (4 mod 16: conflict-free fragments; 16B aligned rows)
+constexpr int TA_ROWS = 16;     // K slab
+constexpr int TA_LD = 20;       // slab stride (4 mod 16: conflict-free fragments; 16B aligned rows)
+constexpr int TA_NST = 4;       // cp.async stages (three slabs in flight while one is consumed)
+constexpr int TA_RP = TA_ROWS / 2;    // row pairs per slab (16-byte copies)
+constexpr int TA_CL = TA_T / TA_RP;   // column lanes of the copy grid
 constexpr int TW_LD = DMQR_KP;  // 72 = 8 mod 16
-// 2 slab stages, reused by the fused T^T Z tail (T and Z tiles)
-constexpr size_t TA_SMEM = sizeof(double) * 2 * DMQR_KP * TW_LD;
-static_assert(2 * DMQR_KP * TW_LD >= 2 * (DMQR_KP + TA_COLS) * TA_LD, "smem reuse");
+// TA_NST slab stages, reused by the fused T^T Z tail (T and Z tiles)
+constexpr size_t TA_SMEM_ST = sizeof(double) * TA_NST * (DMQR_KP + TA_COLS) * TA_LD;
+constexpr size_t TA_SMEM_TZ = sizeof(double) * 2 * DMQR_KP * TW_LD;
+constexpr size_t TA_SMEM = TA_SMEM_ST > TA_SMEM_TZ ? TA_SMEM_ST : TA_SMEM_TZ;
 
 // Look-ahead bookkeeping of a step's own panel columns, by one CTA: u of the
 // accepted columns is cleared; the columns [n_s + l, tc0) that the Householder
@@ -187,28 +191,27 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
   const int odd = (int)(n_s & 1);  // slabs start one row early so global rows are even
 
   extern __shared__ __align__(16) double tas[];
-  double* ysb[2] = {tas, tas + DMQR_KP * TA_LD};
-  double* csb[2] = {tas + 2 * DMQR_KP * TA_LD, tas + 2 * DMQR_KP * TA_LD + TA_COLS * TA_LD};
+  // stage q: Y slab at tas + q KP LD, C slab after all the Y slabs
+  auto ysb = [&](int q) { return tas + q * DMQR_KP * TA_LD; };
+  auto csb = [&](int q) { return tas + TA_NST * DMQR_KP * TA_LD + q * TA_COLS * TA_LD; };
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t span = (re > rb) ? re - rb + odd : 0;
   const int nslab = (int)ceil_div(span, TA_ROWS);
   // thread -> (row pair rp, first column cb) of the 16 x {72 | 64} chunk grid of a slab
-  const int rp = tid & 15, cb = tid >> 4;  // 16 row pairs, 16 column lanes
+  const int rp = tid % TA_RP, cb = tid / TA_RP;  // row pairs x column lanes
   const double* Yp = A + n_s * lda + n_s;   // Y[r][i] at Yp[r + i*lda]
   const double* Cp = A + n_s + c0 * lda;    // C[r][cc] at Cp[r + cc*lda]
 
-  for (int e = tid; e < (lp - l) * TA_LD; e += TA_T) {  // rows i in [l, lp) stay zero
-    ysb[0][l * TA_LD + e] = 0.0;
-    ysb[1][l * TA_LD + e] = 0.0;
-  }
+  for (int e = tid; e < (lp - l) * TA_LD; e += TA_T)  // rows i in [l, lp) stay zero
+    for (int q = 0; q < TA_NST; ++q) ysb(q)[l * TA_LD + e] = 0.0;
   auto issue = [&](int sl) {
-    double* ys = ysb[sl & 1];
-    double* cs = csb[sl & 1];
+    double* ys = ysb(sl % TA_NST);
+    double* cs = csb(sl % TA_NST);
     const int64_t r = rb - odd + (int64_t)sl * TA_ROWS + 2 * rp;  // panel-relative, even global row
     const int64_t gr = n_s + r;
     const int bytes = (gr + 1 < m) ? 16 : ((gr < m) ? 8 : 0);
-    for (int i = cb; i < l; i += 16) cp_async16(ys + i * TA_LD + 2 * rp, Yp + r + (int64_t)i * lda, bytes);
-    for (int cc = cb; cc < TA_COLS; cc += 16)
+    for (int i = cb; i < l; i += TA_CL) cp_async16(ys + i * TA_LD + 2 * rp, Yp + r + (int64_t)i * lda, bytes);
+    for (int cc = cb; cc < TA_COLS; cc += TA_CL)
       cp_async16(cs + cc * TA_LD + 2 * rp, Cp + r + (col0 + cc) * lda, (col0 + cc < ncols) ? bytes : 0);
     cp_async_commit();
   };
@@ -216,9 +219,9 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
   auto fix = [&](int sl) {
     const int64_t r0 = rb - odd + (int64_t)sl * TA_ROWS;
     if (r0 >= 72 && r0 >= rb && r0 + TA_ROWS <= re) return;
-    double* ys = ysb[sl & 1];
+    double* ys = ysb(sl % TA_NST);
     for (int e = tid; e < l * TA_ROWS; e += TA_T) {
-      const int i = e >> 5, rr = e & 31;
+      const int i = e / TA_ROWS, rr = e % TA_ROWS;
       const int64_t r = r0 + rr;
       if (r < rb || r >= re || r <= i) ys[i * TA_LD + rr] = (r == i && r >= rb && r < re) ? 1.0 : 0.0;
     }
@@ -226,14 +229,14 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
   double acc[DMQR_KP / 8][2];
 #pragma unroll
   for (int q = 0; q < DMQR_KP / 8; ++q) acc[q][0] = acc[q][1] = 0.0;
-  if (nslab > 0) issue(0);
+  for (int q = 0; q < TA_NST - 1; ++q) {  // prologue: TA_NST - 1 slabs in flight (empty groups past the end)
+    if (q < nslab)
+      issue(q);
+    else
+      cp_async_commit();
+  }
   for (int sl = 0; sl < nslab; ++sl) {
-    if (sl + 1 < nslab) {
-      issue(sl + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    cp_async_wait<TA_NST - 2>();  // slab sl has landed (one group committed per slab)
     __syncthreads();
     {  // Y structure / rows outside [rb, re): only the first and boundary slabs (uniform branch)
       const int64_t r0 = rb - odd + (int64_t)sl * TA_ROWS;
@@ -242,8 +245,8 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
         __syncthreads();
       }
     }
-    const double* ys = ysb[sl & 1];
-    const double* cs = csb[sl & 1];
+    const double* ys = ysb(sl % TA_NST);
+    const double* cs = csb(sl % TA_NST);
 #pragma unroll
     for (int ks = 0; ks < TA_ROWS / 4; ++ks) {
       const int kr = 4 * ks + (lane & 3);
@@ -252,7 +255,11 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
       for (int q = 0; q < DMQR_KP / 8; ++q)
         if (q < lt) dmma884(acc[q][0], acc[q][1], ys[(q * 8 + (lane >> 2)) * TA_LD + kr], b);
     }
-    __syncthreads();
+    __syncthreads();  // (stage sl % TA_NST is refilled by the issue below, TA_NST - 1 slabs ahead)
+    if (sl + TA_NST - 1 < nslab)
+      issue(sl + TA_NST - 1);
+    else
+      cp_async_commit();
   }
   // ---- partial tile -> Zp[split] ----
   double* out = Zp + (int64_t)blockIdx.y * DMQR_KP * ldz;
@@ -500,36 +507,35 @@ __device__ void g_partial(const double* __restrict__ A, const double* __restrict
   const int lt = (l + 7) / 8, lp = lt * 8;
   const int odd = (int)(n_s & 1);
   extern __shared__ __align__(16) double gps[];
-  double* ysb[2] = {gps, gps + DMQR_KP * TA_LD};
-  double* csb[2] = {gps + 2 * DMQR_KP * TA_LD, gps + 2 * DMQR_KP * TA_LD + TA_COLS * TA_LD};
+  // stage q: Y slab at gps + q KP LD, C slab after all the Y slabs
+  auto ysb = [&](int q) { return gps + q * DMQR_KP * TA_LD; };
+  auto csb = [&](int q) { return gps + TA_NST * DMQR_KP * TA_LD + q * TA_COLS * TA_LD; };
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t span = (re > rb) ? re - rb + odd : 0;
   const int nslab = (int)ceil_div(span, TA_ROWS);
-  const int rp = tid & 15, cb = tid >> 4;
+  const int rp = tid % TA_RP, cb = tid / TA_RP;
   const int64_t ldq = q1_ld(m);
   const double* Yp = Q1g + odd;            // Q1[r][i] at Yp[r + i*ldq]
   const double* Cp = A + n_s + n_s * lda;  // C[r][cc] at Cp[r + cc*lda], columns from n_s
-  for (int e = tid; e < (lp - l) * TA_LD; e += TA_T) {
-    ysb[0][l * TA_LD + e] = 0.0;
-    ysb[1][l * TA_LD + e] = 0.0;
-  }
+  for (int e = tid; e < (lp - l) * TA_LD; e += TA_T)
+    for (int q = 0; q < TA_NST; ++q) ysb(q)[l * TA_LD + e] = 0.0;
   auto issue = [&](int sl) {
-    double* ys = ysb[sl & 1];
-    double* cs = csb[sl & 1];
+    double* ys = ysb(sl % TA_NST);
+    double* cs = csb(sl % TA_NST);
     const int64_t r = rb - odd + (int64_t)sl * TA_ROWS + 2 * rp;
     const int64_t gr = n_s + r;
     const int bytes = (gr + 1 < m) ? 16 : ((gr < m) ? 8 : 0);
-    for (int i = cb; i < l; i += 16) cp_async16(ys + i * TA_LD + 2 * rp, Yp + r + (int64_t)i * ldq, bytes);
-    for (int cc = cb; cc < TA_COLS; cc += 16)
+    for (int i = cb; i < l; i += TA_CL) cp_async16(ys + i * TA_LD + 2 * rp, Yp + r + (int64_t)i * ldq, bytes);
+    for (int cc = cb; cc < TA_COLS; cc += TA_CL)
       cp_async16(cs + cc * TA_LD + 2 * rp, Cp + r + (col0 + cc) * lda, (col0 + cc < ncols) ? bytes : 0);
     cp_async_commit();
   };
   auto fix = [&](int sl) {  // rows outside [rb, re) contribute nothing
     const int64_t r0 = rb - odd + (int64_t)sl * TA_ROWS;
     if (r0 >= rb && r0 + TA_ROWS <= re) return;
-    double* ys = ysb[sl & 1];
+    double* ys = ysb(sl % TA_NST);
     for (int e = tid; e < l * TA_ROWS; e += TA_T) {
-      const int i = e >> 5, rr = e & 31;
+      const int i = e / TA_ROWS, rr = e % TA_ROWS;
       const int64_t r = r0 + rr;
       if (r < rb || r >= re) ys[i * TA_LD + rr] = 0.0;
     }
@@ -537,14 +543,14 @@ __device__ void g_partial(const double* __restrict__ A, const double* __restrict
   double acc[DMQR_KP / 8][2];
 #pragma unroll
   for (int q = 0; q < DMQR_KP / 8; ++q) acc[q][0] = acc[q][1] = 0.0;
-  if (nslab > 0) issue(0);
+  for (int q = 0; q < TA_NST - 1; ++q) {  // prologue: TA_NST - 1 slabs in flight (empty groups past the end)
+    if (q < nslab)
+      issue(q);
+    else
+      cp_async_commit();
+  }
   for (int sl = 0; sl < nslab; ++sl) {
-    if (sl + 1 < nslab) {
-      issue(sl + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    cp_async_wait<TA_NST - 2>();  // slab sl has landed (one group committed per slab)
     __syncthreads();
     {  // rows outside [rb, re): only the boundary slabs (uniform branch, no extra barrier otherwise)
       const int64_t r0 = rb - odd + (int64_t)sl * TA_ROWS;
@@ -553,8 +559,8 @@ __device__ void g_partial(const double* __restrict__ A, const double* __restrict
         __syncthreads();
       }
     }
-    const double* ys = ysb[sl & 1];
-    const double* cs = csb[sl & 1];
+    const double* ys = ysb(sl % TA_NST);
+    const double* cs = csb(sl % TA_NST);
 #pragma unroll
     for (int ks = 0; ks < TA_ROWS / 4; ++ks) {
       const int kr = 4 * ks + (lane & 3);
@@ -563,7 +569,11 @@ __device__ void g_partial(const double* __restrict__ A, const double* __restrict
       for (int q = 0; q < DMQR_KP / 8; ++q)
         if (q < lt) dmma884(acc[q][0], acc[q][1], ys[(q * 8 + (lane >> 2)) * TA_LD + kr], b);
     }
-    __syncthreads();
+    __syncthreads();  // (stage sl % TA_NST is refilled by the issue below, TA_NST - 1 slabs ahead)
+    if (sl + TA_NST - 1 < nslab)
+      issue(sl + TA_NST - 1);
+    else
+      cp_async_commit();
   }
   double* out = Gp + (int64_t)split * DMQR_KP * ldz;
   const int64_t cc = col0 + wid * 8 + 2 * (lane & 3);
