@@ -417,6 +417,8 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   const bool trail_persistent = getenv("DMQR_TRAIL_PERSISTENT") != nullptr;  // A/B switch
   const bool spare_all = getenv("DMQR_SPARE_FREE_ONLY") == nullptr;          // A/B switch
   const bool no_helpers = getenv("DMQR_NO_HELPERS") != nullptr;               // A/B switch
+  // (test hook: DMQR_HELPER_WAIT_NS=0 makes the tall panel abandon its helpers)
+  const long long hwait_ns = getenv("DMQR_HELPER_WAIT_NS") ? atoll(getenv("DMQR_HELPER_WAIT_NS")) : 5000000ll;
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
 
   int64_t prev_ns_lo = 0;  // the lower bound the previous step was sized with
@@ -512,7 +514,8 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     const int G = cl_path ? P : ((P > 1) ? P + 1 : 1);
     PanelArgs pa{ctl, A, coeffs, T, red, use_smem, P,
                  (g_prof.load() >= 2 && steps_done == 2) ? pdbg : nullptr, std::max(0, g_prof.load() - 2), 0,
-                 q1g, 0, tline, 0, (double*)(ws + L.hpart), (double*)(ws + L.hR), (unsigned*)(ws + L.hctr)};
+                 q1g, 0, tline, 0, (double*)(ws + L.hpart), (double*)(ws + L.hR), (unsigned*)(ws + L.hctr),
+                 hwait_ns};
     void* kargs[] = {&pa};
     auto launch_cluster = [&](const void* fn, int ncta, unsigned threads, size_t dsm) -> cudaError_t {
       cudaLaunchConfig_t cfg = {};

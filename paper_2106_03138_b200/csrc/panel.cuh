@@ -139,7 +139,9 @@ struct PanelArgs {
   int helpers;
   double* hpart;     // [chunks][KP x KP] per-chunk Gram partials (upper tiles)
   double* hR;        // R1^-1 (KP x KP) + [kk, fail] published by rank 0
-  unsigned* hctr;    // [0] G1 items, [1] G1 done, [2] Q1 items, [3] Q1 done, [4] R1^-1 published (step + 1)
+  unsigned* hctr;    // [0] G1 items, [1] G1 done, [2] Q1 items, [3] Q1 done, [4] R1^-1 published (step + 1),
+                     // [6] / [7] pass 1 / 2 decision (2 use the partials, 1 abandoned)
+  long long hwait_ns;  // how long rank 0 waits for the helpers before streaming its own rows
 };
 
 // deterministic all-reduce of `len` doubles across the grid; in: s_part (this

@@ -730,15 +730,40 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     }
   };
   // sum the helper partials of chunks me, me + nr, ... (upper tiles, fixed order) into G
-  auto h_gather = [&](unsigned want_idx, double* G) {
+  // Whether the helpers' partials are used for a pass: rank 0 waits (bounded)
+  // for all chunks and decides for the whole cluster (hctr[dec] = 2: use them,
+  // 1: abandoned -- the helpers stop and the cluster streams its own rows, as
+  // without helpers).  Bounded, so a serialised launch (a profiler replaying
+  // kernels one at a time, CUDA_LAUNCH_BLOCKING) cannot deadlock.
+  __shared__ int s_use;
+  auto h_decide = [&](int done_idx, int dec_idx) -> bool {
     if (tid == 0) {
-      unsigned v;
+      if (me == 0) {
+        const long long deadline = gtimer() + a.hwait_ns;  // default 5 ms (a pass takes ~0.1 ms)
+        unsigned v;
+        bool ok = false;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.hctr + done_idx) : "memory");
+          if (v >= (unsigned)hnch) {
+            ok = true;
+            break;
+          }
+          if (gtimer() > deadline) break;
+          __nanosleep(100);
+        }
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.hctr + dec_idx), "r"(ok ? 2u : 1u) : "memory");
+      }
+      unsigned d;
       do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.hctr + want_idx) : "memory");
-        if (v < (unsigned)hnch) __nanosleep(100);
-      } while (v < (unsigned)hnch);
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d) : "l"(a.hctr + dec_idx) : "memory");
+      } while (d == 0u);
+      s_use = (d == 2u);
     }
     __syncthreads();
+    return s_use != 0;
+  };
+  // sum the helper partials of chunks me, me + nr, ... (upper tiles, fixed order) into G
+  auto h_gather = [&](double* G) {
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
       double g = 0.0;
       if ((e % DMQR_KP) / 8 >= (e / DMQR_KP) / 8)
@@ -747,12 +772,16 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     }
     __syncthreads();
   };
+  // without the helpers' partials (no helpers, or abandoned) a helper-mode
+  // panel streams its rows like a chunked one (the slice was never loaded)
+  const bool chunked_eff = chunked || hmode;
   if (a.helpers && !hmode) h_publish(true, 0);  // (nothing for the helpers' second pass)
   // ---- P0/P1: slice <- P (rows zero-padded to a multiple of 4), G = P^T P ----
-  if (hmode) {
+  const bool h1 = hmode && h_decide(1, 6);  // (pass 1 abandoned: no helper runs pass 2 either)
+  if (h1) {
     CQT();
-    h_gather(1, A2);
-  } else if (!chunked) {
+    h_gather(A2);
+  } else if (!chunked_eff) {
     load_chunk(gA, lda, 0, k);
     CQT();
     cq_gram(sl, R4, k, A2);
@@ -808,12 +837,15 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
       if (i == j) vD[i] = A2[i * DMQR_KP + i];
     }
     __syncthreads();
-    if (hmode) {
-      // the helpers form Q1 = P R1^-1 into q1g and the per-chunk Q1 Grams
+    bool use_h2 = false;
+    if (h1) {  // the helpers form Q1 = P R1^-1 into q1g and the per-chunk Q1 Grams
       h_publish(false, kk);
-      h_gather(3, A1);
+      use_h2 = h_decide(3, 7);
+    }
+    if (use_h2) {
+      h_gather(A1);
       CQT();
-    } else if (!chunked) {
+    } else if (!chunked_eff) {
       cq_slice_gemm(sl, R4, kk, kk, A1);
       CQT();
       // publish this rank's Q1 rows: k_ygemm forms Y = Q1 M from them, and
@@ -994,7 +1026,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     r2_inverse();
     CQT();
     // ---- P12: top l x l block of Q = Q1 R2^-1 -> A1 ----
-    if (!chunked && !hmode)
+    if (!chunked_eff)
       cq_small_gemm<true>([&](int i, int t) { return sl[t * CQ_LDS + i]; },
                           [&](int t, int j) { return A2[t * DMQR_KP + j]; }, A1, l);
     else  // (rank 0's first rows, published)
@@ -1158,8 +1190,19 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_helper(PanelArgs a) {
       atomicAdd(a.hctr + idx, 1u);
     }
   };
+  auto abandoned = [&](int dec_idx) {  // the panel gave up on the helpers for this pass
+    __shared__ int s_ab;
+    if (tid == 0) {
+      unsigned d;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d) : "l"(a.hctr + dec_idx) : "memory");
+      s_ab = (d == 1u);
+    }
+    __syncthreads();
+    return s_ab != 0;
+  };
   // ---- pass 1: G1 partials ----
   for (;;) {
+    if (abandoned(6)) break;
     const int ch = next(0);
     if (ch >= nch) break;
     const int cR4 = load(ch, k);
@@ -1170,13 +1213,15 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_helper(PanelArgs a) {
   }
   // ---- pass 2 once R1^-1 is published (or nothing to do) ----
   if (tid == 0) {
-    unsigned v;
-    do {
+    unsigned v, d6;
+    for (;;) {  // R1^-1 published, or pass 1 abandoned (then the panel never publishes)
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.hctr + 4) : "memory");
-      if (v != (unsigned)S.step_idx + 1u) __nanosleep(200);
-    } while (v != (unsigned)S.step_idx + 1u);
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d6) : "l"(a.hctr + 6) : "memory");
+      if (v == (unsigned)S.step_idx + 1u || d6 == 1u) break;
+      __nanosleep(200);
+    }
     s_hdr[0] = __ldcg(a.hR + DMQR_KP * DMQR_KP);
-    s_hdr[1] = __ldcg(a.hR + DMQR_KP * DMQR_KP + 1);
+    s_hdr[1] = (v == (unsigned)S.step_idx + 1u) ? __ldcg(a.hR + DMQR_KP * DMQR_KP + 1) : 1.0;
   }
   __syncthreads();
   if (s_hdr[1] != 0.0) {
@@ -1187,6 +1232,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_helper(PanelArgs a) {
   for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) Rs[e] = __ldcg(a.hR + e);
   __syncthreads();
   for (;;) {
+    if (abandoned(7)) break;
     const int ch = next(2);
     if (ch >= nch) break;
     const int cR4 = load(ch, kk);

@@ -456,3 +456,26 @@ def test_batched_graph_lanes_with_fallback_runs():
             ref = O.qrdm2(B[i], margins=True, stop_rule="none")
         _compare(B[i], r, ref, f"batch-fallback[{i}]")
     assert saw_fallback
+
+
+@pytest.mark.parametrize("wait_ns", ["0", None])
+def test_tall_panel_helpers_and_their_fallback(wait_ns, monkeypatch):
+    """Tall panels (m' > 16 x 256, serial schedule) take their row passes from
+    k_panel_helper; with no wait (DMQR_HELPER_WAIT_NS=0) the cluster abandons
+    them and streams its own rows -- the path a serialised launch takes.  Both
+    must give the no-helper factorization's decisions and factors to rounding."""
+    from paper_2106_03138_b200 import qrdm2
+
+    rng = np.random.default_rng(44)
+    A = rng.standard_normal((9000, 300)) * np.logspace(0, -4, 300)[rng.permutation(300)]
+    monkeypatch.setenv("DMQR_NO_HELPERS", "1")
+    base = qrdm2(A)
+    monkeypatch.delenv("DMQR_NO_HELPERS")
+    if wait_ns is not None:
+        monkeypatch.setenv("DMQR_HELPER_WAIT_NS", wait_ns)
+    res = qrdm2(A)
+    assert np.array_equal(res.perm.forward, base.perm.forward) and res.rank == base.rank
+    scale = np.abs(base.packed).max()
+    assert np.abs(res.packed - base.packed).max() <= 1e-10 * scale
+    resid, orth = parity.residuals(A, res)
+    assert resid <= 50 * 9000 * O.EPS and orth <= 50 * 9000 * O.EPS
