@@ -40,13 +40,15 @@ struct PlanSmem {
   int lastw[DMQR_KP];  // latest content written into window slot d (-1: none)
 };
 
-__device__ void plan_swaps_warp(Ctl* c, const CtlSnap& S, int nsel, double gamma, PlanSmem& ps) {
+// sel_smem: the selected columns already in shared memory (else read from c->sel)
+__device__ void plan_swaps_warp(Ctl* c, const CtlSnap& S, int nsel, double gamma, PlanSmem& ps,
+                                const int* sel_smem = nullptr) {
   const int lane = threadIdx.x & 31;
   const int n_s = S.n_s;
   const int k_s = (int)min((int64_t)nsel, S.kmax - n_s);
   for (int d = lane; d < DMQR_KP; d += 32) {
     ps.lastw[d] = -1;
-    ps.sel[d] = (d < nsel) ? c->sel[d] : 0;
+    ps.sel[d] = (d < nsel) ? (sel_smem ? sel_smem[d] : c->sel[d]) : 0;
   }
   __syncwarp();
   if (lane == 0) {
@@ -305,6 +307,8 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __
 
 struct FinSmem {
   double g[DMQR_KP * DMQR_KP];  // Gram, then Theta (upper)
+  int cand[DMQR_KP];            // c->cand staged with the Gram (no round trip in the serial tail)
+  int sel[DMQR_KP];             // the selected columns (seed first)
   double inv[DMQR_KP];
   double rowsum[DMQR_KP];
   double amax[DMQR_KP];
@@ -382,6 +386,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
     const int i = e / DMQR_KP, j = e % DMQR_KP;
     if (j >= i && j < ncand) sm.g[e] = __ldcg(gfin + e);
   }
+  for (int q = tid; q < ncand; q += GRAM_T) sm.cand[q] = c->cand[q];
   __syncthreads();
   // over/underflow risk: the diagonal (sums of squares) bounds every entry
   for (int i = tid; i < ncand; i += GRAM_T) {
@@ -494,10 +499,14 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
     for (int p = lane; p < nch; p += 32) gmin = fmin(gmin, sm.rowsum[p]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) gmin = fmin(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
-    for (int q = lane; q < nch; q += 32) c->sel[q] = c->cand[sm.chosen[q]];
+    for (int q = lane; q < nch; q += 32) {
+      const int sq = sm.cand[sm.chosen[q]];
+      sm.sel[q] = sq;
+      c->sel[q] = sq;
+    }
     __syncwarp();
     GFT(4);
-    plan_swaps_warp(c, S, nch, gmin, sm.plan);
+    plan_swaps_warp(c, S, nch, gmin, sm.plan, sm.sel);
     GFT(5);
     return;
   }
@@ -552,9 +561,13 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) gmin = fmin(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
-  for (int q = lane; q < nch; q += 32) c->sel[q] = c->cand[sm.chosen[q]];
+  for (int q = lane; q < nch; q += 32) {
+    const int sq = sm.cand[sm.chosen[q]];
+    sm.sel[q] = sq;
+    c->sel[q] = sq;
+  }
   __syncwarp();
-  plan_swaps_warp(c, S, nch, gmin, sm.plan);
+  plan_swaps_warp(c, S, nch, gmin, sm.plan, sm.sel);
 }
 
 }  // namespace dmqr
