@@ -68,6 +68,20 @@ struct Ctl {
   uint32_t pad1[3];
 };
 
+// Batched launches (grid.z = matrices of a batch, small matrices): every
+// per-matrix buffer -- control block, workspace, matrix, outputs -- sits in a
+// per-matrix block at a fixed byte stride g_zstride, so a kernel shifts its
+// pointer arguments by blockIdx.z * g_zstride at entry (gridDim.z == 1: no-op).
+// The stride is set by the batched driver (process-wide lock while it runs).
+__constant__ int64_t g_zstride;
+template <typename... Ts>
+__device__ __forceinline__ void zshift(Ts&... ps) {
+  if (gridDim.z > 1) {
+    const int64_t o = (int64_t)blockIdx.z * g_zstride;
+    ((ps = ps ? (Ts)((char*)(ps) + o) : ps), ...);
+  }
+}
+
 // Entry snapshot of the scalar decision state.  Every field is loaded
 // unconditionally and independently at kernel entry, so the loads overlap in
 // one L2 round trip instead of trickling through early-exit branches (unused

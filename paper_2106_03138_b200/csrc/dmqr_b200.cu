@@ -306,7 +306,13 @@ struct StepGraph {
 int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* p, double* coeffs, int64_t* perm,
                int64_t* swaps, int64_t swap_cap, dmqr_step* steps, int64_t step_cap, double* norm_trace,
                void* workspace, size_t ws_bytes, dmqr_info* info, double* host_packed, int64_t host_ld, void* stream,
-               int qrp, StepGraph* sgraph = nullptr) {
+               int qrp, StepGraph* sgraph = nullptr, int nz = 1, int64_t zs = 0, HostRec* zrec = nullptr) {
+  // nz > 1: a batch of nz matrices in per-matrix blocks zs bytes apart (all
+  // pointers are block 0's; kernels shift by blockIdx.z * zs, grids get z = nz);
+  // small matrices, serial schedule, no streaming / trace / scalar-pivot engine;
+  // zrec: nz pairs of pinned poll records
+  const unsigned NZ = (unsigned)std::max(1, nz);
+  if (nz > 1 && (qrp || p->trace_norms || host_packed || !zrec)) return DMQR_EINVAL;
   if (host_packed && host_ld < m) return DMQR_EINVAL;
   int rc = validate(m, n, lda, p);
   if (rc) return rc;
@@ -348,7 +354,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   // graded inputs make its guard path expensive: serial -- measured on cfg2 /
   // cfg5 at 8192, 12288, 16384)
   const bool la_all = !qrp && !p->trace_norms && getenv("DMQR_NO_LOOKAHEAD") == nullptr &&
-                      m * n >= (int64_t)1 << 20 && m <= 4 * n && n <= 12288;
+                      m * n >= (int64_t)1 << 20 && m <= 4 * n && n <= 12288 && NZ == 1;
 
 
   const int64_t kmax = std::min(m, n);
@@ -356,26 +362,29 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   if (p->stop_rule == DMQR_STOP_EPS_N) eps1 = p->epsilon * (double)n;
   if (p->stop_rule == DMQR_STOP_EPS_SQRT_N) eps1 = p->epsilon * std::sqrt((double)n);
 
-  CK(cudaMemsetAsync(ws, 0, L.ctl + sizeof(Ctl), st));
-  CK(cudaMemsetAsync(tbits, 0, sizeof(unsigned long long) * 4, st));
+  auto zmemset = [&](void* ptr, size_t bytes) -> cudaError_t {
+    return NZ > 1 ? cudaMemset2DAsync(ptr, (size_t)zs, 0, bytes, NZ, st) : cudaMemsetAsync(ptr, 0, bytes, st);
+  };
+  CK(zmemset(ws, L.ctl + sizeof(Ctl)));
+  CK(zmemset(tbits, sizeof(unsigned long long) * 4));
   int32_t* nonfinite = (int32_t*)(tbits + 2);
-  CK(cudaMemsetAsync(T, 0, sizeof(double) * DMQR_KP * DMQR_KP, st));
-  CK(cudaMemsetAsync(tcount, 0, sizeof(unsigned) * (ceil_div(std::max<int64_t>(n, 1), TA_COLS) + 1), st));
-  CK(cudaMemsetAsync(upd, 0, (size_t)std::max<int64_t>(n, 1), st));
-  CK(cudaMemsetAsync(lacount, 0, sizeof(unsigned) * 16, st));
+  CK(zmemset(T, sizeof(double) * DMQR_KP * DMQR_KP));
+  CK(zmemset(tcount, sizeof(unsigned) * (ceil_div(std::max<int64_t>(n, 1), TA_COLS) + 1)));
+  CK(zmemset(upd, (size_t)std::max<int64_t>(n, 1)));
+  CK(zmemset(lacount, sizeof(unsigned) * 16));
   if (n > 0) {
     if (m > 0) {
       int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)d.sms * 16);
-      k_colnorms_init<<<(unsigned)blocks, 256, 0, st>>>(A, m, n, lda, u, uref, nonfinite);
+      k_colnorms_init<<<dim3((unsigned)blocks, 1, NZ), 256, 0, st>>>(A, m, n, lda, u, uref, nonfinite);
       NOTE_LAUNCH();
     } else {
-      CK(cudaMemsetAsync(u, 0, sizeof(double) * n, st));
-      CK(cudaMemsetAsync(uref, 0, sizeof(double) * n, st));
+      CK(zmemset(u, sizeof(double) * n));
+      CK(zmemset(uref, sizeof(double) * n));
     }
   }
   InitArgs ia{ctl, u, perm, coeffs, m, n, lda, kmax, p->tau, p->delta, eps1, p->k_dm, p->use_delta_max,
               p->break_check, p->trace_norms, swap_cap, step_cap, nonfinite, 0};
-  k_init<<<1, 1024, 0, st>>>(ia);
+  k_init<<<dim3(1, 1, NZ), 1024, 0, st>>>(ia);
   NOTE_LAUNCH();
   CK(cudaGetLastError());
 
@@ -391,7 +400,8 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     CK(cudaMallocHost(&hrec, 2 * sizeof(HostRec)));
     for (auto& e : hev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  for (int q = 0; q < 2; ++q) ((volatile HostRec*)hrec)[q].seq = -1;
+  HostRec* const hrecs = (NZ > 1) ? zrec : hrec;  // (one pair per matrix; k_step_end offsets by blockIdx.z)
+  for (unsigned q = 0; q < 2 * NZ; ++q) ((volatile HostRec*)hrecs)[q].seq = -1;
   const bool prof = g_prof.load() != 0;
   cudaEvent_t ev[2][5];
   if (prof)
@@ -453,18 +463,18 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     }
     // ---- selection ----
     PROF(0);
-    CK(pdl_launch(k_select, dim3(1), dim3(SEL_T), 0, st, ctl, (const double*)u));
+    CK(pdl_launch(k_select, dim3(1, 1, NZ), dim3(SEL_T), 0, st, ctl, (const double*)u));
     NOTE_LAUNCH();
     const int64_t ldz = ldz_for(n);
     const int GG = (int)std::clamp<int64_t>(ceil_div(mp, GRAM_ROWS), 1, std::min(GRAM_GMAX, d.sms));
-    CK(pdl_launch(k_gram, dim3(GG), dim3(GRAM_T), GRAM_SMEM, st, ctl, A, gpart, (const double*)Z, ldz,
+    CK(pdl_launch(k_gram, dim3(GG, 1, NZ), dim3(GRAM_T), GRAM_SMEM, st, ctl, A, gpart, (const double*)Z, ldz,
                   (const uint8_t*)upd));
     NOTE_LAUNCH();
-    CK(pdl_launch(k_gram_finish, dim3(45), dim3(GRAM_T), sizeof(FinSmem), st, ctl, (const double*)A,
+    CK(pdl_launch(k_gram_finish, dim3(45, 1, NZ), dim3(GRAM_T), sizeof(FinSmem), st, ctl, (const double*)A,
                   (const double*)gpart, GG, gfin, upd, tline));
     NOTE_LAUNCH();
     {
-      CK(pdl_launch(k_swap, dim3((unsigned)ceil_div(m + (la ? DMQR_KP : 0), SWAP_ROWS)), dim3(SWAP_T), SWAP_SMEM,
+      CK(pdl_launch(k_swap, dim3((unsigned)ceil_div(m + (la ? DMQR_KP : 0), SWAP_ROWS), 1, NZ), dim3(SWAP_T), SWAP_SMEM,
                     st, ctl, A, u, uref, perm, swaps, Z, ldz, upd));
       NOTE_LAUNCH();
     }
@@ -521,7 +531,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     void* kargs[] = {&pa};
     auto launch_cluster = [&](const void* fn, int ncta, unsigned threads, size_t dsm) -> cudaError_t {
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(ncta);
+      cfg.gridDim = dim3(ncta, 1, NZ);
       cfg.blockDim = dim3(threads);
       cfg.dynamicSmemBytes = dsm;
       cfg.stream = st;
@@ -550,7 +560,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
                                        (int)std::min<int64_t>(NSPLIT_MAX, std::max<int64_t>(1, ceil_div(mp, 256))));
     if (la_rest && !cq_path) CK(launch_la_rest(false));
     // tall CholeskyQR2 panel, serial schedule: its row passes go to the free SMs
-    const bool helpers = cq_path && !spare && mp > (int64_t)Pcq * CQ_RMAX && d.sms - Pcq >= 16 && !no_helpers;
+    const bool helpers = cq_path && !spare && mp > (int64_t)Pcq * CQ_RMAX && d.sms - Pcq >= 16 && !no_helpers && NZ == 1;
     if (cq_path) {
       pa.spare = spare ? 1 : 0;
       pa.helpers = helpers ? 1 : 0;
@@ -607,7 +617,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
       CK(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(PANEL_T), kargs, rr_path ? 0 : smem, st));
       NOTE_LAUNCH();
     } else if (rr_path) {
-      k_panel_rr<GridRed><<<1, PANEL_T, 0, st>>>(pa);
+      k_panel_rr<GridRed><<<dim3(1, 1, NZ), PANEL_T, 0, st>>>(pa);
       NOTE_LAUNCH();
     } else {
       k_panel<<<1, PANEL_T, smem, st>>>(pa);
@@ -615,7 +625,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     }
     if (cq_path && mp > 1 && !spare) {  // Y below the top block of a CholeskyQR2 panel, on every SM
       // (with the look-ahead, k_spare does this as its third phase)
-      CK(pdl_launch(k_ygemm, dim3((unsigned)ceil_div(mp - 1, YG_ROWS)), dim3(256), YG_SMEM, st, ctl, A,
+      CK(pdl_launch(k_ygemm, dim3((unsigned)ceil_div(mp - 1, YG_ROWS), 1, NZ), dim3(256), YG_SMEM, st, ctl, A,
                     (const double*)q1g, (const double*)(red + 37 * DMQR_KP * DMQR_KP)));
       NOTE_LAUNCH();
     }
@@ -632,7 +642,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
                       glist));
         NOTE_LAUNCH();
       }
-      CK(pdl_launch(k_trail_a, dim3((unsigned)ntile, nsplit), dim3(TA_T), TA_SMEM, st, ctl, A, Zp,
+      CK(pdl_launch(k_trail_a, dim3((unsigned)ntile, nsplit, NZ), dim3(TA_T), TA_SMEM, st, ctl, A, Zp,
                     (const double*)T, Z, tcount, ldz, u, uref, upd, spare ? 1 : 0, glist));
       NOTE_LAUNCH();
       if (la) {
@@ -643,7 +653,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
         k_trail_bq<<<(unsigned)std::min<int64_t>(work, d.sms), TQ_T, TQ_SMEM, st>>>(ctl, A, Z, ldz);
         NOTE_LAUNCH();
       } else if (!trail_persistent) {
-        k_trail_b<false><<<dim3((unsigned)ceil_div(mp + 1, TB_ROWS), (unsigned)ceil_div(ncols_ub, TB_COLS)), TB_T,
+        k_trail_b<false><<<dim3((unsigned)ceil_div(mp + 1, TB_ROWS), (unsigned)ceil_div(ncols_ub, TB_COLS), NZ), TB_T,
                            TB_SMEM, st>>>(ctl, A, Z, ldz, upd, lacount + 1);
         NOTE_LAUNCH();
       } else {
@@ -670,7 +680,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
       const int64_t blocks = std::min<int64_t>(ceil_div(np * 32, 256), (int64_t)d.sms * 16);
       // tall columns: the guard columns' exact norms row-split over the grid
       const bool gsplit = mp > 4 * GN_ROWS && !p->trace_norms;
-      k_downdate<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, uref, gsplit ? glist : nullptr);
+      k_downdate<<<dim3((unsigned)blocks, 1, NZ), 256, 0, st>>>(ctl, A, u, uref, gsplit ? glist : nullptr);
       NOTE_LAUNCH();
       if (gsplit) {
         k_gnorm_part<<<(unsigned)(2 * d.sms), 256, 0, st>>>(ctl, (const double*)A, (const int32_t*)glist, gnp);
@@ -681,8 +691,8 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
       }
       if (p->trace_norms) { k_norm_trace<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, tbits); NOTE_LAUNCH(); }
     }
-    CK(pdl_launch(k_step_end, dim3(1), dim3(32), 0, st, ctl, srec, norm_trace, tbits, (const double*)A, Z, ldz, u,
-                  uref, upd, hrec, eidx));
+    CK(pdl_launch(k_step_end, dim3(1, 1, NZ), dim3(32), 0, st, ctl, srec, norm_trace, tbits, (const double*)A, Z, ldz, u,
+                  uref, upd, hrecs, eidx));
     NOTE_LAUNCH();
     PROF(4);
     CK(cudaGetLastError());
@@ -707,14 +717,14 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   int known = 0, enq = 0, known_steps = 0;
   bool qp_mode = qrp != 0;
   // k_qp3 splits each column into at most QP_RMAX staged row segments
-  const bool qp_ok = m <= (int64_t)QP_RMAX * QP_XCH;
+  const bool qp_ok = m <= (int64_t)QP_RMAX * QP_XCH && NZ == 1;
   if (qrp && !qp_ok) return DMQR_EINVAL;
   // replayed step graph (batched small matrices; serial schedule only)
   const bool use_graph = sgraph != nullptr && !la_all && !qrp && !p->trace_norms && !prof && !tline &&
-                         getenv("DMQR_NO_GRAPH") == nullptr;
+                         getenv("DMQR_NO_GRAPH") == nullptr && getenv("DMQR_NO_STEP_GRAPH") == nullptr;
   std::vector<unsigned char> gkey;
   if (use_graph) {
-    const void* parts[] = {A, coeffs, perm, swaps, steps, workspace, (const void*)hrec};
+    const void* parts[] = {A, coeffs, perm, swaps, steps, workspace, (const void*)hrecs};
     const int64_t dims[] = {m, n, lda, swap_cap, step_cap};
     gkey.resize(sizeof(parts) + sizeof(dims) + sizeof(dmqr_params));
     std::memcpy(gkey.data(), parts, sizeof(parts));
@@ -732,7 +742,25 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     const int sl = known & 1;
     // poll the step's record (k_step_end posts it); check the stream now and
     // then so that a failed launch cannot hang the loop
-    volatile HostRec* r = hrec + sl;
+    volatile HostRec* r = hrecs + sl;
+    // (a batch: every matrix's record of this step; the lowest n_s and 'all done')
+    int32_t zmin_ns = 0x7fffffff, zall_done = 1;
+    for (unsigned z = 1; z < NZ; ++z) {
+      volatile HostRec* rz = hrecs + 2 * z + sl;
+      for (long spins = 1; rz->seq != known + 1; ++spins) {
+        if (spins > 64) std::this_thread::yield();
+        if ((spins & 1023) == 0) {
+          const cudaError_t e = cudaStreamQuery(st);
+          if (e != cudaSuccess && e != cudaErrorNotReady) return DMQR_ECUDA;
+          if (e == cudaSuccess && rz->seq != known + 1) {
+            std::atomic_thread_fence(std::memory_order_seq_cst);
+            if (rz->seq != known + 1) return DMQR_ECUDA;
+          }
+        }
+      }
+      zmin_ns = std::min<int32_t>(zmin_ns, (int32_t)rz->n_s);
+      zall_done &= (rz->flags & 1);
+    }
     for (long spins = 1; r->seq != known + 1; ++spins) {
       // batch lanes may outnumber the host cores: give the core away while waiting
       if (sgraph && spins > 64) std::this_thread::yield();
@@ -761,10 +789,10 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
       }
       g_acc.steps += 1;
     }
-    known_ns = r->n_s;
+    known_ns = std::min<int32_t>((int32_t)r->n_s, zmin_ns);
     known_steps = r->step_idx;
     ++known;
-    if (r->flags & 1) finished = true;
+    if ((r->flags & 1) && zall_done) finished = true;
     if (r->flags & 2) want_serial = true;
     // a scalar-fallback step hands the run to the blocked scalar-pivot engine;
     // its blocks keep it until a fallback run ends on the floor test
@@ -808,7 +836,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
       k_qp3_trace<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, tbits);
       NOTE_LAUNCH();
     }
-    k_qp3_post<<<1, 32, 0, st>>>(ctl, p->trace_norms ? norm_trace : nullptr, tbits, hrec, enq);
+    k_qp3_post<<<1, 32, 0, st>>>(ctl, p->trace_norms ? norm_trace : nullptr, tbits, hrecs, enq);
     NOTE_LAUNCH();
     PROF(4);
     CK(cudaGetLastError());
@@ -891,7 +919,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
       for (auto& e : r) cudaEventDestroy(e);
 #undef PROF
   g_calls.fetch_add(1);
-  k_finalize<<<1, 256, 0, st>>>(ctl, A, p->stop_rule == DMQR_STOP_NONE);
+  k_finalize<<<dim3(1, 1, NZ), 256, 0, st>>>(ctl, A, p->stop_rule == DMQR_STOP_NONE);
   NOTE_LAUNCH();
   CK(cudaGetLastError());
   if (host_packed && m > 0 && n > 0) {  // the rest of the packed factor
@@ -899,6 +927,25 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     copied = std::min(copied, n);
     if (stream_cols(n, hev[0])) return DMQR_ECUDA;
     CK(cudaStreamSynchronize(sCopy));
+  }
+  if (NZ > 1) {  // a batch: every matrix's control block
+    std::vector<Ctl> hcs(NZ);
+    CK(cudaMemcpy2DAsync(hcs.data(), sizeof(Ctl), ctl, (size_t)zs, sizeof(Ctl), NZ, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int rc0 = 0;
+    for (unsigned z = 0; z < NZ; ++z) {
+      const Ctl& h = hcs[z];
+      dmqr_info& in = info[z];
+      in.rank = (kmax == 0) ? 0 : h.rank;
+      in.n_factored = (kmax == 0) ? 0 : h.n_factored;
+      in.n_steps = (kmax == 0) ? 0 : h.step_idx;
+      in.n_swaps = (kmax == 0) ? 0 : h.n_swaps;
+      in.stopped_early = (kmax == 0) ? 0 : h.stopped;
+      in.status = h.status;
+      in.a_max0 = h.a_max0;
+      if (!rc0 && h.status) rc0 = h.status;
+    }
+    return rc0;
   }
   Ctl hc;
   CK(cudaMemcpyAsync(&hc, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
@@ -976,13 +1023,16 @@ LaneBufs lane_bufs(int64_t m, int64_t n, int64_t lda) {
   return b;
 }
 bool batch_graph_ok(int64_t m, int64_t n) { return m * n < ((int64_t)1 << 20); }
+constexpr int ZG = 32;  // small matrices per batched launch (grid.z)
+std::mutex g_zstride_mu;  // g_zstride is process-wide: one batched call at a time
 }  // namespace
 
 extern "C" {
 
 size_t dmqr_batched_workspace_bytes(int64_t m, int64_t n, const dmqr_params* params, int32_t nlanes) {
-  const size_t extra = batch_graph_ok(m, n) ? lane_bufs(m, n, (m + 7) / 8 * 8).total : 0;
-  return (size_t)std::max(1, nlanes) * (al(dmqr_workspace_bytes(m, n, params)) + extra);
+  const size_t eng = al(dmqr_workspace_bytes(m, n, params));
+  const size_t per = batch_graph_ok(m, n) ? (size_t)ZG * (eng + lane_bufs(m, n, (m + 7) / 8 * 8).total) : eng;
+  return (size_t)std::max(1, nlanes) * per;
 }
 
 int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_t lda, int64_t stride,
@@ -993,15 +1043,25 @@ int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_
   if (rc) return rc;
   if (batch < 0 || stride < lda * n || !infos || nlanes < 1) return DMQR_EINVAL;
   const size_t per_engine = al(dmqr_workspace_bytes(m, n, p));
-  // small matrices: lane-private buffers + a replayed step graph per lane
-  // (needs the caller's lda to match the lane buffers' and caps within theirs)
+  // small matrices: groups of ZG per launch (grid.z) in lane-private per-matrix
+  // blocks + a replayed step graph per lane (needs the caller's lda to match the
+  // blocks' and caps within theirs)
   const LaneBufs lb = lane_bufs(m, n, lda);
   const bool graphs = batch_graph_ok(m, n) && lda == (m + 7) / 8 * 8 && swap_cap <= lb.swap_cap &&
                       step_cap <= lb.step_cap && getenv("DMQR_NO_GRAPH") == nullptr;
-  const size_t per = per_engine + (batch_graph_ok(m, n) ? lb.total : 0);
+  const size_t zblk = per_engine + lb.total;  // (both multiples of 256 bytes)
+  const size_t per = batch_graph_ok(m, n) ? (size_t)ZG * zblk : per_engine;
   nlanes = (int32_t)std::min<int64_t>(nlanes, std::max<int64_t>(batch, 1));
   if (m > 4096) nlanes = 1;  // cooperative panel launches must not compete for co-residency
   if (ws_bytes < per * (size_t)nlanes || !workspace) return DMQR_EINVAL;
+  if (graphs) nlanes = (int32_t)std::min<int64_t>(nlanes, ceil_div(batch, ZG));
+  // the per-matrix block stride the batched kernels shift by (process-wide)
+  std::unique_lock<std::mutex> zlock(g_zstride_mu, std::defer_lock);
+  if (graphs) {
+    zlock.lock();
+    const int64_t zs64 = (int64_t)zblk;
+    CK(cudaMemcpyToSymbol(g_zstride, &zs64, sizeof(int64_t)));
+  }
   if (batch == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   int dev = 0;
@@ -1034,40 +1094,55 @@ int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_
         if (r && !lane_rc[q]) lane_rc[q] = r;
       }
     } else {
-      unsigned char* lbuf = ws + per_engine;
-      double* Aw = (double*)(lbuf + lb.a);
-      double* cw = (double*)(lbuf + lb.coeffs);
-      int64_t* pw = (int64_t*)(lbuf + lb.perm);
-      int64_t* sw = (int64_t*)(lbuf + lb.swaps);
-      dmqr_step* tw = (dmqr_step*)(lbuf + lb.steps);
-      StepGraph sg;
+      // groups of up to ZG matrices in lane-private per-matrix blocks (engine
+      // workspace + matrix + outputs, zblk bytes apart): one launch per kernel
+      // per step for the whole group (grid.z), the step replayed as a graph
+      unsigned char* zbase = ws;
+      unsigned char* zb = ws + per_engine;  // block 0's matrix and outputs (after its engine workspace)
       const cudaStream_t s = ls[q];
       const size_t abytes = sizeof(double) * (size_t)lda * (size_t)n;
-      for (int64_t b = q; b < batch; b += nlanes) {
+      StepGraph sg;
+      HostRec* zrec = nullptr;
+      if (cudaMallocHost(&zrec, sizeof(HostRec) * 2 * ZG) != cudaSuccess) {
+        lane_rc[q] = DMQR_ECUDA;
+        cudaEventRecord(done[q], ls[q]);
+        return;
+      }
+      for (int64_t g0 = (int64_t)q * ZG; g0 < batch; g0 += (int64_t)nlanes * ZG) {
+        const int g = (int)std::min<int64_t>(ZG, batch - g0);
         int r = 0;
-        if (cudaMemcpyAsync(Aw, A + b * stride, abytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess) r = DMQR_ECUDA;
+        auto cp2 = [&](void* dst, size_t dp, const void* src, size_t sp, size_t w) {
+          if (r) return;
+          const cudaError_t e = cudaMemcpy2DAsync(dst, dp, src, sp, w, (size_t)g, cudaMemcpyDeviceToDevice, s);
+          if (e != cudaSuccess) {
+            last_cuda_error() = e;
+            r = DMQR_ECUDA;
+            if (getenv("DMQR_DEBUG_BATCH"))
+              fprintf(stderr, "[dmqr] batch copy failed: %s (dp %zu sp %zu w %zu h %d)\n", cudaGetErrorString(e), dp,
+                      sp, w, g);
+          }
+        };
+        cp2(zb + lb.a, zblk, A + g0 * stride, sizeof(double) * stride, abytes);
         if (!r)
-          r = run_engine(Aw, m, n, lda, p, cw, pw, sw, lb.swap_cap, tw, lb.step_cap, nullptr, ws, per_engine,
-                         &infos[b], nullptr, 0, (void*)s, 0, &sg);
-        if (!r && infos[b].n_swaps > swap_cap) r = DMQR_ECAP;
-        if (!r) {
-          const int64_t nsw = infos[b].n_swaps, nst = infos[b].n_steps;
-          bool ok = cudaMemcpyAsync(A + b * stride, Aw, abytes, cudaMemcpyDeviceToDevice, s) == cudaSuccess;
-          ok = ok && cudaMemcpyAsync(coeffs + b * kmax, cw, sizeof(double) * kmax, cudaMemcpyDeviceToDevice, s) ==
-                         cudaSuccess;
-          ok = ok && cudaMemcpyAsync(perm + b * n, pw, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, s) == cudaSuccess;
-          if (nsw > 0)
-            ok = ok && cudaMemcpyAsync(swaps + b * 2 * swap_cap, sw, sizeof(int64_t) * 2 * nsw,
-                                       cudaMemcpyDeviceToDevice, s) == cudaSuccess;
-          if (nst > 0)
-            ok = ok && cudaMemcpyAsync(steps + b * step_cap, tw, sizeof(dmqr_step) * nst, cudaMemcpyDeviceToDevice,
-                                       s) == cudaSuccess;
-          if (!ok) r = DMQR_ECUDA;
-        }
-        infos[b].status = r;
+          r = run_engine((double*)(zb + lb.a), m, n, lda, p, (double*)(zb + lb.coeffs),
+                         (int64_t*)(zb + lb.perm), (int64_t*)(zb + lb.swaps), lb.swap_cap,
+                         (dmqr_step*)(zb + lb.steps), lb.step_cap, nullptr, zbase, per_engine, &infos[g0], nullptr,
+                         0, (void*)s, 0, &sg, g, (int64_t)zblk, zrec);
+        for (int z = 0; z < g && !r; ++z)
+          if (infos[g0 + z].n_swaps > swap_cap) r = DMQR_ECAP;
+        cp2(A + g0 * stride, sizeof(double) * stride, zb + lb.a, zblk, abytes);
+        cp2(coeffs + g0 * kmax, sizeof(double) * kmax, zb + lb.coeffs, zblk, sizeof(double) * kmax);
+        cp2(perm + g0 * n, sizeof(int64_t) * n, zb + lb.perm, zblk, sizeof(int64_t) * n);
+        cp2(swaps + g0 * 2 * swap_cap, sizeof(int64_t) * 2 * swap_cap, zb + lb.swaps, zblk,
+            sizeof(int64_t) * 2 * swap_cap);
+        cp2(steps + g0 * step_cap, sizeof(dmqr_step) * step_cap, zb + lb.steps, zblk,
+            sizeof(dmqr_step) * step_cap);
+        for (int z = 0; z < g; ++z)
+          if (r || !infos[g0 + z].status) infos[g0 + z].status = r ? r : infos[g0 + z].status;
         if (r && !lane_rc[q]) lane_rc[q] = r;
       }
-      cudaStreamSynchronize(s);  // (the graph exec is destroyed with sg)
+      cudaStreamSynchronize(s);  // (the graph exec and the records are released below)
+      cudaFreeHost(zrec);
     }
     cudaEventRecord(done[q], ls[q]);
   };

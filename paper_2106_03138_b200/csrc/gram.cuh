@@ -148,6 +148,7 @@ __device__ __forceinline__ void tile_ij(int t, int nt, int& ti, int& tj) {
 __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __restrict__ A,
                                                  double* __restrict__ part, const double* __restrict__ Wt,
                                                  int64_t ldz, const uint8_t* __restrict__ upd) {
+  zshift(c, A, part, Wt, upd);
   pdl_enter();
   const CtlSnap S = snap(c);
   TLSpan tl_span(S.step_idx, 1);
@@ -323,6 +324,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
                                                         const double* __restrict__ part, int G,
                                                         double* __restrict__ gfin, uint8_t* __restrict__ upd,
                                                         long long* __restrict__ tline) {
+  zshift(c, A, part, gfin, upd);
   const long long t_in = gtimer();
   pdl_enter();
   const CtlSnap S = snap(c);

@@ -24,6 +24,7 @@ struct InitArgs {
 };
 
 __global__ void __launch_bounds__(1024) k_init(InitArgs a) {
+  zshift(a.c, a.u, a.perm, a.coeffs, a.nonfinite);
   __shared__ double red[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   double mx = 0.0;
@@ -123,6 +124,8 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
                            double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
                            double* __restrict__ uref, uint8_t* __restrict__ upd, HostRec* __restrict__ hrec,
                            int enq) {
+  zshift(c, steps, norm_trace, trace_bits, A, Wt, u, uref, upd);
+  if (gridDim.z > 1 && hrec) hrec += 2 * blockIdx.z;  // (host records: two slots per matrix)
   pdl_enter();
   const CtlSnap S = snap(c);
   TLSpan tl_span(S.step_idx, 10);
@@ -157,6 +160,7 @@ __global__ void k_set_la(Ctl* __restrict__ c, int on) {
 
 // rank / n_factored (rrqr.py:406-412)
 __global__ void k_finalize(Ctl* __restrict__ c, const double* __restrict__ A, int stop_none) {
+  zshift(c, A);
   __shared__ int cnt[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t n_s = c->n_s;

@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(SWAP_T) k_swap(Ctl* __restrict__ c, double* __
                                                  double* __restrict__ uref, int64_t* __restrict__ perm,
                                                  int64_t* __restrict__ swaplog, double* __restrict__ Wt, int64_t ldz,
                                                  uint8_t* __restrict__ upd) {
+  zshift(c, A, u, uref, perm, swaplog, Wt, upd);
   pdl_enter();
   const CtlSnap S = snap(c);
   TLSpan tl_span(S.step_idx, 3);

@@ -654,6 +654,7 @@ __device__ void cq_cluster_reduce(double* part, double* tot, int k) {
 }
 
 __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
+  zshift(a.c, a.A, a.coeffs, a.T, a.red, a.q1g, a.hpart, a.hR, a.hctr);
   // wait for the step's column swaps, then let the look-ahead grid behind this
   // one start (trailing.cuh: it runs beside the panel and must see the swaps)
   asm volatile("griddepcontrol.wait;" ::: "memory");

@@ -48,6 +48,7 @@ constexpr size_t RR_CL_SMEM = sizeof(double) * 2 * RR_MAXCL * RED_LD;  // receiv
 
 template <class Red>
 __global__ void __launch_bounds__(PANEL_T, 1) k_panel_rr(PanelArgs a) {
+  zshift(a.c, a.A, a.coeffs, a.T, a.red, a.q1g, a.hpart, a.hR, a.hctr);
   pdl_enter();
   Ctl* c = a.c;
   {

@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
                                                      int64_t ldz, double* __restrict__ u,
                                                      double* __restrict__ uref, uint8_t* __restrict__ upd,
                                                      int only_if_cq_fail, int32_t* __restrict__ glist) {
+  zshift(c, A, Zp, T, Wt, counters, u, uref, upd, glist);
   pdl_enter();
   const CtlSnap S = snap(c);
   TLSpan tl_span(S.step_idx, 8);
@@ -439,6 +440,7 @@ template <bool LA>
 __global__ void __launch_bounds__(TB_T, 2) k_trail_b(Ctl* __restrict__ c, double* __restrict__ A,
                                                      const double* __restrict__ Wt, int64_t ldz,
                                                      uint8_t* __restrict__ upd, unsigned* __restrict__ counter) {
+  zshift(c, A, Wt, upd, counter);
   pdl_enter();
   const CtlSnap S = snap(c);
   TLSpan tl_span(S.step_idx, 11);

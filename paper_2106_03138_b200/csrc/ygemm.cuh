@@ -61,6 +61,7 @@ __device__ __forceinline__ void ygemm_tile(double* __restrict__ A, const double*
 
 __global__ void __launch_bounds__(256) k_ygemm(Ctl* __restrict__ c, double* __restrict__ A,
                                                const double* __restrict__ q1g, const double* __restrict__ gM) {
+  zshift(c, A, q1g, gM);
   pdl_enter();
   const CtlSnap S = snap(c);
   TLSpan tl_span(S.step_idx, 6);
