@@ -474,7 +474,7 @@ def main():
     ap.add_argument("--no-extra", action="store_true", help="skip the cfg4 / cfg5 / qrp information block")
     ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3"])
     ap.add_argument("--batch", type=int, default=1024)
-    ap.add_argument("--lanes", type=int, default=8)
+    ap.add_argument("--lanes", type=int, default=4)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     world = int(os.environ.get("WORLD_SIZE", "1"))

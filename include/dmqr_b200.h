@@ -149,6 +149,10 @@ int dmqr_qrp_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr
  * Returns the first non-zero per-matrix status (all matrices are attempted).
  */
 size_t dmqr_batched_workspace_bytes(int64_t m, int64_t n, const dmqr_params* params, int32_t nlanes);
+/* Matrices a lane factors per launch (grid.z groups of small matrices; 1 when
+ * m x n is too large to batch).  Lanes beyond ceil(batch / group) stay idle, so
+ * callers size the workspace for min(nlanes, ceil(batch / group)) lanes. */
+int32_t dmqr_batched_group(int64_t m, int64_t n);
 int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_t lda, int64_t stride,
                           const dmqr_params* params, double* coeffs, int64_t* perm, int64_t* swaps,
                           int64_t swap_cap, dmqr_step* steps, int64_t step_cap, dmqr_info* infos,

@@ -20,6 +20,7 @@ EXPORTS = (
     "dmqr_qrp_stream_f64",
     "dmqr_qrdm_batched_f64",
     "dmqr_batched_workspace_bytes",
+    "dmqr_batched_group",
     "dmqr_form_q_f64",
     "dmqr_form_q_workspace_bytes",
     "dmqr_check_finite_f64",
@@ -121,6 +122,8 @@ def load() -> C.CDLL:
     lib.dmqr_qrdm_batched_f64.restype = C.c_int
     lib.dmqr_batched_workspace_bytes.argtypes = [I64, I64, C.POINTER(Params), I32]
     lib.dmqr_batched_workspace_bytes.restype = SZ
+    lib.dmqr_batched_group.argtypes = [I64, I64]
+    lib.dmqr_batched_group.restype = I32
     lib.dmqr_form_q_f64.argtypes = [P, I64, I64, I64, P, I64, P, I64, I64, P, SZ, VP]
     lib.dmqr_form_q_f64.restype = C.c_int
     lib.dmqr_form_q_workspace_bytes.argtypes = [I64, I64]

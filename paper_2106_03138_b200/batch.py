@@ -109,7 +109,8 @@ def factorize_batch(A, params: DMParams = DMParams(), stop: StopCriterion = Stop
     swaps = torch.empty((b, swap_cap, 2), dtype=torch.int64, device=dev)
     steps = torch.empty((b, step_cap * _lib.STEP_BYTES), dtype=torch.uint8, device=dev)
     infos = (_lib.Info * max(b, 1))()
-    lanes = max(1, min(int(lanes), max(b, 1)))
+    group = max(1, int(lib.dmqr_batched_group(m, n)))  # matrices per lane launch (grid.z)
+    lanes = max(1, min(int(lanes), max(b, 1), -(-max(b, 1) // group)))
     wsb = int(lib.dmqr_batched_workspace_bytes(m, n, C.byref(p), lanes))
     ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=dev)
     sh = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)

@@ -1023,11 +1023,13 @@ LaneBufs lane_bufs(int64_t m, int64_t n, int64_t lda) {
   return b;
 }
 bool batch_graph_ok(int64_t m, int64_t n) { return m * n < ((int64_t)1 << 20); }
-constexpr int ZG = 32;  // small matrices per batched launch (grid.z)
+constexpr int ZG = 128;  // small matrices per batched launch (grid.z)
 std::mutex g_zstride_mu;  // g_zstride is process-wide: one batched call at a time
 }  // namespace
 
 extern "C" {
+
+int32_t dmqr_batched_group(int64_t m, int64_t n) { return batch_graph_ok(m, n) ? ZG : 1; }
 
 size_t dmqr_batched_workspace_bytes(int64_t m, int64_t n, const dmqr_params* params, int32_t nlanes) {
   const size_t eng = al(dmqr_workspace_bytes(m, n, params));
