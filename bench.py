@@ -242,6 +242,24 @@ def other_configs(torch, dev, peak_tf):
                                       "peak plus one HBM read of the trailing block per scalar-pivot column"}
         del work, b0, f
         torch.cuda.empty_cache()
+    # cfg3: the batch of 1024 independent 256 x 256 matrices (bench.py --config cfg3 times it alone)
+    from paper_2106_03138_b200.batch import factorize_batch, to_batch_work
+
+    w0 = to_batch_work(inputs.cfg3(seed=3, batch=1024), dev)
+    wb = w0[0].clone()
+    best = 1e30
+    for _ in range(3):
+        wb.copy_(w0[0])
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        factorize_batch(None, lanes=4, work=(wb, w0[1], w0[2], w0[3]))
+        e1.record()
+        torch.cuda.synchronize(dev)
+        best = min(best, e0.elapsed_time(e1))
+    out["cfg3"] = {"algo": "qrdm2", "batch": 1024, "m": 256, "n": 256, "ms": best,
+                   "matrices_per_s": 1024 / (best / 1e3), "gflops_nominal": 1024 * nominal(256, 256) / (best / 1e3) / 1e9}
+    del w0, wb
+    torch.cuda.empty_cache()
     return out
 
 
