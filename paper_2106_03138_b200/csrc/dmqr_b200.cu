@@ -144,7 +144,6 @@ int set_attrs(const DevInfo& d) {
   CK(cudaFuncSetAttribute(k_guard, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GU_SMEM));
   CK(cudaFuncSetAttribute(k_ygemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YG_SMEM));
   CK(cudaFuncSetAttribute(k_trail_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TP_SMEM));
-  CK(cudaFuncSetAttribute(k_trail_bq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TQ_SMEM));
   CK(cudaFuncSetAttribute(k_qp3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QP_SMEM));
   CK(cudaFuncSetAttribute(k_panel_helper, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CQH_SMEM));
   CK(cudaFuncSetAttribute(k_fq_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FQ_SMEM2));
@@ -426,7 +425,6 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     CK(cudaMemcpyToSymbolAsync(g_tl_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
   }
   const bool trail_persistent = getenv("DMQR_TRAIL_PERSISTENT") != nullptr;  // A/B switch
-  const bool trail_stream = getenv("DMQR_TRAIL_STREAM") != nullptr;          // A/B switch (k_trail_bq: slower so far)
   const bool spare_all = getenv("DMQR_SPARE_FREE_ONLY") == nullptr;          // A/B switch
   const bool no_helpers = getenv("DMQR_NO_HELPERS") != nullptr;               // A/B switch
   // (test hook: DMQR_HELPER_WAIT_NS=0 makes the tall panel abandon its helpers)
@@ -647,11 +645,6 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
       NOTE_LAUNCH();
       if (la) {
         // the rest of C -= Y Wt runs beside the next step's panel
-      } else if (trail_stream) {
-        // streaming persistent form (one CTA per SM, next tile's C in registers)
-        const int64_t work = ceil_div(mp + 1, TQ_ROWS) * ceil_div(ncols_ub, TQ_COLS);
-        k_trail_bq<<<(unsigned)std::min<int64_t>(work, d.sms), TQ_T, TQ_SMEM, st>>>(ctl, A, Z, ldz);
-        NOTE_LAUNCH();
       } else if (!trail_persistent) {
         k_trail_b<false><<<dim3((unsigned)ceil_div(mp + 1, TB_ROWS), (unsigned)ceil_div(ncols_ub, TB_COLS), NZ), TB_T,
                            TB_SMEM, st>>>(ctl, A, Z, ldz, upd, lacount + 1);
@@ -1077,6 +1070,7 @@ int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_
   CK(cudaEventRecord(start, st));
   const int64_t kmax = std::min(m, n);
   std::vector<int> lane_rc(nlanes, 0);
+  std::vector<cudaError_t> lane_err(nlanes, cudaSuccess);  // (last_cuda_error is per thread)
   std::vector<cudaStream_t> ls(nlanes);
   std::vector<cudaEvent_t> done(nlanes);
   for (int q = 0; q < nlanes; ++q) {
@@ -1146,6 +1140,7 @@ int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_
       cudaStreamSynchronize(s);  // (the graph exec and the records are released below)
       cudaFreeHost(zrec);
     }
+    lane_err[q] = last_cuda_error();
     cudaEventRecord(done[q], ls[q]);
   };
   std::vector<std::thread> th;
@@ -1159,7 +1154,10 @@ int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_
   }
   cudaEventDestroy(start);
   for (int q = 0; q < nlanes; ++q)
-    if (lane_rc[q]) return lane_rc[q];
+    if (lane_rc[q]) {
+      if (lane_rc[q] == DMQR_ECUDA) last_cuda_error() = lane_err[q];
+      return lane_rc[q];
+    }
   return 0;
 }
 

@@ -1172,155 +1172,4 @@ __global__ void __launch_bounds__(TP_T, 1) k_trail_bp(const Ctl* __restrict__ c,
 }
 
 
-// ---------------------------------------------------------------------------
-// Serial-schedule C -= Y Wt, persistent and streaming: one 512-thread CTA per
-// SM walks a contiguous range of (128-row block, 64-column tile) items.  The
-// C tile lives in registers (16 doubles a thread); the NEXT item's C tile is
-// loaded into a second register set while the current one runs on the DMMA
-// pipe, so every SM keeps a whole tile (64 KB) of HBM reads in flight
-// continuously (the 2-CTA form loads, then computes, then stores: ~50% of the
-// HBM bandwidth on tall/large trailing blocks, where the update is
-// bandwidth-bound at K = l <= 65).  Y (per row block) and Wt (per item,
-// double-buffered) are staged in shared memory with cp.async.
-// Warps 4 (32 rows) x 4 (16 columns); the DMMA sequence per element is
-// k_trail_b's (acc = C, += (-Y) Wt in ascending k groups).
-// ---------------------------------------------------------------------------
-constexpr int TQ_T = 512;
-constexpr int TQ_ROWS = 128;
-constexpr int TQ_COLS = 64;
-constexpr int TQ_VLD = TQ_ROWS + 4;   // 132 (4 mod 16)
-constexpr int TQ_ZLD = TQ_COLS + 4;   // 68  (4 mod 16)
-constexpr size_t TQ_SMEM = sizeof(double) * (TB_KMAX * TQ_VLD + 2 * TB_KMAX * TQ_ZLD);  // 143 KB
-
-__global__ void __launch_bounds__(TQ_T, 1) k_trail_bq(const Ctl* __restrict__ c, double* __restrict__ A,
-                                                      const double* __restrict__ Wt, int64_t ldz) {
-  if (c->done) return;
-  const int64_t n_s = c->n_s, m = c->m, n = c->n, lda = c->lda;
-  const int l = c->l_acc;
-  const int64_t c0 = c->tc0, ncols = n - c0, mp = m - n_s;
-  if (l == 0 || ncols <= 0) return;
-  const int odd = (int)(n_s & 1);
-  const int64_t nrb = ceil_div(mp + odd, TQ_ROWS), ntc = ceil_div(ncols, TQ_COLS);
-  const int64_t total = nrb * ntc;
-  const int64_t it0 = (int64_t)blockIdx.x * total / gridDim.x, it1 = (int64_t)(blockIdx.x + 1) * total / gridDim.x;
-  if (it0 >= it1) return;
-  const int lp4 = (l + 3) / 4 * 4;
-  extern __shared__ __align__(16) double tqs[];
-  double* vs = tqs;                                                 // [68][132] Y[r][t]
-  double* zsb[2] = {vs + TB_KMAX * TQ_VLD, vs + TB_KMAX * TQ_VLD + TB_KMAX * TQ_ZLD};  // [68][68] Wt
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int wm = wid & 3, wn = wid >> 2;
-  const double* Yp = A + n_s * lda + n_s;
-  double* Cp = A + n_s + c0 * lda;
-
-  auto load_y = [&](int64_t rbk) {
-    const int64_t row0 = rbk * TQ_ROWS - odd;
-    const int rp = tid & 63, tb = tid >> 6;  // 64 row pairs x 8 lanes
-    const int64_t r = row0 + 2 * rp;
-    const int64_t gr = n_s + r;
-    const int bytes = (gr + 1 < m) ? 16 : ((gr < m) ? 8 : 0);
-    for (int t = tb; t < l; t += 8) cp_async16(vs + t * TQ_VLD + 2 * rp, Yp + r + (int64_t)t * lda, bytes);
-  };
-  auto fix_y = [&](int64_t rbk) {  // Y structure (unit diagonal, zeros above / outside), padding rows
-    const int64_t row0 = rbk * TQ_ROWS - odd;
-    if (row0 < 72 || row0 + TQ_ROWS > mp)
-      for (int e = tid; e < l * TQ_ROWS; e += TQ_T) {
-        const int t = e >> 7, rr = e & 127;
-        const int64_t r = row0 + rr;
-        if (r < 0 || r >= mp || r <= t) vs[t * TQ_VLD + rr] = (r == t) ? 1.0 : 0.0;
-      }
-    for (int e = tid; e < (lp4 - l) * TQ_ROWS; e += TQ_T) vs[(l + e / TQ_ROWS) * TQ_VLD + e % TQ_ROWS] = 0.0;
-  };
-  auto load_wt = [&](int64_t it, int buf) {
-    const int64_t col0 = (it % ntc) * TQ_COLS;
-    const int cp2 = tid & 31, tz = tid >> 5;  // 32 column pairs x 16 row lanes
-    for (int t = tz; t < l; t += 16)
-      cp_async16(zsb[buf] + t * TQ_ZLD + 2 * cp2, Wt + (int64_t)t * ldz + col0 + 2 * cp2, 16);
-  };
-  // this thread's C fragments of item it: rows wm*32 + mt*8 + lane/4, columns wn*16 + nt*8 + 2 (lane&3) + {0,1}
-  auto load_c = [&](int64_t it, double (*d)[2][2]) {
-    const int64_t row0 = (it / ntc) * TQ_ROWS - odd, col0 = (it % ntc) * TQ_COLS;
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      const int64_t r = row0 + wm * 32 + mt * 8 + (lane >> 2);
-      const bool rv = r >= 0 && r < mp;
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const int64_t cc = col0 + wn * 16 + nt * 8 + 2 * (lane & 3);
-        const double* p = Cp + r + cc * lda;
-        d[mt][nt][0] = (rv && cc < ncols) ? p[0] : 0.0;
-        d[mt][nt][1] = (rv && cc + 1 < ncols) ? p[lda] : 0.0;
-      }
-    }
-  };
-  double acc[4][2][2], nxt[4][2][2];
-  int64_t cur_rb = it0 / ntc;
-  load_y(cur_rb);
-  load_wt(it0, 0);
-  cp_async_commit();
-  load_c(it0, nxt);
-  for (int64_t it = it0; it < it1; ++it) {
-    const int buf = (int)((it - it0) & 1);
-    const int64_t rbk = it / ntc;
-    const bool more = it + 1 < it1;
-    const bool next_same_rb = more && ((it + 1) / ntc == rbk);
-    if (next_same_rb) {  // the next item's Wt behind this one
-      load_wt(it + 1, buf ^ 1);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    if (it == it0 || rbk != cur_rb) {
-      cur_rb = rbk;
-      fix_y(rbk);
-    }
-    double* zs = zsb[buf];
-    for (int e = tid; e < (lp4 - l) * TQ_COLS; e += TQ_T) zs[(l + e / TQ_COLS) * TQ_ZLD + e % TQ_COLS] = 0.0;
-    __syncthreads();
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        acc[mt][nt][0] = nxt[mt][nt][0];
-        acc[mt][nt][1] = nxt[mt][nt][1];
-      }
-    if (more) load_c(it + 1, nxt);  // in flight while this tile runs on the DMMA pipe
-    for (int ks = 0; ks < lp4; ks += 4) {
-      const int t = ks + (lane & 3);
-      double af[4], bf[2];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) af[mt] = -vs[t * TQ_VLD + wm * 32 + mt * 8 + (lane >> 2)];
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) bf[nt] = zs[t * TQ_ZLD + wn * 16 + nt * 8 + (lane >> 2)];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
-    }
-    {
-      const int64_t row0 = rbk * TQ_ROWS - odd, col0 = (it % ntc) * TQ_COLS;
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const int64_t r = row0 + wm * 32 + mt * 8 + (lane >> 2);
-        if (r < 0 || r >= mp) continue;
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          const int64_t cc = col0 + wn * 16 + nt * 8 + 2 * (lane & 3);
-          double* pp = Cp + r + cc * lda;
-          if (cc < ncols) pp[0] = acc[mt][nt][0];
-          if (cc + 1 < ncols) pp[lda] = acc[mt][nt][1];
-        }
-      }
-    }
-    __syncthreads();  // (Y and this Wt buffer are reloaded behind this point)
-    if (more && !next_same_rb) {  // new row block: its Y and Wt
-      load_y((it + 1) / ntc);
-      load_wt(it + 1, buf ^ 1);
-      cp_async_commit();
-    }
-  }
-}
-
 }  // namespace dmqr
