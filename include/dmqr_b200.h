@@ -141,8 +141,12 @@ int dmqr_qrp_stream_f64(double* A, int64_t m, int64_t n, int64_t lda, const dmqr
 /*
  * Batched QRDM / QRDM2 over `batch` independent m x n matrices stored at
  * A + b*stride (cfg3: batches of small matrices).  The batch is spread over
- * `nlanes` concurrent CUDA streams (one host thread each, every lane running
- * the same device-resident engine as dmqr_qrdm_f64), joined back to `stream`.
+ * `nlanes` concurrent CUDA streams (one host thread each), joined back to
+ * `stream`.  Small matrices (m*n < 2^20, lda = round_up(m, 8)) are factored
+ * dmqr_batched_group(m, n) at a time per lane: every kernel of an outer step
+ * is launched once for the group (grid.z), on per-matrix copies in the
+ * workspace, and the step is replayed as a CUDA graph; larger matrices run
+ * the single-matrix engine (dmqr_qrdm_f64) on each lane.
  * Per-matrix outputs are strided: coeffs + b*min(m,n), perm + b*n,
  * swaps + b*2*swap_cap, steps + b*step_cap (device); infos[b] (HOST).
  * workspace >= dmqr_batched_workspace_bytes(m, n, params, nlanes).
