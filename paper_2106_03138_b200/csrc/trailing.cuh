@@ -612,12 +612,16 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
   const int podd = (int)(pns & 1);
   const int ntx = (int)ceil_div(pmp + 1, TB_ROWS);
   const int ntb = (pend && pncols > 0 && pl > 0) ? ntx * (int)ceil_div(pncols, TB_COLS) : 0;
+  // (the next item's index is fetched while the current tile runs: the
+  // counter's L2 round trip is off the per-item path)
+  __shared__ int s_next;
+  if (tid == 0) s_next = (ntb > 0) ? (int)atomicAdd(&ctr[0], 1u) : ntb;
   for (;;) {
-    if (tid == 0) s_item = (int)atomicAdd(&ctr[0], 1u);
     __syncthreads();
-    const int it = s_item;
+    const int it = s_next;
     __syncthreads();
     if (it >= ntb) break;
+    if (tid == 0) s_next = (int)atomicAdd(&ctr[0], 1u);
     const int64_t row0 = (int64_t)(it % ntx) * TB_ROWS - podd, col0 = (int64_t)(it / ntx) * TB_COLS;
     if (!(row0 >= pmp || col0 >= pncols || row0 + TB_ROWS <= pl))
       trail_b_tile<true>(A, Wt, ldz, upd, pns, m, lda, pl, pc0, pncols, pmp, row0, col0);
