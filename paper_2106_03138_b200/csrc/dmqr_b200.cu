@@ -72,7 +72,7 @@ Layout layout(int64_t m, int64_t n) {
   L.Z = take(sizeof(double) * DMQR_KP * ldz_for(n));
   L.trace = take(sizeof(unsigned long long) * 4);
   L.pdbg = take(sizeof(long long) * 64 * 16);
-  L.tcount = take(sizeof(unsigned) * (ceil_div(std::max<int64_t>(n, 1), TA_COLS) + 1));
+  L.tcount = take(sizeof(unsigned) * 2 * (ceil_div(std::max<int64_t>(n, 1), TA_COLS) + 1));  // + k_spare's column counts
   L.upd = take(std::max<int64_t>(n, 1));                      // look-ahead column flags
   L.lacount = take(sizeof(unsigned) * 16);                    // look-ahead work / last-CTA counters
   L.q1g = take(sizeof(double) * DMQR_KP * q1_ld(m));  // published Q1 (k_spare)
@@ -368,7 +368,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   CK(zmemset(tbits, sizeof(unsigned long long) * 4));
   int32_t* nonfinite = (int32_t*)(tbits + 2);
   CK(zmemset(T, sizeof(double) * DMQR_KP * DMQR_KP));
-  CK(zmemset(tcount, sizeof(unsigned) * (ceil_div(std::max<int64_t>(n, 1), TA_COLS) + 1)));
+  CK(zmemset(tcount, sizeof(unsigned) * 2 * (ceil_div(std::max<int64_t>(n, 1), TA_COLS) + 1)));
   CK(zmemset(upd, (size_t)std::max<int64_t>(n, 1)));
   CK(zmemset(lacount, sizeof(unsigned) * 16));
   if (n > 0) {

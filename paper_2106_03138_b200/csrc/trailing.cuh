@@ -589,6 +589,7 @@ __device__ void g_partial(const double* __restrict__ A, const double* __restrict
 }
 
 constexpr size_t SP_SMEM = TB_SMEM > TA_SMEM ? TB_SMEM : TA_SMEM;
+static_assert(TA_COLS == TB_COLS, "k_spare: a phase-2 column tile is a phase-1 column tile");
 static_assert(YG_SMEM <= SP_SMEM, "k_spare runs the Y = Q1 M tiles in its dynamic shared memory");
 constexpr int NSPLIT_MAXG = 16;
 
@@ -609,6 +610,9 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
   const int64_t pns = S.pend_ns;
   const int pl = S.pend_l;
   const int64_t pc0 = pns + pl, pmp = m - pns, pncols = n - pc0;
+  // per 64-column tile: phase-1 tiles done (after the split counters in tcnt)
+  const int64_t ncoltiles = ceil_div(max(n, (int64_t)1), TA_COLS) + 1;
+  unsigned* colcnt = tcnt + ncoltiles;
   const int podd = (int)(pns & 1);
   const int ntx = (int)ceil_div(pmp + 1, TB_ROWS);
   const int ntb = (pend && pncols > 0 && pl > 0) ? ntx * (int)ceil_div(pncols, TB_COLS) : 0;
@@ -628,6 +632,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
     __syncthreads();
     if (tid == 0) {
       __threadfence();
+      atomicAdd(&colcnt[it / ntx], 1u);  // (column tile it / ntx: phase 2's tile of the same columns)
       s_flag = (atomicAdd(&ctr[1], 1u) == (unsigned)ntb - 1);
       if (g_tl_on) atomicMax(&g_tl[(S.step_idx & 63) * 32 + 29], (unsigned long long)gtimer());  // phase 1 end
     }
@@ -637,10 +642,10 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
       if (tid == 0) c->pend = 0;
     }
   }
-  // ---- phase 2: G = Q1^T C once phase 1 is done and Q1 is published ----
+  // ---- phase 2: G = Q1^T C once Q1 is published; each tile once phase 1 has
+  // updated its columns (its column tile's counter), not the whole of phase 1 ----
   if (!S.done) {
     if (tid == 0) {
-      while (ld_acquire(&ctr[1]) < (unsigned)ntb) __nanosleep(200);
       while (ld_acquire(&c->q1_count) < (unsigned)P) __nanosleep(200);
       s_flag = !c->q1_fail;
       if (g_tl_on) atomicMin(&g_tl[(S.step_idx & 63) * 32 + 28], (unsigned long long)gtimer());  // Q1 seen
@@ -673,6 +678,11 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
           ygemm_tile(A, Q1g, gM, n_s, m, lda, c->l_acc, -2 - it);
           __syncthreads();
           continue;
+        }
+        if (it < ng && ntb > 0) {  // the pending update of these columns must be complete
+          if (tid == 0)
+            while (ld_acquire(&colcnt[it % ntile]) < (unsigned)ntx) __nanosleep(100);
+          __syncthreads();
         }
         if (it >= ng) {
           if (tid == 0 && g_tl_on) atomicMax(&g_tl[(S.step_idx & 63) * 32 + 31], (unsigned long long)gtimer());
@@ -740,6 +750,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
   }
   __syncthreads();
   if (s_flag) {
+    for (int64_t q = tid; q < ncoltiles; q += blockDim.x) colcnt[q] = 0u;
     if (tid == 0) {
       ctr[0] = ctr[1] = ctr[2] = ctr[3] = ctr[4] = 0u;
       if (tline) {
