@@ -799,24 +799,36 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* __restrict__ c, double* _
   const int cb = wid & 3, q0 = (wid >> 2) * 5, q1 = min(q0 + 5, lt);
   const double* gFT = FM;
   const double* gMT = FM + DMQR_KP * DMQR_KP;
-  // (unrolled so the L2 loads of several iterations are in flight together)
-#pragma unroll 9
+  // every operand staged with cp.async: all of the tile's L2 / HBM reads are in
+  // flight at once (one round trip), zeros stored directly
   for (int e = tid; e < DMQR_KP * TW_COLS; e += TA_T) {
     const int t = e / TW_COLS, c2 = e % TW_COLS;
     const int64_t col = col0 + c2;
-    const bool in = t < l && col < ncols;
-    gs[t * TW_CLD + c2] = in ? __ldcg(Gp + (int64_t)t * ldz + l + col) : 0.0;  // G columns from n_s
-    cts[t * TW_CLD + c2] = in ? A[(n_s + t) + (c0 + col) * lda] : 0.0;
+    if (t < l && col < ncols) {
+      cp_async8(gs + t * TW_CLD + c2, Gp + (int64_t)t * ldz + l + col);  // G columns from n_s
+      cp_async8(cts + t * TW_CLD + c2, A + (n_s + t) + (c0 + col) * lda);
+    } else {
+      gs[t * TW_CLD + c2] = 0.0;
+      cts[t * TW_CLD + c2] = 0.0;
+    }
   }
-#pragma unroll 6
   for (int e = tid; e < DMQR_KP * DMQR_KP; e += TA_T) {
     const int t = e / DMQR_KP, i = e % DMQR_KP;
-    const bool in = t < l && i < l;
-    a1[t * DMQR_KP + i] = in ? gFT[t * DMQR_KP + i] : 0.0;
-    a2[t * DMQR_KP + i] = in ? gMT[t * DMQR_KP + i] : 0.0;
+    if (t < l && i < l) {
+      cp_async8(a1 + t * DMQR_KP + i, gFT + t * DMQR_KP + i);
+      cp_async8(a2 + t * DMQR_KP + i, gMT + t * DMQR_KP + i);
+    } else {
+      a1[t * DMQR_KP + i] = 0.0;
+      a2[t * DMQR_KP + i] = 0.0;
+    }
     // Y1[i][t] from the packed panel (column n_s + t, row n_s + i): coalesced over i
-    y1[i * DMQR_KP + t] = in ? ((t < i) ? A[(n_s + t) * lda + n_s + i] : ((t == i) ? 1.0 : 0.0)) : 0.0;
+    if (t < i && i < l)
+      cp_async8(y1 + i * DMQR_KP + t, A + (n_s + t) * lda + n_s + i);
+    else
+      y1[i * DMQR_KP + t] = (t == i && i < l) ? 1.0 : 0.0;
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   const int lr = lane >> 2, lk = lane & 3;
   const int64_t cc = col0 + cb * 8 + 2 * lk;
