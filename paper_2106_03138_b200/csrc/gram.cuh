@@ -179,17 +179,22 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __
   const int plp4 = (pl + 3) / 4 * 4;
   double* ysl = gsm + 2 * DMQR_KP * GRAM_LD;
   double* wsm = gsm + 4 * DMQR_KP * GRAM_LD;
-  for (int q = tid; q < DMQR_KP; q += GRAM_T) {
-    s_cand[q] = (q < ncand) ? c->cand[q] : 0;
-    s_live[q] = (q < ncand) && pendu && !upd[c->cand[q]];
-  }
+  for (int q = tid; q < DMQR_KP; q += GRAM_T) s_cand[q] = (q < ncand) ? c->cand[q] : 0;
   __syncthreads();
-  if (pendu)  // Wt columns of the candidates (indexed from n_s = pending n_s + l)
-#pragma unroll 6
+  // the candidates' Wt columns (indexed from n_s = pending n_s + l) by cp.async,
+  // in flight with their upd flags and the first slab; columns whose update
+  // is already applied (upd) are zeroed once everything has landed
+  bool live = false;
+  if (tid < DMQR_KP) live = (tid < ncand) && pendu && !upd[s_cand[tid]];
+  if (pendu)
     for (int e = tid; e < plp4 * DMQR_KP; e += GRAM_T) {
       const int t = e / DMQR_KP, q = e % DMQR_KP;
-      wsm[t * DMQR_KP + q] = (t < pl && s_live[q]) ? Wt[t * ldz + (s_cand[q] - n_s)] : 0.0;
+      if (t < pl && q < ncand)
+        cp_async8(wsm + t * DMQR_KP + q, Wt + t * ldz + (s_cand[q] - n_s));
+      else
+        wsm[t * DMQR_KP + q] = 0.0;
     }
+  if (tid < DMQR_KP) s_live[tid] = live;
 
   const int64_t rpc = ceil_div(ceil_div(mp, (int64_t)gridDim.x), GRAM_ROWS) * GRAM_ROWS;
   const int64_t r_begin = (int64_t)blockIdx.x * rpc;
@@ -238,7 +243,12 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __
     }
     cp_async_commit();
   };
-  if (nslab > 0) issue(0);
+  if (nslab > 0) {
+    issue(0);
+  } else {  // (no rows here: drain the Wt copies)
+    cp_async_commit();
+    cp_async_wait<0>();
+  }
   for (int sl = 0; sl < nslab; ++sl) {
     if (sl + 1 < nslab) {
       issue(sl + 1);
@@ -247,6 +257,11 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __
       cp_async_wait<0>();
     }
     __syncthreads();
+    if (sl == 0 && pendu) {  // (the Wt copies landed with slab 0)
+      for (int e = tid; e < plp4 * DMQR_KP; e += GRAM_T)
+        if (!s_live[e % DMQR_KP]) wsm[e] = 0.0;
+      __syncthreads();
+    }
     double* buf = gsm + (sl & 1) * DMQR_KP * GRAM_LD;
     if (pendu) {
       // buf[col][row] += (-Y) Wt for live candidates: warp w owns rows
