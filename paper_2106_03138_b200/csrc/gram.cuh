@@ -398,12 +398,12 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
     sm.bad = 0;
     sm.zero = 0;
   }
-#pragma unroll 4
-  for (int e = tid; e < DMQR_KP * DMQR_KP; e += GRAM_T) {
-    const int i = e / DMQR_KP, j = e % DMQR_KP;
-    if (j >= i && j < ncand) sm.g[e] = __ldcg(gfin + e);
-  }
+  // the whole reduced Gram in one round trip (16-byte L2 copies; only the
+  // upper entries of the first ncand rows / columns are read)
+  for (int e2 = tid; e2 < DMQR_KP * DMQR_KP / 2; e2 += GRAM_T) cp_async16(sm.g + 2 * e2, gfin + 2 * e2, 16);
+  cp_async_commit();
   for (int q = tid; q < ncand; q += GRAM_T) sm.cand[q] = c->cand[q];
+  cp_async_wait<0>();
   __syncthreads();
   // over/underflow risk: the diagonal (sums of squares) bounds every entry
   for (int i = tid; i < ncand; i += GRAM_T) {

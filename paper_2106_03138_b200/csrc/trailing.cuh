@@ -24,11 +24,6 @@
 
 namespace dmqr {
 
-// 16-byte cp.async; src_bytes < 16 zero-fills the rest (src_bytes = 0: all zeros)
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
-}
 
 constexpr int TA_T = 256;       // 8 warps
 constexpr int TA_COLS = 64;     // output columns per CTA
