@@ -86,7 +86,8 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const dou
   // ---- first argmax over u[n_s:] (np.argmax semantics) ----
   double bv = -1.0;
   int bi = 0x7fffffff;
-  for (int i = s0; i < s1; ++i) {
+#pragma unroll 4
+  for (int i = s0; i < s1; ++i) {  // (unrolled: the loads of four elements in flight together)
     double v = u[i];
     if (v > bv) {
       bv = v;
