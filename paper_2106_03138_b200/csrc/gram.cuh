@@ -150,6 +150,8 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __
                                                  int64_t ldz, const uint8_t* __restrict__ upd) {
   zshift(c, A, part, Wt, upd);
   pdl_enter();
+  // the candidate list is read with the control block snapshot (one round trip)
+  const int cand_pre = (threadIdx.x < DMQR_KP) ? c->cand[threadIdx.x] : 0;
   const CtlSnap S = snap(c);
   TLSpan tl_span(S.step_idx, 1);
   if (S.done) return;
@@ -179,7 +181,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __
   const int plp4 = (pl + 3) / 4 * 4;
   double* ysl = gsm + 2 * DMQR_KP * GRAM_LD;
   double* wsm = gsm + 4 * DMQR_KP * GRAM_LD;
-  for (int q = tid; q < DMQR_KP; q += GRAM_T) s_cand[q] = (q < ncand) ? c->cand[q] : 0;
+  if (tid < DMQR_KP) s_cand[tid] = (tid < ncand) ? cand_pre : 0;
   __syncthreads();
   // the candidates' Wt columns (indexed from n_s = pending n_s + l) by cp.async,
   // in flight with their upd flags and the first slab; columns whose update

@@ -40,6 +40,14 @@ __global__ void __launch_bounds__(SWAP_T) k_swap(Ctl* __restrict__ c, double* __
                                                  uint8_t* __restrict__ upd) {
   zshift(c, A, u, uref, perm, swaplog, Wt, upd);
   pdl_enter();
+  // the move lists are read with the control block snapshot (one round trip)
+  __shared__ int s_src[SWAP_MAXMV], s_dst[SWAP_MAXMV];
+  const int tid = threadIdx.x;
+  int ms_src = 0, ms_dst = 0;
+  if (tid < SWAP_MAXMV) {
+    ms_src = c->mv_src[tid];
+    ms_dst = c->mv_dst[tid];
+  }
   const CtlSnap S = snap(c);
   TLSpan tl_span(S.step_idx, 3);
   if (S.done) return;
@@ -48,12 +56,10 @@ __global__ void __launch_bounds__(SWAP_T) k_swap(Ctl* __restrict__ c, double* __
   const bool wt = S.la && S.pend;
   const int64_t nrow = m + (wt ? S.pend_l : 0);
   const int64_t n_s = S.n_s;
-  const int tid = threadIdx.x;
-  __shared__ int s_src[SWAP_MAXMV], s_dst[SWAP_MAXMV];
   extern __shared__ __align__(16) double sws[];  // [move][row]
-  for (int q = tid; q < nmv; q += SWAP_T) {
-    s_src[q] = c->mv_src[q];
-    s_dst[q] = c->mv_dst[q];
+  if (tid < SWAP_MAXMV) {
+    s_src[tid] = ms_src;
+    s_dst[tid] = ms_dst;
   }
   __syncthreads();
   const int64_t r0 = (int64_t)blockIdx.x * SWAP_ROWS;
