@@ -55,7 +55,10 @@ struct Ctl {
   uint32_t q1_count;
   int32_t q1_fail, q1_kk;
   int32_t pend_done;  // k_guard finished the whole update of this step (nothing pending)
-  int32_t pad3;
+  // P-mode look-ahead: the panel's ranks copied P (p_k columns) into pg before
+  // factoring it; k_spare forms G = P^T C at once and k_trail_w folds R1^-T into MT
+  uint32_t p_count;
+  int32_t p_k, pad5;
   // blocked scalar pivoting (k_qp3): columns factored by the last launch and why it ended
   int32_t qp_cols, qp_exit;
   uint32_t m_pub;  // k_panel_cq: step_idx + 1 once M (Y = Q1 M) and l are final

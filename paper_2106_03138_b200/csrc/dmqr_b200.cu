@@ -42,7 +42,7 @@ constexpr int NSPLIT_MAX = 16;
 constexpr int PANEL_PMAX = 160;
 
 struct Layout {
-  size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, trace, pdbg, tcount, upd, lacount, q1g, glist;
+  size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, trace, pdbg, tcount, upd, lacount, q1g, pg, glist;
   size_t qvb, qwb, qpart, qgpart, qcnt, hpart, hR, hctr, gnp, total;
 };
 
@@ -65,7 +65,7 @@ Layout layout(int64_t m, int64_t n) {
   L.uref = take(sizeof(double) * std::max<int64_t>(n, 1));
   L.T = take(sizeof(double) * DMQR_KP * DMQR_KP);
   // panel all-reduce partials; the CholeskyQR2 panel also keeps R, Y1 and per-rank R = R2 R1 here
-  L.red = take(sizeof(double) * std::max<size_t>(2 * PANEL_PMAX * RED_LD, 38 * DMQR_KP * DMQR_KP));
+  L.red = take(sizeof(double) * std::max<size_t>(2 * PANEL_PMAX * RED_LD, 39 * DMQR_KP * DMQR_KP));
   L.gram = take(sizeof(double) * GRAM_GMAX * GRAM_PART);
   L.gfin = take(sizeof(double) * DMQR_KP * DMQR_KP);
   L.Zp = take(sizeof(double) * NSPLIT_MAX * DMQR_KP * ldz_for(n));
@@ -76,6 +76,7 @@ Layout layout(int64_t m, int64_t n) {
   L.upd = take(std::max<int64_t>(n, 1));                      // look-ahead column flags
   L.lacount = take(sizeof(unsigned) * 16);                    // look-ahead work / last-CTA counters
   L.q1g = take(sizeof(double) * DMQR_KP * q1_ld(m));  // published Q1 (k_spare)
+  L.pg = take(sizeof(double) * DMQR_KP * q1_ld(m));   // P copy (k_spare, P-mode look-ahead)
   L.glist = take(sizeof(int32_t) * std::max<int64_t>(n, 1));  // look-ahead / k_qp3 guard columns
   // blocked scalar pivoting (k_qp3; its F = Zp, its Wt = Z: both are free between steps)
   L.qvb = take(sizeof(double) * std::max<int64_t>(m, 1));
@@ -139,7 +140,8 @@ int set_attrs(const DevInfo& d) {
   CK(cudaFuncSetAttribute(k_gram_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FinSmem)));
   CK(cudaFuncSetAttribute(k_trail_b<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
   CK(cudaFuncSetAttribute(k_trail_b<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
-  CK(cudaFuncSetAttribute(k_spare, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SP_SMEM));
+  CK(cudaFuncSetAttribute(k_spare<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SP_SMEM));
+  CK(cudaFuncSetAttribute(k_spare<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SP_SMEM));
   CK(cudaFuncSetAttribute(k_trail_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TW_SMEM));
   CK(cudaFuncSetAttribute(k_guard, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GU_SMEM));
   CK(cudaFuncSetAttribute(k_ygemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YG_SMEM));
@@ -427,6 +429,9 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   const bool trail_persistent = getenv("DMQR_TRAIL_PERSISTENT") != nullptr;  // A/B switch
   const bool spare_all = getenv("DMQR_SPARE_FREE_ONLY") == nullptr;          // A/B switch
   const bool no_helpers = getenv("DMQR_NO_HELPERS") != nullptr;               // A/B switch
+  // P-mode look-ahead (G = R1^-T P^T C from the panel's start; panel_cq.cuh): correct, but on cfg2 the
+  // earlier G traffic slows the latency-bound panel more than it shortens k_spare (16.9 vs 16.6 ms), so opt-in
+  const bool pmode_on = getenv("DMQR_PMODE") != nullptr;
   // (test hook: DMQR_HELPER_WAIT_NS=0 makes the tall panel abandon its helpers)
   const long long hwait_ns = getenv("DMQR_HELPER_WAIT_NS") ? atoll(getenv("DMQR_HELPER_WAIT_NS")) : 5000000ll;
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
@@ -525,7 +530,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     PanelArgs pa{ctl, A, coeffs, T, red, use_smem, P,
                  (g_prof.load() >= 2 && steps_done == 2) ? pdbg : nullptr, std::max(0, g_prof.load() - 2), 0,
                  q1g, 0, tline, 0, (double*)(ws + L.hpart), (double*)(ws + L.hR), (unsigned*)(ws + L.hctr),
-                 hwait_ns};
+                 hwait_ns, pmode_on ? (double*)(ws + L.pg) : nullptr};
     void* kargs[] = {&pa};
     auto launch_cluster = [&](const void* fn, int ncta, unsigned threads, size_t dsm) -> cudaError_t {
       cudaLaunchConfig_t cfg = {};
@@ -602,9 +607,9 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
         cfg.attrs = at;
         cfg.numAttrs = 1;
         NOTE_LAUNCH();
-        CK(cudaLaunchKernelEx(&cfg, k_spare, ctl, A, (const double*)Z, ldz, upd, (const double*)q1g, Zp,
+        CK(cudaLaunchKernelEx(&cfg, pmode_on ? k_spare<true> : k_spare<false>, ctl, A, (const double*)Z, ldz, upd, (const double*)q1g, Zp,
                               lacount + 4, Pcq, nsplit_g, tcount, tline,
-                              (const double*)(red + 37 * DMQR_KP * DMQR_KP)));
+                              (const double*)(red + 37 * DMQR_KP * DMQR_KP), (const double*)(ws + L.pg)));
       }
     }
     if (cl_path) {

@@ -149,6 +149,7 @@ struct PanelArgs {
   unsigned* hctr;    // [0] G1 items, [1] G1 done, [2] Q1 items, [3] Q1 done, [4] R1^-1 published (step + 1),
                      // [6] / [7] pass 1 / 2 decision (2 use the partials, 1 abandoned)
   long long hwait_ns;  // how long rank 0 waits for the helpers before streaming its own rows
+  double* pg;          // look-ahead P-mode: copy of the panel columns P (q1g layout), or null
 };
 
 // deterministic all-reduce of `len` doubles across the grid; in: s_part (this

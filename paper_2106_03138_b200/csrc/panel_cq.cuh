@@ -654,7 +654,7 @@ __device__ void cq_cluster_reduce(double* part, double* tot, int k) {
 }
 
 __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
-  zshift(a.c, a.A, a.coeffs, a.T, a.red, a.q1g, a.hpart, a.hR, a.hctr);
+  zshift(a.c, a.A, a.coeffs, a.T, a.red, a.q1g, a.hpart, a.hR, a.hctr, a.pg);
   // wait for the step's column swaps, then let the look-ahead grid behind this
   // one start (trailing.cuh: it runs beside the panel and must see the swaps)
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -776,6 +776,10 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   // without the helpers' partials (no helpers, or abandoned) a helper-mode
   // panel streams its rows like a chunked one (the slice was never loaded)
   const bool chunked_eff = chunked || hmode;
+  // P-mode look-ahead (unchunked panels): G = Q1^T C = R1^-T (P^T C), so k_spare
+  // forms P^T C from the start of the panel and MT absorbs R1^-1 (MT' = R1^-1 MT)
+  const bool pmode = a.spare && a.pg != nullptr && !chunked_eff;
+  double* gR1i = a.red + 38 * DMQR_KP * DMQR_KP;  // R1^-1 (P-mode)
   if (a.helpers && !hmode) h_publish(true, 0);  // (nothing for the helpers' second pass)
   // ---- P0/P1: slice <- P (rows zero-padded to a multiple of 4), G = P^T P ----
   const bool h1 = hmode && h_decide(1, 6);  // (pass 1 abandoned: no helper runs pass 2 either)
@@ -784,6 +788,19 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     h_gather(A2);
   } else if (!chunked_eff) {
     load_chunk(gA, lda, 0, k);
+    if (pmode) {  // P rows -> pg: k_spare's G = P^T C starts now, not after Q1
+      if (trow < R) {
+        double* dp = a.pg + qodd + r0 + trow;
+#pragma unroll 4
+        for (int cc = tcol0; cc < k; cc += tcstep) dp[(int64_t)cc * ldq] = sl[cc * CQ_LDS + trow];
+      }
+      __syncthreads();
+      if (tid == 0) {
+        if (me == 0) c->p_k = k;
+        __threadfence();
+        atomicAdd(&c->p_count, 1u);
+      }
+    }
     CQT();
     cq_gram(sl, R4, k, A2);
   } else {
@@ -829,6 +846,13 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     // ---- P4/P5: Q1 = P R1^-1 (in place) ----
     cq_trinv_upper(A2, A1, kk);
     CQT();
+    if (pmode && me == min(2, nr - 1)) {  // (rank_MT below)
+      __syncthreads();
+      for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
+        const int i = e / DMQR_KP, j = e % DMQR_KP;
+        gR1i[e] = (i < kk && j < kk && j >= i) ? A1[e] : 0.0;
+      }
+    }
     // keep R1: transpose into the lower triangle of A2, diagonal in vD
     __syncthreads();
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
@@ -1000,7 +1024,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   // aux task: out = (-R2^-1 S) src^-1 for an upper triangular src (l x l, KP
   // row-major, possibly in rank 0's shared memory); r2i: R2^-1 (upper), sg: S;
   // scr: two KP x KP scratch blocks
-  auto aux = [&](const double* src, const double* r2i, const double* sg, double* scr, double* out) {
+  auto aux = [&](const double* src, const double* r2i, const double* sg, double* scr, double* out, bool r1pre) {
     double* P = scr;
     double* X = scr + DMQR_KP * DMQR_KP;
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
@@ -1013,6 +1037,13 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
     cq_small_gemm([&](int i, int t) { return -sg[t] * r2i[i * DMQR_KP + t]; },
                   [&](int t, int j) { return X[t * DMQR_KP + j]; }, P, l);
     __syncthreads();
+    if (r1pre) {  // P-mode: R1^-1 (this rank stored it) times MT
+      cq_small_gemm([&](int i, int t) { return gR1i[i * DMQR_KP + t]; },
+                    [&](int t, int j) { return P[t * DMQR_KP + j]; }, X, l);
+      __syncthreads();
+      for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) P[e] = X[e];
+      __syncthreads();
+    }
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
       const int i = e / DMQR_KP, j = e % DMQR_KP;
       out[e] = (i < l && j < l && j >= i) ? P[e] : 0.0;
@@ -1099,8 +1130,8 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   }
   // rank_M / rank_MT: the inverses of rank 0's U and Y1^T, times -R2^-1 S
   const bool on0 = (me == 0);
-  if (me == rk_M) aux(A2r, on0 ? r2c : A2, vSr, on0 ? scr0 : sl, gM);
-  if (do_mt && me == rk_MT) aux(A1r, on0 ? r2c : A2, vSr, on0 ? scr0 : sl, gMT);
+  if (me == rk_M) aux(A2r, on0 ? r2c : A2, vSr, on0 ? scr0 : sl, gM, false);
+  if (do_mt && me == rk_MT) aux(A1r, on0 ? r2c : A2, vSr, on0 ? scr0 : sl, gMT, pmode);
   if (me == 0 && rk_R == 0) {
     for (int e = tid; e < DMQR_KP * DMQR_KP; e += PANEL_T) {
       const int p = e / DMQR_KP, cc = e % DMQR_KP;

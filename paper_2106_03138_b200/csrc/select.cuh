@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const dou
     c->bar_count = 0u;  // the panel's grid-barrier counter restarts each step
     c->cq_fail = 1;     // the CholeskyQR2 panel (if launched) clears this on success
     c->q1_count = 0u;
+    c->p_count = 0u;
     c->q1_fail = 0;
   }
   __shared__ SelSmem sm;

@@ -588,12 +588,25 @@ static_assert(TA_COLS == TB_COLS, "k_spare: a phase-2 column tile is a phase-1 c
 static_assert(YG_SMEM <= SP_SMEM, "k_spare runs the Y = Q1 M tiles in its dynamic shared memory");
 constexpr int NSPLIT_MAXG = 16;
 
+// k_spare's wait for the panel: P published (P-mode: returns its column count)
+// or Q1 published / the panel's release (returns 0).  Out of line: inlined, the
+// polling loop pushes the kernel past its 2-CTA register cap.
+__device__ __noinline__ int spare_wait_panel(Ctl* c, int P) {
+  for (;;) {
+    if (ld_acquire(&c->p_count) >= (unsigned)P) return c->p_k;
+    if (ld_acquire(&c->q1_count) >= (unsigned)P) return (ld_acquire(&c->p_count) >= (unsigned)P) ? c->p_k : 0;
+    __nanosleep(200);
+  }
+}
+
+template <bool PM>  // PM: P-mode look-ahead (opt-in; panel_cq.cuh)
 __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* __restrict__ A,
                                                    const double* __restrict__ Wt, int64_t ldz,
                                                    uint8_t* __restrict__ upd, const double* __restrict__ Q1g,
                                                    double* __restrict__ Gp, unsigned* __restrict__ ctr, int P,
                                                    int nsplit_g, unsigned* __restrict__ tcnt,
-                                                   long long* __restrict__ tline, const double* __restrict__ gM) {
+                                                   long long* __restrict__ tline, const double* __restrict__ gM,
+                                                   const double* __restrict__ Pg) {
   const long long t_first = gtimer();
   __shared__ int s_item, s_flag;
   const int tid = threadIdx.x;
@@ -640,16 +653,30 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
   // ---- phase 2: G = Q1^T C once Q1 is published; each tile once phase 1 has
   // updated its columns (its column tile's counter), not the whole of phase 1 ----
   if (!S.done) {
+    __shared__ int s_pk;
     if (tid == 0) {
-      while (ld_acquire(&c->q1_count) < (unsigned)P) __nanosleep(200);
-      s_flag = !c->q1_fail;
+      // P-mode: the panel published its columns P first (G = P^T C, R1^-T folded
+      // into k_trail_w's MT); otherwise wait for Q1 (or the panel's release)
+      if constexpr (PM) {
+        s_pk = spare_wait_panel(c, P);
+      } else {
+        while (ld_acquire(&c->q1_count) < (unsigned)P) __nanosleep(200);
+        s_pk = 0;
+      }
+      s_flag = (s_pk > 0) || !c->q1_fail;
       if (g_tl_on) atomicMin(&g_tl[(S.step_idx & 63) * 32 + 28], (unsigned long long)gtimer());  // Q1 seen
       if (g_tl_on && S.step_idx == 20 && blockIdx.x < 256) g_tl[2048 + blockIdx.x * 4 + 0] = gtimer();
     }
     __syncthreads();
     if (s_flag) {
       const int64_t n_s = S.n_s;
-      const int kk = c->q1_kk;
+      // (the P-mode choice stays in shared memory: registers are at the 2-CTA cap)
+      __shared__ const double* s_yg;
+      if (tid == 0) {
+        s_yg = (PM && s_pk > 0) ? Pg : Q1g;
+        if (s_pk == 0) s_pk = c->q1_kk;
+      }
+      __syncthreads();
       const int64_t ncols = n - n_s;
       const int ntile = (int)ceil_div(ncols, TA_COLS);
       const int ng = ntile * nsplit_g;
@@ -689,7 +716,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
           g_tl[2048 + blockIdx.x * 4 + 3] += 1;
         }
         const int tile = it % ntile;
-        g_partial(A, Q1g, Gp, ldz, n_s, m, lda, kk, ncols, (int64_t)tile * TA_COLS, it / ntile, nsplit_g);
+        g_partial(A, s_yg, Gp, ldz, n_s, m, lda, s_pk, ncols, (int64_t)tile * TA_COLS, it / ntile, nsplit_g);
         __syncthreads();
         // the CTA finishing a tile's last split sums its partials into split 0
         // (fixed order) for k_trail_w
@@ -701,7 +728,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
         if (s_flag) {
           __threadfence();
           const int64_t col0 = (int64_t)tile * TA_COLS;
-          for (int e = tid; e < kk * TA_COLS; e += blockDim.x) {
+          for (int e = tid; e < s_pk * TA_COLS; e += blockDim.x) {
             const int i = e / TA_COLS, c2 = e % TA_COLS;
             const double* gp = Gp + (int64_t)i * ldz + col0 + c2;
             double v[NSPLIT_MAXG];

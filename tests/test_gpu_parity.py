@@ -481,6 +481,25 @@ def test_tall_panel_helpers_and_their_fallback(wait_ns, monkeypatch):
     assert resid <= 50 * 9000 * O.EPS and orth <= 50 * 9000 * O.EPS
 
 
+@pytest.mark.parametrize("n", [1000, 2500])
+def test_pmode_lookahead_matches_default(monkeypatch, n):
+    """Opt-in P-mode look-ahead (DMQR_PMODE: k_spare forms P^T C from the panel's
+    start, k_trail_w folds R1^-T into MT): same decisions as the default schedule,
+    factor equal to rounding of a cond(R1)-scaled product."""
+    from paper_2106_03138_b200 import qrdm2
+
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((n, n)) * np.logspace(0, -6, n)[rng.permutation(n)]
+    base = qrdm2(A)
+    monkeypatch.setenv("DMQR_PMODE", "1")
+    res = qrdm2(A)
+    assert np.array_equal(res.perm.forward, base.perm.forward) and res.rank == base.rank
+    scale = np.abs(base.packed).max()
+    assert np.abs(res.packed - base.packed).max() <= 1e-10 * scale
+    resid, orth = parity.residuals(A, res)
+    assert resid <= 50 * n * O.EPS and orth <= 50 * n * O.EPS
+
+
 def test_batched_large_matrices_per_matrix_path():
     """Batches of matrices too large to group (m n >= 2^20) take the per-matrix
     engine on concurrent lanes: identical to the single-matrix calls."""
