@@ -195,16 +195,22 @@ void dmqr_stats_enable(int32_t on);
 void dmqr_stats_get(dmqr_stats* out, int32_t reset);
 
 /* Debug: copy the device control block of a workspace (after a call) into
- * out[16 + 4*72] int64 on the device: n_s, done, stopped, status, kind, k_max,
+ * out[16 + 4*72 + 5] int64 on the device: n_s, done, stopped, status, kind, k_max,
  * ncand, nsel, k_s, l_acc, nsw, step_idx, n_swaps, bits(umax), bits(eps_s),
- * bits(gamma), cand[72], sel[72], sw_a[72], sw_b[72]. */
+ * bits(gamma), cand[72], sel[72], sw_a[72], sw_b[72], bits(cq_diag[4]),
+ * cq_fail * 10^6 + tc0. */
 int dmqr_debug_ctl(const void* workspace, int64_t* out, void* stream);
 /* Debug: per-reflector phase clocks (clock64) of one panel CTA at step 2, recorded
  * when dmqr_stats_enable(2) was set; out = 64 x 8 int64 on the host. */
 int dmqr_debug_panel_clocks(const void* workspace, int64_t m, int64_t n, int64_t* out);
-/* debug: kernel spans per step of the last factorization run with
- * DMQR_TIMELINE set (out[64 * 32 + 1024] int64, globaltimer ns; see the source) */
-int dmqr_debug_timeline(int64_t* out);
+/* debug: kernel spans per step of the last factorization run in `workspace`
+ * (sized for m x n) with DMQR_TIMELINE set (out[64 * 32 + 1024] int64 on the
+ * host, globaltimer ns; see the source) */
+int dmqr_debug_timeline(const void* workspace, int64_t m, int64_t n, int64_t* out);
+/* Free the library's pooled pinned poll records, events and copy streams (all
+ * devices).  Optional; only while no call is running.  The pool holds one entry
+ * per concurrently running engine call. */
+void dmqr_release_resources(void);
 
 /* Build identification (compile arch, version) for logs and the loader check. */
 const char* dmqr_version(void);

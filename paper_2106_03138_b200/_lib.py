@@ -31,6 +31,7 @@ EXPORTS = (
     "dmqr_stats_get",
     "dmqr_debug_panel_clocks",
     "dmqr_debug_timeline",
+    "dmqr_release_resources",
 )
 
 DMQR_OK, DMQR_EINVAL, DMQR_ENONFINITE, DMQR_EZEROCOL, DMQR_ECUDA, DMQR_ECAP = 0, -1, -2, -3, -4, -5
@@ -140,8 +141,10 @@ def load() -> C.CDLL:
     lib.dmqr_stats_get.restype = None
     lib.dmqr_debug_panel_clocks.argtypes = [P, I64, I64, P]
     lib.dmqr_debug_panel_clocks.restype = C.c_int
-    lib.dmqr_debug_timeline.argtypes = [P]
+    lib.dmqr_debug_timeline.argtypes = [P, I64, I64, P]
     lib.dmqr_debug_timeline.restype = C.c_int
+    lib.dmqr_release_resources.argtypes = []
+    lib.dmqr_release_resources.restype = None
     lib.dmqr_version.argtypes = []
     lib.dmqr_version.restype = C.c_char_p
     _lib = lib

@@ -129,8 +129,9 @@ def qrdm2_batched(A, params: DMParams = DMParams(), stop: StopCriterion = StopCr
 
 
 def summary_tensor(f: BatchFactor, device):
-    """(b, 4 + n + kmax) float64 summary rows: rank, n_factored, stopped, n_steps, perm, coeffs."""
-    torch = _torch()
+    """(b, 4 + n + kmax) float64 summary rows: rank, n_factored, stopped, n_steps, perm, coeffs.
+    (Host-side table logic: plain torch, any device.)"""
+    import torch
     b = len(f.infos)
     rows = [[i.rank, i.n_factored, i.stopped_early, i.n_steps] for i in f.infos]
     head = torch.tensor(rows, dtype=torch.float64, device=device).reshape(b, 4)

@@ -69,20 +69,29 @@ struct Ctl {
   uint32_t bar_gen;
   uint32_t trace_bits_lo, trace_bits_hi;
   uint32_t pad1[3];
+  // fixed at init (k_init): the per-matrix block stride of a batched launch
+  // (zshift) and the debug timeline buffer in the workspace (null: off)
+  int64_t zstride;
+  unsigned long long* tl;
 };
 
 // Batched launches (grid.z = matrices of a batch, small matrices): every
 // per-matrix buffer -- control block, workspace, matrix, outputs -- sits in a
-// per-matrix block at a fixed byte stride g_zstride, so a kernel shifts its
-// pointer arguments by blockIdx.z * g_zstride at entry (gridDim.z == 1: no-op).
-// The stride is set by the batched driver (process-wide lock while it runs).
-__constant__ int64_t g_zstride;
+// per-matrix block at a fixed byte stride, so a kernel shifts its pointer
+// arguments by blockIdx.z * stride at entry (gridDim.z == 1: no-op).  The
+// stride is read from block 0's control block (k_init stores it there; every
+// later kernel of the factorization runs after k_init has completed), so no
+// process-wide state is involved.
 template <typename... Ts>
-__device__ __forceinline__ void zshift(Ts&... ps) {
+__device__ __forceinline__ void zshift_by(int64_t zs, Ts&... ps) {
   if (gridDim.z > 1) {
-    const int64_t o = (int64_t)blockIdx.z * g_zstride;
+    const int64_t o = (int64_t)blockIdx.z * zs;
     ((ps = ps ? (Ts)((char*)(ps) + o) : ps), ...);
   }
+}
+template <typename... Ts>
+__device__ __forceinline__ void zshift(const Ctl* c0, Ts&... ps) {
+  if (gridDim.z > 1) zshift_by(c0->zstride, ps...);
 }
 
 // Entry snapshot of the scalar decision state.  Every field is loaded
@@ -95,6 +104,7 @@ struct CtlSnap {
   int32_t stop_active, break_check, k_dm, use_delta_max, trace_norms, swap_cap, step_cap;
   int32_t n_s, done, step_idx, n_swaps, kind, k_max, nsel, k_s, l_acc, ncand, nsw, nmv;
   int32_t cq_fail, tc0, la, pend, pend_ns, pend_l, q1_fail, q1_kk;
+  unsigned long long* tl;
 };
 __device__ __forceinline__ CtlSnap snap(const Ctl* __restrict__ c) {
   CtlSnap s;
@@ -106,7 +116,7 @@ __device__ __forceinline__ CtlSnap snap(const Ctl* __restrict__ c) {
   s.kind = c->kind; s.k_max = c->k_max; s.nsel = c->nsel; s.k_s = c->k_s; s.l_acc = c->l_acc;
   s.ncand = c->ncand; s.nsw = c->nsw; s.nmv = c->nmv; s.cq_fail = c->cq_fail; s.tc0 = c->tc0;
   s.la = c->la; s.pend = c->pend; s.pend_ns = c->pend_ns; s.pend_l = c->pend_l;
-  s.q1_fail = c->q1_fail; s.q1_kk = c->q1_kk;
+  s.q1_fail = c->q1_fail; s.q1_kk = c->q1_kk; s.tl = c->tl;
   return s;
 }
 
@@ -134,19 +144,20 @@ struct __align__(16) HostRec {
 };
 
 // debug timeline (DMQR_TIMELINE): per step and kernel, the first CTA's start
-// (after its dependency wait) and the last CTA's exit, globaltimer ns
-__device__ unsigned long long g_tl[64 * 32 + 1024];  // + k_spare per-CTA debug of step 20
-__constant__ int g_tl_on;
+// (after its dependency wait) and the last CTA's exit, globaltimer ns, in a
+// workspace buffer of TL_WORDS words (Ctl::tl; null when the timeline is off)
+constexpr int TL_WORDS = 64 * 32 + 1024;  // + k_spare per-CTA debug of step 20
 struct TLSpan {
+  unsigned long long* tl;
   int slot;
-  __device__ __forceinline__ TLSpan(int step, int k) : slot(-1) {
-    if (threadIdx.x == 0 && g_tl_on) {
+  __device__ __forceinline__ TLSpan(unsigned long long* t, int step, int k) : tl(t), slot(-1) {
+    if (threadIdx.x == 0 && tl) {
       slot = (step & 63) * 32 + 2 * k;
-      atomicMin(&g_tl[slot], (unsigned long long)gtimer());
+      atomicMin(&tl[slot], (unsigned long long)gtimer());
     }
   }
   __device__ __forceinline__ ~TLSpan() {
-    if (slot >= 0) atomicMax(&g_tl[slot + 1], (unsigned long long)gtimer());
+    if (slot >= 0) atomicMax(&tl[slot + 1], (unsigned long long)gtimer());
   }
 };
 

@@ -43,7 +43,7 @@ constexpr int PANEL_PMAX = 160;
 
 struct Layout {
   size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, trace, pdbg, tcount, upd, lacount, q1g, pg, glist;
-  size_t qvb, qwb, qpart, qgpart, qcnt, hpart, hR, hctr, gnp, total;
+  size_t qvb, qwb, qpart, qgpart, qcnt, hpart, hR, hctr, gnp, tl, total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -90,6 +90,7 @@ Layout layout(int64_t m, int64_t n) {
   L.hctr = take(sizeof(unsigned) * 8);
   // serial guard norms: (column, 4096-row chunk) partials
   L.gnp = take(sizeof(double) * 2 * (size_t)std::max<int64_t>(n, 1) * (size_t)std::max<int64_t>(1, (m + GN_ROWS - 1) / GN_ROWS));
+  L.tl = take(sizeof(unsigned long long) * TL_WORDS);  // debug timeline (DMQR_TIMELINE)
   L.total = off;
   return L;
 }
@@ -126,15 +127,29 @@ cudaError_t& last_cuda_error() {
   return e;
 }
 
-bool attrs_done = false;
-bool cluster16 = false;
-int qp_grid = 1;  // k_qp3 cooperative grid (all CTAs co-resident)
-
+// Function attributes apply per device, so they are set once per device id
+// (the first call on a device), together with the launch limits derived from
+// them.  Read-only once `done` is published.
+struct DevAttrs {
+  std::atomic<bool> done{false};
+  bool cluster16 = false;
+  int qp_grid = 1;  // k_qp3 cooperative grid (all CTAs co-resident)
+};
+constexpr int kMaxDevices = 64;
+DevAttrs g_dev_attrs[kMaxDevices];
 std::mutex g_attr_mu;
 
-int set_attrs(const DevInfo& d) {
+int set_attrs(const DevInfo& d, DevAttrs** out) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return DMQR_EINVAL;
+  DevAttrs& A = g_dev_attrs[dev];
+  *out = &A;
+  if (A.done.load(std::memory_order_acquire)) return 0;
   std::lock_guard<std::mutex> lk(g_attr_mu);
-  if (attrs_done) return 0;
+  if (A.done.load(std::memory_order_relaxed)) return 0;
+  bool& cluster16 = A.cluster16;
+  int& qp_grid = A.qp_grid;
   CK(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GRAM_SMEM));
   CK(cudaFuncSetAttribute(k_trail_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA_SMEM));
   CK(cudaFuncSetAttribute(k_gram_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FinSmem)));
@@ -145,7 +160,6 @@ int set_attrs(const DevInfo& d) {
   CK(cudaFuncSetAttribute(k_trail_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TW_SMEM));
   CK(cudaFuncSetAttribute(k_guard, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GU_SMEM));
   CK(cudaFuncSetAttribute(k_ygemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YG_SMEM));
-  CK(cudaFuncSetAttribute(k_trail_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TP_SMEM));
   CK(cudaFuncSetAttribute(k_qp3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QP_SMEM));
   CK(cudaFuncSetAttribute(k_panel_helper, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CQH_SMEM));
   CK(cudaFuncSetAttribute(k_fq_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FQ_SMEM2));
@@ -179,9 +193,59 @@ int set_attrs(const DevInfo& d) {
     cluster16 = cudaOccupancyMaxActiveClusters(&ncl, k_panel_rr<ClusterRed>, &cfg) == cudaSuccess && ncl >= 1;
   }
   cudaGetLastError();
-  attrs_done = true;
+  A.done.store(true, std::memory_order_release);
   return 0;
 }
+
+// Pinned poll records, their events and the packed-factor copy stream of one
+// engine call, recycled through a small per-device pool (an engine call holds
+// one entry for its duration; entries live until dmqr_release_resources or
+// process exit, so repeated calls -- from any thread -- allocate nothing).
+struct HostSlot {
+  int dev = -1;
+  HostRec* rec = nullptr;            // two records
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaStream_t copy = nullptr;       // created on first use
+};
+std::mutex g_slot_mu;
+std::vector<HostSlot*> g_slot_free;
+std::vector<HostSlot*> g_slot_all;
+
+HostSlot* slot_acquire(int dev) {
+  {
+    std::lock_guard<std::mutex> lk(g_slot_mu);
+    for (size_t i = 0; i < g_slot_free.size(); ++i)
+      if (g_slot_free[i]->dev == dev) {
+        HostSlot* h = g_slot_free[i];
+        g_slot_free.erase(g_slot_free.begin() + (long)i);
+        return h;
+      }
+  }
+  HostSlot* h = new HostSlot;
+  h->dev = dev;
+  if (cudaMallocHost(&h->rec, 2 * sizeof(HostRec)) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev[1], cudaEventDisableTiming) != cudaSuccess) {
+    last_cuda_error() = cudaGetLastError();
+    if (h->rec) cudaFreeHost(h->rec);
+    for (auto e : h->ev)
+      if (e) cudaEventDestroy(e);
+    delete h;
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_slot_mu);
+  g_slot_all.push_back(h);
+  return h;
+}
+void slot_release(HostSlot* h) {
+  if (!h) return;
+  std::lock_guard<std::mutex> lk(g_slot_mu);
+  g_slot_free.push_back(h);
+}
+struct SlotGuard {
+  HostSlot* h;
+  ~SlotGuard() { slot_release(h); }
+};
 
 int validate(int64_t m, int64_t n, int64_t lda, const dmqr_params* p) {
   if (!p) return DMQR_EINVAL;
@@ -323,7 +387,10 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   if (p->trace_norms && !norm_trace) return DMQR_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   const DevInfo d = dev_info();
-  if ((rc = set_attrs(d))) return rc;
+  DevAttrs* da = nullptr;
+  if ((rc = set_attrs(d, &da))) return rc;
+  const bool cluster16 = da->cluster16;
+  const int qp_grid = da->qp_grid;
 
   unsigned char* ws = (unsigned char*)workspace;
   Ctl* ctl = (Ctl*)(ws + L.ctl);
@@ -376,15 +443,21 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   if (n > 0) {
     if (m > 0) {
       int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)d.sms * 16);
-      k_colnorms_init<<<dim3((unsigned)blocks, 1, NZ), 256, 0, st>>>(A, m, n, lda, u, uref, nonfinite);
+      k_colnorms_init<<<dim3((unsigned)blocks, 1, NZ), 256, 0, st>>>(A, m, n, lda, u, uref, nonfinite, zs);
       NOTE_LAUNCH();
     } else {
       CK(zmemset(u, sizeof(double) * n));
       CK(zmemset(uref, sizeof(double) * n));
     }
   }
+  long long* tline = (getenv("DMQR_TIMELINE") && NZ == 1) ? pdbg : nullptr;  // debug: panel / k_spare timestamps
+  unsigned long long* tlbuf = tline ? (unsigned long long*)(ws + L.tl) : nullptr;
+  if (tlbuf) {
+    k_tl_init<<<(TL_WORDS + 255) / 256, 256, 0, st>>>(tlbuf);
+    NOTE_LAUNCH();
+  }
   InitArgs ia{ctl, u, perm, coeffs, m, n, lda, kmax, p->tau, p->delta, eps1, p->k_dm, p->use_delta_max,
-              p->break_check, p->trace_norms, swap_cap, step_cap, nonfinite, 0};
+              p->break_check, p->trace_norms, swap_cap, step_cap, nonfinite, 0, NZ > 1 ? zs : 0, tlbuf};
   k_init<<<dim3(1, 1, NZ), 1024, 0, st>>>(ia);
   NOTE_LAUNCH();
   CK(cudaGetLastError());
@@ -395,13 +468,14 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   // still in flight -- every step accepts at least one).  Grids are therefore
   // upper bounds; kernels read the true extents from Ctl and exit surplus
   // CTAs, and steps enqueued after `done` exit at once.
-  static thread_local HostRec* hrec = nullptr;  // pinned poll slots, one pair per host thread
-  static thread_local cudaEvent_t hev[2] = {nullptr, nullptr};
-  if (!hrec) {
-    CK(cudaMallocHost(&hrec, 2 * sizeof(HostRec)));
-    for (auto& e : hev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
-  HostRec* const hrecs = (NZ > 1) ? zrec : hrec;  // (one pair per matrix; k_step_end offsets by blockIdx.z)
+  // pinned poll records (+ events, copy stream) from the per-device pool; a
+  // batch brings its own records (one pair per matrix; k_step_end offsets by blockIdx.z)
+  int cur_dev = 0;
+  CK(cudaGetDevice(&cur_dev));
+  SlotGuard slot_guard{NZ > 1 ? nullptr : slot_acquire(cur_dev)};
+  if (NZ == 1 && !slot_guard.h) return DMQR_ECUDA;
+  HostRec* const hrecs = (NZ > 1) ? zrec : slot_guard.h->rec;
+  cudaEvent_t* const hev = (NZ > 1) ? nullptr : slot_guard.h->ev;
   for (unsigned q = 0; q < 2 * NZ; ++q) ((volatile HostRec*)hrecs)[q].seq = -1;
   const bool prof = g_prof.load() != 0;
   cudaEvent_t ev[2][5];
@@ -416,18 +490,6 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   const int max_coop_p = std::min(d.sms, PANEL_PMAX);
   const int max_cluster = cluster16 ? 16 : 8;
   const bool use_cq = getenv("DMQR_NO_CHOLQR") == nullptr;  // debug switch: Householder panel only
-  long long* tline = getenv("DMQR_TIMELINE") ? pdbg : nullptr;  // debug: panel / k_spare timestamps
-  {
-    const int on = tline ? 1 : 0;
-    if (tline) {
-      static unsigned long long init[64 * 32 + 1024];
-      for (int q = 0; q < 64 * 32 + 1024; ++q) init[q] = (q >= 64 * 32 || (q & 1)) ? 0ull : ~0ull;
-      CK(cudaMemcpyToSymbolAsync(g_tl, init, sizeof(init), 0, cudaMemcpyHostToDevice, st));
-    }
-    CK(cudaMemcpyToSymbolAsync(g_tl_on, &on, sizeof(int), 0, cudaMemcpyHostToDevice, st));
-  }
-  const bool trail_persistent = getenv("DMQR_TRAIL_PERSISTENT") != nullptr;  // A/B switch
-  const bool spare_all = getenv("DMQR_SPARE_FREE_ONLY") == nullptr;          // A/B switch
   const bool no_helpers = getenv("DMQR_NO_HELPERS") != nullptr;               // A/B switch
   // P-mode look-ahead (G = R1^-T P^T C from the panel's start; panel_cq.cuh): correct, but on cfg2 the
   // earlier G traffic slows the latency-bound panel more than it shortens k_spare (16.9 vs 16.6 ms), so opt-in
@@ -596,8 +658,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
         // that start once the panel is done (they pull what is left); no more than
         // work items
         const int64_t items = (int64_t)lag.x * lag.y * (la_rest ? 1 : 0) + ntile_g * nsplit_g;
-        const int sp_sms = spare_all ? d.sms : std::max(1, d.sms - Pcq);
-        cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(2 * sp_sms, items)));
+        cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(2 * d.sms, items)));
         cfg.blockDim = dim3(TB_T);
         cfg.dynamicSmemBytes = SP_SMEM;
         cfg.stream = st;
@@ -650,13 +711,9 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
       NOTE_LAUNCH();
       if (la) {
         // the rest of C -= Y Wt runs beside the next step's panel
-      } else if (!trail_persistent) {
+      } else {
         k_trail_b<false><<<dim3((unsigned)ceil_div(mp + 1, TB_ROWS), (unsigned)ceil_div(ncols_ub, TB_COLS), NZ), TB_T,
                            TB_SMEM, st>>>(ctl, A, Z, ldz, upd, lacount + 1);
-        NOTE_LAUNCH();
-      } else {
-        const int64_t work = ceil_div(mp + 1, TP_ROWS) * ceil_div(ncols_ub, TP_COLS);
-        k_trail_bp<<<(unsigned)std::min<int64_t>(work, d.sms), TP_T, TP_SMEM, st>>>(ctl, A, Z, ldz);
         NOTE_LAUNCH();
       }
     }
@@ -698,8 +755,8 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   };
 
   // streamed packed factor: final columns go to the host on a side stream
-  static thread_local cudaStream_t sCopy = nullptr;
-  if (host_packed && !sCopy) CK(cudaStreamCreateWithFlags(&sCopy, cudaStreamNonBlocking));
+  if (host_packed && !slot_guard.h->copy) CK(cudaStreamCreateWithFlags(&slot_guard.h->copy, cudaStreamNonBlocking));
+  const cudaStream_t sCopy = host_packed ? slot_guard.h->copy : nullptr;
   int64_t copied = 0;
   auto stream_cols = [&](int64_t upto, cudaEvent_t after) -> int {
     upto = std::min(upto, n);
@@ -1022,7 +1079,6 @@ LaneBufs lane_bufs(int64_t m, int64_t n, int64_t lda) {
 }
 bool batch_graph_ok(int64_t m, int64_t n) { return m * n < ((int64_t)1 << 20); }
 constexpr int ZG = 128;  // small matrices per batched launch (grid.z)
-std::mutex g_zstride_mu;  // g_zstride is process-wide: one batched call at a time
 }  // namespace
 
 extern "C" {
@@ -1055,19 +1111,13 @@ int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_
   if (m > 4096) nlanes = 1;  // cooperative panel launches must not compete for co-residency
   if (ws_bytes < per * (size_t)nlanes || !workspace) return DMQR_EINVAL;
   if (graphs) nlanes = (int32_t)std::min<int64_t>(nlanes, ceil_div(batch, ZG));
-  // the per-matrix block stride the batched kernels shift by (process-wide)
-  std::unique_lock<std::mutex> zlock(g_zstride_mu, std::defer_lock);
-  if (graphs) {
-    zlock.lock();
-    const int64_t zs64 = (int64_t)zblk;
-    CK(cudaMemcpyToSymbol(g_zstride, &zs64, sizeof(int64_t)));
-  }
   if (batch == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   int dev = 0;
   CK(cudaGetDevice(&dev));
   const DevInfo d = dev_info();
-  if ((rc = set_attrs(d))) return rc;
+  DevAttrs* da = nullptr;
+  if ((rc = set_attrs(d, &da))) return rc;
   // lanes start after the caller's stream reaches this point, and the caller's
   // stream waits for every lane at the end
   cudaEvent_t start;
@@ -1184,7 +1234,8 @@ int dmqr_form_q_f64(const double* packed, int64_t m, int64_t n, int64_t lda, con
   cudaStream_t st = (cudaStream_t)stream;
   if (m == 0 || qcols == 0) return 0;
   {
-    int rc = set_attrs(dev_info());
+    DevAttrs* da = nullptr;
+    int rc = set_attrs(dev_info(), &da);
     if (rc) return rc;
   }
   const size_t q = (size_t)qcols;
@@ -1248,12 +1299,32 @@ int dmqr_debug_panel_clocks(const void* workspace, int64_t m, int64_t n, int64_t
   return 0;
 }
 
-/* debug: per-step kernel spans of the last factorization run with
- * DMQR_TIMELINE set: out[64 * 32], step s, kernel k -> [32 s + 2 k] first
- * start, [32 s + 2 k + 1] last exit (globaltimer ns) */
-int dmqr_debug_timeline(int64_t* out) {
-  CK(cudaMemcpyFromSymbol(out, g_tl, sizeof(unsigned long long) * (64 * 32 + 1024)));
+/* debug: per-step kernel spans of the last factorization run in this
+ * workspace with DMQR_TIMELINE set: out[64 * 32 + 1024], step s, kernel k ->
+ * [32 s + 2 k] first start, [32 s + 2 k + 1] last exit (globaltimer ns) */
+int dmqr_debug_timeline(const void* workspace, int64_t m, int64_t n, int64_t* out) {
+  const Layout L = layout(m, n);
+  CK(cudaMemcpy(out, (const unsigned char*)workspace + L.tl, sizeof(unsigned long long) * TL_WORDS,
+                cudaMemcpyDeviceToHost));
   return 0;
+}
+
+/* release the pooled pinned poll records / events / copy streams (all devices);
+ * only while no engine call is running */
+void dmqr_release_resources(void) {
+  std::lock_guard<std::mutex> lk(g_slot_mu);
+  for (HostSlot* h : g_slot_all) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(h->dev);
+    if (h->copy) cudaStreamDestroy(h->copy);
+    for (auto e : h->ev) cudaEventDestroy(e);
+    cudaFreeHost(h->rec);
+    cudaSetDevice(cur);
+    delete h;
+  }
+  g_slot_all.clear();
+  g_slot_free.clear();
 }
 
 int dmqr_debug_ctl(const void* workspace, int64_t* out, void* stream) {

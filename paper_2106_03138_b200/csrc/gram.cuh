@@ -148,12 +148,12 @@ __device__ __forceinline__ void tile_ij(int t, int nt, int& ti, int& tj) {
 __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __restrict__ A,
                                                  double* __restrict__ part, const double* __restrict__ Wt,
                                                  int64_t ldz, const uint8_t* __restrict__ upd) {
-  zshift(c, A, part, Wt, upd);
+  zshift(c, c, A, part, Wt, upd);
   pdl_enter();
   // the candidate list is read with the control block snapshot (one round trip)
   const int cand_pre = (threadIdx.x < DMQR_KP) ? c->cand[threadIdx.x] : 0;
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.step_idx, 1);
+  TLSpan tl_span(S.tl, S.step_idx, 1);
   if (S.done) return;
   const bool pendu = S.la && S.pend;
   if (S.kind != 0 && !pendu) return;
@@ -341,11 +341,11 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
                                                         const double* __restrict__ part, int G,
                                                         double* __restrict__ gfin, uint8_t* __restrict__ upd,
                                                         long long* __restrict__ tline) {
-  zshift(c, A, part, gfin, upd);
+  zshift(c, c, A, part, gfin, upd);
   const long long t_in = gtimer();
   pdl_enter();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.step_idx, 2);
+  TLSpan tl_span(S.tl, S.step_idx, 2);
   if (S.done) return;
 #define GFT(k) \
   if (tline && threadIdx.x == 0) tline[512 + 8 * (S.step_idx & 63) + (k)] = gtimer()

@@ -21,10 +21,12 @@ struct InitArgs {
   int64_t swap_cap, step_cap;
   const int32_t* nonfinite;  // set by k_colnorms_init
   int32_t lookahead;
+  int64_t zstride;         // per-matrix block stride of a batched launch (grid.z > 1)
+  unsigned long long* tl;  // debug timeline buffer (workspace) or null
 };
 
 __global__ void __launch_bounds__(1024) k_init(InitArgs a) {
-  zshift(a.c, a.u, a.perm, a.coeffs, a.nonfinite);
+  zshift_by(a.zstride, a.c, a.u, a.perm, a.coeffs, a.nonfinite);
   __shared__ double red[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   double mx = 0.0;
@@ -53,6 +55,8 @@ __global__ void __launch_bounds__(1024) k_init(InitArgs a) {
       c->break_check = a.break_check;
       c->trace_norms = a.trace_norms;
       c->la = a.lookahead;
+      c->zstride = a.zstride;
+      c->tl = a.tl;
       c->pend = 0;
       c->gcount = 0;
       c->swap_cap = (int32_t)min(a.swap_cap, (int64_t)0x7fffffff);
@@ -124,11 +128,11 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
                            double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
                            double* __restrict__ uref, uint8_t* __restrict__ upd, HostRec* __restrict__ hrec,
                            int enq) {
-  zshift(c, steps, norm_trace, trace_bits, A, Wt, u, uref, upd);
+  zshift(c, c, steps, norm_trace, trace_bits, A, Wt, u, uref, upd);
   if (gridDim.z > 1 && hrec) hrec += 2 * blockIdx.z;  // (host records: two slots per matrix)
   pdl_enter();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.step_idx, 10);
+  TLSpan tl_span(S.tl, S.step_idx, 10);
   if (!S.done) step_end_body(S, c, steps, norm_trace, trace_bits, A, Wt, ldz, u, uref, upd);
   // the host's poll record of this step (no stream operation between the
   // steps, so the programmatic launches chain across step boundaries)
@@ -158,9 +162,15 @@ __global__ void k_set_la(Ctl* __restrict__ c, int on) {
   if (threadIdx.x == 0) c->la = on;
 }
 
+// debug timeline buffer: span starts (even slots) at +inf for atomicMin, the rest 0
+__global__ void k_tl_init(unsigned long long* __restrict__ tl) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < TL_WORDS) tl[q] = (q >= 64 * 32 || (q & 1)) ? 0ull : ~0ull;
+}
+
 // rank / n_factored (rrqr.py:406-412)
 __global__ void k_finalize(Ctl* __restrict__ c, const double* __restrict__ A, int stop_none) {
-  zshift(c, A);
+  zshift(c, c, A);
   __shared__ int cnt[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t n_s = c->n_s;
@@ -215,11 +225,12 @@ __global__ void k_debug_ctl(const Ctl* __restrict__ c, int64_t* __restrict__ out
   *o++ = c->n_s; *o++ = c->done; *o++ = c->stopped; *o++ = c->status;
   *o++ = c->kind; *o++ = c->k_max; *o++ = c->ncand; *o++ = c->nsel; *o++ = c->k_s; *o++ = c->l_acc;
   *o++ = c->nsw; *o++ = c->step_idx; *o++ = c->n_swaps;
-  *o++ = __double_as_longlong(c->umax); *o++ = __double_as_longlong(c->eps_s); *o++ = c->cq_fail * 1000000LL + c->tc0;
+  *o++ = __double_as_longlong(c->umax); *o++ = __double_as_longlong(c->eps_s); *o++ = __double_as_longlong(c->gamma);
   for (int i = 0; i < DMQR_KP; ++i) *o++ = c->cand[i];
   for (int i = 0; i < DMQR_KP; ++i) *o++ = c->sel[i];
   for (int i = 0; i < DMQR_KP; ++i) *o++ = c->sw_a[i];
   for (int i = 0; i < DMQR_KP; ++i) *o++ = c->sw_b[i];
   for (int i = 0; i < 4; ++i) *o++ = __double_as_longlong(c->cq_diag[i]);
+  *o++ = c->cq_fail * 1000000LL + c->tc0;
 }
 }  // namespace dmqr

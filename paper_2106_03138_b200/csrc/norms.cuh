@@ -76,8 +76,9 @@ __device__ __forceinline__ double warp_col_norm(const double* __restrict__ x, in
 // flagged here (dense() rejects such input, matrix.py:32-33) -- so the input
 // validation costs no extra pass over the matrix.
 __global__ void k_colnorms_init(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
-                                double* __restrict__ u, double* __restrict__ uref, int32_t* __restrict__ nonfinite) {
-  zshift(A, u, uref, nonfinite);
+                                double* __restrict__ u, double* __restrict__ uref, int32_t* __restrict__ nonfinite,
+                                int64_t zs) {
+  zshift_by(zs, A, u, uref, nonfinite);
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -126,9 +127,9 @@ __global__ void k_colnorms_init(const double* __restrict__ A, int64_t m, int64_t
 // exactly from rows n_s1.. and their u_ref refreshed.
 __global__ void k_downdate(Ctl* __restrict__ c, const double* __restrict__ A, double* __restrict__ u,
                            double* __restrict__ uref, int32_t* __restrict__ glist = nullptr) {
-  zshift(c, A, u, uref, glist);
+  zshift(c, c, A, u, uref, glist);
   if (c->done) return;
-  TLSpan tl_span(c->step_idx, 12);
+  TLSpan tl_span(c->tl, c->step_idx, 12);
   const int64_t n_s = c->n_s, n_s1 = n_s + c->l_acc, n = c->n, m = c->m, lda = c->lda;
   const int lane = threadIdx.x & 31;
   if (blockIdx.x == 0)

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(SWAP_T) k_swap(Ctl* __restrict__ c, double* __
                                                  double* __restrict__ uref, int64_t* __restrict__ perm,
                                                  int64_t* __restrict__ swaplog, double* __restrict__ Wt, int64_t ldz,
                                                  uint8_t* __restrict__ upd) {
-  zshift(c, A, u, uref, perm, swaplog, Wt, upd);
+  zshift(c, c, A, u, uref, perm, swaplog, Wt, upd);
   pdl_enter();
   // the move lists are read with the control block snapshot (one round trip)
   __shared__ int s_src[SWAP_MAXMV], s_dst[SWAP_MAXMV];
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(SWAP_T) k_swap(Ctl* __restrict__ c, double* __
     ms_dst = c->mv_dst[tid];
   }
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.step_idx, 3);
+  TLSpan tl_span(S.tl, S.step_idx, 3);
   if (S.done) return;
   const int nmv = S.nmv;
   const int64_t m = S.m, lda = S.lda;

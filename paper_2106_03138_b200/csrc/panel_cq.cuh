@@ -654,7 +654,7 @@ __device__ void cq_cluster_reduce(double* part, double* tot, int k) {
 }
 
 __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
-  zshift(a.c, a.A, a.coeffs, a.T, a.red, a.q1g, a.hpart, a.hR, a.hctr, a.pg);
+  zshift(a.c, a.c, a.A, a.coeffs, a.T, a.red, a.q1g, a.hpart, a.hR, a.hctr, a.pg);
   // wait for the step's column swaps, then let the look-ahead grid behind this
   // one start (trailing.cuh: it runs beside the panel and must see the swaps)
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -662,7 +662,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   Ctl* c = a.c;
   const long long t_start = gtimer();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.step_idx, 4);
+  TLSpan tl_span(S.tl, S.step_idx, 4);
   if (S.done) return;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double cqs[];

@@ -48,14 +48,14 @@ constexpr size_t RR_CL_SMEM = sizeof(double) * 2 * RR_MAXCL * RED_LD;  // receiv
 
 template <class Red>
 __global__ void __launch_bounds__(PANEL_T, 1) k_panel_rr(PanelArgs a) {
-  zshift(a.c, a.A, a.coeffs, a.T, a.red, a.q1g, a.hpart, a.hR, a.hctr);
+  zshift(a.c, a.c, a.A, a.coeffs, a.T, a.red, a.q1g, a.hpart, a.hR, a.hctr);
   pdl_enter();
   Ctl* c = a.c;
   {
     const int done = c->done, cqf = c->cq_fail;  // (both loads in flight together)
     if (done || (a.only_if_fail && !cqf)) return;
   }
-  TLSpan tl_span(c->step_idx, 13);
+  TLSpan tl_span(c->tl, c->step_idx, 13);
   __shared__ double vbuf[RR_RMAX];
   __shared__ double xs4[RR_RMAX];  // column 64 (warp 0, slot 4)
   __shared__ double s_part[RED_LD];

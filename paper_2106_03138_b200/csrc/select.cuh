@@ -57,10 +57,10 @@ __device__ __forceinline__ int block_excl_scan(int v, int* scan_smem, int* total
 }
 
 __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const double* __restrict__ u) {
-  zshift(c, u);
+  zshift(c, c, u);
   pdl_enter();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.step_idx, 0);
+  TLSpan tl_span(S.tl, S.step_idx, 0);
   if (S.done) return;
   if (threadIdx.x == 0) {
     c->bar_count = 0u;  // the panel's grid-barrier counter restarts each step

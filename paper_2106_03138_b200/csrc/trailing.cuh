@@ -167,10 +167,10 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
                                                      int64_t ldz, double* __restrict__ u,
                                                      double* __restrict__ uref, uint8_t* __restrict__ upd,
                                                      int only_if_cq_fail, int32_t* __restrict__ glist) {
-  zshift(c, A, Zp, T, Wt, counters, u, uref, upd, glist);
+  zshift(c, c, A, Zp, T, Wt, counters, u, uref, upd, glist);
   pdl_enter();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.step_idx, 8);
+  TLSpan tl_span(S.tl, S.step_idx, 8);
   if (S.done || (only_if_cq_fail && !S.cq_fail)) return;  // (k_trail_w did it)
   const int64_t n_s = S.n_s, m = S.m, n = S.n, lda = S.lda;
   const int l = S.l_acc;
@@ -435,10 +435,10 @@ template <bool LA>
 __global__ void __launch_bounds__(TB_T, 2) k_trail_b(Ctl* __restrict__ c, double* __restrict__ A,
                                                      const double* __restrict__ Wt, int64_t ldz,
                                                      uint8_t* __restrict__ upd, unsigned* __restrict__ counter) {
-  zshift(c, A, Wt, upd, counter);
+  zshift(c, c, A, Wt, upd, counter);
   pdl_enter();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.step_idx, 11);
+  TLSpan tl_span(S.tl, S.step_idx, 11);
   if (LA ? !S.pend : S.done) return;
   const int64_t m = S.m, n = S.n, lda = S.lda;
   const int64_t n_s = LA ? S.pend_ns : S.n_s;
@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
   __shared__ int s_item, s_flag;
   const int tid = threadIdx.x;
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.step_idx, 5);
+  TLSpan tl_span(S.tl, S.step_idx, 5);
   const int64_t m = S.m, n = S.n, lda = S.lda;
   // ---- phase 1: the pending update of the previous step ----
   const bool pend = S.la && S.pend;
@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
       __threadfence();
       atomicAdd(&colcnt[it / ntx], 1u);  // (column tile it / ntx: phase 2's tile of the same columns)
       s_flag = (atomicAdd(&ctr[1], 1u) == (unsigned)ntb - 1);
-      if (g_tl_on) atomicMax(&g_tl[(S.step_idx & 63) * 32 + 29], (unsigned long long)gtimer());  // phase 1 end
+      if (S.tl) atomicMax(&S.tl[(S.step_idx & 63) * 32 + 29], (unsigned long long)gtimer());  // phase 1 end
     }
     __syncthreads();
     if (s_flag) {  // every tile has read the flags
@@ -664,8 +664,8 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
         s_pk = 0;
       }
       s_flag = (s_pk > 0) || !c->q1_fail;
-      if (g_tl_on) atomicMin(&g_tl[(S.step_idx & 63) * 32 + 28], (unsigned long long)gtimer());  // Q1 seen
-      if (g_tl_on && S.step_idx == 20 && blockIdx.x < 256) g_tl[2048 + blockIdx.x * 4 + 0] = gtimer();
+      if (S.tl) atomicMin(&S.tl[(S.step_idx & 63) * 32 + 28], (unsigned long long)gtimer());  // Q1 seen
+      if (S.tl && S.step_idx == 20 && blockIdx.x < 256) S.tl[2048 + blockIdx.x * 4 + 0] = gtimer();
     }
     __syncthreads();
     if (s_flag) {
@@ -707,13 +707,13 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
           __syncthreads();
         }
         if (it >= ng) {
-          if (tid == 0 && g_tl_on) atomicMax(&g_tl[(S.step_idx & 63) * 32 + 31], (unsigned long long)gtimer());
-          if (tid == 0 && g_tl_on && S.step_idx == 20 && blockIdx.x < 256) g_tl[2048 + blockIdx.x * 4 + 2] = gtimer();
+          if (tid == 0 && S.tl) atomicMax(&S.tl[(S.step_idx & 63) * 32 + 31], (unsigned long long)gtimer());
+          if (tid == 0 && S.tl && S.step_idx == 20 && blockIdx.x < 256) S.tl[2048 + blockIdx.x * 4 + 2] = gtimer();
           break;
         }
-        if (tid == 0 && g_tl_on && S.step_idx == 20 && blockIdx.x < 256) {
-          if (g_tl[2048 + blockIdx.x * 4 + 1] == 0) g_tl[2048 + blockIdx.x * 4 + 1] = gtimer();
-          g_tl[2048 + blockIdx.x * 4 + 3] += 1;
+        if (tid == 0 && S.tl && S.step_idx == 20 && blockIdx.x < 256) {
+          if (S.tl[2048 + blockIdx.x * 4 + 1] == 0) S.tl[2048 + blockIdx.x * 4 + 1] = gtimer();
+          S.tl[2048 + blockIdx.x * 4 + 3] += 1;
         }
         const int tile = it % ntile;
         g_partial(A, s_yg, Gp, ldz, n_s, m, lda, s_pk, ncols, (int64_t)tile * TA_COLS, it / ntile, nsplit_g);
@@ -802,7 +802,7 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* __restrict__ c, double* _
                                                   int32_t* __restrict__ glist) {
   pdl_enter();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.step_idx, 7);
+  TLSpan tl_span(S.tl, S.step_idx, 7);
   if (S.done || S.cq_fail) return;
   const int64_t n_s = S.n_s, m = S.m, n = S.n, lda = S.lda;
   const int l = S.l_acc;
@@ -960,7 +960,7 @@ __global__ void __launch_bounds__(GU_T) k_guard(Ctl* __restrict__ c, double* __r
                                                 unsigned* __restrict__ counter) {
   pdl_enter();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.step_idx, 9);
+  TLSpan tl_span(S.tl, S.step_idx, 9);
   const int cnt = c->gcount;
   if (S.done || cnt == 0) return;
   const int64_t m = S.m, lda = S.lda, n_s = S.n_s;
@@ -1079,146 +1079,5 @@ __global__ void __launch_bounds__(256) k_guard_norms(Ctl* __restrict__ c, const 
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.n; j += (int64_t)gridDim.x * blockDim.x)
       upd[j] = 0;
 }
-
-// ---------------------------------------------------------------------------
-// Persistent form of C -= Y Wt: one CTA per SM walks a contiguous range of
-// (row block, 32-column tile) work items; the 128 x 68 Y block stays in shared
-// memory while the CTA sweeps its columns, and the next tile's C and Wt are
-// prefetched with cp.async while the current one runs on the DMMA pipe.
-// ---------------------------------------------------------------------------
-constexpr int TP_T = 256;               // 8 warps: 4 (rows) x 2 (cols), each 32 x 16
-constexpr int TP_ROWS = 128;
-constexpr int TP_COLS = 32;
-constexpr int TP_VLD = TP_ROWS + 8;     // 136
-constexpr int TP_ZLD = TP_COLS + 8;     // 40 = 8 mod 16
-constexpr int TP_CLD = TP_ROWS + 2;     // 130: fragment reads conflict-free, 16B aligned pairs
-constexpr size_t TP_SMEM = sizeof(double) * (TB_KMAX * TP_VLD + 2 * TB_KMAX * TP_ZLD + 2 * TP_COLS * TP_CLD);
-
-__global__ void __launch_bounds__(TP_T, 1) k_trail_bp(const Ctl* __restrict__ c, double* __restrict__ A,
-                                                      const double* __restrict__ Wt, int64_t ldz) {
-  if (c->done) return;
-  const int64_t n_s = c->n_s, m = c->m, n = c->n, lda = c->lda;
-  const int l = c->l_acc;
-  const int64_t c0 = c->tc0, ncols = n - c0, mp = m - n_s;
-  if (l == 0 || ncols <= 0) return;
-  const int odd = (int)(n_s & 1);
-  const int64_t nrb = ceil_div(mp + odd, TP_ROWS), ntc = ceil_div(ncols, TP_COLS);
-  const int64_t total = nrb * ntc;
-  const int64_t it0 = (int64_t)blockIdx.x * total / gridDim.x, it1 = (int64_t)(blockIdx.x + 1) * total / gridDim.x;
-  if (it0 >= it1) return;
-  const int lp4 = (l + 3) / 4 * 4;
-  extern __shared__ __align__(16) double tps[];
-  double* vs = tps;                                   // [68][136]  Y[r][t]
-  double* zsb[2] = {vs + TB_KMAX * TP_VLD, vs + TB_KMAX * TP_VLD + TB_KMAX * TP_ZLD};
-  double* csb[2] = {zsb[1] + TB_KMAX * TP_ZLD, zsb[1] + TB_KMAX * TP_ZLD + TP_COLS * TP_CLD};
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int wm = wid & 3, wn = wid >> 2;
-  const double* Yp = A + n_s * lda + n_s;
-  double* Cp = A + n_s + c0 * lda;
-
-  auto load_y = [&](int64_t rbk) {
-    const int64_t row0 = rbk * TP_ROWS - odd;
-    const int rp = tid & 63, tb = tid >> 6;
-    const int64_t r = row0 + 2 * rp;
-    const int64_t gr = n_s + r;
-    const int bytes = (gr + 1 < m) ? 16 : ((gr < m) ? 8 : 0);
-    for (int t = tb; t < l; t += 4) cp_async16(vs + t * TP_VLD + 2 * rp, Yp + r + (int64_t)t * lda, bytes);
-  };
-  auto fix_y = [&](int64_t rbk) {  // after the copy landed
-    const int64_t row0 = rbk * TP_ROWS - odd;
-    if (row0 < 72 || row0 + TP_ROWS > mp)
-      for (int e = tid; e < l * TP_ROWS; e += TP_T) {
-        const int t = e >> 7, rr = e & 127;
-        const int64_t r = row0 + rr;
-        if (r < 0 || r >= mp || r <= t) vs[t * TP_VLD + rr] = (r == t) ? 1.0 : 0.0;
-      }
-    for (int e = tid; e < (lp4 - l) * TP_ROWS; e += TP_T) vs[(l + e / TP_ROWS) * TP_VLD + e % TP_ROWS] = 0.0;
-  };
-  auto load_tile = [&](int64_t it, int buf) {  // C (128 x 32) and Wt (68 x 32) of work item it
-    const int64_t rbk = it / ntc, ctk = it % ntc;
-    const int64_t row0 = rbk * TP_ROWS - odd, col0 = ctk * TP_COLS;
-    {
-      const int rp = tid & 63, cb = tid >> 6;  // 64 row pairs x 4 column lanes
-      const int64_t r = row0 + 2 * rp;
-      const int64_t gr = n_s + r;
-      const int bytes = (gr + 1 < m) ? 16 : ((gr < m) ? 8 : 0);
-      for (int cc = cb; cc < TP_COLS; cc += 4)
-        cp_async16(csb[buf] + cc * TP_CLD + 2 * rp, Cp + r + (col0 + cc) * lda, (col0 + cc < ncols) ? bytes : 0);
-    }
-    {
-      const int cp2 = tid & 15, tz = tid >> 4;  // 16 column pairs x 16 row lanes
-      for (int t = tz; t < l; t += 16)
-        cp_async16(zsb[buf] + t * TP_ZLD + 2 * cp2, Wt + (int64_t)t * ldz + col0 + 2 * cp2, 16);
-    }
-  };
-
-  int64_t cur_rb = it0 / ntc;
-  load_y(cur_rb);
-  load_tile(it0, 0);
-  cp_async_commit();
-  for (int64_t it = it0; it < it1; ++it) {
-    const int buf = (int)((it - it0) & 1);
-    const int64_t rbk = it / ntc, ctk = it % ntc;
-    const bool next_same_rb = (it + 1 < it1) && ((it + 1) / ntc == rbk);
-    if (it + 1 < it1 && next_same_rb) {
-      load_tile(it + 1, buf ^ 1);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    if (it == it0 || rbk != cur_rb) {
-      cur_rb = rbk;
-      fix_y(rbk);
-    }
-    double* zs = zsb[buf];
-    const double* cs = csb[buf];
-    for (int e = tid; e < (lp4 - l) * TP_COLS; e += TP_T) zs[(l + e / TP_COLS) * TP_ZLD + e % TP_COLS] = 0.0;
-    __syncthreads();
-    const int64_t row0 = rbk * TP_ROWS - odd, col0 = ctk * TP_COLS;
-    double acc[4][2][2];
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const int rr = wm * 32 + mt * 8 + (lane >> 2);
-        const int cc = wn * 16 + nt * 8 + 2 * (lane & 3);
-        acc[mt][nt][0] = cs[cc * TP_CLD + rr];
-        acc[mt][nt][1] = cs[(cc + 1) * TP_CLD + rr];
-      }
-    for (int ks = 0; ks < lp4; ks += 4) {
-      const int t = ks + (lane & 3);
-      double af[4], bf[2];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) af[mt] = -vs[t * TP_VLD + wm * 32 + mt * 8 + (lane >> 2)];
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) bf[nt] = zs[t * TP_ZLD + wn * 16 + nt * 8 + (lane >> 2)];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
-    }
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      const int64_t r = row0 + wm * 32 + mt * 8 + (lane >> 2);
-      if (r < 0 || r >= mp) continue;
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const int64_t cc = col0 + wn * 16 + nt * 8 + 2 * (lane & 3);
-        double* p = Cp + r + cc * lda;
-        if (cc < ncols) p[0] = acc[mt][nt][0];
-        if (cc + 1 < ncols) p[lda] = acc[mt][nt][1];
-      }
-    }
-    __syncthreads();
-    if (it + 1 < it1 && !next_same_rb) {  // new row block: reload Y (and the tile) after this one
-      load_y((it + 1) / ntc);
-      load_tile(it + 1, buf ^ 1);
-      cp_async_commit();
-    }
-  }
-}
-
 
 }  // namespace dmqr

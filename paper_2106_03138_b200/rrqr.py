@@ -300,7 +300,7 @@ class DeviceFactor:
     def debug_ctl(self) -> dict:
         """Decision state of the last step (debug aid)."""
         import torch
-        out = torch.zeros(16 + 4 * 72 + 4, dtype=torch.int64, device=self.buf.device)
+        out = torch.zeros(16 + 4 * 72 + 5, dtype=torch.int64, device=self.buf.device)
         _check(_lib.load().dmqr_debug_ctl(self.workspace.data_ptr(), out.data_ptr(),
                                           C.c_void_p(torch.cuda.current_stream().cuda_stream)))
         v = out.cpu().numpy()
@@ -312,6 +312,7 @@ class DeviceFactor:
         d["cand"], d["sel"] = v[16:88].tolist(), v[88:160].tolist()
         d["sw_a"], d["sw_b"] = v[160:232].tolist(), v[232:304].tolist()
         d["cq_diag"] = v[304:308].view(np.float64).tolist()
+        d["cq_fail"], d["tc0"] = int(v[308]) // 1000000, int(v[308]) % 1000000
         return d
 
 

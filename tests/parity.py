@@ -30,6 +30,8 @@ def robust_prefix(ref: O.OracleResult):
 
 def diag_close(d_gpu, d_ref, n) -> tuple[bool, float]:
     """| |d_gpu| - |d_ref| | <= 1e-10 |d_ref| + n eps |d_1|."""
+    if hasattr(d_gpu, "cpu"):  # a device result (torch)
+        d_gpu = d_gpu.cpu().numpy()
     a, b = np.abs(np.asarray(d_gpu)), np.abs(np.asarray(d_ref))
     k = min(a.size, b.size)
     if k == 0:

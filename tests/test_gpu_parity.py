@@ -30,11 +30,16 @@ def _steps(log):
              s.k_max if not s.fell_back_to_scalar else -1) for s in log]
 
 
-def _compare(A, res, ref, label):
+def _compare(A, res, ref, label, require_full=False, min_cut=0):
     """Exact decisions up to the first ambiguous one (all of them when the run is
-    robust), |diag R| to 1e-10 there, residual/orthogonality <= 50 n eps always."""
+    robust, or when ``require_full``: inputs the reference itself decides stably,
+    SURVEY App. B), at least ``min_cut`` columns, |diag R| to 1e-10 there,
+    residual/orthogonality <= 50 n eps always."""
     m, n = A.shape
     cut, full = parity.robust_prefix(ref)
+    assert cut >= min(min_cut, ref.n_factored), f"{label}: robust prefix {cut} < {min_cut} (vacuous gate)"
+    if require_full:
+        cut, full = ref.n_factored, True
     assert np.array_equal(res.perm.forward[:cut], ref.forward[:cut]), f"{label}: pivots differ before column {cut}"
     want = [s for s in ref.steps if s.n_s < cut]
     assert _steps(res.step_log[:len(want)]) == _steps(want), f"{label}: step log differs before column {cut}"
@@ -74,7 +79,14 @@ def test_golden_case(name):
             ref = (O.qrdm2 if meta["algo"] == "qrdm2" else O.qrdm)(A, margins=True, **kw)
     # the oracle itself is pinned to the golden vectors (test_oracle_golden.py)
     assert np.array_equal(ref.forward, G.case_field(name, "forward"))
-    _compare(A, res, ref, name)
+    # BASELINE cfg1 is stable under 1-ulp input perturbation:
+    # with an active stop rule the whole run must match, rank included (with
+    # StopRule.NONE the run continues into the 1e-18 noise block, whose pivots
+    # are round-off-determined).  Exact ties (identity, duplicate
+    # columns, Kahan) have a zero margin by construction; everything else must be
+    # robust for at least its first pivot.
+    tie = name.split("/")[-1].startswith(("identity", "duplicate", "kahan")) or "/kahan" in name
+    _compare(A, res, ref, name, require_full=name in ("cfg1/qrdm", "cfg1/qrdm2"), min_cut=0 if tie else 1)
 
 
 @pytest.mark.parametrize("seed", range(12))
@@ -334,10 +346,12 @@ def test_cfg2_full_size_vs_oracle(algo):
     A = inputs.cfg2(seed=1)
     res = (qrdm2 if algo == "qrdm2" else qrdm)(A, device=True)
     ref = (O.qrdm2 if algo == "qrdm2" else O.qrdm)(A, margins=True)
-    cut, full = parity.robust_prefix(ref)
-    assert np.array_equal(np.asarray(res.perm.forward)[:cut], ref.forward[:cut])
-    if full:
-        assert np.array_equal(np.asarray(res.perm.forward), ref.forward) and res.rank == ref.rank
+    # cfg2 is decided stably by the reference (identical under a
+    # 1-ulp perturbation): the whole run must match
+    assert np.array_equal(np.asarray(res.perm.forward), ref.forward) and res.rank == ref.rank
+    assert _steps(res.step_log) == _steps(ref.steps)
+    ok, worst = parity.diag_close(res.r_diagonal(), ref.r_diagonal(), 4096)
+    assert ok, f"|diag R| off by {worst:.3g} x tolerance"
     assert res.rank == 4096 and len(res.step_log) == len(ref.steps)
     resid, orth = _device_residuals(torch.as_tensor(A, device="cuda"), res)
     bound = 50 * 4096 * O.EPS

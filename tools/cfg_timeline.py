@@ -25,7 +25,7 @@ for _ in range(2):
     f = rrqr.factorize(None, work=work, max_steps=ms)
     torch.cuda.synchronize()
 tl_all = np.zeros(64 * 32 + 1024, dtype=np.int64)
-_lib.load().dmqr_debug_timeline(tl_all.ctypes.data_as(C.c_void_p))
+_lib.load().dmqr_debug_timeline(f.workspace.data_ptr(), int(A.shape[0]), int(A.shape[1]), tl_all.ctypes.data_as(C.c_void_p))
 tl = tl_all[:2048].reshape(64, 16, 2).astype(np.float64)
 sp = tl_all[2048:].reshape(256, 4).astype(np.float64)
 ok = (tl[:, :, 0] > 0) & (tl[:, :, 0] < 2 ** 62) & (tl[:, :, 1] > 0)

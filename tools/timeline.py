@@ -35,7 +35,7 @@ for i, r in enumerate(g[:12]):
 # ---- kernel spans (dmqr_debug_timeline): start after the dependency wait, end at the last CTA exit
 names = ["select", "gram", "gfinish", "swap", "panel", "spare", "ygemm", "trail_w", "trail_a", "guard", "step_end"]
 tl = np.zeros(64 * 32 + 1024, dtype=np.int64)  # (the last 1024: k_spare per-CTA debug)
-_lib.load().dmqr_debug_timeline(tl.ctypes.data_as(C.c_void_p))
+_lib.load().dmqr_debug_timeline(f.workspace.data_ptr(), int(A.shape[0]), int(A.shape[1]), tl.ctypes.data_as(C.c_void_p))
 tl = tl[:2048].reshape(64, 32)
 ns = int(f.info.n_steps)
 U64MAX = np.int64(-1)
