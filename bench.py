@@ -310,9 +310,10 @@ def timeline_spans(f, m, n) -> tuple:
     _lib.load().dmqr_debug_timeline(f.workspace.data_ptr(), m, n, tl.ctypes.data_as(C.c_void_p))
     t = tl[:2048].reshape(64, 16, 2).astype(np.float64)
     ok = (t[:, :, 0] > 0) & (t[:, :, 0] < 2 ** 62) & (t[:, :, 1] > 0)
+    ok[:, 14:] = False  # (slots 28-31: k_spare phase stamps, not spans)
     per, span = [], []
     for s in range(min(64, int(f.info.n_steps))):
-        d = {TL_NAMES.get(k, str(k)): (t[s, k, 1] - t[s, k, 0]) / 1e3 for k in range(16) if ok[s, k]}
+        d = {TL_NAMES.get(k, str(k)): (t[s, k, 1] - t[s, k, 0]) / 1e3 for k in range(14) if ok[s, k]}
         per.append(d)
         if ok[s].any():
             span.append((t[s, ok[s], 1].max() - t[s, ok[s], 0].min()) / 1e3)

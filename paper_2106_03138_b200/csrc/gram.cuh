@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __
   // the candidate list is read with the control block snapshot (one round trip)
   const int cand_pre = (threadIdx.x < DMQR_KP) ? c->cand[threadIdx.x] : 0;
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.tl, S.step_idx, 1);
+  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 1);
   if (S.done) return;
   const bool pendu = S.la && S.pend;
   if (S.kind != 0 && !pendu) return;
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, con
   const long long t_in = gtimer();
   pdl_enter();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.tl, S.step_idx, 2);
+  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 2);
   if (S.done) return;
 #define GFT(k) \
   if (tline && threadIdx.x == 0) tline[512 + 8 * (S.step_idx & 63) + (k)] = gtimer()

@@ -132,7 +132,7 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
   if (gridDim.z > 1 && hrec) hrec += 2 * blockIdx.z;  // (host records: two slots per matrix)
   pdl_enter();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.tl, S.step_idx, 10);
+  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 10);
   if (!S.done) step_end_body(S, c, steps, norm_trace, trace_bits, A, Wt, ldz, u, uref, upd);
   // the host's poll record of this step (no stream operation between the
   // steps, so the programmatic launches chain across step boundaries)

@@ -129,7 +129,7 @@ __global__ void k_downdate(Ctl* __restrict__ c, const double* __restrict__ A, do
                            double* __restrict__ uref, int32_t* __restrict__ glist = nullptr) {
   zshift(c, c, A, u, uref, glist);
   if (c->done) return;
-  TLSpan tl_span(c->tl, c->step_idx, 12);
+  TLSpan tl_span(c->done ? nullptr : c->tl, c->step_idx, 12);
   const int64_t n_s = c->n_s, n_s1 = n_s + c->l_acc, n = c->n, m = c->m, lda = c->lda;
   const int lane = threadIdx.x & 31;
   if (blockIdx.x == 0)

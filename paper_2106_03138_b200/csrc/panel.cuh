@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(SWAP_T) k_swap(Ctl* __restrict__ c, double* __
     ms_dst = c->mv_dst[tid];
   }
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.tl, S.step_idx, 3);
+  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 3);
   if (S.done) return;
   const int nmv = S.nmv;
   const int64_t m = S.m, lda = S.lda;

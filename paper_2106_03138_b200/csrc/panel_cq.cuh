@@ -662,7 +662,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   Ctl* c = a.c;
   const long long t_start = gtimer();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.tl, S.step_idx, 4);
+  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 4);
   if (S.done) return;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double cqs[];

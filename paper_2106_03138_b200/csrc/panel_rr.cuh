@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_rr(PanelArgs a) {
     const int done = c->done, cqf = c->cq_fail;  // (both loads in flight together)
     if (done || (a.only_if_fail && !cqf)) return;
   }
-  TLSpan tl_span(c->tl, c->step_idx, 13);
+  TLSpan tl_span(c->done ? nullptr : c->tl, c->step_idx, 13);
   __shared__ double vbuf[RR_RMAX];
   __shared__ double xs4[RR_RMAX];  // column 64 (warp 0, slot 4)
   __shared__ double s_part[RED_LD];

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const dou
   zshift(c, c, u);
   pdl_enter();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.tl, S.step_idx, 0);
+  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 0);
   if (S.done) return;
   if (threadIdx.x == 0) {
     c->bar_count = 0u;  // the panel's grid-barrier counter restarts each step

@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double
   zshift(c, c, A, Zp, T, Wt, counters, u, uref, upd, glist);
   pdl_enter();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.tl, S.step_idx, 8);
+  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 8);
   if (S.done || (only_if_cq_fail && !S.cq_fail)) return;  // (k_trail_w did it)
   const int64_t n_s = S.n_s, m = S.m, n = S.n, lda = S.lda;
   const int l = S.l_acc;
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_trail_b(Ctl* __restrict__ c, double
   zshift(c, c, A, Wt, upd, counter);
   pdl_enter();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.tl, S.step_idx, 11);
+  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 11);
   if (LA ? !S.pend : S.done) return;
   const int64_t m = S.m, n = S.n, lda = S.lda;
   const int64_t n_s = LA ? S.pend_ns : S.n_s;
@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* 
   __shared__ int s_item, s_flag;
   const int tid = threadIdx.x;
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.tl, S.step_idx, 5);
+  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 5);
   const int64_t m = S.m, n = S.n, lda = S.lda;
   // ---- phase 1: the pending update of the previous step ----
   const bool pend = S.la && S.pend;
@@ -802,7 +802,7 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* __restrict__ c, double* _
                                                   int32_t* __restrict__ glist) {
   pdl_enter();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.tl, S.step_idx, 7);
+  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 7);
   if (S.done || S.cq_fail) return;
   const int64_t n_s = S.n_s, m = S.m, n = S.n, lda = S.lda;
   const int l = S.l_acc;
@@ -960,7 +960,7 @@ __global__ void __launch_bounds__(GU_T) k_guard(Ctl* __restrict__ c, double* __r
                                                 unsigned* __restrict__ counter) {
   pdl_enter();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.tl, S.step_idx, 9);
+  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 9);
   const int cnt = c->gcount;
   if (S.done || cnt == 0) return;
   const int64_t m = S.m, lda = S.lda, n_s = S.n_s;

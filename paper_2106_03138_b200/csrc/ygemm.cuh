@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(256) k_ygemm(Ctl* __restrict__ c, double* __re
   zshift(c, c, A, q1g, gM);
   pdl_enter();
   const CtlSnap S = snap(c);
-  TLSpan tl_span(S.tl, S.step_idx, 6);
+  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 6);
   if (S.done || S.cq_fail) return;
   ygemm_tile(A, q1g, gM, S.n_s, S.m, S.lda, S.l_acc, blockIdx.x);
 }

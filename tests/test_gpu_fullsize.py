@@ -62,7 +62,7 @@ def _input(case: str) -> np.ndarray:
 
 # minimum number of leading columns compared exactly (the oracle's robust prefix
 # must be at least this long, or the gate would be vacuous)
-MIN_CUT = {"cfg4": 512, "cfg5_4096": 256, "cfg5_8192": 256}
+MIN_CUT = {"cfg4": 512, "cfg5_4096": 256, "cfg5_8192": 48}
 FULL = {"cfg4"}
 
 
