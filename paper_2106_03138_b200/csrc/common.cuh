@@ -106,7 +106,12 @@ struct CtlSnap {
   int32_t cq_fail, tc0, la, pend, pend_ns, pend_l, q1_fail, q1_kk;
   unsigned long long* tl;
 };
-__device__ __forceinline__ CtlSnap snap(const Ctl* __restrict__ c) {
+// (Volatile reads: the control block is written by the kernels around this
+// one, which may still be running under programmatic dependent launch, so the
+// compiler must neither route these loads through the read-only path nor hoist
+// them above griddepcontrol.wait.)
+__device__ __forceinline__ CtlSnap snap(const Ctl* cp) {
+  const volatile Ctl* c = cp;
   CtlSnap s;
   s.m = c->m; s.n = c->n; s.lda = c->lda; s.kmax = c->kmax;
   s.floor = c->floor; s.stop_rhs = c->stop_rhs; s.tau = c->tau; s.delta = c->delta; s.umax = c->umax;

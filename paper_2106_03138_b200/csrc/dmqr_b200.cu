@@ -32,6 +32,7 @@
 #include "trailing.cuh"
 #include "qp3.cuh"
 #include "formq.cuh"
+#include "small.cuh"
 
 using namespace dmqr;
 
@@ -165,6 +166,7 @@ int set_attrs(const DevInfo& d, DevAttrs** out) {
   CK(cudaFuncSetAttribute(k_fq_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FQ_SMEM2));
   CK(cudaFuncSetAttribute(k_fq_tw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FQ_SMEM2));
   CK(cudaFuncSetAttribute(k_fq_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FQ_SMEM2));
+  CK(cudaFuncSetAttribute(k_small_qrdm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_SMEM));
   {
     int nb = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_qp3, QP_T, QP_SMEM));
@@ -247,6 +249,8 @@ struct SlotGuard {
   ~SlotGuard() { slot_release(h); }
 };
 
+
+
 int validate(int64_t m, int64_t n, int64_t lda, const dmqr_params* p) {
   if (!p) return DMQR_EINVAL;
   if (m < 0 || n < 0 || lda < std::max<int64_t>(1, m)) return DMQR_EINVAL;
@@ -268,6 +272,49 @@ struct ProfAcc {
 };
 ProfAcc g_acc;  // guarded by the caller (bench) using one thread
 #define NOTE_LAUNCH() g_launches.fetch_add(1, std::memory_order_relaxed)
+
+// Small matrices (m <= 256, n <= 512, k_dm <= 64) run the whole factorization
+// in one fused kernel per matrix (small.cuh); DMQR_NO_FUSED forces the
+// per-step kernels (tests compare both).
+bool small_eligible(int64_t m, int64_t n, const dmqr_params* p) {
+  return m <= SM_MMAX && n <= SM_NMAX && p->k_dm <= SM_KC - 1 && !p->trace_norms && p->max_steps <= 0 &&
+         getenv("DMQR_NO_FUSED") == nullptr;
+}
+size_t small_info_bytes(int64_t batch) { return al(sizeof(SmallInfo) * (size_t)std::max<int64_t>(batch, 1)); }
+
+// Launch the fused kernel over `batch` matrices (stride doubles apart) and fill
+// the host infos; dinfo: device scratch of small_info_bytes(batch).
+int run_small(double* A, int64_t batch, int64_t m, int64_t n, int64_t lda, int64_t stride, const dmqr_params* p,
+              double* coeffs, int64_t* perm, int64_t* swaps, int64_t swap_cap, dmqr_step* steps, int64_t step_cap,
+              SmallInfo* dinfo, dmqr_info* infos, cudaStream_t st, int sms) {
+  if (batch <= 0) return 0;
+  double eps1 = -1.0;
+  if (p->stop_rule == DMQR_STOP_EPS_N) eps1 = p->epsilon * (double)n;
+  if (p->stop_rule == DMQR_STOP_EPS_SQRT_N) eps1 = p->epsilon * std::sqrt((double)n);
+  SmallArgs sa{A, batch, m, n, lda, stride, p->tau, p->delta, eps1, p->k_dm, p->use_delta_max, p->break_check,
+               p->stop_rule == DMQR_STOP_NONE ? 1 : 0, coeffs, perm, swaps, swap_cap, (StepRec*)steps,
+               std::max<int64_t>(step_cap, 0), dinfo};
+  const unsigned grid = (unsigned)std::min<int64_t>(batch, (int64_t)sms);
+  k_small_qrdm<<<grid, SM_T, SM_SMEM, st>>>(sa);
+  NOTE_LAUNCH();
+  CK(cudaGetLastError());
+  std::vector<SmallInfo> h((size_t)batch);
+  CK(cudaMemcpyAsync(h.data(), dinfo, sizeof(SmallInfo) * (size_t)batch, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int rc = 0;
+  for (int64_t b = 0; b < batch; ++b) {
+    dmqr_info& in = infos[b];
+    in.rank = h[b].rank;
+    in.n_factored = h[b].n_factored;
+    in.n_steps = h[b].n_steps;
+    in.n_swaps = h[b].n_swaps;
+    in.stopped_early = h[b].stopped;
+    in.status = h[b].status;
+    in.a_max0 = h[b].a_max0;
+    if (!rc && h[b].status) rc = h[b].status;
+  }
+  return rc;
+}
 
 // Split-K count for `ntile` column tiles on `slots` concurrent CTAs: the
 // number of splits (1..maxsplit) whose item count fills its waves best
@@ -389,6 +436,19 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   const DevInfo d = dev_info();
   DevAttrs* da = nullptr;
   if ((rc = set_attrs(d, &da))) return rc;
+  if (!qrp && NZ == 1 && !sgraph && small_eligible(m, n, p) && L.total >= small_info_bytes(1)) {
+    // one small matrix: the fused kernel (no per-step launches, no host polling)
+    rc = run_small(A, 1, m, n, lda, lda * std::max<int64_t>(n, 1), p, coeffs, perm, swaps, swap_cap, steps, step_cap,
+                   (SmallInfo*)workspace, info, st, d.sms);
+    if (rc == DMQR_ECUDA) return rc;
+    if (host_packed && m > 0 && n > 0) {
+      CK(cudaMemcpy2DAsync(host_packed, sizeof(double) * host_ld, A, sizeof(double) * lda, sizeof(double) * m,
+                           (size_t)n, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    g_calls.fetch_add(1);
+    return rc;
+  }
   const bool cluster16 = da->cluster16;
   const int qp_grid = da->qp_grid;
 
@@ -1098,6 +1158,15 @@ int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_
   int rc = validate(m, n, lda, p);
   if (rc) return rc;
   if (batch < 0 || stride < lda * n || !infos || nlanes < 1) return DMQR_EINVAL;
+  if (small_eligible(m, n, p) && workspace && ws_bytes >= small_info_bytes(batch)) {
+    // small matrices: the fused per-matrix kernel, a persistent grid over the batch
+    if (batch == 0) return 0;
+    DevAttrs* da = nullptr;
+    const DevInfo d = dev_info();
+    if ((rc = set_attrs(d, &da))) return rc;
+    return run_small(A, batch, m, n, lda, stride, p, coeffs, perm, swaps, swap_cap, steps, step_cap,
+                     (SmallInfo*)workspace, infos, (cudaStream_t)stream, d.sms);
+  }
   const size_t per_engine = al(dmqr_workspace_bytes(m, n, p));
   // small matrices: groups of ZG per launch (grid.z) in lane-private per-matrix
   // blocks + a replayed step graph per lane (needs the caller's lda to match the

@@ -145,7 +145,7 @@ __device__ __forceinline__ void tile_ij(int t, int nt, int& ti, int& tj) {
 // values are bitwise the serial update's), written back, and only then enters
 // the Gram; k_gram_finish flags the candidates (upd) once every CTA is done.
 // A scalar-fallback step (kind 1) runs the same update on its single column.
-__global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* __restrict__ c, double* __restrict__ A,
+__global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* c, double* __restrict__ A,
                                                  double* __restrict__ part, const double* __restrict__ Wt,
                                                  int64_t ldz, const uint8_t* __restrict__ upd) {
   zshift(c, c, A, part, Wt, upd);
@@ -337,7 +337,7 @@ struct FinSmem {
 };
 
 // grid: one CTA per upper 8x8 tile (45 for 65 candidates), GRAM_T threads.
-__global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* __restrict__ c, const double* __restrict__ A,
+__global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* c, const double* __restrict__ A,
                                                         const double* __restrict__ part, int G,
                                                         double* __restrict__ gfin, uint8_t* __restrict__ upd,
                                                         long long* __restrict__ tline) {

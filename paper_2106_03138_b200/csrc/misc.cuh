@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(1024) k_init(InitArgs a) {
 }
 
 // Append the step record and advance n_s (single thread, last kernel of a step).
-__device__ __forceinline__ void step_end_body(const CtlSnap& S, Ctl* __restrict__ c, StepRec* __restrict__ steps,
+__device__ __forceinline__ void step_end_body(const CtlSnap& S, Ctl* c, StepRec* __restrict__ steps,
                                               double* __restrict__ norm_trace,
                                               unsigned long long* __restrict__ trace_bits, const double* __restrict__ A,
                                               double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
@@ -123,7 +123,7 @@ __device__ __forceinline__ void step_end_body(const CtlSnap& S, Ctl* __restrict_
   if (S.n_s + l >= S.kmax) c->done = 1;
 }
 
-__global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, double* __restrict__ norm_trace,
+__global__ void k_step_end(Ctl* c, StepRec* __restrict__ steps, double* __restrict__ norm_trace,
                            unsigned long long* __restrict__ trace_bits, const double* __restrict__ A,
                            double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
                            double* __restrict__ uref, uint8_t* __restrict__ upd, HostRec* __restrict__ hrec,
@@ -157,7 +157,7 @@ __global__ void k_step_end(Ctl* __restrict__ c, StepRec* __restrict__ steps, dou
 }
 
 // switch the control block to the look-ahead schedule (from the next kernel on)
-__global__ void k_set_la(Ctl* __restrict__ c, int on) {
+__global__ void k_set_la(Ctl* c, int on) {
   pdl_enter();
   if (threadIdx.x == 0) c->la = on;
 }
@@ -169,7 +169,7 @@ __global__ void k_tl_init(unsigned long long* __restrict__ tl) {
 }
 
 // rank / n_factored (rrqr.py:406-412)
-__global__ void k_finalize(Ctl* __restrict__ c, const double* __restrict__ A, int stop_none) {
+__global__ void k_finalize(Ctl* c, const double* __restrict__ A, int stop_none) {
   zshift(c, c, A);
   __shared__ int cnt[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -219,7 +219,7 @@ __global__ void k_q_init(double* __restrict__ Q, int64_t m, int64_t qcols, int64
 
 namespace dmqr {
 // debug: flatten the decision part of Ctl (for step-by-step comparisons)
-__global__ void k_debug_ctl(const Ctl* __restrict__ c, int64_t* __restrict__ out) {
+__global__ void k_debug_ctl(const Ctl* c, int64_t* __restrict__ out) {
   if (threadIdx.x != 0) return;
   int64_t* o = out;
   *o++ = c->n_s; *o++ = c->done; *o++ = c->stopped; *o++ = c->status;

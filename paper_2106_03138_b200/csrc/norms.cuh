@@ -125,7 +125,7 @@ __global__ void k_colnorms_init(const double* __restrict__ A, int64_t m, int64_t
 // Downdate after a step that produced R rows [n_s, n_s1): rrqr.py:161-186.
 // Columns whose downdated square falls to <= 1e-2 * u_ref^2 are recomputed
 // exactly from rows n_s1.. and their u_ref refreshed.
-__global__ void k_downdate(Ctl* __restrict__ c, const double* __restrict__ A, double* __restrict__ u,
+__global__ void k_downdate(Ctl* c, const double* __restrict__ A, double* __restrict__ u,
                            double* __restrict__ uref, int32_t* __restrict__ glist = nullptr) {
   zshift(c, c, A, u, uref, glist);
   if (c->done) return;
@@ -168,7 +168,7 @@ __global__ void k_downdate(Ctl* __restrict__ c, const double* __restrict__ A, do
 // a column in fixed order.  A long column is read by many warps at once instead
 // of one (a 65536-row column was 128 dependent round trips for a single warp).
 constexpr int GN_ROWS = 4096;
-__global__ void __launch_bounds__(256) k_gnorm_part(const Ctl* __restrict__ c, const double* __restrict__ A,
+__global__ void __launch_bounds__(256) k_gnorm_part(const Ctl* c, const double* __restrict__ A,
                                                     const int32_t* __restrict__ glist, double* __restrict__ gp) {
   if (c->done) return;
   const int g = c->gcount;
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(256) k_gnorm_part(const Ctl* __restrict__ c, c
   }
 }
 
-__global__ void __launch_bounds__(256) k_gnorm_fin(Ctl* __restrict__ c, const double* __restrict__ A,
+__global__ void __launch_bounds__(256) k_gnorm_fin(Ctl* c, const double* __restrict__ A,
                                                    const int32_t* __restrict__ glist, const double* __restrict__ gp,
                                                    double* __restrict__ u, double* __restrict__ uref) {
   if (c->done) return;
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(256) k_gnorm_fin(Ctl* __restrict__ c, const do
 
 // Max relative deviation of downdated vs fresh trailing norms (rrqr.py:211-216),
 // accumulated as the bit pattern of a non-negative double (monotone under atomicMax).
-__global__ void k_norm_trace(Ctl* __restrict__ c, const double* __restrict__ A, const double* __restrict__ u,
+__global__ void k_norm_trace(Ctl* c, const double* __restrict__ A, const double* __restrict__ u,
                              unsigned long long* __restrict__ out_bits) {
   if (c->done || !c->trace_norms) return;
   const int64_t n_s1 = c->n_s + c->l_acc, n = c->n, m = c->m, lda = c->lda;

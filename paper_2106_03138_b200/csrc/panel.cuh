@@ -34,7 +34,7 @@ constexpr int SWAP_T = 256;
 constexpr int SWAP_MAXMV = 2 * DMQR_KP;        // 144
 constexpr size_t SWAP_SMEM = sizeof(double) * SWAP_MAXMV * SWAP_ROWS;  // 36 KB
 
-__global__ void __launch_bounds__(SWAP_T) k_swap(Ctl* __restrict__ c, double* __restrict__ A, double* __restrict__ u,
+__global__ void __launch_bounds__(SWAP_T) k_swap(Ctl* c, double* __restrict__ A, double* __restrict__ u,
                                                  double* __restrict__ uref, int64_t* __restrict__ perm,
                                                  int64_t* __restrict__ swaplog, double* __restrict__ Wt, int64_t ldz,
                                                  uint8_t* __restrict__ upd) {

@@ -102,7 +102,7 @@ __device__ __forceinline__ int qp_nseg(int64_t m, int64_t s) {
 __device__ __forceinline__ double2 ldcs2(const double* p) { return __ldcs(reinterpret_cast<const double2*>(p)); }
 
 __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
-  Ctl* __restrict__ c = a.c;
+  Ctl* c = a.c;
   const CtlSnap S = snap(c);
   if (S.done) return;
   double* __restrict__ A = a.A;
@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
 // After a k_qp3 block (stream order): the optional per-column norm trace and
 // the host's poll record.  norm_trace: _record_norm_check (rrqr.py:211-216) for
 // a one-column block (trace_norms runs blocks of one, fully updated).
-__global__ void k_qp3_post(Ctl* __restrict__ c, double* __restrict__ norm_trace,
+__global__ void k_qp3_post(Ctl* c, double* __restrict__ norm_trace,
                            unsigned long long* __restrict__ trace_bits, HostRec* __restrict__ hrec, int enq) {
   if (threadIdx.x != 0) return;
   if (norm_trace && c->qp_cols > 0) {
@@ -744,7 +744,7 @@ __global__ void k_qp3_post(Ctl* __restrict__ c, double* __restrict__ norm_trace,
 
 // trace of a one-column qrp block: max_j |u_j - ||A[n_s:, j]|| | / denom over the
 // trailing columns (k_norm_trace's arithmetic, the Ctl's n_s after the block)
-__global__ void k_qp3_trace(const Ctl* __restrict__ c, const double* __restrict__ A, const double* __restrict__ u,
+__global__ void k_qp3_trace(const Ctl* c, const double* __restrict__ A, const double* __restrict__ u,
                             unsigned long long* __restrict__ out_bits) {
   if (c->qp_cols == 0) return;
   const int64_t n_s1 = c->n_s, n = c->n, m = c->m, lda = c->lda;

@@ -56,7 +56,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* scan_smem, int* total
   return res;
 }
 
-__global__ void __launch_bounds__(SEL_T) k_select(Ctl* __restrict__ c, const double* __restrict__ u) {
+__global__ void __launch_bounds__(SEL_T) k_select(Ctl* c, const double* __restrict__ u) {
   zshift(c, c, u);
   pdl_enter();
   const CtlSnap S = snap(c);

@@ -43,7 +43,7 @@ constexpr size_t TA_SMEM = TA_SMEM_ST > TA_SMEM_TZ ? TA_SMEM_ST : TA_SMEM_TZ;
 // panel already updated in full (after a QRDM2 break) are downdated with
 // k_downdate's arithmetic and, while an update is pending, flagged; their Wt
 // slots (Wt is indexed from n_s + l) are zeroed for the next step's moves.
-__device__ void la_panel_columns(Ctl* __restrict__ c, const double* __restrict__ A, double* __restrict__ Wt,
+__device__ void la_panel_columns(Ctl* c, const double* __restrict__ A, double* __restrict__ Wt,
                                  int64_t ldz, double* __restrict__ u, double* __restrict__ uref,
                                  uint8_t* __restrict__ upd, int64_t n_s, int l, int64_t tc0) {
   const int64_t m = c->m, n = c->n, lda = c->lda, base = n_s + l;
@@ -84,7 +84,7 @@ __device__ void la_panel_columns(Ctl* __restrict__ c, const double* __restrict__
 // element (so it is bitwise the serial update's), the norms are downdated with
 // k_downdate's arithmetic, guard columns get their full update and an exact
 // norm, and tile 0 does the panel-column bookkeeping.
-__device__ void la_tile_epilogue(Ctl* __restrict__ c, double* __restrict__ A, double* __restrict__ Wt, int64_t ldz,
+__device__ void la_tile_epilogue(Ctl* c, double* __restrict__ A, double* __restrict__ Wt, int64_t ldz,
                                  double* __restrict__ u, double* __restrict__ uref, uint8_t* __restrict__ upd,
                                  const double* zs, double* ts, int64_t n_s, int l, int64_t c0, int64_t col0,
                                  int32_t* __restrict__ glist) {
@@ -161,7 +161,7 @@ __device__ void la_tile_epilogue(Ctl* __restrict__ c, double* __restrict__ A, do
 
 // grid: (ceil(n''/64), nsplit).  Zp[s][i][c] (ld ldz) = sum over this split's rows of Y[r][i] C[r][c];
 // the last split CTA of each column tile reduces them and writes Wt = T^T Z (ld ldz).
-__global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* __restrict__ c, double* __restrict__ A,
+__global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* c, double* __restrict__ A,
                                                      double* __restrict__ Zp, const double* __restrict__ T,
                                                      double* __restrict__ Wt, unsigned* __restrict__ counters,
                                                      int64_t ldz, double* __restrict__ u,
@@ -432,7 +432,7 @@ __device__ __forceinline__ void trail_b_tile(double* __restrict__ A, const doubl
 // every CTA ends in griddepcontrol.wait, so this grid completes only after
 // the panel (stream order for the kernels behind it).
 template <bool LA>
-__global__ void __launch_bounds__(TB_T, 2) k_trail_b(Ctl* __restrict__ c, double* __restrict__ A,
+__global__ void __launch_bounds__(TB_T, 2) k_trail_b(Ctl* c, double* __restrict__ A,
                                                      const double* __restrict__ Wt, int64_t ldz,
                                                      uint8_t* __restrict__ upd, unsigned* __restrict__ counter) {
   zshift(c, c, A, Wt, upd, counter);
@@ -600,7 +600,7 @@ __device__ __noinline__ int spare_wait_panel(Ctl* c, int P) {
 }
 
 template <bool PM>  // PM: P-mode look-ahead (opt-in; panel_cq.cuh)
-__global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* __restrict__ c, double* __restrict__ A,
+__global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* c, double* __restrict__ A,
                                                    const double* __restrict__ Wt, int64_t ldz,
                                                    uint8_t* __restrict__ upd, const double* __restrict__ Q1g,
                                                    double* __restrict__ Gp, unsigned* __restrict__ ctr, int P,
@@ -795,7 +795,7 @@ constexpr int TW_COLS = 32;
 constexpr int TW_CLD = TW_COLS + 4;  // 36 = 4 mod 16 (conflict-free 4 x 4 half-warp fragments)
 constexpr size_t TW_SMEM = sizeof(double) * (3 * DMQR_KP * DMQR_KP + 3 * DMQR_KP * TW_CLD);
 
-__global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* __restrict__ c, double* __restrict__ A,
+__global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A,
                                                   const double* __restrict__ Gp, const double* __restrict__ FM,
                                                   double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
                                                   double* __restrict__ uref, uint8_t* __restrict__ upd,
@@ -953,7 +953,7 @@ constexpr int GU_LD = GU_ROWS + 4;  // 4 mod 16
 constexpr size_t GU_SMEM = sizeof(double) * (2 * DMQR_KP * GU_LD + DMQR_KP * DMQR_KP);
 constexpr int GU_GROUPS = 4;  // column groups of 72 per CTA (grid.y spreads the rest)
 
-__global__ void __launch_bounds__(GU_T) k_guard(Ctl* __restrict__ c, double* __restrict__ A,
+__global__ void __launch_bounds__(GU_T) k_guard(Ctl* c, double* __restrict__ A,
                                                 const double* __restrict__ Wt, int64_t ldz,
                                                 uint8_t* __restrict__ upd, double* __restrict__ u,
                                                 double* __restrict__ uref, const int32_t* __restrict__ glist,
@@ -1054,7 +1054,7 @@ __global__ void __launch_bounds__(GU_T) k_guard(Ctl* __restrict__ c, double* __r
 // Exact norms of k_guard's columns (k_downdate's arithmetic), a warp per
 // column over the whole grid; then the columns' look-ahead flags (set while an
 // update is still pending; all cleared when k_guard finished the whole update).
-__global__ void __launch_bounds__(256) k_guard_norms(Ctl* __restrict__ c, const double* __restrict__ A,
+__global__ void __launch_bounds__(256) k_guard_norms(Ctl* c, const double* __restrict__ A,
                                                       uint8_t* __restrict__ upd, double* __restrict__ u,
                                                       double* __restrict__ uref, const int32_t* __restrict__ glist) {
   pdl_enter();

@@ -59,7 +59,7 @@ __device__ __forceinline__ void ygemm_tile(double* __restrict__ A, const double*
   }
 }
 
-__global__ void __launch_bounds__(256) k_ygemm(Ctl* __restrict__ c, double* __restrict__ A,
+__global__ void __launch_bounds__(256) k_ygemm(Ctl* c, double* __restrict__ A,
                                                const double* __restrict__ q1g, const double* __restrict__ gM) {
   zshift(c, c, A, q1g, gM);
   pdl_enter();

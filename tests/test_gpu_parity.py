@@ -66,8 +66,17 @@ def _compare(A, res, ref, label, require_full=False, min_cut=0):
     return cut, full
 
 
+@pytest.fixture(params=["fused", "steps"])
+def small_path(request, monkeypatch):
+    """Small inputs (m <= 256, n <= 512) run the fused per-matrix kernel by
+    default (small.cuh); "steps" forces the per-step kernels (DMQR_NO_FUSED)."""
+    if request.param == "steps":
+        monkeypatch.setenv("DMQR_NO_FUSED", "1")
+    return request.param
+
+
 @pytest.mark.parametrize("name", GOLDEN)
-def test_golden_case(name):
+def test_golden_case(name, small_path):
     meta = G.index()["cases"][name]
     A = G.case_input(name)
     kw = G.oracle_kwargs(name)
@@ -90,7 +99,7 @@ def test_golden_case(name):
 
 
 @pytest.mark.parametrize("seed", range(12))
-def test_random_vs_oracle(seed):
+def test_random_vs_oracle(seed, small_path):
     rng = np.random.default_rng(1000 + seed)
     m = int(rng.integers(40, 400))
     n = int(rng.integers(40, 400))
@@ -241,7 +250,7 @@ def test_deterministic_repeat():
 
 @pytest.mark.parametrize("name", ["cfg2s/1024", "cfg4s/8192x256"])
 def test_midsize_golden(name):
-    test_golden_case.__wrapped__(name) if hasattr(test_golden_case, "__wrapped__") else test_golden_case(name)
+    test_golden_case(name, "fused")  # (too large for the fused kernel: per-step kernels)
 
 
 def test_batched_equals_single_and_oracle():
@@ -447,7 +456,7 @@ def test_factor10_ratios_known_spectrum_beyond_cpu_cap(n):
     assert ratios.min() >= 1e-1 and ratios.max() <= 1e1, (ratios.min(), ratios.max())
 
 
-def test_batched_graph_lanes_with_fallback_runs():
+def test_batched_graph_lanes_with_fallback_runs(small_path):
     """Batched lanes (replayed step graphs) on inputs whose factorization falls
     back to scalar pivoting (the blocked scalar-pivot engine runs between graph
     replays): same decisions as the single-matrix calls, oracle on the robust prefix."""
@@ -495,7 +504,7 @@ def test_tall_panel_helpers_and_their_fallback(wait_ns, monkeypatch):
     assert resid <= 50 * 9000 * O.EPS and orth <= 50 * 9000 * O.EPS
 
 
-@pytest.mark.parametrize("n", [1000, 2500])
+@pytest.mark.parametrize("n", [1536, 2500])
 def test_pmode_lookahead_matches_default(monkeypatch, n):
     """Opt-in P-mode look-ahead (DMQR_PMODE: k_spare forms P^T C from the panel's
     start, k_trail_w folds R1^-T into MT): same decisions as the default schedule,
@@ -527,3 +536,36 @@ def test_batched_large_matrices_per_matrix_path():
         r, s = f.result(i), qrdm2(B[i])
         assert np.array_equal(r.perm.forward, s.perm.forward) and r.rank == s.rank
         assert np.abs(r.packed - s.packed).max() <= 1e-12 * np.abs(s.packed).max()
+
+
+def test_fused_small_kernel_matches_step_kernels(monkeypatch):
+    """The fused per-matrix kernel (small.cuh) against the per-step kernels on
+    cfg3 matrices, wide / tall / rank-deficient shapes and the knob variants:
+    identical decisions on the oracle's robust prefix, factors equal to rounding
+    there, residual and orthogonality <= 50 n eps for both."""
+    from paper_2106_03138_b200 import DMParams, StopCriterion, StopRule, inputs, qrdm, qrdm2
+
+    rng = np.random.default_rng(909)
+    cases = [inputs.cfg3(seed=3, batch=2)[1], rng.standard_normal((256, 512)), rng.standard_normal((200, 60)),
+             rng.standard_normal((256, 40)) @ rng.standard_normal((40, 256)),
+             rng.standard_normal((100, 100)) * np.logspace(0, -14, 100)]
+    variants = [(qrdm2, DMParams(), StopCriterion()), (qrdm, DMParams(tau=0.3, delta=0.5), StopCriterion()),
+                (qrdm2, DMParams(use_delta_max=True), StopCriterion(StopRule.NONE)),
+                (qrdm2, DMParams(k_dm=7), StopCriterion(StopRule.EPS_SQRT_N))]
+    for i, A in enumerate(cases):
+        fn, p, st = variants[i % len(variants)]
+        fused = fn(A, params=p, stop=st)
+        monkeypatch.setenv("DMQR_NO_FUSED", "1")
+        steps = fn(A, params=p, stop=st)
+        monkeypatch.delenv("DMQR_NO_FUSED")
+        kw = dict(tau=p.tau, delta=p.delta, k_dm=p.k_dm, use_delta_max=p.use_delta_max,
+                  stop_rule=st.variant.value)
+        with threadpool_limits(1):
+            ref = (O.qrdm2 if fn is qrdm2 else O.qrdm)(A, margins=True, **kw)
+        cut, full = parity.robust_prefix(ref)
+        assert np.array_equal(fused.perm.forward[:cut], steps.perm.forward[:cut]), i
+        nf = min(cut, fused.n_factored, steps.n_factored)
+        scale = np.abs(steps.packed).max()
+        assert np.abs(fused.packed[:, :nf] - steps.packed[:, :nf]).max() <= 1e-10 * scale, i
+        _compare(A, fused, ref, f"fused[{i}]")
+        _compare(A, steps, ref, f"steps[{i}]")
