@@ -207,6 +207,9 @@ int dmqr_debug_panel_clocks(const void* workspace, int64_t m, int64_t n, int64_t
  * (sized for m x n) with DMQR_TIMELINE set (out[64 * 32 + 1024] int64 on the
  * host, globaltimer ns; see the source) */
 int dmqr_debug_timeline(const void* workspace, int64_t m, int64_t n, int64_t* out);
+/* debug: CTA 0's per-phase cycle counts of the last fused small-matrix launch
+ * run with DMQR_SMALL_CLOCKS set (out[32] int64 on the host) */
+int dmqr_debug_small_clocks(int64_t* out);
 /* Free the library's pooled pinned poll records, events and copy streams (all
  * devices).  Optional; only while no call is running.  The pool holds one entry
  * per concurrently running engine call. */

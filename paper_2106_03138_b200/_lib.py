@@ -32,6 +32,7 @@ EXPORTS = (
     "dmqr_debug_panel_clocks",
     "dmqr_debug_timeline",
     "dmqr_release_resources",
+    "dmqr_debug_small_clocks",
 )
 
 DMQR_OK, DMQR_EINVAL, DMQR_ENONFINITE, DMQR_EZEROCOL, DMQR_ECUDA, DMQR_ECAP = 0, -1, -2, -3, -4, -5
@@ -143,6 +144,8 @@ def load() -> C.CDLL:
     lib.dmqr_debug_panel_clocks.restype = C.c_int
     lib.dmqr_debug_timeline.argtypes = [P, I64, I64, P]
     lib.dmqr_debug_timeline.restype = C.c_int
+    lib.dmqr_debug_small_clocks.argtypes = [P]
+    lib.dmqr_debug_small_clocks.restype = C.c_int
     lib.dmqr_release_resources.argtypes = []
     lib.dmqr_release_resources.restype = None
     lib.dmqr_version.argtypes = []

@@ -273,6 +273,7 @@ struct ProfAcc {
 ProfAcc g_acc;  // guarded by the caller (bench) using one thread
 #define NOTE_LAUNCH() g_launches.fetch_add(1, std::memory_order_relaxed)
 
+long long* g_small_clk = nullptr;  // debug (DMQR_SMALL_CLOCKS): device phase-cycle slots
 // Small matrices (m <= 256, n <= 512, k_dm <= 64) run the whole factorization
 // in one fused kernel per matrix (small.cuh); DMQR_NO_FUSED forces the
 // per-step kernels (tests compare both).
@@ -293,7 +294,14 @@ int run_small(double* A, int64_t batch, int64_t m, int64_t n, int64_t lda, int64
   if (p->stop_rule == DMQR_STOP_EPS_SQRT_N) eps1 = p->epsilon * std::sqrt((double)n);
   SmallArgs sa{A, batch, m, n, lda, stride, p->tau, p->delta, eps1, p->k_dm, p->use_delta_max, p->break_check,
                p->stop_rule == DMQR_STOP_NONE ? 1 : 0, coeffs, perm, swaps, swap_cap, (StepRec*)steps,
-               std::max<int64_t>(step_cap, 0), dinfo};
+               std::max<int64_t>(step_cap, 0), dinfo, nullptr};
+  if (getenv("DMQR_SMALL_CLOCKS")) {  // debug: CTA 0's phase cycles (tools/small_clocks.py)
+    static long long* dclk = nullptr;  // (debug only)
+    if (!dclk) CK(cudaMalloc(&dclk, sizeof(long long) * 32));
+    CK(cudaMemsetAsync(dclk, 0, sizeof(long long) * 32, st));
+    sa.dbg = dclk;
+    g_small_clk = dclk;
+  }
   const unsigned grid = (unsigned)std::min<int64_t>(batch, (int64_t)sms);
   k_small_qrdm<<<grid, SM_T, SM_SMEM, st>>>(sa);
   NOTE_LAUNCH();
@@ -1375,6 +1383,14 @@ int dmqr_debug_timeline(const void* workspace, int64_t m, int64_t n, int64_t* ou
   const Layout L = layout(m, n);
   CK(cudaMemcpy(out, (const unsigned char*)workspace + L.tl, sizeof(unsigned long long) * TL_WORDS,
                 cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+/* debug: CTA 0's phase cycles of the last fused small-matrix launch run with
+ * DMQR_SMALL_CLOCKS set (out[16] int64 on the host; slots in small.cuh) */
+int dmqr_debug_small_clocks(int64_t* out) {
+  if (!g_small_clk) return DMQR_EINVAL;
+  CK(cudaMemcpy(out, g_small_clk, sizeof(long long) * 32, cudaMemcpyDeviceToHost));
   return 0;
 }
 

@@ -64,6 +64,7 @@ struct SmallArgs {
   StepRec* steps;   // batch x step_cap
   int64_t step_cap;
   SmallInfo* info;  // batch
+  long long* dbg;   // debug: CTA 0's cycles per phase (16 slots, accumulated) or null
 };
 
 struct SmallSmem {
@@ -79,9 +80,13 @@ struct SmallSmem {
   int cols[DMQR_KP];   // absolute column of candidate t (seed first)
   int selt[DMQR_KP];   // chosen candidate indices, in order
   int mv_dst[2 * DMQR_KP], mv_src[2 * DMQR_KP];
+  int cyc_pos[2 * DMQR_KP], cyc_beg[2 * DMQR_KP + 1];  // move cycles: new[p_i] = old[p_{i+1}]
+  int ncyc;
   int redi[2 * SM_W];
   int nmv, nsel, kmax_c, status, nsw_log;
   int brk[2];
+  int pub, brkat;      // panel dataflow: reflectors published, break column (k_s: none)
+  int prog[SM_W];      // panel dataflow: reflectors whose v each warp has loaded
   double gamma, coeff, umax;
   int seed;
 };
@@ -95,23 +100,37 @@ __device__ __forceinline__ double sm_wmax(double v) {
 
 // Scaled Euclidean norm (matrix.py:61-78) of x[0, len) (shared or global,
 // plain loads: the data may have been written by this kernel), warp-wide.
-__device__ __forceinline__ double sm_norm(const double* x, int len, int lane) {
-  double s = 0.0, a = 0.0;
-  for (int i = lane; i < len; i += 32) {
-    const double v = x[i];
-    s = fma(v, v, s);
-    a = fmax(a, fabs(v));
+// (len <= SM_MMAX: the eight row slots of a lane are unrolled, so their loads
+// are all in flight together)
+__device__ __forceinline__ double sm_norm_regs(const double (&v)[SM_MMAX / 32], int lane) {
+  double s0 = 0.0, s1 = 0.0, a = 0.0;
+#pragma unroll
+  for (int q = 0; q < SM_MMAX / 32; q += 2) {
+    s0 = fma(v[q], v[q], s0);
+    s1 = fma(v[q + 1], v[q + 1], s1);
+    a = fmax(a, fmax(fabs(v[q]), fabs(v[q + 1])));
   }
-  s = warp_sum(s);
-  a = sm_wmax(a);
+  double s = s0 + s1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+  }
   if (a == 0.0) return 0.0;
   if (norm_range_ok(a)) return sqrt(s);
   double t = 0.0;
-  for (int i = lane; i < len; i += 32) {
-    const double v = x[i] / a;
-    t = fma(v, v, t);
+#pragma unroll
+  for (int q = 0; q < SM_MMAX / 32; ++q) {
+    const double z = v[q] / a;
+    t = fma(z, z, t);
   }
   return a * sqrt(warp_sum(t));
+}
+__device__ __forceinline__ double sm_norm(const double* x, int len, int lane) {
+  double v[SM_MMAX / 32];
+#pragma unroll
+  for (int q = 0; q < SM_MMAX / 32; ++q) v[q] = (lane + 32 * q < len) ? x[lane + 32 * q] : 0.0;
+  return sm_norm_regs(v, lane);
 }
 
 // Upper 8x8 tiles (a <= b < nt) of X^T X for the columns of P (K = k4 rows,
@@ -309,23 +328,396 @@ __device__ void sm_downdate(const SmallArgs& a, double* A, int64_t lda, int m, i
     s.u[j] = 0.0;
     s.uref[j] = 0.0;
   }
-  for (int j = n_s1 + wid; j < n; j += SM_W) {
-    const double* col = A + (int64_t)j * lda;
-    double d = 0.0;
-    for (int r = n_s + lane; r < n_s1; r += 32) {
-      const double x = col[r];
-      d = fma(x, x, d);
+  // (l = n_s1 - n_s <= 65 rows: three row slots per lane; four columns per pass)
+  for (int j0 = n_s1 + 4 * wid; j0 < n; j0 += 4 * SM_W) {
+    double x[4][3];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int r = n_s + lane + 32 * q;
+        x[c][q] = (j0 + c < n && r < n_s1) ? A[(int64_t)(j0 + c) * lda + r] : 0.0;
+      }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = j0 + c;
+      const double d = warp_sum(fma(x[c][0], x[c][0], fma(x[c][1], x[c][1], x[c][2] * x[c][2])));
+      if (j >= n) continue;
+      const double uj = s.u[j], rj = s.uref[j];
+      const double sq = __dsub_rn(__dmul_rn(uj, uj), d);
+      double nu = sqrt(fmax(sq, 0.0));
+      if (sq <= __dmul_rn(1e-2, __dmul_rn(rj, rj))) {
+        nu = sm_norm(A + (int64_t)j * lda + n_s1, m - n_s1, lane);
+        if (lane == 0) s.uref[j] = nu;
+      }
+      if (lane == 0) s.u[j] = nu;
     }
-    d = warp_sum(d);
-    const double uj = s.u[j], rj = s.uref[j];
-    const double sq = __dsub_rn(__dmul_rn(uj, uj), d);
-    double nu = sqrt(fmax(sq, 0.0));
-    if (sq <= __dmul_rn(1e-2, __dmul_rn(rj, rj))) {
-      nu = sm_norm(col + n_s1, m - n_s1, lane);
-      if (lane == 0) s.uref[j] = nu;
-    }
-    if (lane == 0) s.u[j] = nu;
   }
+}
+
+// Reflector j of the panel in shared memory (make_reflector, householder.py:57-79),
+// by one warp: x = P[j][j:mp); the QRDM2 break test on its fresh norm first
+// (rrqr.py:375-379: ||work[col+1:, col+1]|| < eps_s); beta on the diagonal,
+// v[1:] = x[1:] / (x0 - beta) below it, coeff -> cf[j]; brk[j & 1] published.
+__device__ __forceinline__ void sm_reflector(SmallSmem& s, int j, int mp, double eps_s, int break_check, int lane) {
+  double* x = s.P + j * SM_LDP;
+  const double nrm = sm_norm(x + j, mp - j, lane);
+  const int brk = (break_check && j >= 1 && nrm < eps_s) ? 1 : 0;
+  if (!brk) {
+    const double x0 = x[j];
+    double beta = 0.0, cf = 0.0;
+    if (nrm > 0.0) {
+      beta = (x0 != 0.0) ? -copysign(nrm, x0) : -nrm;
+      const double rden = 1.0 / (x0 - beta);  // (v = x / (x0 - beta) as x * rden: <= 1 ulp apart)
+#pragma unroll
+      for (int q = 0; q < SM_MMAX / 32; ++q) {
+        const int r = j + 1 + lane + 32 * q;
+        if (r < mp) x[r] *= rden;
+      }
+      cf = (beta - x0) / beta;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      x[j] = beta;
+      s.cf[j] = cf;
+    }
+  }
+  if (lane == 0) s.brk[j & 1] = brk;
+}
+
+// col <- (I - cf v v^T) col on rows [j, mp) (apply_reflector_left, householder.py:82-89), one warp
+__device__ __forceinline__ void sm_apply1(double* col, const double* v, double cf, int j, int mp, int lane) {
+  constexpr int NQ = SM_MMAX / 32;
+  double vr[NQ], cr[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int r = j + 1 + lane + 32 * q;
+    const bool ok = r < mp;
+    vr[q] = ok ? v[r] : 0.0;
+    cr[q] = ok ? col[r] : 0.0;
+  }
+  double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+  for (int q = 0; q < NQ; q += 2) {
+    t0 = fma(vr[q], cr[q], t0);
+    t1 = fma(vr[q + 1], cr[q + 1], t1);
+  }
+  const double t = warp_sum(t0 + t1) + col[j];
+  const double w = cf * t;
+  __syncwarp();
+  if (lane == 0) col[j] -= w;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int r = j + 1 + lane + 32 * q;
+    if (r < mp) col[r] = fma(-vr[q], w, cr[q]);
+  }
+}
+
+// The same for the columns first, first + 8, ... (< k_s, at most 8) in one
+// pass: v is read once per row, the eight sums are reduced together
+// (16 -> 8 -> 4 lanes exchange halves, then a plain butterfly).
+__device__ __forceinline__ void sm_apply8(double* P, const double* v, double cf, int j, int mp, int first, int k_s,
+                                          int lane) {
+  constexpr int NQ = SM_MMAX / 32;
+  double vr[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int r = j + 1 + lane + 32 * q;
+    vr[q] = (r < mp) ? v[r] : 0.0;  // (rows past mp: v = 0, P rows there are zero padding or unused)
+  }
+  double t[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int c = first + SM_W * i;
+    double acc = 0.0;
+    if (c < k_s) {
+      const double* pc = P + c * SM_LDP + j + 1 + lane;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (j + 1 + lane + 32 * q < mp) acc = fma(vr[q], pc[32 * q], acc);
+    }
+    t[i] = acc;
+  }
+  // level 16: keep 4 of 8
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool hi = lane & 16;
+    const double keep = hi ? t[i + 4] : t[i], send = hi ? t[i] : t[i + 4];
+    t[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool hi = lane & 8;
+    const double keep = hi ? t[i + 2] : t[i], send = hi ? t[i] : t[i + 2];
+    t[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const bool hi = lane & 4;
+    const double keep = hi ? t[1] : t[0], send = hi ? t[0] : t[1];
+    t[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  t[0] += __shfl_xor_sync(0xffffffffu, t[0], 2);
+  t[0] += __shfl_xor_sync(0xffffffffu, t[0], 1);
+  // lane 16a + 8b + 4c holds the sum of column index 4a + 2b + c
+  double w[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const double ti = __shfl_sync(0xffffffffu, t[0], 16 * (i >> 2) + 8 * ((i >> 1) & 1) + 4 * (i & 1));
+    const int c = first + SM_W * i;
+    w[i] = (c < k_s) ? cf * (ti + P[c * SM_LDP + j]) : 0.0;
+  }
+  __syncwarp();
+  if (lane < 8) {
+    const int c = first + SM_W * lane;
+    double wl = w[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i)
+      if (lane == i) wl = w[i];
+    if (c < k_s) P[c * SM_LDP + j] -= wl;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int c = first + SM_W * i;
+    if (c < k_s) {
+      double* pc = P + c * SM_LDP + j + 1 + lane;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (j + 1 + lane + 32 * q < mp) pc[32 * q] = fma(-vr[q], w[i], pc[32 * q]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Register-resident panel (make_reflector / apply_reflector_left / the QRDM2
+// break, householder.py:57-89, rrqr.py:360-379).  Warp w keeps the panel
+// columns c = w + 8 i (i < 9) in registers, lane l rows l + 32 q (q < 8):
+// each reflector costs one block barrier, one shared-memory read of the
+// published v and register FMAs -- the panel is never swept through shared
+// memory.  Reflector j+1 is formed by the owner of column j+1 right after it
+// applied reflector j to that column, ahead of its other columns.
+// ---------------------------------------------------------------------------
+constexpr int SMP_NQ = SM_MMAX / 32;  // row slots per lane
+constexpr int SMP_NI = 9;             // column slots per warp (65 columns / 8 warps)
+constexpr int SMP_RING = 4;           // published-reflector buffers
+
+// reflector from the column held in x (rows jj.. of the panel): v -> x (beta on
+// the diagonal row), published to V (unit diagonal, zeros above and past mp),
+// coeff -> cf[jj], break flag -> brk[jj & 1]
+__device__ __forceinline__ int smp_reflector(double (&x)[SMP_NQ], SmallSmem& s, double* V, int jj, int mp,
+                                             double eps_s, int break_check, int lane) {
+  double xv[SMP_NQ];
+  double ss = 0.0, am = 0.0;
+#pragma unroll
+  for (int q = 0; q < SMP_NQ; ++q) {
+    const int r = lane + 32 * q;
+    xv[q] = (r >= jj && r < mp) ? x[q] : 0.0;
+    ss = fma(xv[q], xv[q], ss);
+    am = fmax(am, fabs(xv[q]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    am = fmax(am, __shfl_xor_sync(0xffffffffu, am, o));
+  }
+  double nrm = 0.0;
+  if (am > 0.0) {
+    if (norm_range_ok(am)) {
+      nrm = sqrt(ss);
+    } else {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < SMP_NQ; ++q) {
+        const double z = xv[q] / am;
+        t = fma(z, z, t);
+      }
+      nrm = am * sqrt(warp_sum(t));
+    }
+  }
+  const int brk = (break_check && jj >= 1 && nrm < eps_s) ? 1 : 0;  // fresh ||work[col+1:, col+1]|| < eps_s
+  double x0 = 0.0;
+#pragma unroll
+  for (int q = 0; q < SMP_NQ; ++q)
+    if (q == (jj >> 5)) x0 = __shfl_sync(0xffffffffu, x[q], jj & 31);
+  if (!brk) {
+    double beta = 0.0, cf = 0.0, rden = 0.0;
+    if (nrm > 0.0) {
+      beta = (x0 != 0.0) ? -copysign(nrm, x0) : -nrm;
+      rden = __drcp_rn(x0 - beta);  // (v = x / (x0 - beta) as x * rden: <= 1 ulp apart)
+      cf = (beta - x0) * __drcp_rn(beta);
+    }
+    double* vb = V + (jj & (SMP_RING - 1)) * SM_LDP;
+#pragma unroll
+    for (int q = 0; q < SMP_NQ; ++q) {
+      const int r = lane + 32 * q;
+      double vr = 0.0;
+      if (r > jj && r < mp) {
+        vr = x[q] * rden;
+        x[q] = vr;
+      } else if (r == jj) {
+        vr = 1.0;
+        x[q] = beta;
+      }
+      vb[r] = vr;
+    }
+    if (lane == 0) s.cf[jj] = cf;
+  }
+  return brk;
+}
+
+// publish reflector jj (or the break at jj) to the other warps of the panel
+__device__ __forceinline__ void smp_publish(SmallSmem& s, int jj, int brk, int lane) {
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_block();
+    if (brk)
+      *(volatile int*)&s.brkat = jj;
+    else
+      *(volatile int*)&s.pub = jj + 1;
+  }
+}
+
+__device__ int sm_panel_regs(SmallSmem& s, int k_s, int mp, double eps_s, int break_check, long long* dclk) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double pc[SMP_NI][SMP_NQ];
+#pragma unroll
+  for (int i = 0; i < SMP_NI; ++i) {
+    const int c = wid + SM_W * i;
+#pragma unroll
+    for (int q = 0; q < SMP_NQ; ++q) {
+      const int r = lane + 32 * q;
+      pc[i][q] = (c < k_s && r < mp) ? s.P[c * SM_LDP + r] : 0.0;
+    }
+  }
+  // Dataflow instead of one block barrier per reflector: the owner of column
+  // j+1 publishes reflector j+1 (ring of SMP_RING v buffers; a slot is reused
+  // once every warp has loaded the reflector it held) and each warp applies the
+  // reflectors to its columns in order, as they appear.  The chain of owners is
+  // the critical path; the other warps' updates trail it.
+  double* V = s.G;  // [SMP_RING][SM_LDP] published reflectors
+  if (threadIdx.x == 0) {
+    s.pub = 0;
+    s.brkat = k_s;
+  }
+  if (threadIdx.x < SM_W) s.prog[threadIdx.x] = 0;
+  __syncthreads();
+  if (wid == 0) smp_publish(s, 0, smp_reflector(pc[0], s, V, 0, mp, eps_s, break_check, lane), lane);
+  for (int j = 0; j < k_s; ++j) {
+    const bool pk = dclk && j == 16 && ((j + 1) & (SM_W - 1)) == wid && lane == 0;
+    long long c0 = pk ? clock64() : 0;
+    int p, bk;
+    for (;;) {
+      p = *(volatile int*)&s.pub;
+      bk = *(volatile int*)&s.brkat;
+      if (p > j || bk <= j) break;
+      __nanosleep(32);  // (leave the issue slots to the warp forming the next reflector)
+    }
+    __threadfence_block();
+    if (pk) dclk[16] = clock64() - c0;
+    if (bk <= j) break;
+    const double cf = s.cf[j];
+    double vq[SMP_NQ];
+#pragma unroll
+    for (int q = 0; q < SMP_NQ; ++q) vq[q] = V[(j & (SMP_RING - 1)) * SM_LDP + lane + 32 * q];
+    __syncwarp();
+    if (lane == 0) *(volatile int*)&s.prog[wid] = j + 1;  // (v_j is in registers)
+    if (pk) dclk[17] = clock64() - c0;
+    const int j1 = j + 1;
+    const bool owner = ((j1 & (SM_W - 1)) == wid) && j1 < k_s;
+    const int i1 = j1 >> 3;
+    if (owner) {  // column j+1 first: reflector j, then form and publish reflector j+1
+#pragma unroll
+      for (int i = 0; i < SMP_NI; ++i)
+        if (i == i1) {
+          if (cf != 0.0) {
+            double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < SMP_NQ; q += 2) {
+              t0 = fma(vq[q], pc[i][q], t0);
+              t1 = fma(vq[q + 1], pc[i][q + 1], t1);
+            }
+            const double w = cf * warp_sum(t0 + t1);
+#pragma unroll
+            for (int q = 0; q < SMP_NQ; ++q) pc[i][q] = fma(-vq[q], w, pc[i][q]);
+          }
+          if (pk) dclk[18] = clock64() - c0;
+          // ring slot of reflector j1 held reflector j1 - SMP_RING: every warp must have loaded it
+          if (j1 >= SMP_RING) {
+            for (;;) {
+              int mn = 0x7fffffff;
+#pragma unroll
+              for (int w = 0; w < SM_W; ++w) mn = min(mn, *(volatile int*)&s.prog[w]);
+              if (mn > j1 - SMP_RING) break;
+              __nanosleep(32);
+            }
+            __threadfence_block();
+          }
+          if (pk) dclk[19] = clock64() - c0;
+          const int bkr = smp_reflector(pc[i], s, V, j1, mp, eps_s, break_check, lane);
+          if (pk) dclk[20] = clock64() - c0;
+          smp_publish(s, j1, bkr, lane);
+          if (pk) dclk[21] = clock64() - c0;
+        }
+    }
+    if (cf == 0.0) continue;  // reflect_left with coeff 0 is a no-op (householder.py:86-87)
+    // the warp's other columns c > j: all slots computed (independent chains), dead ones masked
+    double t[SMP_NI];
+#pragma unroll
+    for (int i = 0; i < SMP_NI; ++i) {
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < SMP_NQ; q += 2) {
+        a0 = fma(vq[q], pc[i][q], a0);
+        a1 = fma(vq[q + 1], pc[i][q + 1], a1);
+      }
+      const int c = wid + SM_W * i;
+      t[i] = (c > j && c < k_s && !(owner && i == i1)) ? a0 + a1 : 0.0;
+    }
+    // reduce t[0..7] together (halves exchanged at 16, 8, 4), t[8] alone
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool hi = lane & 16;
+      const double keep = hi ? t[i + 4] : t[i], send = hi ? t[i] : t[i + 4];
+      t[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const bool hi = lane & 8;
+      const double keep = hi ? t[i + 2] : t[i], send = hi ? t[i] : t[i + 2];
+      t[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    {
+      const bool hi = lane & 4;
+      const double keep = hi ? t[1] : t[0], send = hi ? t[0] : t[1];
+      t[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    t[0] += __shfl_xor_sync(0xffffffffu, t[0], 2);
+    t[0] += __shfl_xor_sync(0xffffffffu, t[0], 1);
+    const double t8 = warp_sum(t[8]);
+#pragma unroll
+    for (int i = 0; i < SMP_NI; ++i) {
+      const double ti = (i < 8) ? __shfl_sync(0xffffffffu, t[0], 16 * (i >> 2) + 8 * ((i >> 1) & 1) + 4 * (i & 1))
+                                : t8;
+      const double w = cf * ti;  // (0 for dead slots: their columns are unchanged)
+#pragma unroll
+      for (int q = 0; q < SMP_NQ; ++q) pc[i][q] = fma(-vq[q], w, pc[i][q]);
+    }
+    if (pk) dclk[22] = clock64() - c0;
+  }
+  __syncthreads();
+  const int l = s.brkat;
+  // columns back to shared memory (R above the diagonal, beta, v below; rejected columns updated)
+#pragma unroll
+  for (int i = 0; i < SMP_NI; ++i) {
+    const int c = wid + SM_W * i;
+    if (c < k_s) {
+#pragma unroll
+      for (int q = 0; q < SMP_NQ; ++q) {
+        const int r = lane + 32 * q;
+        if (r < mp) s.P[c * SM_LDP + r] = pc[i][q];
+      }
+    }
+  }
+  return l;
 }
 
 __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
@@ -334,6 +726,14 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int m = (int)a.m, n = (int)a.n, kmax = min(m, n);
   const int64_t lda = a.lda;
+  const bool clk = a.dbg && blockIdx.x == 0 && tid == 0;
+  long long t_last = clk ? clock64() : 0;
+#define SMT(i)                          \
+  if (clk) {                            \
+    const long long t_now = clock64();  \
+    a.dbg[i] += t_now - t_last;         \
+    t_last = t_now;                     \
+  }
   for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
     double* A = a.A + b * a.stride;
     double* coeffs = a.coeffs + b * (int64_t)max(kmax, 1);
@@ -352,8 +752,12 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
     int bad = 0;
     for (int j = wid; j < n; j += SM_W) {
       const double* col = A + (int64_t)j * lda;
-      for (int r = lane; r < m; r += 32) bad |= !isfinite(col[r]);
-      const double nu = sm_norm(col, m, lane);
+      double v[SM_MMAX / 32];
+#pragma unroll
+      for (int q = 0; q < SM_MMAX / 32; ++q) v[q] = (lane + 32 * q < m) ? col[lane + 32 * q] : 0.0;
+#pragma unroll
+      for (int q = 0; q < SM_MMAX / 32; ++q) bad |= !isfinite(v[q]);
+      const double nu = sm_norm_regs(v, lane);
       if (lane == 0) {
         s.u[j] = nu;
         s.uref[j] = nu;
@@ -366,6 +770,7 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
     sm_argmax(s.u, 0, n, s, a0, a0i);
     a0 = fmax(a0, 0.0);  // (n == 0: max of nothing is 0, rrqr.py:326)
     const double floor_v = (double)n * kEps * a0;
+    SMT(0);
     const bool stop_active = a.eps1 >= 0.0;
     const double stop_rhs = stop_active ? a.eps1 * a0 : 0.0;
     int n_s = 0, step = 0;
@@ -380,6 +785,7 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
       double umax;
       int seed;
       sm_argmax(s.u, n_s, n, s, umax, seed);
+      SMT(1);
       if (stop_active && sqrt((double)(n - n_s)) * umax <= stop_rhs) {  // rrqr.py:197-203 (<=)
         stopped = true;
         break;
@@ -443,6 +849,7 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
         }
         __syncthreads();
         sm_downdate(a, A, lda, m, n, sc, sc + 1, s);
+        SMT(15);
         if (tid == 0) {
           StepRec rec;
           rec.n_s = sc;
@@ -500,6 +907,7 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
         }
         __syncthreads();
       }
+      SMT(2);
       const int k_max = s.kmax_c;
       const int ncand = k_max + 1;
       const int k8 = (mp + 7) & ~7;
@@ -508,12 +916,18 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
         double* dst = s.P + t * SM_LDP;
         if (t < ncand) {
           const double* src = A + (int64_t)s.cols[t] * lda + n_s;
-          for (int r = lane; r < k8; r += 32) dst[r] = (r < mp) ? src[r] : 0.0;
+          double v[SM_MMAX / 32];
+#pragma unroll
+          for (int q = 0; q < SM_MMAX / 32; ++q) v[q] = (lane + 32 * q < mp) ? src[lane + 32 * q] : 0.0;
+#pragma unroll
+          for (int q = 0; q < SM_MMAX / 32; ++q)
+            if (lane + 32 * q < k8) dst[lane + 32 * q] = v[q];
         } else {
           for (int r = lane; r < k8; r += 32) dst[r] = 0.0;
         }
       }
       __syncthreads();
+      SMT(3);
       double gamma = 1.0;
       int nsel = 1;
       if (k_max > 0) {
@@ -541,6 +955,7 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
         }
         __syncthreads();
         for (int t = tid; t < ncand; t += SM_T) s.G[t * SM_GLD + t] = 1.0;
+        SMT(4);
         // ---- greedy delta filter (dm.py:151-177) ----
         const bool dmax = a.use_delta_max != 0;
         const double dlt = dmax ? a.tau * a.tau / (double)max(k_max - 1, 1) : a.delta;
@@ -616,6 +1031,7 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
         }
         __syncthreads();
       }
+      SMT(5);
       const int k_s = min(nsel, kmax - n_s);  // rrqr.py:355
       const double eps_s = a.tau * umax;      // rrqr.py:357 (before the swaps)
       // ---- swaps (rrqr.py:294-312): the transposition sequence on warp 0 ----
@@ -664,26 +1080,29 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
         if (lane == 0) s.nsw_log = nlog;
       }
       __syncthreads();
+      SMT(6);
       // composed moves new[dst] = old[src] over the touched positions
-      if (tid == 0) {
+      if (wid == 0) {  // (ballot compaction: block positions, then selected columns outside it)
         int nm = 0;
-        for (int i = 0; i < k_s; ++i) {
-          const int p = n_s + i;
-          if (s.srcof[p] != p) {
-            s.mv_dst[nm] = p;
-            s.mv_src[nm++] = s.srcof[p];
+        for (int pass = 0; pass < 2; ++pass)
+          for (int h0 = 0; h0 < k_s; h0 += 32) {
+            const int i = h0 + lane;
+            int p = -1;
+            if (i < k_s) p = pass == 0 ? n_s + i : s.cols[s.selt[i]];
+            const int sp = (p >= 0) ? s.srcof[p] : -1;
+            const bool mv = p >= 0 && sp != p && (pass == 0 || p >= n_s + k_s);
+            const unsigned bal = __ballot_sync(0xffffffffu, mv);
+            if (mv) {
+              const int o = nm + __popc(bal & ((1u << lane) - 1u));
+              s.mv_dst[o] = p;
+              s.mv_src[o] = sp;
+            }
+            nm += __popc(bal);
           }
-        }
-        for (int i = 0; i < k_s; ++i) {
-          const int p = s.cols[s.selt[i]];
-          if (p >= n_s + k_s && s.srcof[p] != p) {
-            s.mv_dst[nm] = p;
-            s.mv_src[nm++] = s.srcof[p];
-          }
-        }
-        s.nmv = nm;
+        if (lane == 0) s.nmv = nm;
       }
       __syncthreads();
+      SMT(23);
       const int nmv = s.nmv;
       {  // u, u_ref, perm
         double uu[2], ur[2];
@@ -709,23 +1128,47 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
           }
         }
       }
-      // column data: rows < n_s of every move; rows >= n_s of moves out of the
-      // block (the block's rows >= n_s are written from the panel below)
-      for (int r0 = 0; r0 < m; r0 += SM_MVROWS) {
-        double* stg = s.G;
-        for (int e = tid; e < nmv * SM_MVROWS; e += SM_T) {
-          const int q = e / SM_MVROWS, r = r0 + e % SM_MVROWS;
-          const bool need = r < m && (r < n_s || s.mv_dst[q] >= n_s + k_s);
-          stg[e] = need ? A[(int64_t)s.mv_src[q] * lda + r] : 0.0;
+      SMT(24);
+      // column data.  Rows >= n_s: only the moves out of the block write there
+      // (the block's rows >= n_s come from the panel), reading block columns
+      // nobody writes in this phase: direct copies.  Rows < n_s (R rows of
+      // earlier steps): every move; 32-row chunks, all reads of a chunk (24 per
+      // thread in flight) before its writes.
+      for (int q = wid; q < nmv; q += SM_W) {
+        if (s.mv_dst[q] < n_s + k_s) continue;
+        const double* src = A + (int64_t)s.mv_src[q] * lda;
+        double* dst = A + (int64_t)s.mv_dst[q] * lda;
+        double v[SM_MMAX / 32];
+#pragma unroll
+        for (int k = 0; k < SM_MMAX / 32; ++k) {
+          const int r = n_s + lane + 32 * k;
+          v[k] = (r < m) ? src[r] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < SM_MMAX / 32; ++k) {
+          const int r = n_s + lane + 32 * k;
+          if (r < m) dst[r] = v[k];
+        }
+      }
+      for (int r0 = 0; r0 < n_s; r0 += 32) {
+        const int r = r0 + lane;
+        double v[24];
+#pragma unroll
+        for (int k = 0; k < 24; ++k) {
+          const int q = wid + SM_W * k;
+          v[k] = (q < nmv && r < n_s) ? A[(int64_t)s.mv_src[q] * lda + r] : 0.0;
         }
         __syncthreads();
-        for (int e = tid; e < nmv * SM_MVROWS; e += SM_T) {
-          const int q = e / SM_MVROWS, r = r0 + e % SM_MVROWS;
-          const bool need = r < m && (r < n_s || s.mv_dst[q] >= n_s + k_s);
-          if (need) A[(int64_t)s.mv_dst[q] * lda + r] = stg[e];
+#pragma unroll
+        for (int k = 0; k < 24; ++k) {
+          const int q = wid + SM_W * k;
+          if (q < nmv && r < n_s) A[(int64_t)s.mv_dst[q] * lda + r] = v[k];
         }
         __syncthreads();
       }
+      __syncthreads();
+      SMT(25);
+      SMT(7);
       // ---- panel columns in selection order (candidate t_i -> slot i; t_i >= i, increasing) ----
       for (int r = tid; r < k8; r += SM_T)
         for (int i = 1; i < k_s; ++i) {
@@ -733,51 +1176,11 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
           if (t != i) s.P[i * SM_LDP + r] = s.P[t * SM_LDP + r];
         }
       __syncthreads();
-      // ---- panel: reflectors with the QRDM2 break (rrqr.py:360-379) ----
-      int l = k_s;
-      for (int j = 0; j < k_s; ++j) {
-        if (wid == (j & (SM_W - 1))) {
-          double* x = s.P + j * SM_LDP;
-          const double nrm = sm_norm(x + j, mp - j, lane);
-          int brk = 0;
-          if (a.break_check && j >= 1 && nrm < eps_s) brk = 1;  // fresh ||work[col+1:, col+1]|| < eps_s
-          if (!brk) {
-            const double x0 = x[j];
-            double beta = 0.0, cf = 0.0;
-            if (nrm > 0.0) {
-              beta = (x0 != 0.0) ? -copysign(nrm, x0) : -nrm;
-              const double den = x0 - beta;
-              for (int r = j + 1 + lane; r < mp; r += 32) x[r] = x[r] / den;
-              cf = (beta - x0) / beta;
-            }
-            __syncwarp();
-            if (lane == 0) {
-              x[j] = beta;
-              s.cf[j] = cf;
-            }
-          }
-          if (lane == 0) s.brk[j & 1] = brk;
-        }
-        __syncthreads();
-        if (s.brk[j & 1]) {
-          l = j;
-          break;
-        }
-        const double cf = s.cf[j];
-        if (cf != 0.0) {
-          const double* v = s.P + j * SM_LDP;
-          for (int c = j + 1 + ((wid - j - 1) & (SM_W - 1)); c < k_s; c += SM_W) {  // columns c = wid mod 8
-            double* col = s.P + c * SM_LDP;
-            double t = 0.0;
-            for (int r = j + 1 + lane; r < mp; r += 32) t = fma(v[r], col[r], t);
-            t = warp_sum(t) + col[j];
-            const double w = cf * t;
-            if (lane == 0) col[j] -= w;
-            for (int r = j + 1 + lane; r < mp; r += 32) col[r] = fma(-v[r], w, col[r]);
-          }
-        }
-        // (column j+1 is owned by the warp that computes reflector j+1: no barrier here)
-      }
+      SMT(8);
+      // ---- panel: reflectors with the QRDM2 break (rrqr.py:360-379), register-resident ----
+      const int l = sm_panel_regs(s, k_s, mp, eps_s, a.break_check, (a.dbg && blockIdx.x == 0 && b == 0 && step == 0) ? a.dbg : nullptr);
+      __syncthreads();
+      SMT(9);
       // ---- write the panel back (R + v for accepted columns, updated rejected ones) ----
       for (int c = wid; c < k_s; c += SM_W) {
         double* dst = A + (int64_t)(n_s + c) * lda + n_s;
@@ -788,6 +1191,7 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
       const int tc0 = n_s + k_s;
       const bool trail = tc0 < n;
       __syncthreads();
+      SMT(10);
       if (trail) {
         // ---- Y (unit lower) in P, zero past column l; W = T (accumulate_wy) in G ----
         for (int e = tid; e < DMQR_KP * k8; e += SM_T) {
@@ -801,14 +1205,42 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
         const int lt = (l + 7) >> 3;
         sm_gram(s.P, lt, (mp + 3) & ~3, s.G);  // S = Y^T Y (upper tiles)
         __syncthreads();
-        // W[:j, j] = -coeff_j W[:j, :j] S[:j, j]; W[j, j] = coeff_j (householder.py:105-113)
-        for (int j = 0; j < l; ++j) {
-          double sum = 0.0;
-          if (tid < j)
-            for (int t = tid; t < j; ++t) sum = fma(s.G[tid * SM_GLD + t], s.G[t * SM_GLD + j], sum);
+        SMT(11);
+        // W[:j, j] = -coeff_j W[:j, :j] S[:j, j]; W[j, j] = coeff_j (householder.py:105-113),
+        // blocked by 8: the diagonal blocks by the recurrence (a warp each), then
+        // block column J: W[:8J, J] = -W[:8J, :8J] (S[:8J, J] W_JJ)
+        for (int bk = wid; bk < lt; bk += SM_W) {
+          const int i = 8 * bk + (lane & 7);
+          for (int j = 8 * bk; j < min(8 * bk + 8, l); ++j) {
+            double sum = 0.0;
+            if (lane < 8 && i < j)
+              for (int t = i; t < j; ++t) sum = fma(s.G[i * SM_GLD + t], s.G[t * SM_GLD + j], sum);
+            __syncwarp();
+            if (lane < 8 && i < j) s.G[i * SM_GLD + j] = -s.cf[j] * sum;
+            if (lane == 0) s.G[j * SM_GLD + j] = s.cf[j];
+            __syncwarp();
+          }
+        }
+        __syncthreads();
+        double* X = s.G + DMQR_KP;  // scratch columns 72..79 of G's rows
+        for (int J = 1; J < lt; ++J) {
+          const int nb = min(8, l - 8 * J), r8 = 8 * J;
+          for (int e = tid; e < r8 * 8; e += SM_T) {  // X = S[:8J, J] W_JJ
+            const int i = e >> 3, c = e & 7;
+            double x = 0.0;
+            if (c < nb)
+              for (int t = 0; t <= c; ++t) x = fma(s.G[i * SM_GLD + r8 + t], s.G[(r8 + t) * SM_GLD + r8 + c], x);
+            X[i * SM_GLD + c] = x;
+          }
           __syncthreads();
-          if (tid < j) s.G[tid * SM_GLD + j] = -s.cf[j] * sum;
-          if (tid == j) s.G[j * SM_GLD + j] = s.cf[j];
+          for (int e = tid; e < r8 * 8; e += SM_T) {  // W[:8J, J] = -W[:8J, :8J] X
+            const int i = e >> 3, c = e & 7;
+            if (c < nb) {
+              double x = 0.0;
+              for (int t = i; t < r8; ++t) x = fma(s.G[i * SM_GLD + t], X[t * SM_GLD + c], x);
+              s.G[i * SM_GLD + r8 + c] = -x;
+            }
+          }
           __syncthreads();
         }
         for (int e = tid; e < DMQR_KP * DMQR_KP; e += SM_T) {  // strict lower (S values) -> 0
@@ -816,11 +1248,13 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
           if (j < i) s.G[i * SM_GLD + j] = 0.0;
         }
         __syncthreads();
+        SMT(12);
         // ---- C <- C - Y W^T Y^T C on the trailing columns, warp per 8-column tile ----
         const int64_t ncend = n;
         for (int64_t c0 = tc0 + 8 * wid; c0 < n; c0 += 8 * SM_W) sm_trail(lt, A, lda, n_s, mp, l, c0, ncend, s.P, s.G);
         __syncthreads();
       }
+      SMT(13);
       // ---- norms (rrqr.py:161-186) and the step record ----
       sm_downdate(a, A, lda, m, n, n_s, n_s + l, s);
       if (tid == 0) {
@@ -838,6 +1272,7 @@ __global__ void __launch_bounds__(SM_T, 1) k_small_qrdm(SmallArgs a) {
       __syncthreads();
       n_s += l;
       ++step;
+      SMT(14);
     }
     __syncthreads();
     // ---- rank / n_factored (rrqr.py:406-412; StopRule.NONE: _posthoc_rank 206-208) ----
