@@ -24,7 +24,7 @@ from .rrqr import (
     Permutation,
     RRQRResult,
     StopCriterion,
-    _RULE_CODE,
+    rule_code,
     _check,
     _steps_from_raw,
     _torch,
@@ -102,7 +102,7 @@ def factorize_batch(A, params: DMParams = DMParams(), stop: StopCriterion = Stop
     swap_cap = max(kmax * (params.k_dm + 1) + 8, 8)
     p = _lib.Params(tau=float(params.tau), delta=float(params.delta), epsilon=float(stop.epsilon),
                     k_dm=int(params.k_dm), use_delta_max=int(bool(params.use_delta_max)),
-                    stop_rule=_RULE_CODE[stop.variant], break_check=int(bool(break_check)), trace_norms=0,
+                    stop_rule=rule_code(stop), break_check=int(bool(break_check)), trace_norms=0,
                     max_steps=0)
     coeffs = torch.zeros((b, max(kmax, 1)), dtype=torch.float64, device=dev)
     perm = torch.zeros((b, max(n, 1)), dtype=torch.int64, device=dev)

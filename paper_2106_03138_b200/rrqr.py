@@ -69,6 +69,13 @@ class StopRule(Enum):
 _RULE_CODE = {StopRule.EPS_N: 0, StopRule.EPS_SQRT_N: 1, StopRule.NONE: 2}
 
 
+def rule_code(stop) -> int:
+    """C-ABI stop_rule code of a StopCriterion -- ours or the reference's own
+    (rrqr.py:58-80): the reference harness passes dmqr.rrqr.StopCriterion
+    objects, whose StopRule enum is keyed by the same values."""
+    return {"n": 0, "sqrt-n": 1, "none": 2}[StopRule(getattr(stop.variant, "value", stop.variant)).value]
+
+
 @dataclass(frozen=True)
 class StopCriterion:
     variant: StopRule = StopRule.EPS_N
@@ -334,7 +341,7 @@ def factorize(A, params: DMParams = DMParams(), stop: StopCriterion = StopCriter
     sh = C.c_void_p(st.cuda_stream)
     p = _lib.Params(tau=float(params.tau), delta=float(params.delta), epsilon=float(stop.epsilon),
                     k_dm=int(params.k_dm), use_delta_max=int(bool(params.use_delta_max)),
-                    stop_rule=_RULE_CODE[stop.variant], break_check=int(bool(break_check)),
+                    stop_rule=rule_code(stop), break_check=int(bool(break_check)),
                     trace_norms=int(bool(trace_norms)), max_steps=int(max_steps))
     kmax = min(m, n)
     step_cap = max(kmax, 1)

@@ -569,3 +569,50 @@ def test_fused_small_kernel_matches_step_kernels(monkeypatch):
         assert np.abs(fused.packed[:, :nf] - steps.packed[:, :nf]).max() <= 1e-10 * scale, i
         _compare(A, fused, ref, f"fused[{i}]")
         _compare(A, steps, ref, f"steps[{i}]")
+
+
+@pytest.mark.parametrize("algo", ["qrdm2", "qrp"])
+@pytest.mark.parametrize("large_rows", [False, True])
+def test_column_norms_overflow_underflow_kat(algo, large_rows):
+    """column_norms' max-scaled path (matrix.py:61-78; KAT test_matrix.py:86-91):
+    columns of 1e300 and 1e-300 entries, whose plain sums of squares overflow /
+    underflow, must come out as 2e300 / 2e-300 (rel 1e-15) through the device
+    norms, the pivot order and the reflectors.  ``large_rows`` repeats it on a
+    2^20-element matrix so the look-ahead schedule's norm kernels run too."""
+    m = 4 if not large_rows else 4096
+    n = 3 if not large_rows else 256
+    rng = np.random.default_rng(11)
+    A = np.zeros((m, n))
+    A[:, 0] = 1e-300 * np.where(np.arange(m) % 2 == 0, 1.0, -1.0)
+    A[:, 1] = 1e300
+    A[:2, 2] = [3.0, 4.0]
+    if n > 3:
+        A[:, 3:] = 1e-3 * rng.standard_normal((m, n - 3))
+    sc = np.sqrt(m / 4.0)  # column norms scale with sqrt(m)
+    res = _gpu(A, algo, stop_rule="none", trace_norms=True)
+    ref = (O.qrp if algo == "qrp" else O.qrdm2)(A, stop_rule=O.STOP_NONE, trace_norms=True)
+    d = np.abs(res.r_diagonal())
+    assert np.all(np.isfinite(d))
+    assert res.perm.forward[0] == 1
+    assert d[0] == pytest.approx(2e300 * sc, rel=1e-15)
+    j0 = int(np.flatnonzero(res.perm.forward == 0)[0])
+    dr = np.abs(ref.r_diagonal())
+    assert d[j0] == pytest.approx(dr[j0], rel=1e-10) and 0.9 * 2e-300 * sc < d[j0] < 1.1 * 2e-300 * sc
+    assert np.array_equal(res.perm.forward, ref.forward)
+    assert res.rank == ref.rank
+    assert np.all(np.isfinite(res.norm_trace))
+
+
+@pytest.mark.parametrize("e2", [500, -996])
+def test_power_of_two_scaled_matrix_vs_oracle(e2):
+    """A whole matrix scaled by 2^500 (~3e150: squares near overflow) or 2^-996
+    (~1e-300: squares underflow to 0): the norms take the scaled
+    branch; pivots, rank and |diag R| must match the oracle on the same input."""
+    rng = np.random.default_rng(5)
+    A = np.ldexp(rng.standard_normal((96, 80)) @ np.diag(np.logspace(0, -3, 80)), e2)
+    res = _gpu(A, "qrdm2")
+    ref = O.qrdm2(A)
+    assert np.array_equal(res.perm.forward, ref.forward)
+    assert res.rank == ref.rank
+    ok, worst = parity.diag_close(res.r_diagonal(), ref.r_diagonal(), 96)
+    assert ok, worst
