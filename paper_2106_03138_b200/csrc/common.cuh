@@ -106,23 +106,62 @@ struct CtlSnap {
   int32_t cq_fail, tc0, la, pend, pend_ns, pend_l, q1_fail, q1_kk;
   unsigned long long* tl;
 };
-// (Volatile reads: the control block is written by the kernels around this
-// one, which may still be running under programmatic dependent launch, so the
-// compiler must neither route these loads through the read-only path nor hoist
-// them above griddepcontrol.wait.)
-__device__ __forceinline__ CtlSnap snap(const Ctl* cp) {
-  const volatile Ctl* c = cp;
+// (GPU-scope relaxed loads in volatile asm: the control block is written by
+// the kernels around this one, which may still be running under programmatic
+// dependent launch, so these loads must neither take the read-only path nor
+// move above griddepcontrol.wait.  A C++ `volatile` read would compile to
+// LDG.STRONG.SYS, which measured 35% slower end to end on cfg2.)
+__device__ __forceinline__ int32_t ctl_ld(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ctl_ld(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int64_t ctl_ld(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ctl_ld(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+template <class T>
+__device__ __forceinline__ T* ctl_ld(T* const* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p));
+  return reinterpret_cast<T*>(v);
+}
+__device__ __forceinline__ CtlSnap snap_load(const Ctl* c) {
   CtlSnap s;
-  s.m = c->m; s.n = c->n; s.lda = c->lda; s.kmax = c->kmax;
-  s.floor = c->floor; s.stop_rhs = c->stop_rhs; s.tau = c->tau; s.delta = c->delta; s.umax = c->umax;
-  s.stop_active = c->stop_active; s.break_check = c->break_check; s.k_dm = c->k_dm;
-  s.use_delta_max = c->use_delta_max; s.trace_norms = c->trace_norms; s.swap_cap = c->swap_cap;
-  s.step_cap = c->step_cap; s.n_s = c->n_s; s.done = c->done; s.step_idx = c->step_idx; s.n_swaps = c->n_swaps;
-  s.kind = c->kind; s.k_max = c->k_max; s.nsel = c->nsel; s.k_s = c->k_s; s.l_acc = c->l_acc;
-  s.ncand = c->ncand; s.nsw = c->nsw; s.nmv = c->nmv; s.cq_fail = c->cq_fail; s.tc0 = c->tc0;
-  s.la = c->la; s.pend = c->pend; s.pend_ns = c->pend_ns; s.pend_l = c->pend_l;
-  s.q1_fail = c->q1_fail; s.q1_kk = c->q1_kk; s.tl = c->tl;
+#define CTL_LD(f) s.f = ctl_ld(&c->f)
+  CTL_LD(m); CTL_LD(n); CTL_LD(lda); CTL_LD(kmax);
+  CTL_LD(floor); CTL_LD(stop_rhs); CTL_LD(tau); CTL_LD(delta); CTL_LD(umax);
+  CTL_LD(stop_active); CTL_LD(break_check); CTL_LD(k_dm); CTL_LD(use_delta_max); CTL_LD(trace_norms);
+  CTL_LD(swap_cap); CTL_LD(step_cap); CTL_LD(n_s); CTL_LD(done); CTL_LD(step_idx); CTL_LD(n_swaps);
+  CTL_LD(kind); CTL_LD(k_max); CTL_LD(nsel); CTL_LD(k_s); CTL_LD(l_acc);
+  CTL_LD(ncand); CTL_LD(nsw); CTL_LD(nmv); CTL_LD(cq_fail); CTL_LD(tc0);
+  CTL_LD(la); CTL_LD(pend); CTL_LD(pend_ns); CTL_LD(pend_l);
+  CTL_LD(q1_fail); CTL_LD(q1_kk); CTL_LD(tl);
+#undef CTL_LD
   return s;
+}
+// The CTA's snapshot: thread 0 loads it and every thread reads the same copy.
+// (Per-thread loads could tear: a CTA of a large grid may start while another
+// CTA of the same grid -- or a concurrent kernel -- updates the control block,
+// e.g. k_spare's phase 1 clearing `pend`; warps that then disagree on a
+// loop bound diverge at a barrier and the CTA hangs.)  Called by every thread
+// of the CTA, at top level.
+__device__ __forceinline__ const CtlSnap& snap(const Ctl* c) {
+  __shared__ CtlSnap s_snap;
+  if (threadIdx.x == 0) s_snap = snap_load(c);
+  __syncthreads();
+  return s_snap;
 }
 
 // Programmatic dependent launch: the per-step kernels are launched so the
@@ -203,6 +242,24 @@ __device__ __forceinline__ bool norm_range_ok(double amax) {
   return amax == 0.0 || (amax > 1e-140 && amax < 1e140);
 }
 
+// Bounded device-side waits.  Every spin on another CTA or kernel (grid
+// barriers, look-ahead publications, helper passes) ticks a SpinGuard; a wait
+// that has not ended after 2^21 polls (~1-2 s: no legitimate wait comes near,
+// a whole cfg5 outer step takes milliseconds) reports its site and values and
+// traps, so the host sees a CUDA error instead of a hang.  (One counter
+// register; the report is out of line.)
+__device__ __noinline__ void spin_timeout(int site, long long a, long long b) {
+  printf("[dmqr] device wait timed out: site %d block (%d,%d,%d) thread %d values %lld %lld\n", site,
+         (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z, (int)threadIdx.x, a, b);
+  __trap();
+}
+struct SpinGuard {
+  unsigned polls = 0;
+  __device__ __forceinline__ void tick(int site, long long a, long long b) {
+    if (++polls == (1u << 21)) spin_timeout(site, a, b);
+  }
+};
+
 // Grid-wide barrier for cooperatively launched kernels (all CTAs co-resident):
 // a monotonic arrival counter (zeroed by an earlier kernel of the step) --
 // arrive with a gpu-scope release add, wait with acquire loads until the
@@ -213,9 +270,12 @@ __device__ __forceinline__ void grid_sync_count(uint32_t* count, uint32_t target
   if (threadIdx.x == 0) {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(count) : "memory");
     uint32_t v;
-    do {
+    SpinGuard sg;
+    for (;;) {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(count) : "memory");
-    } while (v < target);
+      if (v >= target) break;
+      sg.tick(1, v, target);
+    }
   }
   __syncthreads();
 }

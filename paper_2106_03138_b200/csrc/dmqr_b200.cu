@@ -861,6 +861,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     }
   }
   bool finished = (kmax == 0);
+  const bool step_verbose = getenv("DMQR_STEP_VERBOSE") != nullptr;  // debug: every consumed step record
   auto consume = [&]() -> int {
     const int sl = known & 1;
     // poll the step's record (k_step_end posts it); check the stream now and
@@ -914,6 +915,9 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     }
     known_ns = std::min<int32_t>((int32_t)r->n_s, zmin_ns);
     known_steps = r->step_idx;
+    if (step_verbose)
+      fprintf(stderr, "[dmqr] step record %d: n_s %d step_idx %d flags %d\n", known, (int)r->n_s, (int)r->step_idx,
+              (int)r->flags);
     ++known;
     if ((r->flags & 1) && zall_done) finished = true;
     if (r->flags & 2) want_serial = true;

@@ -755,9 +755,12 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
         asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.hctr + dec_idx), "r"(ok ? 2u : 1u) : "memory");
       }
       unsigned d;
-      do {
+      SpinGuard sg;
+      for (;;) {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d) : "l"(a.hctr + dec_idx) : "memory");
-      } while (d == 0u);
+        if (d != 0u) break;
+        sg.tick(5, dec_idx, 0);
+      }
       s_use = (d == 2u);
     }
     __syncthreads();
@@ -1246,11 +1249,13 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_helper(PanelArgs a) {
   // ---- pass 2 once R1^-1 is published (or nothing to do) ----
   if (tid == 0) {
     unsigned v, d6;
+    SpinGuard sg;
     for (;;) {  // R1^-1 published, or pass 1 abandoned (then the panel never publishes)
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.hctr + 4) : "memory");
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d6) : "l"(a.hctr + 6) : "memory");
       if (v == (unsigned)S.step_idx + 1u || d6 == 1u) break;
       __nanosleep(200);
+      sg.tick(6, v, S.step_idx);
     }
     s_hdr[0] = __ldcg(a.hR + DMQR_KP * DMQR_KP);
     s_hdr[1] = (v == (unsigned)S.step_idx + 1u) ? __ldcg(a.hR + DMQR_KP * DMQR_KP + 1) : 1.0;

@@ -163,9 +163,12 @@ __global__ void __launch_bounds__(QP_T, 2) k_qp3(Qp3Args a) {
     if (g_prev > 0 && g_prev <= QP_GMAX) {  // the guard phase's last CTA has published the fresh norms
       if (tid == 0) {
         unsigned v;
-        do {
+        SpinGuard sg;
+        for (;;) {
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(a.cnt + 3) : "memory");
-        } while (v < (unsigned)t);
+          if (v >= (unsigned)t) break;
+          sg.tick(7, v, t);
+        }
       }
       __syncthreads();
     }

@@ -38,6 +38,36 @@ constexpr size_t TA_SMEM_ST = sizeof(double) * TA_NST * (DMQR_KP + TA_COLS) * TA
 constexpr size_t TA_SMEM_TZ = sizeof(double) * 2 * DMQR_KP * TW_LD;
 constexpr size_t TA_SMEM = TA_SMEM_ST > TA_SMEM_TZ ? TA_SMEM_ST : TA_SMEM_TZ;
 
+// One landed 16-row slab of Z += Y^T C: warp w owns output columns 8w..8w+7,
+// all lt row tiles.  Instantiated per lt so that no predicated (dead) DMMA is
+// issued when fewer than 9 reflector tiles are in use (l <= 16 steps of tall
+// or graded inputs issue 2 of 9).
+template <int LT>
+__device__ __forceinline__ void ta_slab_mma_t(double (&acc)[DMQR_KP / 8][2], const double* ys, const double* cs,
+                                              int lane, int wid) {
+#pragma unroll
+  for (int ks = 0; ks < TA_ROWS / 4; ++ks) {
+    const int kr = 4 * ks + (lane & 3);
+    const double b = cs[(wid * 8 + (lane >> 2)) * TA_LD + kr];
+#pragma unroll
+    for (int q = 0; q < LT; ++q) dmma884(acc[q][0], acc[q][1], ys[(q * 8 + (lane >> 2)) * TA_LD + kr], b);
+  }
+}
+__device__ __forceinline__ void ta_slab_mma(int lt, double (&acc)[DMQR_KP / 8][2], const double* ys,
+                                            const double* cs, int lane, int wid) {
+  switch (lt) {
+    case 1: ta_slab_mma_t<1>(acc, ys, cs, lane, wid); break;
+    case 2: ta_slab_mma_t<2>(acc, ys, cs, lane, wid); break;
+    case 3: ta_slab_mma_t<3>(acc, ys, cs, lane, wid); break;
+    case 4: ta_slab_mma_t<4>(acc, ys, cs, lane, wid); break;
+    case 5: ta_slab_mma_t<5>(acc, ys, cs, lane, wid); break;
+    case 6: ta_slab_mma_t<6>(acc, ys, cs, lane, wid); break;
+    case 7: ta_slab_mma_t<7>(acc, ys, cs, lane, wid); break;
+    case 8: ta_slab_mma_t<8>(acc, ys, cs, lane, wid); break;
+    default: ta_slab_mma_t<DMQR_KP / 8>(acc, ys, cs, lane, wid); break;
+  }
+}
+
 // Look-ahead bookkeeping of a step's own panel columns, by one CTA: u of the
 // accepted columns is cleared; the columns [n_s + l, tc0) that the Householder
 // panel already updated in full (after a QRDM2 break) are downdated with
@@ -243,14 +273,7 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* c, double* __restrict_
     }
     const double* ys = ysb(sl % TA_NST);
     const double* cs = csb(sl % TA_NST);
-#pragma unroll
-    for (int ks = 0; ks < TA_ROWS / 4; ++ks) {
-      const int kr = 4 * ks + (lane & 3);
-      const double b = cs[(wid * 8 + (lane >> 2)) * TA_LD + kr];
-#pragma unroll
-      for (int q = 0; q < DMQR_KP / 8; ++q)
-        if (q < lt) dmma884(acc[q][0], acc[q][1], ys[(q * 8 + (lane >> 2)) * TA_LD + kr], b);
-    }
+    ta_slab_mma(lt, acc, ys, cs, lane, wid);
     __syncthreads();  // (stage sl % TA_NST is refilled by the issue below, TA_NST - 1 slabs ahead)
     if (sl + TA_NST - 1 < nslab)
       issue(sl + TA_NST - 1);
@@ -559,7 +582,7 @@ __device__ void g_partial(const double* __restrict__ A, const double* __restrict
     const double* ys = ysb(sl % TA_NST);
     const double* cs = csb(sl % TA_NST);
 #pragma unroll
-    for (int ks = 0; ks < TA_ROWS / 4; ++ks) {
+    for (int ks = 0; ks < TA_ROWS / 4; ++ks) {  // (predicated: a switch over lt spills k_spare)
       const int kr = 4 * ks + (lane & 3);
       const double b = cs[(wid * 8 + (lane >> 2)) * TA_LD + kr];
 #pragma unroll
@@ -592,10 +615,12 @@ constexpr int NSPLIT_MAXG = 16;
 // or Q1 published / the panel's release (returns 0).  Out of line: inlined, the
 // polling loop pushes the kernel past its 2-CTA register cap.
 __device__ __noinline__ int spare_wait_panel(Ctl* c, int P) {
+  SpinGuard sg;
   for (;;) {
     if (ld_acquire(&c->p_count) >= (unsigned)P) return c->p_k;
     if (ld_acquire(&c->q1_count) >= (unsigned)P) return (ld_acquire(&c->p_count) >= (unsigned)P) ? c->p_k : 0;
     __nanosleep(200);
+    sg.tick(2, c->q1_count, P);
   }
 }
 
@@ -610,7 +635,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* c, double* __restrict__ 
   const long long t_first = gtimer();
   __shared__ int s_item, s_flag;
   const int tid = threadIdx.x;
-  const CtlSnap S = snap(c);
+  const CtlSnap& S = snap(c);  // (read from shared memory on use: registers are at the 2-CTA cap)
   TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 5);
   const int64_t m = S.m, n = S.n, lda = S.lda;
   // ---- phase 1: the pending update of the previous step ----
@@ -660,7 +685,11 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* c, double* __restrict__ 
       if constexpr (PM) {
         s_pk = spare_wait_panel(c, P);
       } else {
-        while (ld_acquire(&c->q1_count) < (unsigned)P) __nanosleep(200);
+        SpinGuard sg;
+        while (ld_acquire(&c->q1_count) < (unsigned)P) {
+          __nanosleep(200);
+          sg.tick(3, c->q1_count, P);
+        }
         s_pk = 0;
       }
       s_flag = (s_pk > 0) || !c->q1_fail;
@@ -703,7 +732,10 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* c, double* __restrict__ 
         }
         if (it < ng && ntb > 0) {  // the pending update of these columns must be complete
           if (tid == 0)
-            while (ld_acquire(&colcnt[it % ntile]) < (unsigned)ntx) __nanosleep(100);
+            for (SpinGuard sg; ld_acquire(&colcnt[it % ntile]) < (unsigned)ntx;) {
+              __nanosleep(100);
+              sg.tick(4, colcnt[it % ntile], ntx);
+            }
           __syncthreads();
         }
         if (it >= ng) {

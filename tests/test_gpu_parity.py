@@ -1,6 +1,8 @@
 """GPU parity: the CUDA path (through the C-ABI) vs the reference's golden
 vectors and the live CPU oracle.  Needs a B200 (``-m gpu``)."""
 
+import functools
+
 import numpy as np
 import pytest
 from threadpoolctl import threadpool_limits
@@ -75,17 +77,25 @@ def small_path(request, monkeypatch):
     return request.param
 
 
+@functools.lru_cache(maxsize=None)
+def _golden_oracle(name):
+    """The oracle's run (with margins) of a golden case, shared by both small paths."""
+    meta = G.index()["cases"][name]
+    A = G.case_input(name)
+    kw = G.oracle_kwargs(name)
+    with threadpool_limits(1):
+        if meta["algo"] == "qrp":
+            return O.qrp(A, margins=True, stop_rule=kw["stop_rule"])
+        return (O.qrdm2 if meta["algo"] == "qrdm2" else O.qrdm)(A, margins=True, **kw)
+
+
 @pytest.mark.parametrize("name", GOLDEN)
 def test_golden_case(name, small_path):
     meta = G.index()["cases"][name]
     A = G.case_input(name)
     kw = G.oracle_kwargs(name)
     res = _gpu(A, meta["algo"], **kw)
-    with threadpool_limits(1):
-        if meta["algo"] == "qrp":
-            ref = O.qrp(A, margins=True, stop_rule=kw["stop_rule"])
-        else:
-            ref = (O.qrdm2 if meta["algo"] == "qrdm2" else O.qrdm)(A, margins=True, **kw)
+    ref = _golden_oracle(name)
     # the oracle itself is pinned to the golden vectors (test_oracle_golden.py)
     assert np.array_equal(ref.forward, G.case_field(name, "forward"))
     # BASELINE cfg1 is stable under 1-ulp input perturbation (SURVEY App. B):
@@ -616,3 +626,32 @@ def test_power_of_two_scaled_matrix_vs_oracle(e2):
     assert res.rank == ref.rank
     ok, worst = parity.diag_close(res.r_diagonal(), ref.r_diagonal(), 96)
     assert ok, worst
+
+
+@pytest.mark.parametrize("switch", ["DMQR_NO_CHOLQR", "DMQR_NO_LOOKAHEAD", "DMQR_NO_GRAPH", "DMQR_NO_STEP_GRAPH"])
+def test_schedule_switches_keep_parity(monkeypatch, switch):
+    """Every schedule switch the engine reads (Householder-only panel, serial
+    schedule, no replayed step graphs) gives the default run's decisions and a
+    factor within rounding of it -- single matrices at a look-ahead size and a
+    batched group of small ones."""
+    from paper_2106_03138_b200 import qrdm2
+    from paper_2106_03138_b200.batch import factorize_batch
+
+    rng = np.random.default_rng(90)
+    A = rng.standard_normal((1100, 1024)) * np.logspace(0, -8, 1024)[rng.permutation(1024)]
+    B = rng.standard_normal((6, 160, 144)) @ np.diag(np.logspace(0, -12, 144))
+    base, bb = qrdm2(A), factorize_batch(B)
+    monkeypatch.setenv(switch, "1")
+    monkeypatch.setenv("DMQR_NO_FUSED", "1")  # batched groups through the step kernels (graph path)
+    res, rb = qrdm2(A), factorize_batch(B)
+    assert np.array_equal(res.perm.forward, base.perm.forward) and res.rank == base.rank
+    assert np.abs(res.packed - base.packed).max() <= 1e-9 * np.abs(base.packed).max()
+    resid, orth = parity.residuals(A, res)
+    assert resid <= 50 * 1100 * O.EPS and orth <= 50 * 1100 * O.EPS
+    for i in range(len(B)):
+        r, s = rb.result(i), bb.result(i)
+        ref = O.qrdm2(B[i], margins=True)
+        cut, _ = parity.robust_prefix(ref)
+        assert np.array_equal(r.perm.forward[:cut], s.perm.forward[:cut])
+        rr, oo = parity.residuals(B[i], r)
+        assert rr <= 50 * 160 * O.EPS and oo <= 50 * 160 * O.EPS
