@@ -8,9 +8,12 @@ on a machine without the built .so or without a CUDA device fails loudly.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libdmqr_b200.so"
+if os.environ.get("DMQR_LIB_PATH"):  # A/B builds (tools/); the product loads the in-tree library
+    LIB_PATH = Path(os.environ["DMQR_LIB_PATH"]).resolve()
 
 EXPORTS = (
     "dmqr_workspace_bytes",

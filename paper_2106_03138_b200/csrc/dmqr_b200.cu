@@ -489,8 +489,9 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   // (past n = 12288 the trailing update outweighs the panel it would hide, and
   // graded inputs make its guard path expensive: serial -- measured on cfg2 /
   // cfg5 at 8192, 12288, 16384)
+  const bool la_force = getenv("DMQR_FORCE_LOOKAHEAD") != nullptr;  // A/B switch: look-ahead at any shape
   const bool la_all = !qrp && !p->trace_norms && getenv("DMQR_NO_LOOKAHEAD") == nullptr &&
-                      m * n >= (int64_t)1 << 20 && m <= 4 * n && n <= 12288 && NZ == 1;
+                      m * n >= (int64_t)1 << 20 && ((m <= 4 * n && n <= 12288) || la_force) && NZ == 1;
 
 
   const int64_t kmax = std::min(m, n);

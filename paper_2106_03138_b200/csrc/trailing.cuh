@@ -27,9 +27,15 @@ namespace dmqr {
 
 constexpr int TA_T = 256;       // 8 warps
 constexpr int TA_COLS = 64;     // output columns per CTA
-constexpr int TA_ROWS = 16;     // K slab
-constexpr int TA_LD = 20;       // slab stride (4 mod 16: conflict-free fragments; 16B aligned rows)
-constexpr int TA_NST = 4;       // cp.async stages (three slabs in flight while one is consumed)
+#ifndef DMQR_TA_ROWS
+#define DMQR_TA_ROWS 16
+#endif
+#ifndef DMQR_TA_NST
+#define DMQR_TA_NST 4
+#endif
+constexpr int TA_ROWS = DMQR_TA_ROWS;  // K slab
+constexpr int TA_LD = TA_ROWS + 4;     // slab stride (4 mod 16: conflict-free fragments; 16B aligned rows)
+constexpr int TA_NST = DMQR_TA_NST;    // cp.async stages (TA_NST - 1 slabs in flight while one is consumed)
 constexpr int TA_RP = TA_ROWS / 2;    // row pairs per slab (16-byte copies)
 constexpr int TA_CL = TA_T / TA_RP;   // column lanes of the copy grid
 constexpr int TW_LD = DMQR_KP;  // 72 = 8 mod 16
