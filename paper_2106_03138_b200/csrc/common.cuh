@@ -245,18 +245,29 @@ __device__ __forceinline__ bool norm_range_ok(double amax) {
 // Bounded device-side waits.  Every spin on another CTA or kernel (grid
 // barriers, look-ahead publications, helper passes) ticks a SpinGuard; a wait
 // that has not ended after 2^21 polls (~1-2 s: no legitimate wait comes near,
-// a whole cfg5 outer step takes milliseconds) reports its site and values and
-// traps, so the host sees a CUDA error instead of a hang.  (One counter
-// register; the report is out of line.)
+// a whole cfg5 outer step takes milliseconds) traps, so the host sees a CUDA
+// error instead of a hang.  One counter register and an inline trap: a call
+// to a reporting function would cost the spinning kernels registers (several
+// run at their register cap).  (Debug builds, -DDMQR_SPIN_REPORT, print the
+// site and the polled values first.)
+#ifdef DMQR_SPIN_REPORT
 __device__ __noinline__ void spin_timeout(int site, long long a, long long b) {
   printf("[dmqr] device wait timed out: site %d block (%d,%d,%d) thread %d values %lld %lld\n", site,
          (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z, (int)threadIdx.x, a, b);
   __trap();
 }
+#endif
 struct SpinGuard {
   unsigned polls = 0;
   __device__ __forceinline__ void tick(int site, long long a, long long b) {
-    if (++polls == (1u << 21)) spin_timeout(site, a, b);
+    if (++polls == (1u << 21)) {
+#ifdef DMQR_SPIN_REPORT
+      spin_timeout(site, a, b);
+#else
+      (void)site, (void)a, (void)b;
+      asm volatile("trap;");
+#endif
+    }
   }
 };
 
@@ -300,6 +311,56 @@ __device__ __forceinline__ void grid_barrier(uint32_t* count, uint32_t* gen, uin
   }
   __syncthreads();
 }
+
+// A/B builds: -DDMQR_NO_TMA_GRAM / -DDMQR_NO_TMA_SWAP select the cp.async /
+// plain-load staging of k_gram / k_swap instead of the bulk copies
+#ifdef DMQR_NO_TMA_GRAM
+constexpr bool kTMAGram = false;
+#else
+constexpr bool kTMAGram = true;
+#endif
+#ifdef DMQR_NO_TMA_SWAP
+constexpr bool kTMASwap = false;
+#else
+constexpr bool kTMASwap = true;
+#endif
+// ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) with mbarrier completion ----
+// Contiguous global <-> shared transfers done by the copy engine: one thread
+// issues a whole column segment (16-byte aligned addresses, a multiple of 16
+// bytes); the bytes land on an mbarrier (expect_tx / complete_tx), and the
+// shared -> global direction is tracked by bulk groups.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// arrive (the barrier's one expected arrival) and add `bytes` to the transaction count
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem)),
+               "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_u32(smem)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the issuing thread's bulk stores have read their shared-memory source (the
+// CTA may exit; the writes complete with the grid, before any dependent grid's
+// griddepcontrol.wait returns)
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);

@@ -511,9 +511,17 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   CK(zmemset(lacount, sizeof(unsigned) * 16));
   if (n > 0) {
     if (m > 0) {
-      int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)d.sms * 16);
-      k_colnorms_init<<<dim3((unsigned)blocks, 1, NZ), 256, 0, st>>>(A, m, n, lda, u, uref, nonfinite, zs);
+      // tall columns: (column, 4096-row chunk) items, combined by k_colnorms_fin
+      const int nch = (NZ == 1 && m > 2 * GN_ROWS) ? (int)ceil_div(m, GN_ROWS) : 1;
+      double* gpn = (double*)(ws + L.gnp);
+      int64_t blocks = std::min<int64_t>(ceil_div(n * nch * 32, 256), (int64_t)d.sms * 16);
+      k_colnorms_init<<<dim3((unsigned)blocks, 1, NZ), 256, 0, st>>>(A, m, n, lda, u, uref, nonfinite, zs, gpn, nch);
       NOTE_LAUNCH();
+      if (nch > 1) {
+        k_colnorms_fin<<<(unsigned)std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)d.sms * 16), 256, 0, st>>>(
+            A, m, n, lda, u, uref, nonfinite, gpn, nch);
+        NOTE_LAUNCH();
+      }
     } else {
       CK(zmemset(u, sizeof(double) * n));
       CK(zmemset(uref, sizeof(double) * n));

@@ -16,6 +16,7 @@
 namespace dmqr {
 
 constexpr int GRAM_T = 256;
+static_assert(DMQR_KP <= 128, "k_gram: one bulk copy per thread for the candidate and the reflector columns");
 constexpr int GRAM_ROWS = 32;  // slab height (one slab per CTA up to 148 x 32 rows)
 constexpr int GRAM_LD = 36;    // 32 rows + 4: conflict-free fragment loads (ld = 4 mod 16)
 constexpr int GRAM_PART = DMQR_KP * DMQR_KP;
@@ -220,10 +221,44 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* c, double* __restrict__ A,
   }
   __syncthreads();
   const int nslab = (r_end > r_begin) ? (int)ceil_div(r_end - r_begin, GRAM_ROWS) : 0;
+  // Whole slabs (the usual case) arrive by TMA bulk copies: one 256-byte
+  // column segment per candidate and per pending-Y column, issued by warp 0 and
+  // landing on the buffer's mbarrier.  A slab whose first global row is odd is
+  // fetched from the row above (16-byte alignment) into a buffer shifted by one
+  // element, so row r of the slab sits at buf + off + r either way.  Partial
+  // slabs at the end of a CTA's range keep the zero-filling cp.async path.
+  __shared__ __align__(8) uint64_t s_bar[2];
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+  }
+  __syncthreads();
+  auto slab_full = [&](int sl) { return kTMAGram && r_begin + (int64_t)(sl + 1) * GRAM_ROWS <= r_end; };
+  auto slab_off = [&](int sl) { return slab_full(sl) ? (int)((n_s + r_begin + (int64_t)sl * GRAM_ROWS) & 1) : 0; };
   auto issue = [&](int sl) {
     double* buf = gsm + (sl & 1) * DMQR_KP * GRAM_LD;
     double* ys = ysl + (sl & 1) * DMQR_KP * GRAM_LD;
     const int64_t r0 = r_begin + (int64_t)sl * GRAM_ROWS;
+    if (slab_full(sl)) {
+      const int off = slab_off(sl);
+      for (int e = tid; e < (np8 - ncand) * GRAM_ROWS; e += GRAM_T)  // padding candidates
+        buf[(ncand + e / GRAM_ROWS) * GRAM_LD + off + e % GRAM_ROWS] = 0.0;
+      for (int e = tid; e < (plp4 - pl) * GRAM_ROWS; e += GRAM_T)  // padding reflectors
+        ys[(pl + e / GRAM_ROWS) * GRAM_LD + off + e % GRAM_ROWS] = 0.0;
+      {  // one copy per thread (the issue is spread over the CTA)
+        const unsigned seg = (unsigned)(GRAM_ROWS + 2 * off) * (unsigned)sizeof(double);
+        const int ncols = (gram || pendu) ? ncand : 0;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // buffer reuse after generic accesses
+        if (tid == 0) mbar_arrive_expect_tx(&s_bar[sl & 1], seg * (unsigned)(ncols + pl));
+        const double* g0 = A + (n_s + r0 - off);
+        if (tid < ncols)
+          bulk_g2s(buf + tid * GRAM_LD, g0 + (int64_t)s_cand[tid] * lda, seg, &s_bar[sl & 1]);
+        else if (tid >= 128 && tid - 128 < pl)
+          bulk_g2s(ys + (tid - 128) * GRAM_LD, g0 + (pns + tid - 128) * lda, seg, &s_bar[sl & 1]);
+      }
+      cp_async_commit();  // (an empty group keeps the cp.async group accounting per slab)
+      return;
+    }
     for (int e = tid; e < np8 * GRAM_ROWS; e += GRAM_T) {
       const int col = e / GRAM_ROWS, row = e % GRAM_ROWS;
       const int64_t r = r0 + row;
@@ -258,17 +293,18 @@ __global__ void __launch_bounds__(GRAM_T) k_gram(Ctl* c, double* __restrict__ A,
     } else {
       cp_async_wait<0>();
     }
+    if (slab_full(sl)) mbar_wait_parity(&s_bar[sl & 1], (unsigned)(sl >> 1) & 1u);
     __syncthreads();
     if (sl == 0 && pendu) {  // (the Wt copies landed with slab 0)
       for (int e = tid; e < plp4 * DMQR_KP; e += GRAM_T)
         if (!s_live[e % DMQR_KP]) wsm[e] = 0.0;
       __syncthreads();
     }
-    double* buf = gsm + (sl & 1) * DMQR_KP * GRAM_LD;
+    double* buf = gsm + (sl & 1) * DMQR_KP * GRAM_LD + slab_off(sl);
     if (pendu) {
       // buf[col][row] += (-Y) Wt for live candidates: warp w owns rows
       // 8 (w & 3) .. +8 and column tiles [5 (w >> 2), +5)
-      const double* ys = ysl + (sl & 1) * DMQR_KP * GRAM_LD;
+      const double* ys = ysl + (sl & 1) * DMQR_KP * GRAM_LD + slab_off(sl);
       const int rr = (wid & 3) * 8 + (lane >> 2);
       const int64_t r0 = r_begin + (int64_t)sl * GRAM_ROWS;
       const int qh1 = min(nt, (wid >> 2) * 5 + 5);

@@ -10,6 +10,8 @@
 
 namespace dmqr {
 
+constexpr int GN_ROWS = 4096;  // rows per chunk of the row-split norm kernels
+
 // Norm of a contiguous column segment of length len, computed by one warp
 // (all lanes return the result).  Unscaled sum of squares when the max
 // magnitude keeps squares normal, else a second max-scaled pass (the
@@ -74,51 +76,73 @@ __device__ __forceinline__ double warp_col_norm(const double* __restrict__ x, in
 // u[j] = u_ref[j] = ||A[:, j]||  (PartialNorms.from_matrix).  A NaN/Inf entry
 // makes the column's sum of squares NaN or its max magnitude Inf, which is
 // flagged here (dense() rejects such input, matrix.py:32-33) -- so the input
-// validation costs no extra pass over the matrix.
+// validation costs no extra pass over the matrix.  (A finite column whose
+// squares overflow has sum Inf but a finite max: not flagged.)
+// Work items are (column, GN_ROWS-row chunk) pairs, a warp each, 16-byte loads
+// with eight pairs in flight per lane (warp_col_sums): a tall input (cfg4,
+// 65536 x 1024) has 16 chunks per column, so the grid is not limited to one
+// warp per column.  With one chunk per column the warp finishes the norm;
+// otherwise it stores (sum of squares, max) and k_colnorms_fin combines the
+// chunks in fixed order.
+__device__ __forceinline__ bool sums_bad(double s, double amax) { return isnan(s) || isinf(amax); }
+__device__ __forceinline__ void colnorm_finish(const double* x, int64_t m, double s, double amax, int lane,
+                                               double* u, double* uref, int32_t* nonfinite, int64_t j) {
+  double r;
+  if (norm_range_ok(amax)) {
+    r = sqrt(s);
+  } else {  // the reference's max-scaled second pass (matrix.py:73-77)
+    double t = 0.0;
+    for (int64_t k = lane; k < m; k += 32) {
+      const double y = __ldg(x + k) / amax;
+      t = fma(y, y, t);
+    }
+    r = amax * sqrt(warp_sum(t));
+  }
+  if (lane == 0) {
+    if (sums_bad(s, amax)) atomicOr(nonfinite, 1);
+    u[j] = r;
+    uref[j] = r;
+  }
+}
 __global__ void k_colnorms_init(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
                                 double* __restrict__ u, double* __restrict__ uref, int32_t* __restrict__ nonfinite,
-                                int64_t zs) {
-  zshift_by(zs, A, u, uref, nonfinite);
+                                int64_t zs, double* __restrict__ gp, int nch) {
+  zshift_by(zs, A, u, uref, nonfinite, gp);
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t it = w0; it < n * nch; it += nw) {
+    const int64_t j = it / nch;
+    const int ch = (int)(it % nch);
+    const double* x = A + j * lda;
+    const int64_t r0 = (int64_t)ch * GN_ROWS, r1 = (nch == 1) ? m : min(m, r0 + GN_ROWS);
+    double s, amax;
+    warp_col_sums(x + r0, r1 - r0, lane, s, amax);
+    if (nch == 1) {
+      colnorm_finish(x, m, s, amax, lane, u, uref, nonfinite, j);
+    } else if (lane == 0) {
+      gp[2 * it] = s;
+      gp[2 * it + 1] = amax;
+    }
+  }
+}
+// the chunks of a tall column, summed in chunk order (a warp per column)
+__global__ void k_colnorms_fin(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+                               double* __restrict__ u, double* __restrict__ uref, int32_t* __restrict__ nonfinite,
+                               const double* __restrict__ gp, int nch) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t j = w0; j < n; j += nw) {
-    const double* x = A + j * lda;
-    double s0 = 0.0, s1 = 0.0, a0 = 0.0, a1 = 0.0;
-    int bad = 0;
-    int64_t i = lane;
-    for (; i + 32 < m; i += 64) {
-      const double p = __ldg(x + i), q = __ldg(x + i + 32);
-      s0 = fma(p, p, s0);
-      s1 = fma(q, q, s1);
-      a0 = fmax(a0, fabs(p));
-      a1 = fmax(a1, fabs(q));
-      bad |= !isfinite(p) | !isfinite(q);
+    double s = 0.0, amax = 0.0;
+    for (int ch = lane; ch < nch; ch += 32) {
+      s += gp[2 * (j * nch + ch)];
+      amax = fmax(amax, gp[2 * (j * nch + ch) + 1]);
+      if (isinf(gp[2 * (j * nch + ch) + 1])) amax = gp[2 * (j * nch + ch) + 1];
     }
-    if (i < m) {
-      const double p = __ldg(x + i);
-      s0 = fma(p, p, s0);
-      a0 = fmax(a0, fabs(p));
-      bad |= !isfinite(p);
-    }
-    const double s = warp_sum(s0 + s1);
-    const double amax = warp_max(fmax(a0, a1));
-    double r;
-    if (norm_range_ok(amax)) {
-      r = sqrt(s);
-    } else {
-      double t = 0.0;
-      for (int64_t k = lane; k < m; k += 32) {
-        const double y = __ldg(x + k) / amax;
-        t = fma(y, y, t);
-      }
-      r = amax * sqrt(warp_sum(t));
-    }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(nonfinite, 1);
-    if (lane == 0) {
-      u[j] = r;
-      uref[j] = r;
-    }
+    s = warp_sum(s);
+    amax = warp_max(amax);
+    colnorm_finish(A + j * lda, m, s, amax, lane, u, uref, nonfinite, j);
   }
 }
 
@@ -167,7 +191,6 @@ __global__ void k_downdate(Ctl* c, const double* __restrict__ A, double* __restr
 // partial sum of squares and max |x| per item; k_gnorm_fin sums the chunks of
 // a column in fixed order.  A long column is read by many warps at once instead
 // of one (a 65536-row column was 128 dependent round trips for a single warp).
-constexpr int GN_ROWS = 4096;
 __global__ void __launch_bounds__(256) k_gnorm_part(const Ctl* c, const double* __restrict__ A,
                                                     const int32_t* __restrict__ glist, double* __restrict__ gp) {
   if (c->done) return;

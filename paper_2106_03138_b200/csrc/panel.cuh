@@ -29,7 +29,7 @@ namespace dmqr {
 // appended verbatim.
 // Look-ahead: while the previous step's update is pending, a column's Wt
 // column (l rows, indexed from n_s) rides along as extra rows m .. m + l.
-constexpr int SWAP_ROWS = 16;                  // rows per CTA
+constexpr int SWAP_ROWS = 32;                  // rows per CTA (256-byte column segments)
 constexpr int SWAP_T = 256;
 constexpr int SWAP_MAXMV = 2 * DMQR_KP;        // 144
 constexpr size_t SWAP_SMEM = sizeof(double) * SWAP_MAXMV * SWAP_ROWS;  // 36 KB
@@ -63,7 +63,24 @@ __global__ void __launch_bounds__(SWAP_T) k_swap(Ctl* c, double* __restrict__ A,
   }
   __syncthreads();
   const int64_t r0 = (int64_t)blockIdx.x * SWAP_ROWS;
-  if (nmv > 0 && r0 < nrow) {
+  if (kTMASwap && nmv > 0 && r0 + SWAP_ROWS <= m) {
+    // a whole 256-byte segment of every moved column: TMA bulk copies (one
+    // lane per move) into shared memory, then bulk stores to the destinations
+    // (the row range is closed under the moves: every source is read before
+    // any destination is written)
+    __shared__ __align__(8) uint64_t s_bar;
+    if (tid == 0) mbar_init(&s_bar, 1);
+    __syncthreads();
+    constexpr unsigned SEG = SWAP_ROWS * sizeof(double);
+    if (tid < 32) {
+      if (tid == 0) mbar_arrive_expect_tx(&s_bar, SEG * (unsigned)nmv);
+      for (int q = tid; q < nmv; q += 32) bulk_g2s(sws + q * SWAP_ROWS, A + (int64_t)s_src[q] * lda + r0, SEG, &s_bar);
+      mbar_wait_parity(&s_bar, 0);
+      for (int q = tid; q < nmv; q += 32) bulk_s2g(A + (int64_t)s_dst[q] * lda + r0, sws + q * SWAP_ROWS, SEG);
+      bulk_commit();
+      bulk_wait_read();
+    }
+  } else if (nmv > 0 && r0 < nrow) {  // the partial last segment and the moved Wt columns
 #pragma unroll 9
     for (int e = tid; e < nmv * SWAP_ROWS; e += SWAP_T) {
       const int q = e / SWAP_ROWS, rr = e % SWAP_ROWS;
