@@ -172,6 +172,19 @@ int dmqr_form_q_f64(const double* packed, int64_t m, int64_t n, int64_t lda, con
                     size_t ws_bytes, void* stream);
 size_t dmqr_form_q_workspace_bytes(int64_t m, int64_t qcols);
 
+/*
+ * Singular values of `batch` m x n column-major device matrices (ld, `stride`
+ * doubles apart; n <= 512, m >= n) by one-sided Jacobi with the reference
+ * oracle's rotation and stopping rule (jacobi_svd, svd.py:117-143, sweeps
+ * svd.py:74-114; round-robin pair order).  X is overwritten; sig (batch x n)
+ * receives the column norms of the converged X, unsorted; sweeps / converged
+ * per matrix.  Verification tooling for the ratio diagnostics
+ * (harness._ratio_fields, harness.py:201-216).
+ */
+int dmqr_jacobi_svd_batched_f64(double* X, int64_t batch, int64_t m, int64_t n, int64_t ld, int64_t stride,
+                                double tol, int32_t max_sweeps, double* sig, int32_t* sweeps, int32_t* converged,
+                                void* stream);
+
 /* 1 if any entry of the m x n column-major device matrix is NaN/Inf (dense(), matrix.py:32-33). */
 int dmqr_check_finite_f64(const double* A, int64_t m, int64_t n, int64_t lda, int32_t* nonfinite,
                           void* stream);

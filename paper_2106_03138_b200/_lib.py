@@ -27,6 +27,7 @@ EXPORTS = (
     "dmqr_form_q_f64",
     "dmqr_form_q_workspace_bytes",
     "dmqr_check_finite_f64",
+    "dmqr_jacobi_svd_batched_f64",
     "dmqr_strerror",
     "dmqr_version",
     "dmqr_debug_ctl",
@@ -133,6 +134,8 @@ def load() -> C.CDLL:
     lib.dmqr_form_q_f64.restype = C.c_int
     lib.dmqr_form_q_workspace_bytes.argtypes = [I64, I64]
     lib.dmqr_form_q_workspace_bytes.restype = SZ
+    lib.dmqr_jacobi_svd_batched_f64.argtypes = [P, I64, I64, I64, I64, I64, D, I32, P, P, P, VP]
+    lib.dmqr_jacobi_svd_batched_f64.restype = C.c_int
     lib.dmqr_check_finite_f64.argtypes = [P, I64, I64, I64, P, VP]
     lib.dmqr_check_finite_f64.restype = C.c_int
     lib.dmqr_strerror.argtypes = [C.c_int]

@@ -260,7 +260,11 @@ __device__ __noinline__ void spin_timeout(int site, long long a, long long b) {
 struct SpinGuard {
   unsigned polls = 0;
   __device__ __forceinline__ void tick(int site, long long a, long long b) {
+#ifdef DMQR_NO_SPIN_GUARD  // A/B builds
+    if (false) {
+#else
     if (++polls == (1u << 21)) {
+#endif
 #ifdef DMQR_SPIN_REPORT
       spin_timeout(site, a, b);
 #else

@@ -33,6 +33,7 @@
 #include "qp3.cuh"
 #include "formq.cuh"
 #include "small.cuh"
+#include "jacobi.cuh"
 
 using namespace dmqr;
 
@@ -1312,6 +1313,25 @@ size_t dmqr_form_q_workspace_bytes(int64_t m, int64_t qcols) {
   // Wp (splits x 64 x qcols), W (64 x qcols), Sp (splits x 64 x 64), T (64 x 64)
   return al(sizeof(double) * FQ_NSPLIT * FQ_NB * q) + al(sizeof(double) * FQ_NB * q) +
          al(sizeof(double) * FQ_NSPLIT * FQ_NB * FQ_NB) + al(sizeof(double) * FQ_NB * FQ_NB);
+}
+
+/* Singular values of a batch of small matrices by one-sided Jacobi (the
+ * reference's verification oracle jacobi_svd, svd.py:117-143); X is
+ * overwritten.  Verification tooling for the ratio diagnostics. */
+int dmqr_jacobi_svd_batched_f64(double* X, int64_t batch, int64_t m, int64_t n, int64_t ld, int64_t stride,
+                                double tol, int32_t max_sweeps, double* sig, int32_t* sweeps, int32_t* converged,
+                                void* stream) {
+  if (batch < 0 || m < 0 || n < 0 || n > JS_NMAX || ld < std::max<int64_t>(1, m) || stride < ld * n ||
+      max_sweeps < 1 || !(tol > 0.0))
+    return DMQR_EINVAL;
+  if (batch == 0 || n == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const DevInfo d = dev_info();
+  const unsigned grid = (unsigned)std::min<int64_t>(batch, (int64_t)d.sms * 4);
+  k_jacobi_svd<<<grid, JS_T, 0, st>>>(X, batch, m, (int)n, ld, stride, tol, max_sweeps, sig, sweeps, converged);
+  NOTE_LAUNCH();
+  CK(cudaGetLastError());
+  return 0;
 }
 
 int dmqr_form_q_f64(const double* packed, int64_t m, int64_t n, int64_t lda, const double* coeffs,

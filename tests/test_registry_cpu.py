@@ -39,7 +39,7 @@ def test_ratio_fields_identity_like_reference():
     from paper_2106_03138_b200.diagnostics import ratio_fields
 
     res = SimpleNamespace(packed=np.eye(8), n_factored=8)
-    out = ratio_fields(res, np.ones(8), 8)
+    out = ratio_fields(res, np.ones(8), 8, r11_svd="host")
     assert all(abs(v - 1.0) <= 1e-12 for v in out[:4]) and out[4] == ""
-    short = ratio_fields(SimpleNamespace(packed=np.eye(8), n_factored=5), np.ones(8), 8)
+    short = ratio_fields(SimpleNamespace(packed=np.eye(8), n_factored=5), np.ones(8), 8, r11_svd="host")
     assert short[4] == "short_factorization"

@@ -25,4 +25,5 @@ for r in range(reps + 1):
     torch.cuda.synchronize()
     if r:
         ts.append(e0.elapsed_time(e1))
-print(f"{Path.cwd().name} {cfg} n={n}: best {min(ts):.2f} ms median {sorted(ts)[len(ts) // 2]:.2f} ms rank {int(f.info.rank)}")
+if ts:
+    print(f"{Path.cwd().name} {cfg} n={n}: best {min(ts):.2f} ms median {sorted(ts)[len(ts) // 2]:.2f} ms rank {int(f.info.rank)}")
