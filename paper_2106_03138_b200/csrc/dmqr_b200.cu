@@ -699,6 +699,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     // G = Q1^T C split-K items over the spare CTAs: as many splits as keep the
     // items within whole waves of the CTAs (a CTA with one item more than the
     // rest sets the phase's length)
+    // (one wave: finer items, 2-3 waves, measured slower -- their partial sums cost more than the tail they trim)
     const int nsplit_g = choose_nsplit(ntile_g, 2 * std::max(1, d.sms - Pcq),
                                        (int)std::min<int64_t>(NSPLIT_MAX, std::max<int64_t>(1, ceil_div(mp, 256))));
     if (la_rest && !cq_path) CK(launch_la_rest(false));
