@@ -40,7 +40,15 @@ using namespace dmqr;
 namespace {
 
 constexpr int GRAM_GMAX = 148;
-constexpr int NSPLIT_MAX = 16;
+constexpr int NSPLIT_MAX = 16;  // split-K partials of Y^T C (k_spare's G: at most this many)
+int64_t ldz_for(int64_t n);
+// k_trail_a's split count cap: 16, or up to 64 when the partials stay small
+// (few columns: a tall input like cfg4, 65536 x 1024, has only 16 column tiles
+// and needs the row splits to fill the GPU)
+int nsplit_cap(int64_t n) {
+  const int64_t per = (int64_t)sizeof(double) * DMQR_KP * ldz_for(n);
+  return (int)std::clamp<int64_t>(((int64_t)64 << 20) / per, NSPLIT_MAX, 64);
+}
 constexpr int PANEL_PMAX = 160;
 
 struct Layout {
@@ -70,7 +78,7 @@ Layout layout(int64_t m, int64_t n) {
   L.red = take(sizeof(double) * std::max<size_t>(2 * PANEL_PMAX * RED_LD, 39 * DMQR_KP * DMQR_KP));
   L.gram = take(sizeof(double) * GRAM_GMAX * GRAM_PART);
   L.gfin = take(sizeof(double) * DMQR_KP * DMQR_KP);
-  L.Zp = take(sizeof(double) * NSPLIT_MAX * DMQR_KP * ldz_for(n));
+  L.Zp = take(sizeof(double) * nsplit_cap(n) * DMQR_KP * ldz_for(n));
   L.Z = take(sizeof(double) * DMQR_KP * ldz_for(n));
   L.trace = take(sizeof(unsigned long long) * 4);
   L.pdbg = take(sizeof(long long) * 64 * 16);
@@ -778,7 +786,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     if (ncols_ub > 0) {
       const int64_t ntile = ceil_div(ncols_ub, TA_COLS);
       const int nsplit = choose_nsplit(ntile, 2 * d.sms,
-                                       (int)std::min<int64_t>(NSPLIT_MAX, std::max<int64_t>(1, ceil_div(mp, 256))));
+                                       (int)std::min<int64_t>(nsplit_cap(n), std::max<int64_t>(1, ceil_div(mp, 256))));
       if (spare) {
         CK(pdl_launch(k_trail_w, dim3((unsigned)ceil_div(ncols_ub, TW_COLS)), dim3(TA_T), TW_SMEM, st, ctl, A,
                       (const double*)Zp, (const double*)(red + 19 * DMQR_KP * DMQR_KP), Z, ldz, u, uref, upd,

@@ -44,12 +44,14 @@ constexpr size_t TA_SMEM_ST = sizeof(double) * TA_NST * (DMQR_KP + TA_COLS) * TA
 constexpr size_t TA_SMEM_TZ = sizeof(double) * 2 * DMQR_KP * TW_LD;
 constexpr size_t TA_SMEM = TA_SMEM_ST > TA_SMEM_TZ ? TA_SMEM_ST : TA_SMEM_TZ;
 
-// One landed 16-row slab of Z += Y^T C: warp w owns output columns 8w..8w+7,
-// all lt row tiles.  Instantiated per lt so that no predicated (dead) DMMA is
-// issued when fewer than 9 reflector tiles are in use (l <= 16 steps of tall
-// or graded inputs issue 2 of 9).
+// One landed slab of Z += Y^T C, instantiated per lt (no predicated dead DMMA):
+// warp w owns output columns 8w..8w+7 and all lt row tiles (per k-step one C
+// fragment and lt Y fragments).  (A 2 x 4 warp grid with 16 columns per warp,
+// 0.7 instead of 1.1 shared loads per DMMA, measured 1% slower on cfg4 and at
+// 8192^2: shared-memory bandwidth does not bound this loop.)
+constexpr int TA_ACC = DMQR_KP / 8;
 template <int LT>
-__device__ __forceinline__ void ta_slab_mma_t(double (&acc)[DMQR_KP / 8][2], const double* ys, const double* cs,
+__device__ __forceinline__ void ta_slab_mma_t(double (&acc)[TA_ACC][2], const double* ys, const double* cs,
                                               int lane, int wid) {
 #pragma unroll
   for (int ks = 0; ks < TA_ROWS / 4; ++ks) {
@@ -59,20 +61,30 @@ __device__ __forceinline__ void ta_slab_mma_t(double (&acc)[DMQR_KP / 8][2], con
     for (int q = 0; q < LT; ++q) dmma884(acc[q][0], acc[q][1], ys[(q * 8 + (lane >> 2)) * TA_LD + kr], b);
   }
 }
-__device__ __forceinline__ void ta_slab_mma(int lt, double (&acc)[DMQR_KP / 8][2], const double* ys,
-                                            const double* cs, int lane, int wid) {
-  switch (lt) {
-    case 1: ta_slab_mma_t<1>(acc, ys, cs, lane, wid); break;
-    case 2: ta_slab_mma_t<2>(acc, ys, cs, lane, wid); break;
-    case 3: ta_slab_mma_t<3>(acc, ys, cs, lane, wid); break;
-    case 4: ta_slab_mma_t<4>(acc, ys, cs, lane, wid); break;
-    case 5: ta_slab_mma_t<5>(acc, ys, cs, lane, wid); break;
-    case 6: ta_slab_mma_t<6>(acc, ys, cs, lane, wid); break;
-    case 7: ta_slab_mma_t<7>(acc, ys, cs, lane, wid); break;
-    case 8: ta_slab_mma_t<8>(acc, ys, cs, lane, wid); break;
-    default: ta_slab_mma_t<DMQR_KP / 8>(acc, ys, cs, lane, wid); break;
+// the warp's partial tiles -> out (a Zp split, ld ldz) at columns col0 + 8w ..
+template <int LT>
+__device__ __forceinline__ void ta_store_t(const double (&acc)[TA_ACC][2], double* out, int64_t ldz, int64_t col0,
+                                           int lane, int wid) {
+  const int64_t cc = col0 + wid * 8 + 2 * (lane & 3);
+#pragma unroll
+  for (int q = 0; q < LT; ++q) {
+    const int i = q * 8 + (lane >> 2);
+    out[(int64_t)i * ldz + cc] = acc[q][0];
+    out[(int64_t)i * ldz + cc + 1] = acc[q][1];
   }
 }
+#define TA_DISPATCH(fn, ...)                     \
+  switch (lt) {                                  \
+    case 1: fn<1>(__VA_ARGS__); break;           \
+    case 2: fn<2>(__VA_ARGS__); break;           \
+    case 3: fn<3>(__VA_ARGS__); break;           \
+    case 4: fn<4>(__VA_ARGS__); break;           \
+    case 5: fn<5>(__VA_ARGS__); break;           \
+    case 6: fn<6>(__VA_ARGS__); break;           \
+    case 7: fn<7>(__VA_ARGS__); break;           \
+    case 8: fn<8>(__VA_ARGS__); break;           \
+    default: fn<DMQR_KP / 8>(__VA_ARGS__); break; \
+  }
 
 // Look-ahead bookkeeping of a step's own panel columns, by one CTA: u of the
 // accepted columns is cleared; the columns [n_s + l, tc0) that the Householder
@@ -258,9 +270,9 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* c, double* __restrict_
       if (r < rb || r >= re || r <= i) ys[i * TA_LD + rr] = (r == i && r >= rb && r < re) ? 1.0 : 0.0;
     }
   };
-  double acc[DMQR_KP / 8][2];
+  double acc[TA_ACC][2];
 #pragma unroll
-  for (int q = 0; q < DMQR_KP / 8; ++q) acc[q][0] = acc[q][1] = 0.0;
+  for (int q = 0; q < TA_ACC; ++q) acc[q][0] = acc[q][1] = 0.0;
   for (int q = 0; q < TA_NST - 1; ++q) {  // prologue: TA_NST - 1 slabs in flight (empty groups past the end)
     if (q < nslab)
       issue(q);
@@ -279,7 +291,7 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* c, double* __restrict_
     }
     const double* ys = ysb(sl % TA_NST);
     const double* cs = csb(sl % TA_NST);
-    ta_slab_mma(lt, acc, ys, cs, lane, wid);
+    TA_DISPATCH(ta_slab_mma_t, acc, ys, cs, lane, wid)
     __syncthreads();  // (stage sl % TA_NST is refilled by the issue below, TA_NST - 1 slabs ahead)
     if (sl + TA_NST - 1 < nslab)
       issue(sl + TA_NST - 1);
@@ -288,14 +300,8 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* c, double* __restrict_
   }
   // ---- partial tile -> Zp[split] ----
   double* out = Zp + (int64_t)blockIdx.y * DMQR_KP * ldz;
+  TA_DISPATCH(ta_store_t, acc, out, ldz, col0, lane, wid)
   const int64_t cc = col0 + wid * 8 + 2 * (lane & 3);
-#pragma unroll
-  for (int q = 0; q < DMQR_KP / 8; ++q) {
-    if (q >= lt) break;
-    const int i = q * 8 + (lane >> 2);
-    out[(int64_t)i * ldz + cc] = acc[q][0];
-    out[(int64_t)i * ldz + cc + 1] = acc[q][1];
-  }
   // ---- last split CTA of this column tile: Wt = T^T * sum_s Zp[s] ----
   __threadfence();
   __syncthreads();
@@ -320,11 +326,14 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* c, double* __restrict_
     double s = 0.0;
     if (t < l) {
       const double* zp = Zp + (int64_t)t * ldz + col0 + c2;
-      double v[16];
+      for (int sp0 = 0; sp0 < nsplit; sp0 += 16) {  // (16 loads in flight; fixed order)
+        double v[16];
 #pragma unroll
-      for (int sp = 0; sp < 16; ++sp) v[sp] = (sp < nsplit) ? __ldcg(zp + (int64_t)sp * DMQR_KP * ldz) : 0.0;
+        for (int sp = 0; sp < 16; ++sp)
+          v[sp] = (sp0 + sp < nsplit) ? __ldcg(zp + (int64_t)(sp0 + sp) * DMQR_KP * ldz) : 0.0;
 #pragma unroll
-      for (int sp = 0; sp < 16; ++sp) s += v[sp];
+        for (int sp = 0; sp < 16; ++sp) s += v[sp];
+      }
     }
     zs[t * TW_LD + c2] = s;
   }
