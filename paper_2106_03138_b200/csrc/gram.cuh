@@ -43,7 +43,7 @@ struct PlanSmem {
 
 // sel_smem: the selected columns already in shared memory (else read from c->sel)
 __device__ void plan_swaps_warp(Ctl* c, const CtlSnap& S, int nsel, double gamma, PlanSmem& ps,
-                                const int* sel_smem = nullptr) {
+                                const int* sel_smem = nullptr, bool write_gamma = true) {
   const int lane = threadIdx.x & 31;
   const int n_s = S.n_s;
   const int k_s = (int)min((int64_t)nsel, S.kmax - n_s);
@@ -55,7 +55,7 @@ __device__ void plan_swaps_warp(Ctl* c, const CtlSnap& S, int nsel, double gamma
   if (lane == 0) {
     c->nsel = nsel;
     c->k_s = k_s;
-    c->gamma = gamma;
+    if (write_gamma) c->gamma = gamma;
     c->eps_s = S.tau * S.umax;
     for (int i = 0; i < k_s; ++i) {
       int p = ps.sel[i];
@@ -516,29 +516,55 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* c, const double* __
     }
     __syncthreads();
     GFT(6);
-    if (tid == 0) {  // (masks loaded 8 at a time: only the AND chain is serial)
-      unsigned long long acc = 1ull;  // accepted q < 64 (t = 64 is the last candidate)
-      int nch = 1;
-      sm.chosen[0] = 0;
-      for (int t0 = 1; t0 < ncand; t0 += 8) {
-        unsigned long long cf[8];
+    if (wid == 0) {
+      // the AND chain on one lane, branch-free (the accepted set as a bit mask;
+      // candidate 64, the last possible, separately), then the chosen list by
+      // ballot compaction in candidate order
+      unsigned long long acc = 1ull;  // accepted q < 64
+      int last = 0;                   // candidate 64 accepted
+      if (lane == 0) {
+        const int nb = min(ncand, 64);
+        for (int t0 = 1; t0 < nb; t0 += 8) {
+          unsigned long long cf[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) cf[q] = (t0 + q < ncand) ? sm.conf[t0 + q] : ~0ull;
+          for (int q = 0; q < 8; ++q) cf[q] = (t0 + q < nb) ? sm.conf[t0 + q] : ~0ull;
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (!(cf[q] & acc)) {
-            const int t = t0 + q;
-            if (t < 64) acc |= 1ull << t;
-            sm.chosen[nch++] = t;
-          }
+          for (int q = 0; q < 8; ++q)
+            if (t0 + q < nb) acc |= (unsigned long long)((cf[q] & acc) == 0ull) << (t0 + q);
+        }
+        if (ncand > 64) last = (sm.conf[64] & acc) == 0ull;
       }
-      sm.nch = nch;
+      acc = __shfl_sync(0xffffffffu, acc, 0);
+      last = __shfl_sync(0xffffffffu, last, 0);
+      const bool b0 = (acc >> lane) & 1ull, b1 = (acc >> (lane + 32)) & 1ull;
+      const unsigned m0 = __ballot_sync(0xffffffffu, b0), m1 = __ballot_sync(0xffffffffu, b1);
+      const unsigned below = (1u << lane) - 1u;
+      if (b0) sm.chosen[__popc(m0 & below)] = lane;
+      if (b1) sm.chosen[__popc(m0) + __popc(m1 & below)] = lane + 32;
+      if (lane == 0) {
+        const int n64 = __popc(m0) + __popc(m1);
+        if (last) sm.chosen[n64] = 64;
+        sm.nch = n64 + last;
+      }
     }
     __syncthreads();
     GFT(7);
     const int nch = sm.nch;
+    if (wid == 0) {
+      // the selection and the swap plan (warp 0) beside gamma (warps 1..7)
+      for (int q = lane; q < nch; q += 32) {
+        const int sq = sm.cand[sm.chosen[q]];
+        sm.sel[q] = sq;
+        c->sel[q] = sq;
+      }
+      __syncwarp();
+      GFT(4);
+      plan_swaps_warp(c, S, nch, 1.0, sm.plan, sm.sel, /*write_gamma=*/false);
+      GFT(5);
+      return;
+    }
     // gamma = min_i 1 - (sum_j |theta_ij| - 1) over the chosen submatrix (dm.py:175-176)
-    for (int p = wid; p < nch; p += GRAM_T / 32) {
+    for (int p = wid - 1; p < nch; p += GRAM_T / 32 - 1) {
       const int i = sm.chosen[p];
       double sacc = 0.0;
       for (int q = lane; q < nch; q += 32) {
@@ -548,21 +574,13 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* c, const double* __
       sacc = warp_sum(sacc);
       if (lane == 0) sm.rowsum[p] = 1.0 - (sacc - 1.0);
     }
-    __syncthreads();
-    if (wid != 0) return;
+    asm volatile("bar.sync 1, %0;" ::"n"(GRAM_T - 32) : "memory");  // warps 1..7 only
+    if (wid != 1) return;
     double gmin = 1e300;
     for (int p = lane; p < nch; p += 32) gmin = fmin(gmin, sm.rowsum[p]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) gmin = fmin(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
-    for (int q = lane; q < nch; q += 32) {
-      const int sq = sm.cand[sm.chosen[q]];
-      sm.sel[q] = sq;
-      c->sel[q] = sq;
-    }
-    __syncwarp();
-    GFT(4);
-    plan_swaps_warp(c, S, nch, gmin, sm.plan, sm.sel);
-    GFT(5);
+    if (lane == 0) c->gamma = gmin;
     return;
   }
   if (wid != 0) return;
