@@ -53,7 +53,10 @@ typedef struct dmqr_params {
   double tau;            /* (0, 1]   default 0.15 */
   double delta;          /* [0, 1)   default 0.9  */
   double epsilon;        /* StopCriterion.epsilon, default 2^-52 */
-  int32_t k_dm;          /* >= 1     default 64   */
+  int32_t k_dm;          /* >= 1     default 64; above 64 the wide selection
+                            kernels run (csrc/wide.cuh) and the workspace
+                            grows with min(k_dm, n - 1) -- size it with the
+                            same params (dmqr_workspace_bytes) */
   int32_t use_delta_max; /* 0/1 */
   int32_t stop_rule;     /* DMQR_STOP_* */
   int32_t break_check;   /* 1 = qrdm2, 0 = qrdm */

@@ -28,8 +28,10 @@ from .rrqr import (
     _check,
     _steps_from_raw,
     _torch,
+    engine_k_dm,
     lda_for,
     replay_counters,
+    swap_capacity,
 )
 
 
@@ -99,9 +101,10 @@ def factorize_batch(A, params: DMParams = DMParams(), stop: StopCriterion = Stop
     dev = buf.device
     kmax = min(m, n)
     step_cap = max(kmax, 1)
-    swap_cap = max(kmax * (params.k_dm + 1) + 8, 8)
+    k_dm = engine_k_dm(params.k_dm, n)
+    swap_cap = swap_capacity(kmax, k_dm)
     p = _lib.Params(tau=float(params.tau), delta=float(params.delta), epsilon=float(stop.epsilon),
-                    k_dm=int(params.k_dm), use_delta_max=int(bool(params.use_delta_max)),
+                    k_dm=k_dm, use_delta_max=int(bool(params.use_delta_max)),
                     stop_rule=rule_code(stop), break_check=int(bool(break_check)), trace_norms=0,
                     max_steps=0)
     coeffs = torch.zeros((b, max(kmax, 1)), dtype=torch.float64, device=dev)

@@ -69,10 +69,40 @@ struct Ctl {
   uint32_t bar_gen;
   uint32_t trace_bits_lo, trace_bits_hi;
   uint32_t pad1[3];
+  // wide selection (k_dm > DMQR_MAXK - 1, wide.cuh): one deviation-maximization
+  // step of more than DMQR_MAXK selected columns runs as consecutive panel
+  // chunks without a new selection.  w_total: the step's k_s; w_done: columns
+  // accepted by its chunks so far; w_next: columns the next chunk continues
+  // with (0: the step is over); w_cont: the current chunk continues a step;
+  // w_ns0: the step's n_s; w_nmv: column moves of its swap plan
+  int32_t w_total, w_done, w_next, w_cont, w_ns0, w_nmv;
   // fixed at init (k_init): the per-matrix block stride of a batched launch
   // (zshift) and the debug timeline buffer in the workspace (null: off)
   int64_t zstride;
   unsigned long long* tl;
+};
+
+// Workspace buffers of the wide selection (k_dm > DMQR_MAXK - 1, wide.cuh),
+// sized for W = 1 + min(k_dm, n - 1) candidates (WP = W rounded up to 32)
+struct WideBufs {
+  int32_t* cand;     // [W] candidates, seed first (absolute columns)
+  int32_t* list_i;   // [W] candidate list before the sort
+  double* list_u;    // [W]
+  double* gpart;     // [nsplit][WP][WP] Gram partials (upper tiles)
+  double* theta;     // [WP][WP] cosines (when they do not fit in shared memory)
+  double* vec;       // [3][W] chosen / rowsum / inv (when they do not fit in shared memory)
+  int32_t* pos;      // [W] positions of the selected columns during the swap plan
+  int32_t* pstamp;   // [n] position-map validity (stamp = step_idx + 1)
+  int32_t* pmap;     // [n] position -> index into pos
+  int32_t* cstamp;   // [n] content-map validity
+  int32_t* cmap;     // [n] slot -> column it holds after the transpositions
+  int32_t* mv_src;   // [2W] composed moves new[dst] = old[src]
+  int32_t* mv_dst;   // [2W]
+  double* tmpA;      // [2W][m] moved column contents
+  double* tmpu;      // [2W] moved u / uref / perm
+  double* tmpr;
+  int64_t* tmpp;
+  int32_t W, WP, nsplit, m_tmp;
 };
 
 // Batched launches (grid.z = matrices of a batch, small matrices): every
@@ -103,7 +133,7 @@ struct CtlSnap {
   double floor, stop_rhs, tau, delta, umax;
   int32_t stop_active, break_check, k_dm, use_delta_max, trace_norms, swap_cap, step_cap;
   int32_t n_s, done, step_idx, n_swaps, kind, k_max, nsel, k_s, l_acc, ncand, nsw, nmv;
-  int32_t cq_fail, tc0, la, pend, pend_ns, pend_l, q1_fail, q1_kk;
+  int32_t cq_fail, tc0, la, pend, pend_ns, pend_l, q1_fail, q1_kk, w_cont;
   unsigned long long* tl;
 };
 // (GPU-scope relaxed loads in volatile asm: the control block is written by
@@ -147,7 +177,7 @@ __device__ __forceinline__ CtlSnap snap_load(const Ctl* c) {
   CTL_LD(kind); CTL_LD(k_max); CTL_LD(nsel); CTL_LD(k_s); CTL_LD(l_acc);
   CTL_LD(ncand); CTL_LD(nsw); CTL_LD(nmv); CTL_LD(cq_fail); CTL_LD(tc0);
   CTL_LD(la); CTL_LD(pend); CTL_LD(pend_ns); CTL_LD(pend_l);
-  CTL_LD(q1_fail); CTL_LD(q1_kk); CTL_LD(tl);
+  CTL_LD(q1_fail); CTL_LD(q1_kk); CTL_LD(w_cont); CTL_LD(tl);
 #undef CTL_LD
   return s;
 }

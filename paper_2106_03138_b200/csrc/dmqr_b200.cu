@@ -34,6 +34,7 @@
 #include "formq.cuh"
 #include "small.cuh"
 #include "jacobi.cuh"
+#include "wide.cuh"
 
 using namespace dmqr;
 
@@ -53,7 +54,12 @@ constexpr int PANEL_PMAX = 160;
 
 struct Layout {
   size_t ctl, u, uref, T, red, gram, gfin, Zp, Z, trace, pdbg, tcount, upd, lacount, q1g, pg, glist;
-  size_t qvb, qwb, qpart, qgpart, qcnt, hpart, hR, hctr, gnp, tl, total;
+  size_t qvb, qwb, qpart, qgpart, qcnt, hpart, hR, hctr, gnp, tl;
+  // wide selection (k_dm > WIDE_K): W candidates, WP = W rounded to 32
+  int W, WP, wsplit;
+  size_t wcand, wlist_i, wlist_u, wgpart, wtheta, wvec, wpos, wpstamp, wpmap, wcstamp, wcmap, wmv_src, wmv_dst, wtmpA,
+      wtmpu, wtmpr, wtmpp;
+  size_t total;
 };
 
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -62,7 +68,7 @@ size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 int64_t ldz_for(int64_t n) { return (std::max<int64_t>(n, 1) + 7) / 8 * 8 + 64; }
 
 
-Layout layout(int64_t m, int64_t n) {
+Layout layout(int64_t m, int64_t n, int64_t k_dm = 0) {
   Layout L{};
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -101,6 +107,32 @@ Layout layout(int64_t m, int64_t n) {
   // serial guard norms: (column, 4096-row chunk) partials
   L.gnp = take(sizeof(double) * 2 * (size_t)std::max<int64_t>(n, 1) * (size_t)std::max<int64_t>(1, (m + GN_ROWS - 1) / GN_ROWS));
   L.tl = take(sizeof(unsigned long long) * TL_WORDS);  // debug timeline (DMQR_TIMELINE)
+  if (k_dm > WIDE_K) {  // wide selection buffers (wide.cuh)
+    const int64_t W = 1 + std::min<int64_t>(k_dm, std::max<int64_t>(n - 1, 0));
+    const int64_t WP = (W + 31) / 32 * 32;
+    const int64_t nt = WP / 32, tiles = nt * (nt + 1) / 2;
+    L.W = (int)W;
+    L.WP = (int)WP;
+    L.wsplit = (int)std::clamp<int64_t>(ceil_div(296, tiles), 1, WIDE_SPLIT_MAX);
+    const size_t nn = (size_t)std::max<int64_t>(n, 1), mm = (size_t)std::max<int64_t>(m, 1);
+    L.wcand = take(sizeof(int32_t) * W);
+    L.wlist_i = take(sizeof(int32_t) * W);
+    L.wlist_u = take(sizeof(double) * W);
+    L.wgpart = take(sizeof(double) * (size_t)L.wsplit * WP * WP);
+    L.wtheta = take(sizeof(double) * (size_t)WP * WP);
+    L.wvec = take(sizeof(double) * 3 * (size_t)W);
+    L.wpos = take(sizeof(int32_t) * W);
+    L.wpstamp = take(sizeof(int32_t) * nn);
+    L.wpmap = take(sizeof(int32_t) * nn);
+    L.wcstamp = take(sizeof(int32_t) * nn);
+    L.wcmap = take(sizeof(int32_t) * nn);
+    L.wmv_src = take(sizeof(int32_t) * 2 * W);
+    L.wmv_dst = take(sizeof(int32_t) * 2 * W);
+    L.wtmpA = take(sizeof(double) * 2 * (size_t)W * mm);
+    L.wtmpu = take(sizeof(double) * 2 * W);
+    L.wtmpr = take(sizeof(double) * 2 * W);
+    L.wtmpp = take(sizeof(int64_t) * 2 * W);
+  }
   L.total = off;
   return L;
 }
@@ -265,7 +297,7 @@ int validate(int64_t m, int64_t n, int64_t lda, const dmqr_params* p) {
   if (m < 0 || n < 0 || lda < std::max<int64_t>(1, m)) return DMQR_EINVAL;
   if (!(p->tau > 0.0 && p->tau <= 1.0)) return DMQR_EINVAL;
   if (!(p->delta >= 0.0 && p->delta < 1.0)) return DMQR_EINVAL;
-  if (p->k_dm < 1 || p->k_dm > DMQR_MAXK - 1) return DMQR_EINVAL;
+  if (p->k_dm < 1) return DMQR_EINVAL;  // (k_dm > 64: wide selection, wide.cuh)
   if (p->stop_rule < 0 || p->stop_rule > 2) return DMQR_EINVAL;
   if (m > 0x7fffffffLL || n > 0x7fffffffLL) return DMQR_EINVAL;
   return 0;
@@ -390,8 +422,7 @@ const char* dmqr_strerror(int code) {
 }
 
 size_t dmqr_workspace_bytes(int64_t m, int64_t n, const dmqr_params* params) {
-  (void)params;
-  return layout(m, n).total;
+  return layout(m, n, params ? params->k_dm : 0).total;
 }
 
 int dmqr_check_finite_f64(const double* A, int64_t m, int64_t n, int64_t lda, int32_t* nonfinite, void* stream) {
@@ -446,7 +477,9 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   int rc = validate(m, n, lda, p);
   if (rc) return rc;
   if (!info) return DMQR_EINVAL;
-  const Layout L = layout(m, n);
+  const bool wide = !qrp && p->k_dm > WIDE_K;  // wide selection (wide.cuh)
+  if (wide && nz > 1) return DMQR_EINVAL;
+  const Layout L = layout(m, n, qrp ? 0 : p->k_dm);
   if (ws_bytes < L.total || !workspace) return DMQR_EINVAL;
   if (p->trace_norms && !norm_trace) return DMQR_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
@@ -489,6 +522,37 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   int32_t* glist = (int32_t*)(ws + L.glist);
   unsigned* lacount = (unsigned*)(ws + L.lacount);
   StepRec* srec = (StepRec*)steps;
+  WideBufs wb{};
+  int wf_smode = 0;
+  if (wide) {
+    wb.cand = (int32_t*)(ws + L.wcand);
+    wb.list_i = (int32_t*)(ws + L.wlist_i);
+    wb.list_u = (double*)(ws + L.wlist_u);
+    wb.gpart = (double*)(ws + L.wgpart);
+    wb.theta = (double*)(ws + L.wtheta);
+    wb.vec = (double*)(ws + L.wvec);
+    wb.pos = (int32_t*)(ws + L.wpos);
+    wb.pstamp = (int32_t*)(ws + L.wpstamp);
+    wb.pmap = (int32_t*)(ws + L.wpmap);
+    wb.cstamp = (int32_t*)(ws + L.wcstamp);
+    wb.cmap = (int32_t*)(ws + L.wcmap);
+    wb.mv_src = (int32_t*)(ws + L.wmv_src);
+    wb.mv_dst = (int32_t*)(ws + L.wmv_dst);
+    wb.tmpA = (double*)(ws + L.wtmpA);
+    wb.tmpu = (double*)(ws + L.wtmpu);
+    wb.tmpr = (double*)(ws + L.wtmpr);
+    wb.tmpp = (int64_t*)(ws + L.wtmpp);
+    wb.W = L.W;
+    wb.WP = L.WP;
+    wb.nsplit = L.wsplit;
+    wb.m_tmp = (int32_t)std::max<int64_t>(m, 1);
+    const size_t cap = std::min<size_t>(d.smem_optin, 200 * 1024);
+    wf_smode = wfin_smem(L.W, 2) <= cap ? 2 : (wfin_smem(L.W, 1) <= cap ? 1 : 0);
+    CK(cudaFuncSetAttribute(k_wfin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wfin_smem(L.W, wf_smode)));
+    // stamps from an earlier call on this workspace must not match this one's
+    CK(cudaMemsetAsync(wb.pstamp, 0, sizeof(int32_t) * std::max<int64_t>(n, 1), st));
+    CK(cudaMemsetAsync(wb.cstamp, 0, sizeof(int32_t) * std::max<int64_t>(n, 1), st));
+  }
   // Look-ahead (default; not with the per-step norm trace, which needs fully
   // updated columns at every step end): step k's C -= Y Wt below its R rows
   // runs beside step k+1's panel (programmatic dependent launch); step k+1's
@@ -500,7 +564,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   // cfg5 at 8192, 12288, 16384)
   const bool la_force = getenv("DMQR_FORCE_LOOKAHEAD") != nullptr;  // A/B switch: look-ahead at any shape
   const bool la_all = !qrp && !p->trace_norms && getenv("DMQR_NO_LOOKAHEAD") == nullptr &&
-                      m * n >= (int64_t)1 << 20 && ((m <= 4 * n && n <= 12288) || la_force) && NZ == 1;
+                      m * n >= (int64_t)1 << 20 && ((m <= 4 * n && n <= 12288) || la_force) && NZ == 1 && !wide;
 
 
   const int64_t kmax = std::min(m, n);
@@ -614,16 +678,40 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     }
     // ---- selection ----
     PROF(0);
-    CK(pdl_launch(k_select, dim3(1, 1, NZ), dim3(SEL_T), 0, st, ctl, (const double*)u));
-    NOTE_LAUNCH();
     const int64_t ldz = ldz_for(n);
-    const int GG = (int)std::clamp<int64_t>(ceil_div(mp, GRAM_ROWS), 1, std::min(GRAM_GMAX, d.sms));
-    CK(pdl_launch(k_gram, dim3(GG, 1, NZ), dim3(GRAM_T), GRAM_SMEM, st, ctl, A, gpart, (const double*)Z, ldz,
-                  (const uint8_t*)upd));
-    NOTE_LAUNCH();
-    CK(pdl_launch(k_gram_finish, dim3(45, 1, NZ), dim3(GRAM_T), sizeof(FinSmem), st, ctl, (const double*)A,
-                  (const double*)gpart, GG, gfin, upd, tline));
-    NOTE_LAUNCH();
+    if (wide) {
+      // wide selection (wide.cuh): candidates in the workspace, tiled Gram,
+      // one-CTA filter + swap plan, moves over every row; a continuing step's
+      // next chunk makes all of these no-ops
+      CK(pdl_launch(k_select_t<true>, dim3(1), dim3(SEL_T), 0, st, ctl, (const double*)u, wb));
+      NOTE_LAUNCH();
+      const int64_t W_ub = 1 + std::min<int64_t>(p->k_dm, std::max<int64_t>(np - 1, 0));
+      const int64_t nt = ceil_div(W_ub, 32), tiles = nt * (nt + 1) / 2;
+      const int wsp = (int)std::clamp<int64_t>(std::min<int64_t>(ceil_div(2 * d.sms, tiles), ceil_div(mp, 256)), 1,
+                                               wb.nsplit);
+      CK(pdl_launch(k_wgram, dim3((unsigned)tiles, (unsigned)wsp), dim3(WG_T), 0, st, ctl, (const double*)A, wb));
+      NOTE_LAUNCH();
+      CK(pdl_launch(k_wfin, dim3(1), dim3(WF_T), wfin_smem(wb.W, wf_smode), st, ctl, (const double*)A, swaps, wb, wsp,
+                    wf_smode));
+      NOTE_LAUNCH();
+      const dim3 mvg((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), 64)),
+                     (unsigned)std::min<int64_t>(2 * W_ub, 65535));
+      CK(pdl_launch(k_wgather, mvg, dim3(256), 0, st, ctl, (const double*)A, (const double*)u, (const double*)uref,
+                    (const int64_t*)perm, wb));
+      NOTE_LAUNCH();
+      CK(pdl_launch(k_wscatter, mvg, dim3(256), 0, st, ctl, A, u, uref, perm, wb));
+      NOTE_LAUNCH();
+    } else {
+      CK(pdl_launch(k_select_t<false>, dim3(1, 1, NZ), dim3(SEL_T), 0, st, ctl, (const double*)u, WideBufs{}));
+      NOTE_LAUNCH();
+      const int GG = (int)std::clamp<int64_t>(ceil_div(mp, GRAM_ROWS), 1, std::min(GRAM_GMAX, d.sms));
+      CK(pdl_launch(k_gram, dim3(GG, 1, NZ), dim3(GRAM_T), GRAM_SMEM, st, ctl, A, gpart, (const double*)Z, ldz,
+                    (const uint8_t*)upd));
+      NOTE_LAUNCH();
+      CK(pdl_launch(k_gram_finish, dim3(45, 1, NZ), dim3(GRAM_T), sizeof(FinSmem), st, ctl, (const double*)A,
+                    (const double*)gpart, GG, gfin, upd, tline));
+      NOTE_LAUNCH();
+    }
     {
       CK(pdl_launch(k_swap, dim3((unsigned)ceil_div(m + (la ? DMQR_KP : 0), SWAP_ROWS), 1, NZ), dim3(SWAP_T), SWAP_SMEM,
                     st, ctl, A, u, uref, perm, swaps, Z, ldz, upd));
@@ -832,6 +920,10 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
         NOTE_LAUNCH();
       }
       if (p->trace_norms) { k_norm_trace<<<(unsigned)blocks, 256, 0, st>>>(ctl, A, u, tbits); NOTE_LAUNCH(); }
+    }
+    if (wide) {  // does the step continue with its next chunk?
+      CK(pdl_launch(k_wcont, dim3(1), dim3(1024), 0, st, ctl, (const double*)A));
+      NOTE_LAUNCH();
     }
     CK(pdl_launch(k_step_end, dim3(1, 1, NZ), dim3(32), 0, st, ctl, srec, norm_trace, tbits, (const double*)A, Z, ldz, u,
                   uref, upd, hrecs, eidx));
@@ -1169,6 +1261,8 @@ LaneBufs lane_bufs(int64_t m, int64_t n, int64_t lda) {
   return b;
 }
 bool batch_graph_ok(int64_t m, int64_t n) { return m * n < ((int64_t)1 << 20); }
+// grouped launches (grid.z) need the standard selection; wide k_dm runs per matrix
+bool batch_groups(int64_t m, int64_t n, const dmqr_params* p) { return batch_graph_ok(m, n) && p->k_dm <= WIDE_K; }
 constexpr int ZG = 128;  // small matrices per batched launch (grid.z)
 }  // namespace
 
@@ -1178,7 +1272,7 @@ int32_t dmqr_batched_group(int64_t m, int64_t n) { return batch_graph_ok(m, n) ?
 
 size_t dmqr_batched_workspace_bytes(int64_t m, int64_t n, const dmqr_params* params, int32_t nlanes) {
   const size_t eng = al(dmqr_workspace_bytes(m, n, params));
-  const size_t per = batch_graph_ok(m, n) ? (size_t)ZG * (eng + lane_bufs(m, n, (m + 7) / 8 * 8).total) : eng;
+  const size_t per = batch_groups(m, n, params) ? (size_t)ZG * (eng + lane_bufs(m, n, (m + 7) / 8 * 8).total) : eng;
   return (size_t)std::max(1, nlanes) * per;
 }
 
@@ -1203,10 +1297,10 @@ int dmqr_qrdm_batched_f64(double* A, int64_t batch, int64_t m, int64_t n, int64_
   // blocks + a replayed step graph per lane (needs the caller's lda to match the
   // blocks' and caps within theirs)
   const LaneBufs lb = lane_bufs(m, n, lda);
-  const bool graphs = batch_graph_ok(m, n) && lda == (m + 7) / 8 * 8 && swap_cap <= lb.swap_cap &&
+  const bool graphs = batch_groups(m, n, p) && lda == (m + 7) / 8 * 8 && swap_cap <= lb.swap_cap &&
                       step_cap <= lb.step_cap && getenv("DMQR_NO_GRAPH") == nullptr;
   const size_t zblk = per_engine + lb.total;  // (both multiples of 256 bytes)
-  const size_t per = batch_graph_ok(m, n) ? (size_t)ZG * zblk : per_engine;
+  const size_t per = batch_groups(m, n, p) ? (size_t)ZG * zblk : per_engine;
   nlanes = (int32_t)std::min<int64_t>(nlanes, std::max<int64_t>(batch, 1));
   if (m > 4096) nlanes = 1;  // cooperative panel launches must not compete for co-residency
   if (ws_bytes < per * (size_t)nlanes || !workspace) return DMQR_EINVAL;

@@ -91,10 +91,14 @@ __device__ __forceinline__ void step_end_body(const CtlSnap& S, Ctl* c, StepRec*
   }
   const int broke = c->broke;
   const double eps_s = c->eps_s, gamma = c->gamma;
+  // a wide step (k_dm > DMQR_MAXK - 1, wide.cuh) keeps one record over its
+  // panel chunks: rewritten after every chunk, committed after the last
+  const bool wide = S.k_dm > DMQR_MAXK - 1 && S.kind == 0;
+  const bool w_more = wide && c->w_next > 0;
   StepRec r;
-  r.n_s = S.n_s;
-  r.k_selected = S.k_s;
-  r.k_accepted = l;
+  r.n_s = wide ? c->w_ns0 : S.n_s;
+  r.k_selected = wide ? c->w_total : S.k_s;
+  r.k_accepted = wide ? c->w_done : l;
   r.k_max = (S.kind == 0) ? S.k_max : -1;
   r.broke_early = broke;
   r.fell_back_to_scalar = (S.kind == 1);
@@ -115,7 +119,7 @@ __device__ __forceinline__ void step_end_body(const CtlSnap& S, Ctl* c, StepRec*
   }
   c->gcount = 0;  // (look-ahead and serial guard lists)
   c->n_s = S.n_s + l;
-  c->step_idx = idx + 1;
+  c->step_idx = idx + (w_more ? 0 : 1);
   c->l_acc = 0;
   c->broke = 0;
   c->nsw = 0;

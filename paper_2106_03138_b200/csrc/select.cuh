@@ -56,7 +56,12 @@ __device__ __forceinline__ int block_excl_scan(int v, int* scan_smem, int* total
   return res;
 }
 
-__global__ void __launch_bounds__(SEL_T) k_select(Ctl* c, const double* __restrict__ u) {
+// Wide selection (k_dm > DMQR_MAXK - 1; wide.cuh): the candidate list lives in
+// the workspace (WideBufs) instead of shared memory and the control block, and
+// a step that continues with its next panel chunk (Ctl::w_next) takes no new
+// selection: its columns already sit at n_s, n_s+1, ...
+template <bool WIDE>
+__global__ void __launch_bounds__(SEL_T) k_select_t(Ctl* c, const double* __restrict__ u, WideBufs wb) {
   zshift(c, c, u);
   pdl_enter();
   const CtlSnap S = snap(c);
@@ -77,6 +82,30 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* c, const double* __restri
   if (n_s >= S.kmax) {  // loop condition of rrqr.py:335
     if (tid == 0) c->done = 1;
     return;
+  }
+  if constexpr (WIDE) {
+    __shared__ int s_wn;
+    if (tid == 0) s_wn = ctl_ld(&c->w_next);
+    __syncthreads();
+    if (s_wn > 0) {  // the step's next chunk (rrqr.py:360-379 continues with column n_s)
+      if (tid == 0) {
+        const int k = min(s_wn, DMQR_MAXK);
+        c->kind = 0;
+        c->nsel = k;
+        c->k_s = k;
+        c->nsw = 0;
+        c->nmv = 0;
+        c->w_cont = 1;
+        c->w_next = 0;
+      }
+      if (tid < DMQR_MAXK) c->sel[tid] = n_s + tid;
+      return;
+    }
+    if (tid == 0) {
+      c->w_cont = 0;
+      c->w_done = 0;
+      c->w_nmv = 0;
+    }
   }
   const int np = n - n_s;
   // contiguous per-thread segments keep index order for compaction
@@ -176,14 +205,16 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* c, const double* __restri
   __syncthreads();
   total = s_total;
 
+  int* const list_i = WIDE ? wb.list_i : sm.list_i;
+  double* const list_u = WIDE ? wb.list_u : sm.list_u;
   int nlist;
   if (total <= k_dm) {
     // all candidates, index order
     int p = off;
     for (int i = s0; i < s1; ++i)
       if (i != seed && u[i] >= thr) {
-        sm.list_i[p] = i;
-        sm.list_u[p] = u[i];
+        list_i[p] = i;
+        list_u[p] = u[i];
         ++p;
       }
     nlist = total;
@@ -288,13 +319,13 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* c, const double* __restri
       if (i == seed || !(v >= thr)) continue;
       unsigned long long key = (unsigned long long)__double_as_longlong(v) & mask;
       if (key > T) {
-        sm.list_i[pg] = i;
-        sm.list_u[pg] = v;
+        list_i[pg] = i;
+        list_u[pg] = v;
         ++pg;
       } else if (key == T) {
         if (pe < k_rem) {
-          sm.list_i[total_gt + pe] = i;
-          sm.list_u[total_gt + pe] = v;
+          list_i[total_gt + pe] = i;
+          list_u[total_gt + pe] = v;
         }
         ++pe;
       }
@@ -303,19 +334,35 @@ __global__ void __launch_bounds__(SEL_T) k_select(Ctl* c, const double* __restri
   }
   __syncthreads();
   // ---- stable descending sort of the <= k_dm candidates by rank counting ----
-  int my_i = 0, my_rank = 0;
-  double my_u = 0.0;
-  if (tid < nlist) {
-    my_i = sm.list_i[tid];
-    my_u = sm.list_u[tid];
-    for (int q = 0; q < nlist; ++q) {
-      double ou = sm.list_u[q];
-      int oi = sm.list_i[q];
-      my_rank += (ou > my_u) || (ou == my_u && oi < my_i);
+  if constexpr (WIDE) {
+    int* const cand = wb.cand;
+    for (int t = tid; t < nlist; t += SEL_T) {
+      const int my_i = list_i[t];
+      const double my_u = list_u[t];
+      int my_rank = 0;
+      for (int q = 0; q < nlist; ++q) {
+        const double ou = list_u[q];
+        const int oi = list_i[q];
+        my_rank += (ou > my_u) || (ou == my_u && oi < my_i);
+      }
+      cand[1 + my_rank] = my_i;
     }
+    if (tid == 0) cand[0] = seed;
+  } else {
+    int my_i = 0, my_rank = 0;
+    double my_u = 0.0;
+    if (tid < nlist) {
+      my_i = list_i[tid];
+      my_u = list_u[tid];
+      for (int q = 0; q < nlist; ++q) {
+        double ou = list_u[q];
+        int oi = list_i[q];
+        my_rank += (ou > my_u) || (ou == my_u && oi < my_i);
+      }
+    }
+    __syncthreads();
+    if (tid < nlist) c->cand[1 + my_rank] = my_i;
   }
-  __syncthreads();
-  if (tid < nlist) c->cand[1 + my_rank] = my_i;
   if (tid == 0) {
     c->kind = 0;
     c->k_max = nlist;

@@ -15,7 +15,8 @@ device or the built library these functions raise.
 Differences from the reference that are by design:
   * ``packed``/``coeffs`` come back as numpy arrays by default (as in the
     reference); ``device=True`` keeps them as torch CUDA tensors.
-  * k_dm is limited to <= 64 (the paper's recommended block size is 64).
+  * any k_dm >= 1 is accepted (dm.py:56-62); above 64 the engine selects with
+    the wide kernels (csrc/wide.cuh) and runs a step's block as panel chunks.
 """
 
 from __future__ import annotations
@@ -30,7 +31,21 @@ import numpy as np
 from . import _lib
 
 EPS = float(np.finfo(np.float64).eps)
-K_DM_MAX = 64
+K_DM_FAST = 64  # k_dm above this: wide selection kernels (csrc/wide.cuh)
+
+
+def engine_k_dm(k_dm: int, n: int) -> int:
+    """k_dm as the engine takes it: at most n - 1 candidates exist besides the
+    seed, so min(k_dm, n - 1) selects exactly what k_dm does (dm.py:95-97)."""
+    return int(max(1, min(int(k_dm), max(n - 1, 1))))
+
+
+def swap_capacity(kmax: int, k_dm: int) -> int:
+    """Swap-log capacity: at most k_s <= k_dm + 1 transpositions per step
+    (rrqr.py:294-312); very wide selections are capped at 2^24 entries (the
+    engine reports DMQR_ECAP past it)."""
+    cap = max(kmax * (k_dm + 1) + 8, 8)
+    return cap if k_dm <= K_DM_FAST else max(kmax * (K_DM_FAST + 1) + 8, min(cap, 1 << 24))
 
 __all__ = [
     "EPS", "DMParams", "StopRule", "StopCriterion", "StepRecord", "WorkCounters", "Permutation",
@@ -333,19 +348,18 @@ def factorize(A, params: DMParams = DMParams(), stop: StopCriterion = StopCriter
     """
     torch = _torch()
     lib = _lib.load()
-    if params.k_dm > K_DM_MAX:
-        raise ValueError(f"k_dm > {K_DM_MAX} is not supported by the B200 engine")
     buf, m, n, lda = work if work is not None else to_work(A)
+    k_dm = engine_k_dm(params.k_dm, n)
     dev = buf.device
     st = stream if stream is not None else torch.cuda.current_stream(dev)
     sh = C.c_void_p(st.cuda_stream)
     p = _lib.Params(tau=float(params.tau), delta=float(params.delta), epsilon=float(stop.epsilon),
-                    k_dm=int(params.k_dm), use_delta_max=int(bool(params.use_delta_max)),
+                    k_dm=k_dm, use_delta_max=int(bool(params.use_delta_max)),
                     stop_rule=rule_code(stop), break_check=int(bool(break_check)),
                     trace_norms=int(bool(trace_norms)), max_steps=int(max_steps))
     kmax = min(m, n)
     step_cap = max(kmax, 1)
-    swap_cap = max(kmax * (params.k_dm + 1) + 8, 8)
+    swap_cap = swap_capacity(kmax, k_dm)
     coeffs = torch.zeros(max(kmax, 1), dtype=torch.float64, device=dev)
     perm = torch.arange(max(n, 1), dtype=torch.int64, device=dev)
     swaps = torch.empty((swap_cap, 2), dtype=torch.int64, device=dev)
@@ -475,7 +489,7 @@ def form_q(packed, coeffs, n_factored: int, qcols: int | None = None):
 def reconstruct(result: RRQRResult):
     """(Q, R) with Q m x m orthogonal and Q @ R == A @ Pi (rrqr.py:459-480); Q formed on the device."""
     Q = form_q(result.packed, result.coeffs, result.n_factored)
-    Q = Q.cpu().numpy() if not isinstance(result.packed, np.ndarray) or True else Q
+    Q = Q.cpu().numpy()
     packed = result.packed if isinstance(result.packed, np.ndarray) else result.packed.cpu().numpy()
     R = np.asfortranarray(np.array(packed, copy=True))
     for j in range(min(result.n_factored, R.shape[1])):

@@ -45,6 +45,9 @@ def case_input(name: str) -> np.ndarray:
         return np.array(store()[f"{name}/input"])
     from paper_2106_03138_b200 import inputs
     src = meta["source"]
+    if src.startswith("wide:"):
+        import wide_cases
+        return wide_cases.make(src[5:])
     if src == "fixture":
         parts = name.split("/")
         return _fixtures()[parts[2] if parts[0] == "qrp" else parts[1]]

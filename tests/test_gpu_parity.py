@@ -655,3 +655,76 @@ def test_schedule_switches_keep_parity(monkeypatch, switch):
         assert np.array_equal(r.perm.forward[:cut], s.perm.forward[:cut])
         rr, oo = parity.residuals(B[i], r)
         assert rr <= 50 * 160 * O.EPS and oo <= 50 * 160 * O.EPS
+
+
+# ---- wide k_dm (k_dm > 64: csrc/wide.cuh; dm.py:56-62 accepts any k_dm >= 1) ----
+
+WIDE_FULL = ["wide/gauss_k128", "wide/wide_qrdm_k200", "wide/break_boundary", "wide/break_boundary_qrdm",
+             "wide/break_chunk2", "wide/break_chunk3"]
+
+
+@pytest.mark.parametrize("name", WIDE_FULL)
+def test_wide_kdm_golden_full(name):
+    """Blocks of more than one 65-column panel chunk, with the QRDM2 break on a
+    chunk boundary (break_boundary: k_wcont's test), inside the second chunk and
+    inside the third: the whole run equals the reference's (swap log, step log
+    with one record per step, rank, counters)."""
+    meta = G.index()["cases"][name]
+    A = G.case_input(name)
+    assert G.sha(A) == meta["input_sha256"]
+    res = _gpu(A, meta["algo"], **G.oracle_kwargs(name))
+    ref = _golden_oracle(name)
+    _compare(A, res, ref, name, require_full=True)
+    steps = G.case_field(name, "steps")
+    assert [tuple(s) for s in _steps(res.step_log)] == [tuple(int(x) for x in s) for s in steps]
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_wide_kdm_random_vs_oracle(seed):
+    rng = np.random.default_rng(6400 + seed)
+    m = int(rng.integers(100, 700))
+    n = int(rng.integers(100, 700))
+    k_dm = [65, 66, 80, 128, 129, 200, 300, 10**9][seed]
+    kind = seed % 3
+    if kind == 0:
+        A = rng.standard_normal((m, n))
+    elif kind == 1:
+        r = int(rng.integers(1, min(m, n)))
+        A = rng.standard_normal((m, r)) @ rng.standard_normal((r, n))
+    else:
+        A = rng.standard_normal((m, n)) * np.logspace(0, -10, n)[rng.permutation(n)]
+    algo = "qrdm2" if seed % 2 == 0 else "qrdm"
+    res = _gpu(A, algo, k_dm=k_dm, use_delta_max=(seed == 5))
+    with threadpool_limits(1):
+        ref = (O.qrdm2 if algo == "qrdm2" else O.qrdm)(A, margins=True, k_dm=k_dm, use_delta_max=(seed == 5))
+    _compare(A, res, ref, f"wide-random{seed}", min_cut=1)
+    assert max(s.k_selected for s in res.step_log) == max(s.k_selected for s in ref.steps)
+
+
+@pytest.mark.parametrize("shape", [(1100, 1024), (9000, 300)])
+def test_wide_kdm_large_shapes(shape):
+    """Shapes that take the look-ahead schedule (1100 x 1024) or the tall
+    cluster panel (9000 x 300) at k_dm = 64 run serial with the wide selection."""
+    rng = np.random.default_rng(shape[0])
+    m, n = shape
+    A = rng.standard_normal((m, n)) * np.logspace(0, -6, n)[rng.permutation(n)]
+    res = _gpu(A, "qrdm2", k_dm=128)
+    with threadpool_limits(4):
+        ref = O.qrdm2(A, margins=True, k_dm=128)
+    _compare(A, res, ref, f"wide-{m}x{n}", min_cut=64)
+
+
+def test_wide_kdm_batched_per_matrix():
+    """Batches with wide k_dm run every matrix on the per-matrix engine: identical
+    to the single calls."""
+    from paper_2106_03138_b200 import DMParams, qrdm2
+    from paper_2106_03138_b200.batch import factorize_batch
+
+    rng = np.random.default_rng(99)
+    B = rng.standard_normal((5, 200, 180))
+    f = factorize_batch(B, params=DMParams(k_dm=100), lanes=2)
+    for b in range(5):
+        one = qrdm2(B[b], params=DMParams(k_dm=100))
+        r = f.result(b)
+        assert np.array_equal(r.perm.forward, one.perm.forward) and r.rank == one.rank
+        assert _steps(r.step_log) == _steps(one.step_log)

@@ -51,6 +51,25 @@ def test_workspace_bytes_no_device():
     assert 0 < small < big
 
 
+def test_wide_kdm_host_sizing():
+    """k_dm > 64 (any k_dm >= 1, dm.py:56-62): the engine takes min(k_dm, n - 1),
+    the workspace grows with it (wide selection buffers), and the swap log
+    capacity covers k_s <= k_dm + 1 transpositions per step."""
+    from paper_2106_03138_b200 import _lib
+    from paper_2106_03138_b200.rrqr import engine_k_dm, swap_capacity
+
+    assert engine_k_dm(128, 500) == 128 and engine_k_dm(10**9, 500) == 499 and engine_k_dm(5, 1) == 1
+    assert swap_capacity(100, 64) == 100 * 65 + 8
+    assert swap_capacity(100, 128) == 100 * 129 + 8
+    assert swap_capacity(20000, 19999) == 1 << 24
+    lib = _lib.load()
+    base = _lib.Params(tau=0.15, delta=0.9, epsilon=2.0 ** -52, k_dm=64)
+    wide = _lib.Params(tau=0.15, delta=0.9, epsilon=2.0 ** -52, k_dm=128)
+    b = lib.dmqr_workspace_bytes(1000, 900, C.byref(base))
+    w = lib.dmqr_workspace_bytes(1000, 900, C.byref(wide))
+    assert w > b + 2 * 129 * 1000 * 8  # (+ the moved-column staging)
+
+
 def test_params_validation_messages():
     from paper_2106_03138_b200 import DMParams
 
