@@ -30,6 +30,7 @@
 #include "panel_cq.cuh"
 #include "select.cuh"
 #include "trailing.cuh"
+#include "tail.cuh"
 #include "qp3.cuh"
 #include "formq.cuh"
 #include "small.cuh"
@@ -197,6 +198,7 @@ int set_attrs(const DevInfo& d, DevAttrs** out) {
   CK(cudaFuncSetAttribute(k_gram_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FinSmem)));
   CK(cudaFuncSetAttribute(k_trail_b<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
   CK(cudaFuncSetAttribute(k_trail_b<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
+  CK(cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TAIL_SMEM));
   CK(cudaFuncSetAttribute(k_spare<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SP_SMEM));
   CK(cudaFuncSetAttribute(k_spare<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SP_SMEM));
   CK(cudaFuncSetAttribute(k_trail_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TW_SMEM));
@@ -644,6 +646,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   // P-mode look-ahead (G = R1^-T P^T C from the panel's start; panel_cq.cuh): correct, but on cfg2 the
   // earlier G traffic slows the latency-bound panel more than it shortens k_spare (16.9 vs 16.6 ms), so opt-in
   const bool pmode_on = getenv("DMQR_PMODE") != nullptr;
+  const bool fused_tail = getenv("DMQR_NO_FUSED_TAIL") == nullptr;  // schedule switch (tests): separate tail kernels
   // (test hook: DMQR_HELPER_WAIT_NS=0 makes the tall panel abandon its helpers)
   const long long hwait_ns = getenv("DMQR_HELPER_WAIT_NS") ? atoll(getenv("DMQR_HELPER_WAIT_NS")) : 5000000ll;
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
@@ -871,19 +874,24 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     // ---- trailing update ----
     PROF(2);
     const int64_t ncols_ub = std::max<int64_t>(np - 1, 0);
+    int tail_nsplit = 1;
     if (ncols_ub > 0) {
       const int64_t ntile = ceil_div(ncols_ub, TA_COLS);
       const int nsplit = choose_nsplit(ntile, 2 * d.sms,
                                        (int)std::min<int64_t>(nsplit_cap(n), std::max<int64_t>(1, ceil_div(mp, 256))));
+      tail_nsplit = nsplit;
       if (spare) {
+        // (its last CTA closes the step when no guard column came up: k_tail then exits at once)
         CK(pdl_launch(k_trail_w, dim3((unsigned)ceil_div(ncols_ub, TW_COLS)), dim3(TA_T), TW_SMEM, st, ctl, A,
                       (const double*)Zp, (const double*)(red + 19 * DMQR_KP * DMQR_KP), Z, ldz, u, uref, upd,
-                      glist));
+                      glist, fused_tail ? StepClose{srec, hrecs, lacount + 12} : StepClose{nullptr, nullptr, nullptr}));
         NOTE_LAUNCH();
       }
-      CK(pdl_launch(k_trail_a, dim3((unsigned)ntile, nsplit, NZ), dim3(TA_T), TA_SMEM, st, ctl, A, Zp,
-                    (const double*)T, Z, tcount, ldz, u, uref, upd, spare ? 1 : 0, glist));
-      NOTE_LAUNCH();
+      if (!(spare && fused_tail)) {
+        CK(pdl_launch(k_trail_a, dim3((unsigned)ntile, nsplit, NZ), dim3(TA_T), TA_SMEM, st, ctl, A, Zp,
+                      (const double*)T, Z, tcount, ldz, u, uref, upd, spare ? 1 : 0, glist));
+        NOTE_LAUNCH();
+      }
       if (la) {
         // the rest of C -= Y Wt runs beside the next step's panel
       } else {
@@ -894,6 +902,17 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     }
     // ---- norms, log ----
     PROF(3);
+    if (spare && fused_tail) {
+      // one launch for the rest of the step (tail.cuh): the panel's fallback update, guard columns,
+      // bookkeeping, host record -- or nothing at all when k_trail_w closed the step
+      TailArgs ta{ctl, A, Zp, (const double*)T, Z, tcount, ldz, u, uref, upd, glist, tail_nsplit, srec, hrecs, eidx,
+                  lacount + 13};
+      CK(pdl_launch(k_tail, dim3((unsigned)d.sms), dim3(TA_T), TAIL_SMEM, st, ta));
+      NOTE_LAUNCH();
+      PROF(4);
+      CK(cudaGetLastError());
+      return 0;
+    }
     if (la) {
       // norms: downdated in the Wt epilogues; guard columns recomputed here
       CK(pdl_launch(k_guard,

@@ -127,6 +127,25 @@ __device__ __forceinline__ void step_end_body(const CtlSnap& S, Ctl* c, StepRec*
   if (S.n_s + l >= S.kmax) c->done = 1;
 }
 
+// The host's poll record of a step (one thread): written once the step's
+// bookkeeping is done.  No stream operation sits between the steps, so the
+// programmatic launches chain across step boundaries.  The record's index is
+// counted on the device -- one per enqueued step -- so a replayed CUDA graph
+// of the step posts the right slot and sequence.  Columns left of n_s are
+// final once the record is seen (the caller fences its writes first); the
+// record itself is one 16-byte store.
+__device__ __forceinline__ void step_post(const CtlSnap& S, Ctl* c, HostRec* __restrict__ hrec) {
+  const int enq = c->posted;
+  c->posted = enq + 1;
+  // (a fallback step hands the run to the blocked scalar-pivot engine, k_qp3;
+  // not with the per-step norm trace)
+  const int fb = (!S.done && S.kind == 1 && !S.trace_norms) ? 4 : 0;
+  const int4 rec = make_int4(c->n_s, (c->done ? 1 : 0) | (c->la_bad ? 2 : 0) | fb, c->step_idx, enq + 1);
+  asm volatile("st.volatile.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(hrec + (enq & 1)), "r"(rec.x), "r"(rec.y),
+               "r"(rec.z), "r"(rec.w)
+               : "memory");
+}
+
 __global__ void k_step_end(Ctl* c, StepRec* __restrict__ steps, double* __restrict__ norm_trace,
                            unsigned long long* __restrict__ trace_bits, const double* __restrict__ A,
                            double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
@@ -138,26 +157,10 @@ __global__ void k_step_end(Ctl* c, StepRec* __restrict__ steps, double* __restri
   const CtlSnap S = snap(c);
   TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 10);
   if (!S.done) step_end_body(S, c, steps, norm_trace, trace_bits, A, Wt, ldz, u, uref, upd);
-  // the host's poll record of this step (no stream operation between the
-  // steps, so the programmatic launches chain across step boundaries)
-  // (columns left of n_s are final once the record is seen: this warp's own
-  // writes to them are fenced first; the record itself is one 16-byte store)
   __threadfence();
   __syncwarp();
-  // (the record's index is counted on the device -- one per enqueued step --
-  // so a replayed CUDA graph of the step posts the right slot and sequence)
-  if (threadIdx.x == 0 && hrec) {
-    (void)enq;
-    enq = c->posted;
-    c->posted = enq + 1;
-    // (a fallback step hands the run to the blocked scalar-pivot engine, k_qp3;
-    // not with the per-step norm trace)
-    const int fb = (!S.done && S.kind == 1 && !S.trace_norms) ? 4 : 0;
-    const int4 rec = make_int4(c->n_s, (c->done ? 1 : 0) | (c->la_bad ? 2 : 0) | fb, c->step_idx, enq + 1);
-    asm volatile("st.volatile.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(hrec + (enq & 1)), "r"(rec.x), "r"(rec.y),
-                 "r"(rec.z), "r"(rec.w)
-                 : "memory");
-  }
+  (void)enq;
+  if (threadIdx.x == 0 && hrec) step_post(S, c, hrec);
 }
 
 // switch the control block to the look-ahead schedule (from the next kernel on)

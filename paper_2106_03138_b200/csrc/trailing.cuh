@@ -204,32 +204,28 @@ __device__ void la_tile_epilogue(Ctl* c, double* __restrict__ A, double* __restr
         u[j] = sqrt(fmax(sq, 0.0));
     }
   }
-  if (blockIdx.x == 0) la_panel_columns(c, A, Wt, ldz, u, uref, upd, n_s, l, c0);
+  if (col0 == 0) la_panel_columns(c, A, Wt, ldz, u, uref, upd, n_s, l, c0);  // (the step's tile 0)
 }
 
 // grid: (ceil(n''/64), nsplit).  Zp[s][i][c] (ld ldz) = sum over this split's rows of Y[r][i] C[r][c];
 // the last split CTA of each column tile reduces them and writes Wt = T^T Z (ld ldz).
-__global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* c, double* __restrict__ A,
-                                                     double* __restrict__ Zp, const double* __restrict__ T,
-                                                     double* __restrict__ Wt, unsigned* __restrict__ counters,
-                                                     int64_t ldz, double* __restrict__ u,
-                                                     double* __restrict__ uref, uint8_t* __restrict__ upd,
-                                                     int only_if_cq_fail, int32_t* __restrict__ glist) {
-  zshift(c, c, A, Zp, T, Wt, counters, u, uref, upd, glist);
-  pdl_enter();
-  const CtlSnap S = snap(c);
-  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 8);
-  if (S.done || (only_if_cq_fail && !S.cq_fail)) return;  // (k_trail_w did it)
+// (one CTA's work: column tile bx, row split by of nsplit; k_tail runs the
+// same items from a persistent grid)
+__device__ __forceinline__ void trail_a_cta(const CtlSnap& S, Ctl* c, double* __restrict__ A,
+                                            double* __restrict__ Zp, const double* __restrict__ T,
+                                            double* __restrict__ Wt, unsigned* __restrict__ counters,
+                                            int64_t ldz, double* __restrict__ u, double* __restrict__ uref,
+                                            uint8_t* __restrict__ upd, int32_t* __restrict__ glist, const int bx,
+                                            const int by, const int nsplit) {
   const int64_t n_s = S.n_s, m = S.m, n = S.n, lda = S.lda;
   const int l = S.l_acc;
   const int64_t c0 = S.tc0;
   const int64_t ncols = n - c0;
-  const int64_t col0 = (int64_t)blockIdx.x * TA_COLS;
+  const int64_t col0 = (int64_t)bx * TA_COLS;
   if (col0 >= ncols || l == 0) return;
   const int64_t mp = m - n_s;
-  const int nsplit = gridDim.y;
   const int64_t rps = ceil_div(ceil_div(mp, nsplit), TA_ROWS) * TA_ROWS;
-  const int64_t rb = (int64_t)blockIdx.y * rps, re = min(mp, rb + rps);
+  const int64_t rb = (int64_t)by * rps, re = min(mp, rb + rps);
   const int lt = (l + 7) / 8;  // M tiles in use
   const int lp = lt * 8;
   const int odd = (int)(n_s & 1);  // slabs start one row early so global rows are even
@@ -299,7 +295,7 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* c, double* __restrict_
       cp_async_commit();
   }
   // ---- partial tile -> Zp[split] ----
-  double* out = Zp + (int64_t)blockIdx.y * DMQR_KP * ldz;
+  double* out = Zp + (int64_t)by * DMQR_KP * ldz;
   TA_DISPATCH(ta_store_t, acc, out, ldz, col0, lane, wid)
   const int64_t cc = col0 + wid * 8 + 2 * (lane & 3);
   // ---- last split CTA of this column tile: Wt = T^T * sum_s Zp[s] ----
@@ -307,13 +303,13 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* c, double* __restrict_
   __syncthreads();
   __shared__ int s_last;
   if (tid == 0) {
-    const unsigned prev = atomicAdd(&counters[blockIdx.x], 1u);
+    const unsigned prev = atomicAdd(&counters[bx], 1u);
     s_last = (prev == (unsigned)nsplit - 1);
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (tid == 0) counters[blockIdx.x] = 0u;
+  if (tid == 0) counters[bx] = 0u;
   const int lp4 = (l + 3) / 4 * 4;
   double* ts = tas;                        // ts[t][i] = T[t][i]   (KP x TW_LD)
   double* zs = tas + DMQR_KP * TW_LD;      // zs[t][c]             (KP x TW_LD)
@@ -373,6 +369,21 @@ __global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* c, double* __restrict_
   la_tile_epilogue(c, A, Wt, ldz, u, uref, upd, zs, ts, n_s, l, c0, col0, glist);
 }
 
+
+__global__ void __launch_bounds__(TA_T, 2) k_trail_a(Ctl* c, double* __restrict__ A,
+                                                     double* __restrict__ Zp, const double* __restrict__ T,
+                                                     double* __restrict__ Wt, unsigned* __restrict__ counters,
+                                                     int64_t ldz, double* __restrict__ u,
+                                                     double* __restrict__ uref, uint8_t* __restrict__ upd,
+                                                     int only_if_cq_fail, int32_t* __restrict__ glist) {
+  zshift(c, c, A, Zp, T, Wt, counters, u, uref, upd, glist);
+  pdl_enter();
+  const CtlSnap S = snap(c);
+  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 8);
+  if (S.done || (only_if_cq_fail && !S.cq_fail)) return;  // (k_trail_w did it)
+  trail_a_cta(S, c, A, Zp, T, Wt, counters, ldz, u, uref, upd, glist, (int)blockIdx.x, (int)blockIdx.y, (int)gridDim.y);
+}
+
 constexpr int TB_T = 256;     // 8 warps: 4 (rows) x 2 (cols), each 32x32
 constexpr int TB_ROWS = 128;
 constexpr int TB_COLS = 64;
@@ -409,17 +420,31 @@ __device__ __forceinline__ void trail_b_tile(double* __restrict__ A, const doubl
     cp_async_commit();
   }
   // ---- the C tile into the accumulators (HBM reads overlap the staging) ----
+  // The product is formed transposed, C^T -= Wt^T Y^T (Wt fragments as the DMMA's
+  // row operand, Y fragments as its column operand: the same products summed in
+  // the same order, so the result is bitwise the untransposed one), because the
+  // accumulator pair of a lane then holds two consecutive ROWS of one column:
+  // 16 contiguous, 16-byte-aligned bytes (tiles start on even global rows), so
+  // the tile moves with LDG.128 / STG.128 -- half the memory instructions.
+  // acc[ct][rt]: column ct*8 + (lane >> 2), rows rt*8 + 2*(lane & 3) + {0, 1}
+  // of the warp's 32 x 32 block.
   double acc[4][4][2];
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
-    const int64_t r = row0 + wm * 32 + mt * 8 + (lane >> 2);
-    const bool rv = r >= 0 && r < mp;
+  for (int ct = 0; ct < 4; ++ct) {
+    const int64_t cc = col0 + wn * 32 + ct * 8 + (lane >> 2);
+    const bool cv = cc < ncols;
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      const int64_t cc = col0 + wn * 32 + nt * 8 + 2 * (lane & 3);
+    for (int rt = 0; rt < 4; ++rt) {
+      const int64_t r = row0 + wm * 32 + rt * 8 + 2 * (lane & 3);
       const double* p = Cp + r + cc * lda;
-      acc[mt][nt][0] = (rv && cc < ncols) ? p[0] : 0.0;
-      acc[mt][nt][1] = (rv && cc + 1 < ncols) ? p[lda] : 0.0;
+      if (cv && r >= 0 && r + 1 < mp) {
+        const double2 v = *reinterpret_cast<const double2*>(p);
+        acc[ct][rt][0] = v.x;
+        acc[ct][rt][1] = v.y;
+      } else {
+        acc[ct][rt][0] = (cv && r >= 0 && r < mp) ? p[0] : 0.0;
+        acc[ct][rt][1] = (cv && r + 1 >= 0 && r + 1 < mp) ? p[1] : 0.0;
+      }
     }
   }
   cp_async_wait<0>();
@@ -437,26 +462,31 @@ __device__ __forceinline__ void trail_b_tile(double* __restrict__ A, const doubl
   __syncthreads();
   for (int ks = 0; ks < lp4; ks += 4) {
     const int t = ks + (lane & 3);
-    double af[4], bf[4];
+    double yf[4], wf[4];
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) af[mt] = -vs[t * TB_VLD + wm * 32 + mt * 8 + (lane >> 2)];
+    for (int rt = 0; rt < 4; ++rt) yf[rt] = -vs[t * TB_VLD + wm * 32 + rt * 8 + (lane >> 2)];
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) bf[nt] = zs[t * TB_ZLD + wn * 32 + nt * 8 + (lane >> 2)];
+    for (int ct = 0; ct < 4; ++ct) wf[ct] = zs[t * TB_ZLD + wn * 32 + ct * 8 + (lane >> 2)];
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
+    for (int ct = 0; ct < 4; ++ct)
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+      for (int rt = 0; rt < 4; ++rt) dmma884(acc[ct][rt][0], acc[ct][rt][1], wf[ct], yf[rt]);
   }
+  const int64_t rlo = LA ? (int64_t)l : 0;
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
-    const int64_t r = row0 + wm * 32 + mt * 8 + (lane >> 2);
-    if (r < (LA ? (int64_t)l : 0) || r >= mp) continue;
+  for (int ct = 0; ct < 4; ++ct) {
+    const int64_t cc = col0 + wn * 32 + ct * 8 + (lane >> 2);
+    if (cc >= ncols || (LA && upd && upd[c0 + cc])) continue;
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      const int64_t cc = col0 + wn * 32 + nt * 8 + 2 * (lane & 3);
+    for (int rt = 0; rt < 4; ++rt) {
+      const int64_t r = row0 + wm * 32 + rt * 8 + 2 * (lane & 3);
       double* p = Cp + r + cc * lda;
-      if (cc < ncols && !(LA && upd && upd[c0 + cc])) p[0] = acc[mt][nt][0];
-      if (cc + 1 < ncols && !(LA && upd && upd[c0 + cc + 1])) p[lda] = acc[mt][nt][1];
+      if (r >= rlo && r + 1 < mp) {
+        *reinterpret_cast<double2*>(p) = make_double2(acc[ct][rt][0], acc[ct][rt][1]);
+      } else {
+        if (r >= rlo && r < mp) p[0] = acc[ct][rt][0];
+        if (r + 1 >= rlo && r + 1 < mp) p[1] = acc[ct][rt][1];
+      }
     }
   }
 }
@@ -842,11 +872,29 @@ constexpr int TW_COLS = 32;
 constexpr int TW_CLD = TW_COLS + 4;  // 36 = 4 mod 16 (conflict-free 4 x 4 half-warp fragments)
 constexpr size_t TW_SMEM = sizeof(double) * (3 * DMQR_KP * DMQR_KP + 3 * DMQR_KP * TW_CLD);
 
+// Step close (close != nullptr): the CTA finishing the step's last tile ends
+// the step itself when nothing else is left to do -- no guard column was
+// listed -- i.e. it runs k_step_end's bookkeeping and posts the host record;
+// k_tail (tail.cuh), launched behind, then finds the record posted and exits
+// at once.  That is the common case; k_tail does the rest otherwise.
+struct StepRec;
+__device__ __forceinline__ void step_end_body(const CtlSnap& S, Ctl* c, StepRec* __restrict__ steps,
+                                              double* __restrict__ norm_trace,
+                                              unsigned long long* __restrict__ trace_bits, const double* __restrict__ A,
+                                              double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
+                                              double* __restrict__ uref, uint8_t* __restrict__ upd);
+__device__ __forceinline__ void step_post(const CtlSnap& S, Ctl* c, HostRec* __restrict__ hrec);
+struct StepClose {
+  StepRec* steps;
+  HostRec* hrec;
+  unsigned* counter;  // tiles done (reset by the closing CTA)
+};
+
 __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A,
                                                   const double* __restrict__ Gp, const double* __restrict__ FM,
                                                   double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
                                                   double* __restrict__ uref, uint8_t* __restrict__ upd,
-                                                  int32_t* __restrict__ glist) {
+                                                  int32_t* __restrict__ glist, const StepClose close) {
   pdl_enter();
   const CtlSnap S = snap(c);
   TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 7);
@@ -985,6 +1033,29 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A
     }
   }
   if (blockIdx.x == 0) la_panel_columns(c, A, Wt, ldz, u, uref, upd, n_s, l, c0);
+  // ---- the last tile's CTA closes the step when no guard column was listed ----
+  if (close.counter) {
+    __shared__ int s_close;
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      const unsigned ntiles = (unsigned)ceil_div(ncols, TW_COLS);
+      int cl = 0;
+      if (atomicAdd(close.counter, 1u) == ntiles - 1) {
+        __threadfence();
+        *close.counter = 0u;
+        cl = (ctl_ld(&c->gcount) == 0 && S.tc0 < n);
+      }
+      s_close = cl;
+    }
+    __syncthreads();
+    if (s_close && wid == 0) {
+      step_end_body(S, c, close.steps, nullptr, nullptr, A, Wt, ldz, u, uref, upd);
+      __threadfence();
+      __syncwarp();
+      if (lane == 0 && close.hrec) step_post(S, c, close.hrec);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1000,16 +1071,12 @@ constexpr int GU_LD = GU_ROWS + 4;  // 4 mod 16
 constexpr size_t GU_SMEM = sizeof(double) * (2 * DMQR_KP * GU_LD + DMQR_KP * DMQR_KP);
 constexpr int GU_GROUPS = 4;  // column groups of 72 per CTA (grid.y spreads the rest)
 
-__global__ void __launch_bounds__(GU_T) k_guard(Ctl* c, double* __restrict__ A,
-                                                const double* __restrict__ Wt, int64_t ldz,
-                                                uint8_t* __restrict__ upd, double* __restrict__ u,
-                                                double* __restrict__ uref, const int32_t* __restrict__ glist,
-                                                unsigned* __restrict__ counter) {
-  pdl_enter();
-  const CtlSnap S = snap(c);
-  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 9);
-  const int cnt = c->gcount;
-  if (S.done || cnt == 0) return;
+// (one CTA's work: 64-row block bx, column-group range by; k_tail runs the same
+// items from a persistent grid)
+__device__ __forceinline__ void guard_cta(const CtlSnap& S, double* __restrict__ A, const double* __restrict__ Wt,
+                                          int64_t ldz, const uint8_t* __restrict__ upd,
+                                          const int32_t* __restrict__ glist, const int cnt, const int bx,
+                                          const int by) {
   const int64_t m = S.m, lda = S.lda, n_s = S.n_s;
   const int l = S.l_acc;
   const int64_t base = n_s + l;
@@ -1024,7 +1091,7 @@ __global__ void __launch_bounds__(GU_T) k_guard(Ctl* c, double* __restrict__ A,
   double* cs = gus + DMQR_KP * GU_LD;      // cs[q][rr] = C[r0 + rr][col_q]
   double* ws = gus + 2 * DMQR_KP * GU_LD;  // ws[t][q]  = Wt[t][col_q]
   __shared__ int s_col[DMQR_KP];
-  const int64_t r0 = base + (int64_t)blockIdx.x * GU_ROWS;
+  const int64_t r0 = base + (int64_t)bx * GU_ROWS;
   const int lp4 = (l + 3) / 4 * 4;
   if (r0 < m) {
     const int nr = (int)min((int64_t)GU_ROWS, m - r0);
@@ -1033,7 +1100,7 @@ __global__ void __launch_bounds__(GU_T) k_guard(Ctl* c, double* __restrict__ A,
       ys[t * GU_LD + rr] = (t < l && rr < nr) ? A[(n_s + t) * lda + r0 + rr] : 0.0;
     }
     // blockIdx.y: a range of GU_GROUPS column groups of the list
-    const int gbeg = blockIdx.y * GU_GROUPS * DMQR_KP, gend = min(nlist, gbeg + GU_GROUPS * DMQR_KP);
+    const int gbeg = by * GU_GROUPS * DMQR_KP, gend = min(nlist, gbeg + GU_GROUPS * DMQR_KP);
     for (int g0 = gbeg; g0 < gend; g0 += DMQR_KP) {
       const int ng = min(DMQR_KP, gend - g0);
       if (tid < DMQR_KP) {
@@ -1081,6 +1148,27 @@ __global__ void __launch_bounds__(GU_T) k_guard(Ctl* c, double* __restrict__ A,
       __syncthreads();
     }
   }
+}
+
+// After every guard item: the step's flags (one thread).
+__device__ __forceinline__ void guard_flags(const CtlSnap& S, Ctl* c, const int cnt) {
+  const bool full = (int64_t)cnt * 8 > S.n - (S.n_s + S.l_acc);
+  if (full) c->pend_done = 1;           // k_step_end: nothing is pending after this step
+  if (full || cnt > 32) c->la_bad = 1;  // guards are not rare here: the host goes serial
+}
+
+__global__ void __launch_bounds__(GU_T) k_guard(Ctl* c, double* __restrict__ A,
+                                                const double* __restrict__ Wt, int64_t ldz,
+                                                uint8_t* __restrict__ upd, double* __restrict__ u,
+                                                double* __restrict__ uref, const int32_t* __restrict__ glist,
+                                                unsigned* __restrict__ counter) {
+  pdl_enter();
+  const CtlSnap S = snap(c);
+  TLSpan tl_span(S.done ? nullptr : S.tl, S.step_idx, 9);
+  const int cnt = c->gcount;
+  if (S.done || cnt == 0) return;
+  guard_cta(S, A, Wt, ldz, upd, glist, cnt, (int)blockIdx.x, (int)blockIdx.y);
+  const int tid = threadIdx.x;
   __shared__ int s_last;
   __syncthreads();
   if (tid == 0) {
@@ -1092,8 +1180,7 @@ __global__ void __launch_bounds__(GU_T) k_guard(Ctl* c, double* __restrict__ A,
   __threadfence();
   if (tid == 0) {
     *counter = 0u;
-    if (full) c->pend_done = 1;      // k_step_end: nothing is pending after this step
-    if (full || cnt > 32) c->la_bad = 1;  // guards are not rare here: the host goes serial
+    guard_flags(S, c, cnt);
   }
   // (the guard columns' exact norms: k_guard_norms, grid-wide, right behind)
 }
@@ -1101,18 +1188,15 @@ __global__ void __launch_bounds__(GU_T) k_guard(Ctl* c, double* __restrict__ A,
 // Exact norms of k_guard's columns (k_downdate's arithmetic), a warp per
 // column over the whole grid; then the columns' look-ahead flags (set while an
 // update is still pending; all cleared when k_guard finished the whole update).
-__global__ void __launch_bounds__(256) k_guard_norms(Ctl* c, const double* __restrict__ A,
-                                                      uint8_t* __restrict__ upd, double* __restrict__ u,
-                                                      double* __restrict__ uref, const int32_t* __restrict__ glist) {
-  pdl_enter();
-  const CtlSnap S = snap(c);
-  const int cnt = c->gcount;
-  if (S.done || cnt == 0) return;
+// (the warps w0, w0 + nw, ... of a grid; threads t0, t0 + nt, ... for the flag sweep)
+__device__ __forceinline__ void guard_norms_part(const CtlSnap& S, const double* __restrict__ A,
+                                                 uint8_t* __restrict__ upd, double* __restrict__ u,
+                                                 double* __restrict__ uref, const int32_t* __restrict__ glist,
+                                                 const int cnt, const int64_t w0, const int64_t nw, const int64_t t0,
+                                                 const int64_t nt) {
   const int64_t m = S.m, lda = S.lda, base = S.n_s + S.l_acc;
   const bool full = (int64_t)cnt * 8 > S.n - base;
   const int lane = threadIdx.x & 31;
-  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t q = w0; q < cnt; q += nw) {
     const int64_t j = glist[q];
     const double nu = warp_col_norm(A + j * lda + base, m - base, lane);
@@ -1123,8 +1207,19 @@ __global__ void __launch_bounds__(256) k_guard_norms(Ctl* c, const double* __res
     }
   }
   if (full)
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.n; j += (int64_t)gridDim.x * blockDim.x)
-      upd[j] = 0;
+    for (int64_t j = t0; j < S.n; j += nt) upd[j] = 0;
+}
+
+__global__ void __launch_bounds__(256) k_guard_norms(Ctl* c, const double* __restrict__ A,
+                                                      uint8_t* __restrict__ upd, double* __restrict__ u,
+                                                      double* __restrict__ uref, const int32_t* __restrict__ glist) {
+  pdl_enter();
+  const CtlSnap S = snap(c);
+  const int cnt = c->gcount;
+  if (S.done || cnt == 0) return;
+  guard_norms_part(S, A, upd, u, uref, glist, cnt, (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5,
+                   (int64_t(gridDim.x) * blockDim.x) >> 5, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                   (int64_t)gridDim.x * blockDim.x);
 }
 
 }  // namespace dmqr

@@ -628,7 +628,32 @@ def test_power_of_two_scaled_matrix_vs_oracle(e2):
     assert ok, worst
 
 
-@pytest.mark.parametrize("switch", ["DMQR_NO_CHOLQR", "DMQR_NO_LOOKAHEAD", "DMQR_NO_GRAPH", "DMQR_NO_STEP_GRAPH"])
+@pytest.mark.parametrize("grade", [0, -3, -8, -13])
+def test_fused_step_tail_is_bitwise_the_separate_kernels(monkeypatch, grade):
+    """The look-ahead step's tail in one launch (k_trail_w's closing CTA + k_tail, csrc/tail.cuh) runs the
+    separate kernels' device functions (k_trail_a fallback, k_guard, k_guard_norms, k_step_end): the
+    factor, pivots, step log and counters must be identical bit for bit.  Graded columns bring in guard
+    columns and declined CholeskyQR2 panels (the slow phases of k_tail)."""
+    from paper_2106_03138_b200 import qrdm2
+
+    rng = np.random.default_rng(91 - grade)
+    A = rng.standard_normal((1300, 1100)) * np.logspace(0, grade, 1100)[rng.permutation(1100)]
+    if grade == -13:  # a rank-deficient tail: panels decline, steps break and fall back
+        A[:, 700:] = A[:, :400] @ rng.standard_normal((400, 400)) * 1e-9 + A[:, 700:] * 1e-14
+    fused = qrdm2(A)
+    monkeypatch.setenv("DMQR_NO_FUSED_TAIL", "1")
+    sep = qrdm2(A)
+    assert np.array_equal(fused.packed, sep.packed)
+    assert np.array_equal(fused.coeffs, sep.coeffs)
+    assert np.array_equal(fused.perm.forward, sep.perm.forward) and fused.rank == sep.rank
+    assert _steps(fused.step_log) == _steps(sep.step_log)
+    assert fused.counters == sep.counters
+    resid, orth = parity.residuals(A, fused)
+    assert resid <= 50 * 1300 * O.EPS and orth <= 50 * 1300 * O.EPS
+
+
+@pytest.mark.parametrize("switch", ["DMQR_NO_CHOLQR", "DMQR_NO_LOOKAHEAD", "DMQR_NO_GRAPH", "DMQR_NO_STEP_GRAPH",
+                                    "DMQR_NO_FUSED_TAIL"])
 def test_schedule_switches_keep_parity(monkeypatch, switch):
     """Every schedule switch the engine reads (Householder-only panel, serial
     schedule, no replayed step graphs) gives the default run's decisions and a
