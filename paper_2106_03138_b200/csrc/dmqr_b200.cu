@@ -846,9 +846,11 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
         cfg.attrs = at;
         cfg.numAttrs = 1;
         NOTE_LAUNCH();
+        // (fused tail: the Y = Q1 M tiles run in k_trail_w's extra CTAs instead of here)
         CK(cudaLaunchKernelEx(&cfg, pmode_on ? k_spare<true> : k_spare<false>, ctl, A, (const double*)Z, ldz, upd, (const double*)q1g, Zp,
                               lacount + 4, Pcq, nsplit_g, tcount, tline,
-                              (const double*)(red + 37 * DMQR_KP * DMQR_KP), (const double*)(ws + L.pg)));
+                              fused_tail ? (const double*)nullptr : (const double*)(red + 37 * DMQR_KP * DMQR_KP),
+                              (const double*)(ws + L.pg)));
       }
     }
     if (cl_path) {
@@ -875,16 +877,26 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     PROF(2);
     const int64_t ncols_ub = std::max<int64_t>(np - 1, 0);
     int tail_nsplit = 1;
+    if (spare && fused_tail) {
+      // Wt tiles (their last CTA closes the step when no guard column came up: k_tail then exits at
+      // once) and, on the CTAs past them, the Y = Q1 M tiles; launched even without trailing columns
+      const int wgrid = (int)ceil_div(ncols_ub, TW_COLS);
+      const int ygrid = (int)ceil_div(std::max<int64_t>(mp - 1, 0), YG_ROWS);
+      CK(pdl_launch(k_trail_w, dim3((unsigned)std::max(1, wgrid + ygrid)), dim3(TA_T), TW_SMEM, st, ctl, A,
+                    (const double*)Zp, (const double*)(red + 19 * DMQR_KP * DMQR_KP), Z, ldz, u, uref, upd, glist,
+                    StepClose{srec, hrecs, lacount + 12, (const double*)q1g,
+                              (const double*)(red + 37 * DMQR_KP * DMQR_KP), wgrid}));
+      NOTE_LAUNCH();
+    }
     if (ncols_ub > 0) {
       const int64_t ntile = ceil_div(ncols_ub, TA_COLS);
       const int nsplit = choose_nsplit(ntile, 2 * d.sms,
                                        (int)std::min<int64_t>(nsplit_cap(n), std::max<int64_t>(1, ceil_div(mp, 256))));
       tail_nsplit = nsplit;
-      if (spare) {
-        // (its last CTA closes the step when no guard column came up: k_tail then exits at once)
+      if (spare && !fused_tail) {
         CK(pdl_launch(k_trail_w, dim3((unsigned)ceil_div(ncols_ub, TW_COLS)), dim3(TA_T), TW_SMEM, st, ctl, A,
                       (const double*)Zp, (const double*)(red + 19 * DMQR_KP * DMQR_KP), Z, ldz, u, uref, upd,
-                      glist, fused_tail ? StepClose{srec, hrecs, lacount + 12} : StepClose{nullptr, nullptr, nullptr}));
+                      glist, StepClose{nullptr, nullptr, nullptr, nullptr, nullptr, 0}));
         NOTE_LAUNCH();
       }
       if (!(spare && fused_tail)) {

@@ -760,7 +760,7 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* c, double* __restrict__ 
         // latency-bound and would otherwise trail the G tiles)
         if (tid == 0) {
           int it = -1;
-          if (ld_acquire(&c->m_pub) == (unsigned)S.step_idx + 1u && ld_acquire(&ctr[4]) < (unsigned)nyg) {
+          if (gM && ld_acquire(&c->m_pub) == (unsigned)S.step_idx + 1u && ld_acquire(&ctr[4]) < (unsigned)nyg) {
             const int y = (int)atomicAdd(&ctr[4], 1u);
             if (y < nyg) it = -2 - y;
           }
@@ -825,7 +825,8 @@ __global__ void __launch_bounds__(TB_T, 2) k_spare(Ctl* c, double* __restrict__ 
   // ---- phase 3: Y = Q1 M below the top block once the panel has completed
   // (griddepcontrol.wait: the panel grid finished and its writes are visible),
   // here on the spare SMs instead of a kernel behind this one ----
-  if (!S.done) {
+  // (gM == nullptr: k_trail_w's extra CTAs do these tiles, off the step's critical path)
+  if (!S.done && gM) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     if (!c->cq_fail) {
@@ -888,6 +889,12 @@ struct StepClose {
   StepRec* steps;
   HostRec* hrec;
   unsigned* counter;  // tiles done (reset by the closing CTA)
+  // the Y = Q1 M tiles below the panel's top block (ygemm_tile) run here, on the CTAs past the first
+  // `wgrid` (the Wt tiles' share of the grid), beside the Wt tiles: nothing before the next step's
+  // k_gram reads those rows, so they need not sit between the panel and this kernel
+  const double* q1g;
+  const double* gM;
+  int wgrid;
 };
 
 __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A,
@@ -903,6 +910,12 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A
   const int l = S.l_acc;
   const int64_t c0 = n_s + l, ncols = n - c0, n_s1 = c0;
   const int64_t col0 = (int64_t)blockIdx.x * TW_COLS;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (close.counter && (int)blockIdx.x >= close.wgrid) {  // a Y = Q1 M tile
+    const int64_t yb = (int)blockIdx.x - close.wgrid;
+    if (l == 0 || l + yb * YG_ROWS >= m - n_s) return;
+    ygemm_tile(A, close.q1g, close.gM, n_s, m, lda, l, yb);
+  } else {
   if (col0 >= ncols || l == 0) return;  // (no trailing columns: k_step_end does the bookkeeping)
   extern __shared__ __align__(16) double tws[];
   double* a1 = tws;                          // FT[t][i]  (A1 = FT^T)
@@ -911,7 +924,6 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A
   double* gs = y1 + DMQR_KP * DMQR_KP;       // G[t][c], then R12[i][c]
   double* cts = gs + DMQR_KP * TW_CLD;       // C_top[t][c]
   double* ws = cts + DMQR_KP * TW_CLD;       // Wt[t][c]
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int lp4 = (l + 3) / 4 * 4, lt = (l + 7) / 8;
   const int cb = wid & 3, q0 = (wid >> 2) * 5, q1 = min(q0 + 5, lt);
   const double* gFT = FM;
@@ -1033,13 +1045,15 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A
     }
   }
   if (blockIdx.x == 0) la_panel_columns(c, A, Wt, ldz, u, uref, upd, n_s, l, c0);
+  }
   // ---- the last tile's CTA closes the step when no guard column was listed ----
   if (close.counter) {
     __shared__ int s_close;
     __syncthreads();
     if (tid == 0) {
       __threadfence();
-      const unsigned ntiles = (unsigned)ceil_div(ncols, TW_COLS);
+      const unsigned ntiles = (unsigned)((ncols > 0 ? ceil_div(ncols, TW_COLS) : 0) +
+                                         (m - n_s > l ? ceil_div(m - n_s - l, YG_ROWS) : 0));
       int cl = 0;
       if (atomicAdd(close.counter, 1u) == ntiles - 1) {
         __threadfence();
