@@ -897,6 +897,9 @@ struct StepClose {
   int wgrid;
 };
 
+// (debug timeline: the first Wt tile's phase stamps, slots 22.. of the step's row)
+#define TW_STAMP(k) \
+  if (S.tl && blockIdx.x == 0 && tid == 0) S.tl[(S.step_idx & 63) * 32 + (k)] = (unsigned long long)gtimer()
 __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A,
                                                   const double* __restrict__ Gp, const double* __restrict__ FM,
                                                   double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
@@ -920,7 +923,7 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A
   extern __shared__ __align__(16) double tws[];
   double* a1 = tws;                          // FT[t][i]  (A1 = FT^T)
   double* a2 = a1 + DMQR_KP * DMQR_KP;       // MT[t][i]  (A2 = MT^T)
-  double* y1 = a2 + DMQR_KP * DMQR_KP;       // Y1[i][t] (unit lower)
+  double* y1 = a2 + DMQR_KP * DMQR_KP;       // Y1[i][t] (unit lower) at y1[t * KP + i]
   double* gs = y1 + DMQR_KP * DMQR_KP;       // G[t][c], then R12[i][c]
   double* cts = gs + DMQR_KP * TW_CLD;       // C_top[t][c]
   double* ws = cts + DMQR_KP * TW_CLD;       // Wt[t][c]
@@ -941,24 +944,25 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A
       cts[t * TW_CLD + c2] = 0.0;
     }
   }
+  // FT and MT are published whole (zero outside their l x l upper triangles): 16-byte copies
+  for (int e = tid; e < DMQR_KP * DMQR_KP / 2; e += TA_T) {
+    cp_async16(a1 + 2 * e, gFT + 2 * e, 16);
+    cp_async16(a2 + 2 * e, gMT + 2 * e, 16);
+  }
   for (int e = tid; e < DMQR_KP * DMQR_KP; e += TA_T) {
     const int t = e / DMQR_KP, i = e % DMQR_KP;
-    if (t < l && i < l) {
-      cp_async8(a1 + t * DMQR_KP + i, gFT + t * DMQR_KP + i);
-      cp_async8(a2 + t * DMQR_KP + i, gMT + t * DMQR_KP + i);
-    } else {
-      a1[t * DMQR_KP + i] = 0.0;
-      a2[t * DMQR_KP + i] = 0.0;
-    }
-    // Y1[i][t] from the packed panel (column n_s + t, row n_s + i): coalesced over i
+    // Y1[i][t] from the packed panel (column n_s + t, row n_s + i), stored as y1[t][i]: global reads
+    // and shared writes both run along i (a transposed y1[i][t] made every copy a 16-way bank conflict)
     if (t < i && i < l)
-      cp_async8(y1 + i * DMQR_KP + t, A + (n_s + t) * lda + n_s + i);
+      cp_async8(y1 + t * DMQR_KP + i, A + (n_s + t) * lda + n_s + i);
     else
-      y1[i * DMQR_KP + t] = (t == i && i < l) ? 1.0 : 0.0;
+      y1[t * DMQR_KP + i] = (t == i && i < l) ? 1.0 : 0.0;
   }
   cp_async_commit();
+  TW_STAMP(22);
   cp_async_wait<0>();
   __syncthreads();
+  TW_STAMP(23);
   const int lr = lane >> 2, lk = lane & 3;
   const int64_t cc = col0 + cb * 8 + 2 * lk;
   // ---- Wt = A1 C_top + A2 G ----
@@ -1001,7 +1005,7 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A
     const double b = ws[t * TW_CLD + cb * 8 + lr];
 #pragma unroll
     for (int q = 0; q < 5; ++q)
-      if (q0 + q < q1) dmma884(r[q][0], r[q][1], -y1[((q0 + q) * 8 + lr) * DMQR_KP + t], b);
+      if (q0 + q < q1) dmma884(r[q][0], r[q][1], -y1[t * DMQR_KP + (q0 + q) * 8 + lr], b);
   }
   __syncthreads();  // all reads of gs (G) are done
 #pragma unroll
@@ -1016,6 +1020,7 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A
       }
     }
   __syncthreads();
+  TW_STAMP(24);
   // ---- downdate: warp w, columns 4w .. 4w+3 (k_downdate's per-column order) ----
   double d[4];
 #pragma unroll
@@ -1045,6 +1050,7 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A
     }
   }
   if (blockIdx.x == 0) la_panel_columns(c, A, Wt, ldz, u, uref, upd, n_s, l, c0);
+  TW_STAMP(25);
   }
   // ---- the last tile's CTA closes the step when no guard column was listed ----
   if (close.counter) {
@@ -1063,6 +1069,7 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A
       s_close = cl;
     }
     __syncthreads();
+    if (s_close && tid == 0 && S.tl) S.tl[(S.step_idx & 63) * 32 + 26] = (unsigned long long)gtimer();
     if (s_close && wid == 0) {
       step_end_body(S, c, close.steps, nullptr, nullptr, A, Wt, ldz, u, uref, upd);
       __threadfence();

@@ -28,13 +28,18 @@ __device__ __forceinline__ void ygemm_tile(double* __restrict__ A, const double*
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nr = (int)min((int64_t)YG_ROWS, mp - r0);
   const int lp4 = (l + 3) / 4 * 4;
-#pragma unroll 6
-  for (int e = tid; e < DMQR_KP * DMQR_KP; e += blockDim.x) ms[e] = __ldcg(gM + e);
-#pragma unroll 6
+  // both operands by cp.async: every load of the tile is in flight at once (one L2 round trip; the
+  // load -> store pairs of a plain copy loop serialise into one round trip per iteration)
+  for (int e = tid; e < DMQR_KP * DMQR_KP / 2; e += blockDim.x) cp_async16(ms + 2 * e, gM + 2 * e, 16);
   for (int e = tid; e < lp4 * YG_ROWS; e += blockDim.x) {
     const int k = e / YG_ROWS, rr = e % YG_ROWS;
-    qs[k * YG_LD + rr] = (k < l && rr < nr) ? __ldcg(q1g + (int64_t)k * ldq + qodd + r0 + rr) : 0.0;
+    if (k < l && rr < nr)
+      cp_async8(qs + k * YG_LD + rr, q1g + (int64_t)k * ldq + qodd + r0 + rr);
+    else
+      qs[k * YG_LD + rr] = 0.0;
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   const int nt_n = (l + 7) / 8;
   const int r = wid * 8 + (lane >> 2);

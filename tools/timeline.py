@@ -65,3 +65,11 @@ if mid:
             a = np.mean([x[0] for x in v]); b = np.mean([x[1] for x in v])
             print(f"  {nm:9s} {a:7.1f} {b:7.1f} {b - a:7.1f}  (n={len(v)})")
     print("  step      ", np.mean([r[2] for r in mid if r[2]]))
+
+# k_trail_w's first Wt tile (slots 22..26): staged-issue, landed, R12 done, tile done, close start; relative to the kernel's span start
+print("\nk_trail_w CTA 0 (us after the span start): copies issued, landed, R12 stored, tile done, close start, span end")
+for s in (8, 20, 32, 33, 48):
+    r = tl[s]
+    if r[14] in (0, U64MAX):
+        continue
+    print(s, [round(float(r[k] - r[14]) / 1e3, 1) if r[k] else None for k in (22, 23, 24, 25, 26, 15)])
