@@ -704,11 +704,17 @@ __global__ void __launch_bounds__(PANEL_T, 1) k_panel_cq(PanelArgs a) {
   const int trow = tid & (CQ_RMAX - 1), tcol0 = tid / CQ_RMAX, tcstep = PANEL_T / CQ_RMAX;
   auto load_chunk = [&](const double* src, int64_t ld, int ch, int ncol) {  // rows of chunk ch -> sl
     const int c0r = ch * CQ_RMAX, cR = min(CQ_RMAX, R - c0r), cR4 = (cR + 3) & ~3;
+    // (cp.async: the whole chunk in flight at once -- a plain copy loop waits a round trip per unrolled group)
     if (trow < cR4) {
       const double* sp = src + c0r + trow;
-#pragma unroll 4
-      for (int cc = tcol0; cc < ncol; cc += tcstep) sl[cc * CQ_LDS + trow] = (trow < cR) ? sp[(int64_t)cc * ld] : 0.0;
+      if (trow < cR) {
+        for (int cc = tcol0; cc < ncol; cc += tcstep) cp_async8(sl + cc * CQ_LDS + trow, sp + (int64_t)cc * ld);
+      } else {
+        for (int cc = tcol0; cc < ncol; cc += tcstep) sl[cc * CQ_LDS + trow] = 0.0;
+      }
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     return cR4;
   };
