@@ -256,13 +256,22 @@ __device__ void cq_trinv_upper(const double* U, double* X, int n, int xr = DMQR_
     for (int bi = wid; bi < nb - d; bi += nw) {
       const int bj = bi + d;
       const int ar = bi * 8 + lr, bc = bj * 8 + lr;
-      double c0 = 0.0, c1 = 0.0;
-      for (int t0 = (bi + 1) * 8; t0 < (bj + 1) * 8; t0 += 4) {
-        const int t = t0 + lk;
-        const double av = (ar < n && t < n) ? U[ar * DMQR_KP + t] : 0.0;
-        const double bv = (t < n && bc < n) ? X[t * xr + bc * xc] : 0.0;
-        dmma884(c0, c1, av, bv);
+      // (four partial sums over alternating k-steps: the dependent DMMA chain of a far diagonal --
+      // up to 16 k-steps -- is a quarter as long)
+      double cp[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      for (int t0 = (bi + 1) * 8; t0 < (bj + 1) * 8; t0 += 16) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int t = t0 + 4 * h + lk;
+          if (t0 + 4 * h < (bj + 1) * 8) {
+            const double av = (ar < n && t < n) ? U[ar * DMQR_KP + t] : 0.0;
+            const double bv = (t < n && bc < n) ? X[t * xr + bc * xc] : 0.0;
+            dmma884(cp[h][0], cp[h][1], av, bv);
+          }
+        }
       }
+      const double c0 = (cp[0][0] + cp[1][0]) + (cp[2][0] + cp[3][0]);
+      const double c1 = (cp[0][1] + cp[1][1]) + (cp[2][1] + cp[3][1]);
       w[lr * 8 + 2 * lk] = c0;
       w[lr * 8 + 2 * lk + 1] = c1;
       __syncwarp();
@@ -535,6 +544,8 @@ template <bool AFULL = false, class LA, class LB>
 __device__ void cq_small_gemm(LA la, LB lb, double* C, int n) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int nt = (n + 7) / 8;
+  // (running a warp's tiles together -- interleaved chains -- measured slower: the loop is bound by
+  // the loaders' address arithmetic, not by the DMMA chain)
   for (int t = wid; t < nt * nt; t += nw) {
     const int ti = t / nt, tj = t % nt;
     double c0 = 0.0, c1 = 0.0;
