@@ -268,14 +268,14 @@ def trailing_flops(m, n, steps) -> float:
 def spare_flops(m, n, steps) -> list:
     """Algorithmic flops of k_spare per step (look-ahead schedule):
     phase 1 = the previous step's C -= Y Wt below its R rows (2 (m - n_s) l_prev
-    n''_prev), phase 2 = G = Q1^T C (2 (m - n_s) k_s n''_s), phase 3 = Y = Q1 M
-    (2 (m - n_s) k_s l_s)."""
+    n''_prev), phase 2 = G = Q1^T C (2 (m - n_s) k_s n''_s).  (Y = Q1 M runs in
+    k_trail_w's extra CTAs.)"""
     out = []
     prev = None
     for s in steps:
         mp = m - s.n_s
         nn = max(n - s.n_s - s.k_selected, 0)
-        f = 2.0 * mp * s.k_selected * nn + 2.0 * mp * s.k_selected * s.k_accepted
+        f = 2.0 * mp * s.k_selected * nn
         if prev is not None:
             f += 2.0 * mp * prev.k_accepted * max(n - prev.n_s - prev.k_selected, 0)
         out.append(f)
@@ -296,7 +296,7 @@ def panel_bytes(m, n, steps) -> float:
 
 
 TL_NAMES = {0: "select", 1: "gram", 2: "gram_finish", 3: "swap", 4: "panel_cq", 5: "spare", 6: "ygemm",
-            7: "trail_w", 8: "trail_a", 9: "guard", 10: "step_end", 11: "trail_b", 12: "downdate", 13: "panel_rr"}
+            7: "trail_w", 8: "trail_a", 9: "guard", 10: "step_tail", 11: "trail_b", 12: "downdate", 13: "panel_rr"}
 
 
 def timeline_spans(f, m, n) -> tuple:
@@ -310,10 +310,21 @@ def timeline_spans(f, m, n) -> tuple:
     _lib.load().dmqr_debug_timeline(f.workspace.data_ptr(), m, n, tl.ctypes.data_as(C.c_void_p))
     t = tl[:2048].reshape(64, 16, 2).astype(np.float64)
     ok = (t[:, :, 0] > 0) & (t[:, :, 0] < 2 ** 62) & (t[:, :, 1] > 0)
-    ok[:, 14:] = False  # (slots 28-31: k_spare phase stamps, not spans)
+    ok[:, 11:] = False  # (slots 22-27: k_trail_w's phase stamps; 28-31: k_spare's -- not spans)
     per, span = [], []
     for s in range(min(64, int(f.info.n_steps))):
-        d = {TL_NAMES.get(k, str(k)): (t[s, k, 1] - t[s, k, 0]) / 1e3 for k in range(14) if ok[s, k]}
+        d = {TL_NAMES.get(k, str(k)): (t[s, k, 1] - t[s, k, 0]) / 1e3 for k in range(11) if ok[s, k]}
+        # k_spare's busy time: phase 1 (start .. last tile done) + phase 2 (Q1 seen, after phase 1 ..
+        # last G tile done); the rest of its span waits for the panel
+        if ok[s, 5]:
+            st0, q1_seen, p1_end, p2_end = t[s, 5, 0], t[s, 14, 0], t[s, 14, 1], t[s, 15, 1]
+            busy = 0.0
+            if p1_end > st0:
+                busy += p1_end - st0
+            if p2_end > 0 and 0 < q1_seen < 2 ** 62:
+                busy += max(0.0, p2_end - max(q1_seen, p1_end, st0))
+            if busy > 0:
+                d["spare_busy"] = busy / 1e3
         per.append(d)
         if ok[s].any():
             span.append((t[s, ok[s], 1].max() - t[s, ok[s], 0].min()) / 1e3)
@@ -589,6 +600,8 @@ def run_b200(args, rank, world):
     sp_us = [d.get("spare") for d in per_kernel]
     pairs = [(fl, us) for fl, us in zip(fsp, sp_us) if us]
     achieved = (sum(fl for fl, _ in pairs) / (sum(us for _, us in pairs) / 1e6) / 1e12) if pairs else None
+    bpairs = [(fl, d.get("spare_busy")) for fl, d in zip(fsp, per_kernel) if d.get("spare_busy")]
+    achieved_busy = (sum(fl for fl, _ in bpairs) / (sum(us for _, us in bpairs) / 1e6) / 1e12) if bpairs else None
     step_sum = {}
     for d in per_kernel:
         for k, v in d.items():
@@ -605,15 +618,24 @@ def run_b200(args, rank, world):
 
         from oracle import qrdm_oracle as O  # the checker / baseline only
 
+        dmqr_ref = _reference_module()  # the unmodified reference when baseline/_ref travelled, else the port
         t0 = time.perf_counter()
-        ref = O.qrdm2(A)
+        if dmqr_ref is not None:
+            ref = dmqr_ref.qrdm2(A)
+            ref_fwd, ref_rank = np.asarray(ref.perm.forward), int(ref.rank)
+        else:
+            ref = O.qrdm2(A)
+            ref_fwd, ref_rank = ref.forward, ref.rank
         t_cpu = time.perf_counter() - t0
         threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
-        same = bool(np.array_equal(ref.forward, last.perm.forward)) and ref.rank == last.rank
-        cpu = {"value": nominal(n, n) / t_cpu / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"one full qrdm2 of the same cfg2 {n}x{n} matrix ({t_cpu:.1f} s) with the numpy "
-                         f"oracle port (oracle/qrdm_oracle.py), {threads} BLAS threads of "
-                         f"{len(os.sched_getaffinity(0))} host cores; GPU perm/rank identical: {same}"}
+        same = bool(np.array_equal(ref_fwd, last.perm.forward)) and ref_rank == last.rank
+        who = ("the unmodified reference dmqr.qrdm2 (baseline/_ref)" if dmqr_ref is not None
+               else "the numpy oracle port (oracle/qrdm_oracle.py)")
+        cpu = {"value": nominal(n, n) / t_cpu / 1e9, "unit": UNIT, "cores": threads,
+               "kind": "reference" if dmqr_ref is not None else "port",
+               "sample": f"one full qrdm2 of the same cfg2 {n}x{n} matrix ({t_cpu:.1f} s) with {who}, "
+                         f"{threads} BLAS threads of {len(os.sched_getaffinity(0))} host cores; "
+                         f"GPU perm/rank identical: {same}"}
     extra = None
     if world == 1 and not args.no_extra:
         extra = other_configs(torch, dev, peak_tf)
@@ -643,9 +665,14 @@ def run_b200(args, rank, world):
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": (achieved / peak_tf) if achieved else None,
                      "traffic": load_profile_number("r02_spare_traffic.json", "traffic_bytes_per_launch"),
-                     "kernel": "k_spare (persistent, beside the panel: previous step's C -= Y Wt + G = Q1^T C + "
-                               "Y = Q1 M; DMMA m8n8k4 f64), spans from the timed run's device timeline "
-                               "(last timed factorization)",
+                     "kernel": "k_spare (persistent, beside the panel: previous step's C -= Y Wt, then G = Q1^T C "
+                               "once the panel has published Q1; DMMA m8n8k4 f64), spans from the timed run's "
+                               "device timeline (last timed factorization)",
+                     "achieved_busy": achieved_busy,
+                     "frac_busy": (achieved_busy / peak_tf) if achieved_busy else None,
+                     "busy_note": "achieved/frac are over k_spare's whole spans, which include its wait for the "
+                                  "panel's Q1; *_busy count only the time between its first tile and the last "
+                                  "tile of each phase (phase stamps of the same timeline)",
                      "algorithmic_flops_per_factorization": sum(fsp),
                      "spare_us_per_factorization": sum(us for _, us in pairs),
                      "peak_source": "cuBLAS DGEMM 8192^3 best-of-5 measured in this run (FP64 peak; "

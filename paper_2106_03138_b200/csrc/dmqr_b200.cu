@@ -885,7 +885,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
       CK(pdl_launch(k_trail_w, dim3((unsigned)std::max(1, wgrid + ygrid)), dim3(TA_T), TW_SMEM, st, ctl, A,
                     (const double*)Zp, (const double*)(red + 19 * DMQR_KP * DMQR_KP), Z, ldz, u, uref, upd, glist,
                     StepClose{srec, hrecs, lacount + 12, (const double*)q1g,
-                              (const double*)(red + 37 * DMQR_KP * DMQR_KP), wgrid}));
+                              (const double*)(red + 37 * DMQR_KP * DMQR_KP), ygrid}));
       NOTE_LAUNCH();
     }
     if (ncols_ub > 0) {

@@ -889,17 +889,19 @@ struct StepClose {
   StepRec* steps;
   HostRec* hrec;
   unsigned* counter;  // tiles done (reset by the closing CTA)
-  // the Y = Q1 M tiles below the panel's top block (ygemm_tile) run here, on the CTAs past the first
-  // `wgrid` (the Wt tiles' share of the grid), beside the Wt tiles: nothing before the next step's
-  // k_gram reads those rows, so they need not sit between the panel and this kernel
+  // the Y = Q1 M tiles below the panel's top block (ygemm_tile) run here, on the FIRST `ygrid` CTAs,
+  // beside the Wt tiles: nothing before the next step's k_gram reads those rows, so they need not sit
+  // between the panel and this kernel.  (They are short and come first in block order: when the grid
+  // exceeds one wave, the Wt tiles left over start a few us later instead of the Y tiles a whole Wt
+  // tile later.)
   const double* q1g;
   const double* gM;
-  int wgrid;
+  int ygrid;
 };
 
 // (debug timeline: the first Wt tile's phase stamps, slots 22.. of the step's row)
 #define TW_STAMP(k) \
-  if (S.tl && blockIdx.x == 0 && tid == 0) S.tl[(S.step_idx & 63) * 32 + (k)] = (unsigned long long)gtimer()
+  if (S.tl && wbx == 0 && tid == 0) S.tl[(S.step_idx & 63) * 32 + (k)] = (unsigned long long)gtimer()
 __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A,
                                                   const double* __restrict__ Gp, const double* __restrict__ FM,
                                                   double* __restrict__ Wt, int64_t ldz, double* __restrict__ u,
@@ -912,10 +914,11 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A
   const int64_t n_s = S.n_s, m = S.m, n = S.n, lda = S.lda;
   const int l = S.l_acc;
   const int64_t c0 = n_s + l, ncols = n - c0, n_s1 = c0;
-  const int64_t col0 = (int64_t)blockIdx.x * TW_COLS;
+  const int wbx = (int)blockIdx.x - (close.counter ? close.ygrid : 0);  // index among the Wt tiles
+  const int64_t col0 = (int64_t)wbx * TW_COLS;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (close.counter && (int)blockIdx.x >= close.wgrid) {  // a Y = Q1 M tile
-    const int64_t yb = (int)blockIdx.x - close.wgrid;
+  if (wbx < 0) {  // a Y = Q1 M tile
+    const int64_t yb = (int)blockIdx.x;
     if (l == 0 || l + yb * YG_ROWS >= m - n_s) return;
     ygemm_tile(A, close.q1g, close.gM, n_s, m, lda, l, yb);
   } else {
@@ -1049,7 +1052,7 @@ __global__ void __launch_bounds__(TA_T) k_trail_w(Ctl* c, double* __restrict__ A
         u[j] = sqrt(fmax(sq, 0.0));
     }
   }
-  if (blockIdx.x == 0) la_panel_columns(c, A, Wt, ldz, u, uref, upd, n_s, l, c0);
+  if (wbx == 0) la_panel_columns(c, A, Wt, ldz, u, uref, upd, n_s, l, c0);
   TW_STAMP(25);
   }
   // ---- the last tile's CTA closes the step when no guard column was listed ----

@@ -753,3 +753,20 @@ def test_wide_kdm_batched_per_matrix():
         r = f.result(b)
         assert np.array_equal(r.perm.forward, one.perm.forward) and r.rank == one.rank
         assert _steps(r.step_log) == _steps(one.step_log)
+
+
+def test_forced_lookahead_on_a_tall_input_matches_default(monkeypatch):
+    """DMQR_FORCE_LOOKAHEAD (the A/B switch that runs the look-ahead schedule at shapes
+    the default keeps serial: m > 4n, n > 12288): same decisions, factor within rounding."""
+    from paper_2106_03138_b200 import qrdm2
+
+    rng = np.random.default_rng(93)
+    A = rng.standard_normal((5000, 1100)) * np.logspace(0, -4, 1100)[rng.permutation(1100)]
+    base = qrdm2(A)
+    monkeypatch.setenv("DMQR_FORCE_LOOKAHEAD", "1")
+    la = qrdm2(A)
+    assert np.array_equal(la.perm.forward, base.perm.forward) and la.rank == base.rank
+    assert _steps(la.step_log) == _steps(base.step_log)
+    assert np.abs(la.packed - base.packed).max() <= 1e-9 * np.abs(base.packed).max()
+    resid, orth = parity.residuals(A, la)
+    assert resid <= 50 * 5000 * O.EPS and orth <= 50 * 5000 * O.EPS
