@@ -2,7 +2,7 @@
 
 Run here (the build container), where /root/reference exists:
 
-    python tests/golden/make_fullsize.py [cfg3] [cfg4] [cfg5_4096] [cfg5_8192]
+    python tests/golden/make_fullsize.py [cfg3] [cfg4] [cfg5_4096] [cfg5_8192] [cfg5_16384]
 
 For each case it generates the BASELINE input on the host with one OpenBLAS
 thread (``paper_2106_03138_b200.inputs``, byte-reproducible; its sha256 is
@@ -156,7 +156,7 @@ def main(which):
         put(store, index, "cfg4", summarize(A), dict(m=65536, n=1024, source="inputs.cfg4(seed=4)"))
         save(store, index)
         del A
-    for n in (4096, 8192):
+    for n in (4096, 8192, 16384):  # (16384: ~45 min each for the reference and the oracle, one thread)
         if f"cfg5_{n}" in which:
             A = inputs.cfg5(seed=4, n=n)
             put(store, index, f"cfg5_{n}", summarize(A), dict(m=n, n=n, source=f"inputs.cfg5(seed=4,n={n})"))
