@@ -73,3 +73,12 @@ for s in (8, 20, 32, 33, 48):
     if r[14] in (0, U64MAX):
         continue
     print(s, [round(float(r[k] - r[14]) / 1e3, 1) if r[k] else None for k in (22, 23, 24, 25, 26, 15)])
+
+# k_spare phases (slots 28, 29, 31): Q1 seen, phase 1 (pending update) end, phase 2 (G tiles) end; us after k_spare's start
+print("\nk_spare (us after its start): Q1 seen, phase-1 end, phase-2 end, span end; panel end")
+for s in (1, 2, 4, 8, 12, 16, 20, 32, 48):
+    r = tl[s]
+    if r[10] in (0, U64MAX):
+        continue
+    f = lambda k: round(float(r[k] - r[10]) / 1e3, 1) if r[k] not in (0, U64MAX) else None
+    print(s, [f(28), f(29), f(31), f(11)], f(9))
