@@ -647,6 +647,8 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   // earlier G traffic slows the latency-bound panel more than it shortens k_spare (16.9 vs 16.6 ms), so opt-in
   const bool pmode_on = getenv("DMQR_PMODE") != nullptr;
   const bool fused_tail = getenv("DMQR_NO_FUSED_TAIL") == nullptr;  // schedule switch (tests): separate tail kernels
+  // rows per CTA the CholeskyQR2 cluster aims for in the look-ahead schedule (A/B knob)
+  const int64_t cq_rows = getenv("DMQR_CQ_ROWS") ? std::max<int64_t>(16, atoll(getenv("DMQR_CQ_ROWS"))) : 96;
   // (test hook: DMQR_HELPER_WAIT_NS=0 makes the tall panel abandon its helpers)
   const long long hwait_ns = getenv("DMQR_HELPER_WAIT_NS") ? atoll(getenv("DMQR_HELPER_WAIT_NS")) : 5000000ll;
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);
@@ -792,7 +794,12 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
     // kernels behind it run only if it declined (ill-conditioned panel)
     // (more than max_cluster x 256 rows: the cluster streams its rows in chunks)
     const bool cq_path = use_cq;
-    const int Pcq = (int)std::min<int64_t>(Prr, max_cluster);
+    // (look-ahead: fewer rows per CTA -- the Gram / Q1 phases of the panel scale with a CTA's rows, and
+    // late in the factorization the SMs the wider cluster takes are idle anyway)
+    // (mp is the host's upper bound: the true panel can be up to two steps' columns shorter, and rank 0
+    // must keep the whole top block -- at least DMQR_MAXK rows -- so the count is taken from mp - 2 MAXK)
+    const int Pcq = (int)std::min<int64_t>(
+        std::max<int64_t>(Prr, (la && cq_rows < RR_RMAX) ? (mp - 2 * DMQR_MAXK) / cq_rows : 1), max_cluster);
     const bool spare = la && cq_path;  // k_spare beside the panel, then k_trail_w
     const int64_t ntile_g = std::max<int64_t>(1, ceil_div(np, TA_COLS));
     // G = Q1^T C split-K items over the spare CTAs: as many splits as keep the
