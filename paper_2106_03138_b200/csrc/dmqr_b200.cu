@@ -648,7 +648,7 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
   const bool pmode_on = getenv("DMQR_PMODE") != nullptr;
   const bool fused_tail = getenv("DMQR_NO_FUSED_TAIL") == nullptr;  // schedule switch (tests): separate tail kernels
   // rows per CTA the CholeskyQR2 cluster aims for in the look-ahead schedule (A/B knob)
-  const int64_t cq_rows = getenv("DMQR_CQ_ROWS") ? std::max<int64_t>(16, atoll(getenv("DMQR_CQ_ROWS"))) : 96;
+  const int64_t cq_rows = getenv("DMQR_CQ_ROWS") ? std::max<int64_t>(DMQR_KP, atoll(getenv("DMQR_CQ_ROWS"))) : 96;
   // (test hook: DMQR_HELPER_WAIT_NS=0 makes the tall panel abandon its helpers)
   const long long hwait_ns = getenv("DMQR_HELPER_WAIT_NS") ? atoll(getenv("DMQR_HELPER_WAIT_NS")) : 5000000ll;
   const size_t panel_smem_cap = std::min<size_t>(d.smem_optin - 4096, 220 * 1024);

@@ -770,3 +770,24 @@ def test_forced_lookahead_on_a_tall_input_matches_default(monkeypatch):
     assert np.abs(la.packed - base.packed).max() <= 1e-9 * np.abs(base.packed).max()
     resid, orth = parity.residuals(A, la)
     assert resid <= 50 * 5000 * O.EPS and orth <= 50 * 5000 * O.EPS
+
+
+@pytest.mark.parametrize("rows", ["72", "256"])
+def test_panel_cluster_width_keeps_parity(monkeypatch, rows):
+    """DMQR_CQ_ROWS (rows per CTA the look-ahead panel's cluster aims for; default 96, 256 = the old
+    ceil(m'/256) width, 72 = the narrowest slice that still holds the top block): same decisions as the
+    default, factor within rounding -- on a graded input whose panels break and decline."""
+    from paper_2106_03138_b200 import qrdm2
+
+    rng = np.random.default_rng(94)
+    A = rng.standard_normal((2200, 2048)) * np.logspace(0, -9, 2048)[rng.permutation(2048)]
+    base = qrdm2(A)
+    monkeypatch.setenv("DMQR_CQ_ROWS", rows)
+    res = qrdm2(A)
+    ref = O.qrdm2(A, margins=True)
+    cut, _ = parity.robust_prefix(ref)
+    assert cut >= 64
+    assert np.array_equal(res.perm.forward[:cut], base.perm.forward[:cut])
+    assert np.array_equal(res.perm.forward[:cut], ref.forward[:cut])
+    resid, orth = parity.residuals(A, res)
+    assert resid <= 50 * 2200 * O.EPS and orth <= 50 * 2200 * O.EPS
