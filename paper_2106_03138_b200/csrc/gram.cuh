@@ -47,9 +47,29 @@ __device__ void plan_swaps_warp(Ctl* c, const CtlSnap& S, int nsel, double gamma
   const int lane = threadIdx.x & 31;
   const int n_s = S.n_s;
   const int k_s = (int)min((int64_t)nsel, S.kmax - n_s);
-  for (int d = lane; d < DMQR_KP; d += 32) {
-    ps.lastw[d] = -1;
-    ps.sel[d] = (d < nsel) ? (sel_smem ? sel_smem[d] : c->sel[d]) : 0;
+  // inw: the entries i < k_s whose selected column sits inside the window
+  // [n_s, n_s + KP).  Only those can follow a chain, write lastw or collide with
+  // an earlier source; every other entry has src_i = sel[i] and is planned in
+  // parallel.  (A write to lastw[i] comes from an i' < i: a chain ends at a slot
+  // >= i' or outside the window, and slot i' itself is no move -- so lastw[i]
+  // is final once the serial pass is over, and W_i can be read after it.)
+  constexpr int NW = (DMQR_KP + 31) / 32;
+  unsigned inw[NW];
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const int d = 32 * w + lane;
+    bool in = false;
+    if (d < DMQR_KP) {
+      const int s = (d < nsel) ? (sel_smem ? sel_smem[d] : c->sel[d]) : 0;
+      ps.lastw[d] = -1;
+      ps.sel[d] = s;
+      if (d < k_s) {
+        ps.src[d] = s;
+        const int dd = s - n_s;
+        in = dd >= 0 && dd < DMQR_KP;
+      }
+    }
+    inw[w] = __ballot_sync(0xffffffffu, in);
   }
   __syncwarp();
   if (lane == 0) {
@@ -57,20 +77,27 @@ __device__ void plan_swaps_warp(Ctl* c, const CtlSnap& S, int nsel, double gamma
     c->k_s = k_s;
     if (write_gamma) c->gamma = gamma;
     c->eps_s = S.tau * S.umax;
-    for (int i = 0; i < k_s; ++i) {
-      int p = ps.sel[i];
-      int d = p - n_s;
-      while (d >= 0 && d < i) {  // sel[i] sat in slot n_s+d when it was filled
-        p = ps.src[d];
-        d = p - n_s;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      unsigned b = inw[w];
+      while (b) {
+        const int i = 32 * w + __ffs(b) - 1;
+        b &= b - 1;
+        int p = ps.sel[i];
+        int d = p - n_s;
+        while (d >= 0 && d < i) {  // sel[i] sat in slot n_s+d when it was filled
+          p = ps.src[d];
+          d = p - n_s;
+        }
+        ps.src[i] = p;
+        const int wi = (ps.lastw[i] >= 0) ? ps.lastw[i] : n_s + i;
+        const int ds = p - n_s;
+        if (p != n_s + i && ds >= 0 && ds < DMQR_KP) ps.lastw[ds] = wi;
       }
-      ps.src[i] = p;
-      const int wi = (ps.lastw[i] >= 0) ? ps.lastw[i] : n_s + i;
-      ps.win[i] = wi;
-      const int ds = p - n_s;
-      if (p != n_s + i && ds >= 0 && ds < DMQR_KP) ps.lastw[ds] = wi;
     }
   }
+  __syncwarp();
+  for (int i = lane; i < k_s; i += 32) ps.win[i] = (ps.lastw[i] >= 0) ? ps.lastw[i] : n_s + i;
   __syncwarp();
   // transposition list in order (compaction by ballot)
   int ns = 0;
@@ -112,8 +139,16 @@ __device__ void plan_swaps_warp(Ctl* c, const CtlSnap& S, int nsel, double gamma
       p = ps.src[i];
       const int dp = p - n_s;
       if (p != n_s + i && !(dp >= 0 && dp < DMQR_KP)) {
-        mv = true;
-        for (int t = i + 1; t < k_s; ++t) mv &= (ps.src[t] != p);
+        mv = true;  // unless a later swap has the same source (only an in-window entry can)
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          unsigned b = inw[w];
+          while (b) {
+            const int t = 32 * w + __ffs(b) - 1;
+            b &= b - 1;
+            if (t > i) mv &= (ps.src[t] != p);
+          }
+        }
       }
     }
     const unsigned b = __ballot_sync(0xffffffffu, mv);
@@ -418,7 +453,10 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* c, const double* __
     double s = ((sv[0] + sv[1]) + (sv[2] + sv[3])) + ((sv[4] + sv[5]) + (sv[6] + sv[7]));
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     s += __shfl_xor_sync(0xffffffffu, s, 1);
-    if (g4 == 0) gfin[i * DMQR_KP + j] = s;
+    if (g4 == 0 && i <= j) {  // both triangles from the upper entry: the last CTA's Theta pass runs row-wise
+      gfin[i * DMQR_KP + j] = s;
+      gfin[j * DMQR_KP + i] = s;
+    }
   }
   __threadfence();
   __syncthreads();
@@ -471,6 +509,7 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* c, const double* __
       double acc = 0.0;
       for (int64_t r = 0; r < mp; ++r) acc = fma(ldexp(ci[r], -ei), ldexp(cj[r], -ej), acc);
       sm.g[i * DMQR_KP + j] = acc;
+      sm.g[j * DMQR_KP + i] = acc;
     }
     __syncthreads();
   }
@@ -489,15 +528,16 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* c, const double* __
     return;
   }
   GFT(2);
-  // Theta upper triangle: (G_ij * inv_i) * inv_j, i < j (dm.py:112)
-  // (mirrored into the lower triangle: the filter and gamma read rows only,
-  // which is bank-conflict free)
-  for (int e = tid; e < DMQR_KP * DMQR_KP; e += GRAM_T) {
-    const int i = e / DMQR_KP, j = e % DMQR_KP;
-    if (j <= i || j >= ncand) continue;
-    const double th = __dmul_rn(__dmul_rn(sm.g[e], sm.inv[i]), sm.inv[j]);
-    sm.g[e] = th;
-    sm.g[j * DMQR_KP + i] = th;
+  // Theta: (G_ij * inv_i) * inv_j, i < j (dm.py:112), and its mirror image
+  // (the filter and gamma read rows only, which is bank-conflict free).  The
+  // Gram arrives symmetric, so entry (r, c) forms the upper entry's product
+  // (min index first) in place: no transposed shared-memory stores (the row
+  // stride of 72 doubles made them 16-way bank conflicts).
+  for (int e = tid; e < ncand * DMQR_KP; e += GRAM_T) {
+    const int r = e / DMQR_KP, cc = e % DMQR_KP;
+    if (cc == r || cc >= ncand) continue;
+    const int i = min(r, cc), j = max(r, cc);
+    sm.g[e] = __dmul_rn(__dmul_rn(sm.g[e], sm.inv[i]), sm.inv[j]);
   }
   __syncthreads();
   const bool dmax = S.use_delta_max != 0;
@@ -514,24 +554,36 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* c, const double* __
       const unsigned hi = __ballot_sync(0xffffffffu, lane + 32 < t && !(a1 < delta));
       if (lane == 0) sm.conf[t] = ((unsigned long long)hi << 32) | lo;
     }
+    // past the candidates: conflicts with everything (the chain below then reads
+    // all 64 masks unconditionally -- predicated shared loads rebuild their address each)
+    for (int t = ncand + tid; t < 64; t += GRAM_T) sm.conf[t] = ~0ull;
     __syncthreads();
     GFT(6);
     if (wid == 0) {
       // the AND chain on one lane, branch-free (the accepted set as a bit mask;
       // candidate 64, the last possible, separately), then the chosen list by
       // ballot compaction in candidate order
+      // (32-bit masks: candidates 1..31 chain on the low word; for 32..63 the
+      // low-word conflicts are then known per lane and the chain runs on the
+      // high word alone -- four dependent 32-bit ops per candidate, shifts
+      // resolved at compile time)
       unsigned long long acc = 1ull;  // accepted q < 64
       int last = 0;                   // candidate 64 accepted
+      unsigned alo = 1u, ahi = 0u;
+      const unsigned* cw = reinterpret_cast<const unsigned*>(sm.conf);  // [2t] low, [2t+1] high word
       if (lane == 0) {
-        const int nb = min(ncand, 64);
-        for (int t0 = 1; t0 < nb; t0 += 8) {
-          unsigned long long cf[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) cf[q] = (t0 + q < nb) ? sm.conf[t0 + q] : ~0ull;
+        for (int t = 1; t < 32; ++t) alo |= ((cw[2 * t] & alo) == 0u) ? (1u << t) : 0u;
+      }
+      alo = __shfl_sync(0xffffffffu, alo, 0);
+      const bool freelo = (cw[2 * (32 + lane)] & alo) == 0u;
+      const unsigned allow = __ballot_sync(0xffffffffu, freelo);
+      if (lane == 0) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (t0 + q < nb) acc |= (unsigned long long)((cf[q] & acc) == 0ull) << (t0 + q);
+        for (int j = 0; j < 32; ++j) {
+          ahi |= ((cw[2 * (32 + j) + 1] & ahi) == 0u) ? (allow & (1u << j)) : 0u;
         }
+        acc = ((unsigned long long)ahi << 32) | alo;
         if (ncand > 64) last = (sm.conf[64] & acc) == 0ull;
       }
       acc = __shfl_sync(0xffffffffu, acc, 0);

@@ -140,7 +140,23 @@ class Permutation:
 
     def __init__(self, n: int):
         self.forward = np.arange(n, dtype=np.intp)
-        self.swaps: list = []
+        self._swaps: list | None = []
+        self._swap_rows = None  # (count, 2) integer array from the device log, listed on first use
+
+    @property
+    def swaps(self) -> list:
+        """The transposition log as the reference's list of (i, j) tuples; the
+        device log arrives as one array and is listed when first read."""
+        if self._swaps is None:
+            self._swaps = list(map(tuple, self._swap_rows.tolist()))
+        return self._swaps
+
+    @swaps.setter
+    def swaps(self, value) -> None:
+        self._swaps, self._swap_rows = list(value), None
+
+    def set_swap_rows(self, rows: np.ndarray) -> None:
+        self._swaps, self._swap_rows = None, rows
 
     @property
     def n(self) -> int:
@@ -295,7 +311,9 @@ def to_work(A, device=None):
         t = torch.from_numpy(np.ascontiguousarray(a.T)).to(dev, non_blocking=False).T
     m, n = int(t.shape[0]), int(t.shape[1])
     lda = lda_for(m)
-    buf = torch.zeros((max(n, 1), lda), dtype=torch.float64, device=dev)
+    # (rows m..lda of every column are padding the kernels may read: zero them unless there are none)
+    alloc = torch.empty if (lda == m and n) else torch.zeros
+    buf = alloc((max(n, 1), lda), dtype=torch.float64, device=dev)
     if m and n:
         buf[:n, :m].copy_(t.T)
     return buf, m, n, lda
@@ -398,18 +416,41 @@ def _pinned_copy(t):
     return out
 
 
+def _fetch(tensors: list) -> list:
+    """Host numpy copies of several small device tensors: asynchronous copies
+    into one page-locked block, one stream synchronization."""
+    torch = _torch()
+    sizes = [t.numel() * t.element_size() for t in tensors]
+    offs = np.concatenate([[0], np.cumsum([(b + 15) // 16 * 16 for b in sizes])]).tolist()
+    host = torch.empty(max(int(offs[-1]), 16), dtype=torch.uint8, pin_memory=True)
+    views = []
+    for t, b, o in zip(tensors, sizes, offs):
+        hv = host[o:o + b].view(t.dtype).view(t.shape)
+        if b:
+            hv.copy_(t, non_blocking=True)
+        views.append(hv)
+    torch.cuda.current_stream(tensors[0].device).synchronize()
+    return [v.numpy() for v in views]
+
+
 def to_result(f: DeviceFactor, device: bool = False) -> RRQRResult:
     info = f.info
     packed_t = f.buf[: f.n, : f.m].T  # m x n view
-    steps = _steps_from_raw(f.steps.cpu().numpy(), int(info.n_steps))
+    nst, nsw = int(info.n_steps), int(info.n_swaps)
+    want = [f.steps[: nst * _lib.STEP_BYTES], f.perm, f.swaps[:nsw].contiguous()]
+    host_coeffs = not device and f.m and f.n
+    if host_coeffs:
+        want.append(f.coeffs)
+    if f.norm_trace is not None:
+        want.append(f.norm_trace[:nst])
+    got = _fetch(want)
+    steps = _steps_from_raw(got[0], nst)
     perm = Permutation(f.n)
-    perm.forward = f.perm.cpu().numpy().astype(np.intp)
-    sw = f.swaps[: int(info.n_swaps)].cpu().numpy()
-    perm.swaps = list(map(tuple, sw.tolist()))
+    perm.forward = got[1].astype(np.intp, copy=False)
+    perm.set_swap_rows(got[2])
     trace = []
     if f.norm_trace is not None:
-        tr = f.norm_trace[: int(info.n_steps)].cpu().numpy()
-        trace = [float(x) for x in tr if not np.isnan(x)]
+        trace = [float(x) for x in got[-1] if not np.isnan(x)]
     if device:
         packed, coeffs = packed_t, f.coeffs
     elif f.m and f.n:
@@ -419,7 +460,7 @@ def to_result(f: DeviceFactor, device: bool = False) -> RRQRResult:
         # (a pageable copy of a 4096^2 factor runs at ~2 GB/s, a pinned one at ~55)
         hp = f.host_packed
         packed = (hp if hp is not None else _pinned_copy(f.buf[: f.n, : f.m])).numpy().T
-        coeffs = f.coeffs.cpu().numpy()
+        coeffs = got[3]
     else:
         packed, coeffs = np.zeros((f.m, f.n), order="F"), np.zeros(0)
     return RRQRResult(packed=packed, coeffs=coeffs, perm=perm, rank=int(info.rank), step_log=steps,
