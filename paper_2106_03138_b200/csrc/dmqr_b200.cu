@@ -718,7 +718,8 @@ int run_engine(double* A, int64_t m, int64_t n, int64_t lda, const dmqr_params* 
       NOTE_LAUNCH();
     }
     {
-      CK(pdl_launch(k_swap, dim3((unsigned)ceil_div(m + (la ? DMQR_KP : 0), SWAP_ROWS), 1, NZ), dim3(SWAP_T), SWAP_SMEM,
+      // (+1: block 0 owns no rows and moves u / u_ref / perm / flags and appends the swap log)
+      CK(pdl_launch(k_swap, dim3((unsigned)ceil_div(m + (la ? DMQR_KP : 0), SWAP_ROWS) + 1, 1, NZ), dim3(SWAP_T), SWAP_SMEM,
                     st, ctl, A, u, uref, perm, swaps, Z, ldz, upd));
       NOTE_LAUNCH();
     }

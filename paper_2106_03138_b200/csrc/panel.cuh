@@ -25,8 +25,8 @@ namespace dmqr {
 // sources of all moves on those rows into shared memory, then writes the
 // destinations -- moves only exchange columns, so each row range is closed
 // under them and needs no global scratch.  u, u_ref, perm (and the look-ahead
-// flags) get the same moves in block 0; the transposition log itself is
-// appended verbatim.
+// flags) get the same moves in block 0, which owns no rows; the transposition
+// log itself is appended verbatim.
 // Look-ahead: while the previous step's update is pending, a column's Wt
 // column (l rows, indexed from n_s) rides along as extra rows m .. m + l.
 constexpr int SWAP_ROWS = 32;                  // rows per CTA (256-byte column segments)
@@ -62,7 +62,8 @@ __global__ void __launch_bounds__(SWAP_T) k_swap(Ctl* c, double* __restrict__ A,
     s_dst[tid] = ms_dst;
   }
   __syncthreads();
-  const int64_t r0 = (int64_t)blockIdx.x * SWAP_ROWS;
+  // block 0 owns no rows (the bookkeeping moves below); block b >= 1 owns rows [32 (b-1), 32 b)
+  const int64_t r0 = (blockIdx.x == 0) ? nrow : ((int64_t)blockIdx.x - 1) * SWAP_ROWS;
   if (kTMASwap && nmv > 0 && r0 + SWAP_ROWS <= m) {
     // a whole 256-byte segment of every moved column: TMA bulk copies (one
     // lane per move) into shared memory, then bulk stores to the destinations
@@ -104,6 +105,8 @@ __global__ void __launch_bounds__(SWAP_T) k_swap(Ctl* c, double* __restrict__ A,
       }
     }
   }
+  // the bookkeeping moves run on their own CTA (the host launches one more than
+  // the row ranges need), beside the column moves instead of after a range's
   if (blockIdx.x == 0) {
     __shared__ double su[SWAP_MAXMV], sr[SWAP_MAXMV];
     __shared__ int64_t sp[SWAP_MAXMV];
