@@ -14,6 +14,7 @@
 namespace dmqr {
 
 constexpr int SEL_T = 1024;
+constexpr int SEL_FCAP = 512;  // short-list capacity of the top-k_dm fast path
 
 struct SelSmem {
   double red_v[32];
@@ -25,6 +26,9 @@ struct SelSmem {
   int bc_i[4];
   unsigned long long bc_u64[2];
   double bc_d[2];
+  double fl_u[SEL_FCAP];  // top-k_dm fast path: the short list (any order)
+  int fl_i[SEL_FCAP];
+  int fl_cnt;
 };
 
 // exclusive block scan of one int per thread (1024 threads); returns prefix, writes total
@@ -219,6 +223,91 @@ __global__ void __launch_bounds__(SEL_T) k_select_t(Ctl* c, const double* __rest
       }
     nlist = total;
   } else {
+    // Fast path (k_dm <= 64): a short list that is sure to hold the k_dm
+    // largest candidates, then rank counting in the reference's order (u
+    // descending, ties by index ascending) -- the rank IS the position in the
+    // stable argsort, so no select and no separate sort.  The list: every
+    // candidate at or above T0 = the smallest, over the 32 warps, of a warp's
+    // second-largest candidate (elements dealt round-robin): each warp then
+    // holds two candidates >= T0, 64 >= k_dm in all.  A warp with fewer than
+    // two candidates gives T0 = -1 (all candidates); a list that overflows
+    // (heavy ties) falls through to the radix select below.
+    bool fast_done = false;
+    if constexpr (!WIDE) {
+      if (k_dm <= 64) {
+        double T0 = -1.0;
+        if (total > SEL_FCAP) {
+          double v1 = -1.0;
+          int i1 = -1;
+          for (int i = n_s + tid; i < n; i += SEL_T) {
+            const double v = u[i];
+            if (i != seed && v >= thr && v > v1) {
+              v1 = v;
+              i1 = i;
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v1, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, i1, o);
+            if (ov > v1 || (ov == v1 && oi < i1)) {
+              v1 = ov;
+              i1 = oi;
+            }
+          }
+          double v2 = -1.0;  // the warp's largest candidate other than element i1
+          for (int i = n_s + tid; i < n; i += SEL_T) {
+            const double v = u[i];
+            if (i != seed && i != i1 && v >= thr) v2 = fmax(v2, v);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v2 = fmax(v2, __shfl_xor_sync(0xffffffffu, v2, o));
+          if (lane == 0) sm.red_v[wid] = v2;
+          __syncthreads();
+          T0 = sm.red_v[lane];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) T0 = fmin(T0, __shfl_xor_sync(0xffffffffu, T0, o));
+        }
+        if (tid == 0) sm.fl_cnt = 0;
+        __syncthreads();
+        for (int i = n_s + tid; i < n; i += SEL_T) {
+          const double v = u[i];
+          if (i != seed && v >= thr && v >= T0) {
+            const int p = atomicAdd(&sm.fl_cnt, 1);
+            if (p < SEL_FCAP) {
+              sm.fl_i[p] = i;
+              sm.fl_u[p] = v;
+            }
+          }
+        }
+        __syncthreads();
+        const int C = sm.fl_cnt;
+        if (C <= SEL_FCAP) {
+          // four threads per listed candidate count the candidates ahead of it
+          const int part = tid & 3;
+          for (int t0 = 0; t0 < C; t0 += SEL_T / 4) {
+            const int t = t0 + (tid >> 2);
+            const bool valid = t < C;
+            const int my_i = valid ? sm.fl_i[t] : 0;
+            const double my_u = valid ? sm.fl_u[t] : 0.0;
+            int r = 0;
+            if (valid)
+              for (int q = part; q < C; q += 4) {
+                const double ou = sm.fl_u[q];
+                const int oi = sm.fl_i[q];
+                r += (ou > my_u) || (ou == my_u && oi < my_i);
+              }
+            r += __shfl_xor_sync(0xffffffffu, r, 1);
+            r += __shfl_xor_sync(0xffffffffu, r, 2);
+            if (valid && part == 0 && r < k_dm) c->cand[1 + r] = my_i;
+          }
+          fast_done = true;
+        }
+      }
+    }
+    if (fast_done) {
+      nlist = -k_dm;  // (negative: cand[] is already written in order)
+    } else {
     // radix select of the k_dm-th largest key among candidates.  Every
     // candidate key lies in [key(thr), key(umax)], so the digits above their
     // highest differing bit are common and need no histogram; and once the
@@ -331,8 +420,11 @@ __global__ void __launch_bounds__(SEL_T) k_select_t(Ctl* c, const double* __rest
       }
     }
     nlist = k_dm;
+    }
   }
   __syncthreads();
+  const bool presorted = nlist < 0;
+  if (presorted) nlist = -nlist;
   // ---- stable descending sort of the <= k_dm candidates by rank counting ----
   if constexpr (WIDE) {
     int* const cand = wb.cand;
@@ -351,7 +443,7 @@ __global__ void __launch_bounds__(SEL_T) k_select_t(Ctl* c, const double* __rest
   } else {
     int my_i = 0, my_rank = 0;
     double my_u = 0.0;
-    if (tid < nlist) {
+    if (!presorted && tid < nlist) {
       my_i = list_i[tid];
       my_u = list_u[tid];
       for (int q = 0; q < nlist; ++q) {
@@ -361,7 +453,7 @@ __global__ void __launch_bounds__(SEL_T) k_select_t(Ctl* c, const double* __rest
       }
     }
     __syncthreads();
-    if (tid < nlist) c->cand[1 + my_rank] = my_i;
+    if (!presorted && tid < nlist) c->cand[1 + my_rank] = my_i;
   }
   if (tid == 0) {
     c->kind = 0;

@@ -791,3 +791,21 @@ def test_panel_cluster_width_keeps_parity(monkeypatch, rows):
     assert np.array_equal(res.perm.forward[:cut], ref.forward[:cut])
     resid, orth = parity.residuals(A, res)
     assert resid <= 50 * 2200 * O.EPS and orth <= 50 * 2200 * O.EPS
+
+
+@pytest.mark.parametrize("shape", [(600, 400), (1200, 1100)])
+def test_equal_norm_columns_tie_order(shape):
+    """Random +-1 entries: every column norm is exactly sqrt(m), so the first
+    candidate set is one big tie class that must come out in index order
+    (candidate_set's stable argsort, dm.py:81-97).  n = 400 goes through
+    k_select's short-list rank counting, n = 1100 overflows the short list and
+    takes the radix select with its index-ordered tie compaction."""
+    m, n = shape
+    rng = np.random.default_rng(m + n)
+    A = rng.choice([-1.0, 1.0], size=(m, n))
+    res = _gpu(A, "qrdm2")
+    with threadpool_limits(1):
+        ref = O.qrdm2(A, margins=True)
+    assert np.array_equal(res.perm.forward[:64], ref.forward[:64]), "first block's pivots differ"
+    assert _steps(res.step_log[:1]) == _steps(ref.steps[:1])
+    _compare(A, res, ref, f"pm1_{m}x{n}")
