@@ -481,15 +481,23 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* c, const double* __
   for (int q = tid; q < ncand; q += GRAM_T) sm.cand[q] = c->cand[q];
   cp_async_wait<0>();
   __syncthreads();
-  // over/underflow risk: the diagonal (sums of squares) bounds every entry
-  for (int i = tid; i < ncand; i += GRAM_T) {
-    const double d = sm.g[i * DMQR_KP + i];
-    if (!(d > 1e-280 && d < 1e280)) sm.bad = 1;
-  }
+  // over/underflow risk: the diagonal (sums of squares) bounds every entry;
+  // norms and the zero-column check (dm.py:107-109) in the same pass
+  auto norms_pass = [&]() {
+    for (int i = tid; i < ncand; i += GRAM_T) {
+      const double d = sm.g[i * DMQR_KP + i];
+      if (!(d > 1e-280 && d < 1e280)) sm.bad = 1;
+      const double nr = sqrt(d);
+      if (nr == 0.0) sm.zero = 1;
+      sm.inv[i] = 1.0 / nr;
+    }
+  };
+  norms_pass();
   __syncthreads();
   const int64_t n_s = S.n_s, m = S.m, lda = S.lda, mp = m - n_s;
   if (sm.bad) {
     // slow path (extreme magnitudes only): recompute with exact 2^-e column scales
+    if (tid == 0) sm.zero = 0;  // (set from the unusable Gram; decided again below)
     for (int i = wid; i < ncand; i += GRAM_T / 32) {
       const double* ci = A + (int64_t)c->cand[i] * lda + n_s;
       double am = 0.0;
@@ -512,14 +520,9 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* c, const double* __
       sm.g[j * DMQR_KP + i] = acc;
     }
     __syncthreads();
+    norms_pass();  // (sets bad again when the scaled Gram is still out of range: harmless, not read again)
+    __syncthreads();
   }
-  // norms, zero-column check (dm.py:107-109)
-  for (int i = tid; i < ncand; i += GRAM_T) {
-    const double nr = sqrt(sm.g[i * DMQR_KP + i]);
-    if (nr == 0.0) sm.zero = 1;
-    sm.inv[i] = 1.0 / nr;
-  }
-  __syncthreads();
   if (sm.zero) {
     if (tid == 0) {
       c->status = -3;
@@ -530,34 +533,38 @@ __global__ void __launch_bounds__(GRAM_T) k_gram_finish(Ctl* c, const double* __
   GFT(2);
   // Theta: (G_ij * inv_i) * inv_j, i < j (dm.py:112), and its mirror image
   // (the filter and gamma read rows only, which is bank-conflict free).  The
-  // Gram arrives symmetric, so entry (r, c) forms the upper entry's product
+  // Gram arrives symmetric, so entry (t, q) forms the upper entry's product
   // (min index first) in place: no transposed shared-memory stores (the row
-  // stride of 72 doubles made them 16-way bank conflicts).
-  for (int e = tid; e < ncand * DMQR_KP; e += GRAM_T) {
-    const int r = e / DMQR_KP, cc = e % DMQR_KP;
-    if (cc == r || cc >= ncand) continue;
-    const int i = min(r, cc), j = max(r, cc);
-    sm.g[e] = __dmul_rn(__dmul_rn(sm.g[e], sm.inv[i]), sm.inv[j]);
-  }
-  __syncthreads();
+  // stride of 72 doubles made them 16-way bank conflicts).  A warp per row;
+  // the same pass ballots the row's conflict mask for the greedy filter
+  // (dm.py:151-173): bit q of conf[t] is set when candidate q < t fails
+  // |theta_qt| < delta; t is then accepted iff no accepted q conflicts.
   const bool dmax = S.use_delta_max != 0;
-  GFT(3);
-  if (!dmax) {
-    // ---- greedy filter (dm.py:151-173) via conflict masks: bit q of conf[t] is
-    // set when candidate q < t fails |theta_qt| < delta; then t is accepted iff
-    // no accepted q conflicts -- one 64-step bit loop on one thread ----
+  {
     const double delta = S.delta;
-    for (int t = wid + 1; t < ncand; t += GRAM_T / 32) {
-      const double a0 = (lane < t) ? fabs(sm.g[t * DMQR_KP + lane]) : 0.0;
-      const double a1 = (lane + 32 < t) ? fabs(sm.g[t * DMQR_KP + lane + 32]) : 0.0;
-      const unsigned lo = __ballot_sync(0xffffffffu, lane < t && !(a0 < delta));
-      const unsigned hi = __ballot_sync(0xffffffffu, lane + 32 < t && !(a1 < delta));
-      if (lane == 0) sm.conf[t] = ((unsigned long long)hi << 32) | lo;
+    for (int t = wid; t < ncand; t += GRAM_T / 32) {
+      unsigned bal[2] = {0u, 0u};
+#pragma unroll
+      for (int h = 0; h < 3; ++h) {
+        const int q = lane + 32 * h;
+        double av = 0.0;
+        if (q < ncand && q != t) {
+          const int i = min(t, q), j = max(t, q);
+          const double th = __dmul_rn(__dmul_rn(sm.g[t * DMQR_KP + q], sm.inv[i]), sm.inv[j]);
+          sm.g[t * DMQR_KP + q] = th;
+          av = fabs(th);
+        }
+        if (h < 2) bal[h] = __ballot_sync(0xffffffffu, q < t && !(av < delta));
+      }
+      if (lane == 0 && t >= 1) sm.conf[t] = ((unsigned long long)bal[1] << 32) | bal[0];
     }
     // past the candidates: conflicts with everything (the chain below then reads
     // all 64 masks unconditionally -- predicated shared loads rebuild their address each)
     for (int t = ncand + tid; t < 64; t += GRAM_T) sm.conf[t] = ~0ull;
-    __syncthreads();
+  }
+  __syncthreads();
+  GFT(3);
+  if (!dmax) {
     GFT(6);
     if (wid == 0) {
       // the AND chain on one lane, branch-free (the accepted set as a bit mask;
